@@ -1,0 +1,191 @@
+/*
+ * h2g — B200-native (sm_100a) H² factorize / solve, C ABI.
+ *
+ * Drop-in boundary for the hot path of the reference h2lu library
+ * (arXiv 1703.06155, Ma & Jiao). The reference is header-only C++ on Eigen and
+ * exposes no C ABI; each entry point below names the reference interface it
+ * replaces (paths relative to /root/reference/proj). Plain pointers and sizes
+ * only; complex data is interleaved complex128 (re, im), column-major — the
+ * memory layout of Eigen::MatrixXcd / VectorXcd. Vectors are in TREE order,
+ * like the reference library (solve.hpp:104-110; the CLI permutes at I/O,
+ * tools/h2lu_cli.cpp:47-57).
+ *
+ * Every call returns H2G_OK (0) or an error code; details land in the
+ * optional h2g_error* (and in h2g_last_error for the calling thread). The
+ * codes mirror the reference exception types (include/h2lu/types.hpp:18-47).
+ * There is no CPU fallback: without a CUDA device every compute call fails
+ * with H2G_ERR_CUDA.
+ */
+#ifndef H2G_H
+#define H2G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum h2g_status {
+  H2G_OK = 0,
+  H2G_ERR_INVALID_INPUT = 1,   /* InvalidInputError */
+  H2G_ERR_SIZE_GUARD = 2,      /* SizeGuardError */
+  H2G_ERR_NON_FINITE = 3,      /* NonFiniteError */
+  H2G_ERR_SINGULAR_PIVOT = 4,  /* SingularPivotError{pivot_index, pivot_magnitude, cluster, level} */
+  H2G_ERR_UNDEFINED_METRIC = 5,/* UndefinedMetricError */
+  H2G_ERR_CUDA = 8,            /* no device / CUDA runtime failure / out of memory */
+  H2G_ERR_INTERNAL = 9
+};
+
+typedef struct h2g_error {
+  int32_t code;
+  int32_t cluster;          /* heap id of the failing cluster; -1 = root block / none */
+  int32_t level;            /* tree level; -1 = none */
+  int32_t pad_;
+  int64_t pivot_index;
+  double pivot_magnitude;
+  char msg[256];
+} h2g_error;
+
+/* Within-level elimination order. REFERENCE reproduces the reference's
+ * ascending-heap-id order (factorization.hpp:618) exactly, executed as
+ * dependency wavefronts; COLORED runs a greedy distance-1 colouring, one
+ * colour per batch (a different, equally valid elimination order). */
+enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1 };
+
+/* Solve modes: solve.hpp:105 solve, :43 forward, :65 backward, :113
+ * apply_inverse (alias of solve), plus the explicit-inverse application
+ * (precomputed triangular inverses, applied as ZGEMMs). */
+enum h2g_solve_mode {
+  H2G_SOLVE = 0,
+  H2G_FORWARD = 1,
+  H2G_BACKWARD = 2,
+  H2G_APPLY_INVERSE = 3,
+  H2G_APPLY_INVERSE_EXPLICIT = 4
+};
+
+/* Kernel of the H² construction (kernel.hpp:13-61; the diagonal is widened to
+ * complex for the BASELINE volume integral equation). Off-diagonal entries are
+ * scale * f(r), f = 1/(4 pi r) (LAPLACE) or exp(-i k r)/(4 pi r) (HELMHOLTZ);
+ * ZERO is the reference's zero custom kernel. */
+enum h2g_kernel_kind { H2G_KERNEL_LAPLACE = 0, H2G_KERNEL_HELMHOLTZ = 1, H2G_KERNEL_ZERO = 2 };
+
+typedef struct h2g_kernel_spec {
+  int32_t kind;
+  int32_t pad_;
+  double wavenumber_re, wavenumber_im;
+  double scale_re, scale_im;
+  double diag_re, diag_im;
+} h2g_kernel_spec;
+
+/* Host description of an H2Matrix (h2_matrix.hpp:29-39) with its cluster
+ * tree (cluster_tree.hpp:31-69, heap order, uniform depth) and block
+ * partition (block_tree.hpp:21-97, pair lists sorted by (row, col)).
+ * num_clusters = 2^(depth+1) - 1. */
+typedef struct h2g_matrix_desc {
+  int64_t n;
+  int32_t depth;
+  int32_t pad_;
+  double eta;
+  double eps_h2;
+  const int64_t* cluster_begin;   /* [num_clusters] tree-order ranges */
+  const int64_t* cluster_end;
+  const int64_t* adm_offsets;     /* [depth+2]: admissible pairs of level l at [adm_offsets[l], adm_offsets[l+1]) */
+  const int32_t* adm_pairs;       /* 2 * num_adm, (row, col) heap ids */
+  const int64_t* split_offsets;   /* [depth+2] */
+  const int32_t* split_pairs;
+  int64_t num_leaf_pairs;
+  const int32_t* leaf_pairs;      /* inadmissible leaf pairs (dense blocks) */
+  /* numerical data, offsets in complex elements */
+  const int64_t* basis_rows;      /* [num_clusters]: leaf size, or rank(c1)+rank(c2) */
+  const int64_t* basis_rank;      /* [num_clusters]: columns */
+  const int64_t* basis_offset;
+  const double* basis_data;
+  const int64_t* coupling_offset; /* [num_adm], level-major admissible order; rank_t x rank_s */
+  const double* coupling_data;
+  const int64_t* dense_offset;    /* [num_leaf_pairs]; |t| x |s| */
+  const double* dense_data;
+} h2g_matrix_desc;
+
+typedef struct h2g_context h2g_context;
+typedef struct h2g_matrix h2g_matrix;
+typedef struct h2g_chain h2g_chain;
+
+/* ---- runtime -------------------------------------------------------- */
+int h2g_device_count(void);
+int h2g_context_create(int device, h2g_context** out, h2g_error* err);
+int h2g_context_destroy(h2g_context* ctx);
+int h2g_last_error(h2g_error* err);
+const char* h2g_version(void);
+
+/* ---- input ------------------------------------------------------------ */
+/* Replaces passing `const H2Matrix&` into factorize (factorization.hpp:600):
+ * uploads a host H2Matrix; the device copy is immutable (factorize never
+ * modifies its input, test_factorization.cpp:241-254). */
+int h2g_matrix_upload(h2g_context* ctx, const h2g_matrix_desc* desc, h2g_matrix** out, h2g_error* err);
+/* build_cluster_tree + build_block_tree (cluster_tree.hpp:71, block_tree.hpp:114)
+ * on the host and build_h2 (h2_matrix.hpp:300) on the device. points: n x 3
+ * row-major doubles in original order. */
+int h2g_matrix_build(h2g_context* ctx, const double* points, int64_t n, int64_t leafsize, double eta,
+                     const h2g_kernel_spec* kernel, double eps_h2, h2g_matrix** out, h2g_error* err);
+int h2g_matrix_destroy(h2g_matrix* m);
+/* sizes[8]: n, depth, num_clusters, num_adm, num_leaf_pairs, basis_elems, coupling_elems, dense_elems */
+int h2g_matrix_sizes(const h2g_matrix* m, int64_t* sizes);
+/* Download into caller arrays sized from h2g_matrix_sizes (same layout as the
+ * desc; pair arrays optional). perm: tree index -> original index. */
+int h2g_matrix_download(const h2g_matrix* m, int64_t* cluster_begin, int64_t* cluster_end, int64_t* perm,
+                        int64_t* adm_offsets, int32_t* adm_pairs, int64_t* split_offsets, int32_t* split_pairs,
+                        int32_t* leaf_pairs, int64_t* basis_rows, int64_t* basis_rank, int64_t* basis_offset,
+                        double* basis_data, int64_t* coupling_offset, double* coupling_data, int64_t* dense_offset,
+                        double* dense_data);
+/* y = A x through the compressed operator (h2_matrix.hpp:80-137), host buffers, nrhs columns. */
+int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y, int32_t nrhs, h2g_error* err);
+
+/* ---- hot path --------------------------------------------------------- */
+/* factorize(A, eps_fill_in, stop_level_override) (factorization.hpp:600-653).
+ * stop_level < 0 means "default" (l0). */
+int h2g_factorize(h2g_context* ctx, const h2g_matrix* m, double eps_fill_in, int32_t stop_level, int32_t schedule,
+                  h2g_chain** out, h2g_error* err);
+int h2g_chain_destroy(h2g_chain* c);
+
+/* solve / forward_substitute / backward_substitute / apply_inverse
+ * (solve.hpp:43-113) with host buffers: b, x are n x nrhs column-major
+ * complex128 (x may alias b: solve_in_place). */
+int h2g_solve(h2g_chain* c, const double* b, double* x, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err);
+/* Same on device memory (x_dev holds b on entry), on the chain's stream. */
+int h2g_solve_device(h2g_chain* c, double* x_dev, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err);
+
+/* ---- chain inspection (FactorChain fields, factorization.hpp:22-98) ---- */
+/* info[6]: n, stop_level, root_size, num_levels, storage_bytes, schedule */
+int h2g_chain_info(const h2g_chain* c, int64_t* info);
+/* out[9]: level, nrecs, rank_sum_before, rank_sum_after, eliminated, ledger_blocks, chain_bytes, perm_len, active_after */
+int h2g_chain_level(const h2g_chain* c, int32_t level_index, int64_t* out);
+/* 10 per record, in the level's record order: cluster, level, pos, bsize,
+ * eliminated, rank_before, rank_after, fill_targets, n_lbar, n_ubar */
+int h2g_chain_records(const h2g_chain* c, int32_t level_index, int64_t* out);
+int h2g_chain_perm(const h2g_chain* c, int32_t level_index, int64_t* src);
+/* Qtilde (bsize^2), L11 and U11 (eliminated^2) of one record (record order). */
+int h2g_chain_record_mats(const h2g_chain* c, int32_t level_index, int32_t record, double* qtilde, double* l11, double* u11);
+/* Lbar / Ubar blocks of one record: positions and column-major data
+ * concatenated in record order; sizes from h2g_chain_record_blocks_sizes. */
+int h2g_chain_record_blocks_sizes(const h2g_chain* c, int32_t level_index, int32_t record, int64_t* sizes4);
+int h2g_chain_record_blocks(const h2g_chain* c, int32_t level_index, int32_t record, int64_t* lbar_pos, int64_t* lbar_rows,
+                            double* lbar_data, int64_t* ubar_pos, int64_t* ubar_cols, double* ubar_data);
+int h2g_chain_root(const h2g_chain* c, double* root_l, double* root_u);
+/* FNV-1a over the chain contents (determinism checks). */
+uint64_t h2g_chain_hash(const h2g_chain* c);
+/* Device time (ms, CUDA events on the chain's stream) of the last factorize
+ * and the last solve, and the number of kernels each launched. */
+int h2g_chain_timing(const h2g_chain* c, double* factor_ms, double* solve_ms, int64_t* factor_launches, int64_t* solve_launches);
+/* Algorithmic work of the factorization (SURVEY §8d F_factor, from the shapes
+ * executed) and of one nrhs=1 solve (bytes of chain + vector traffic):
+ * out[4]: factor_flops, schur_flops, solve_bytes, schur_bytes */
+int h2g_chain_work(const h2g_chain* c, double* out);
+
+/* Seeded complex-normal vector: mt19937_64(seed) + std::normal_distribution,
+ * cxd(g(rng), g(rng)) (tools/h2lu_cli.cpp:181-191), ORIGINAL order. */
+void h2g_random_rhs(int64_t n, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2G_H */

@@ -324,6 +324,32 @@ class H2:
         )
         return out
 
+    def arrays(self):
+        """Tree + partition + numerical data: the full include/h2g.h matrix
+        description (what the GPU path's h2g_matrix_upload consumes)."""
+        out = self.export()
+        b, e = self.tree.ranges()
+        L = self.tree.depth
+        adm = [self.blocks.admissible(l) for l in range(L + 1)]
+        spl = [self.blocks.split(l) for l in range(L + 1)]
+        out.update(
+            n=self.n,
+            depth=L,
+            eta=self.blocks.eta,
+            eps_h2=self.eps_h2 or 0.0,
+            cluster_begin=b,
+            cluster_end=e,
+            adm_offsets=np.concatenate([[0], np.cumsum([len(a) for a in adm])]).astype(np.int64),
+            adm_pairs=np.ascontiguousarray(np.vstack(adm + [np.zeros((0, 2), np.int32)]).astype(np.int32)),
+            split_offsets=np.concatenate([[0], np.cumsum([len(a) for a in spl])]).astype(np.int64),
+            split_pairs=np.ascontiguousarray(np.vstack(spl + [np.zeros((0, 2), np.int32)]).astype(np.int32)),
+            leaf_pairs=np.ascontiguousarray(self.blocks.inadmissible_leaves().astype(np.int32)),
+        )
+        for k in ("adm_pairs", "split_pairs", "leaf_pairs"):
+            if out[k].shape[0] == 0:
+                out[k] = np.zeros((1, 2), np.int32)
+        return out
+
     @classmethod
     def from_arrays(cls, blocks, eps_h2, arrs, kernel=None):
         a = {k: np.ascontiguousarray(v) for k, v in arrs.items()}

@@ -1,0 +1,541 @@
+"""B200-native H² factorize / solve (arXiv 1703.06155), Python mirror of the
+reference h2lu API over the C ABI of ``include/h2g.h`` (``libh2g.so``).
+
+Reference interface mirrored (paths under /root/reference/proj):
+  factorize(A, eps_fill_in, stop_level_override)  include/h2lu/factorization.hpp:600
+  solve / solve_in_place / apply_inverse           include/h2lu/solve.hpp:99-113
+  forward_substitute / backward_substitute         include/h2lu/solve.hpp:85-97
+  FactorChain fields (levels, records, root)       include/h2lu/factorization.hpp:22-98
+  error types                                      include/h2lu/types.hpp:18-47
+Vectors are in tree order, like the reference library. The compute path is
+CUDA only: without the built library or without a device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import geometry  # noqa: F401
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libh2g.so")
+
+SCHEDULES = {"reference": 0, "colored": 1}
+KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2
+_SOLVE, _FORWARD, _BACKWARD, _APPLY_INVERSE, _APPLY_INVERSE_EXPLICIT = 0, 1, 2, 3, 4
+
+
+class H2GError(RuntimeError):
+    code = 9
+
+    def __init__(self, msg, cluster=-1, level=-1, pivot_index=-1, pivot_magnitude=0.0):
+        super().__init__(msg)
+        self.cluster = cluster
+        self.level = level
+        self.pivot_index = pivot_index
+        self.pivot_magnitude = pivot_magnitude
+
+
+class InvalidInputError(H2GError):
+    code = 1
+
+
+class SizeGuardError(H2GError):
+    code = 2
+
+
+class NonFiniteError(H2GError):
+    code = 3
+
+
+class SingularPivotError(H2GError):
+    code = 4
+
+
+class UndefinedMetricError(H2GError):
+    code = 5
+
+
+class CudaError(H2GError):
+    code = 8
+
+
+_ERR = {1: InvalidInputError, 2: SizeGuardError, 3: NonFiniteError, 4: SingularPivotError, 5: UndefinedMetricError, 8: CudaError}
+
+
+class _Err(C.Structure):
+    _fields_ = [
+        ("code", C.c_int32),
+        ("cluster", C.c_int32),
+        ("level", C.c_int32),
+        ("pad", C.c_int32),
+        ("pivot_index", C.c_int64),
+        ("pivot_magnitude", C.c_double),
+        ("msg", C.c_char * 256),
+    ]
+
+
+class _Kernel(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("pad", C.c_int32),
+        ("wavenumber_re", C.c_double),
+        ("wavenumber_im", C.c_double),
+        ("scale_re", C.c_double),
+        ("scale_im", C.c_double),
+        ("diag_re", C.c_double),
+        ("diag_im", C.c_double),
+    ]
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+_I32 = C.POINTER(C.c_int32)
+
+
+class _Desc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("depth", C.c_int32),
+        ("pad", C.c_int32),
+        ("eta", C.c_double),
+        ("eps_h2", C.c_double),
+        ("cluster_begin", _I64),
+        ("cluster_end", _I64),
+        ("adm_offsets", _I64),
+        ("adm_pairs", _I32),
+        ("split_offsets", _I64),
+        ("split_pairs", _I32),
+        ("num_leaf_pairs", C.c_int64),
+        ("leaf_pairs", _I32),
+        ("basis_rows", _I64),
+        ("basis_rank", _I64),
+        ("basis_offset", _I64),
+        ("basis_data", _D),
+        ("coupling_offset", _I64),
+        ("coupling_data", _D),
+        ("dense_offset", _I64),
+        ("dense_data", _D),
+    ]
+
+
+# Public C symbols (kept in sync with include/h2g.h; the CPU tests check both).
+SYMBOLS = {
+    "h2g_version": (C.c_char_p, []),
+    "h2g_device_count": (C.c_int, []),
+    "h2g_context_create": (C.c_int, [C.c_int, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_context_destroy": (C.c_int, [_P]),
+    "h2g_last_error": (C.c_int, [C.POINTER(_Err)]),
+    "h2g_matrix_upload": (C.c_int, [_P, C.POINTER(_Desc), C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_matrix_build": (C.c_int, [_P, _D, C.c_int64, C.c_int64, C.c_double, C.POINTER(_Kernel), C.c_double, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_matrix_destroy": (C.c_int, [_P]),
+    "h2g_matrix_sizes": (C.c_int, [_P, _I64]),
+    "h2g_matrix_download": (C.c_int, [_P, _I64, _I64, _I64, _I64, _I32, _I64, _I32, _I32, _I64, _I64, _I64, _D, _I64, _D, _I64, _D]),
+    "h2g_matvec": (C.c_int, [_P, _P, _D, _D, C.c_int32, C.POINTER(_Err)]),
+    "h2g_factorize": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_int32, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_chain_destroy": (C.c_int, [_P]),
+    "h2g_solve": (C.c_int, [_P, _D, _D, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_Err)]),
+    "h2g_solve_device": (C.c_int, [_P, _D, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_Err)]),
+    "h2g_chain_info": (C.c_int, [_P, _I64]),
+    "h2g_chain_level": (C.c_int, [_P, C.c_int32, _I64]),
+    "h2g_chain_records": (C.c_int, [_P, C.c_int32, _I64]),
+    "h2g_chain_perm": (C.c_int, [_P, C.c_int32, _I64]),
+    "h2g_chain_record_mats": (C.c_int, [_P, C.c_int32, C.c_int32, _D, _D, _D]),
+    "h2g_chain_record_blocks_sizes": (C.c_int, [_P, C.c_int32, C.c_int32, _I64]),
+    "h2g_chain_record_blocks": (C.c_int, [_P, C.c_int32, C.c_int32, _I64, _I64, _D, _I64, _I64, _D]),
+    "h2g_chain_root": (C.c_int, [_P, _D, _D]),
+    "h2g_chain_hash": (C.c_uint64, [_P]),
+    "h2g_chain_timing": (C.c_int, [_P, _D, _D, _I64, _I64]),
+    "h2g_chain_work": (C.c_int, [_P, _D]),
+    "h2g_random_rhs": (None, [C.c_int64, C.c_uint64, _D]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libh2g.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C paper_1703_06155_b200)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in SYMBOLS.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _raise(err):
+    cls = _ERR.get(err.code, H2GError)
+    raise cls(err.msg.decode(errors="replace"), err.cluster, err.level, err.pivot_index, err.pivot_magnitude)
+
+
+def _check(rc, err):
+    if rc != 0:
+        _raise(err)
+
+
+def _d(a):
+    return a.ctypes.data_as(_D)
+
+
+def _i64(a):
+    return a.ctypes.data_as(_I64)
+
+
+def _i32(a):
+    return a.ctypes.data_as(_I32)
+
+
+class Context:
+    """One CUDA device + stream."""
+
+    _default = {}
+
+    def __init__(self, device=0):
+        err = _Err()
+        h = _P()
+        _check(lib().h2g_context_create(device, C.byref(h), C.byref(err)), err)
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device=0):
+        if device not in cls._default:
+            cls._default[device] = cls(device)
+        return cls._default[device]
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.h2g_context_destroy(self.h)
+            self.h = None
+
+
+def device_count():
+    return int(lib().h2g_device_count())
+
+
+class Kernel:
+    """Kernel spec (kernel.hpp:13-61 with a complex diagonal)."""
+
+    def __init__(self, kind=KERNEL_LAPLACE, wavenumber=0.0, scale=1.0, diag=1.0):
+        self.kind, self.wavenumber, self.scale, self.diag = kind, complex(wavenumber), complex(scale), complex(diag)
+
+    def c(self):
+        return _Kernel(self.kind, 0, self.wavenumber.real, self.wavenumber.imag, self.scale.real, self.scale.imag, self.diag.real, self.diag.imag)
+
+
+def laplace_kernel(shift=1.0):
+    return Kernel(KERNEL_LAPLACE, 0.0, 1.0, shift)
+
+
+def helmholtz_kernel(k, shift=1.0, scale=1.0):
+    return Kernel(KERNEL_HELMHOLTZ, k, scale, shift)
+
+
+def zero_kernel(shift=0.0):
+    return Kernel(KERNEL_ZERO, 0.0, 0.0, shift)
+
+
+def vie_kernel(cells_per_side, side_lambda, eps_r=4.0):
+    k0, scale, diag = geometry.vie_constants(cells_per_side, side_lambda, eps_r)
+    return Kernel(KERNEL_HELMHOLTZ, k0, scale, diag)
+
+
+class H2Matrix:
+    """Device-resident H² matrix (the input of factorize; never modified)."""
+
+    def __init__(self, handle, ctx):
+        self.h = handle
+        self.ctx = ctx
+        sz = np.zeros(8, np.int64)
+        lib().h2g_matrix_sizes(self.h, _i64(sz))
+        self.n, self.depth, self.num_clusters, self.num_adm, self.num_leaf_pairs, self.basis_elems, self.coupling_elems, self.dense_elems = (int(v) for v in sz)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.h2g_matrix_destroy(self.h)
+            self.h = None
+
+    @classmethod
+    def upload(cls, arrays, ctx=None):
+        """From host arrays in the include/h2g.h layout (keys as exported by
+        oracle/pyoracle.H2.export() plus the tree/partition arrays)."""
+        ctx = ctx or Context.default()
+        a = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
+        keep = a  # keep buffers alive during the call
+        d = _Desc()
+        d.n = int(a["n"])
+        d.depth = int(a["depth"])
+        d.eta = float(a.get("eta", 1.0))
+        d.eps_h2 = float(a.get("eps_h2", 0.0))
+        d.cluster_begin = _i64(a["cluster_begin"].astype(np.int64, copy=False))
+        d.cluster_end = _i64(a["cluster_end"].astype(np.int64, copy=False))
+        d.adm_offsets = _i64(a["adm_offsets"])
+        d.adm_pairs = _i32(a["adm_pairs"])
+        d.split_offsets = _i64(a["split_offsets"])
+        d.split_pairs = _i32(a["split_pairs"])
+        d.num_leaf_pairs = int(a["leaf_pairs"].shape[0])
+        d.leaf_pairs = _i32(a["leaf_pairs"])
+        d.basis_rows = _i64(a["basis_rows"])
+        d.basis_rank = _i64(a["basis_rank"])
+        d.basis_offset = _i64(a["basis_offset"])
+        d.basis_data = _d(a["basis_data"].view(np.float64))
+        d.coupling_offset = _i64(a["coupling_offset"])
+        d.coupling_data = _d(a["coupling_data"].view(np.float64))
+        d.dense_offset = _i64(a["dense_offset"])
+        d.dense_data = _d(a["dense_data"].view(np.float64))
+        err = _Err()
+        h = _P()
+        rc = lib().h2g_matrix_upload(ctx.h, C.byref(d), C.byref(h), C.byref(err))
+        del keep
+        _check(rc, err)
+        return cls(h, ctx)
+
+    @classmethod
+    def build(cls, points, leafsize, eta, kernel, eps_h2, ctx=None):
+        """Tree + partition on the host, H² construction on the device."""
+        ctx = ctx or Context.default()
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        err = _Err()
+        h = _P()
+        kc = kernel.c()
+        _check(lib().h2g_matrix_build(ctx.h, _d(pts), pts.shape[0], leafsize, eta, C.byref(kc), eps_h2, C.byref(h), C.byref(err)), err)
+        return cls(h, ctx)
+
+    def download(self):
+        nc, L = self.num_clusters, self.depth
+        o = dict(
+            cluster_begin=np.zeros(nc, np.int64),
+            cluster_end=np.zeros(nc, np.int64),
+            perm=np.zeros(self.n, np.int64),
+            adm_offsets=np.zeros(L + 2, np.int64),
+            adm_pairs=np.zeros((max(self.num_adm, 1), 2), np.int32),
+            split_offsets=np.zeros(L + 2, np.int64),
+            split_pairs=np.zeros((max(nc, 1), 2), np.int32),
+            leaf_pairs=np.zeros((max(self.num_leaf_pairs, 1), 2), np.int32),
+            basis_rows=np.zeros(nc, np.int64),
+            basis_rank=np.zeros(nc, np.int64),
+            basis_offset=np.zeros(nc, np.int64),
+            basis_data=np.zeros(max(self.basis_elems, 1), np.complex128),
+            coupling_offset=np.zeros(max(self.num_adm, 1), np.int64),
+            coupling_data=np.zeros(max(self.coupling_elems, 1), np.complex128),
+            dense_offset=np.zeros(max(self.num_leaf_pairs, 1), np.int64),
+            dense_data=np.zeros(max(self.dense_elems, 1), np.complex128),
+        )
+        # split pair count is only known after the offsets: two passes
+        rc = lib().h2g_matrix_download(self.h, *([None] * 3), _i64(o["adm_offsets"]), None, _i64(o["split_offsets"]), *([None] * 10))
+        if rc:
+            raise H2GError("download failed")
+        o["split_pairs"] = np.zeros((max(int(o["split_offsets"][-1]), 1), 2), np.int32)
+        rc = lib().h2g_matrix_download(
+            self.h, _i64(o["cluster_begin"]), _i64(o["cluster_end"]), _i64(o["perm"]), _i64(o["adm_offsets"]), _i32(o["adm_pairs"]),
+            _i64(o["split_offsets"]), _i32(o["split_pairs"]), _i32(o["leaf_pairs"]), _i64(o["basis_rows"]), _i64(o["basis_rank"]),
+            _i64(o["basis_offset"]), _d(o["basis_data"].view(np.float64)), _i64(o["coupling_offset"]), _d(o["coupling_data"].view(np.float64)),
+            _i64(o["dense_offset"]), _d(o["dense_data"].view(np.float64)))
+        if rc:
+            raise H2GError("download failed")
+        o["n"], o["depth"] = self.n, self.depth
+        return o
+
+    def matvec(self, x):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        nrhs = 1 if x.ndim == 1 else x.shape[1]
+        xf = np.asfortranarray(x.reshape(self.n, nrhs))
+        y = np.zeros((self.n, nrhs), np.complex128, order="F")
+        err = _Err()
+        _check(lib().h2g_matvec(self.ctx.h, self.h, xf.ctypes.data_as(_D), y.ctypes.data_as(_D), nrhs, C.byref(err)), err)
+        return y[:, 0].copy() if x.ndim == 1 else y
+
+    def relative_residual(self, x, b):
+        """||A x - b|| / ||b|| through the compressed operator (verify.hpp:14-19)."""
+        nb = np.linalg.norm(b)
+        if nb == 0.0:
+            raise UndefinedMetricError("relative_residual: right-hand side is zero")
+        return float(np.linalg.norm(self.matvec(x) - b) / nb)
+
+
+REC_FIELDS = ("cluster", "level", "pos", "bsize", "eliminated", "rank_before", "rank_after", "fill_targets", "n_lbar", "n_ubar")
+LEVEL_FIELDS = ("level", "nrecs", "rank_sum_before", "rank_sum_after", "eliminated", "ledger_blocks", "chain_bytes", "perm_len", "active_after")
+
+
+class FactorChain:
+    """Device-resident factorization (FactorChain, factorization.hpp:76-98)."""
+
+    def __init__(self, handle, matrix):
+        self.h = handle
+        self.matrix = matrix  # keep the context alive
+        info = np.zeros(6, np.int64)
+        lib().h2g_chain_info(self.h, _i64(info))
+        self.n, self.stop_level, self.root_size, self.num_levels, self.storage_bytes, sch = (int(v) for v in info)
+        self.schedule = {v: k for k, v in SCHEDULES.items()}[sch]
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.h2g_chain_destroy(self.h)
+            self.h = None
+
+    def level(self, li):
+        out = np.zeros(9, np.int64)
+        lib().h2g_chain_level(self.h, li, _i64(out))
+        return dict(zip(LEVEL_FIELDS, (int(v) for v in out)))
+
+    def levels(self):
+        return [self.level(i) for i in range(self.num_levels)]
+
+    def records(self, li):
+        n = self.level(li)["nrecs"]
+        out = np.zeros((n, 10), np.int64)
+        if n:
+            lib().h2g_chain_records(self.h, li, _i64(out))
+        return [dict(zip(REC_FIELDS, (int(v) for v in row))) for row in out]
+
+    def all_records(self):
+        r = []
+        for li in range(self.num_levels):
+            r.extend(self.records(li))
+        return r
+
+    def perm(self, li):
+        n = self.level(li)["perm_len"]
+        out = np.zeros(n, np.int64)
+        if n:
+            lib().h2g_chain_perm(self.h, li, _i64(out))
+        return out
+
+    def record_mats(self, li, ri):
+        rec = self.records(li)[ri]
+        b, e = rec["bsize"], rec["eliminated"]
+        Q = np.zeros((b, b), np.complex128, order="F")
+        L = np.zeros((e, e), np.complex128, order="F")
+        U = np.zeros((e, e), np.complex128, order="F")
+        lib().h2g_chain_record_mats(self.h, li, ri, Q.ctypes.data_as(_D), L.ctypes.data_as(_D), U.ctypes.data_as(_D))
+        return Q, L, U
+
+    def record_blocks(self, li, ri):
+        """(Lbar, Ubar) as lists of (pos, matrix) in record order."""
+        rec = self.records(li)[ri]
+        e = rec["eliminated"]
+        sz = np.zeros(4, np.int64)
+        lib().h2g_chain_record_blocks_sizes(self.h, li, ri, _i64(sz))
+        nl, el, nu, eu = (int(v) for v in sz)
+        lp, lr = np.zeros(max(nl, 1), np.int64), np.zeros(max(nl, 1), np.int64)
+        up, uc = np.zeros(max(nu, 1), np.int64), np.zeros(max(nu, 1), np.int64)
+        ld, ud = np.zeros(max(el, 1), np.complex128), np.zeros(max(eu, 1), np.complex128)
+        if nl or nu:
+            lib().h2g_chain_record_blocks(self.h, li, ri, _i64(lp), _i64(lr), _d(ld.view(np.float64)), _i64(up), _i64(uc), _d(ud.view(np.float64)))
+        Lb, Ub = [], []
+        off = 0
+        for q in range(nl):
+            r = int(lr[q])
+            Lb.append((int(lp[q]), ld[off: off + r * e].reshape((r, e), order="F")))
+            off += r * e
+        off = 0
+        for q in range(nu):
+            c = int(uc[q])
+            Ub.append((int(up[q]), ud[off: off + e * c].reshape((e, c), order="F")))
+            off += e * c
+        return Lb, Ub
+
+    def root(self):
+        r = self.root_size
+        L = np.zeros((r, r), np.complex128, order="F")
+        U = np.zeros((r, r), np.complex128, order="F")
+        if r:
+            lib().h2g_chain_root(self.h, L.ctypes.data_as(_D), U.ctypes.data_as(_D))
+        return L, U
+
+    def hash(self):
+        return int(lib().h2g_chain_hash(self.h))
+
+    def timing(self):
+        f, s = C.c_double(), C.c_double()
+        fl, sl = C.c_int64(), C.c_int64()
+        lib().h2g_chain_timing(self.h, C.byref(f), C.byref(s), C.byref(fl), C.byref(sl))
+        return dict(factor_ms=f.value, solve_ms=s.value, factor_launches=fl.value, solve_launches=sl.value)
+
+    def work(self):
+        out = np.zeros(4)
+        lib().h2g_chain_work(self.h, _d(out))
+        return dict(factor_flops=out[0], schur_flops=out[1], solve_bytes=out[2], schur_bytes=out[3])
+
+    def _solve(self, b, mode):
+        b = np.asarray(b)
+        nrhs = 1 if b.ndim == 1 else b.shape[1]
+        n = b.shape[0]
+        bf = np.asfortranarray(b.reshape(n, nrhs), dtype=np.complex128)
+        x = np.zeros((n, nrhs), np.complex128, order="F")
+        err = _Err()
+        _check(lib().h2g_solve(self.h, bf.ctypes.data_as(_D), x.ctypes.data_as(_D), n, nrhs, mode, C.byref(err)), err)
+        return x[:, 0].copy() if b.ndim == 1 else x
+
+    def solve(self, b):
+        return self._solve(b, _SOLVE)
+
+    def forward(self, b):
+        return self._solve(b, _FORWARD)
+
+    def backward(self, y):
+        return self._solve(y, _BACKWARD)
+
+    def apply_inverse(self, b):
+        return self._solve(b, _APPLY_INVERSE)
+
+    def apply_inverse_explicit(self, b):
+        return self._solve(b, _APPLY_INVERSE_EXPLICIT)
+
+    def solve_device(self, ptr, n, nrhs=1, mode=_SOLVE):
+        """In-place solve on device memory (pointer from e.g. torch.Tensor.data_ptr())."""
+        err = _Err()
+        _check(lib().h2g_solve_device(self.h, C.cast(C.c_void_p(ptr), _D), n, nrhs, mode, C.byref(err)), err)
+
+
+def factorize(A, eps_fill_in, stop_level_override=None, schedule="reference"):
+    """factorize(A, eps_fill_in, stop_level_override) on the GPU."""
+    err = _Err()
+    h = _P()
+    stop = -1 if stop_level_override is None else int(stop_level_override)
+    if schedule not in SCHEDULES:
+        raise InvalidInputError(f"unknown schedule {schedule!r}")
+    _check(lib().h2g_factorize(A.ctx.h, A.h, float(eps_fill_in), stop, SCHEDULES[schedule], C.byref(h), C.byref(err)), err)
+    return FactorChain(h, A)
+
+
+def solve(chain, b):
+    return chain.solve(b)
+
+
+def apply_inverse(chain, b):
+    return chain.apply_inverse(b)
+
+
+def forward_substitute(chain, b):
+    return chain.forward(b)
+
+
+def backward_substitute(chain, y):
+    return chain.backward(y)
+
+
+def solve_in_place(chain, b):
+    """Overwrites the 1-D complex128 array b with the solution."""
+    if b.dtype != np.complex128 or not b.flags.c_contiguous:
+        raise InvalidInputError("solve_in_place: b must be a contiguous complex128 array")
+    b[...] = chain.solve(b)
+    return b
+
+
+def random_rhs(n, seed=1234):
+    """mt19937_64 + std::normal_distribution complex vector (original order)."""
+    out = np.zeros(n, np.complex128)
+    lib().h2g_random_rhs(n, seed, _d(out.view(np.float64)))
+    return out

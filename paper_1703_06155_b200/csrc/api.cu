@@ -1,0 +1,1230 @@
+// Host driver of the B200 H² factorize / solve: implements the C ABI of
+// include/h2g.h. The level loop mirrors factorize()
+// (proj/include/h2lu/factorization.hpp:600-653): per level, batches of
+// clusters run the step kernels of factor.cu; at the level boundary the host
+// reads back the final ranks (one small copy), finishes the level and merges
+// to the parent (finish_level :445-475, merge_permute :483-584) with
+// descriptor-driven batched copies/GEMMs; the remainder is LU-factored on the
+// device (:637-651). There is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/h2g.h"
+#include "build.cuh"
+#include "factor.cuh"
+#include "plan.hpp"
+#include "solve.cuh"
+
+using namespace h2g;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  int cluster = -1, level = -1;
+  long long pivot_index = -1;
+  double pivot_magnitude = 0.0;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+thread_local h2g_error g_last{};
+
+void set_error(h2g_error* out, int code, const char* msg, int cluster = -1, int level = -1, long long piv = -1, double mag = 0.0) {
+  h2g_error e{};
+  e.code = code;
+  e.cluster = cluster;
+  e.level = level;
+  e.pivot_index = piv;
+  e.pivot_magnitude = mag;
+  std::snprintf(e.msg, sizeof e.msg, "%s", msg);
+  g_last = e;
+  if (out) *out = e;
+}
+
+#define CK(x)                                                                                                   \
+  do {                                                                                                          \
+    cudaError_t e_ = (x);                                                                                       \
+    if (e_ != cudaSuccess) throw Error(H2G_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class F>
+int guarded(h2g_error* err, F&& f) {
+  try {
+    f();
+    if (err) *err = h2g_error{};
+    return H2G_OK;
+  } catch (const Error& e) {
+    set_error(err, e.code, e.what(), e.cluster, e.level, e.pivot_index, e.pivot_magnitude);
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    set_error(err, H2G_ERR_INVALID_INPUT, e.what());
+    return H2G_ERR_INVALID_INPUT;
+  } catch (const std::bad_alloc& e) {
+    set_error(err, H2G_ERR_CUDA, "host out of memory");
+    return H2G_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_error(err, H2G_ERR_INTERNAL, e.what());
+    return H2G_ERR_INTERNAL;
+  }
+}
+
+// ------------------------------------------------------------ device buffers
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr, o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, bytes = o.bytes, s = o.s;
+      o.p = nullptr, o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n, cudaStream_t st, bool zero = false) {
+    release();
+    s = st;
+    bytes = n;
+    if (n) {
+      CK(cudaMallocAsync(&p, n, st));
+      if (zero) CK(cudaMemsetAsync(p, 0, n, st));
+    }
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
+  b.alloc(std::max<size_t>(v.size(), 1) * sizeof(T), s);
+  if (!v.empty()) CK(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+// =============================================================== handles
+struct h2g_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevError* d_err = nullptr;
+  int* d_flag = nullptr;
+};
+
+struct PlanCache {
+  int stop = 0, schedule = 0;
+  std::vector<LevelSym> levels;
+  std::vector<LevelSchedule> sched;
+  std::vector<LevelWork> work;
+};
+
+struct h2g_matrix {
+  h2g_context* ctx = nullptr;
+  Structure S;
+  std::vector<int64_t> perm;
+  double eps_h2 = 0.0;
+  std::vector<int64_t> basis_rows, basis_rank, basis_off, coup_off, dense_off;
+  int64_t basis_elems = 0, coup_elems = 0, dense_elems = 0;
+  DBuf basis, coup, dense;
+  std::vector<std::unique_ptr<PlanCache>> plans;
+  std::mutex mu;
+};
+
+struct ChainLevelHost {
+  int level = 0;
+  std::vector<int64_t> rec;  // 10 per record
+  std::vector<int64_t> diag; // 9
+  std::vector<int64_t> src;  // permutation
+  // device-resident solve data
+  DBuf arena;                // chain numeric data of this level
+  DBuf meta;                 // packed int / offset arrays
+  SolveLevel sl{};
+  std::vector<int> batch_ptr;
+  const int* d_batch = nullptr;
+  std::vector<int> fs_ptr;
+  const SolveTargetD* d_fs = nullptr;
+  const SolveContribD* d_fc = nullptr;
+  DBuf d_src;
+  // host copies of sizes/offsets for downloads
+  std::vector<int> bsz, kfin, korig, R_ptr, R_nb, C_ptr, C_nb;
+  std::vector<long long> pos, Qt_off, L11_off, U11_off, Lbar_off, Ubar_off, Lself_off, Uself_off;
+  std::vector<int> rec_cluster;  // local id per record (record order)
+};
+
+struct h2g_chain {
+  h2g_context* ctx = nullptr;
+  int64_t n = 0;
+  int stop_level = 0;
+  int schedule = 0;
+  int depth = 0;
+  double eps = 0.0;
+  std::vector<std::unique_ptr<ChainLevelHost>> levels;
+  int64_t root_size = 0;
+  DBuf root;  // LU packed (n_root^2)
+  DBuf ybuf, tmpbuf;
+  size_t storage_bytes = 0;
+  double factor_ms = 0.0, solve_ms = 0.0;
+  long long factor_launches = 0, solve_launches = 0;
+  double factor_flops = 0.0, schur_flops = 0.0, solve_bytes = 0.0, schur_bytes = 0.0;
+};
+
+namespace {
+
+std::string fmt(const char* f, long long a = 0, long long b = 0) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, f, a, b);
+  return buf;
+}
+
+void check_device_error(h2g_context* ctx, int level_fallback) {
+  DevError e{};
+  CK(cudaMemcpyAsync(&e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (e.code == 0) return;
+  CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), ctx->stream));
+  if (e.code == H2G_ERR_SINGULAR_PIVOT) {
+    Error x(H2G_ERR_SINGULAR_PIVOT, e.cluster >= 0 ? fmt("partial_lu: pivot %lld below tolerance (cluster %lld)", e.pivot_index, e.cluster)
+                                                   : fmt("partial_lu: pivot %lld below tolerance (root block)", e.pivot_index));
+    x.cluster = e.cluster;
+    x.level = e.level >= 0 ? e.level : level_fallback;
+    x.pivot_index = e.pivot_index;
+    x.pivot_magnitude = e.pivot_magnitude;
+    throw x;
+  }
+  Error x(e.code, e.code == 1 ? fmt("unitary_completion: input columns are not orthonormal (cluster %lld)", e.cluster)
+                              : fmt("device error %lld at cluster %lld", e.code, e.cluster));
+  x.cluster = e.cluster;
+  x.level = e.level;
+  throw x;
+}
+
+PlanCache* get_plan(h2g_matrix* M, int stop, int schedule) {
+  std::lock_guard<std::mutex> g(M->mu);
+  for (auto& p : M->plans)
+    if (p->stop == stop && p->schedule == schedule) return p.get();
+  auto P = std::make_unique<PlanCache>();
+  P->stop = stop;
+  P->schedule = schedule;
+  P->levels = build_levels(M->S, stop);
+  for (const auto& L : P->levels) {
+    if (L.level >= stop && stop <= M->S.depth) {
+      P->sched.push_back(build_schedule(L, schedule));
+      P->work.push_back(build_work(L, P->sched.back()));
+    }
+  }
+  M->plans.push_back(std::move(P));
+  return M->plans.back().get();
+}
+
+// Packs host arrays into one device buffer; returns device pointers.
+struct Packer {
+  std::vector<char> host;
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    size_t off = (host.size() + 15) & ~size_t(15);
+    host.resize(off + std::max<size_t>(v.size(), 1) * sizeof(T));
+    if (!v.empty()) std::memcpy(host.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+  template <class T>
+  size_t add_raw(const T* p, size_t n) {
+    size_t off = (host.size() + 15) & ~size_t(15);
+    host.resize(off + std::max<size_t>(n, 1) * sizeof(T));
+    if (n) std::memcpy(host.data() + off, p, n * sizeof(T));
+    return off;
+  }
+  void upload(DBuf& b, cudaStream_t s) {
+    b.alloc(host.size() + 16, s);
+    CK(cudaMemcpyAsync(b.p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+  }
+};
+
+template <class T>
+T* at(const DBuf& b, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(b.p) + off);
+}
+
+int pick_gram_parts(int maxlist) { return std::max(1, std::min(32, (maxlist + 3) / 4)); }
+
+struct LevelData {
+  // level-entry sizes
+  std::vector<int> bsz, korig;
+  std::vector<long long> pos;
+  int bmax = 0;
+  DBuf D, F, fex, V0, Vp;
+};
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* h2g_version(void) { return "h2g 0.1 (sm_100a)"; }
+
+int h2g_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int h2g_last_error(h2g_error* err) {
+  if (err) *err = g_last;
+  return g_last.code;
+}
+
+int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
+  return guarded(err, [&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) throw Error(H2G_ERR_CUDA, "no CUDA device available (h2g has no CPU fallback)");
+    if (device < 0 || device >= n) throw Error(H2G_ERR_INVALID_INPUT, "bad device index");
+    CK(cudaSetDevice(device));
+    auto* c = new h2g_context();
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaMalloc(&c->d_err, sizeof(DevError)));
+    CK(cudaMemset(c->d_err, 0, sizeof(DevError)));
+    CK(cudaMalloc(&c->d_flag, 64));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+  });
+}
+
+int h2g_context_destroy(h2g_context* ctx) {
+  if (!ctx) return H2G_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_flag);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return H2G_OK;
+}
+
+int h2g_matrix_upload(h2g_context* ctx, const h2g_matrix_desc* d, h2g_matrix** out, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !d || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    CK(cudaSetDevice(ctx->device));
+    auto M = std::make_unique<h2g_matrix>();
+    M->ctx = ctx;
+    M->S = structure_from_desc(d);
+    M->eps_h2 = d->eps_h2;
+    const Structure& S = M->S;
+    const int nc = S.num_clusters();
+    M->basis_rows.assign(d->basis_rows, d->basis_rows + nc);
+    M->basis_rank.assign(d->basis_rank, d->basis_rank + nc);
+    M->basis_off.assign(d->basis_offset, d->basis_offset + nc);
+    for (int id = 0; id < nc; ++id) {
+      const bool leaf = id >= Structure::first(S.depth);
+      const int64_t rows = leaf ? S.end[id] - S.begin[id] : M->basis_rank[2 * id + 1] + M->basis_rank[2 * id + 2];
+      if (M->basis_rows[id] != rows) throw Error(H2G_ERR_INVALID_INPUT, fmt("basis of cluster %lld has %lld rows", id, M->basis_rows[id]));
+      M->basis_elems = std::max<int64_t>(M->basis_elems, M->basis_off[id] + rows * M->basis_rank[id]);
+    }
+    const int64_t na = S.num_adm();
+    M->coup_off.assign(d->coupling_offset, d->coupling_offset + na);
+    for (int l = 0; l <= S.depth; ++l)
+      for (size_t q = 0; q < S.adm[l].size(); ++q) {
+        const int64_t g = S.adm_offset[l] + static_cast<int64_t>(q);
+        M->coup_elems = std::max<int64_t>(M->coup_elems, M->coup_off[g] + M->basis_rank[S.adm[l][q].row] * M->basis_rank[S.adm[l][q].col]);
+      }
+    M->dense_off.assign(d->dense_offset, d->dense_offset + d->num_leaf_pairs);
+    for (size_t q = 0; q < S.leaf.size(); ++q) {
+      const auto& p = S.leaf[q];
+      M->dense_elems = std::max<int64_t>(M->dense_elems, M->dense_off[q] + (S.end[p.row] - S.begin[p.row]) * (S.end[p.col] - S.begin[p.col]));
+    }
+    cudaStream_t s = ctx->stream;
+    M->basis.alloc(std::max<int64_t>(M->basis_elems, 1) * 16, s);
+    M->coup.alloc(std::max<int64_t>(M->coup_elems, 1) * 16, s);
+    M->dense.alloc(std::max<int64_t>(M->dense_elems, 1) * 16, s);
+    if (M->basis_elems) CK(cudaMemcpyAsync(M->basis.p, d->basis_data, M->basis_elems * 16, cudaMemcpyHostToDevice, s));
+    if (M->coup_elems) CK(cudaMemcpyAsync(M->coup.p, d->coupling_data, M->coup_elems * 16, cudaMemcpyHostToDevice, s));
+    if (M->dense_elems) CK(cudaMemcpyAsync(M->dense.p, d->dense_data, M->dense_elems * 16, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    *out = M.release();
+  });
+}
+
+int h2g_matrix_build(h2g_context* ctx, const double* points, int64_t n, int64_t leafsize, double eta, const h2g_kernel_spec* kernel,
+                     double eps_h2, h2g_matrix** out, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !points || !kernel || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    if (eps_h2 <= 0.0) throw Error(H2G_ERR_INVALID_INPUT, "build_h2: eps_h2 must be positive");
+    CK(cudaSetDevice(ctx->device));
+    auto M = std::make_unique<h2g_matrix>();
+    M->ctx = ctx;
+    M->S = build_structure(points, n, leafsize, eta, &M->perm);
+    M->eps_h2 = eps_h2;
+    BuildResult R = build_h2_device(M->S, points, M->perm, *kernel, eps_h2, ctx->stream);
+    M->basis_rows = std::move(R.basis_rows);
+    M->basis_rank = std::move(R.basis_rank);
+    M->basis_off = std::move(R.basis_off);
+    M->coup_off = std::move(R.coup_off);
+    M->dense_off = std::move(R.dense_off);
+    M->basis_elems = R.basis_elems;
+    M->coup_elems = R.coup_elems;
+    M->dense_elems = R.dense_elems;
+    M->basis.p = R.basis;
+    M->basis.s = ctx->stream;
+    M->coup.p = R.coup;
+    M->coup.s = ctx->stream;
+    M->dense.p = R.dense;
+    M->dense.s = ctx->stream;
+    *out = M.release();
+  });
+}
+
+int h2g_matrix_destroy(h2g_matrix* m) {
+  if (!m) return H2G_OK;
+  cudaSetDevice(m->ctx->device);
+  delete m;
+  return H2G_OK;
+}
+
+int h2g_matrix_sizes(const h2g_matrix* m, int64_t* s) {
+  if (!m || !s) return H2G_ERR_INVALID_INPUT;
+  s[0] = m->S.n;
+  s[1] = m->S.depth;
+  s[2] = m->S.num_clusters();
+  s[3] = m->S.num_adm();
+  s[4] = static_cast<int64_t>(m->S.leaf.size());
+  s[5] = m->basis_elems;
+  s[6] = m->coup_elems;
+  s[7] = m->dense_elems;
+  return H2G_OK;
+}
+
+int h2g_matrix_download(const h2g_matrix* m, int64_t* cb, int64_t* ce, int64_t* perm, int64_t* adm_off, int32_t* adm_pairs, int64_t* split_off,
+                        int32_t* split_pairs, int32_t* leaf_pairs, int64_t* basis_rows, int64_t* basis_rank, int64_t* basis_offset,
+                        double* basis_data, int64_t* coupling_offset, double* coupling_data, int64_t* dense_offset, double* dense_data) {
+  return guarded(nullptr, [&] {
+    const Structure& S = m->S;
+    const int nc = S.num_clusters();
+    cudaStream_t s = m->ctx->stream;
+    if (cb) std::copy(S.begin.begin(), S.begin.begin() + nc, cb);
+    if (ce) std::copy(S.end.begin(), S.end.begin() + nc, ce);
+    if (perm) {
+      if (m->perm.empty())
+        for (int64_t i = 0; i < S.n; ++i) perm[i] = i;
+      else
+        std::copy(m->perm.begin(), m->perm.end(), perm);
+    }
+    int64_t qa = 0, qs = 0;
+    for (int l = 0; l <= S.depth; ++l) {
+      if (adm_off) adm_off[l] = qa;
+      if (split_off) split_off[l] = qs;
+      for (const auto& p : S.adm[l]) {
+        if (adm_pairs) adm_pairs[2 * qa] = p.row, adm_pairs[2 * qa + 1] = p.col;
+        ++qa;
+      }
+      for (const auto& p : S.split[l]) {
+        if (split_pairs) split_pairs[2 * qs] = p.row, split_pairs[2 * qs + 1] = p.col;
+        ++qs;
+      }
+    }
+    if (adm_off) adm_off[S.depth + 1] = qa;
+    if (split_off) split_off[S.depth + 1] = qs;
+    if (leaf_pairs)
+      for (size_t q = 0; q < S.leaf.size(); ++q) leaf_pairs[2 * q] = S.leaf[q].row, leaf_pairs[2 * q + 1] = S.leaf[q].col;
+    if (basis_rows) std::copy(m->basis_rows.begin(), m->basis_rows.end(), basis_rows);
+    if (basis_rank) std::copy(m->basis_rank.begin(), m->basis_rank.end(), basis_rank);
+    if (basis_offset) std::copy(m->basis_off.begin(), m->basis_off.end(), basis_offset);
+    if (coupling_offset) std::copy(m->coup_off.begin(), m->coup_off.end(), coupling_offset);
+    if (dense_offset) std::copy(m->dense_off.begin(), m->dense_off.end(), dense_offset);
+    if (basis_data && m->basis_elems) CK(cudaMemcpyAsync(basis_data, m->basis.p, m->basis_elems * 16, cudaMemcpyDeviceToHost, s));
+    if (coupling_data && m->coup_elems) CK(cudaMemcpyAsync(coupling_data, m->coup.p, m->coup_elems * 16, cudaMemcpyDeviceToHost, s));
+    if (dense_data && m->dense_elems) CK(cudaMemcpyAsync(dense_data, m->dense.p, m->dense_elems * 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  });
+}
+
+int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y, int32_t nrhs, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !m || !x || !y || nrhs < 1) throw Error(H2G_ERR_INVALID_INPUT, "matvec: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    matvec_device(m->S, m->basis_rows, m->basis_rank, m->basis_off, m->coup_off, m->dense_off, m->basis.as<cplx>(), m->coup.as<cplx>(),
+                  m->dense.as<cplx>(), x, y, nrhs, ctx->stream);
+  });
+}
+
+// ------------------------------------------------------------- factorize
+int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t stop_level, int32_t schedule, h2g_chain** out, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !mc || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    if (!(eps > 0.0)) throw Error(H2G_ERR_INVALID_INPUT, "factorize: eps_fill_in must be positive");
+    if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED) throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
+    CK(cudaSetDevice(ctx->device));
+    h2g_matrix* M = const_cast<h2g_matrix*>(mc);
+    const Structure& S = M->S;
+    const int L = S.depth, l0 = S.l0;
+    int stop = L + 1;
+    if (l0 >= 0) {
+      stop = stop_level >= 0 ? stop_level : l0;
+      if (stop < l0 || stop > L)
+        throw Error(H2G_ERR_INVALID_INPUT, fmt("factorize: stop level %lld outside [l0, depth] = [%lld, depth]", stop, l0));
+    }
+    cudaStream_t st = ctx->stream;
+    PlanCache* P = get_plan(M, stop, schedule);
+
+    auto C = std::make_unique<h2g_chain>();
+    C->ctx = ctx;
+    C->n = S.n;
+    C->stop_level = stop;
+    C->schedule = schedule;
+    C->depth = L;
+    C->eps = eps;
+    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), st));
+    CK(cudaEventRecord(ctx->ev0, st));
+    long long launches = 0;
+    double flops = 0.0, sflops = 0.0, sbytes = 0.0;
+
+    // ---- leaf level entry state
+    LevelData cur;
+    {
+      const int nl = 1 << L, first = Structure::first(L);
+      cur.bsz.resize(nl);
+      cur.korig.resize(nl);
+      cur.pos.resize(nl);
+      for (int t = 0; t < nl; ++t) {
+        cur.bsz[t] = static_cast<int>(S.end[first + t] - S.begin[first + t]);
+        cur.korig[t] = static_cast<int>(M->basis_rank[first + t]);
+        cur.pos[t] = S.begin[first + t];
+      }
+      cur.bmax = std::max(1, *std::max_element(cur.bsz.begin(), cur.bsz.end()));
+      const size_t bb = (size_t)cur.bmax * cur.bmax * 16;
+      const LevelSym& Y = P->levels[0];
+      cur.D.alloc(std::max<size_t>(Y.drow.size(), 1) * bb, st, true);
+      cur.V0.alloc((size_t)nl * bb, st, true);
+      std::vector<CopyDesc> cd;
+      for (size_t q = 0; q < Y.drow.size(); ++q) {
+        const int r = Y.drow[q], c = Y.dcol[q];
+        cd.push_back({M->dense.as<cplx>() + M->dense_off[q], at<cplx>(cur.D, q * bb), cur.bsz[r], cur.bsz[r], cur.bsz[r], cur.bsz[c], 0, 0});
+      }
+      for (int t = 0; t < nl; ++t)
+        if (cur.korig[t] > 0)
+          cd.push_back({M->basis.as<cplx>() + M->basis_off[first + t], at<cplx>(cur.V0, t * bb), cur.bsz[t], cur.bsz[t], cur.bsz[t], cur.korig[t], 0, 0});
+      DBuf dd;
+      upload(dd, cd, st);
+      launch_copy(dd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
+      ++launches;
+      cur.F.alloc(std::max<size_t>(Y.frow.size(), 1) * bb, st, true);
+      cur.fex.alloc(std::max<size_t>(Y.frow.size(), 1) * 4, st, true);
+      CK(cudaStreamSynchronize(st));
+    }
+
+    int li = 0;
+    int last_level = L;  // level whose state is "cur" at the root
+    if (stop <= L) {
+      for (int l = L; l >= stop; --l, ++li) {
+        const LevelSym& Y = P->levels[li];
+        const LevelSchedule& SC = P->sched[li];
+        const LevelWork& W = P->work[li];
+        const int nl = Y.nl;
+        const int bm = cur.bmax;
+        if (bm > 64) throw Error(H2G_ERR_INTERNAL, fmt("level %lld: block size %lld > 64 not supported yet", l, bm));
+        const size_t bb = (size_t)bm * bm;
+        // ---- chain offsets (upper bound e <= b - korig)
+        std::vector<long long> Qt_off(nl), L11_off(nl), U11_off(nl), Linv_off(nl), Uinv_off(nl), Lself_off(nl), Uself_off(nl);
+        std::vector<long long> Lbar_off(Y.R_nb.size()), Ubar_off(Y.C_nb.size());
+        long long top = 0;
+        for (int t = 0; t < nl; ++t) {
+          const long long b = cur.bsz[t], em = b - cur.korig[t];
+          Qt_off[t] = top, top += b * b;
+          L11_off[t] = top, top += em * em;
+          U11_off[t] = top, top += em * em;
+          Linv_off[t] = top, top += em * em;
+          Uinv_off[t] = top, top += em * em;
+          Lself_off[t] = top, top += b * em;
+          Uself_off[t] = top, top += b * em;
+          for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) Lbar_off[a] = top, top += (long long)cur.bsz[Y.R_nb[a]] * em;
+          for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) Ubar_off[a] = top, top += (long long)cur.bsz[Y.C_nb[a]] * em;
+        }
+        auto CL = std::make_unique<ChainLevelHost>();
+        CL->level = l;
+        CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
+        DBuf lift;
+        lift.alloc(std::max<long long>(top, 1) * 16, st);
+        // ---- per-level device metadata
+        Packer pk;
+        std::vector<int> posi(nl);
+        std::vector<long long> posl(cur.pos.begin(), cur.pos.end());
+        size_t o_bsz = pk.add(cur.bsz), o_korig = pk.add(cur.korig), o_pos = pk.add(posl);
+        std::vector<int> kfin0(cur.korig);
+        size_t o_kfin = pk.add(kfin0);
+        size_t o_drow = pk.add(Y.drow), o_dcol = pk.add(Y.dcol), o_diag = pk.add(Y.diag_blk);
+        size_t o_frow = pk.add(Y.frow), o_fcol = pk.add(Y.fcol);
+        size_t o_Rp = pk.add(Y.R_ptr), o_Rn = pk.add(Y.R_nb), o_Cp = pk.add(Y.C_ptr), o_Cn = pk.add(Y.C_nb);
+        size_t o_Gp = pk.add(Y.G_ptr), o_Gf = pk.add(Y.G_fill), o_Gt = pk.add(Y.G_tr);
+        size_t o_Qt = pk.add(Qt_off), o_L11 = pk.add(L11_off), o_U11 = pk.add(U11_off), o_Li = pk.add(Linv_off), o_Ui = pk.add(Uinv_off);
+        size_t o_Lb = pk.add(Lbar_off), o_Ub = pk.add(Ubar_off), o_Ls = pk.add(Lself_off), o_Us = pk.add(Uself_off);
+        size_t o_bat = pk.add(SC.batch_cl);
+        size_t o_pan = pk.add_raw(reinterpret_cast<const PanelItemD*>(W.panel.data()), W.panel.size());
+        size_t o_sch = pk.add_raw(reinterpret_cast<const SchurTargetD*>(W.schur.data()), W.schur.size());
+        size_t o_con = pk.add_raw(reinterpret_cast<const SchurContribD*>(W.contrib.data()), W.contrib.size());
+        size_t o_fs = pk.add_raw(reinterpret_cast<const SolveTargetD*>(W.fsolve.data()), W.fsolve.size());
+        size_t o_fc = pk.add_raw(reinterpret_cast<const SolveContribD*>(W.fcontrib.data()), W.fcontrib.size());
+        pk.upload(CL->meta, st);
+        const DBuf& mt = CL->meta;
+        // gram partial buffers
+        int maxlist = 0;
+        for (int t = 0; t < nl; ++t) maxlist = std::max(maxlist, Y.G_ptr[t + 1] - Y.G_ptr[t]);
+        const int GP = pick_gram_parts(maxlist);
+        DBuf gram, gcm;
+        gram.alloc((size_t)std::max(1, W.max_batch) * GP * bb * 16, st);
+        gcm.alloc((size_t)std::max(1, W.max_batch) * GP * 8, st);
+        cur.Vp.alloc((size_t)nl * bb * 16, st, true);
+
+        DevLevel DL{};
+        DL.level = l;
+        DL.nl = nl;
+        DL.bmax = bm;
+        DL.eps = eps;
+        DL.bsz = at<int>(mt, o_bsz);
+        DL.pos = at<int>(mt, o_pos);  // unused on device (long long copy kept for solve)
+        DL.korig = at<int>(mt, o_korig);
+        DL.kfin = at<int>(mt, o_kfin);
+        DL.D = cur.D.as<cplx>();
+        DL.drow = at<int>(mt, o_drow);
+        DL.dcol = at<int>(mt, o_dcol);
+        DL.diag_blk = at<int>(mt, o_diag);
+        DL.F = cur.F.as<cplx>();
+        DL.fexists = cur.fex.as<int>();
+        DL.frow = at<int>(mt, o_frow);
+        DL.fcol = at<int>(mt, o_fcol);
+        DL.R_ptr = at<int>(mt, o_Rp);
+        DL.R_nb = at<int>(mt, o_Rn);
+        DL.C_ptr = at<int>(mt, o_Cp);
+        DL.C_nb = at<int>(mt, o_Cn);
+        DL.G_ptr = at<int>(mt, o_Gp);
+        DL.G_fill = at<int>(mt, o_Gf);
+        DL.G_tr = at<unsigned char>(mt, o_Gt);
+        DL.V0 = cur.V0.as<cplx>();
+        DL.Vp = cur.Vp.as<cplx>();
+        DL.chain = CL->arena.as<cplx>();
+        DL.Qt_off = at<long long>(mt, o_Qt);
+        DL.L11_off = at<long long>(mt, o_L11);
+        DL.U11_off = at<long long>(mt, o_U11);
+        DL.Lbar_off = at<long long>(mt, o_Lb);
+        DL.Ubar_off = at<long long>(mt, o_Ub);
+        DL.Lself_off = at<long long>(mt, o_Ls);
+        DL.Uself_off = at<long long>(mt, o_Us);
+        DL.lift = lift.as<cplx>();
+        DL.Linv_off = at<long long>(mt, o_Li);
+        DL.Uinv_off = at<long long>(mt, o_Ui);
+        DL.gram = gram.as<cplx>();
+        DL.gram_cmax = gcm.as<double>();
+        DL.gram_parts = GP;
+        DL.err = ctx->d_err;
+
+        launch_complement(DL, st);
+        ++launches;
+        const int nbat = static_cast<int>(SC.batch_ptr.size()) - 1;
+        const int* d_bat = at<int>(mt, o_bat);
+        const PanelItemD* d_pan = at<PanelItemD>(mt, o_pan);
+        const SchurTargetD* d_sch = at<SchurTargetD>(mt, o_sch);
+        const SchurContribD* d_con = at<SchurContribD>(mt, o_con);
+        for (int bi = 0; bi < nbat; ++bi) {
+          const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
+          launch_gram(DL, d_bat + p0, nb, st);
+          launch_head(DL, d_bat + p0, nb, st);
+          launch_panel(DL, d_bat + p0, d_pan + W.panel_ptr[bi], W.panel_ptr[bi + 1] - W.panel_ptr[bi], st);
+          launch_schur(DL, d_sch + W.schur_ptr[bi], W.schur_ptr[bi + 1] - W.schur_ptr[bi], d_con, st);
+          launches += 2 + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
+        }
+        CK(cudaGetLastError());
+        check_device_error(ctx, l);
+        // ---- read back final ranks and fill existence
+        std::vector<int> kfin(nl), fex(Y.frow.size());
+        CK(cudaMemcpyAsync(kfin.data(), DL.kfin, nl * 4, cudaMemcpyDeviceToHost, st));
+        if (!fex.empty()) CK(cudaMemcpyAsync(fex.data(), DL.fexists, fex.size() * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+
+        // ---- records + diagnostics
+        long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
+        std::vector<int> rec_order;
+        if (schedule == H2G_SCHEDULE_REFERENCE) {
+          for (int t = 0; t < nl; ++t) rec_order.push_back(t);
+        } else {
+          rec_order = SC.batch_cl;
+        }
+        size_t lvl_bytes = 0;
+        for (int t : rec_order) {
+          const int b = cur.bsz[t], kf = kfin[t], e = b - kf;
+          const int nr = Y.R_ptr[t + 1] - Y.R_ptr[t], ncn = Y.C_ptr[t + 1] - Y.C_ptr[t];
+          const int nlb = e > 0 ? nr + (kf > 0) : 0, nub = e > 0 ? ncn + (kf > 0) : 0;
+          const int64_t r[10] = {Y.first + t, l, cur.pos[t], b, e, cur.korig[t], kf, e > 0 ? (int64_t)nlb * nub : 0, nlb, nub};
+          CL->rec.insert(CL->rec.end(), r, r + 10);
+          CL->rec_cluster.push_back(t);
+          lvl_bytes += 16 * ((size_t)b * b + 2 * (size_t)e * e);
+          if (e > 0) {
+            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) lvl_bytes += 16 * (size_t)cur.bsz[Y.R_nb[a]] * e;
+            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) lvl_bytes += 16 * (size_t)cur.bsz[Y.C_nb[a]] * e;
+            if (kf > 0) lvl_bytes += 16 * 2 * (size_t)kf * e;
+          }
+          rsb += cur.korig[t];
+          rsa += kf;
+          elim += e;
+          // algorithmic flops (SURVEY §8d F_factor)
+          const double bd = b, ed = e, md = b - cur.korig[t];
+          double gram_cols = 0;
+          for (int f = Y.G_ptr[t]; f < Y.G_ptr[t + 1]; ++f)
+            if (fex[Y.G_fill[f]]) gram_cols += Y.G_tr[f] ? cur.bsz[Y.frow[Y.G_fill[f]]] : cur.bsz[Y.fcol[Y.G_fill[f]]];
+          flops += 8.0 * md * bd * gram_cols + 8.0 * md * md * gram_cols;  // Vp^H W and Y Y^H
+          flops += 16.0 * bd * bd * bd;                                      // rotation of D(t,t)
+          double rot = 0;
+          for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) rot += cur.bsz[Y.R_nb[a]];
+          for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) rot += cur.bsz[Y.C_nb[a]];
+          flops += 8.0 * bd * bd * rot;  // step 2 on off-diagonal blocks
+          if (e > 0) {
+            flops += 8.0 / 3.0 * ed * ed * ed + 4.0 * ed * ed * (rot + 2.0 * kf);  // LU + TRSMs
+            // Schur: sum_j b_j * e * sum_c b_c (incl. self rows/cols of kf)
+            double rows = kf, cols = kf;
+            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) rows += cur.bsz[Y.R_nb[a]];
+            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) cols += cur.bsz[Y.C_nb[a]];
+            const double sch = 8.0 * rows * ed * cols;
+            flops += sch;
+            sflops += sch;
+            sbytes += 16.0 * 2.0 * rows * cols;  // read + write of every target entry
+          }
+        }
+        for (size_t f = 0; f < Y.frow.size(); ++f)
+          if (Y.fadm[f] >= 0 && fex[f]) ++ledger;
+        // ---- permutation (merge_permute :492-509)
+        const int lp = l - 1;
+        const int nlp = nl / 2;
+        std::vector<long long> src;
+        src.reserve(S.n);
+        for (int P2 = 0; P2 < nlp; ++P2)
+          for (int ch = 2 * P2; ch <= 2 * P2 + 1; ++ch) {
+            const long long base = cur.pos[ch] + (cur.bsz[ch] - kfin[ch]);
+            for (int q = 0; q < kfin[ch]; ++q) src.push_back(base + q);
+          }
+        const long long active_new = static_cast<long long>(src.size());
+        for (int t = 0; t < nl; ++t)
+          for (int q = 0; q < cur.bsz[t] - kfin[t]; ++q) src.push_back(cur.pos[t] + q);
+        lvl_bytes += 8 * src.size();
+        C->storage_bytes += lvl_bytes;
+        CL->diag = {l, (int64_t)rec_order.size(), rsb, rsa, elim, ledger, (int64_t)C->storage_bytes, (int64_t)src.size(), active_new};
+        CL->src.assign(src.begin(), src.end());
+        upload(CL->d_src, CL->src, st);
+
+        // ---- keep solve data
+        CL->bsz = cur.bsz;
+        CL->kfin = kfin;
+        CL->korig = cur.korig;
+        CL->pos = posl;
+        CL->R_ptr = Y.R_ptr;
+        CL->R_nb = Y.R_nb;
+        CL->C_ptr = Y.C_ptr;
+        CL->C_nb = Y.C_nb;
+        CL->Qt_off = Qt_off;
+        CL->L11_off = L11_off;
+        CL->U11_off = U11_off;
+        CL->Lbar_off = Lbar_off;
+        CL->Ubar_off = Ubar_off;
+        CL->Lself_off = Lself_off;
+        CL->Uself_off = Uself_off;
+        CL->batch_ptr = SC.batch_ptr;
+        CL->d_batch = d_bat;
+        CL->fs_ptr = W.fsolve_ptr;
+        CL->d_fs = at<SolveTargetD>(mt, o_fs);
+        CL->d_fc = at<SolveContribD>(mt, o_fc);
+        SolveLevel& SL = CL->sl;
+        SL.nl = nl;
+        SL.bmax = bm;
+        SL.bsz = DL.bsz;
+        SL.pos = at<long long>(mt, o_pos);
+        SL.kfin = DL.kfin;
+        SL.C_ptr = DL.C_ptr;
+        SL.C_nb = DL.C_nb;
+        SL.chain = DL.chain;
+        SL.Qt_off = DL.Qt_off;
+        SL.L11_off = DL.L11_off;
+        SL.U11_off = DL.U11_off;
+        SL.Linv_off = DL.Linv_off;
+        SL.Uinv_off = DL.Uinv_off;
+        SL.Lbar_off = DL.Lbar_off;
+        SL.Ubar_off = DL.Ubar_off;
+        SL.Lself_off = DL.Lself_off;
+        SL.Uself_off = DL.Uself_off;
+        // solve traffic (nrhs = 1): chain read (Qtilde twice) + vector
+        C->solve_bytes += (double)lvl_bytes;
+        for (int t = 0; t < nl; ++t) C->solve_bytes += 16.0 * (double)cur.bsz[t] * cur.bsz[t];  // second Qtilde pass
+        C->solve_bytes += 4.0 * 16.0 * (double)S.n;
+
+        // ---- merge to level lp (finish_level + merge_permute)
+        const LevelSym& YP = P->levels[li + 1];
+        LevelData nxt;
+        nxt.bsz.resize(nlp);
+        nxt.korig.resize(nlp);
+        nxt.pos.resize(nlp);
+        long long off = 0;
+        const int firstp = Structure::first(lp);
+        for (int P2 = 0; P2 < nlp; ++P2) {
+          nxt.bsz[P2] = kfin[2 * P2] + kfin[2 * P2 + 1];
+          nxt.korig[P2] = static_cast<int>(M->basis_rank[firstp + P2]);
+          nxt.pos[P2] = off;
+          off += nxt.bsz[P2];
+        }
+        if (off != active_new) throw Error(H2G_ERR_INVALID_INPUT, "merge_permute: parent layout does not match the permutation");
+        nxt.bmax = std::max(1, *std::max_element(nxt.bsz.begin(), nxt.bsz.end()));
+        const size_t bbp = (size_t)nxt.bmax * nxt.bmax;
+        nxt.D.alloc(std::max<size_t>(YP.drow.size(), 1) * bbp * 16, st, true);
+        nxt.F.alloc(std::max<size_t>(YP.frow.size(), 1) * bbp * 16, st, true);
+        nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
+        nxt.V0.alloc((size_t)nlp * bbp * 16, st, true);
+        std::vector<CopyDesc> cd;
+        std::vector<GemmDesc> g1, g2;
+        long long tmp_top = 0;
+        std::vector<long long> tmp_off;
+        cplx* Dp = nxt.D.as<cplx>();
+        cplx* Fp = nxt.F.as<cplx>();
+        const cplx* chainp = CL->arena.as<cplx>();
+        auto Vptr = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kfin[t]) * cur.bsz[t]; };
+        struct PendingG {
+          int a, c, fi;
+          cplx* dst;
+          int ldd;
+        };
+        std::vector<PendingG> pend;
+        const auto& admL = S.adm[l];
+        for (size_t pq = 0; pq < YP.drow.size(); ++pq) {
+          const int Pr = YP.drow[pq], Pc = YP.dcol[pq];
+          cplx* dst = Dp + pq * bbp;
+          const int ldd = nxt.bsz[Pr];
+          for (int ia = 0; ia < 2; ++ia)
+            for (int ic = 0; ic < 2; ++ic) {
+              const int a = 2 * Pr + ia, c = 2 * Pc + ic;
+              const int ro = ia ? kfin[2 * Pr] : 0, co = ic ? kfin[2 * Pc] : 0;
+              const int di = Y.dense_index(a, c);
+              if (di >= 0) {
+                const int ea = cur.bsz[a] - kfin[a], ec = cur.bsz[c] - kfin[c];
+                if (kfin[a] && kfin[c])
+                  cd.push_back({cur.D.as<cplx>() + di * bb + ea + (size_t)ec * cur.bsz[a], dst + ro + (size_t)co * ldd, cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
+              } else {
+                const Pair hp{a + Y.first, c + Y.first};
+                auto it = std::lower_bound(admL.begin(), admL.end(), hp, [](const Pair& x, const Pair& y) { return x.row < y.row || (x.row == y.row && x.col < y.col); });
+                if (it == admL.end() || it->row != hp.row || it->col != hp.col)
+                  throw Error(H2G_ERR_INVALID_INPUT, "merge_permute: child block is neither dense nor admissible");
+                const int64_t gi = S.adm_offset[l] + (it - admL.begin());
+                const int ka = cur.korig[a], kc = cur.korig[c];
+                if (ka && kc) cd.push_back({M->coup.as<cplx>() + M->coup_off[gi], dst + ro + (size_t)co * ldd, ka, ldd, ka, kc, 0, 0});
+                const int fi = Y.fill_index(a, c);
+                if (fi >= 0 && fex[fi] && kfin[a] && kfin[c]) pend.push_back({a, c, fi, dst + ro + (size_t)co * ldd, ldd});
+              }
+            }
+        }
+        std::vector<int> fexp(YP.frow.size(), 0);
+        for (size_t f = 0; f < Y.frow.size(); ++f) {
+          if (Y.fadm[f] >= 0 || !fex[f]) continue;
+          const int pf = Y.carried_parent[f];
+          if (pf < 0) throw Error(H2G_ERR_INTERNAL, "carried fill without a parent target");
+          fexp[pf] = 1;
+          const int j = Y.frow[f], c = Y.fcol[f];
+          if (!kfin[j] || !kfin[c]) continue;
+          const int ro = (j & 1) ? kfin[j - 1] : 0, co = (c & 1) ? kfin[c - 1] : 0;
+          const int ldd = nxt.bsz[YP.frow[pf]];
+          pend.push_back({j, c, static_cast<int>(f), Fp + (size_t)pf * bbp + ro + (size_t)co * ldd, ldd});
+        }
+        for (const auto& pg : pend) {
+          const int a = pg.a, c = pg.c;
+          tmp_off.push_back(tmp_top);
+          tmp_top += (long long)kfin[a] * cur.bsz[c];
+        }
+        DBuf tmp;
+        tmp.alloc(std::max<long long>(tmp_top, 1) * 16, st);
+        for (size_t q = 0; q < pend.size(); ++q) {
+          const auto& pg = pend[q];
+          const int a = pg.a, c = pg.c;
+          cplx* X = tmp.as<cplx>() + tmp_off[q];
+          // X = V_a^H F (kfin_a x b_c);  dst += X conj(V_c)   (factorization.hpp:455, :540)
+          g1.push_back({Vptr(a), cur.F.as<cplx>() + (size_t)pg.fi * bb, X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
+          g2.push_back({X, Vptr(c), pg.dst, kfin[a], cur.bsz[c], pg.ldd, kfin[a], kfin[c], cur.bsz[c], OP_N, OP_R, 1.0, 1.0});
+        }
+        // padded transfers (finish_level :464-474)
+        for (int P2 = 0; P2 < nlp; ++P2) {
+          const int id = firstp + P2;
+          const int k1 = cur.korig[2 * P2], k2 = cur.korig[2 * P2 + 1], kp = nxt.korig[P2];
+          const int rows = static_cast<int>(M->basis_rows[id]);
+          const cplx* T = M->basis.as<cplx>() + M->basis_off[id];
+          cplx* dst = nxt.V0.as<cplx>() + (size_t)P2 * bbp;
+          if (kp == 0) continue;
+          if (k1) cd.push_back({T, dst, rows, nxt.bsz[P2], k1, kp, 0, 0});
+          if (k2) cd.push_back({T + k1, dst + kfin[2 * P2], rows, nxt.bsz[P2], k2, kp, 0, 0});
+        }
+        DBuf dcd, dg1, dg2;
+        upload(dcd, cd, st);
+        upload(dg1, g1, st);
+        upload(dg2, g2, st);
+        launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
+        launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st);
+        launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st);
+        launches += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
+        if (!fexp.empty()) CK(cudaMemcpyAsync(nxt.fex.p, fexp.data(), fexp.size() * 4, cudaMemcpyHostToDevice, st));
+        for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));  // temporaries die here
+
+        C->levels.push_back(std::move(CL));
+        cur = std::move(nxt);
+        last_level = lp;
+        if (elim == 0 && l > stop) {
+          C->stop_level = l;
+          ++li;
+          break;
+        }
+      }
+    }
+
+    // ---- root (factorization.hpp:637-651)
+    {
+      const int lv = last_level;
+      const LevelSym* YR = nullptr;
+      for (const auto& Y : P->levels)
+        if (Y.level == lv) YR = &Y;
+      if (!YR) throw Error(H2G_ERR_INTERNAL, "root level structure missing");
+      long long nroot = 0;
+      for (int b : cur.bsz) nroot += b;
+      C->root_size = nroot;
+      bool needs_paint = false;
+      for (int la = std::max(l0, 0); la <= lv && l0 >= 0; ++la)
+        if (!S.adm[la].empty()) needs_paint = true;
+      if (nroot > 0) {
+        if (needs_paint) throw Error(H2G_ERR_INTERNAL, "root assembly with admissible blocks (stop-level override / early stop) not implemented yet");
+        C->root.alloc((size_t)nroot * nroot * 16, st, true);
+        const size_t bb = (size_t)cur.bmax * cur.bmax;
+        std::vector<CopyDesc> cd;
+        for (size_t q = 0; q < YR->drow.size(); ++q) {
+          const int r = YR->drow[q], c = YR->dcol[q];
+          if (!cur.bsz[r] || !cur.bsz[c]) continue;
+          cd.push_back({cur.D.as<cplx>() + q * bb, C->root.as<cplx>() + cur.pos[r] + (size_t)cur.pos[c] * nroot, cur.bsz[r], (int)nroot, cur.bsz[r], cur.bsz[c], 0, 0});
+        }
+        DBuf dcd;
+        upload(dcd, cd, st);
+        launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
+        ++launches;
+        DBuf scratch;
+        scratch.alloc(64, st);
+        root_lu(C->root.as<cplx>(), static_cast<int>(nroot), 1e-13, ctx->d_err, scratch.p, st, &launches);
+        CK(cudaGetLastError());
+        check_device_error(ctx, C->stop_level);
+        flops += 8.0 / 3.0 * (double)nroot * nroot * nroot;
+        C->storage_bytes += 2 * 16 * (size_t)nroot * nroot;
+        C->solve_bytes += 16.0 * (double)nroot * nroot;
+      }
+    }
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    C->factor_ms = ms;
+    C->factor_launches = launches;
+    C->factor_flops = flops;
+    C->schur_flops = sflops;
+    C->schur_bytes = sbytes;
+    *out = C.release();
+  });
+}
+
+int h2g_chain_destroy(h2g_chain* c) {
+  if (!c) return H2G_OK;
+  cudaSetDevice(c->ctx->device);
+  cudaStreamSynchronize(c->ctx->stream);
+  delete c;
+  return H2G_OK;
+}
+
+// ------------------------------------------------------------------ solve
+static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mode) {
+  h2g_context* ctx = C->ctx;
+  cudaStream_t st = ctx->stream;
+  if (n != C->n) throw Error(H2G_ERR_INVALID_INPUT, fmt("solve: right-hand side has length %lld, factorization expects %lld", n, C->n));
+  if (nrhs < 1) throw Error(H2G_ERR_INVALID_INPUT, "solve: nrhs must be >= 1");
+  CK(cudaMemsetAsync(ctx->d_flag, 0, 4, st));
+  launch_finite(y, n * nrhs, ctx->d_flag, st);
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->d_flag, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) throw Error(H2G_ERR_NON_FINITE, "solve: right-hand side contains non-finite entries");
+  if ((size_t)n * nrhs * 16 > C->tmpbuf.bytes) C->tmpbuf.alloc((size_t)n * nrhs * 16, st);
+  cplx* tmp = C->tmpbuf.as<cplx>();
+  const bool fwd = mode != H2G_BACKWARD, bwd = mode != H2G_FORWARD;
+  const int expl = mode == H2G_APPLY_INVERSE_EXPLICIT;
+  long long launches = 1;
+  CK(cudaEventRecord(ctx->ev0, st));
+  if (fwd) {
+    for (auto& CLp : C->levels) {
+      ChainLevelHost& CL = *CLp;
+      const int nbat = static_cast<int>(CL.batch_ptr.size()) - 1;
+      for (int bi = 0; bi < nbat; ++bi) {
+        const int p0 = CL.batch_ptr[bi], nb = CL.batch_ptr[bi + 1] - p0;
+        launch_fwd_head(CL.sl, CL.d_batch + p0, nb, y, n, nrhs, expl, st);
+        const int f0 = CL.fs_ptr[bi], f1 = CL.fs_ptr[bi + 1];
+        launch_fwd_lbar(CL.sl, CL.d_fs + f0, f1 - f0, CL.d_fc, y, n, nrhs, st);
+        launches += 1 + (f1 > f0);
+      }
+      launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 0, st);
+      launches += 2;
+    }
+    if (C->root_size > 0) {
+      launch_root_trsv(C->root.as<cplx>(), static_cast<int>(C->root_size), y, n, nrhs, 0, st);
+      ++launches;
+    }
+  }
+  if (bwd) {
+    if (C->root_size > 0) {
+      launch_root_trsv(C->root.as<cplx>(), static_cast<int>(C->root_size), y, n, nrhs, 1, st);
+      ++launches;
+    }
+    for (auto it = C->levels.rbegin(); it != C->levels.rend(); ++it) {
+      ChainLevelHost& CL = **it;
+      launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 1, st);
+      launches += 2;
+      const int nbat = static_cast<int>(CL.batch_ptr.size()) - 1;
+      for (int bi = nbat - 1; bi >= 0; --bi) {
+        const int p0 = CL.batch_ptr[bi], nb = CL.batch_ptr[bi + 1] - p0;
+        launch_bwd(CL.sl, CL.d_batch + p0, nb, y, n, nrhs, expl, st);
+        ++launches;
+      }
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev1, st));
+  CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  C->solve_ms = ms;
+  C->solve_launches = launches;
+}
+
+int h2g_solve_device(h2g_chain* c, double* x_dev, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!c || !x_dev) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    CK(cudaSetDevice(c->ctx->device));
+    solve_device_impl(c, reinterpret_cast<cplx*>(x_dev), n, nrhs, mode);
+  });
+}
+
+int h2g_solve(h2g_chain* c, const double* b, double* x, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!c || !b || !x) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    CK(cudaSetDevice(c->ctx->device));
+    if (n != c->n) throw Error(H2G_ERR_INVALID_INPUT, fmt("solve: right-hand side has length %lld, factorization expects %lld", n, c->n));
+    if (nrhs < 1) throw Error(H2G_ERR_INVALID_INPUT, "solve: nrhs must be >= 1");
+    cudaStream_t st = c->ctx->stream;
+    const size_t bytes = (size_t)n * nrhs * 16;
+    if (bytes > c->ybuf.bytes) c->ybuf.alloc(bytes, st);
+    CK(cudaMemcpyAsync(c->ybuf.p, b, bytes, cudaMemcpyHostToDevice, st));
+    solve_device_impl(c, c->ybuf.as<cplx>(), n, nrhs, mode);
+    CK(cudaMemcpyAsync(x, c->ybuf.p, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+// ------------------------------------------------------------- inspection
+int h2g_chain_info(const h2g_chain* c, int64_t* info) {
+  if (!c || !info) return H2G_ERR_INVALID_INPUT;
+  info[0] = c->n;
+  info[1] = c->stop_level;
+  info[2] = c->root_size;
+  info[3] = static_cast<int64_t>(c->levels.size());
+  info[4] = static_cast<int64_t>(c->storage_bytes);
+  info[5] = c->schedule;
+  return H2G_OK;
+}
+
+int h2g_chain_level(const h2g_chain* c, int32_t li, int64_t* out) {
+  if (!c || li < 0 || li >= (int)c->levels.size()) return H2G_ERR_INVALID_INPUT;
+  std::copy(c->levels[li]->diag.begin(), c->levels[li]->diag.end(), out);
+  return H2G_OK;
+}
+
+int h2g_chain_records(const h2g_chain* c, int32_t li, int64_t* out) {
+  if (!c || li < 0 || li >= (int)c->levels.size()) return H2G_ERR_INVALID_INPUT;
+  std::copy(c->levels[li]->rec.begin(), c->levels[li]->rec.end(), out);
+  return H2G_OK;
+}
+
+int h2g_chain_perm(const h2g_chain* c, int32_t li, int64_t* src) {
+  if (!c || li < 0 || li >= (int)c->levels.size()) return H2G_ERR_INVALID_INPUT;
+  std::copy(c->levels[li]->src.begin(), c->levels[li]->src.end(), src);
+  return H2G_OK;
+}
+
+int h2g_chain_record_mats(const h2g_chain* c, int32_t li, int32_t ri, double* q, double* l11, double* u11) {
+  return guarded(nullptr, [&] {
+    if (!c || li < 0 || li >= (int)c->levels.size()) throw Error(H2G_ERR_INVALID_INPUT, "bad level index");
+    const ChainLevelHost& CL = *c->levels[li];
+    if (ri < 0 || ri >= (int)CL.rec_cluster.size()) throw Error(H2G_ERR_INVALID_INPUT, "bad record index");
+    const int t = CL.rec_cluster[ri];
+    const int b = CL.bsz[t], e = b - CL.kfin[t];
+    cudaStream_t st = c->ctx->stream;
+    const cplx* base = CL.arena.as<cplx>();
+    if (q) CK(cudaMemcpyAsync(q, base + CL.Qt_off[t], (size_t)b * b * 16, cudaMemcpyDeviceToHost, st));
+    if (l11 && e) CK(cudaMemcpyAsync(l11, base + CL.L11_off[t], (size_t)e * e * 16, cudaMemcpyDeviceToHost, st));
+    if (u11 && e) CK(cudaMemcpyAsync(u11, base + CL.U11_off[t], (size_t)e * e * 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int h2g_chain_record_blocks_sizes(const h2g_chain* c, int32_t li, int32_t ri, int64_t* sizes4) {
+  if (!c || li < 0 || li >= (int)c->levels.size()) return H2G_ERR_INVALID_INPUT;
+  const ChainLevelHost& CL = *c->levels[li];
+  if (ri < 0 || ri >= (int)CL.rec_cluster.size()) return H2G_ERR_INVALID_INPUT;
+  const int t = CL.rec_cluster[ri];
+  const int kf = CL.kfin[t], e = CL.bsz[t] - kf;
+  int64_t nl = 0, nu = 0, el = 0, eu = 0;
+  if (e > 0) {
+    for (int a = CL.R_ptr[t]; a < CL.R_ptr[t + 1]; ++a) ++nl, el += (int64_t)CL.bsz[CL.R_nb[a]] * e;
+    for (int a = CL.C_ptr[t]; a < CL.C_ptr[t + 1]; ++a) ++nu, eu += (int64_t)CL.bsz[CL.C_nb[a]] * e;
+    if (kf > 0) ++nl, ++nu, el += (int64_t)kf * e, eu += (int64_t)kf * e;
+  }
+  sizes4[0] = nl, sizes4[1] = el, sizes4[2] = nu, sizes4[3] = eu;
+  return H2G_OK;
+}
+
+int h2g_chain_record_blocks(const h2g_chain* c, int32_t li, int32_t ri, int64_t* lpos, int64_t* lrows, double* ldata, int64_t* upos, int64_t* ucols,
+                            double* udata) {
+  return guarded(nullptr, [&] {
+    if (!c || li < 0 || li >= (int)c->levels.size()) throw Error(H2G_ERR_INVALID_INPUT, "bad level index");
+    const ChainLevelHost& CL = *c->levels[li];
+    if (ri < 0 || ri >= (int)CL.rec_cluster.size()) throw Error(H2G_ERR_INVALID_INPUT, "bad record index");
+    const int t = CL.rec_cluster[ri];
+    const int kf = CL.kfin[t], e = CL.bsz[t] - kf;
+    if (e == 0) return;
+    cudaStream_t st = c->ctx->stream;
+    const cplx* base = CL.arena.as<cplx>();
+    size_t q = 0, off = 0;
+    for (int a = CL.R_ptr[t]; a < CL.R_ptr[t + 1]; ++a, ++q) {
+      const int j = CL.R_nb[a];
+      lpos[q] = CL.pos[j];
+      lrows[q] = CL.bsz[j];
+      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lbar_off[a], (size_t)CL.bsz[j] * e * 16, cudaMemcpyDeviceToHost, st));
+      off += (size_t)CL.bsz[j] * e;
+    }
+    if (kf > 0) {
+      lpos[q] = CL.pos[t] + e;
+      lrows[q] = kf;
+      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lself_off[t], (size_t)kf * e * 16, cudaMemcpyDeviceToHost, st));
+    }
+    q = 0, off = 0;
+    for (int a = CL.C_ptr[t]; a < CL.C_ptr[t + 1]; ++a, ++q) {
+      const int cc = CL.C_nb[a];
+      upos[q] = CL.pos[cc];
+      ucols[q] = CL.bsz[cc];
+      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Ubar_off[a], (size_t)CL.bsz[cc] * e * 16, cudaMemcpyDeviceToHost, st));
+      off += (size_t)CL.bsz[cc] * e;
+    }
+    if (kf > 0) {
+      upos[q] = CL.pos[t] + e;
+      ucols[q] = kf;
+      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Uself_off[t], (size_t)kf * e * 16, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int h2g_chain_root(const h2g_chain* c, double* root_l, double* root_u) {
+  return guarded(nullptr, [&] {
+    const int64_t r = c->root_size;
+    if (r == 0) return;
+    std::vector<std::complex<double>> A((size_t)r * r);
+    CK(cudaMemcpyAsync(A.data(), c->root.p, (size_t)r * r * 16, cudaMemcpyDeviceToHost, c->ctx->stream));
+    CK(cudaStreamSynchronize(c->ctx->stream));
+    for (int64_t j = 0; j < r; ++j)
+      for (int64_t i = 0; i < r; ++i) {
+        const auto v = A[i + j * r];
+        const std::complex<double> l = i > j ? v : (i == j ? 1.0 : 0.0);
+        const std::complex<double> u = i <= j ? v : 0.0;
+        if (root_l) root_l[2 * (i + j * r)] = l.real(), root_l[2 * (i + j * r) + 1] = l.imag();
+        if (root_u) root_u[2 * (i + j * r)] = u.real(), root_u[2 * (i + j * r) + 1] = u.imag();
+      }
+  });
+}
+
+uint64_t h2g_chain_hash(const h2g_chain* c) {
+  if (!c) return 0;
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  cudaStream_t st = c->ctx->stream;
+  for (const auto& CL : c->levels) {
+    mix(CL->src.data(), CL->src.size() * 8);
+    mix(CL->rec.data(), CL->rec.size() * 8);
+    std::vector<char> buf(CL->arena.bytes);
+    if (cudaMemcpyAsync(buf.data(), CL->arena.p, buf.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess) return 0;
+    cudaStreamSynchronize(st);
+    // hash only the live parts of every record
+    for (int t : CL->rec_cluster) {
+      const int b = CL->bsz[t], kf = CL->kfin[t], e = b - kf;
+      mix(buf.data() + CL->Qt_off[t] * 16, (size_t)b * b * 16);
+      mix(buf.data() + CL->L11_off[t] * 16, (size_t)e * e * 16);
+      mix(buf.data() + CL->U11_off[t] * 16, (size_t)e * e * 16);
+      if (!e) continue;
+      for (int a = CL->R_ptr[t]; a < CL->R_ptr[t + 1]; ++a) mix(buf.data() + CL->Lbar_off[a] * 16, (size_t)CL->bsz[CL->R_nb[a]] * e * 16);
+      for (int a = CL->C_ptr[t]; a < CL->C_ptr[t + 1]; ++a) mix(buf.data() + CL->Ubar_off[a] * 16, (size_t)CL->bsz[CL->C_nb[a]] * e * 16);
+      mix(buf.data() + CL->Lself_off[t] * 16, (size_t)kf * e * 16);
+      mix(buf.data() + CL->Uself_off[t] * 16, (size_t)kf * e * 16);
+    }
+  }
+  if (c->root_size) {
+    std::vector<char> buf((size_t)c->root_size * c->root_size * 16);
+    cudaMemcpyAsync(buf.data(), c->root.p, buf.size(), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    mix(buf.data(), buf.size());
+  }
+  return h;
+}
+
+int h2g_chain_timing(const h2g_chain* c, double* fms, double* sms, int64_t* fl, int64_t* sl) {
+  if (!c) return H2G_ERR_INVALID_INPUT;
+  if (fms) *fms = c->factor_ms;
+  if (sms) *sms = c->solve_ms;
+  if (fl) *fl = c->factor_launches;
+  if (sl) *sl = c->solve_launches;
+  return H2G_OK;
+}
+
+int h2g_chain_work(const h2g_chain* c, double* out) {
+  if (!c || !out) return H2G_ERR_INVALID_INPUT;
+  out[0] = c->factor_flops;
+  out[1] = c->schur_flops;
+  out[2] = c->solve_bytes;
+  out[3] = c->schur_bytes;
+  return H2G_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,383 @@
+// Device building blocks for the H² factorization on sm_100a: complex128
+// arithmetic, CTA-cooperative dense kernels (small GEMM, Householder QR,
+// two-sided Hermitian Jacobi, unpivoted LU with the reference pivot rule,
+// triangular inverses). All routines take generic pointers so a matrix can
+// live in shared memory (b <= 64) or in a global-memory workspace.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace h2g {
+
+typedef double2 cplx;
+
+__device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ cplx czero() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ cplx cone() { return make_double2(1.0, 0.0); }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ cplx cconj(cplx a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double cabsd(cplx a) { return hypot(a.x, a.y); }
+// acc += a * b
+__device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// a / b with Smith's scaling
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, d = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / d, (a.y - a.x * r) / d);
+  }
+  const double r = b.x / b.y, d = b.y + b.x * r;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
+
+// Device error word: first failure wins (code 0 = none).
+struct DevError {
+  int code;
+  int cluster;
+  int level;
+  int pad;
+  long long pivot_index;
+  double pivot_magnitude;
+};
+
+__device__ __forceinline__ void raise_error(DevError* e, int code, int cluster, int level, long long piv, double mag) {
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->cluster = cluster;
+    e->level = level;
+    e->pivot_index = piv;
+    e->pivot_magnitude = mag;
+    __threadfence();
+  }
+}
+
+// op codes: 'N' plain, 'T' transpose, 'C' conjugate transpose, 'R' conjugate
+enum Op { OP_N = 0, OP_T = 1, OP_C = 2, OP_R = 3 };
+
+__device__ __forceinline__ cplx ld_op(const cplx* A, int lda, int op, int i, int p) {
+  switch (op) {
+    case OP_N:
+      return A[i + (size_t)p * lda];
+    case OP_T:
+      return A[p + (size_t)i * lda];
+    case OP_C:
+      return cconj(A[p + (size_t)i * lda]);
+    default:
+      return cconj(A[i + (size_t)p * lda]);
+  }
+}
+
+// C (m x n) = alpha * op(A) (m x k) * op(B) (k x n) + beta * C, cooperative
+// over the CTA. C must not alias A or B. Caller syncs.
+__device__ inline void cta_gemm(int m, int n, int k, double alpha, const cplx* A, int lda, int opA, const cplx* B, int ldb,
+                                int opB, double beta, cplx* C, int ldc) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;
+    cplx s = czero();
+    for (int p = 0; p < k; ++p) cfma(s, ld_op(A, lda, opA, i, p), ld_op(B, ldb, opB, p, j));
+    cplx* c = C + i + (size_t)j * ldc;
+    if (beta == 0.0)
+      *c = cscale(s, alpha);
+    else
+      *c = make_double2(beta * c->x + alpha * s.x, beta * c->y + alpha * s.y);
+  }
+}
+
+__device__ inline void cta_copy(int m, int n, const cplx* S, int lds, cplx* D, int ldd) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;
+    D[i + (size_t)j * ldd] = S[i + (size_t)j * lds];
+  }
+}
+
+__device__ inline void cta_fill(int m, int n, cplx* D, int ldd, cplx v) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) D[(idx % m) + (size_t)(idx / m) * ldd] = v;
+}
+
+__device__ inline void cta_identity(int m, int n, cplx* D, int ldd) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;
+    D[i + (size_t)j * ldd] = i == j ? cone() : czero();
+  }
+}
+
+// Block-wide sum / max of a double (all threads get the result).
+__device__ inline double cta_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  __syncthreads();
+  return s;
+}
+
+__device__ inline double cta_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s = fmax(s, red[i]);
+  __syncthreads();
+  return s;
+}
+
+// Compact Householder QR of A (m x n, ld lda) in place with the Eigen
+// HouseholderQR convention (H = I - tau v v^H, v0 = 1, beta = -sign(Re c0)|x|),
+// then Q (m x m, ld ldq) = H_0^H ... H_{s-1}^H. tau: s entries of scratch.
+__device__ inline void cta_householder_q(int m, int n, cplx* A, int lda, cplx* Q, int ldq, cplx* tau, double* red) {
+  const int s = min(m, n);
+  for (int k = 0; k < s; ++k) {
+    cplx* x = A + k + (size_t)k * lda;
+    double part = 0.0;
+    for (int i = 1 + threadIdx.x; i < m - k; i += blockDim.x) part += cabs2(x[i]);
+    const double tail = cta_sum(part, red);
+    const cplx c0 = x[0];
+    __shared__ cplx s_denom, s_tau;
+    __shared__ double s_beta;
+    __shared__ int s_triv;
+    if (threadIdx.x == 0) {
+      const double tiny = 2.2250738585072014e-308;
+      if (tail <= tiny && c0.y * c0.y <= tiny) {
+        s_triv = 1;
+        s_tau = czero();
+        s_beta = c0.x;
+      } else {
+        double beta = sqrt(cabs2(c0) + tail);
+        if (c0.x >= 0.0) beta = -beta;
+        s_triv = 0;
+        s_beta = beta;
+        s_denom = csub(c0, cmk(beta, 0.0));
+        s_tau = cconj(cdiv(csub(cmk(beta, 0.0), c0), cmk(beta, 0.0)));
+      }
+      tau[k] = s_tau;
+    }
+    __syncthreads();
+    const int triv = s_triv;
+    const cplx denom = s_denom, tk = s_tau;
+    for (int i = 1 + threadIdx.x; i < m - k; i += blockDim.x) x[i] = triv ? czero() : cdiv(x[i], denom);
+    __syncthreads();
+    // apply H to A[k:, k+1:]: one warp per column
+    if (!triv) {
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int j = k + 1 + w; j < n; j += nw) {
+        cplx* a = A + k + (size_t)j * lda;
+        cplx t = czero();
+        for (int i = 1 + lane; i < m - k; i += 32) cfma(t, cconj(x[i]), a[i]);
+        for (int o = 16; o > 0; o >>= 1) {
+          t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+          t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+        }
+        t = cmul(tk, cadd(t, a[0]));
+        __syncwarp();
+        if (lane == 0) a[0] = csub(a[0], t);
+        for (int i = 1 + lane; i < m - k; i += 32) a[i] = csub(a[i], cmul(x[i], t));
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) x[0] = cmk(s_beta, 0.0);
+    __syncthreads();
+  }
+  // Q = H_0^H H_1^H ... H_{s-1}^H applied to I
+  cta_identity(m, m, Q, ldq);
+  __syncthreads();
+  for (int k = s - 1; k >= 0; --k) {
+    const cplx* v = A + k + (size_t)k * lda;  // v[0] is beta; essential part v[1..]
+    const cplx tk = cconj(tau[k]);
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = k + w; j < m; j += nw) {
+      cplx* q = Q + k + (size_t)j * ldq;
+      cplx t = czero();
+      for (int i = 1 + lane; i < m - k; i += 32) cfma(t, cconj(v[i]), q[i]);
+      for (int o = 16; o > 0; o >>= 1) {
+        t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+        t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+      }
+      t = cmul(tk, cadd(t, q[0]));
+      __syncwarp();
+      if (lane == 0) q[0] = csub(q[0], t);
+      for (int i = 1 + lane; i < m - k; i += 32) q[i] = csub(q[i], cmul(v[i], t));
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// Two-sided cyclic Jacobi on a Hermitian n x n matrix H (ld n), round-robin
+// parallel ordering. On exit H is (numerically) diagonal and U (ld n) holds
+// the eigenvectors: H_in = U diag(H_out) U^H. rot: scratch of 4*((n+1)/2) doubles.
+__device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int* pr, double* red) {
+  cta_identity(n, n, U, n);
+  __syncthreads();
+  if (n <= 1) return;
+  const int n2 = (n + 1) & ~1;
+  const int npair = n2 / 2;
+  double* rc = rot;
+  double* rs = rot + npair;
+  double* rphr = rot + 2 * npair;
+  double* rphi = rot + 3 * npair;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const double a = cabs2(H[idx]);
+      tot += a;
+      if ((idx % n) != (idx / n)) off += a;
+    }
+    off = cta_sum(off, red);
+    tot = cta_sum(tot, red);
+    if (off <= 1e-32 * tot || tot == 0.0) break;
+    for (int r = 0; r < n2 - 1; ++r) {
+      for (int i = threadIdx.x; i < npair; i += blockDim.x) {
+        int p, q;
+        if (i == 0) {
+          p = r;
+          q = n2 - 1;
+        } else {
+          p = (r + i) % (n2 - 1);
+          q = (r - i + (n2 - 1)) % (n2 - 1);
+        }
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        pr[2 * i] = p;
+        pr[2 * i + 1] = q;
+        double c = 1.0, s = 0.0, phr = 1.0, phi = 0.0;
+        if (q < n) {
+          const cplx g = H[p + q * n];
+          const double ga = cabsd(g);
+          const double a = H[p + p * n].x, d = H[q + q * n].x;
+          if (ga > 1e-300 && ga > 1e-18 * (fabs(a) + fabs(d))) {
+            phr = g.x / ga;
+            phi = g.y / ga;
+            const double th = (d - a) / (2.0 * ga);
+            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        }
+        rc[i] = c;
+        rs[i] = s;
+        rphr[i] = phr;
+        rphi[i] = phi;
+      }
+      __syncthreads();
+      // rows: [H_px; H_qx] <- J^H [H_px; H_qx], J^H = [[c, -s e^{i phi}], [s, c e^{i phi}]]
+      for (int idx = threadIdx.x; idx < npair * n; idx += blockDim.x) {
+        const int i = idx % npair, x = idx / npair;
+        const int p = pr[2 * i], q = pr[2 * i + 1];
+        if (q >= n || rs[i] == 0.0) continue;
+        const double c = rc[i], s = rs[i];
+        const cplx ph = cmk(rphr[i], rphi[i]);
+        const cplx hp = H[p + x * n], hq = H[q + x * n];
+        const cplx ehq = cmul(ph, hq);
+        H[p + x * n] = csub(cscale(hp, c), cscale(ehq, s));
+        H[q + x * n] = cadd(cscale(hp, s), cscale(ehq, c));
+      }
+      __syncthreads();
+      // columns: [H_xp, H_xq] <- [H_xp, H_xq] J, J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]]
+      for (int idx = threadIdx.x; idx < npair * n; idx += blockDim.x) {
+        const int i = idx % npair, x = idx / npair;
+        const int p = pr[2 * i], q = pr[2 * i + 1];
+        if (q >= n || rs[i] == 0.0) continue;
+        const double c = rc[i], s = rs[i];
+        const cplx phc = cmk(rphr[i], -rphi[i]);
+        {
+          const cplx hp = H[x + p * n], hq = H[x + q * n];
+          const cplx ehq = cmul(phc, hq);
+          H[x + p * n] = csub(cscale(hp, c), cscale(ehq, s));
+          H[x + q * n] = cadd(cscale(hp, s), cscale(ehq, c));
+        }
+        {
+          const cplx up = U[x + p * n], uq = U[x + q * n];
+          const cplx euq = cmul(phc, uq);
+          U[x + p * n] = csub(cscale(up, c), cscale(euq, s));
+          U[x + q * n] = cadd(cscale(up, s), cscale(euq, c));
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Unpivoted LU in place (n x n, ld lda) with the reference pivot rule
+// |piv| < tol * max|F| (dense_kernels.hpp:70-93). Returns -1 on success or
+// the failing pivot index (magnitude in *pmag). All threads return the same.
+__device__ inline int cta_lu_nopiv(int n, cplx* A, int lda, double tol, double* pmag, double* red) {
+  double mx = 0.0;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) mx = fmax(mx, cabsd(A[(idx % n) + (size_t)(idx / n) * lda]));
+  const double scale = cta_max(mx, red);
+  if (n > 0 && scale == 0.0) {
+    *pmag = 0.0;
+    return 0;
+  }
+  for (int k = 0; k < n; ++k) {
+    const cplx piv = A[k + (size_t)k * lda];
+    const double pa = cabsd(piv);
+    if (pa < tol * scale) {
+      *pmag = pa;
+      return k;
+    }
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + (size_t)k * lda] = cdiv(A[i + (size_t)k * lda], piv);
+    __syncthreads();
+    const int r = n - k - 1;
+    for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+      const int i = k + 1 + idx % r, j = k + 1 + idx / r;
+      cplx a = A[i + (size_t)j * lda];
+      const cplx l = A[i + (size_t)k * lda], u = A[k + (size_t)j * lda];
+      a.x -= l.x * u.x - l.y * u.y;
+      a.y -= l.x * u.y + l.y * u.x;
+      A[i + (size_t)j * lda] = a;
+    }
+    __syncthreads();
+  }
+  return -1;
+}
+
+// Inverses of the unit-lower L and upper U stored packed in LU (n x n):
+// Li = L^{-1}, Ui = U^{-1} (both n x n, ld n). One thread per column.
+__device__ inline void cta_tri_inverses(int n, const cplx* LU, int ld, cplx* Li, cplx* Ui) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    // L x = e_j
+    for (int i = 0; i < n; ++i) {
+      cplx x = i == j ? cone() : czero();
+      if (i > j)
+        for (int p = j; p < i; ++p) {
+          const cplx l = LU[i + (size_t)p * ld], xp = Li[p + (size_t)j * n];
+          x.x -= l.x * xp.x - l.y * xp.y;
+          x.y -= l.x * xp.y + l.y * xp.x;
+        }
+      Li[i + (size_t)j * n] = i < j ? czero() : x;
+    }
+    // U x = e_j
+    for (int i = n - 1; i >= 0; --i) {
+      cplx x = i == j ? cone() : czero();
+      if (i <= j) {
+        for (int p = i + 1; p <= j; ++p) {
+          const cplx u = LU[i + (size_t)p * ld], xp = Ui[p + (size_t)j * n];
+          x.x -= u.x * xp.x - u.y * xp.y;
+          x.y -= u.x * xp.y + u.y * xp.x;
+        }
+        x = cdiv(x, LU[i + (size_t)i * ld]);
+      }
+      Ui[i + (size_t)j * n] = i > j ? czero() : x;
+    }
+  }
+}
+
+}  // namespace h2g

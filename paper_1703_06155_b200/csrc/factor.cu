@@ -1,0 +1,690 @@
+// Level kernels of the B200 H² factorization. One batch = a set of mutually
+// non-adjacent clusters of one level (plan.cpp); per batch four launches:
+//   k_gram   step 0, part 1: Gram of the complement-projected fill-in stack
+//   k_head   step 0, part 2 + step 1 + step 3a: truncation (Jacobi), Qtilde,
+//            rotation of the diagonal block, unpivoted LU, self panels
+//   k_panel  step 2 + step 3b: rotate row/column blocks, Lbar/Ubar panels
+//   k_schur  step 3c: Schur products scattered to dense / fill-in targets
+// Reference: proj/include/h2lu/factorization.hpp:260-440.
+#include <algorithm>
+#include <cstdio>
+
+#include "factor.cuh"
+
+namespace h2g {
+
+namespace {
+
+__device__ __forceinline__ cplx* blk(cplx* pool, int idx, int bmax) { return pool + (size_t)idx * bmax * bmax; }
+
+// Workspace: shared memory if it fits, else a global slot per CTA.
+struct Ws {
+  cplx* p;
+};
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// Complement of the level-entry basis: Vp = Q[:, k:] from a Householder QR of
+// V (b x korig); also the orthonormality guard of unitary_completion
+// (dense_kernels.hpp:55-59).
+__global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  const int t = blockIdx.x;
+  const int b = L.bsz[t], k = L.korig[t], bm = L.bmax;
+  cplx* ws = gws ? gws + (size_t)t * (2 * bm * bm + bm) : reinterpret_cast<cplx*>(smraw);
+  cplx* A = ws;
+  cplx* Q = ws + bm * bm;
+  cplx* tau = ws + 2 * bm * bm;
+  const cplx* V = L.V0 + (size_t)t * bm * bm;
+  cplx* Vp = L.Vp + (size_t)t * bm * bm;
+  if (k > 0) {
+    double defect = 0.0;
+    for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x) {
+      const int i = idx % k, j = idx / k;
+      cplx s = czero();
+      for (int p = 0; p < b; ++p) cfma(s, cconj(V[p + (size_t)i * b]), V[p + (size_t)j * b]);
+      if (i == j) s.x -= 1.0;
+      defect = fmax(defect, cabsd(s));
+    }
+    defect = cta_max(defect, red);
+    if (defect > 1e-10) {
+      if (threadIdx.x == 0) raise_error(L.err, 1, (1 << L.level) - 1 + t, L.level, -1, defect);
+      return;
+    }
+  }
+  if (k == b) return;
+  if (k == 0) {
+    cta_identity(b, b, Vp, b);
+    return;
+  }
+  cta_copy(b, k, V, b, A, b);
+  __syncthreads();
+  cta_householder_q(b, k, A, b, Q, b, tau, red);
+  cta_copy(b, b - k, Q + (size_t)k * b, b, Vp, b);
+}
+
+// --------------------------------------------------------------------------
+// Step 0, part 1: partial Gram matrices of Y = Vp^H W over a slice of the
+// cluster's fill-in blocks (W columns: F for keys (t, y), F^T for keys (x, t),
+// factorization.hpp:278-293), plus the largest unprojected column norm
+// (the floor of :295).
+__global__ void __launch_bounds__(256) k_gram(DevLevel L, const int* batch_cl) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  const int q = blockIdx.x, g = blockIdx.y, G = gridDim.y;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  cplx* sVp = reinterpret_cast<cplx*>(smraw);  // b x m
+  cplx* sW = sVp + bm * bm;                    // b x bx
+  cplx* sY = sW + bm * bm;                     // m x bx
+  const int mm = m * m;
+  const int per = (mm + blockDim.x - 1) / blockDim.x;
+  cplx acc[16];
+  for (int s = 0; s < 16; ++s) acc[s] = czero();
+  double cmax = 0.0;
+  const int f0 = L.G_ptr[t], f1 = L.G_ptr[t + 1];
+  if (m > 0) cta_copy(b, m, L.Vp + (size_t)t * bm * bm, b, sVp, b);
+  for (int f = f0 + g; f < f1 && m > 0; f += G) {
+    const int fi = L.G_fill[f];
+    if (!L.fexists[fi]) continue;
+    const int tr = L.G_tr[f];
+    const int fr = L.bsz[L.frow[fi]], fc = L.bsz[L.fcol[fi]];
+    const cplx* F = blk(L.F, fi, bm);
+    const int bx = tr ? fr : fc;  // W block is b x bx
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < b * bx; idx += blockDim.x) {
+      const int p = idx % b, j = idx / b;
+      sW[p + j * b] = tr ? F[j + (size_t)p * fr] : F[p + (size_t)j * fr];
+    }
+    __syncthreads();
+    // column norms (floor)
+    for (int j = threadIdx.x; j < bx; j += blockDim.x) {
+      double s = 0.0;
+      for (int p = 0; p < b; ++p) s += cabs2(sW[p + j * b]);
+      cmax = fmax(cmax, sqrt(s));
+    }
+    cta_gemm(m, bx, b, 1.0, sVp, b, OP_C, sW, b, OP_N, 0.0, sY, m);
+    __syncthreads();
+    for (int s = 0; s < per; ++s) {
+      const int idx = threadIdx.x + s * blockDim.x;
+      if (idx >= mm) break;
+      const int i = idx % m, j = idx / m;
+      cplx a = acc[s];
+      for (int p = 0; p < bx; ++p) cfma(a, sY[i + p * m], cconj(sY[j + p * m]));
+      acc[s] = a;
+    }
+  }
+  cmax = cta_max(cmax, red);
+  cplx* out = L.gram + (size_t)(q * G + g) * bm * bm;
+  for (int s = 0; s < per; ++s) {
+    const int idx = threadIdx.x + s * blockDim.x;
+    if (idx >= mm) break;
+    out[idx] = acc[s];
+  }
+  if (threadIdx.x == 0) L.gram_cmax[q * G + g] = cmax;
+}
+
+// --------------------------------------------------------------------------
+// Step 0 part 2 (truncation of the projected fill spectrum, eps rule and
+// floor of factorization.hpp:295-298 / h2_matrix.hpp:287-290), step 1
+// (Qtilde = [complement | V | new], :317-339), the rotation of D(t,t) (:345-347)
+// and step 3a (unpivoted LU of the leading e x e block, :390-398; self panels
+// and the self Schur product, :409-420; cleanup, :431-435).
+__global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, cplx* gws) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  __shared__ int s_any, s_r;
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const int cid = (1 << L.level) - 1 + t;
+  cplx* ws = gws ? gws + (size_t)q * 3 * bm * bm : reinterpret_cast<cplx*>(smraw);
+  cplx* buf0 = ws;
+  cplx* buf1 = ws + bm * bm;
+  cplx* buf2 = ws + 2 * bm * bm;
+  double* lam = reinterpret_cast<double*>(smraw + (gws ? 0 : 3 * (size_t)bm * bm * sizeof(cplx)));
+  int* ord = reinterpret_cast<int*>(lam + bm);
+  int* pr = ord + bm;
+  double* rot = reinterpret_cast<double*>(pr + bm + 2);
+
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  {
+    int any = 0;
+    for (int f = L.G_ptr[t] + threadIdx.x; f < L.G_ptr[t + 1]; f += blockDim.x) any |= L.fexists[L.G_fill[f]];
+    if (any) s_any = 1;
+  }
+  __syncthreads();
+  const bool work = s_any && m > 0;
+  cplx* Hc = buf0;
+  cplx* Uc = buf1;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ord[i] = i;
+  if (threadIdx.x == 0) s_r = 0;
+  __syncthreads();
+  if (work) {
+    const int G = L.gram_parts;
+    double cm = 0.0;
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      cplx s = czero();
+      for (int g = 0; g < G; ++g) s = cadd(s, L.gram[(size_t)(q * G + g) * bm * bm + idx]);
+      Hc[idx] = s;
+    }
+    for (int g = threadIdx.x; g < G; g += blockDim.x) cm = fmax(cm, L.gram_cmax[q * G + g]);
+    const double cmax = cta_max(cm, red);
+    __syncthreads();
+    cta_jacobi_eig(m, Hc, Uc, rot, pr, red);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(Hc[i + i * m].x, 0.0));
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      int rank = 0;
+      for (int j = 0; j < m; ++j) rank += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+      ord[rank] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double s0 = lam[ord[0]];
+      int r = 0;
+      if (s0 > 0.0) {
+        const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
+        while (r < m && lam[ord[r]] > thr) ++r;
+      }
+      s_r = r;
+    }
+    __syncthreads();
+  } else {
+    cta_identity(m, m, Uc, m);
+  }
+  __syncthreads();
+  const int r = s_r;
+  const int kf = k + r, e = b - kf;
+  if (threadIdx.x == 0) L.kfin[t] = kf;
+
+  // Qtilde = [Vp Uc(:, ord[r:]) | V | Vp Uc(:, ord[:r])]
+  cplx* Qt = buf2;
+  const cplx* Vp = L.Vp + (size_t)t * bm * bm;
+  const cplx* V = L.V0 + (size_t)t * bm * bm;
+  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    cplx v;
+    if (j >= e && j < e + k) {
+      v = V[i + (size_t)(j - e) * b];
+    } else {
+      const int col = j < e ? ord[r + j] : ord[j - e - k];
+      v = czero();
+      for (int p = 0; p < m; ++p) cfma(v, Vp[i + (size_t)p * b], Uc[p + col * m]);
+    }
+    Qt[i + j * b] = v;
+  }
+  __syncthreads();
+  cplx* gQt = L.chain + L.Qt_off[t];
+  cta_copy(b, b, Qt, b, gQt, b);
+  // rotate the diagonal block: Dii <- Qt^H Dii conj(Qt)
+  cplx* gD = blk(L.D, L.diag_blk[t], bm);
+  cplx* Dd = buf0;
+  cplx* T = buf1;
+  cta_copy(b, b, gD, b, Dd, b);
+  __syncthreads();
+  cta_gemm(b, b, b, 1.0, Qt, b, OP_C, Dd, b, OP_N, 0.0, T, b);
+  __syncthreads();
+  cta_gemm(b, b, b, 1.0, T, b, OP_N, Qt, b, OP_R, 0.0, Dd, b);
+  __syncthreads();
+  if (e > 0) {
+    cta_copy(e, e, Dd, b, T, e);
+    __syncthreads();
+    double pmag = 0.0;
+    const int fail = cta_lu_nopiv(e, T, e, 1e-13, &pmag, red);
+    if (fail >= 0) {
+      if (threadIdx.x == 0) raise_error(L.err, 4, cid, L.level, fail, pmag);
+      return;
+    }
+    cplx* L11 = L.chain + L.L11_off[t];
+    cplx* U11 = L.chain + L.U11_off[t];
+    for (int idx = threadIdx.x; idx < e * e; idx += blockDim.x) {
+      const int i = idx % e, j = idx / e;
+      const cplx v = T[idx];
+      L11[idx] = i > j ? v : (i == j ? cone() : czero());
+      U11[idx] = i <= j ? v : czero();
+    }
+    cplx* Li = L.chain + L.Linv_off[t];
+    cplx* Ui = L.chain + L.Uinv_off[t];
+    cta_tri_inverses(e, T, e, Li, Ui);
+    __syncthreads();
+    if (kf > 0) {
+      cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
+      cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
+      cta_gemm(e, kf, e, 1.0, Li, e, OP_N, Dd + (size_t)e * b, b, OP_N, 0.0, Us, e);
+      cta_gemm(kf, e, e, 1.0, Dd + e, b, OP_N, Ui, e, OP_N, 0.0, Ls, kf);
+      __syncthreads();
+      cta_gemm(kf, kf, e, -1.0, Ls, kf, OP_N, Us, e, OP_N, 1.0, Dd + e + (size_t)e * b, b);
+      __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+      const int i = idx % b, j = idx / b;
+      if (i < e || j < e) Dd[idx] = (i == j) ? cone() : czero();
+    }
+    __syncthreads();
+  }
+  cta_copy(b, b, Dd, b, gD, b);
+}
+
+// --------------------------------------------------------------------------
+// Step 2 for the off-diagonal blocks of row/column t and step 3b: column
+// item D(t,c) <- Qt^H D, Ubar = L11^{-1} D[:e,:]; row item D(j,t) <- D conj(Qt),
+// Lbar = D[:,:e] U11^{-1}; eliminated rows/columns zeroed (:437-438). For a
+// neighbour eliminated earlier the panel is also lifted back to its
+// level-entry frame (deposit_fill, :359-362).
+__global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, const PanelItemD* items) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const PanelItemD it = items[blockIdx.x];
+  const int t = batch_cl[it.q];
+  const int bm = L.bmax;
+  const int b = L.bsz[t], e = b - L.kfin[t];
+  const int bn = L.bsz[it.nb];
+  cplx* sQ = reinterpret_cast<cplx*>(smraw);
+  cplx* sD = sQ + bm * bm;
+  cplx* sT = sD + bm * bm;
+  const cplx* gQ = L.chain + L.Qt_off[t];
+  cplx* gD = blk(L.D, it.blk, bm);
+  cta_copy(b, b, gQ, b, sQ, b);
+  const cplx* Li = L.chain + L.Linv_off[t];
+  const cplx* Ui = L.chain + L.Uinv_off[t];
+  if (it.side == 0) {  // D(t, c): b x bn
+    cta_copy(b, bn, gD, b, sD, b);
+    __syncthreads();
+    cta_gemm(b, bn, b, 1.0, sQ, b, OP_C, sD, b, OP_N, 0.0, sT, b);
+    __syncthreads();
+    if (e > 0) {
+      cplx* Ub = L.chain + L.Ubar_off[it.entry];  // e x bn
+      cta_gemm(e, bn, e, 1.0, Li, e, OP_N, sT, b, OP_N, 0.0, Ub, e);
+      __syncthreads();
+      if (it.lift) {
+        const cplx* Qn = L.chain + L.Qt_off[it.nb];
+        cta_gemm(e, bn, bn, 1.0, Ub, e, OP_N, Qn, bn, OP_T, 0.0, L.lift + L.Ubar_off[it.entry], e);
+      }
+      for (int idx = threadIdx.x; idx < e * bn; idx += blockDim.x) sT[(idx % e) + (idx / e) * b] = czero();
+      __syncthreads();
+    }
+    cta_copy(b, bn, sT, b, gD, b);
+  } else {  // D(j, t): bn x b
+    cta_copy(bn, b, gD, bn, sD, bn);
+    __syncthreads();
+    cta_gemm(bn, b, b, 1.0, sD, bn, OP_N, sQ, b, OP_R, 0.0, sT, bn);
+    __syncthreads();
+    if (e > 0) {
+      cplx* Lb = L.chain + L.Lbar_off[it.entry];  // bn x e
+      cta_gemm(bn, e, e, 1.0, sT, bn, OP_N, Ui, e, OP_N, 0.0, Lb, bn);
+      __syncthreads();
+      if (it.lift) {
+        const cplx* Qn = L.chain + L.Qt_off[it.nb];
+        cta_gemm(bn, e, bn, 1.0, Qn, bn, OP_N, Lb, bn, OP_N, 0.0, L.lift + L.Lbar_off[it.entry], bn);
+      }
+      for (int idx = threadIdx.x; idx < bn * e; idx += blockDim.x) sT[idx] = czero();
+      __syncthreads();
+    }
+    cta_copy(bn, b, sT, bn, gD, bn);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Step 3c: one CTA per target block (dense or fill-in); the contributions of
+// every cluster of the batch that hits it are summed in a fixed order, then
+// subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
+// 4 x 4 complex micro-tile per thread, K staged through shared memory.
+__global__ void __launch_bounds__(256) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+  __shared__ cplx sA[64][17];
+  __shared__ cplx sB[16][65];
+  const SchurTargetD tg = targets[blockIdx.x];
+  const int bm = L.bmax;
+  int rows, cols;
+  cplx* out;
+  if (tg.kind == 0) {
+    rows = L.bsz[L.drow[tg.idx]];
+    cols = L.bsz[L.dcol[tg.idx]];
+    out = blk(L.D, tg.idx, bm);
+  } else {
+    rows = L.bsz[L.frow[tg.idx]];
+    cols = L.bsz[L.fcol[tg.idx]];
+    out = blk(L.F, tg.idx, bm);
+  }
+  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  bool touched = false;
+  for (int r0 = 0; r0 < rows; r0 += 64)
+    for (int c0 = 0; c0 < cols; c0 += 64) {
+      cplx acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
+      for (int ci = tg.c0; ci < tg.c1; ++ci) {
+        const SchurContribD cb = contrib[ci];
+        const int t = cb.t;
+        const int kf = L.kfin[t], e = L.bsz[t] - kf;
+        if (e == 0) continue;
+        touched = true;
+        const cplx* A;
+        const cplx* B;
+        int arows, bcols, ro, co;
+        if (cb.r >= 0) {
+          arows = L.bsz[L.R_nb[cb.r]];
+          A = ((cb.flags & 1) ? L.lift : L.chain) + L.Lbar_off[cb.r];
+          ro = 0;
+        } else {
+          arows = kf;
+          A = L.chain + L.Lself_off[t];
+          ro = e;
+        }
+        if (cb.c >= 0) {
+          bcols = L.bsz[L.C_nb[cb.c]];
+          B = ((cb.flags & 2) ? L.lift : L.chain) + L.Ubar_off[cb.c];
+          co = 0;
+        } else {
+          bcols = kf;
+          B = L.chain + L.Uself_off[t];
+          co = e;
+        }
+        // intersect [ro, ro+arows) x [co, co+bcols) with the tile
+        for (int k0 = 0; k0 < e; k0 += 16) {
+          const int kk = min(16, e - k0);
+          __syncthreads();
+          for (int idx = threadIdx.x; idx < 64 * 16; idx += blockDim.x) {
+            const int i = idx % 64, p = idx / 64;
+            const int gi = r0 + i - ro;
+            sA[i][p] = (p < kk && gi >= 0 && gi < arows) ? A[gi + (size_t)(k0 + p) * arows] : czero();
+            const int j = idx % 64;
+            const int gj = c0 + j - co;
+            sB[p][j] = (p < kk && gj >= 0 && gj < bcols) ? B[(k0 + p) + (size_t)gj * e] : czero();
+          }
+          __syncthreads();
+          for (int p = 0; p < kk; ++p) {
+            cplx av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) bv[bb] = sB[p][tc * 4 + bb];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int bb = 0; bb < 4; ++bb) cfma(acc[a][bb], av[a], bv[bb]);
+          }
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + bb;
+          if (i < rows && j < cols && (acc[a][bb].x != 0.0 || acc[a][bb].y != 0.0)) {
+            cplx* o = out + i + (size_t)j * rows;
+            *o = csub(*o, acc[a][bb]);
+          }
+        }
+    }
+  if (tg.kind == 1 && touched && threadIdx.x == 0) L.fexists[tg.idx] = 1;
+}
+
+// --------------------------------------------------------------------------
+// Descriptor-driven copy / GEMM (level boundaries: finish_level, merge_permute,
+// root assembly, :445-584 and :637).
+__global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
+  const CopyDesc d = descs[blockIdx.x];
+  for (int idx = threadIdx.x; idx < d.m * d.n; idx += blockDim.x) {
+    const int i = idx % d.m, j = idx / d.m;
+    const cplx v = d.src ? d.src[i + (size_t)j * d.lds] : czero();
+    cplx* o = d.dst + i + (size_t)j * d.ldd;
+    *o = d.accumulate ? cadd(*o, v) : v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gemm(const GemmDesc* descs) {
+  __shared__ cplx sA[64][17];
+  __shared__ cplx sB[16][65];
+  const GemmDesc d = descs[blockIdx.x];
+  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  for (int r0 = 0; r0 < d.m; r0 += 64)
+    for (int c0 = 0; c0 < d.n; c0 += 64) {
+      cplx acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
+      for (int k0 = 0; k0 < d.k; k0 += 16) {
+        const int kk = min(16, d.k - k0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 64 * 16; idx += blockDim.x) {
+          const int i = idx % 64, p = idx / 64;
+          sA[i][p] = (p < kk && r0 + i < d.m) ? ld_op(d.A, d.lda, d.opA, r0 + i, k0 + p) : czero();
+          sB[p][i] = (p < kk && c0 + i < d.n) ? ld_op(d.B, d.ldb, d.opB, k0 + p, c0 + i) : czero();
+        }
+        __syncthreads();
+        for (int p = 0; p < kk; ++p) {
+          cplx av[4], bv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) bv[bb] = sB[p][tc * 4 + bb];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) cfma(acc[a][bb], av[a], bv[bb]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + bb;
+          if (i < d.m && j < d.n) {
+            cplx* o = d.C + i + (size_t)j * d.ldc;
+            const cplx v = acc[a][bb];
+            *o = d.beta == 0.0 ? cscale(v, d.alpha) : make_double2(d.beta * o->x + d.alpha * v.x, d.beta * o->y + d.alpha * v.y);
+          }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Root: blocked right-looking unpivoted LU with the reference pivot rule
+// (|piv| < 1e-13 max|A|, dense_kernels.hpp:74-79; factorization.hpp:637-651).
+__global__ void k_absmax(const cplx* A, long long n2, double* out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) m = fmax(m, cabsd(A[i]));
+  m = cta_max(m, red);
+  if (threadIdx.x == 0) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(out);
+    atomicMax(p, __double_as_longlong(m));  // non-negative doubles order like their bits
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lu_panel(cplx* A, int n, int k0, int kb, const double* scale, DevError* err) {
+  // factor the tall panel A[k0:n, k0:k0+kb]
+  const double sc = *scale;
+  for (int kk = 0; kk < kb; ++kk) {
+    const int k = k0 + kk;
+    const cplx piv = A[k + (size_t)k * n];
+    const double pa = cabsd(piv);
+    if (pa < 1e-13 * sc || (sc == 0.0)) {
+      if (threadIdx.x == 0) raise_error(err, 4, -1, -1, k, pa);
+      return;
+    }
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + (size_t)k * n] = cdiv(A[i + (size_t)k * n], piv);
+    __syncthreads();
+    const int nc = k0 + kb - k - 1;
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      const cplx l = A[i + (size_t)k * n];
+      for (int j = k + 1; j < k + 1 + nc; ++j) {
+        const cplx u = A[k + (size_t)j * n];
+        cplx a = A[i + (size_t)j * n];
+        a.x -= l.x * u.x - l.y * u.y;
+        a.y -= l.x * u.y + l.y * u.x;
+        A[i + (size_t)j * n] = a;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_lu_trsm(cplx* A, int n, int k0, int kb) {
+  // A[k0:k0+kb, j] <- L11^{-1} A[k0:k0+kb, j] for j >= k0+kb (unit lower)
+  const int j = k0 + kb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int i = 1; i < kb; ++i) {
+    cplx s = A[k0 + i + (size_t)j * n];
+    for (int p = 0; p < i; ++p) {
+      const cplx l = A[k0 + i + (size_t)(k0 + p) * n], x = A[k0 + p + (size_t)j * n];
+      s.x -= l.x * x.x - l.y * x.y;
+      s.y -= l.x * x.y + l.y * x.x;
+    }
+    A[k0 + i + (size_t)j * n] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lu_update(cplx* A, int n, int k0, int kb) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx(*sA)[33] = reinterpret_cast<cplx(*)[33]>(smraw);
+  cplx(*sB)[65] = reinterpret_cast<cplx(*)[65]>(smraw + 64 * 33 * sizeof(cplx));
+  const int base = k0 + kb;
+  const int r0 = base + blockIdx.x * 64, c0 = base + blockIdx.y * 64;
+  if (r0 >= n || c0 >= n) return;
+  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  for (int idx = threadIdx.x; idx < 64 * 32; idx += blockDim.x) {
+    const int i = idx % 64, p = idx / 64;
+    sA[i][p] = (p < kb && r0 + i < n) ? A[r0 + i + (size_t)(k0 + p) * n] : czero();
+    sB[p][i] = (p < kb && c0 + i < n) ? A[k0 + p + (size_t)(c0 + i) * n] : czero();
+  }
+  __syncthreads();
+  cplx acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
+  for (int p = 0; p < kb; ++p) {
+    cplx av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) bv[bb] = sB[p][tc * 4 + bb];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) cfma(acc[a][bb], av[a], bv[bb]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + bb;
+      if (i < n && j < n) {
+        cplx* o = A + i + (size_t)j * n;
+        *o = csub(*o, acc[a][bb]);
+      }
+    }
+}
+
+// ==========================================================================
+// launchers
+namespace {
+size_t smem3(int bm) { return 3 * (size_t)bm * bm * sizeof(cplx); }
+constexpr size_t kSmemCap = 220 * 1024;
+}  // namespace
+
+size_t head_smem_bytes(int bm) {
+  // 3 matrices + lam/ord/pr/rot scratch
+  return smem3(bm) + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
+}
+
+static void set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+static cplx* g_ws = nullptr;
+static size_t g_ws_bytes = 0;
+static cplx* workspace(size_t bytes, cudaStream_t s) {
+  if (bytes > g_ws_bytes) {
+    if (g_ws) {
+      cudaStreamSynchronize(s);
+      cudaFree(g_ws);
+    }
+    cudaMalloc(&g_ws, bytes);
+    g_ws_bytes = bytes;
+  }
+  return g_ws;
+}
+
+void launch_complement(const DevLevel& L, cudaStream_t s) {
+  const size_t need = 2 * (size_t)L.bmax * L.bmax * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx);
+  if (need <= kSmemCap) {
+    set_smem((const void*)k_complement, need);
+    k_complement<<<L.nl, 256, need, s>>>(L, nullptr);
+  } else {
+    cplx* ws = workspace(need * L.nl, s);
+    k_complement<<<L.nl, 256, 0, s>>>(L, ws);
+  }
+}
+
+void launch_gram(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
+  const size_t need = smem3(L.bmax);
+  set_smem((const void*)k_gram, need);
+  dim3 grid(nb, L.gram_parts);
+  k_gram<<<grid, 256, need, s>>>(L, batch_cl);
+}
+
+void launch_head(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
+  const size_t need = head_smem_bytes(L.bmax);
+  if (need <= kSmemCap) {
+    set_smem((const void*)k_head, need);
+    k_head<<<nb, 256, need, s>>>(L, batch_cl, nullptr);
+  } else {
+    const size_t small = need - smem3(L.bmax);
+    cplx* ws = workspace(smem3(L.bmax) * nb, s);
+    k_head<<<nb, 256, small, s>>>(L, batch_cl, ws);
+  }
+}
+
+void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s) {
+  if (nitems <= 0) return;
+  const size_t need = smem3(L.bmax);
+  set_smem((const void*)k_panel, need);
+  k_panel<<<nitems, 256, need, s>>>(L, batch_cl, items);
+}
+
+void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
+  if (ntargets <= 0) return;
+  k_schur<<<ntargets, 256, 0, s>>>(L, targets, contrib);
+}
+
+void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {
+  if (n > 0) k_copy<<<n, 256, 0, s>>>(d);
+}
+
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s) {
+  if (n > 0) k_gemm<<<n, 256, 0, s>>>(d);
+}
+
+int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches) {
+  (void)tol;
+  double* scale = reinterpret_cast<double*>(scratch);
+  cudaMemsetAsync(scale, 0, sizeof(double), s);
+  const long long n2 = (long long)n * n;
+  k_absmax<<<(int)std::min<long long>(1024, (n2 + 255) / 256), 256, 0, s>>>(A, n2, scale);
+  *launches += 1;
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int kb = std::min(32, n - k0);
+    k_lu_panel<<<1, 256, 0, s>>>(A, n, k0, kb, scale, err);
+    const int rest = n - k0 - kb;
+    *launches += 1;
+    if (rest > 0) {
+      k_lu_trsm<<<(rest + 127) / 128, 128, 0, s>>>(A, n, k0, kb);
+      dim3 g((rest + 63) / 64, (rest + 63) / 64);
+      const int sm = (64 * 33 + 32 * 65) * (int)sizeof(cplx);
+      cudaFuncSetAttribute((const void*)k_lu_update, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      k_lu_update<<<g, 256, sm, s>>>(A, n, k0, kb);
+      *launches += 2;
+    }
+  }
+  return 0;
+}
+
+}  // namespace h2g

@@ -1,0 +1,97 @@
+// Device-side state of one tree level during the factorization and the
+// launch entry points of the level kernels (factor.cu).
+#pragma once
+
+#include "device.cuh"
+
+namespace h2g {
+
+struct DevLevel {
+  int level;
+  int nl;
+  int bmax;
+  double eps;
+  const int* bsz;
+  const int* pos;
+  const int* korig;
+  int* kfin;
+  // dense blocks (stride bmax^2, ld = rows)
+  cplx* D;
+  const int* drow;
+  const int* dcol;
+  const int* diag_blk;
+  // fills (stride bmax^2, ld = rows)
+  cplx* F;
+  int* fexists;
+  const int* frow;
+  const int* fcol;
+  // neighbour lists
+  const int* R_ptr;
+  const int* R_nb;
+  const int* C_ptr;
+  const int* C_nb;
+  const int* G_ptr;
+  const int* G_fill;
+  const unsigned char* G_tr;
+  // level-entry basis V (b x korig) and its complement Vp (b x (b-korig)),
+  // stride bmax^2, ld b
+  const cplx* V0;
+  cplx* Vp;
+  // chain storage (complex elements)
+  cplx* chain;
+  const long long* Qt_off;
+  const long long* L11_off;
+  const long long* U11_off;
+  const long long* Lbar_off;  // per R entry
+  const long long* Ubar_off;  // per C entry
+  const long long* Lself_off;
+  const long long* Uself_off;
+  // scratch
+  cplx* lift;                 // lifted panels, same offsets as Lbar/Ubar (pool base)
+  const long long* Linv_off;  // L11^{-1}, U11^{-1} (e x e) in the chain
+  const long long* Uinv_off;
+  cplx* gram;                 // gram partials: [slot][part] stride bmax^2
+  double* gram_cmax;          // [slot][part]
+  int gram_parts;
+  DevError* err;
+};
+
+struct PanelItemD {
+  int q, side, nb, blk, entry, lift;
+};
+struct SchurTargetD {
+  int kind, idx, c0, c1;
+};
+struct SchurContribD {
+  int t, r, c, flags;
+};
+
+// Descriptor-driven batched kernels used for merges, root assembly and paints
+// (sizes known on the host at level boundaries).
+struct CopyDesc {
+  const cplx* src;  // nullptr: zero fill
+  cplx* dst;
+  int lds, ldd, m, n;
+  int accumulate;   // dst += src
+  int pad;
+};
+struct GemmDesc {
+  const cplx* A;
+  const cplx* B;
+  cplx* C;
+  int lda, ldb, ldc, m, n, k, opA, opB;
+  double alpha, beta;
+};
+
+void launch_complement(const DevLevel& L, cudaStream_t s);
+void launch_gram(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
+void launch_head(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
+void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s);
+void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
+void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s);
+void launch_zero_desc_flags(int* p, int n, cudaStream_t s);
+int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches);
+size_t head_smem_bytes(int bmax);
+
+}  // namespace h2g

@@ -1,0 +1,426 @@
+// Host symbolic analysis, see plan.hpp.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <random>
+#include <numeric>
+#include <stdexcept>
+
+#include "../../include/h2g.h"
+
+namespace h2g {
+
+namespace {
+bool pair_less(const Pair& a, const Pair& b) { return a.row < b.row || (a.row == b.row && a.col < b.col); }
+}  // namespace
+
+Structure structure_from_desc(const h2g_matrix_desc* d) {
+  if (!d || d->n <= 0 || d->depth < 0 || d->depth > 24) throw std::invalid_argument("matrix desc: bad n/depth");
+  Structure S;
+  S.n = d->n;
+  S.depth = d->depth;
+  S.eta = d->eta;
+  const int nc = S.num_clusters();
+  S.begin.assign(d->cluster_begin, d->cluster_begin + nc);
+  S.end.assign(d->cluster_end, d->cluster_end + nc);
+  S.adm.resize(static_cast<size_t>(S.depth) + 1);
+  S.split.resize(static_cast<size_t>(S.depth) + 1);
+  S.adm_offset.assign(static_cast<size_t>(S.depth) + 2, 0);
+  for (int l = 0; l <= S.depth; ++l) {
+    for (int64_t q = d->adm_offsets[l]; q < d->adm_offsets[l + 1]; ++q) S.adm[static_cast<size_t>(l)].push_back({d->adm_pairs[2 * q], d->adm_pairs[2 * q + 1]});
+    for (int64_t q = d->split_offsets[l]; q < d->split_offsets[l + 1]; ++q)
+      S.split[static_cast<size_t>(l)].push_back({d->split_pairs[2 * q], d->split_pairs[2 * q + 1]});
+    S.adm_offset[static_cast<size_t>(l) + 1] = d->adm_offsets[l + 1];
+    if (!std::is_sorted(S.adm[static_cast<size_t>(l)].begin(), S.adm[static_cast<size_t>(l)].end(), pair_less) ||
+        !std::is_sorted(S.split[static_cast<size_t>(l)].begin(), S.split[static_cast<size_t>(l)].end(), pair_less))
+      throw std::invalid_argument("matrix desc: block pairs must be sorted by (row, col)");
+  }
+  for (int64_t q = 0; q < d->num_leaf_pairs; ++q) S.leaf.push_back({d->leaf_pairs[2 * q], d->leaf_pairs[2 * q + 1]});
+  if (!std::is_sorted(S.leaf.begin(), S.leaf.end(), pair_less)) throw std::invalid_argument("matrix desc: leaf pairs must be sorted");
+  for (int l = 0; l <= S.depth; ++l)
+    if (!S.adm[static_cast<size_t>(l)].empty()) {
+      S.l0 = l;
+      break;
+    }
+  return S;
+}
+
+// ---------------------------------------------------------------------------
+// Host tree + partition (cluster_tree.hpp:71-118, block_tree.hpp:30-73),
+// used by h2g_matrix_build. Same splitting rule and tie-break (longest bbox
+// axis, median index, coordinate then original index), same strict
+// admissibility diam < eta * dist.
+namespace {
+struct Box {
+  double lo[3], hi[3];
+  double diameter() const {
+    const double x = hi[0] - lo[0], y = hi[1] - lo[1], z = hi[2] - lo[2];
+    return std::sqrt(x * x + y * y + z * z);
+  }
+};
+double box_distance(const Box& a, const Box& b) {
+  double d2 = 0.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    const double g = std::max({a.lo[ax] - b.hi[ax], b.lo[ax] - a.hi[ax], 0.0});
+    d2 += g * g;
+  }
+  return std::sqrt(d2);
+}
+}  // namespace
+
+Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm_out) {
+  if (n <= 0) throw std::invalid_argument("build: empty point cloud");
+  if (leafsize < 1) throw std::invalid_argument("build: leafsize must be >= 1");
+  if (eta <= 0.0) throw std::invalid_argument("build: eta must be positive");
+  Structure S;
+  S.n = n;
+  S.eta = eta;
+  int depth = 0;
+  while ((n + (int64_t(1) << depth) - 1) / (int64_t(1) << depth) > leafsize) ++depth;
+  S.depth = depth;
+  const int nc = S.num_clusters();
+  S.begin.assign(static_cast<size_t>(nc), 0);
+  S.end.assign(static_cast<size_t>(nc), 0);
+  std::vector<Box> box(static_cast<size_t>(nc));
+  std::vector<int64_t> perm(static_cast<size_t>(n));
+  std::iota(perm.begin(), perm.end(), int64_t(0));
+  struct Item {
+    int id, level;
+    int64_t b, e;
+  };
+  std::vector<Item> stack{{0, 0, 0, n}};
+  while (!stack.empty()) {
+    const Item it = stack.back();
+    stack.pop_back();
+    S.begin[static_cast<size_t>(it.id)] = it.b;
+    S.end[static_cast<size_t>(it.id)] = it.e;
+    Box& bx = box[static_cast<size_t>(it.id)];
+    for (int a = 0; a < 3; ++a) bx.lo[a] = bx.hi[a] = 0.0;
+    if (it.b < it.e) {
+      for (int a = 0; a < 3; ++a) bx.lo[a] = bx.hi[a] = pts[3 * perm[static_cast<size_t>(it.b)] + a];
+      for (int64_t i = it.b + 1; i < it.e; ++i)
+        for (int a = 0; a < 3; ++a) {
+          const double v = pts[3 * perm[static_cast<size_t>(i)] + a];
+          bx.lo[a] = std::min(bx.lo[a], v);
+          bx.hi[a] = std::max(bx.hi[a], v);
+        }
+    }
+    if (it.level == depth) continue;
+    const double e0 = bx.hi[0] - bx.lo[0], e1 = bx.hi[1] - bx.lo[1], e2 = bx.hi[2] - bx.lo[2];
+    const double ext[3] = {e0, e1, e2};
+    int ax = 0;
+    if (ext[1] > ext[0]) ax = 1;
+    if (ext[2] > ext[ax]) ax = 2;
+    const int64_t mid = it.b + (it.e - it.b + 1) / 2;
+    std::nth_element(perm.begin() + it.b, perm.begin() + mid, perm.begin() + it.e, [&](int64_t a, int64_t b) {
+      const double ca = pts[3 * a + ax], cb = pts[3 * b + ax];
+      return ca < cb || (ca == cb && a < b);
+    });
+    stack.push_back({2 * it.id + 1, it.level + 1, it.b, mid});
+    stack.push_back({2 * it.id + 2, it.level + 1, mid, it.e});
+  }
+  S.adm.resize(static_cast<size_t>(depth) + 1);
+  S.split.resize(static_cast<size_t>(depth) + 1);
+  auto level_of = [](int id) {
+    int l = 0;
+    while ((2 << l) - 1 <= id) ++l;
+    return l;
+  };
+  std::vector<Pair> st{{0, 0}};
+  while (!st.empty()) {
+    const Pair p = st.back();
+    st.pop_back();
+    const Box& t = box[static_cast<size_t>(p.row)];
+    const Box& s = box[static_cast<size_t>(p.col)];
+    const int lt = level_of(p.row);
+    if (std::max(t.diameter(), s.diameter()) < eta * box_distance(t, s)) {
+      S.adm[static_cast<size_t>(lt)].push_back(p);
+    } else if (lt == depth) {
+      S.leaf.push_back(p);
+    } else {
+      S.split[static_cast<size_t>(lt)].push_back(p);
+      for (int a = 1; a >= 0; --a)
+        for (int b = 1; b >= 0; --b) st.push_back({2 * p.row + 1 + a, 2 * p.col + 1 + b});
+    }
+  }
+  for (auto& v : S.adm) std::sort(v.begin(), v.end(), pair_less);
+  for (auto& v : S.split) std::sort(v.begin(), v.end(), pair_less);
+  std::sort(S.leaf.begin(), S.leaf.end(), pair_less);
+  S.adm_offset.assign(static_cast<size_t>(depth) + 2, 0);
+  for (int l = 0; l <= depth; ++l) S.adm_offset[static_cast<size_t>(l) + 1] = S.adm_offset[static_cast<size_t>(l)] + static_cast<int64_t>(S.adm[static_cast<size_t>(l)].size());
+  for (int l = 0; l <= depth; ++l)
+    if (!S.adm[static_cast<size_t>(l)].empty()) {
+      S.l0 = l;
+      break;
+    }
+  if (perm_out) *perm_out = std::move(perm);
+  return S;
+}
+
+// ---------------------------------------------------------------------------
+std::vector<LevelSym> build_levels(const Structure& S, int stop) {
+  std::vector<LevelSym> out;
+  const int last = std::max(stop - 1, 0);
+  const int L = S.depth;
+  const bool no_levels = stop > L;  // no admissible blocks: root = leaf level
+  const int lowest = no_levels ? L : last;
+  for (int l = L; l >= lowest; --l) {
+    LevelSym Y;
+    Y.level = l;
+    Y.nl = 1 << l;
+    Y.first = Structure::first(l);
+    const int nl = Y.nl, first = Y.first;
+    const bool processed = !no_levels && l >= stop;
+    const std::vector<Pair>& dp = (l == L) ? S.leaf : S.split[static_cast<size_t>(l)];
+    Y.diag_blk.assign(static_cast<size_t>(nl), -1);
+    for (size_t q = 0; q < dp.size(); ++q) {
+      const int r = dp[q].row - first, c = dp[q].col - first;
+      if (r < 0 || r >= nl || c < 0 || c >= nl) throw std::invalid_argument("dense pair outside its level");
+      Y.drow.push_back(r);
+      Y.dcol.push_back(c);
+      Y.dense_of[int64_t(r) * nl + c] = static_cast<int>(q);
+      if (r == c) Y.diag_blk[static_cast<size_t>(r)] = static_cast<int>(q);
+    }
+    for (int t = 0; t < nl; ++t)
+      if (Y.diag_blk[static_cast<size_t>(t)] < 0) throw std::invalid_argument("cluster without a dense diagonal block");
+    // R / C entries
+    std::vector<std::vector<std::pair<int, int>>> R(static_cast<size_t>(nl)), Cc(static_cast<size_t>(nl));
+    for (size_t q = 0; q < Y.drow.size(); ++q) {
+      const int r = Y.drow[q], c = Y.dcol[q];
+      if (r == c) continue;
+      Cc[static_cast<size_t>(r)].push_back({c, static_cast<int>(q)});
+      R[static_cast<size_t>(c)].push_back({r, static_cast<int>(q)});
+    }
+    Y.R_ptr.assign(1, 0);
+    Y.C_ptr.assign(1, 0);
+    for (int t = 0; t < nl; ++t) {
+      auto& rr = R[static_cast<size_t>(t)];
+      std::sort(rr.begin(), rr.end());
+      for (auto& e : rr) Y.R_nb.push_back(e.first), Y.R_blk.push_back(e.second);
+      Y.R_ptr.push_back(static_cast<int>(Y.R_nb.size()));
+      auto& cc = Cc[static_cast<size_t>(t)];
+      std::sort(cc.begin(), cc.end());
+      for (auto& e : cc) Y.C_nb.push_back(e.first), Y.C_blk.push_back(e.second);
+      Y.C_ptr.push_back(static_cast<int>(Y.C_nb.size()));
+    }
+    // fill targets
+    std::vector<int64_t> keys;
+    if (processed) {
+      for (int m = 0; m < nl; ++m)
+        for (int a = Y.R_ptr[static_cast<size_t>(m)]; a < Y.R_ptr[static_cast<size_t>(m) + 1]; ++a)
+          for (int b = Y.C_ptr[static_cast<size_t>(m)]; b < Y.C_ptr[static_cast<size_t>(m) + 1]; ++b) {
+            const int j = Y.R_nb[static_cast<size_t>(a)], c = Y.C_nb[static_cast<size_t>(b)];
+            if (Y.dense_index(j, c) < 0) keys.push_back(int64_t(j) * nl + c);
+          }
+    }
+    if (!out.empty()) {
+      const LevelSym& P = out.back();  // level l+1
+      for (size_t f = 0; f < P.frow.size(); ++f)
+        if (P.fadm[f] < 0) {
+          const int pj = P.frow[f] / 2, pc = P.fcol[f] / 2;
+          if (Y.dense_index(pj, pc) >= 0) throw std::invalid_argument("merge_permute: carried fill-in resurfaced on a dense block");
+          keys.push_back(int64_t(pj) * nl + pc);
+        }
+    }
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    const auto& adm = S.adm[static_cast<size_t>(l)];
+    for (int64_t k : keys) {
+      const int r = static_cast<int>(k / nl), c = static_cast<int>(k % nl);
+      const Pair hp{r + first, c + first};
+      auto it = std::lower_bound(adm.begin(), adm.end(), hp, pair_less);
+      const int ai = (it != adm.end() && it->row == hp.row && it->col == hp.col) ? static_cast<int>(it - adm.begin()) : -1;
+      Y.fill_of[k] = static_cast<int>(Y.frow.size());
+      Y.frow.push_back(r);
+      Y.fcol.push_back(c);
+      Y.fadm.push_back(ai);
+      if (ai >= 0) ++Y.nledger;
+    }
+    // parent links of level l+1 carried fills
+    if (!out.empty()) {
+      LevelSym& P = out.back();
+      P.carried_parent.assign(P.frow.size(), -1);
+      for (size_t f = 0; f < P.frow.size(); ++f)
+        if (P.fadm[f] < 0) P.carried_parent[f] = Y.fill_index(P.frow[f] / 2, P.fcol[f] / 2);
+    }
+    // step-0 gather lists: ledger keys touching t in map order, then carried
+    {
+      std::vector<std::vector<int>> by_row(static_cast<size_t>(nl)), by_col(static_cast<size_t>(nl));
+      for (size_t f = 0; f < Y.frow.size(); ++f) {
+        by_row[static_cast<size_t>(Y.frow[f])].push_back(static_cast<int>(f));
+        by_col[static_cast<size_t>(Y.fcol[f])].push_back(static_cast<int>(f));
+      }
+      Y.G_ptr.assign(1, 0);
+      for (int t = 0; t < nl; ++t) {
+        for (int kind = 0; kind < 2; ++kind) {
+          auto want = [&](int f) { return (Y.fadm[static_cast<size_t>(f)] >= 0) == (kind == 0); };
+          // (x, t), x < t
+          for (int f : by_col[static_cast<size_t>(t)])
+            if (want(f) && Y.frow[static_cast<size_t>(f)] < t) Y.G_fill.push_back(f), Y.G_tr.push_back(1);
+          // (t, y)
+          for (int f : by_row[static_cast<size_t>(t)])
+            if (want(f)) Y.G_fill.push_back(f), Y.G_tr.push_back(0);
+          // (x, t), x > t
+          for (int f : by_col[static_cast<size_t>(t)])
+            if (want(f) && Y.frow[static_cast<size_t>(f)] > t) Y.G_fill.push_back(f), Y.G_tr.push_back(1);
+        }
+        Y.G_ptr.push_back(static_cast<int>(Y.G_fill.size()));
+      }
+    }
+    out.push_back(std::move(Y));
+  }
+  if (!out.empty()) out.back().carried_parent.assign(out.back().frow.size(), -1);
+  return out;
+}
+
+LevelSchedule build_schedule(const LevelSym& L, int kind) {
+  const int nl = L.nl;
+  std::vector<std::vector<int>> nb(static_cast<size_t>(nl));
+  for (size_t q = 0; q < L.drow.size(); ++q) {
+    const int r = L.drow[q], c = L.dcol[q];
+    if (r == c) continue;
+    nb[static_cast<size_t>(r)].push_back(c);
+    nb[static_cast<size_t>(c)].push_back(r);
+  }
+  std::vector<int> key(static_cast<size_t>(nl), 0);
+  if (kind == H2G_SCHEDULE_COLORED) {
+    std::vector<int> mark(static_cast<size_t>(nl) + 1, -1);
+    for (int t = 0; t < nl; ++t) {
+      for (int x : nb[static_cast<size_t>(t)])
+        if (x < t) mark[static_cast<size_t>(key[static_cast<size_t>(x)])] = t;
+      int c = 0;
+      while (mark[static_cast<size_t>(c)] == t) ++c;
+      key[static_cast<size_t>(t)] = c;
+    }
+  } else {
+    // dependency wavefronts of the ascending-id order: every lower-id
+    // neighbour completes before t starts, no higher-id neighbour does.
+    for (int t = 0; t < nl; ++t) {
+      int w = 0;
+      for (int x : nb[static_cast<size_t>(t)])
+        if (x < t) w = std::max(w, key[static_cast<size_t>(x)] + 1);
+      key[static_cast<size_t>(t)] = w;
+    }
+  }
+  const int nb_batches = nl ? *std::max_element(key.begin(), key.end()) + 1 : 0;
+  LevelSchedule S;
+  S.order = key;
+  std::vector<std::vector<int>> bat(static_cast<size_t>(nb_batches));
+  for (int t = 0; t < nl; ++t) bat[static_cast<size_t>(key[static_cast<size_t>(t)])].push_back(t);
+  S.batch_ptr.assign(1, 0);
+  for (auto& b : bat) {
+    for (int t : b) S.batch_cl.push_back(t);
+    S.batch_ptr.push_back(static_cast<int>(S.batch_cl.size()));
+  }
+  return S;
+}
+
+LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
+  LevelWork W;
+  const int nbat = static_cast<int>(sch.batch_ptr.size()) - 1;
+  const auto& ord = sch.order;
+  W.panel_ptr.assign(1, 0);
+  W.schur_ptr.assign(1, 0);
+  W.fsolve_ptr.assign(1, 0);
+  struct Tmp {
+    int64_t key;  // kind, idx
+    SchurContrib c;
+  };
+  std::vector<Tmp> tmp;
+  struct STmp {
+    int64_t seg;
+    SolveContrib c;
+  };
+  std::vector<STmp> stmp;
+  for (int b = 0; b < nbat; ++b) {
+    const int p0 = sch.batch_ptr[static_cast<size_t>(b)], p1 = sch.batch_ptr[static_cast<size_t>(b) + 1];
+    W.max_batch = std::max(W.max_batch, p1 - p0);
+    tmp.clear();
+    stmp.clear();
+    for (int q = p0; q < p1; ++q) {
+      const int t = sch.batch_cl[static_cast<size_t>(q)];
+      const int ot = ord[static_cast<size_t>(t)];
+      for (int e = L.C_ptr[static_cast<size_t>(t)]; e < L.C_ptr[static_cast<size_t>(t) + 1]; ++e) {
+        const int c = L.C_nb[static_cast<size_t>(e)];
+        W.panel.push_back({q - p0, 0, c, L.C_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(c)] < ot ? 1 : 0});
+      }
+      for (int e = L.R_ptr[static_cast<size_t>(t)]; e < L.R_ptr[static_cast<size_t>(t) + 1]; ++e) {
+        const int j = L.R_nb[static_cast<size_t>(e)];
+        W.panel.push_back({q - p0, 1, j, L.R_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(j)] < ot ? 1 : 0});
+      }
+      // Schur products rows x cols, self last (factorization.hpp:403-425)
+      const int r0 = L.R_ptr[static_cast<size_t>(t)], r1 = L.R_ptr[static_cast<size_t>(t) + 1];
+      const int c0 = L.C_ptr[static_cast<size_t>(t)], c1 = L.C_ptr[static_cast<size_t>(t) + 1];
+      for (int a = r0; a <= r1; ++a) {
+        const bool rself = a == r1;
+        const int j = rself ? t : L.R_nb[static_cast<size_t>(a)];
+        for (int e = c0; e <= c1; ++e) {
+          const bool cself = e == c1;
+          if (rself && cself) continue;  // D(t,t) corner: head kernel
+          const int c = cself ? t : L.C_nb[static_cast<size_t>(e)];
+          SchurContrib sc{t, rself ? -1 - t : a, cself ? -1 - t : e, 0};
+          int kind, idx;
+          if (rself) {
+            kind = 0, idx = L.C_blk[static_cast<size_t>(e)];
+          } else if (cself) {
+            kind = 0, idx = L.R_blk[static_cast<size_t>(a)];
+          } else {
+            idx = L.dense_index(j, c);
+            kind = 0;
+            if (idx < 0) {
+              kind = 1;
+              idx = L.fill_index(j, c);
+              if (idx < 0) throw std::logic_error("plan: Schur target neither dense nor fill");
+              if (ord[static_cast<size_t>(j)] < ot) sc.flags |= 1;
+              if (ord[static_cast<size_t>(c)] < ot) sc.flags |= 2;
+            }
+          }
+          tmp.push_back({(int64_t(kind) << 40) | int64_t(idx), sc});
+          ++W.schur_products;
+        }
+        // forward-solve Lbar targets (solve.hpp:51)
+        stmp.push_back({rself ? -1 - int64_t(t) : int64_t(j), {t, rself ? -1 - t : a}});
+      }
+    }
+    std::stable_sort(tmp.begin(), tmp.end(), [](const Tmp& x, const Tmp& y) { return x.key < y.key; });
+    for (size_t i = 0; i < tmp.size();) {
+      size_t j = i;
+      while (j < tmp.size() && tmp[j].key == tmp[i].key) ++j;
+      SchurTarget T{static_cast<int32_t>(tmp[i].key >> 40), static_cast<int32_t>(tmp[i].key & ((int64_t(1) << 40) - 1)),
+                    static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
+      for (size_t k = i; k < j; ++k) W.contrib.push_back(tmp[k].c);
+      W.schur.push_back(T);
+      i = j;
+    }
+    std::stable_sort(stmp.begin(), stmp.end(), [](const STmp& x, const STmp& y) { return x.seg < y.seg; });
+    for (size_t i = 0; i < stmp.size();) {
+      size_t j = i;
+      while (j < stmp.size() && stmp[j].seg == stmp[i].seg) ++j;
+      SolveTarget T{static_cast<int32_t>(stmp[i].seg), static_cast<int32_t>(W.fcontrib.size()), static_cast<int32_t>(W.fcontrib.size() + (j - i))};
+      for (size_t k = i; k < j; ++k) W.fcontrib.push_back(stmp[k].c);
+      W.fsolve.push_back(T);
+      i = j;
+    }
+    W.panel_ptr.push_back(static_cast<int32_t>(W.panel.size()));
+    W.schur_ptr.push_back(static_cast<int32_t>(W.schur.size()));
+    W.fsolve_ptr.push_back(static_cast<int32_t>(W.fsolve.size()));
+  }
+  return W;
+}
+
+}  // namespace h2g
+
+// Seeded right-hand side exactly as proj/tools/h2lu_cli.cpp:181-191. Compiled
+// by g++ (not nvcc) so cxd(g(rng), g(rng)) evaluates its arguments in the
+// same order as the reference build.
+extern "C" void h2g_random_rhs(int64_t n, uint64_t seed, double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> g;
+  for (int64_t i = 0; i < n; ++i) {
+    std::complex<double> v = std::complex<double>(g(rng), g(rng));
+    out[2 * i] = v.real();
+    out[2 * i + 1] = v.imag();
+  }
+}

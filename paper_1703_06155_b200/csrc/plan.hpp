@@ -1,0 +1,130 @@
+// Host-side symbolic analysis of an H² factorization (the structural part of
+// proj/include/h2lu/factorization.hpp, done once per matrix and schedule).
+//
+// The reference discovers structure on the fly by scanning std::maps for every
+// cluster (factorization.hpp:268-293, :345, :404, :436). Here
+// every level's structure — dense blocks, fill-in targets (ledger/carried),
+// Schur target maps, merge maps — is derived once from the block partition,
+// laid out as CSR arrays and uploaded; the device kernels only index them.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/h2g.h"
+
+namespace h2g {
+
+struct Pair {
+  int row, col;
+};
+
+// Cluster tree + block partition, as described by h2g_matrix_desc.
+struct Structure {
+  int64_t n = 0;
+  int depth = 0;
+  double eta = 1.0;
+  std::vector<int64_t> begin, end;          // [num_clusters]
+  std::vector<std::vector<Pair>> adm, split;  // [depth+1], sorted (row, col)
+  std::vector<Pair> leaf;                     // sorted
+  std::vector<int64_t> adm_offset;            // global admissible index of (level, 0)
+  int l0 = -1;
+  int num_clusters() const { return (2 << depth) - 1; }
+  static int first(int l) { return (1 << l) - 1; }
+  int64_t num_adm() const { return adm_offset.empty() ? 0 : adm_offset.back(); }
+};
+
+// One level's static structure. Cluster ids are LOCAL (0..nl-1, heap id =
+// first + local).
+struct LevelSym {
+  int level = 0, nl = 0, first = 0;
+  // dense (inadmissible at this level) blocks, sorted (row, col)
+  std::vector<int> drow, dcol, diag_blk;
+  // row entries R(t): j with (j,t) dense, j != t, ascending j (the "rows"
+  // list of factorization.hpp:403-408) and col entries C(t): c with (t,c)
+  // dense, c != t, ascending (the "cols" list).
+  std::vector<int> R_ptr, R_nb, R_blk, C_ptr, C_nb, C_blk;
+  // fill targets (ledger: admissible at this level; carried: owned by a
+  // coarser admissible ancestor), sorted (row, col)
+  std::vector<int> frow, fcol, fadm;  // fadm = index into adm[level] or -1 (carried)
+  int nledger = 0;
+  // step-0 gather list per cluster (factorization.hpp:278-293 order: ledger
+  // keys touching t in map order, then carried keys): fill index + transposed
+  std::vector<int> G_ptr, G_fill;
+  std::vector<uint8_t> G_tr;
+  // carried fills -> parent fill index at level-1, and which child slots
+  std::vector<int> carried_parent;  // [nfill], -1 for ledger
+  // dense-pair and fill lookup
+  std::unordered_map<int64_t, int> dense_of, fill_of;
+  int dense_index(int r, int c) const {
+    auto it = dense_of.find(int64_t(r) * nl + c);
+    return it == dense_of.end() ? -1 : it->second;
+  }
+  int fill_index(int r, int c) const {
+    auto it = fill_of.find(int64_t(r) * nl + c);
+    return it == fill_of.end() ? -1 : it->second;
+  }
+};
+
+// Processing order of one level: batches of mutually non-adjacent clusters.
+struct LevelSchedule {
+  std::vector<int> batch_ptr, batch_cl;  // local ids, ascending within a batch
+  std::vector<int> order;                // [nl] batch index of each cluster
+};
+
+// Per-batch work lists (static for a schedule; sizes resolved on device).
+struct PanelItem {
+  int32_t q;      // slot of the cluster in its batch
+  int32_t side;   // 0: column item D(t,c) (Ubar), 1: row item D(j,t) (Lbar)
+  int32_t nb;     // neighbour local id
+  int32_t blk;    // dense block index
+  int32_t entry;  // C entry (side 0) or R entry (side 1) global index
+  int32_t lift;   // neighbour eliminated earlier: also store the lifted panel
+};
+
+struct SchurTarget {
+  int32_t kind;   // 0 dense, 1 fill
+  int32_t idx;    // dense block / fill index
+  int32_t c0, c1; // contribution range
+};
+
+struct SchurContrib {
+  int32_t t;      // cluster local id
+  int32_t r;      // R entry global index, or -1 - t for the self row
+  int32_t c;      // C entry global index, or -1 - t for the self column
+  int32_t flags;  // bit0: lifted row panel, bit1: lifted column panel
+};
+
+struct SolveTarget {
+  int32_t seg;    // neighbour local id j (or -1 - m: retained tail of record m)
+  int32_t c0, c1; // contribution range into SolveContrib
+};
+struct SolveContrib {
+  int32_t m;      // record (cluster local id)
+  int32_t entry;  // R entry global index, or -1 - m for self
+};
+
+struct LevelWork {
+  std::vector<int32_t> panel_ptr;  // per batch
+  std::vector<PanelItem> panel;
+  std::vector<int32_t> schur_ptr;  // per batch
+  std::vector<SchurTarget> schur;
+  std::vector<SchurContrib> contrib;
+  std::vector<int32_t> fsolve_ptr;  // per batch
+  std::vector<SolveTarget> fsolve;
+  std::vector<SolveContrib> fcontrib;
+  int max_batch = 0;
+  int64_t schur_products = 0;  // structural count (upper bound)
+};
+
+Structure structure_from_desc(const h2g_matrix_desc* d);
+Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm);
+
+// Levels from depth down to (and including) `stop`.
+std::vector<LevelSym> build_levels(const Structure& S, int stop);
+LevelSchedule build_schedule(const LevelSym& L, int kind);
+LevelWork build_work(const LevelSym& L, const LevelSchedule& sch);
+
+}  // namespace h2g

@@ -1,0 +1,236 @@
+// Forward / backward substitution on the device (proj/include/h2lu/solve.hpp:
+// 43-83), batch by batch in the factorization's elimination order. Vectors
+// are n x nrhs column-major complex128 in tree order, updated in place.
+#include <algorithm>
+
+#include "solve.cuh"
+
+namespace h2g {
+
+// seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50). One CTA per
+// record of the batch.
+__global__ void __launch_bounds__(256) k_fwd_head(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int t = batch_cl[blockIdx.x];
+  const int b = S.bsz[t], e = b - S.kfin[t];
+  const long long p0 = S.pos[t];
+  cplx* sS = reinterpret_cast<cplx*>(smraw);  // b x nrhs
+  cplx* sO = sS + (size_t)b * nrhs;           // b x nrhs
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
+  __syncthreads();
+  const cplx* Q = S.chain + S.Qt_off[t];
+  cta_gemm(b, nrhs, b, 1.0, Q, b, OP_C, sS, b, OP_N, 0.0, sO, b);
+  __syncthreads();
+  if (e > 0) {
+    if (explicit_inv) {
+      const cplx* Li = S.chain + S.Linv_off[t];
+      cta_gemm(e, nrhs, e, 1.0, Li, e, OP_N, sO, b, OP_N, 0.0, sS, b);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sO[(idx % e) + (idx / e) * b] = sS[(idx % e) + (idx / e) * b];
+      __syncthreads();
+    } else {
+      const cplx* L = S.chain + S.L11_off[t];
+      for (int p = 0; p < e; ++p) {
+        for (int idx = threadIdx.x; idx < (e - p - 1) * nrhs; idx += blockDim.x) {
+          const int i = p + 1 + idx % (e - p - 1), c = idx / (e - p - 1);
+          const cplx l = L[i + (size_t)p * e], x = sO[p + c * b];
+          cplx v = sO[i + c * b];
+          v.x -= l.x * x.x - l.y * x.y;
+          v.y -= l.x * x.y + l.y * x.x;
+          sO[i + c * b] = v;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
+}
+
+// y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51), contributions of a
+// target segment summed in a fixed order.
+__global__ void __launch_bounds__(256) k_fwd_lbar(SolveLevel S, const SolveTargetD* targets, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs) {
+  const SolveTargetD tg = targets[blockIdx.x];
+  int rows;
+  long long base;
+  if (tg.seg >= 0) {
+    rows = S.bsz[tg.seg];
+    base = S.pos[tg.seg];
+  } else {
+    const int m = -1 - tg.seg;
+    rows = S.kfin[m];
+    base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
+  }
+  for (int idx = threadIdx.x; idx < rows * nrhs; idx += blockDim.x) {
+    const int i = idx % rows, c = idx / rows;
+    cplx acc = czero();
+    for (int ci = tg.c0; ci < tg.c1; ++ci) {
+      const SolveContribD cb = contrib[ci];
+      const int m = cb.m;
+      const int e = S.bsz[m] - S.kfin[m];
+      if (e == 0) continue;
+      const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[m]);
+      const cplx* h = y + S.pos[m] + c * ldy;
+      for (int p = 0; p < e; ++p) cfma(acc, M[i + (size_t)p * rows], h[p]);
+    }
+    cplx* o = y + base + i + c * ldy;
+    *o = csub(*o, acc);
+  }
+}
+
+// Backward record (solve.hpp:73-81): head -= sum_c Ubar(m,c) y_c; U11 solve;
+// seg <- conj(Qt) seg. One CTA per record.
+__global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int t = batch_cl[blockIdx.x];
+  const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
+  const long long p0 = S.pos[t];
+  cplx* sS = reinterpret_cast<cplx*>(smraw);
+  cplx* sO = sS + (size_t)b * nrhs;
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
+  __syncthreads();
+  if (e > 0) {
+    for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
+      const int i = idx % e, c = idx / e;
+      cplx acc = czero();
+      for (int q = S.C_ptr[t]; q < S.C_ptr[t + 1]; ++q) {
+        const int nb = S.C_nb[q];
+        const int cols = S.bsz[nb];
+        const cplx* M = S.chain + S.Ubar_off[q];
+        const cplx* x = y + S.pos[nb] + c * ldy;
+        for (int p = 0; p < cols; ++p) cfma(acc, M[i + (size_t)p * e], x[p]);
+      }
+      if (kf > 0) {
+        const cplx* M = S.chain + S.Uself_off[t];
+        const cplx* x = sS + e + c * b;
+        for (int p = 0; p < kf; ++p) cfma(acc, M[i + (size_t)p * e], x[p]);
+      }
+      sS[i + c * b] = csub(sS[i + c * b], acc);
+    }
+    __syncthreads();
+    if (explicit_inv) {
+      const cplx* Ui = S.chain + S.Uinv_off[t];
+      cta_gemm(e, nrhs, e, 1.0, Ui, e, OP_N, sS, b, OP_N, 0.0, sO, b);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sS[(idx % e) + (idx / e) * b] = sO[(idx % e) + (idx / e) * b];
+      __syncthreads();
+    } else {
+      const cplx* U = S.chain + S.U11_off[t];
+      for (int p = e - 1; p >= 0; --p) {
+        for (int c = threadIdx.x; c < nrhs; c += blockDim.x) sS[p + c * b] = cdiv(sS[p + c * b], U[p + (size_t)p * e]);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < p * nrhs; idx += blockDim.x) {
+          const int i = idx % p, c = idx / p;
+          const cplx u = U[i + (size_t)p * e], x = sS[p + c * b];
+          cplx v = sS[i + c * b];
+          v.x -= u.x * x.x - u.y * x.y;
+          v.y -= u.x * x.y + u.y * x.x;
+          sS[i + c * b] = v;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  const cplx* Q = S.chain + S.Qt_off[t];
+  cta_gemm(b, nrhs, b, 1.0, Q, b, OP_R, sS, b, OP_N, 0.0, sO, b);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
+}
+
+// (P v)[j] = v[src[j]] (gather, solve.hpp:18-23) or its inverse (scatter, :25-30).
+__global__ void k_permute(const long long* src, long long len, const cplx* in, cplx* out, long long ldy, int nrhs, int scatter) {
+  const long long total = len * nrhs;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total; idx += (long long)gridDim.x * blockDim.x) {
+    const long long j = idx % len, c = idx / len;
+    if (scatter)
+      out[src[j] + c * ldy] = in[j + c * ldy];
+    else
+      out[j + c * ldy] = in[src[j] + c * ldy];
+  }
+}
+
+__global__ void k_copy_cols(const cplx* in, cplx* out, long long len, long long ldy, int nrhs) {
+  const long long total = len * nrhs;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total; idx += (long long)gridDim.x * blockDim.x) {
+    const long long j = idx % len, c = idx / len;
+    out[j + c * ldy] = in[j + c * ldy];
+  }
+}
+
+// Dense root triangular solves (solve.hpp:55-58, :67-70); blocked by 64
+// columns, one CTA.
+__global__ void __launch_bounds__(512) k_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper) {
+  if (!upper) {
+    for (int p = 0; p < n; ++p) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < (n - p - 1) * nrhs; idx += blockDim.x) {
+        const int i = p + 1 + idx % (n - p - 1), c = idx / (n - p - 1);
+        const cplx l = A[i + (size_t)p * n], x = y[p + c * ldy];
+        cplx v = y[i + c * ldy];
+        v.x -= l.x * x.x - l.y * x.y;
+        v.y -= l.x * x.y + l.y * x.x;
+        y[i + c * ldy] = v;
+      }
+    }
+  } else {
+    for (int p = n - 1; p >= 0; --p) {
+      __syncthreads();
+      for (int c = threadIdx.x; c < nrhs; c += blockDim.x) y[p + c * ldy] = cdiv(y[p + c * ldy], A[p + (size_t)p * n]);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < p * nrhs; idx += blockDim.x) {
+        const int i = idx % p, c = idx / p;
+        const cplx u = A[i + (size_t)p * n], x = y[p + c * ldy];
+        cplx v = y[i + c * ldy];
+        v.x -= u.x * x.x - u.y * x.y;
+        v.y -= u.x * x.y + u.y * x.x;
+        y[i + c * ldy] = v;
+      }
+    }
+  }
+}
+
+// Non-finite check of the right-hand side (solve.hpp:15).
+__global__ void k_finite(const cplx* y, long long total, int* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const cplx v = y[i];
+    if (!isfinite(v.x) || !isfinite(v.y)) *bad = 1;
+  }
+}
+
+// ----------------------------------------------------------------- launchers
+static void smem_attr(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_fwd_head(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
+  smem_attr((const void*)k_fwd_head, smem);
+  k_fwd_head<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv);
+}
+
+void launch_fwd_lbar(const SolveLevel& S, const SolveTargetD* t, int nt, const SolveContribD* c, cplx* y, long long ldy, int nrhs, cudaStream_t s) {
+  if (nt > 0) k_fwd_lbar<<<nt, 256, 0, s>>>(S, t, c, y, ldy, nrhs);
+}
+
+void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
+  smem_attr((const void*)k_bwd, smem);
+  k_bwd<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv);
+}
+
+void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s) {
+  if (len <= 0) return;
+  const int grid = (int)std::min<long long>(4096, (len * nrhs + 255) / 256);
+  k_permute<<<grid, 256, 0, s>>>(src, len, y, tmp, ldy, nrhs, scatter);
+  k_copy_cols<<<grid, 256, 0, s>>>(tmp, y, len, ldy, nrhs);
+}
+
+void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s) {
+  if (n > 0) k_root_trsv<<<1, 512, 0, s>>>(A, n, y, ldy, nrhs, upper);
+}
+
+void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s) {
+  const int grid = (int)std::min<long long>(4096, (total + 255) / 256);
+  if (total > 0) k_finite<<<grid, 256, 0, s>>>(y, total, bad);
+}
+
+}  // namespace h2g

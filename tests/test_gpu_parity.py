@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same H² input (oracle-built, uploaded through h2g_matrix_upload).
+
+Tolerances (north_star): per-cluster ranks within +-1, solution within
+10*eps of the oracle's, residual within 2x the oracle's; at tight eps the
+factorizations agree to ~1e-10."""
+import numpy as np
+import pytest
+
+import paper_1703_06155_b200 as h2g
+import pyoracle as O
+from helpers import ranks_by_cluster, rel, rod_problem, vie_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def upload(A):
+    return h2g.H2Matrix.upload(A.arrays())
+
+
+def compare_chains(och, gch, rank_tol=0):
+    assert och.stop_level == gch.stop_level
+    ro, rg = ranks_by_cluster(och.all_records()), ranks_by_cluster(gch.all_records())
+    assert ro.keys() == rg.keys()
+    worst = max(abs(ro[k] - rg[k]) for k in ro) if ro else 0
+    assert worst <= rank_tol, worst
+    return worst
+
+
+def test_rod_tight_eps_matches_oracle():
+    A = rod_problem(256, 1e-12, leaf=32)
+    och = A.factorize(1e-14)
+    G = upload(A)
+    gch = h2g.factorize(G, 1e-14)
+    compare_chains(och, gch, 0)
+    for lo, lg in zip(och.levels(), gch.levels()):
+        for k in ("level", "rank_sum_before", "rank_sum_after", "eliminated", "ledger_blocks", "perm_len", "active_after"):
+            assert lo[k] == lg[k], (k, lo, lg)
+    assert och.root_size == gch.root_size
+    b = O.rhs(256, 11)
+    xo, xg = och.solve(b), gch.solve(b)
+    assert rel(xg, xo) < 1e-10
+    assert rel(xg, A.shadow_solve(b)) < 1e-10
+
+
+def test_rod_substitutions_and_aliases():
+    A = rod_problem(128, 1e-8, leaf=16)
+    och = A.factorize(1e-10)
+    gch = h2g.factorize(upload(A), 1e-10)
+    b = O.rhs(128, 3)
+    assert rel(gch.forward(b), och.forward(b)) < 1e-9
+    assert rel(gch.backward(b), och.backward(b)) < 1e-9
+    x = gch.solve(b)
+    assert np.array_equal(gch.apply_inverse(b), x)
+    assert rel(gch.apply_inverse_explicit(b), x) < 1e-12
+    y = b.copy()
+    h2g.solve_in_place(gch, y)
+    assert np.array_equal(y, x)
+    a, c = O.rhs(128, 1), O.rhs(128, 2)
+    al, be = 0.7 - 1.3j, -0.2 + 0.5j
+    lhs = gch.solve(al * a + be * c)
+    r = al * gch.solve(a) + be * gch.solve(c)
+    assert np.linalg.norm(lhs - r) <= 1e-12 * (np.linalg.norm(r) + 1)
+    assert np.linalg.norm(gch.solve(np.zeros(128))) == 0.0
+
+
+def test_multi_rhs_matches_columnwise():
+    A = rod_problem(200, 1e-10)
+    gch = h2g.factorize(upload(A), 1e-12)
+    B = np.stack([O.rhs(200, s) for s in range(8)], axis=1)
+    X = gch.apply_inverse(B)
+    for j in range(8):
+        assert rel(X[:, j], gch.solve(B[:, j])) < 1e-13
+    Xe = gch.apply_inverse_explicit(B)
+    assert rel(Xe, X) < 1e-12
+
+
+def test_helmholtz_rod():
+    A = rod_problem(200, 1e-10, kernel=O.helmholtz(0.3, 2.0))
+    gch = h2g.factorize(upload(A), 1e-12)
+    b = O.rhs(200, 5)
+    assert rel(gch.solve(b), A.shadow_solve(b)) < 1e-9
+
+
+@pytest.mark.parametrize("schedule", ["reference", "colored"])
+def test_vie_config1_parity(schedule):
+    """BASELINE config 1 (16^3 VIE cube, leaf 32, eps 1e-4) against the oracle
+    run in the same elimination order."""
+    A, K = vie_problem(16, 0.5, 32, 1e-4)
+    eps = 1e-4
+    sched = O.SCHEDULE_REFERENCE if schedule == "reference" else O.SCHEDULE_COLORED
+    och = A.factorize(eps, schedule=sched)
+    gch = h2g.factorize(upload(A), eps, schedule=schedule)
+    compare_chains(och, gch, rank_tol=1)
+    perm = A.tree.perm
+    b = O.rhs(A.n, 1234)[perm]
+    xo, xg = och.solve(b), gch.solve(b)
+    assert rel(xg, xo) <= 10 * eps
+    ro, rg = A.relative_residual(xo, b), A.relative_residual(xg, b)
+    assert rg <= 2 * ro + 1e-14
+
+
+def test_deterministic_and_input_untouched():
+    A = rod_problem(128, 1e-8, leaf=16)
+    G = upload(A)
+    before = G.download()
+    h1 = h2g.factorize(G, 1e-7).hash()
+    h2 = h2g.factorize(G, 1e-7).hash()
+    assert h1 == h2
+    after = G.download()
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+
+
+def test_singular_pivot_reports_cluster_and_level():
+    A = rod_problem(100, 1e-10, kernel=O.zero(0.0))
+    with pytest.raises(h2g.SingularPivotError) as ei:
+        h2g.factorize(upload(A), 1e-8)
+    assert ei.value.cluster >= 0 and ei.value.level == A.tree.depth
+
+
+def test_diagonal_kernel_early_stop():
+    A = rod_problem(400, 1e-8, kernel=O.zero(2.0))
+    gch = h2g.factorize(upload(A), 1e-8)
+    assert gch.level(0)["eliminated"] == 400 and gch.root_size == 0 and gch.stop_level == 3
+    b = O.rhs(400, 9)
+    assert np.linalg.norm(gch.solve(b) - b / 2) < 1e-14 * np.linalg.norm(b)
+
+
+def test_no_admissible_and_single_leaf():
+    for n in (50, 20):
+        A = rod_problem(n, 1e-8)
+        gch = h2g.factorize(upload(A), 1e-8)
+        assert gch.num_levels == 0 and gch.root_size == n
+        L, U = gch.root()
+        Z = A.dense_shadow()
+        assert np.linalg.norm(L @ U - Z) < 1e-12 * np.linalg.norm(Z)
+
+
+def test_input_validation():
+    A = rod_problem(128, 1e-8, leaf=16)
+    G = upload(A)
+    with pytest.raises(h2g.InvalidInputError):
+        h2g.factorize(G, 0.0)
+    for bad in (1, A.tree.depth + 1):
+        with pytest.raises(h2g.InvalidInputError):
+            h2g.factorize(G, 1e-8, stop_level_override=bad)
+    ch = h2g.factorize(G, 1e-8)
+    with pytest.raises(h2g.InvalidInputError):
+        ch.solve(O.rhs(127, 1))
+    bad = O.rhs(128, 1)
+    bad[3] = np.nan
+    with pytest.raises(h2g.NonFiniteError):
+        ch.solve(bad)
+
+
+def test_gpu_matvec_matches_oracle():
+    A, K = vie_problem(16, 0.5, 32, 1e-4)
+    G = upload(A)
+    x = O.rhs(A.n, 7)
+    assert rel(G.matvec(x), A.matvec(x)) < 1e-12
