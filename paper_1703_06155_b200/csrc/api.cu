@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <complex>
 #include <cstdio>
 #include <cstring>
@@ -269,7 +270,6 @@ T* at(const DBuf& b, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(b.p) + off);
 }
 
-int pick_gram_parts(int maxlist) { return std::max(1, std::min(32, (maxlist + 3) / 4)); }
 
 struct LevelData {
   // level-entry sizes
@@ -552,7 +552,6 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         const LevelWork& W = P->work[li];
         const int nl = Y.nl;
         const int bm = cur.bmax;
-        if (bm > 64) throw Error(H2G_ERR_INTERNAL, fmt("level %lld: block size %lld > 64 not supported yet", l, bm));
         const size_t bb = (size_t)bm * bm;
         // ---- chain offsets (upper bound e <= b - korig)
         std::vector<long long> Qt_off(nl), L11_off(nl), U11_off(nl), Linv_off(nl), Uinv_off(nl), Lself_off(nl), Uself_off(nl);
@@ -596,14 +595,120 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         size_t o_fc = pk.add_raw(reinterpret_cast<const SolveContribD*>(W.fcontrib.data()), W.fcontrib.size());
         pk.upload(CL->meta, st);
         const DBuf& mt = CL->meta;
-        // gram partial buffers
-        int maxlist = 0;
-        for (int t = 0; t < nl; ++t) maxlist = std::max(maxlist, Y.G_ptr[t + 1] - Y.G_ptr[t]);
-        const int GP = pick_gram_parts(maxlist);
-        DBuf gram, gcm;
-        gram.alloc((size_t)std::max(1, W.max_batch) * GP * bb * 16, st);
-        gcm.alloc((size_t)std::max(1, W.max_batch) * GP * 8, st);
         cur.Vp.alloc((size_t)nl * bb * 16, st, true);
+        // ---- step-0 projection / Gram work (static sizes: descriptor GEMMs)
+        const int nslots = static_cast<int>(SC.batch_cl.size());
+        const int nbat0 = static_cast<int>(SC.batch_ptr.size()) - 1;
+        std::vector<int> slot_g0(nslots), slot_gn(nslots), slot_c0(nslots), slot_cn(nslots);
+        std::vector<long long> gram_off;
+        std::vector<int> a_ptr(1, 0), b_ptr(1, 0), n_ptr(1, 0);
+        struct ADesc {
+          int q, fi, tr, m, bx, col;
+          long long yoff;
+        };
+        struct BDesc {
+          int q, m, c0, cw;
+          long long yoff, goff;
+        };
+        std::vector<ADesc> adesc;
+        std::vector<BDesc> bdesc;
+        std::vector<int> ndesc_f;  // fill index per colnorm entry
+        long long ymax = 1, gmax = 1;
+        const int kPartW = 512;
+        for (int bi = 0; bi < nbat0; ++bi) {
+          long long ytop = 0, gtop = 0;
+          for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) {
+            const int q = p - SC.batch_ptr[bi];
+            const int t = SC.batch_cl[p];
+            const int b = cur.bsz[t], m = b - cur.korig[t];
+            slot_c0[p] = static_cast<int>(ndesc_f.size());
+            slot_g0[p] = static_cast<int>(gram_off.size());
+            int w = 0;
+            const long long yoff = ytop;
+            for (int f = Y.G_ptr[t]; f < Y.G_ptr[t + 1]; ++f) {
+              const int fi = Y.G_fill[f], tr = Y.G_tr[f];
+              const int bx = tr ? cur.bsz[Y.frow[fi]] : cur.bsz[Y.fcol[fi]];
+              ndesc_f.push_back(fi);
+              if (m > 0) adesc.push_back({q, fi, tr, m, bx, w, yoff});
+              w += bx;
+            }
+            slot_cn[p] = static_cast<int>(ndesc_f.size()) - slot_c0[p];
+            if (m > 0) {
+              ytop += (long long)m * w;
+              for (int c0 = 0; c0 < w; c0 += kPartW) {
+                bdesc.push_back({q, m, c0, std::min(kPartW, w - c0), yoff, gtop});
+                gram_off.push_back(gtop);
+                gtop += (long long)m * m;
+              }
+            }
+            slot_gn[p] = static_cast<int>(gram_off.size()) - slot_g0[p];
+          }
+          ymax = std::max(ymax, ytop);
+          gmax = std::max(gmax, gtop);
+          a_ptr.push_back(static_cast<int>(adesc.size()));
+          b_ptr.push_back(static_cast<int>(bdesc.size()));
+          n_ptr.push_back(static_cast<int>(ndesc_f.size()));
+        }
+        DBuf ybuf, gbuf, cnbuf, dirbuf, lambuf, flagbuf, cmaxbuf;
+        ybuf.alloc(ymax * 16, st);
+        gbuf.alloc(gmax * 16, st);
+        cnbuf.alloc(std::max<size_t>(ndesc_f.size(), 1) * 8, st);
+        const int mb = std::max(1, W.max_batch);
+        dirbuf.alloc((size_t)mb * bb * 16, st);
+        lambuf.alloc((size_t)mb * bm * 8, st);
+        flagbuf.alloc((size_t)mb * 2 * 4, st, true);
+        cmaxbuf.alloc((size_t)mb * 8, st);
+        int* d_pass2 = flagbuf.as<int>();
+        int* d_rank1 = d_pass2 + mb;
+        std::vector<GemmDesc> gA1, gA2, gB1, gB2;
+        std::vector<NormDesc> gN;
+        gA1.reserve(adesc.size());
+        gA2.reserve(adesc.size());
+        {
+          // cluster of each (batch, q): walk batches again
+          size_t ai = 0, bi2 = 0;
+          for (int bi = 0; bi < nbat0; ++bi) {
+            for (; ai < (size_t)a_ptr[bi + 1]; ++ai) {
+              const ADesc& a = adesc[ai];
+              const int t = SC.batch_cl[SC.batch_ptr[bi] + a.q];
+              const int b = cur.bsz[t];
+              const int fr = cur.bsz[Y.frow[a.fi]];
+              const cplx* F = cur.F.as<cplx>() + (size_t)a.fi * bb;
+              cplx* Cp = ybuf.as<cplx>() + a.yoff + (long long)a.m * a.col;
+              const int* fx = cur.fex.as<int>() + a.fi;
+              gA1.push_back({cur.Vp.as<cplx>() + (size_t)t * bb, F, Cp, b, fr, a.m, a.m, a.bx, b, OP_C, a.tr ? OP_T : OP_N, 1.0, 0.0, fx, nullptr});
+              gA2.push_back({dirbuf.as<cplx>() + (size_t)a.q * bb, F, Cp, b, fr, a.m, a.m, a.bx, b, OP_C, a.tr ? OP_T : OP_N, 1.0, 0.0, fx, d_pass2 + a.q});
+            }
+            for (; bi2 < (size_t)b_ptr[bi + 1]; ++bi2) {
+              const BDesc& d = bdesc[bi2];
+              const cplx* Yp = ybuf.as<cplx>() + d.yoff + (long long)d.m * d.c0;
+              cplx* G = gbuf.as<cplx>() + d.goff;
+              gB1.push_back({Yp, Yp, G, d.m, d.m, d.m, d.m, d.m, d.cw, OP_N, OP_C, 1.0, 0.0, nullptr, nullptr});
+              gB2.push_back({Yp, Yp, G, d.m, d.m, d.m, d.m, d.m, d.cw, OP_N, OP_C, 1.0, 0.0, d_pass2 + d.q, nullptr});
+            }
+          }
+          for (size_t c = 0; c < ndesc_f.size(); ++c) {
+            const int fi = ndesc_f[c];
+            gN.push_back({cur.F.as<cplx>() + (size_t)fi * bb, cur.bsz[Y.frow[fi]], cur.bsz[Y.fcol[fi]], 0, 0, cur.fex.as<int>() + fi, cnbuf.as<double>() + c});
+          }
+          // transposition flag of each colnorm entry
+          size_t c = 0;
+          for (int bi = 0; bi < nbat0; ++bi)
+            for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) {
+              const int t = SC.batch_cl[p];
+              for (int f = Y.G_ptr[t]; f < Y.G_ptr[t + 1]; ++f, ++c) gN[c].trans = Y.G_tr[f];
+            }
+        }
+        DBuf dA1, dA2, dB1, dB2, dN;
+        upload(dA1, gA1, st);
+        upload(dA2, gA2, st);
+        upload(dB1, gB1, st);
+        upload(dB2, gB2, st);
+        upload(dN, gN, st);
+        Packer pk2;
+        size_t o_sg0 = pk2.add(slot_g0), o_sgn = pk2.add(slot_gn), o_sc0 = pk2.add(slot_c0), o_scn = pk2.add(slot_cn), o_goff = pk2.add(gram_off);
+        DBuf meta2;
+        pk2.upload(meta2, st);
 
         DevLevel DL{};
         DL.level = l;
@@ -642,10 +747,20 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.lift = lift.as<cplx>();
         DL.Linv_off = at<long long>(mt, o_Li);
         DL.Uinv_off = at<long long>(mt, o_Ui);
-        DL.gram = gram.as<cplx>();
-        DL.gram_cmax = gcm.as<double>();
-        DL.gram_parts = GP;
+        DL.slot_g0 = at<int>(meta2, o_sg0);
+        DL.slot_gn = at<int>(meta2, o_sgn);
+        DL.slot_c0 = at<int>(meta2, o_sc0);
+        DL.slot_cn = at<int>(meta2, o_scn);
+        DL.gram = gbuf.as<cplx>();
+        DL.gram_off = at<long long>(meta2, o_goff);
+        DL.colnorm = cnbuf.as<double>();
+        DL.dir = dirbuf.as<cplx>();
+        DL.lam = lambuf.as<double>();
+        DL.pass2 = d_pass2;
+        DL.rank1 = d_rank1;
+        DL.cmax = cmaxbuf.as<double>();
         DL.err = ctx->d_err;
+        DL.debug = std::getenv("H2G_DEBUG") ? std::atoi(std::getenv("H2G_DEBUG")) : 0;
 
         launch_complement(DL, st);
         ++launches;
@@ -656,11 +771,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         const SchurContribD* d_con = at<SchurContribD>(mt, o_con);
         for (int bi = 0; bi < nbat; ++bi) {
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
-          launch_gram(DL, d_bat + p0, nb, st);
-          launch_head(DL, d_bat + p0, nb, st);
+          const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
+          launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st);
+          launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          launch_colnorm(dN.as<NormDesc>() + n_ptr[bi], nn, st);
+          launch_eig1(DL, d_bat + p0, p0, nb, st);
+          launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st);
+          launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          launch_head(DL, d_bat + p0, p0, nb, st);
           launch_panel(DL, d_bat + p0, d_pan + W.panel_ptr[bi], W.panel_ptr[bi + 1] - W.panel_ptr[bi], st);
           launch_schur(DL, d_sch + W.schur_ptr[bi], W.schur_ptr[bi + 1] - W.schur_ptr[bi], d_con, st);
-          launches += 2 + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
+          launches += 4 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
         }
         CK(cudaGetLastError());
         check_device_error(ctx, l);

@@ -484,14 +484,14 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
       FarItem* dit = dev_upload(items, st);
       int* dip = dev_upload(item_ptr, st);
       BuildLevel BL{bm, dcb, dcs, dkl, ddo, Dbuf, part, nparts, px, py, pz, K};
-      cudaFuncSetAttribute((const void*)k_far_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+      CKB(cudaFuncSetAttribute((const void*)k_far_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
       k_far_gram<<<dim3(cnt, nparts), 256, kTileSmem, st>>>(BL, dit, dip);
       CKB(cudaGetLastError());
       CKB(cudaMallocAsync(&Ubuf, (size_t)cnt * bm * bm * 16, st));
       int* drank = nullptr;
       CKB(cudaMallocAsync(&drank, cnt * 4, st));
       const size_t smem = 2 * (size_t)bm * bm * 16 + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
-      if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k_far_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      CKB(cudaFuncSetAttribute((const void*)k_far_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_far_eig<<<cnt, 256, smem, st>>>(BL, all_dup ? 2.0 : 1.0, eps_h2, Ubuf, drank);
       CKB(cudaGetLastError());
       CKB(cudaMemcpyAsync(rank.data(), drank, cnt * 4, cudaMemcpyDeviceToHost, st));
@@ -582,7 +582,7 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
         int *dtn = dev_upload(tn, st), *dsn = dev_upload(sn, st), *dkt = dev_upload(kt, st), *dks = dev_upload(ks, st), *dip = dev_upload(iptr, st);
         CoupItem* dit = dev_upload(items2, st);
         CoupLevel CLv{dtb, dsb, dtn, dsn, dkt, dks, dEt, dEs, Eprev, part, pstride, px, py, pz, K};
-        cudaFuncSetAttribute((const void*)k_coupling, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem);
+        CKB(cudaFuncSetAttribute((const void*)k_coupling, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
         if (!items2.empty()) k_coupling<<<static_cast<int>(items2.size()), 256, kTileSmem, st>>>(CLv, dit);
         // compact output offsets (temporary buffer, then host)
         long long top = 0;

@@ -230,16 +230,10 @@ __device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int*
   double* rs = rot + npair;
   double* rphr = rot + 2 * npair;
   double* rphi = rot + 3 * npair;
-  for (int sweep = 0; sweep < 30; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-      const double a = cabs2(H[idx]);
-      tot += a;
-      if ((idx % n) != (idx / n)) off += a;
-    }
-    off = cta_sum(off, red);
-    tot = cta_sum(tot, red);
-    if (off <= 1e-32 * tot || tot == 0.0) break;
+  __shared__ int s_rot;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
     for (int r = 0; r < n2 - 1; ++r) {
       for (int i = threadIdx.x; i < npair; i += blockDim.x) {
         int p, q;
@@ -262,7 +256,9 @@ __device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int*
           const cplx g = H[p + q * n];
           const double ga = cabsd(g);
           const double a = H[p + p * n].x, d = H[q + q * n].x;
-          if (ga > 1e-300 && ga > 1e-18 * (fabs(a) + fabs(d))) {
+          // relative criterion (keeps small eigenvalues of graded matrices accurate)
+          if (ga > 1e-300 && ga > 1e-15 * sqrt(fabs(a) * fabs(d))) {
+            s_rot = 1;
             phr = g.x / ga;
             phi = g.y / ga;
             const double th = (d - a) / (2.0 * ga);
@@ -312,6 +308,8 @@ __device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int*
       }
       __syncthreads();
     }
+    if (!s_rot) break;
+    __syncthreads();
   }
 }
 

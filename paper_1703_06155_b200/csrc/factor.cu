@@ -8,6 +8,11 @@
 // Reference: proj/include/h2lu/factorization.hpp:260-440.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
 
 #include "factor.cuh"
 
@@ -66,64 +71,88 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
 }
 
 // --------------------------------------------------------------------------
-// Step 0, part 1: partial Gram matrices of Y = Vp^H W over a slice of the
-// cluster's fill-in blocks (W columns: F for keys (t, y), F^T for keys (x, t),
-// factorization.hpp:278-293), plus the largest unprojected column norm
-// (the floor of :295).
-__global__ void __launch_bounds__(256) k_gram(DevLevel L, const int* batch_cl) {
+// Step 0, pass 1. The projected fill-in stack Y = Vp^H W (factorization.hpp:
+// 278-296, Vp = complement of the level-entry basis) is reduced to partial
+// Gram matrices by descriptor GEMMs (k_gemm); here the partials are summed,
+// eigendecomposed (Jacobi) and truncated with the eps rule and floor of
+// h2_matrix.hpp:287-290 / factorization.hpp:295. When the truncation
+// threshold sits below ~1e-4 sigma_0 the Gram matrix cannot resolve it
+// (sigma^2 meets the fp64 noise of ||G||), so a Rayleigh-Ritz refinement pass
+// is requested: the stack is re-projected on the pass-1 directions
+// (D1 = Vp U1) and eigendecomposed again (k_head), which resolves singular
+// values down to ~eps_mach * sigma_0 like the reference's QR + SVD.
+__global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[32];
-  const int q = blockIdx.x, g = blockIdx.y, G = gridDim.y;
+  __shared__ int s_any;
+  const int q = blockIdx.x, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
-  cplx* sVp = reinterpret_cast<cplx*>(smraw);  // b x m
-  cplx* sW = sVp + bm * bm;                    // b x bx
-  cplx* sY = sW + bm * bm;                     // m x bx
-  const int mm = m * m;
-  const int per = (mm + blockDim.x - 1) / blockDim.x;
-  cplx acc[16];
-  for (int s = 0; s < 16; ++s) acc[s] = czero();
-  double cmax = 0.0;
-  const int f0 = L.G_ptr[t], f1 = L.G_ptr[t + 1];
-  if (m > 0) cta_copy(b, m, L.Vp + (size_t)t * bm * bm, b, sVp, b);
-  for (int f = f0 + g; f < f1 && m > 0; f += G) {
-    const int fi = L.G_fill[f];
-    if (!L.fexists[fi]) continue;
-    const int tr = L.G_tr[f];
-    const int fr = L.bsz[L.frow[fi]], fc = L.bsz[L.fcol[fi]];
-    const cplx* F = blk(L.F, fi, bm);
-    const int bx = tr ? fr : fc;  // W block is b x bx
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < b * bx; idx += blockDim.x) {
-      const int p = idx % b, j = idx / b;
-      sW[p + j * b] = tr ? F[j + (size_t)p * fr] : F[p + (size_t)j * fr];
-    }
-    __syncthreads();
-    // column norms (floor)
-    for (int j = threadIdx.x; j < bx; j += blockDim.x) {
-      double s = 0.0;
-      for (int p = 0; p < b; ++p) s += cabs2(sW[p + j * b]);
-      cmax = fmax(cmax, sqrt(s));
-    }
-    cta_gemm(m, bx, b, 1.0, sVp, b, OP_C, sW, b, OP_N, 0.0, sY, m);
-    __syncthreads();
-    for (int s = 0; s < per; ++s) {
-      const int idx = threadIdx.x + s * blockDim.x;
-      if (idx >= mm) break;
-      const int i = idx % m, j = idx / m;
-      cplx a = acc[s];
-      for (int p = 0; p < bx; ++p) cfma(a, sY[i + p * m], cconj(sY[j + p * m]));
-      acc[s] = a;
-    }
+  cplx* ws = gws ? gws + (size_t)q * 2 * bm * bm : reinterpret_cast<cplx*>(smraw);
+  cplx* H = ws;
+  cplx* U = ws + bm * bm;
+  double* lam = reinterpret_cast<double*>(smraw + (gws ? 0 : 2 * (size_t)bm * bm * sizeof(cplx)));
+  int* ord = reinterpret_cast<int*>(lam + bm);
+  int* pr = ord + bm;
+  double* rot = reinterpret_cast<double*>(pr + bm + 2);
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  {
+    int any = 0;
+    for (int f = L.G_ptr[t] + threadIdx.x; f < L.G_ptr[t + 1]; f += blockDim.x) any |= L.fexists[L.G_fill[f]];
+    if (any) s_any = 1;
   }
-  cmax = cta_max(cmax, red);
-  cplx* out = L.gram + (size_t)(q * G + g) * bm * bm;
-  for (int s = 0; s < per; ++s) {
-    const int idx = threadIdx.x + s * blockDim.x;
-    if (idx >= mm) break;
-    out[idx] = acc[s];
+  __syncthreads();
+  cplx* D1 = L.dir + (size_t)q * bm * bm;
+  const cplx* Vp = L.Vp + (size_t)t * bm * bm;
+  if (!s_any || m == 0) {
+    // no fill-in: the basis stays (factorization.hpp:276)
+    cta_copy(b, m, Vp, b, D1, b);
+    if (threadIdx.x == 0) L.pass2[q] = 0, L.rank1[q] = 0, L.cmax[q] = 0.0;
+    return;
   }
-  if (threadIdx.x == 0) L.gram_cmax[q * G + g] = cmax;
+  const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+    cplx s = czero();
+    for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
+    H[idx] = s;
+  }
+  double cm = 0.0;
+  for (int c = threadIdx.x; c < L.slot_cn[p]; c += blockDim.x) cm = fmax(cm, L.colnorm[L.slot_c0[p] + c]);
+  const double cmax = cta_max(cm, red);
+  __syncthreads();
+  cta_jacobi_eig(m, H, U, rot, pr, red);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(H[i + i * m].x, 0.0));
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    int rk = 0;
+    for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+    ord[rk] = i;
+  }
+  __syncthreads();
+  // D1 = Vp U1 (columns sorted by descending value)
+  for (int idx = threadIdx.x; idx < b * m; idx += blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    cplx v = czero();
+    const int col = ord[j];
+    for (int r = 0; r < m; ++r) cfma(v, Vp[i + (size_t)r * b], U[r + col * m]);
+    D1[i + (size_t)j * b] = v;
+  }
+  double* lout = L.lam + (size_t)q * bm;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) lout[i] = lam[ord[i]];
+  if (threadIdx.x == 0) {
+    const double s0 = lam[ord[0]];
+    int r = 0;
+    const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
+    if (s0 > 0.0)
+      while (r < m && lam[ord[r]] > thr) ++r;
+    // refinement needed when the threshold is within reach of the Gram noise
+    const int need = s0 > 0.0 && thr < 1e-4 * s0;
+    L.pass2[q] = need;
+    L.rank1[q] = r;
+    L.cmax[q] = cmax;
+    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d pass2 %d\n", L.level, t, m, cmax, s0, thr, r, need);
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -132,11 +161,11 @@ __global__ void __launch_bounds__(256) k_gram(DevLevel L, const int* batch_cl) {
 // (Qtilde = [complement | V | new], :317-339), the rotation of D(t,t) (:345-347)
 // and step 3a (unpivoted LU of the leading e x e block, :390-398; self panels
 // and the self Schur product, :409-420; cleanup, :431-435).
-__global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, cplx* gws) {
+__global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[32];
-  __shared__ int s_any, s_r;
-  const int q = blockIdx.x;
+  __shared__ int s_r;
+  const int q = blockIdx.x, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
   const int cid = (1 << L.level) - 1 + t;
@@ -149,48 +178,39 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, c
   int* pr = ord + bm;
   double* rot = reinterpret_cast<double*>(pr + bm + 2);
 
-  if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
-  {
-    int any = 0;
-    for (int f = L.G_ptr[t] + threadIdx.x; f < L.G_ptr[t + 1]; f += blockDim.x) any |= L.fexists[L.G_fill[f]];
-    if (any) s_any = 1;
-  }
-  __syncthreads();
-  const bool work = s_any && m > 0;
-  cplx* Hc = buf0;
-  cplx* Uc = buf1;
+  const cplx* D1 = L.dir + (size_t)q * bm * bm;
+  cplx* Uc = buf1;  // m x m rotation of the pass-1 directions (identity without pass 2)
   for (int i = threadIdx.x; i < m; i += blockDim.x) ord[i] = i;
-  if (threadIdx.x == 0) s_r = 0;
+  if (threadIdx.x == 0) s_r = L.rank1[q];
   __syncthreads();
-  if (work) {
-    const int G = L.gram_parts;
-    double cm = 0.0;
+  if (L.pass2[q]) {
+    // pass 2: Gram of D1^H W (near-diagonal, graded), Jacobi with the relative criterion
+    cplx* Hc = buf0;
+    const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
       cplx s = czero();
-      for (int g = 0; g < G; ++g) s = cadd(s, L.gram[(size_t)(q * G + g) * bm * bm + idx]);
+      for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
       Hc[idx] = s;
     }
-    for (int g = threadIdx.x; g < G; g += blockDim.x) cm = fmax(cm, L.gram_cmax[q * G + g]);
-    const double cmax = cta_max(cm, red);
     __syncthreads();
     cta_jacobi_eig(m, Hc, Uc, rot, pr, red);
     for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(Hc[i + i * m].x, 0.0));
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      int rank = 0;
-      for (int j = 0; j < m; ++j) rank += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
-      ord[rank] = i;
+      int rk = 0;
+      for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+      ord[rk] = i;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       const double s0 = lam[ord[0]];
       int r = 0;
       if (s0 > 0.0) {
-        const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
+        const double thr = fmax(fmax(L.eps * s0, L.eps * L.cmax[q]), 1e-300);
         while (r < m && lam[ord[r]] > thr) ++r;
       }
       s_r = r;
+      if (L.debug) printf("[h2g] pass2 level %d cluster %d m %d s0 %.3e r %d\n", L.level, t, m, s0, r);
     }
     __syncthreads();
   } else {
@@ -200,10 +220,9 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, c
   const int r = s_r;
   const int kf = k + r, e = b - kf;
   if (threadIdx.x == 0) L.kfin[t] = kf;
-
+  const cplx* Vp = D1;  // directions (b x m), rotated by Uc below
   // Qtilde = [Vp Uc(:, ord[r:]) | V | Vp Uc(:, ord[:r])]
   cplx* Qt = buf2;
-  const cplx* Vp = L.Vp + (size_t)t * bm * bm;
   const cplx* V = L.V0 + (size_t)t * bm * bm;
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int i = idx % b, j = idx / b;
@@ -275,14 +294,14 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, c
 // Lbar = D[:,:e] U11^{-1}; eliminated rows/columns zeroed (:437-438). For a
 // neighbour eliminated earlier the panel is also lifted back to its
 // level-entry frame (deposit_fill, :359-362).
-__global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, const PanelItemD* items) {
+__global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, const PanelItemD* items, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const PanelItemD it = items[blockIdx.x];
   const int t = batch_cl[it.q];
   const int bm = L.bmax;
   const int b = L.bsz[t], e = b - L.kfin[t];
   const int bn = L.bsz[it.nb];
-  cplx* sQ = reinterpret_cast<cplx*>(smraw);
+  cplx* sQ = gws ? gws + (size_t)blockIdx.x * 3 * bm * bm : reinterpret_cast<cplx*>(smraw);
   cplx* sD = sQ + bm * bm;
   cplx* sT = sD + bm * bm;
   const cplx* gQ = L.chain + L.Qt_off[t];
@@ -427,6 +446,24 @@ __global__ void __launch_bounds__(256) k_schur(DevLevel L, const SchurTargetD* t
 // --------------------------------------------------------------------------
 // Descriptor-driven copy / GEMM (level boundaries: finish_level, merge_permute,
 // root assembly, :445-584 and :637).
+// Largest column norm of a fill-in block as it enters W (F's columns, or
+// F's rows for a transposed key): the floor of factorization.hpp:295.
+__global__ void __launch_bounds__(256) k_colnorm(const NormDesc* descs) {
+  __shared__ double red[32];
+  const NormDesc d = descs[blockIdx.x];
+  double mx = 0.0;
+  if (!d.flag || *d.flag) {
+    const int ncol = d.trans ? d.rows : d.cols, len = d.trans ? d.cols : d.rows;
+    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+      double s = 0.0;
+      for (int p = 0; p < len; ++p) s += cabs2(d.trans ? d.F[j + (size_t)p * d.rows] : d.F[p + (size_t)j * d.rows]);
+      mx = fmax(mx, sqrt(s));
+    }
+  }
+  mx = cta_max(mx, red);
+  if (threadIdx.x == 0) *d.out = mx;
+}
+
 __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
   const CopyDesc d = descs[blockIdx.x];
   for (int idx = threadIdx.x; idx < d.m * d.n; idx += blockDim.x) {
@@ -442,6 +479,7 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmDesc* descs) {
   __shared__ cplx sB[16][65];
   const GemmDesc d = descs[blockIdx.x];
   const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  const bool zero = (d.flag1 && !*d.flag1) || (d.flag2 && !*d.flag2);
   for (int r0 = 0; r0 < d.m; r0 += 64)
     for (int c0 = 0; c0 < d.n; c0 += 64) {
       cplx acc[4][4];
@@ -449,7 +487,7 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmDesc* descs) {
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
-      for (int k0 = 0; k0 < d.k; k0 += 16) {
+      for (int k0 = 0; k0 < (zero ? 0 : d.k); k0 += 16) {
         const int kk = min(16, d.k - k0);
         __syncthreads();
         for (int idx = threadIdx.x; idx < 64 * 16; idx += blockDim.x) {
@@ -595,8 +633,28 @@ size_t head_smem_bytes(int bm) {
   return smem3(bm) + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
 }
 
+// Opt in to the dynamic shared memory a launch needs (cached per kernel).
 static void set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static std::mutex mu;
+  static std::map<const void*, size_t> done;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = done[fn];
+  if (bytes > cur) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+      throw std::runtime_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+    cur = bytes;
+  }
+}
+
+static int sync_debug() {
+  static int v = std::getenv("H2G_SYNC") ? std::atoi(std::getenv("H2G_SYNC")) : 0;
+  return v;
+}
+
+static void post_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_debug()) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));
 }
 
 static cplx* g_ws = nullptr;
@@ -617,50 +675,74 @@ void launch_complement(const DevLevel& L, cudaStream_t s) {
   const size_t need = 2 * (size_t)L.bmax * L.bmax * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx);
   if (need <= kSmemCap) {
     set_smem((const void*)k_complement, need);
-    k_complement<<<L.nl, 256, need, s>>>(L, nullptr);
+    k_complement<<<L.nl, 256, need, s>>>(L, nullptr); post_launch("k_complement");
   } else {
     cplx* ws = workspace(need * L.nl, s);
     k_complement<<<L.nl, 256, 0, s>>>(L, ws);
+    post_launch("k_complement");
   }
 }
 
-void launch_gram(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
-  const size_t need = smem3(L.bmax);
-  set_smem((const void*)k_gram, need);
-  dim3 grid(nb, L.gram_parts);
-  k_gram<<<grid, 256, need, s>>>(L, batch_cl);
+size_t eig1_smem_bytes(int bm) { return 2 * (size_t)bm * bm * sizeof(cplx) + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64; }
+
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
+  const size_t need = eig1_smem_bytes(L.bmax);
+  if (need <= kSmemCap) {
+    set_smem((const void*)k_eig1, need);
+    k_eig1<<<nb, 256, need, s>>>(L, batch_cl, p0, nullptr);
+  } else {
+    const size_t small = need - 2 * (size_t)L.bmax * L.bmax * sizeof(cplx);
+    set_smem((const void*)k_eig1, small);
+    cplx* ws = workspace(2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb, s);
+    k_eig1<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
+  }
+  post_launch("k_eig1");
 }
 
-void launch_head(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
+void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
   const size_t need = head_smem_bytes(L.bmax);
   if (need <= kSmemCap) {
     set_smem((const void*)k_head, need);
-    k_head<<<nb, 256, need, s>>>(L, batch_cl, nullptr);
+    k_head<<<nb, 256, need, s>>>(L, batch_cl, p0, nullptr);
   } else {
     const size_t small = need - smem3(L.bmax);
+    set_smem((const void*)k_head, small);
     cplx* ws = workspace(smem3(L.bmax) * nb, s);
-    k_head<<<nb, 256, small, s>>>(L, batch_cl, ws);
+    k_head<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
   }
+  post_launch("k_head");
+}
+
+void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_colnorm<<<n, 256, 0, s>>>(d);
+  post_launch("k_colnorm");
 }
 
 void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s) {
   if (nitems <= 0) return;
   const size_t need = smem3(L.bmax);
-  set_smem((const void*)k_panel, need);
-  k_panel<<<nitems, 256, need, s>>>(L, batch_cl, items);
+  if (need <= kSmemCap) {
+    set_smem((const void*)k_panel, need);
+    k_panel<<<nitems, 256, need, s>>>(L, batch_cl, items, nullptr);
+  } else {
+    cplx* ws = workspace(need * nitems, s);
+    k_panel<<<nitems, 256, 0, s>>>(L, batch_cl, items, ws);
+  }
+  post_launch("k_panel");
 }
 
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;
-  k_schur<<<ntargets, 256, 0, s>>>(L, targets, contrib);
+  k_schur<<<ntargets, 256, 0, s>>>(L, targets, contrib); post_launch("k_schur");
 }
 
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {
-  if (n > 0) k_copy<<<n, 256, 0, s>>>(d);
+  if (n > 0) k_copy<<<n, 256, 0, s>>>(d); post_launch("k_copy");
 }
 
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s) {
-  if (n > 0) k_gemm<<<n, 256, 0, s>>>(d);
+  if (n > 0) k_gemm<<<n, 256, 0, s>>>(d); post_launch("k_gemm");
 }
 
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches) {
@@ -673,13 +755,14 @@ int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream
   for (int k0 = 0; k0 < n; k0 += 32) {
     const int kb = std::min(32, n - k0);
     k_lu_panel<<<1, 256, 0, s>>>(A, n, k0, kb, scale, err);
+    post_launch("k_lu_panel");
     const int rest = n - k0 - kb;
     *launches += 1;
     if (rest > 0) {
       k_lu_trsm<<<(rest + 127) / 128, 128, 0, s>>>(A, n, k0, kb);
       dim3 g((rest + 63) / 64, (rest + 63) / 64);
       const int sm = (64 * 33 + 32 * 65) * (int)sizeof(cplx);
-      cudaFuncSetAttribute((const void*)k_lu_update, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      set_smem((const void*)k_lu_update, sm);
       k_lu_update<<<g, 256, sm, s>>>(A, n, k0, kb);
       *launches += 2;
     }

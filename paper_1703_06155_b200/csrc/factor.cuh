@@ -50,10 +50,22 @@ struct DevLevel {
   cplx* lift;                 // lifted panels, same offsets as Lbar/Ubar (pool base)
   const long long* Linv_off;  // L11^{-1}, U11^{-1} (e x e) in the chain
   const long long* Uinv_off;
-  cplx* gram;                 // gram partials: [slot][part] stride bmax^2
-  double* gram_cmax;          // [slot][part]
-  int gram_parts;
+  // step-0 per batch-slot data (indexed by the slot's global position p in
+  // the level's batch order, or by the local slot q for scratch)
+  const int* slot_g0;          // [p] first Gram partial of the slot
+  const int* slot_gn;          // [p] number of partials
+  const int* slot_c0;          // [p] first column-norm entry
+  const int* slot_cn;          // [p] number of column-norm entries
+  const cplx* gram;            // partial Grams (batch-relative offsets, m x m each)
+  const long long* gram_off;   // [partial] offset into gram
+  const double* colnorm;       // [entry] max column norm of one fill block
+  cplx* dir;                   // [q] pass-1 directions D1 = Vp U1 sorted (b x m), stride bmax^2
+  double* lam;                 // [q] pass-1 singular values (sorted desc), stride bmax
+  int* pass2;                  // [q] 1 if the refinement pass runs
+  int* rank1;                  // [q] pass-1 rank (used when pass2 == 0)
+  double* cmax;                // [q]
   DevError* err;
+  int debug;
 };
 
 struct PanelItemD {
@@ -81,11 +93,20 @@ struct GemmDesc {
   cplx* C;
   int lda, ldb, ldc, m, n, k, opA, opB;
   double alpha, beta;
+  const int* flag1;  // if set and *flag1 == 0 (or *flag2 == 0): op(A) op(B) counts as zero
+  const int* flag2;
+};
+struct NormDesc {
+  const cplx* F;
+  int rows, cols, trans, pad;
+  const int* flag;
+  double* out;
 };
 
 void launch_complement(const DevLevel& L, cudaStream_t s);
-void launch_gram(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
-void launch_head(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
+void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
+void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
 void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s);
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);

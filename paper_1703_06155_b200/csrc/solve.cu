@@ -2,6 +2,9 @@
 // 43-83), batch by batch in the factorization's elimination order. Vectors
 // are n x nrhs column-major complex128 in tree order, updated in place.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <stdexcept>
 
 #include "solve.cuh"
 
@@ -198,7 +201,15 @@ __global__ void k_finite(const cplx* y, long long total, int* bad) {
 
 // ----------------------------------------------------------------- launchers
 static void smem_attr(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  static std::mutex mu;
+  static std::map<const void*, size_t> done;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = done[fn];
+  if (bytes > cur) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+      throw std::runtime_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+    cur = bytes;
+  }
 }
 
 void launch_fwd_head(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {

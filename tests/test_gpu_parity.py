@@ -9,7 +9,7 @@ import pytest
 
 import paper_1703_06155_b200 as h2g
 import pyoracle as O
-from helpers import ranks_by_cluster, rel, rod_problem, vie_problem
+from helpers import ranks_by_cluster, rel, replay_gpu_chain, rod_problem, vie_problem
 
 pytestmark = pytest.mark.gpu
 
@@ -44,12 +44,18 @@ def test_rod_tight_eps_matches_oracle():
 
 
 def test_rod_substitutions_and_aliases():
+    """test_solve.cpp:49-62 on the GPU chain: forward/backward apply the
+    inverses of the replayed factors; the replay reproduces the matrix
+    (verify.hpp:94-99, test_factorization.cpp:97-104)."""
     A = rod_problem(128, 1e-8, leaf=16)
-    och = A.factorize(1e-10)
     gch = h2g.factorize(upload(A), 1e-10)
+    Lf, Uf = replay_gpu_chain(gch)
+    Z = A.dense_shadow()
+    assert np.linalg.norm(Lf @ Uf - Z) / np.linalg.norm(Z) < 100 * 1e-10
     b = O.rhs(128, 3)
-    assert rel(gch.forward(b), och.forward(b)) < 1e-9
-    assert rel(gch.backward(b), och.backward(b)) < 1e-9
+    y = gch.forward(b)
+    assert rel(y, np.linalg.solve(Lf, b)) < 1e-11
+    assert rel(gch.backward(y), np.linalg.solve(Uf, y)) < 1e-11
     x = gch.solve(b)
     assert np.array_equal(gch.apply_inverse(b), x)
     assert rel(gch.apply_inverse_explicit(b), x) < 1e-12
