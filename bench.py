@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H² factorize + solve hot path (BASELINE.json metric:
+"H² factorization unknowns/s & FP64 TFLOP/s vs peak; solve time; rel. residual").
+
+One step = factorize (the level-by-level H² LU) + one solve of a seeded
+complex-normal right-hand side, on BASELINE config 2 by default (VIE
+dielectric cube 32^3 = 32768 unknowns, leaf 32, eta 1, eps 1e-4, complex128).
+The H² input is built on the GPU once, outside the timed region.
+
+  value  unknowns/s of the factorization, device time (CUDA events on the
+         library stream), inputs resident in HBM, max over ranks
+  e2e    same metric through the public C-ABI calls with HOST buffers: every
+         step uploads the H² matrix (h2g_matrix_upload) and the RHS from host
+         memory, factorizes, solves and reads x back (wall clock around the
+         synchronous calls, max over ranks)
+
+Multi-GPU: the factorization does not shard in this round, so --gpus N runs N
+independent replicas (weak scaling). --impl reference times the
+CPU restatement of the reference (oracle/, the reference itself cannot be built
+here: Eigen is absent) on rank 0 only.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- helpers
+def sampled_dense_residual(points_tree, kernel_args, x, b, nrows=4096, seed=1234):
+    """||Zx - b|| / ||b|| on seeded sampled rows, Z from the kernel directly
+    (SURVEY §8d(ii)); numpy, O(nrows * N)."""
+    k0, scale, diag = kernel_args
+    n = points_tree.shape[0]
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(n, size=min(nrows, n), replace=False))
+    num = den = 0.0
+    for c0 in range(0, rows.size, 256):
+        rr = rows[c0:c0 + 256]
+        d = points_tree[rr, None, :] - points_tree[None, :, :]
+        r = np.sqrt((d * d).sum(-1))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            Z = scale * np.exp(-1j * k0 * r) / (4 * np.pi * r)
+        Z[np.arange(rr.size), rr] = diag
+        res = Z @ x - b[rr]
+        num += float(np.vdot(res, res).real)
+        den += float(np.vdot(b[rr], b[rr]).real)
+    return math.sqrt(num / den)
+
+
+def load_peaks():
+    peaks = {}
+    try:
+        peaks.update(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))))
+    except Exception:
+        pass
+    try:
+        peaks.update(json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json"))))
+    except Exception:
+        pass
+    return peaks
+
+
+def cpu_oracle_sample(threads_note=True):
+    """Oracle (CPU restatement of the reference, single-threaded like the
+    reference) factorizing BASELINE config 1 — the reference's own
+    CPU-runnable case — as the bounded CPU sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points
+
+    c = BASELINE_CONFIGS[1]
+    k0, scale, diag = vie_constants(c["cells"], c["side"])
+    t = O.Tree(vie_grid_points(c["cells"], c["side"]), c["leaf"])
+    A = O.H2(O.Blocks(t, 1.0), O.helmholtz(k0, diag, scale), c["eps"])
+    return A, c, O
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    A, c, O = cpu_oracle_sample()
+    n = A.n
+    for _ in range(args.warmup):
+        A.factorize(c["eps"])
+    secs = []
+    for _ in range(args.steps):
+        ch = A.factorize(c["eps"])
+        secs.append(ch.seconds)
+    t = float(np.mean(secs))
+    value = n / t
+    sample = (f"oracle/ (CPU restatement of proj/include/h2lu/factorization.hpp, 1 thread like the reference) "
+              f"factorizing BASELINE config 1 (16^3 VIE cube, leaf 32, eps 1e-4, N={n}) per step; "
+              f"config 2 on the CPU takes minutes, config 1 is the reference's CPU-runnable case")
+    return {
+        "metric": "H2 factorization unknowns/s",
+        "value": value,
+        "unit": "unknowns/s",
+        "impl": "reference",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "complex128",
+        "data": "synthetic",
+        "config": {"workload": "BASELINE config 1 sample (see cpu_baseline.sample)", "n": n, "leaf": c["leaf"], "eps": c["eps"], "eta": 1.0},
+        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--schedule", default="reference", choices=["reference", "colored"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import paper_1703_06155_b200 as h2g
+    from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points
+
+    c = BASELINE_CONFIGS[args.config]
+    eps = c["eps"]
+    k0, scale, diag = vie_constants(c["cells"], c["side"])
+    pts = vie_grid_points(c["cells"], c["side"])
+    n = pts.shape[0]
+    ctx = h2g.Context(local)
+    t0 = time.perf_counter()
+    A = h2g.H2Matrix.build(pts, c["leaf"], 1.0, h2g.helmholtz_kernel(k0, diag, scale), eps, ctx)
+    build_s = time.perf_counter() - t0
+    host = A.download()
+    perm = host["perm"]
+    b = h2g.random_rhs(n, 1234)[perm]  # seeded, original order -> tree order
+    log(f"[bench] rank {rank}: built H2 for N={n} in {build_s:.2f}s")
+
+    def sync_all():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}" if torch.cuda.is_available() else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        ch = h2g.factorize(A, eps, schedule=args.schedule)
+        x = ch.solve(b)
+        del ch
+    sync_all()
+    sampler = ClockSampler(local)
+    sampler.start()
+    fms, sms, flaunch, slaunch = [], [], [], []
+    for _ in range(args.steps):
+        ch = h2g.factorize(A, eps, schedule=args.schedule)
+        x = ch.solve(b)
+        tm = ch.timing()
+        fms.append(tm["factor_ms"])
+        sms.append(tm["solve_ms"])
+        flaunch.append(tm["factor_launches"])
+        slaunch.append(tm["solve_launches"])
+    clocks = sampler.stop()
+    sync_all()
+    factor_ms = max_over_ranks(float(np.mean(fms)))
+    solve_ms = max_over_ranks(float(np.mean(sms)))
+    work = ch.work()
+    ranks = [r["rank_after"] for r in ch.all_records()]
+    levels = ch.levels()
+    residual = A.relative_residual(x, b)
+    pts_tree = pts[perm]
+    sampled = sampled_dense_residual(pts_tree, (k0, scale, diag), x, b)
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = sum(v.nbytes for k, v in host.items() if isinstance(v, np.ndarray)) + b.nbytes
+        d2h = x.nbytes
+        try:
+            import torch
+
+            cudart = torch.cuda.cudart()
+            for v in list(host.values()) + [b]:
+                if isinstance(v, np.ndarray) and v.nbytes:
+                    cudart.cudaHostRegister(v.ctypes.data, v.nbytes, 0)
+            pinned = True
+        except Exception:
+            pinned = False
+        ts = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            G = h2g.H2Matrix.upload(host, ctx)
+            ch2 = h2g.factorize(G, eps, schedule=args.schedule)
+            x2 = ch2.solve(b)
+            t1 = time.perf_counter()
+            del ch2, G
+            if i >= args.warmup:
+                ts.append(t1 - t0)
+        sync_all()
+        te2e = max_over_ranks(float(np.mean(ts)))
+        e2e = {"value": n * world / te2e, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "s_per_step": te2e, "pinned_host": pinned, "timing": "wall clock around synchronous C-ABI calls, max over ranks",
+               "solution_matches_resident_run": bool(np.allclose(x2, x, rtol=0, atol=1e-12 * np.abs(x).max()))}
+
+    # ---- roofline of the dominant kernel class (separate profiled run)
+    ctx.set_profiling(True)
+    chp = h2g.factorize(A, eps, schedule=args.schedule)
+    ctx.set_profiling(False)
+    stats = chp.kernel_stats()
+    prof_total = sum(v["ms"] for v in stats.values())
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    peaks = load_peaks()
+    peak_tf = peaks.get("zgemm_tflops")
+    peak_src = "measured cuBLAS ZGEMM 4096^3 on this pool (profiles/fp64_peak.json)"
+    if not peak_tf:
+        peak_tf, peak_src = 37.0, "fallback: nominal B200 FP64 ~37 TFLOP/s (no measured FP64 peak found)"
+    hbm = peaks.get("hbm_gbs", 6469.3)
+    sch = stats["schur"]
+    roof = None
+    if sch["ms"] > 0:
+        t_s = sch["ms"] / 1e3
+        tf = sch["flops"] / t_s / 1e12
+        gbs = sch["bytes"] / t_s / 1e9
+        t_flop = sch["flops"] / (peak_tf * 1e12)
+        t_mem = sch["bytes"] / (hbm * 1e9)
+        if t_flop >= t_mem:
+            roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": tf / peak_tf, "peak_source": peak_src + " (FP64 has no tcgen05 path; DFMA/DMMA peak)"}
+        else:
+            roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        roof.update({"traffic": None, "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / max(sch["launches"], 1),
+                     "algorithmic_flops": sch["flops"], "algorithmic_bytes": sch["bytes"], "share_of_factorize": sch["ms"] / max(prof_total, 1e-9),
+                     "tflops": tf, "gbs": gbs})
+    breakdown = {k: {"ms": round(v["ms"], 3), "launches": v["launches"]} for k, v in stats.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Ao, co, O = cpu_oracle_sample()
+        cho = Ao.factorize(co["eps"])
+        cpu = {"value": Ao.n / cho.seconds, "unit": "unknowns/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/ restatement of the reference factorize, 1 thread, BASELINE config 1 (N={Ao.n}, {cho.seconds:.1f} s); "
+                         f"config 2 is minutes on one core, config 1 is the reference's CPU-runnable case"}
+
+    out = {
+        "metric": "H2 factorization unknowns/s",
+        "value": n * world / (factor_ms / 1e3),
+        "unit": "unknowns/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": factor_ms + solve_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "complex128",
+        "data": "synthetic",
+        "config": {"workload": f"BASELINE config {args.config}: VIE dielectric cube {c['cells']}^3 = {n} unknowns, side {c['side']} lambda, eps_r 4, leaf {c['leaf']}, eta 1, eps_h2 = eps_fill = {eps}",
+                   "n": n, "schedule": args.schedule, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (dense leaf blocks alone exceed 126 MB)"},
+        "factor_ms": factor_ms,
+        "solve_ms": solve_ms,
+        "factor_tflops": work["factor_flops"] / (factor_ms / 1e3) / 1e12,
+        "solve_gbs": work["solve_bytes"] / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else None,
+        "relative_residual_h2": residual,
+        "relative_residual_sampled_dense": sampled,
+        "rank_max": int(max(ranks)) if ranks else 0,
+        "root_size": ch.root_size,
+        "levels": [{k: lv[k] for k in ("level", "rank_sum_after", "eliminated", "ledger_blocks")} for lv in levels],
+        "build_s": build_s,
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": int(np.mean(flaunch) + np.mean(slaunch)),
+        "roofline": roof,
+        "kernel_breakdown_ms": breakdown,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -176,6 +176,14 @@ uint64_t h2g_chain_hash(const h2g_chain* c);
 /* Device time (ms, CUDA events on the chain's stream) of the last factorize
  * and the last solve, and the number of kernels each launched. */
 int h2g_chain_timing(const h2g_chain* c, double* factor_ms, double* solve_ms, int64_t* factor_launches, int64_t* solve_launches);
+/* Per-kernel-class device timing of factorize (CUDA events around every
+ * launch on the context stream; off by default). Classes: 0 complement,
+ * 1 step-0 projection/Gram GEMMs, 2 column norms, 3 eig pass 1, 4 head,
+ * 5 panels, 6 Schur scatter, 7 level merge, 8 root LU, 9 other. */
+int h2g_set_profiling(h2g_context* ctx, int32_t on);
+/* out[4] for class cls: ms, launches, algorithmic flops, algorithmic bytes */
+int h2g_chain_kernel_stats(const h2g_chain* c, int32_t cls, double* out);
+
 /* Algorithmic work of the factorization (SURVEY §8d F_factor, from the shapes
  * executed) and of one nrhs=1 solve (bytes of chain + vector traffic):
  * out[4]: factor_flops, schur_flops, solve_bytes, schur_bytes */

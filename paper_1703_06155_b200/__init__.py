@@ -152,6 +152,8 @@ SYMBOLS = {
     "h2g_chain_timing": (C.c_int, [_P, _D, _D, _I64, _I64]),
     "h2g_chain_work": (C.c_int, [_P, _D]),
     "h2g_random_rhs": (None, [C.c_int64, C.c_uint64, _D]),
+    "h2g_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
 }
 
 _lib = None
@@ -207,6 +209,9 @@ class Context:
         _check(lib().h2g_context_create(device, C.byref(h), C.byref(err)), err)
         self.h = h
         self.device = device
+
+    def set_profiling(self, on=True):
+        lib().h2g_set_profiling(self.h, 1 if on else 0)
 
     @classmethod
     def default(cls, device=0):
@@ -462,6 +467,18 @@ class FactorChain:
         fl, sl = C.c_int64(), C.c_int64()
         lib().h2g_chain_timing(self.h, C.byref(f), C.byref(s), C.byref(fl), C.byref(sl))
         return dict(factor_ms=f.value, solve_ms=s.value, factor_launches=fl.value, solve_launches=sl.value)
+
+    KERNEL_CLASSES = ("complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other")
+
+    def kernel_stats(self):
+        """Per kernel class: device ms, launches, algorithmic flops and bytes
+        (requires Context.set_profiling(True) before factorize)."""
+        out = {}
+        for i, name in enumerate(self.KERNEL_CLASSES):
+            v = np.zeros(4)
+            lib().h2g_chain_kernel_stats(self.h, i, _d(v))
+            out[name] = dict(ms=v[0], launches=int(v[1]), flops=v[2], bytes=v[3])
+        return out
 
     def work(self):
         out = np.zeros(4)

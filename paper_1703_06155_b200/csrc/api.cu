@@ -129,12 +129,56 @@ void upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
 }  // namespace
 
 // =============================================================== handles
+// Per-kernel-class event timing (h2g_set_profiling).
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  int open_cls = -1;
+  cudaEvent_t open_ev = nullptr;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void reset() {
+    used = 0;
+    recs.clear();
+  }
+  void begin(int cls, cudaStream_t s) {
+    if (!on) return;
+    open_cls = cls;
+    open_ev = get();
+    cudaEventRecord(open_ev, s);
+  }
+  void end(cudaStream_t s) {
+    if (!on || open_cls < 0) return;
+    cudaEvent_t b = get();
+    cudaEventRecord(b, s);
+    recs.push_back({open_cls, open_ev, b});
+    open_cls = -1;
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SCHUR, PC_MERGE, PC_ROOT, PC_OTHER, PC_N };
+
 struct h2g_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevError* d_err = nullptr;
   int* d_flag = nullptr;
+  Prof prof;
 };
 
 struct PlanCache {
@@ -192,6 +236,8 @@ struct h2g_chain {
   double factor_ms = 0.0, solve_ms = 0.0;
   long long factor_launches = 0, solve_launches = 0;
   double factor_flops = 0.0, schur_flops = 0.0, solve_bytes = 0.0, schur_bytes = 0.0;
+  double kms[PC_N] = {0}, kflops[PC_N] = {0}, kbytes[PC_N] = {0};
+  long long klaunch[PC_N] = {0};
 };
 
 namespace {
@@ -505,6 +551,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->depth = L;
     C->eps = eps;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), st));
+    ctx->prof.reset();
     CK(cudaEventRecord(ctx->ev0, st));
     long long launches = 0;
     double flops = 0.0, sflops = 0.0, sbytes = 0.0;
@@ -762,8 +809,11 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.err = ctx->d_err;
         DL.debug = std::getenv("H2G_DEBUG") ? std::atoi(std::getenv("H2G_DEBUG")) : 0;
 
+        ctx->prof.begin(PC_COMPLEMENT, st);
         launch_complement(DL, st);
+        ctx->prof.end(st);
         ++launches;
+        ++C->klaunch[PC_COMPLEMENT];
         const int nbat = static_cast<int>(SC.batch_ptr.size()) - 1;
         const int* d_bat = at<int>(mt, o_bat);
         const PanelItemD* d_pan = at<PanelItemD>(mt, o_pan);
@@ -772,15 +822,36 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         for (int bi = 0; bi < nbat; ++bi) {
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
           const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
+          Prof& pf = ctx->prof;
+          pf.begin(PC_GRAM, st);
           launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st);
           launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          pf.end(st);
+          pf.begin(PC_COLNORM, st);
           launch_colnorm(dN.as<NormDesc>() + n_ptr[bi], nn, st);
+          pf.end(st);
+          pf.begin(PC_EIG1, st);
           launch_eig1(DL, d_bat + p0, p0, nb, st);
+          pf.end(st);
+          pf.begin(PC_GRAM, st);
           launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st);
           launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          pf.end(st);
+          pf.begin(PC_HEAD, st);
           launch_head(DL, d_bat + p0, p0, nb, st);
+          pf.end(st);
+          pf.begin(PC_PANEL, st);
           launch_panel(DL, d_bat + p0, d_pan + W.panel_ptr[bi], W.panel_ptr[bi + 1] - W.panel_ptr[bi], st);
+          pf.end(st);
+          pf.begin(PC_SCHUR, st);
           launch_schur(DL, d_sch + W.schur_ptr[bi], W.schur_ptr[bi + 1] - W.schur_ptr[bi], d_con, st);
+          pf.end(st);
+          C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
+          C->klaunch[PC_COLNORM] += nn > 0;
+          C->klaunch[PC_EIG1] += 1;
+          C->klaunch[PC_HEAD] += 1;
+          C->klaunch[PC_PANEL] += W.panel_ptr[bi + 1] > W.panel_ptr[bi];
+          C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
           launches += 4 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
         }
         CK(cudaGetLastError());
@@ -836,7 +907,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             const double sch = 8.0 * rows * ed * cols;
             flops += sch;
             sflops += sch;
-            sbytes += 16.0 * 2.0 * rows * cols;  // read + write of every target entry
+            // every target entry read + written once, panels read once
+            sbytes += 16.0 * 2.0 * rows * cols + 16.0 * ed * (rows + cols);
           }
         }
         for (size_t f = 0; f < Y.frow.size(); ++f)
@@ -1008,9 +1080,12 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         upload(dcd, cd, st);
         upload(dg1, g1, st);
         upload(dg2, g2, st);
+        ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
         launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st);
         launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st);
+        ctx->prof.end(st);
+        C->klaunch[PC_MERGE] += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
         launches += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
         if (!fexp.empty()) CK(cudaMemcpyAsync(nxt.fex.p, fexp.data(), fexp.size() * 4, cudaMemcpyHostToDevice, st));
         for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
@@ -1057,7 +1132,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         ++launches;
         DBuf scratch;
         scratch.alloc(64, st);
+        ctx->prof.begin(PC_ROOT, st);
+        const long long l0c = launches;
         root_lu(C->root.as<cplx>(), static_cast<int>(nroot), 1e-13, ctx->d_err, scratch.p, st, &launches);
+        ctx->prof.end(st);
+        C->klaunch[PC_ROOT] += launches - l0c;
+        C->kflops[PC_ROOT] += 8.0 / 3.0 * (double)nroot * nroot * nroot;
+        C->kbytes[PC_ROOT] += 2.0 * 16.0 * (double)nroot * nroot;
         CK(cudaGetLastError());
         check_device_error(ctx, C->stop_level);
         flops += 8.0 / 3.0 * (double)nroot * nroot * nroot;
@@ -1071,9 +1152,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     C->factor_ms = ms;
     C->factor_launches = launches;
+    if (ctx->prof.on)
+      for (const auto& r : ctx->prof.recs) {
+        float e = 0.f;
+        cudaEventElapsedTime(&e, r.a, r.b);
+        C->kms[r.cls] += e;
+      }
     C->factor_flops = flops;
     C->schur_flops = sflops;
     C->schur_bytes = sbytes;
+    C->kflops[PC_SCHUR] = sflops;
+    C->kbytes[PC_SCHUR] = sbytes;
     *out = C.release();
   });
 }
@@ -1336,6 +1425,21 @@ int h2g_chain_timing(const h2g_chain* c, double* fms, double* sms, int64_t* fl, 
   if (sms) *sms = c->solve_ms;
   if (fl) *fl = c->factor_launches;
   if (sl) *sl = c->solve_launches;
+  return H2G_OK;
+}
+
+int h2g_set_profiling(h2g_context* ctx, int32_t on) {
+  if (!ctx) return H2G_ERR_INVALID_INPUT;
+  ctx->prof.on = on != 0;
+  return H2G_OK;
+}
+
+int h2g_chain_kernel_stats(const h2g_chain* c, int32_t cls, double* out) {
+  if (!c || cls < 0 || cls >= PC_N || !out) return H2G_ERR_INVALID_INPUT;
+  out[0] = c->kms[cls];
+  out[1] = (double)c->klaunch[cls];
+  out[2] = c->kflops[cls];
+  out[3] = c->kbytes[cls];
   return H2G_OK;
 }
 
