@@ -541,7 +541,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         throw Error(H2G_ERR_INVALID_INPUT, fmt("factorize: stop level %lld outside [l0, depth] = [%lld, depth]", stop, l0));
     }
     cudaStream_t st = ctx->stream;
+    const auto tp0 = std::chrono::steady_clock::now();
     PlanCache* P = get_plan(M, stop, schedule);
+    if (std::getenv("H2G_VERBOSE"))
+      std::fprintf(stderr, "[h2g] plan %.3f s\n", std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
 
     auto C = std::make_unique<h2g_chain>();
     C->ctx = ctx;
@@ -592,6 +595,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
 
     int li = 0;
     int last_level = L;  // level whose state is "cur" at the root
+    const int verbose = std::getenv("H2G_VERBOSE") ? std::atoi(std::getenv("H2G_VERBOSE")) : 0;
+    auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tlev = wall();
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
         const LevelSym& Y = P->levels[li];
@@ -854,8 +860,12 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
           launches += 4 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
         }
+        const double t_launched = wall();
         CK(cudaGetLastError());
         check_device_error(ctx, l);
+        if (verbose)
+          std::fprintf(stderr, "[h2g] level %d: nl %d bmax %d batches %d: host setup+launch %.3f s, device drain %.3f s\n", l, nl, bm, nbat,
+                       t_launched - tlev, wall() - t_launched);
         // ---- read back final ranks and fill existence
         std::vector<int> kfin(nl), fex(Y.frow.size());
         CK(cudaMemcpyAsync(kfin.data(), DL.kfin, nl * 4, cudaMemcpyDeviceToHost, st));
@@ -1092,6 +1102,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));  // temporaries die here
 
+        if (verbose) std::fprintf(stderr, "[h2g] level %d: merge done at %.3f s\n", l, wall() - tlev);
+        tlev = wall();
         C->levels.push_back(std::move(CL));
         cur = std::move(nxt);
         last_level = lp;

@@ -134,10 +134,35 @@ __device__ inline double cta_max(double v, double* red) {
   return s;
 }
 
+// A (rows x m, ld lda) <- A * Q where Q = H_0^H H_1^H ... H_{s-1}^H is stored
+// compactly in QR (m x s, ld ldq; essential parts below the diagonal) and tau.
+__device__ inline void cta_apply_q_right(int rows, int m, int s, cplx* A, int lda, const cplx* QR, int ldq, const cplx* tau, cplx* tmp) {
+  for (int k = 0; k < s; ++k) {
+    const cplx tk = cconj(tau[k]);
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    const cplx* v = QR + k + (size_t)k * ldq;  // v[0] = 1 implicit
+    // t_i = sum_j A[i, k + j] v_j
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+      cplx t = A[i + (size_t)k * lda];
+      for (int j = 1; j < m - k; ++j) cfma(t, A[i + (size_t)(k + j) * lda], v[j]);
+      tmp[i] = cmul(t, tk);
+    }
+    __syncthreads();
+    // A[:, k + j] -= t conj(v_j)
+    for (int idx = threadIdx.x; idx < rows * (m - k); idx += blockDim.x) {
+      const int i = idx % rows, j = idx / rows;
+      const cplx vj = j == 0 ? cone() : v[j];
+      cplx* a = A + i + (size_t)(k + j) * lda;
+      *a = csub(*a, cmul(tmp[i], cconj(vj)));
+    }
+    __syncthreads();
+  }
+}
+
 // Compact Householder QR of A (m x n, ld lda) in place with the Eigen
 // HouseholderQR convention (H = I - tau v v^H, v0 = 1, beta = -sign(Re c0)|x|),
 // then Q (m x m, ld ldq) = H_0^H ... H_{s-1}^H. tau: s entries of scratch.
-__device__ inline void cta_householder_q(int m, int n, cplx* A, int lda, cplx* Q, int ldq, cplx* tau, double* red) {
+__device__ inline void cta_householder_qr(int m, int n, cplx* A, int lda, cplx* tau, double* red) {
   const int s = min(m, n);
   for (int k = 0; k < s; ++k) {
     cplx* x = A + k + (size_t)k * lda;
@@ -191,6 +216,11 @@ __device__ inline void cta_householder_q(int m, int n, cplx* A, int lda, cplx* Q
     if (threadIdx.x == 0) x[0] = cmk(s_beta, 0.0);
     __syncthreads();
   }
+}
+
+__device__ inline void cta_householder_q(int m, int n, cplx* A, int lda, cplx* Q, int ldq, cplx* tau, double* red) {
+  const int s = min(m, n);
+  cta_householder_qr(m, n, A, lda, tau, red);
   // Q = H_0^H H_1^H ... H_{s-1}^H applied to I
   cta_identity(m, m, Q, ldq);
   __syncthreads();
@@ -220,7 +250,11 @@ __device__ inline void cta_householder_q(int m, int n, cplx* A, int lda, cplx* Q
 // Two-sided cyclic Jacobi on a Hermitian n x n matrix H (ld n), round-robin
 // parallel ordering. On exit H is (numerically) diagonal and U (ld n) holds
 // the eigenvectors: H_in = U diag(H_out) U^H. rot: scratch of 4*((n+1)/2) doubles.
-__device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int* pr, double* red) {
+// A pair rotates while |h_pq| > 1e-15 sqrt(|h_pp h_qq|) (relative accuracy
+// for graded matrices) and |h_pq| > absfloor (entries below the caller's
+// resolution floor are left alone, so noise-level blocks do not keep the
+// sweeps going).
+__device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int* pr, double* red, double absfloor = 0.0) {
   cta_identity(n, n, U, n);
   __syncthreads();
   if (n <= 1) return;
@@ -257,7 +291,7 @@ __device__ inline void cta_jacobi_eig(int n, cplx* H, cplx* U, double* rot, int*
           const double ga = cabsd(g);
           const double a = H[p + p * n].x, d = H[q + q * n].x;
           // relative criterion (keeps small eigenvalues of graded matrices accurate)
-          if (ga > 1e-300 && ga > 1e-15 * sqrt(fabs(a) * fabs(d))) {
+          if (ga > 1e-300 && ga > absfloor && ga > 1e-15 * sqrt(fabs(a) * fabs(d))) {
             s_rot = 1;
             phr = g.x / ga;
             phi = g.y / ga;
@@ -376,6 +410,163 @@ __device__ inline void cta_tri_inverses(int n, const cplx* LU, int ld, cplx* Li,
       Ui[i + (size_t)j * n] = i > j ? czero() : x;
     }
   }
+}
+
+}  // namespace h2g
+
+namespace h2g {
+
+// ---------------------------------------------------------------------------
+// Hermitian eigen-solver for the step-0 truncation: Householder reduction to
+// a real symmetric tridiagonal T = Q^H H Q (zhetd2 scheme), Sturm-count
+// bisection for the eigenvalues that matter, inverse iteration for the
+// retained eigenvectors, back-transformation by the stored reflectors.
+// H (n x n, ld n, full storage) is overwritten by the reflectors; d, e real
+// (n), tau complex (n), p/w complex scratch (n).
+__device__ inline void cta_hetrd(int n, cplx* H, double* d, double* e, cplx* tau, cplx* p, cplx* w, double* red) {
+  __shared__ cplx s_tau, s_scale;
+  __shared__ double s_beta;
+  __shared__ int s_skip;
+  for (int k = 0; k + 1 < n; ++k) {
+    const int nk = n - k - 1;
+    cplx* x = H + (k + 1) + (size_t)k * n;  // x[0] = H[k+1,k]
+    double part = 0.0;
+    for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) part += cabs2(x[i]);
+    const double xn2 = cta_sum(part, red);
+    if (threadIdx.x == 0) {
+      const cplx al = x[0];
+      if (xn2 == 0.0 && al.y == 0.0) {
+        s_skip = 1;
+        s_tau = czero();
+        s_beta = al.x;
+      } else {
+        double beta = sqrt(cabs2(al) + xn2);
+        if (al.x >= 0.0) beta = -beta;
+        s_skip = 0;
+        s_beta = beta;
+        s_tau = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
+        s_scale = cdiv(cone(), csub(al, cmk(beta, 0.0)));
+      }
+      tau[k] = s_tau;
+      d[k] = H[k + (size_t)k * n].x;
+      e[k] = s_beta;
+    }
+    __syncthreads();
+    if (s_skip) continue;
+    const cplx tk = s_tau, sc = s_scale;
+    for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) x[i] = cmul(x[i], sc);
+    __syncthreads();
+    // p = tau * A22 v, A22 = H[k+1:, k+1:], v = [1; x[1:]]
+    const cplx* A22 = H + (k + 1) + (size_t)(k + 1) * n;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      cplx s = A22[i];  // j = 0, v_0 = 1
+      for (int j = 1; j < nk; ++j) cfma(s, A22[i + (size_t)j * n], x[j]);
+      p[i] = cmul(tk, s);
+    }
+    __syncthreads();
+    // c = v^H p ; w = p - 1/2 conj(tau) c v
+    double cr = 0.0, ci = 0.0;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      const cplx v = i == 0 ? cone() : x[i];
+      const cplx t = cmul(cconj(v), p[i]);
+      cr += t.x;
+      ci += t.y;
+    }
+    cr = cta_sum(cr, red);
+    ci = cta_sum(ci, red);
+    const cplx hc = cscale(cmul(cconj(tk), cmk(cr, ci)), 0.5);
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      const cplx v = i == 0 ? cone() : x[i];
+      w[i] = csub(p[i], cmul(hc, v));
+    }
+    __syncthreads();
+    // A22 -= v w^H + w v^H
+    cplx* B = H + (k + 1) + (size_t)(k + 1) * n;
+    for (int idx = threadIdx.x; idx < nk * nk; idx += blockDim.x) {
+      const int i = idx % nk, j = idx / nk;
+      const cplx vi = i == 0 ? cone() : x[i], vj = j == 0 ? cone() : x[j];
+      cplx a = B[i + (size_t)j * n];
+      a = csub(a, cmul(vi, cconj(w[j])));
+      a = csub(a, cmul(w[i], cconj(vj)));
+      B[i + (size_t)j * n] = a;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    d[n - 1] = H[(n - 1) + (size_t)(n - 1) * n].x;
+    if (n >= 1) e[n - 1] = 0.0;
+  }
+  __syncthreads();
+}
+
+// Number of eigenvalues of T (d, e: off-diagonal e[0..n-2]) strictly below x.
+__device__ inline int sturm_count(int n, const double* d, const double* e, double x, double pivmin) {
+  int c = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0) ++c;
+  for (int i = 1; i < n; ++i) {
+    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) ++c;
+  }
+  return c;
+}
+
+// Eigenvalue with ascending index j of T by bisection on [lo, hi].
+__device__ inline double bisect_eig(int n, const double* d, const double* e, int j, double lo, double hi, double pivmin) {
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(n, d, e, mid, pivmin) > j)
+      hi = mid;
+    else
+      lo = mid;
+    if (hi - lo <= 2e-16 * fmax(fabs(lo), fabs(hi))) break;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// One inverse-iteration solve (T - lam I) y = z, tridiagonal LU with partial
+// pivoting (dgtsv scheme); work: 4n doubles. Result overwrites z.
+__device__ inline void tri_shift_solve(int n, const double* d, const double* e, double lam, double* z, double* wk, double tiny) {
+  double* dl = wk;          // sub
+  double* dd = wk + n;      // diag
+  double* du = wk + 2 * n;  // super
+  double* du2 = wk + 3 * n; // second super (fill-in)
+  for (int i = 0; i < n; ++i) {
+    dd[i] = d[i] - lam;
+    du[i] = i + 1 < n ? e[i] : 0.0;
+    dl[i] = i + 1 < n ? e[i] : 0.0;
+    du2[i] = 0.0;
+  }
+  for (int i = 0; i + 1 < n; ++i) {
+    if (fabs(dd[i]) >= fabs(dl[i])) {
+      if (fabs(dd[i]) < tiny) dd[i] = dd[i] >= 0 ? tiny : -tiny;
+      const double f = dl[i] / dd[i];
+      dd[i + 1] -= f * du[i];
+      z[i + 1] -= f * z[i];
+      dl[i] = 0.0;
+    } else {
+      // swap rows i and i+1
+      const double f = dd[i] / dl[i];
+      dd[i] = dl[i];
+      const double t = dd[i + 1];
+      dd[i + 1] = du[i] - f * t;
+      if (i + 2 < n) {
+        du2[i] = du[i + 1];
+        du[i + 1] = -f * du2[i];
+      }
+      du[i] = t;
+      const double zt = z[i];
+      z[i] = z[i + 1];
+      z[i + 1] = zt - f * z[i + 1];
+    }
+  }
+  if (fabs(dd[n - 1]) < tiny) dd[n - 1] = dd[n - 1] >= 0 ? tiny : -tiny;
+  z[n - 1] /= dd[n - 1];
+  if (n > 1) z[n - 2] = (z[n - 2] - du[n - 2] * z[n - 1]) / dd[n - 2];
+  for (int i = n - 3; i >= 0; --i) z[i] = (z[i] - du[i] * z[i + 1] - du2[i] * z[i + 2]) / dd[i];
 }
 
 }  // namespace h2g

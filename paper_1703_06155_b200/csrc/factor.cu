@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
   cta_copy(b, b - k, Q + (size_t)k * b, b, Vp, b);
 }
 
+__host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 4 + (size_t)bm * bm / 2 + 16; }
+
 // --------------------------------------------------------------------------
 // Step 0, pass 1. The projected fill-in stack Y = Vp^H W (factorization.hpp:
 // 278-296, Vp = complement of the level-entry basis) is reduced to partial
@@ -81,20 +83,32 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
 // is requested: the stack is re-projected on the pass-1 directions
 // (D1 = Vp U1) and eigendecomposed again (k_head), which resolves singular
 // values down to ~eps_mach * sigma_0 like the reference's QR + SVD.
-__global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+__global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[32];
-  __shared__ int s_any;
+  __shared__ int s_any, s_r, s_need;
+  __shared__ double s_s0, s_thr;
   const int q = blockIdx.x, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
-  cplx* ws = gws ? gws + (size_t)q * 2 * bm * bm : reinterpret_cast<cplx*>(smraw);
-  cplx* H = ws;
-  cplx* U = ws + bm * bm;
-  double* lam = reinterpret_cast<double*>(smraw + (gws ? 0 : 2 * (size_t)bm * bm * sizeof(cplx)));
-  int* ord = reinterpret_cast<int*>(lam + bm);
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws ? gws + (size_t)q * eig1_ws_cplx(bm) : reinterpret_cast<cplx*>(smraw);
+  cplx* H = ws;               // m x m
+  cplx* U = ws + bb;          // m x m (Jacobi vectors / retained eigenvectors)
+  double* wk = reinterpret_cast<double*>(ws + 2 * bb);  // 4 m r doubles (inverse iteration)
+  double* Z = wk + 4 * bb;    // m x r real eigenvectors of T
+  unsigned char* sm = smraw + (gws ? 0 : eig1_ws_cplx(bm) * sizeof(cplx));
+  const int bm2 = (bm + 1) & ~1;  // keeps the complex arrays 16-byte aligned
+  double* lam = reinterpret_cast<double*>(sm);
+  double* dg = lam + bm2;
+  double* ed = dg + bm2;
+  cplx* tau = reinterpret_cast<cplx*>(ed + bm2);
+  cplx* pv = tau + bm;
+  cplx* wv = pv + bm;
+  int* ord = reinterpret_cast<int*>(wv + bm);
   int* pr = ord + bm;
   double* rot = reinterpret_cast<double*>(pr + bm + 2);
+
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   {
@@ -103,12 +117,12 @@ __global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, i
     if (any) s_any = 1;
   }
   __syncthreads();
-  cplx* D1 = L.dir + (size_t)q * bm * bm;
-  const cplx* Vp = L.Vp + (size_t)t * bm * bm;
+  cplx* D1 = L.dir + (size_t)q * bb;
+  const cplx* Vp = L.Vp + (size_t)t * bb;
   if (!s_any || m == 0) {
     // no fill-in: the basis stays (factorization.hpp:276)
     cta_copy(b, m, Vp, b, D1, b);
-    if (threadIdx.x == 0) L.pass2[q] = 0, L.rank1[q] = 0, L.cmax[q] = 0.0;
+    if (threadIdx.x == 0) L.pass2[q] = 0, L.rank1[q] = 0, L.cmax[q] = 0.0, L.lam[(size_t)q * bm] = 0.0;
     return;
   }
   const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
@@ -121,37 +135,155 @@ __global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, i
   for (int c = threadIdx.x; c < L.slot_cn[p]; c += blockDim.x) cm = fmax(cm, L.colnorm[L.slot_c0[p] + c]);
   const double cmax = cta_max(cm, red);
   __syncthreads();
-  cta_jacobi_eig(m, H, U, rot, pr, red);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(H[i + i * m].x, 0.0));
-  __syncthreads();
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    int rk = 0;
-    for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
-    ord[rk] = i;
-  }
-  __syncthreads();
-  // D1 = Vp U1 (columns sorted by descending value)
-  for (int idx = threadIdx.x; idx < b * m; idx += blockDim.x) {
-    const int i = idx % b, j = idx / b;
-    cplx v = czero();
-    const int col = ord[j];
-    for (int r = 0; r < m; ++r) cfma(v, Vp[i + (size_t)r * b], U[r + col * m]);
-    D1[i + (size_t)j * b] = v;
-  }
-  double* lout = L.lam + (size_t)q * bm;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) lout[i] = lam[ord[i]];
+  // ---- tridiagonal reduction and the spectrum edge
+  cta_hetrd(m, H, dg, ed, tau, pv, wv, red);
   if (threadIdx.x == 0) {
-    const double s0 = lam[ord[0]];
-    int r = 0;
+    double lo = 0.0, hi = 0.0, emax = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const double off = (i > 0 ? fabs(ed[i - 1]) : 0.0) + (i + 1 < m ? fabs(ed[i]) : 0.0);
+      lo = i == 0 ? dg[i] - off : fmin(lo, dg[i] - off);
+      hi = i == 0 ? dg[i] + off : fmax(hi, dg[i] + off);
+      if (i + 1 < m) emax = fmax(emax, ed[i] * ed[i]);
+    }
+    const double span = fmax(hi - lo, 1e-300);
+    lo -= 1e-14 * span;
+    hi += 1e-14 * span;
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+    lam[0] = lo;  // scratch: bounds
+    lam[1] = hi;
+    lam[2] = pivmin;
+    const double lmax = bisect_eig(m, dg, ed, m - 1, lo, hi, pivmin);
+    const double s0 = sqrt(fmax(lmax, 0.0));
     const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
-    if (s0 > 0.0)
-      while (r < m && lam[ord[r]] > thr) ++r;
-    // refinement needed when the threshold is within reach of the Gram noise
-    const int need = s0 > 0.0 && thr < 1e-4 * s0;
-    L.pass2[q] = need;
+    int r = 0;
+    if (s0 > 0.0) r = m - sturm_count(m, dg, ed, thr * thr, pivmin);
+    r = max(0, min(r, m));
+    s_s0 = s0;
+    s_thr = thr;
+    s_r = r;
+    // the Gram resolves eigenvalues to ~eps_mach * lmax: below ~1e-4 sigma_0
+    // the truncation needs the refinement pass
+    s_need = s0 > 0.0 && thr < 1e-4 * s0;
+  }
+  __syncthreads();
+  const double lo = lam[0], hi = lam[1], pivmin = lam[2];
+  const int r = s_r;
+  __syncthreads();
+  if (s_need) {
+    // rare (eps_fill < 1e-4): full Jacobi decomposition for the two-pass refinement
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      cplx s = czero();
+      for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
+      H[idx] = s;
+    }
+    double dmax = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) dmax = fmax(dmax, H[i + i * m].x);
+    dmax = cta_max(dmax, red);
+    __syncthreads();
+    cta_jacobi_eig(m, H, U, rot, pr, red, 1e-17 * dmax);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(H[i + i * m].x, 0.0));
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      int rk = 0;
+      for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+      ord[rk] = i;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < b * m; idx += blockDim.x) {
+      const int i = idx % b, j = idx / b;
+      cplx v = czero();
+      const int col = ord[j];
+      for (int rr = 0; rr < m; ++rr) cfma(v, Vp[i + (size_t)rr * b], U[rr + col * m]);
+      D1[i + (size_t)j * b] = v;
+    }
+    double* lout = L.lam + (size_t)q * bm;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) lout[i] = lam[ord[i]];
+    if (threadIdx.x == 0) {
+      int rr = 0;
+      while (rr < m && lam[ord[rr]] > s_thr) ++rr;
+      L.pass2[q] = 1, L.rank1[q] = rr, L.cmax[q] = cmax;
+      if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d s0 %.3e thr %.3e r %d (refine)\n", L.level, t, m, s_s0, s_thr, rr);
+    }
+    return;
+  }
+  // ---- top-r eigenpairs of T: bisection + inverse iteration (one thread per
+  // cluster of close eigenvalues, re-orthogonalised within the cluster)
+  const double gaptol = 1e-8 * fmax(fabs(lo), fabs(hi));
+  for (int j = threadIdx.x; j < r; j += blockDim.x) lam[j] = bisect_eig(m, dg, ed, m - 1 - j, lo, hi, pivmin);
+  __syncthreads();
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    if (j > 0 && lam[j - 1] - lam[j] < gaptol) continue;  // handled by the cluster leader
+    int jend = j + 1;
+    while (jend < r && lam[jend - 1] - lam[jend] < gaptol) ++jend;
+    double* w4 = wk + (size_t)4 * m * j;
+    for (int q2 = j; q2 < jend; ++q2) {
+      double* z = Z + (size_t)m * q2;
+      for (int i = 0; i < m; ++i) {
+        unsigned h = (unsigned)(i * 2654435761u) ^ (unsigned)((q2 + 1) * 40503u);
+        h ^= h >> 13;
+        h *= 0x5bd1e995u;
+        h ^= h >> 15;
+        z[i] = 1.0 + 0.5 * ((double)(h & 0xffff) / 65535.0 - 0.5);
+      }
+      for (int it = 0; it < 4; ++it) {
+        tri_shift_solve(m, dg, ed, lam[q2], z, w4, pivmin * 1e10 + 1e-300);
+        for (int q3 = j; q3 < q2; ++q3) {  // Gram-Schmidt within the cluster
+          const double* y = Z + (size_t)m * q3;
+          double dot = 0.0;
+          for (int i = 0; i < m; ++i) dot += y[i] * z[i];
+          for (int i = 0; i < m; ++i) z[i] -= dot * y[i];
+        }
+        double nrm = 0.0;
+        for (int i = 0; i < m; ++i) nrm += z[i] * z[i];
+        nrm = sqrt(nrm);
+        const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+        for (int i = 0; i < m; ++i) z[i] *= inv;
+      }
+    }
+  }
+  __syncthreads();
+  // back-transform U = Q Z (Q = H_0 ... H_{m-2}), one warp per vector
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j < r; j += nw) {
+      cplx* u = U + (size_t)m * j;
+      const double* z = Z + (size_t)m * j;
+      for (int i = lane; i < m; i += 32) u[i] = cmk(z[i], 0.0);
+      __syncwarp();
+      for (int kk = m - 2; kk >= 0; --kk) {
+        const cplx tk = tau[kk];
+        if (tk.x == 0.0 && tk.y == 0.0) continue;
+        const cplx* v = H + (kk + 1) + (size_t)kk * m;  // v[0] = 1
+        cplx* y = u + kk + 1;
+        const int nk = m - kk - 1;
+        cplx s = czero();
+        for (int i = lane; i < nk; i += 32) cfma(s, i == 0 ? cone() : cconj(v[i]), y[i]);
+        for (int o = 16; o > 0; o >>= 1) {
+          s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+          s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+        }
+        s = cmul(tk, s);
+        __syncwarp();
+        for (int i = lane; i < nk; i += 32) y[i] = csub(y[i], cmul(i == 0 ? cone() : v[i], s));
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  // D1 = Vp Qm, Qm = Householder basis of [U_r | complement]
+  cta_copy(b, m, Vp, b, D1, b);
+  if (r > 0) {
+    __syncthreads();
+    cta_householder_qr(m, r, U, m, tau, red);
+    cta_apply_q_right(b, m, r, D1, b, U, m, tau, pv);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    L.pass2[q] = 0;
     L.rank1[q] = r;
     L.cmax[q] = cmax;
-    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d pass2 %d\n", L.level, t, m, cmax, s0, thr, r, need);
+    L.lam[(size_t)q * bm] = s_s0;
+    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d\n", L.level, t, m, cmax, s_s0, s_thr, r);
   }
 }
 
@@ -193,7 +325,9 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
       Hc[idx] = s;
     }
     __syncthreads();
-    cta_jacobi_eig(m, Hc, Uc, rot, pr, red);
+    // pass 2 must resolve values near the pass-1 threshold (sigma^2 ~ thr^2)
+    const double thr1 = fmax(L.eps * L.lam[(size_t)q * bm], L.eps * L.cmax[q]);
+    cta_jacobi_eig(m, Hc, Uc, rot, pr, red, 1e-8 * thr1 * thr1);
     for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(Hc[i + i * m].x, 0.0));
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -683,18 +817,19 @@ void launch_complement(const DevLevel& L, cudaStream_t s) {
   }
 }
 
-size_t eig1_smem_bytes(int bm) { return 2 * (size_t)bm * bm * sizeof(cplx) + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64; }
+size_t eig1_small_bytes(int bm) { return (size_t)(bm + 1) * 8 * 3 + (size_t)bm * 16 * 3 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64; }
+size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_small_bytes(bm); }
 
 void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
   const size_t need = eig1_smem_bytes(L.bmax);
   if (need <= kSmemCap) {
     set_smem((const void*)k_eig1, need);
-    k_eig1<<<nb, 256, need, s>>>(L, batch_cl, p0, nullptr);
+    k_eig1<<<nb, 512, need, s>>>(L, batch_cl, p0, nullptr);
   } else {
-    const size_t small = need - 2 * (size_t)L.bmax * L.bmax * sizeof(cplx);
+    const size_t small = eig1_small_bytes(L.bmax);
     set_smem((const void*)k_eig1, small);
-    cplx* ws = workspace(2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb, s);
-    k_eig1<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
+    cplx* ws = workspace(eig1_ws_cplx(L.bmax) * sizeof(cplx) * nb, s);
+    k_eig1<<<nb, 512, small, s>>>(L, batch_cl, p0, ws);
   }
   post_launch("k_eig1");
 }

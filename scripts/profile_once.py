@@ -1,0 +1,18 @@
+"""One factorize + solve of a BASELINE config (the command profiled by ncu)."""
+import sys
+import time
+
+sys.path.insert(0, ".")
+import paper_1703_06155_b200 as h2g  # noqa: E402
+from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+sched = sys.argv[2] if len(sys.argv) > 2 else "reference"
+c = BASELINE_CONFIGS[cfg]
+k0, scale, diag = vie_constants(c["cells"], c["side"])
+A = h2g.H2Matrix.build(vie_grid_points(c["cells"], c["side"]), c["leaf"], 1.0, h2g.helmholtz_kernel(k0, diag, scale), c["eps"])
+b = h2g.random_rhs(A.n, 1234)
+t0 = time.time()
+ch = h2g.factorize(A, c["eps"], schedule=sched)
+x = ch.solve(b)
+print("factorize+solve wall %.3f s" % (time.time() - t0), ch.timing())
