@@ -209,7 +209,7 @@ struct ChainLevelHost {
   DBuf arena;                // chain numeric data of this level
   DBuf meta;                 // packed int / offset arrays
   SolveLevel sl{};
-  std::vector<int> batch_ptr;
+  std::vector<int> batch_ptr, batch_maxc;
   const int* d_batch = nullptr;
   std::vector<int> fs_ptr;
   const SolveTargetD* d_fs = nullptr;
@@ -231,7 +231,7 @@ struct h2g_chain {
   std::vector<std::unique_ptr<ChainLevelHost>> levels;
   int64_t root_size = 0;
   DBuf root;  // LU packed (n_root^2)
-  DBuf ybuf, tmpbuf;
+  DBuf ybuf, tmpbuf, partbuf;
   size_t storage_bytes = 0;
   double factor_ms = 0.0, solve_ms = 0.0;
   long long factor_launches = 0, solve_launches = 0;
@@ -959,6 +959,14 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CL->Lself_off = Lself_off;
         CL->Uself_off = Uself_off;
         CL->batch_ptr = SC.batch_ptr;
+        for (int bi = 0; bi + 1 < (int)SC.batch_ptr.size(); ++bi) {
+          int mc = 0;
+          for (int pq = SC.batch_ptr[bi]; pq < SC.batch_ptr[bi + 1]; ++pq) {
+            const int tt = SC.batch_cl[pq];
+            mc = std::max(mc, Y.C_ptr[tt + 1] - Y.C_ptr[tt]);
+          }
+          CL->batch_maxc.push_back(mc);
+        }
         CL->d_batch = d_bat;
         CL->fs_ptr = W.fsolve_ptr;
         CL->d_fs = at<SolveTargetD>(mt, o_fs);
@@ -1236,8 +1244,10 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
       const int nbat = static_cast<int>(CL.batch_ptr.size()) - 1;
       for (int bi = nbat - 1; bi >= 0; --bi) {
         const int p0 = CL.batch_ptr[bi], nb = CL.batch_ptr[bi + 1] - p0;
-        launch_bwd(CL.sl, CL.d_batch + p0, nb, y, n, nrhs, expl, st);
-        ++launches;
+        const size_t need = (size_t)nb * (CL.batch_maxc[bi] + 1) * CL.sl.bmax * nrhs * 16;
+        if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
+        launch_bwd(CL.sl, CL.d_batch + p0, nb, CL.batch_maxc[bi], y, n, nrhs, expl, C->partbuf.as<cplx>(), st);
+        launches += 2;
       }
     }
   }

@@ -570,3 +570,69 @@ __device__ inline void tri_shift_solve(int n, const double* d, const double* e, 
 }
 
 }  // namespace h2g
+
+namespace h2g {
+
+// ---------------------------------------------------------------------------
+// CTA-cooperative tiled ZGEMM: C (m x n) = alpha op(A) op(B) + beta C over
+// 64 x 64 output tiles, K staged 16 at a time through shared memory (sm must
+// hold kTileSmemCplx complex), 4 x 4 complex register micro-tile per thread.
+// Requires blockDim.x == 256. C must not alias A or B.
+constexpr int kTileSmemCplx = 64 * 17 + 16 * 65;
+
+__device__ inline void cta_gemm_tiled(int m, int n, int k, double alpha, const cplx* A, int lda, int opA, const cplx* B, int ldb, int opB,
+                                      double beta, cplx* C, int ldc, cplx* sm) {
+  cplx(*sA)[17] = reinterpret_cast<cplx(*)[17]>(sm);
+  cplx(*sB)[65] = reinterpret_cast<cplx(*)[65]>(sm + 64 * 17);
+  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  const bool a_rowmajor = opA == OP_T || opA == OP_C;  // consecutive p contiguous
+  const bool b_rowmajor = opB == OP_N || opB == OP_R;  // consecutive p contiguous
+  for (int r0 = 0; r0 < m; r0 += 64)
+    for (int c0 = 0; c0 < n; c0 += 64) {
+      cplx acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = czero();
+      for (int k0 = 0; k0 < k; k0 += 16) {
+        const int kk = min(16, k - k0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 64 * 16; idx += 256) {
+          int i, p;
+          if (a_rowmajor) p = idx % 16, i = idx / 16;
+          else i = idx % 64, p = idx / 64;
+          sA[i][p] = (p < kk && r0 + i < m) ? ld_op(A, lda, opA, r0 + i, k0 + p) : czero();
+          int j, q;
+          if (b_rowmajor) q = idx % 16, j = idx / 16;
+          else j = idx % 64, q = idx / 64;
+          sB[q][j] = (q < kk && c0 + j < n) ? ld_op(B, ldb, opB, k0 + q, c0 + j) : czero();
+        }
+        __syncthreads();
+        for (int p = 0; p < kk; ++p) {
+          cplx av[4], bv[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) bv[b] = sB[p][tc * 4 + b];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + b;
+          if (i < m && j < n) {
+            cplx* o = C + i + (size_t)j * ldc;
+            const cplx v = acc[a][b];
+            *o = beta == 0.0 ? cscale(v, alpha) : make_double2(beta * o->x + alpha * v.x, beta * o->y + alpha * v.y);
+          }
+        }
+    }
+  __syncthreads();
+}
+
+}  // namespace h2g

@@ -294,30 +294,32 @@ __global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, i
 // and step 3a (unpivoted LU of the leading e x e block, :390-398; self panels
 // and the self Schur product, :409-420; cleanup, :431-435).
 __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ cplx sm[kTileSmemCplx];
   __shared__ double red[32];
   __shared__ int s_r;
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int q = blockIdx.x, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
   const int cid = (1 << L.level) - 1 + t;
-  cplx* ws = gws ? gws + (size_t)q * 3 * bm * bm : reinterpret_cast<cplx*>(smraw);
-  cplx* buf0 = ws;
-  cplx* buf1 = ws + bm * bm;
-  cplx* buf2 = ws + 2 * bm * bm;
-  double* lam = reinterpret_cast<double*>(smraw + (gws ? 0 : 3 * (size_t)bm * bm * sizeof(cplx)));
+  cplx* ws = gws + (size_t)q * 4 * bb;
+  cplx* Hc = ws;          // pass-2 Gram (m x m), later the LU workspace
+  cplx* Uc = ws + bb;     // pass-2 eigenvectors
+  cplx* Dd = ws + 2 * bb; // rotated diagonal block
+  cplx* T = ws + 3 * bb;  // temporaries
+  double* lam = reinterpret_cast<double*>(smraw);
   int* ord = reinterpret_cast<int*>(lam + bm);
   int* pr = ord + bm;
   double* rot = reinterpret_cast<double*>(pr + bm + 2);
 
-  const cplx* D1 = L.dir + (size_t)q * bm * bm;
-  cplx* Uc = buf1;  // m x m rotation of the pass-1 directions (identity without pass 2)
+  const cplx* D1 = L.dir + (size_t)q * bb;
   for (int i = threadIdx.x; i < m; i += blockDim.x) ord[i] = i;
   if (threadIdx.x == 0) s_r = L.rank1[q];
   __syncthreads();
-  if (L.pass2[q]) {
+  const bool p2 = L.pass2[q] != 0;
+  if (p2) {
     // pass 2: Gram of D1^H W (near-diagonal, graded), Jacobi with the relative criterion
-    cplx* Hc = buf0;
     const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
       cplx s = czero();
@@ -347,47 +349,37 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
       if (L.debug) printf("[h2g] pass2 level %d cluster %d m %d s0 %.3e r %d\n", L.level, t, m, s0, r);
     }
     __syncthreads();
-  } else {
-    cta_identity(m, m, Uc, m);
+    // directions D1 Uc (b x m) into T
+    cta_gemm_tiled(b, m, m, 1.0, D1, b, OP_N, Uc, m, OP_N, 0.0, T, b, sm);
   }
-  __syncthreads();
   const int r = s_r;
   const int kf = k + r, e = b - kf;
   if (threadIdx.x == 0) L.kfin[t] = kf;
-  const cplx* Vp = D1;  // directions (b x m), rotated by Uc below
-  // Qtilde = [Vp Uc(:, ord[r:]) | V | Vp Uc(:, ord[:r])]
-  cplx* Qt = buf2;
-  const cplx* V = L.V0 + (size_t)t * bm * bm;
+  const cplx* Dir = p2 ? T : D1;
+
+  // Qtilde = [Dir(:, ord[r:]) | V | Dir(:, ord[:r])] (factorization.hpp:300-333)
+  cplx* Qt = L.chain + L.Qt_off[t];
+  const cplx* V = L.V0 + (size_t)t * bb;
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int i = idx % b, j = idx / b;
     cplx v;
-    if (j >= e && j < e + k) {
+    if (j >= e && j < e + k)
       v = V[i + (size_t)(j - e) * b];
-    } else {
-      const int col = j < e ? ord[r + j] : ord[j - e - k];
-      v = czero();
-      for (int p = 0; p < m; ++p) cfma(v, Vp[i + (size_t)p * b], Uc[p + col * m]);
-    }
-    Qt[i + j * b] = v;
+    else
+      v = Dir[i + (size_t)(j < e ? ord[r + j] : ord[j - e - k]) * b];
+    Qt[i + (size_t)j * b] = v;
   }
   __syncthreads();
-  cplx* gQt = L.chain + L.Qt_off[t];
-  cta_copy(b, b, Qt, b, gQt, b);
-  // rotate the diagonal block: Dii <- Qt^H Dii conj(Qt)
+  // rotate the diagonal block: Dii <- Qt^H Dii conj(Qt) (:345-347)
   cplx* gD = blk(L.D, L.diag_blk[t], bm);
-  cplx* Dd = buf0;
-  cplx* T = buf1;
-  cta_copy(b, b, gD, b, Dd, b);
-  __syncthreads();
-  cta_gemm(b, b, b, 1.0, Qt, b, OP_C, Dd, b, OP_N, 0.0, T, b);
-  __syncthreads();
-  cta_gemm(b, b, b, 1.0, T, b, OP_N, Qt, b, OP_R, 0.0, Dd, b);
-  __syncthreads();
+  cta_gemm_tiled(b, b, b, 1.0, Qt, b, OP_C, gD, b, OP_N, 0.0, T, b, sm);
+  cta_gemm_tiled(b, b, b, 1.0, T, b, OP_N, Qt, b, OP_R, 0.0, Dd, b, sm);
   if (e > 0) {
-    cta_copy(e, e, Dd, b, T, e);
+    cplx* LU = Hc;
+    cta_copy(e, e, Dd, b, LU, e);
     __syncthreads();
     double pmag = 0.0;
-    const int fail = cta_lu_nopiv(e, T, e, 1e-13, &pmag, red);
+    const int fail = cta_lu_nopiv(e, LU, e, 1e-13, &pmag, red);
     if (fail >= 0) {
       if (threadIdx.x == 0) raise_error(L.err, 4, cid, L.level, fail, pmag);
       return;
@@ -396,26 +388,24 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
     cplx* U11 = L.chain + L.U11_off[t];
     for (int idx = threadIdx.x; idx < e * e; idx += blockDim.x) {
       const int i = idx % e, j = idx / e;
-      const cplx v = T[idx];
+      const cplx v = LU[idx];
       L11[idx] = i > j ? v : (i == j ? cone() : czero());
       U11[idx] = i <= j ? v : czero();
     }
     cplx* Li = L.chain + L.Linv_off[t];
     cplx* Ui = L.chain + L.Uinv_off[t];
-    cta_tri_inverses(e, T, e, Li, Ui);
+    cta_tri_inverses(e, LU, e, Li, Ui);
     __syncthreads();
     if (kf > 0) {
       cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
       cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
-      cta_gemm(e, kf, e, 1.0, Li, e, OP_N, Dd + (size_t)e * b, b, OP_N, 0.0, Us, e);
-      cta_gemm(kf, e, e, 1.0, Dd + e, b, OP_N, Ui, e, OP_N, 0.0, Ls, kf);
-      __syncthreads();
-      cta_gemm(kf, kf, e, -1.0, Ls, kf, OP_N, Us, e, OP_N, 1.0, Dd + e + (size_t)e * b, b);
-      __syncthreads();
+      cta_gemm_tiled(e, kf, e, 1.0, Li, e, OP_N, Dd + (size_t)e * b, b, OP_N, 0.0, Us, e, sm);
+      cta_gemm_tiled(kf, e, e, 1.0, Dd + e, b, OP_N, Ui, e, OP_N, 0.0, Ls, kf, sm);
+      cta_gemm_tiled(kf, kf, e, -1.0, Ls, kf, OP_N, Us, e, OP_N, 1.0, Dd + e + (size_t)e * b, b, sm);
     }
     for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
       const int i = idx % b, j = idx / b;
-      if (i < e || j < e) Dd[idx] = (i == j) ? cone() : czero();
+      if (i < e || j < e) Dd[i + (size_t)j * b] = (i == j) ? cone() : czero();
     }
     __syncthreads();
   }
@@ -429,54 +419,39 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
 // neighbour eliminated earlier the panel is also lifted back to its
 // level-entry frame (deposit_fill, :359-362).
 __global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, const PanelItemD* items, cplx* gws) {
-  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ cplx sm[kTileSmemCplx];
   const PanelItemD it = items[blockIdx.x];
   const int t = batch_cl[it.q];
   const int bm = L.bmax;
   const int b = L.bsz[t], e = b - L.kfin[t];
   const int bn = L.bsz[it.nb];
-  cplx* sQ = gws ? gws + (size_t)blockIdx.x * 3 * bm * bm : reinterpret_cast<cplx*>(smraw);
-  cplx* sD = sQ + bm * bm;
-  cplx* sT = sD + bm * bm;
-  const cplx* gQ = L.chain + L.Qt_off[t];
+  cplx* T = gws + (size_t)blockIdx.x * bm * bm;
+  const cplx* Q = L.chain + L.Qt_off[t];
   cplx* gD = blk(L.D, it.blk, bm);
-  cta_copy(b, b, gQ, b, sQ, b);
   const cplx* Li = L.chain + L.Linv_off[t];
   const cplx* Ui = L.chain + L.Uinv_off[t];
   if (it.side == 0) {  // D(t, c): b x bn
-    cta_copy(b, bn, gD, b, sD, b);
-    __syncthreads();
-    cta_gemm(b, bn, b, 1.0, sQ, b, OP_C, sD, b, OP_N, 0.0, sT, b);
-    __syncthreads();
+    cta_gemm_tiled(b, bn, b, 1.0, Q, b, OP_C, gD, b, OP_N, 0.0, T, b, sm);
     if (e > 0) {
       cplx* Ub = L.chain + L.Ubar_off[it.entry];  // e x bn
-      cta_gemm(e, bn, e, 1.0, Li, e, OP_N, sT, b, OP_N, 0.0, Ub, e);
-      __syncthreads();
-      if (it.lift) {
-        const cplx* Qn = L.chain + L.Qt_off[it.nb];
-        cta_gemm(e, bn, bn, 1.0, Ub, e, OP_N, Qn, bn, OP_T, 0.0, L.lift + L.Ubar_off[it.entry], e);
-      }
-      for (int idx = threadIdx.x; idx < e * bn; idx += blockDim.x) sT[(idx % e) + (idx / e) * b] = czero();
-      __syncthreads();
+      cta_gemm_tiled(e, bn, e, 1.0, Li, e, OP_N, T, b, OP_N, 0.0, Ub, e, sm);
+      if (it.lift) cta_gemm_tiled(e, bn, bn, 1.0, Ub, e, OP_N, L.chain + L.Qt_off[it.nb], bn, OP_T, 0.0, L.lift + L.Ubar_off[it.entry], e, sm);
     }
-    cta_copy(b, bn, sT, b, gD, b);
+    for (int idx = threadIdx.x; idx < b * bn; idx += blockDim.x) {
+      const int i = idx % b, j = idx / b;
+      gD[i + (size_t)j * b] = i < e ? czero() : T[i + (size_t)j * b];
+    }
   } else {  // D(j, t): bn x b
-    cta_copy(bn, b, gD, bn, sD, bn);
-    __syncthreads();
-    cta_gemm(bn, b, b, 1.0, sD, bn, OP_N, sQ, b, OP_R, 0.0, sT, bn);
-    __syncthreads();
+    cta_gemm_tiled(bn, b, b, 1.0, gD, bn, OP_N, Q, b, OP_R, 0.0, T, bn, sm);
     if (e > 0) {
       cplx* Lb = L.chain + L.Lbar_off[it.entry];  // bn x e
-      cta_gemm(bn, e, e, 1.0, sT, bn, OP_N, Ui, e, OP_N, 0.0, Lb, bn);
-      __syncthreads();
-      if (it.lift) {
-        const cplx* Qn = L.chain + L.Qt_off[it.nb];
-        cta_gemm(bn, e, bn, 1.0, Qn, bn, OP_N, Lb, bn, OP_N, 0.0, L.lift + L.Lbar_off[it.entry], bn);
-      }
-      for (int idx = threadIdx.x; idx < bn * e; idx += blockDim.x) sT[idx] = czero();
-      __syncthreads();
+      cta_gemm_tiled(bn, e, e, 1.0, T, bn, OP_N, Ui, e, OP_N, 0.0, Lb, bn, sm);
+      if (it.lift) cta_gemm_tiled(bn, e, bn, 1.0, L.chain + L.Qt_off[it.nb], bn, OP_N, Lb, bn, OP_N, 0.0, L.lift + L.Lbar_off[it.entry], bn, sm);
     }
-    cta_copy(bn, b, sT, bn, gD, bn);
+    for (int idx = threadIdx.x; idx < bn * b; idx += blockDim.x) {
+      const int i = idx % bn, j = idx / bn;
+      gD[i + (size_t)j * bn] = j < e ? czero() : T[i + (size_t)j * bn];
+    }
   }
 }
 
@@ -835,16 +810,11 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStr
 }
 
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
-  const size_t need = head_smem_bytes(L.bmax);
-  if (need <= kSmemCap) {
-    set_smem((const void*)k_head, need);
-    k_head<<<nb, 256, need, s>>>(L, batch_cl, p0, nullptr);
-  } else {
-    const size_t small = need - smem3(L.bmax);
-    set_smem((const void*)k_head, small);
-    cplx* ws = workspace(smem3(L.bmax) * nb, s);
-    k_head<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
-  }
+  const int bm = L.bmax;
+  const size_t small = (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
+  set_smem((const void*)k_head, small);
+  cplx* ws = workspace(4 * (size_t)bm * bm * sizeof(cplx) * nb, s);
+  k_head<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
   post_launch("k_head");
 }
 
@@ -856,14 +826,8 @@ void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
 
 void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s) {
   if (nitems <= 0) return;
-  const size_t need = smem3(L.bmax);
-  if (need <= kSmemCap) {
-    set_smem((const void*)k_panel, need);
-    k_panel<<<nitems, 256, need, s>>>(L, batch_cl, items, nullptr);
-  } else {
-    cplx* ws = workspace(need * nitems, s);
-    k_panel<<<nitems, 256, 0, s>>>(L, batch_cl, items, ws);
-  }
+  cplx* ws = workspace((size_t)L.bmax * L.bmax * sizeof(cplx) * nitems, s);
+  k_panel<<<nitems, 256, 0, s>>>(L, batch_cl, items, ws);
   post_launch("k_panel");
 }
 

@@ -80,9 +80,43 @@ __global__ void __launch_bounds__(256) k_fwd_lbar(SolveLevel S, const SolveTarge
   }
 }
 
-// Backward record (solve.hpp:73-81): head -= sum_c Ubar(m,c) y_c; U11 solve;
-// seg <- conj(Qt) seg. One CTA per record.
-__global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv) {
+// Backward gather (solve.hpp:77): partial[q][c] = Ubar(m, c) y[pos_c ...]
+// for one neighbour c of record m = batch[q] (the last slot is the self
+// block), spread over CTAs so the chain blocks stream at full bandwidth.
+__global__ void __launch_bounds__(256) k_bwd_gather(SolveLevel S, const int* batch_cl, const cplx* y, long long ldy, int nrhs, cplx* part,
+                                                    long long pstride) {
+  const int q = blockIdx.x, c = blockIdx.y;
+  const int t = batch_cl[q];
+  const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
+  const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
+  if (e == 0 || c > nC || (c == nC && kf == 0)) return;
+  const cplx* M;
+  const cplx* x;
+  int cols;
+  if (c < nC) {
+    const int ent = S.C_ptr[t] + c, nb = S.C_nb[ent];
+    cols = S.bsz[nb];
+    M = S.chain + S.Ubar_off[ent];
+    x = y + S.pos[nb];
+  } else {
+    cols = kf;
+    M = S.chain + S.Uself_off[t];
+    x = y + S.pos[t] + e;
+  }
+  cplx* out = part + ((size_t)q * gridDim.y + c) * pstride;
+  for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
+    const int i = idx % e, r = idx / e;
+    cplx acc = czero();
+    const cplx* xr = x + r * ldy;
+    for (int p = 0; p < cols; ++p) cfma(acc, M[i + (size_t)p * e], xr[p]);
+    out[i + (size_t)r * e] = acc;
+  }
+}
+
+// Backward record (solve.hpp:73-81): head -= sum of the gathered partials (in
+// neighbour order); U11 solve; seg <- conj(Qt) seg. One CTA per record.
+__global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part,
+                                             long long pstride, int nslot) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int t = batch_cl[blockIdx.x];
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
@@ -92,21 +126,12 @@ __global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, 
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
   __syncthreads();
   if (e > 0) {
+    const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
+    const int nuse = nC + (kf > 0 ? 1 : 0);
     for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
       const int i = idx % e, c = idx / e;
       cplx acc = czero();
-      for (int q = S.C_ptr[t]; q < S.C_ptr[t + 1]; ++q) {
-        const int nb = S.C_nb[q];
-        const int cols = S.bsz[nb];
-        const cplx* M = S.chain + S.Ubar_off[q];
-        const cplx* x = y + S.pos[nb] + c * ldy;
-        for (int p = 0; p < cols; ++p) cfma(acc, M[i + (size_t)p * e], x[p]);
-      }
-      if (kf > 0) {
-        const cplx* M = S.chain + S.Uself_off[t];
-        const cplx* x = sS + e + c * b;
-        for (int p = 0; p < kf; ++p) cfma(acc, M[i + (size_t)p * e], x[p]);
-      }
+      for (int q = 0; q < nuse; ++q) acc = cadd(acc, part[((size_t)blockIdx.x * nslot + (q < nC ? q : nC)) * pstride + i + (size_t)c * e]);
       sS[i + c * b] = csub(sS[i + c * b], acc);
     }
     __syncthreads();
@@ -222,10 +247,14 @@ void launch_fwd_lbar(const SolveLevel& S, const SolveTargetD* t, int nt, const S
   if (nt > 0) k_fwd_lbar<<<nt, 256, 0, s>>>(S, t, c, y, ldy, nrhs);
 }
 
-void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
+void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, int maxc, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
+                cudaStream_t s) {
+  const long long pstride = (long long)S.bmax * nrhs;
+  const int nslot = maxc + 1;
+  k_bwd_gather<<<dim3(nb, nslot), 256, 0, s>>>(S, batch_cl, y, ldy, nrhs, part, pstride);
   const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
   smem_attr((const void*)k_bwd, smem);
-  k_bwd<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv);
+  k_bwd<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv, part, pstride, nslot);
 }
 
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s) {

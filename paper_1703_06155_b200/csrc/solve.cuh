@@ -34,7 +34,8 @@ struct SolveContribD {
 
 void launch_fwd_head(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
 void launch_fwd_lbar(const SolveLevel& S, const SolveTargetD* t, int nt, const SolveContribD* c, cplx* y, long long ldy, int nrhs, cudaStream_t s);
-void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
+void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, int maxc, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
+                cudaStream_t s);
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s);
 void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s);
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s);
