@@ -179,7 +179,8 @@ int h2g_chain_timing(const h2g_chain* c, double* factor_ms, double* solve_ms, in
 /* Per-kernel-class device timing of factorize (CUDA events around every
  * launch on the context stream; off by default). Classes: 0 complement,
  * 1 step-0 projection/Gram GEMMs, 2 column norms, 3 eig pass 1, 4 head,
- * 5 panels, 6 Schur scatter, 7 level merge, 8 root LU, 9 other. */
+ * 5 panels, 6 Schur scatter, 7 level merge, 8 root LU, 9 other, 10 eigenvectors,
+ * 11 retained-basis construction. */
 int h2g_set_profiling(h2g_context* ctx, int32_t on);
 /* out[4] for class cls: ms, launches, algorithmic flops, algorithmic bytes */
 int h2g_chain_kernel_stats(const h2g_chain* c, int32_t cls, double* out);

@@ -468,7 +468,7 @@ class FactorChain:
         lib().h2g_chain_timing(self.h, C.byref(f), C.byref(s), C.byref(fl), C.byref(sl))
         return dict(factor_ms=f.value, solve_ms=s.value, factor_launches=fl.value, solve_launches=sl.value)
 
-    KERNEL_CLASSES = ("complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other")
+    KERNEL_CLASSES = ("complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other", "eigvec", "eig1b")
 
     def kernel_stats(self):
         """Per kernel class: device ms, launches, algorithmic flops and bytes

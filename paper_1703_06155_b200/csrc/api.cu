@@ -137,7 +137,9 @@ struct Prof {
   struct Rec {
     int cls;
     cudaEvent_t a, b;
+    int level;
   };
+  int cur_level = -1;
   std::vector<Rec> recs;
   int open_cls = -1;
   cudaEvent_t open_ev = nullptr;
@@ -163,14 +165,14 @@ struct Prof {
     if (!on || open_cls < 0) return;
     cudaEvent_t b = get();
     cudaEventRecord(b, s);
-    recs.push_back({open_cls, open_ev, b});
+    recs.push_back({open_cls, open_ev, b, cur_level});
     open_cls = -1;
   }
   ~Prof() {
     for (auto e : pool) cudaEventDestroy(e);
   }
 };
-enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SCHUR, PC_MERGE, PC_ROOT, PC_OTHER, PC_N };
+enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SCHUR, PC_MERGE, PC_ROOT, PC_OTHER, PC_EIGVEC, PC_EIG1B, PC_N };
 
 struct h2g_context {
   int device = 0;
@@ -815,6 +817,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.err = ctx->d_err;
         DL.debug = std::getenv("H2G_DEBUG") ? std::atoi(std::getenv("H2G_DEBUG")) : 0;
 
+        ctx->prof.cur_level = l;
         ctx->prof.begin(PC_COMPLEMENT, st);
         launch_complement(DL, st);
         ctx->prof.end(st);
@@ -830,18 +833,24 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
           Prof& pf = ctx->prof;
           pf.begin(PC_GRAM, st);
-          launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st);
-          launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          const int tl = ((bm + 63) / 64) * ((bm + 63) / 64);
+          launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st, tl);
+          launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
           pf.end(st);
           pf.begin(PC_COLNORM, st);
           launch_colnorm(dN.as<NormDesc>() + n_ptr[bi], nn, st);
           pf.end(st);
           pf.begin(PC_EIG1, st);
-          launch_eig1(DL, d_bat + p0, p0, nb, st);
+          int mmax = 0;
+          for (int pq = p0; pq < p0 + nb; ++pq) mmax = std::max(mmax, cur.bsz[SC.batch_cl[pq]] - cur.korig[SC.batch_cl[pq]]);
+          launch_eig1(DL, d_bat + p0, p0, nb, mmax, st, [&](int ph) {
+            pf.end(st);
+            pf.begin(ph == 1 ? PC_EIGVEC : PC_EIG1B, st);
+          });
           pf.end(st);
           pf.begin(PC_GRAM, st);
-          launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st);
-          launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st);
+          launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st, tl);
+          launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
           pf.end(st);
           pf.begin(PC_HEAD, st);
           launch_head(DL, d_bat + p0, p0, nb, st);
@@ -854,7 +863,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           pf.end(st);
           C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
           C->klaunch[PC_COLNORM] += nn > 0;
-          C->klaunch[PC_EIG1] += 1;
+          C->klaunch[PC_EIG1] += 3;
           C->klaunch[PC_HEAD] += 1;
           C->klaunch[PC_PANEL] += W.panel_ptr[bi + 1] > W.panel_ptr[bi];
           C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
@@ -1100,8 +1109,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         upload(dg2, g2, st);
         ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
-        launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st);
-        launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st);
+        const int tlm = ((std::max(bm, nxt.bmax) + 63) / 64) * ((std::max(bm, nxt.bmax) + 63) / 64);
+        launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, tlm);
+        launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, tlm);
         ctx->prof.end(st);
         C->klaunch[PC_MERGE] += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
         launches += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
@@ -1172,12 +1182,19 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     C->factor_ms = ms;
     C->factor_launches = launches;
-    if (ctx->prof.on)
+    if (ctx->prof.on) {
+      std::map<std::pair<int, int>, double> per;
       for (const auto& r : ctx->prof.recs) {
         float e = 0.f;
         cudaEventElapsedTime(&e, r.a, r.b);
         C->kms[r.cls] += e;
+        per[{r.level, r.cls}] += e;
       }
+      if (verbose) {
+        static const char* nm[PC_N] = {"complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other", "eigvec", "eig1b"};
+        for (const auto& kv : per) std::fprintf(stderr, "[h2g] level %d %-10s %9.2f ms\n", kv.first.first, nm[kv.first.second], kv.second);
+      }
+    }
     C->factor_flops = flops;
     C->schur_flops = sflops;
     C->schur_bytes = sbytes;

@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
   cta_copy(b, b - k, Q + (size_t)k * b, b, Vp, b);
 }
 
-__host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 4 + (size_t)bm * bm / 2 + 16; }
+// H, U, then 4.5 bm^2 of scratch (inverse iteration, then the compact-WY GEMMs)
+__host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 6 + (size_t)bm * 8 + 16; }
 
 // --------------------------------------------------------------------------
 // Step 0, pass 1. The projected fill-in stack Y = Vp^H W (factorization.hpp:
@@ -83,11 +84,13 @@ __host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm 
 // is requested: the stack is re-projected on the pass-1 directions
 // (D1 = Vp U1) and eigendecomposed again (k_head), which resolves singular
 // values down to ~eps_mach * sigma_0 like the reference's QR + SVD.
-__global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+__global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ cplx tile_sm[kTileSmemCplx];
   __shared__ double red[32];
   __shared__ int s_any, s_r, s_need;
   __shared__ double s_s0, s_thr;
+  const long long Tstart = clock64();
   const int q = blockIdx.x, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, i
   cplx* H = ws;               // m x m
   cplx* U = ws + bb;          // m x m (Jacobi vectors / retained eigenvectors)
   double* wk = reinterpret_cast<double*>(ws + 2 * bb);  // 4 m r doubles (inverse iteration)
-  double* Z = wk + 4 * bb;    // m x r real eigenvectors of T
+  double* Z = wk + 8 * bb;    // m x r real eigenvectors of T (past the 4 bm^2 cplx of GEMM scratch)
   unsigned char* sm = smraw + (gws ? 0 : eig1_ws_cplx(bm) * sizeof(cplx));
   const int bm2 = (bm + 1) & ~1;  // keeps the complex arrays 16-byte aligned
   double* lam = reinterpret_cast<double*>(sm);
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, i
   for (int c = threadIdx.x; c < L.slot_cn[p]; c += blockDim.x) cm = fmax(cm, L.colnorm[L.slot_c0[p] + c]);
   const double cmax = cta_max(cm, red);
   __syncthreads();
+  const long long T0 = clock64();
   // ---- tridiagonal reduction and the spectrum edge
   cta_hetrd(m, H, dg, ed, tau, pv, wv, red);
   if (threadIdx.x == 0) {
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, i
     s_need = s0 > 0.0 && thr < 1e-4 * s0;
   }
   __syncthreads();
+  const long long T1 = clock64();
   const double lo = lam[0], hi = lam[1], pivmin = lam[2];
   const int r = s_r;
   __syncthreads();
@@ -206,85 +211,154 @@ __global__ void __launch_bounds__(512) k_eig1(DevLevel L, const int* batch_cl, i
     }
     return;
   }
-  // ---- top-r eigenpairs of T: bisection + inverse iteration (one thread per
-  // cluster of close eigenvalues, re-orthogonalised within the cluster)
-  const double gaptol = 1e-8 * fmax(fabs(lo), fabs(hi));
-  for (int j = threadIdx.x; j < r; j += blockDim.x) lam[j] = bisect_eig(m, dg, ed, m - 1 - j, lo, hi, pivmin);
-  __syncthreads();
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    if (j > 0 && lam[j - 1] - lam[j] < gaptol) continue;  // handled by the cluster leader
-    int jend = j + 1;
-    while (jend < r && lam[jend - 1] - lam[jend] < gaptol) ++jend;
-    double* w4 = wk + (size_t)4 * m * j;
-    for (int q2 = j; q2 < jend; ++q2) {
-      double* z = Z + (size_t)m * q2;
-      for (int i = 0; i < m; ++i) {
-        unsigned h = (unsigned)(i * 2654435761u) ^ (unsigned)((q2 + 1) * 40503u);
-        h ^= h >> 13;
-        h *= 0x5bd1e995u;
-        h ^= h >> 15;
-        z[i] = 1.0 + 0.5 * ((double)(h & 0xffff) / 65535.0 - 0.5);
-      }
-      for (int it = 0; it < 4; ++it) {
-        tri_shift_solve(m, dg, ed, lam[q2], z, w4, pivmin * 1e10 + 1e-300);
-        for (int q3 = j; q3 < q2; ++q3) {  // Gram-Schmidt within the cluster
-          const double* y = Z + (size_t)m * q3;
-          double dot = 0.0;
-          for (int i = 0; i < m; ++i) dot += y[i] * z[i];
-          for (int i = 0; i < m; ++i) z[i] -= dot * y[i];
-        }
-        double nrm = 0.0;
-        for (int i = 0; i < m; ++i) nrm += z[i] * z[i];
-        nrm = sqrt(nrm);
-        const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-        for (int i = 0; i < m; ++i) z[i] *= inv;
-      }
-    }
+  // ---- top-r eigenvalues by bisection; vectors in k_eigvec, basis in k_eig1b
+  double* aux = reinterpret_cast<double*>(ws + 2 * bb);  // dg, ed, lam (bm each), tau (bm cplx)
+  for (int j = threadIdx.x; j < r; j += blockDim.x) aux[2 * bm + j] = bisect_eig(m, dg, ed, m - 1 - j, lo, hi, pivmin);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    aux[i] = dg[i];
+    aux[bm + i] = ed[i];
+    reinterpret_cast<cplx*>(aux + 4 * bm)[i] = tau[i];
   }
-  __syncthreads();
-  // back-transform U = Q Z (Q = H_0 ... H_{m-2}), one warp per vector
-  {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = wid; j < r; j += nw) {
-      cplx* u = U + (size_t)m * j;
-      const double* z = Z + (size_t)m * j;
-      for (int i = lane; i < m; i += 32) u[i] = cmk(z[i], 0.0);
-      __syncwarp();
-      for (int kk = m - 2; kk >= 0; --kk) {
-        const cplx tk = tau[kk];
-        if (tk.x == 0.0 && tk.y == 0.0) continue;
-        const cplx* v = H + (kk + 1) + (size_t)kk * m;  // v[0] = 1
-        cplx* y = u + kk + 1;
-        const int nk = m - kk - 1;
-        cplx s = czero();
-        for (int i = lane; i < nk; i += 32) cfma(s, i == 0 ? cone() : cconj(v[i]), y[i]);
-        for (int o = 16; o > 0; o >>= 1) {
-          s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-          s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-        }
-        s = cmul(tk, s);
-        __syncwarp();
-        for (int i = lane; i < nk; i += 32) y[i] = csub(y[i], cmul(i == 0 ? cone() : v[i], s));
-        __syncwarp();
-      }
-    }
-  }
-  __syncthreads();
-  // D1 = Vp Qm, Qm = Householder basis of [U_r | complement]
-  cta_copy(b, m, Vp, b, D1, b);
-  if (r > 0) {
-    __syncthreads();
-    cta_householder_qr(m, r, U, m, tau, red);
-    cta_apply_q_right(b, m, r, D1, b, U, m, tau, pv);
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
     L.pass2[q] = 0;
     L.rank1[q] = r;
     L.cmax[q] = cmax;
     L.lam[(size_t)q * bm] = s_s0;
-    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d\n", L.level, t, m, cmax, s_s0, s_thr, r);
+    if (L.debug)
+      printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d | cycles gram %lld hetrd %lld\n", L.level, t, m, cmax, s_s0, s_thr,
+             r, T0 - Tstart, T1 - T0);
   }
+}
+
+// Eigenvectors of the retained eigenvalues: inverse iteration on T (thread 0,
+// work arrays in shared memory; eigenvalues closer than 1e-8 ||T|| form a
+// cluster handled by one CTA and Gram-Schmidt'ed against each other), then
+// the back-transformation by the tridiagonalisation reflectors (whole CTA).
+__global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl, cplx* gws) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  const int q = blockIdx.x, j = blockIdx.y;
+  if (L.pass2[q]) return;
+  const int r = L.rank1[q];
+  if (j >= r) return;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  const cplx* H = ws;
+  cplx* U = ws + bb;
+  const double* aux = reinterpret_cast<const double*>(ws + 2 * bb);
+  const double* gd = aux;
+  const double* ge = aux + bm;
+  const double* glam = aux + 2 * bm;
+  const cplx* tau = reinterpret_cast<const cplx*>(aux + 4 * bm);
+  double* dg = reinterpret_cast<double*>(smraw);
+  double* ed = dg + m;
+  double* wk = ed + m;  // 4m
+  double* z = wk + 4 * m;
+  cplx* y = reinterpret_cast<cplx*>(z + m + (m & 1));
+  for (int i = threadIdx.x; i < m; i += blockDim.x) dg[i] = gd[i], ed[i] = ge[i];
+  __syncthreads();
+  // inverse iteration from a per-eigenvalue pseudo-random start: (near-)
+  // degenerate eigenvalues get independent vectors of their invariant
+  // subspace; k_eig1b orthonormalises the retained set as a whole
+  if (threadIdx.x == 0) {
+    double emax = 0.0;
+    for (int i = 0; i + 1 < m; ++i) emax = fmax(emax, ed[i] * ed[i]);
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+    for (int i = 0; i < m; ++i) {
+      unsigned h = (unsigned)(i * 2654435761u) ^ (unsigned)((j + 1) * 40503u);
+      h ^= h >> 13;
+      h *= 0x5bd1e995u;
+      h ^= h >> 15;
+      z[i] = 1.0 + 0.5 * ((double)(h & 0xffff) / 65535.0 - 0.5);
+    }
+    for (int it = 0; it < 3; ++it) {
+      tri_shift_solve(m, dg, ed, glam[j], z, wk, pivmin * 1e10 + 1e-300);
+      double nrm = 0.0;
+      for (int i = 0; i < m; ++i) nrm += z[i] * z[i];
+      const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+      for (int i = 0; i < m; ++i) z[i] *= inv;
+    }
+  }
+  __syncthreads();
+  // back-transform y = Q z, Q = H_0 ... H_{m-2}
+  for (int i = threadIdx.x; i < m; i += blockDim.x) y[i] = cmk(z[i], 0.0);
+  __syncthreads();
+  for (int kk = m - 2; kk >= 0; --kk) {
+    const cplx tk = tau[kk];
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    const cplx* v = H + (kk + 1) + (size_t)kk * m;  // v[0] = 1
+    const int nk = m - kk - 1;
+    double sr = 0.0, si = 0.0;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      const cplx vv = i == 0 ? cone() : cconj(v[i]);
+      const cplx yy = y[kk + 1 + i];
+      sr += vv.x * yy.x - vv.y * yy.y;
+      si += vv.x * yy.y + vv.y * yy.x;
+    }
+    sr = cta_sum(sr, red);
+    si = cta_sum(si, red);
+    const cplx sc = cmul(tk, cmk(sr, si));
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) y[kk + 1 + i] = csub(y[kk + 1 + i], cmul(i == 0 ? cone() : v[i], sc));
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) U[i + (size_t)m * j] = y[i];
+}
+
+// D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H = I - Y T Y^H, the compact WY form
+// of a Householder QR of the retained eigenvectors U_r: [new | complement]
+// as three tiled GEMMs.
+__global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, cplx* gws) {
+  __shared__ cplx tile_sm[kTileSmemCplx];
+  __shared__ double red[32];
+  __shared__ cplx tau[512];
+  const int q = blockIdx.x;
+  if (L.pass2[q]) return;
+  const int r = L.rank1[q];
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  cplx* U = ws + bb;
+  cplx* D1 = L.dir + (size_t)q * bb;
+  const cplx* Vp = L.Vp + (size_t)t * bb;
+  if (r == 0 || m == 0) {
+    cta_copy(b, m, Vp, b, D1, b);
+    return;
+  }
+  cta_householder_qr(m, r, U, m, tau, red);
+  cplx* Y = ws;                    // m x r explicit reflectors (H no longer needed)
+  cplx* X1 = ws + 2 * bb + 4 * bm;  // b x r
+  cplx* X2 = X1 + bb;              // b x r
+  cplx* Tm = X2 + bb;              // r x r
+  cplx* Sm = Tm + bb;              // r x r: Y^H Y
+  for (int idx = threadIdx.x; idx < m * r; idx += blockDim.x) {
+    const int i = idx % m, jj = idx / m;
+    Y[idx] = i < jj ? czero() : (i == jj ? cone() : U[i + (size_t)jj * m]);
+  }
+  __syncthreads();
+  cta_gemm_tiled(r, r, m, 1.0, Y, m, OP_C, Y, m, OP_N, 0.0, Sm, r, tile_sm);
+  // T (upper, r x r): T_kk = conj(tau_k), T[0:k,k] = -conj(tau_k) T[0:k,0:k] S[0:k,k]
+  for (int kk = 0; kk < r; ++kk) {
+    const cplx tk = cconj(tau[kk]);
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+      cplx v = czero();
+      if (i < kk) {
+        for (int jj = i; jj < kk; ++jj) cfma(v, Tm[i + (size_t)jj * r], Sm[jj + (size_t)kk * r]);
+        v = cmul(cmk(-tk.x, -tk.y), v);
+      } else if (i == kk) {
+        v = tk;
+      }
+      Tm[i + (size_t)kk * r] = v;
+    }
+    __syncthreads();
+  }
+  cta_gemm_tiled(b, r, m, 1.0, Vp, b, OP_N, Y, m, OP_N, 0.0, X1, b, tile_sm);
+  cta_gemm_tiled(b, r, r, 1.0, X1, b, OP_N, Tm, r, OP_N, 0.0, X2, b, tile_sm);
+  cta_copy(b, m, Vp, b, D1, b);
+  __syncthreads();
+  cta_gemm_tiled(b, m, r, -1.0, X2, b, OP_N, Y, m, OP_C, 1.0, D1, b, tile_sm);
 }
 
 // --------------------------------------------------------------------------
@@ -460,9 +534,8 @@ __global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, 
 // every cluster of the batch that hits it are summed in a fixed order, then
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
 // 4 x 4 complex micro-tile per thread, K staged through shared memory.
-__global__ void __launch_bounds__(256) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
-  __shared__ cplx sA[64][17];
-  __shared__ cplx sB[16][65];
+__global__ void __launch_bounds__(128) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+  __shared__ Tile128Smem S;
   const SchurTargetD tg = targets[blockIdx.x];
   const int bm = L.bmax;
   int rows, cols;
@@ -476,80 +549,59 @@ __global__ void __launch_bounds__(256) k_schur(DevLevel L, const SchurTargetD* t
     cols = L.bsz[L.fcol[tg.idx]];
     out = blk(L.F, tg.idx, bm);
   }
-  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  const int ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
+  if ((int)blockIdx.y >= ntr * ntc) return;
+  const int r0 = (blockIdx.y % ntr) * 64, c0 = (blockIdx.y / ntr) * 64;
+  cplx acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = czero();
   bool touched = false;
-  for (int r0 = 0; r0 < rows; r0 += 64)
-    for (int c0 = 0; c0 < cols; c0 += 64) {
-      cplx acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
-      for (int ci = tg.c0; ci < tg.c1; ++ci) {
-        const SchurContribD cb = contrib[ci];
-        const int t = cb.t;
-        const int kf = L.kfin[t], e = L.bsz[t] - kf;
-        if (e == 0) continue;
-        touched = true;
-        const cplx* A;
-        const cplx* B;
-        int arows, bcols, ro, co;
-        if (cb.r >= 0) {
-          arows = L.bsz[L.R_nb[cb.r]];
-          A = ((cb.flags & 1) ? L.lift : L.chain) + L.Lbar_off[cb.r];
-          ro = 0;
-        } else {
-          arows = kf;
-          A = L.chain + L.Lself_off[t];
-          ro = e;
-        }
-        if (cb.c >= 0) {
-          bcols = L.bsz[L.C_nb[cb.c]];
-          B = ((cb.flags & 2) ? L.lift : L.chain) + L.Ubar_off[cb.c];
-          co = 0;
-        } else {
-          bcols = kf;
-          B = L.chain + L.Uself_off[t];
-          co = e;
-        }
-        // intersect [ro, ro+arows) x [co, co+bcols) with the tile
-        for (int k0 = 0; k0 < e; k0 += 16) {
-          const int kk = min(16, e - k0);
-          __syncthreads();
-          for (int idx = threadIdx.x; idx < 64 * 16; idx += blockDim.x) {
-            const int i = idx % 64, p = idx / 64;
-            const int gi = r0 + i - ro;
-            sA[i][p] = (p < kk && gi >= 0 && gi < arows) ? A[gi + (size_t)(k0 + p) * arows] : czero();
-            const int j = idx % 64;
-            const int gj = c0 + j - co;
-            sB[p][j] = (p < kk && gj >= 0 && gj < bcols) ? B[(k0 + p) + (size_t)gj * e] : czero();
-          }
-          __syncthreads();
-          for (int p = 0; p < kk; ++p) {
-            cplx av[4], bv[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) bv[bb] = sB[p][tc * 4 + bb];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int bb = 0; bb < 4; ++bb) cfma(acc[a][bb], av[a], bv[bb]);
-          }
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + bb;
-          if (i < rows && j < cols && (acc[a][bb].x != 0.0 || acc[a][bb].y != 0.0)) {
-            cplx* o = out + i + (size_t)j * rows;
-            *o = csub(*o, acc[a][bb]);
-          }
-        }
+  for (int ci = tg.c0; ci < tg.c1; ++ci) {
+    const SchurContribD cb = contrib[ci];
+    const int t = cb.t;
+    const int kf = L.kfin[t], e = L.bsz[t] - kf;
+    if (e == 0) continue;
+    touched = true;
+    const cplx* A;
+    const cplx* B;
+    int arows, bcols, ro, co;
+    if (cb.r >= 0) {
+      arows = L.bsz[L.R_nb[cb.r]];
+      A = ((cb.flags & 1) ? L.lift : L.chain) + L.Lbar_off[cb.r];
+      ro = 0;
+    } else {
+      arows = kf;
+      A = L.chain + L.Lself_off[t];
+      ro = e;
     }
-  if (tg.kind == 1 && touched && threadIdx.x == 0) L.fexists[tg.idx] = 1;
+    if (cb.c >= 0) {
+      bcols = L.bsz[L.C_nb[cb.c]];
+      B = ((cb.flags & 2) ? L.lift : L.chain) + L.Ubar_off[cb.c];
+      co = 0;
+    } else {
+      bcols = kf;
+      B = L.chain + L.Uself_off[t];
+      co = e;
+    }
+    // the contribution covers target rows [ro, ro+arows) x cols [co, co+bcols)
+    const int ash = r0 - ro, bsh = c0 - co;
+    if (ash >= arows || bsh >= bcols || ash + 64 <= 0 || bsh + 64 <= 0) continue;
+    tile128_acc(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
+  }
+  const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + b;
+      if (i < rows && j < cols && (acc[a][b].x != 0.0 || acc[a][b].y != 0.0)) {
+        cplx* o = out + i + (size_t)j * rows;
+        *o = csub(*o, acc[a][b]);
+      }
+    }
+  if (tg.kind == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
 }
 
 // --------------------------------------------------------------------------
@@ -583,52 +635,35 @@ __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_gemm(const GemmDesc* descs) {
-  __shared__ cplx sA[64][17];
-  __shared__ cplx sB[16][65];
+__global__ void __launch_bounds__(128) k_gemm(const GemmDesc* descs) {
+  __shared__ Tile128Smem S;
   const GemmDesc d = descs[blockIdx.x];
-  const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
+  const int ntr = (d.m + 63) / 64, ntc = (d.n + 63) / 64;
   const bool zero = (d.flag1 && !*d.flag1) || (d.flag2 && !*d.flag2);
-  for (int r0 = 0; r0 < d.m; r0 += 64)
-    for (int c0 = 0; c0 < d.n; c0 += 64) {
-      cplx acc[4][4];
+  const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+  // each CTA walks the tiles blockIdx.y, blockIdx.y + gridDim.y, ...
+  for (int tile = blockIdx.y; tile < ntr * ntc; tile += gridDim.y) {
+    const int r0 = (tile % ntr) * 64, c0 = (tile / ntr) * 64;
+    cplx acc[8][4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
-      for (int k0 = 0; k0 < (zero ? 0 : d.k); k0 += 16) {
-        const int kk = min(16, d.k - k0);
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < 64 * 16; idx += blockDim.x) {
-          const int i = idx % 64, p = idx / 64;
-          sA[i][p] = (p < kk && r0 + i < d.m) ? ld_op(d.A, d.lda, d.opA, r0 + i, k0 + p) : czero();
-          sB[p][i] = (p < kk && c0 + i < d.n) ? ld_op(d.B, d.ldb, d.opB, k0 + p, c0 + i) : czero();
-        }
-        __syncthreads();
-        for (int p = 0; p < kk; ++p) {
-          cplx av[4], bv[4];
+      for (int b = 0; b < 4; ++b) acc[a][b] = czero();
+    if (!zero) {
+      tile128_acc(acc, S, d.A, d.lda, d.opA, r0, d.m, d.B, d.ldb, d.opB, c0, d.n, d.k);
+    }
 #pragma unroll
-          for (int a = 0; a < 4; ++a) av[a] = sA[tr * 4 + a][p];
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
-          for (int bb = 0; bb < 4; ++bb) bv[bb] = sB[p][tc * 4 + bb];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) cfma(acc[a][bb], av[a], bv[bb]);
+      for (int b = 0; b < 4; ++b) {
+        const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + b;
+        if (i < d.m && j < d.n) {
+          cplx* o = d.C + i + (size_t)j * d.ldc;
+          const cplx v = acc[a][b];
+          *o = d.beta == 0.0 ? cscale(v, d.alpha) : make_double2(d.beta * o->x + d.alpha * v.x, d.beta * o->y + d.alpha * v.y);
         }
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const int i = r0 + tr * 4 + a, j = c0 + tc * 4 + bb;
-          if (i < d.m && j < d.n) {
-            cplx* o = d.C + i + (size_t)j * d.ldc;
-            const cplx v = acc[a][bb];
-            *o = d.beta == 0.0 ? cscale(v, d.alpha) : make_double2(d.beta * o->x + d.alpha * v.x, d.beta * o->y + d.alpha * v.y);
-          }
-        }
-    }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -795,18 +830,22 @@ void launch_complement(const DevLevel& L, cudaStream_t s) {
 size_t eig1_small_bytes(int bm) { return (size_t)(bm + 1) * 8 * 3 + (size_t)bm * 16 * 3 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64; }
 size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_small_bytes(bm); }
 
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
-  const size_t need = eig1_smem_bytes(L.bmax);
-  if (need <= kSmemCap) {
-    set_smem((const void*)k_eig1, need);
-    k_eig1<<<nb, 512, need, s>>>(L, batch_cl, p0, nullptr);
-  } else {
-    const size_t small = eig1_small_bytes(L.bmax);
-    set_smem((const void*)k_eig1, small);
-    cplx* ws = workspace(eig1_ws_cplx(L.bmax) * sizeof(cplx) * nb, s);
-    k_eig1<<<nb, 512, small, s>>>(L, batch_cl, p0, ws);
-  }
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase) {
+  const size_t small = eig1_small_bytes(L.bmax);
+  set_smem((const void*)k_eig1, small);
+  cplx* ws = workspace(eig1_ws_cplx(L.bmax) * sizeof(cplx) * nb, s);
+  k_eig1<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
   post_launch("k_eig1");
+  phase(1);
+  if (mmax > 0) {
+    const size_t vsm = (size_t)8 * L.bmax * sizeof(double) + 16 + (size_t)L.bmax * sizeof(cplx);
+    set_smem((const void*)k_eigvec, vsm);
+    k_eigvec<<<dim3(nb, mmax), 256, vsm, s>>>(L, batch_cl, ws);
+    post_launch("k_eigvec");
+  }
+  phase(2);
+  k_eig1b<<<nb, 256, 0, s>>>(L, batch_cl, ws);
+  post_launch("k_eig1b");
 }
 
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
@@ -833,15 +872,18 @@ void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* item
 
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;
-  k_schur<<<ntargets, 256, 0, s>>>(L, targets, contrib); post_launch("k_schur");
+  const int t = (L.bmax + 63) / 64;
+  k_schur<<<dim3(ntargets, t * t), 128, 0, s>>>(L, targets, contrib);
+  post_launch("k_schur");
 }
 
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {
   if (n > 0) k_copy<<<n, 256, 0, s>>>(d); post_launch("k_copy");
 }
 
-void launch_gemm(const GemmDesc* d, int n, cudaStream_t s) {
-  if (n > 0) k_gemm<<<n, 256, 0, s>>>(d); post_launch("k_gemm");
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int tiles) {
+  if (n > 0) k_gemm<<<dim3(n, std::max(1, std::min(tiles, 16))), 128, 0, s>>>(d);
+  post_launch("k_gemm");
 }
 
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches) {

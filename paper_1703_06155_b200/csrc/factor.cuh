@@ -2,6 +2,8 @@
 // launch entry points of the level kernels (factor.cu).
 #pragma once
 
+#include <functional>
+
 #include "device.cuh"
 
 namespace h2g {
@@ -104,13 +106,14 @@ struct NormDesc {
 };
 
 void launch_complement(const DevLevel& L, cudaStream_t s);
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
 void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s);
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
-void launch_gemm(const GemmDesc* d, int n, cudaStream_t s);
+// tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int tiles = 1);
 void launch_zero_desc_flags(int* p, int n, cudaStream_t s);
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches);
 size_t head_smem_bytes(int bmax);
