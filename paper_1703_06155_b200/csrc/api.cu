@@ -754,7 +754,23 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               for (int f = Y.G_ptr[t]; f < Y.G_ptr[t + 1]; ++f, ++c) gN[c].trans = Y.G_tr[f];
             }
         }
-        DBuf dA1, dA2, dB1, dB2, dN;
+        // diagonal-block rotation Dii <- Qt^H Dii conj(Qt) as descriptor GEMMs (:345-347)
+        DBuf rotbuf;
+        rotbuf.alloc((size_t)mb * bb * 16, st);
+        std::vector<GemmDesc> gR1, gR2;
+        for (int bi = 0; bi < nbat0; ++bi)
+          for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) {
+            const int q = p - SC.batch_ptr[bi], t = SC.batch_cl[p];
+            const int b = cur.bsz[t];
+            cplx* Tq = rotbuf.as<cplx>() + (size_t)q * bb;
+            cplx* Dtt = cur.D.as<cplx>() + (size_t)Y.diag_blk[t] * bb;
+            const cplx* Qt = CL->arena.as<cplx>() + Qt_off[t];
+            gR1.push_back({Qt, Dtt, Tq, b, b, b, b, b, b, OP_C, OP_N, 1.0, 0.0, nullptr, nullptr});
+            gR2.push_back({Tq, Qt, Dtt, b, b, b, b, b, b, OP_N, OP_R, 1.0, 0.0, nullptr, nullptr});
+          }
+        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2;
+        upload(dR1, gR1, st);
+        upload(dR2, gR2, st);
         upload(dA1, gA1, st);
         upload(dA2, gA2, st);
         upload(dB1, gB1, st);
@@ -854,6 +870,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           pf.end(st);
           pf.begin(PC_HEAD, st);
           launch_head(DL, d_bat + p0, p0, nb, st);
+          launch_gemm(dR1.as<GemmDesc>() + p0, nb, st, tl);
+          launch_gemm(dR2.as<GemmDesc>() + p0, nb, st, tl);
+          launch_head2(DL, d_bat + p0, nb, st);
           pf.end(st);
           pf.begin(PC_PANEL, st);
           launch_panel(DL, d_bat + p0, d_pan + W.panel_ptr[bi], W.panel_ptr[bi + 1] - W.panel_ptr[bi], st);
@@ -864,10 +883,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
           C->klaunch[PC_COLNORM] += nn > 0;
           C->klaunch[PC_EIG1] += 3;
-          C->klaunch[PC_HEAD] += 1;
+          C->klaunch[PC_HEAD] += 4;
           C->klaunch[PC_PANEL] += W.panel_ptr[bi + 1] > W.panel_ptr[bi];
           C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
-          launches += 4 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
+          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
         }
         const double t_launched = wall();
         CK(cudaGetLastError());

@@ -714,3 +714,118 @@ __device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, c
 }
 
 }  // namespace h2g
+
+namespace h2g {
+
+// ---------------------------------------------------------------------------
+// Blocked (panel 32) unpivoted LU in place, A n x n (ld lda). Same pivot rule
+// and order of pivots as the right-looking reference (dense_kernels.hpp:70-93);
+// trailing updates are tiled GEMMs. Returns -1 or the failing pivot index.
+__device__ inline int cta_lu_blocked(int n, cplx* A, int lda, double tol, double* pmag, double* red, cplx* tile_sm) {
+  double mx = 0.0;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) mx = fmax(mx, cabsd(A[(idx % n) + (size_t)(idx / n) * lda]));
+  const double scale = cta_max(mx, red);
+  if (n > 0 && scale == 0.0) {
+    *pmag = 0.0;
+    return 0;
+  }
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int kb = min(32, n - j0), je = j0 + kb;
+    for (int k = j0; k < je; ++k) {
+      const cplx piv = A[k + (size_t)k * lda];
+      const double pa = cabsd(piv);
+      if (pa < tol * scale) {
+        *pmag = pa;
+        return k;
+      }
+      for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + (size_t)k * lda] = cdiv(A[i + (size_t)k * lda], piv);
+      __syncthreads();
+      const int nc = je - k - 1, nr = n - k - 1;
+      for (int idx = threadIdx.x; idx < nr * nc; idx += blockDim.x) {
+        const int i = k + 1 + idx % nr, j = k + 1 + idx / nr;
+        cplx a = A[i + (size_t)j * lda];
+        const cplx l = A[i + (size_t)k * lda], u = A[k + (size_t)j * lda];
+        a.x -= l.x * u.x - l.y * u.y;
+        a.y -= l.x * u.y + l.y * u.x;
+        A[i + (size_t)j * lda] = a;
+      }
+      __syncthreads();
+    }
+    if (je < n) {
+      // U12 = L11^{-1} A[j0:je, je:n] (unit lower), one thread per column
+      for (int c = je + threadIdx.x; c < n; c += blockDim.x) {
+        cplx* x = A + j0 + (size_t)c * lda;
+        for (int i = 1; i < kb; ++i) {
+          cplx s = x[i];
+          for (int p = 0; p < i; ++p) {
+            const cplx l = A[j0 + i + (size_t)(j0 + p) * lda];
+            s.x -= l.x * x[p].x - l.y * x[p].y;
+            s.y -= l.x * x[p].y + l.y * x[p].x;
+          }
+          x[i] = s;
+        }
+      }
+      __syncthreads();
+      cta_gemm_tiled(n - je, n - je, kb, -1.0, A + je + (size_t)j0 * lda, lda, OP_N, A + j0 + (size_t)je * lda, lda, OP_N, 1.0,
+                     A + je + (size_t)je * lda, lda, tile_sm);
+    }
+  }
+  return -1;
+}
+
+// X = L^{-1} for the unit-lower factor packed in LU (n x n, ld ldl); X ld ldx.
+__device__ inline void cta_inv_unit_lower(int n, const cplx* LU, int ldl, cplx* X, int ldx, cplx* tile_sm) {
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) X[(idx % n) + (size_t)(idx / n) * ldx] = czero();
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int kb = min(32, n - j0), je = j0 + kb;
+    if (j0 > 0) cta_gemm_tiled(kb, j0, j0, -1.0, LU + j0, ldl, OP_N, X, ldx, OP_N, 0.0, X + j0, ldx, tile_sm);
+    for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+      const int i = idx % kb, c = idx / kb;
+      X[j0 + i + (size_t)(j0 + c) * ldx] = i == c ? cone() : czero();
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < je; c += blockDim.x) {
+      cplx* x = X + j0 + (size_t)c * ldx;
+      for (int i = 1; i < kb; ++i) {
+        cplx s = x[i];
+        for (int p = 0; p < i; ++p) {
+          const cplx l = LU[j0 + i + (size_t)(j0 + p) * ldl];
+          s.x -= l.x * x[p].x - l.y * x[p].y;
+          s.y -= l.x * x[p].y + l.y * x[p].x;
+        }
+        x[i] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Y = U^{-1} for the upper factor packed in LU; W: n x 32 scratch (ld n).
+__device__ inline void cta_inv_upper(int n, const cplx* LU, int ldu, cplx* Y, int ldy, cplx* W, cplx* tile_sm) {
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Y[(idx % n) + (size_t)(idx / n) * ldy] = czero();
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int kb = min(32, n - j0);
+    // Y[J,J] = U_JJ^{-1}, one thread per column
+    for (int c = threadIdx.x; c < kb; c += blockDim.x) {
+      cplx* y = Y + j0 + (size_t)(j0 + c) * ldy;
+      for (int i = c; i >= 0; --i) {
+        cplx s = i == c ? cone() : czero();
+        for (int p = i + 1; p <= c; ++p) {
+          const cplx u = LU[j0 + i + (size_t)(j0 + p) * ldu];
+          s.x -= u.x * y[p].x - u.y * y[p].y;
+          s.y -= u.x * y[p].y + u.y * y[p].x;
+        }
+        y[i] = cdiv(s, LU[j0 + i + (size_t)(j0 + i) * ldu]);
+      }
+    }
+    __syncthreads();
+    if (j0 > 0) {
+      cta_gemm_tiled(j0, kb, j0, 1.0, Y, ldy, OP_N, LU + (size_t)j0 * ldu, ldu, OP_N, 0.0, W, n, tile_sm);
+      cta_gemm_tiled(j0, kb, kb, -1.0, W, n, OP_N, Y + j0 + (size_t)j0 * ldy, ldy, OP_N, 0.0, Y + (size_t)j0 * ldy, ldy, tile_sm);
+    }
+  }
+}
+
+}  // namespace h2g

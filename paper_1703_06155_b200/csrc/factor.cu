@@ -444,46 +444,58 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
     Qt[i + (size_t)j * b] = v;
   }
   __syncthreads();
-  // rotate the diagonal block: Dii <- Qt^H Dii conj(Qt) (:345-347)
-  cplx* gD = blk(L.D, L.diag_blk[t], bm);
-  cta_gemm_tiled(b, b, b, 1.0, Qt, b, OP_C, gD, b, OP_N, 0.0, T, b, sm);
-  cta_gemm_tiled(b, b, b, 1.0, T, b, OP_N, Qt, b, OP_R, 0.0, Dd, b, sm);
-  if (e > 0) {
-    cplx* LU = Hc;
-    cta_copy(e, e, Dd, b, LU, e);
-    __syncthreads();
-    double pmag = 0.0;
-    const int fail = cta_lu_nopiv(e, LU, e, 1e-13, &pmag, red);
-    if (fail >= 0) {
-      if (threadIdx.x == 0) raise_error(L.err, 4, cid, L.level, fail, pmag);
-      return;
-    }
-    cplx* L11 = L.chain + L.L11_off[t];
-    cplx* U11 = L.chain + L.U11_off[t];
-    for (int idx = threadIdx.x; idx < e * e; idx += blockDim.x) {
-      const int i = idx % e, j = idx / e;
-      const cplx v = LU[idx];
-      L11[idx] = i > j ? v : (i == j ? cone() : czero());
-      U11[idx] = i <= j ? v : czero();
-    }
-    cplx* Li = L.chain + L.Linv_off[t];
-    cplx* Ui = L.chain + L.Uinv_off[t];
-    cta_tri_inverses(e, LU, e, Li, Ui);
-    __syncthreads();
-    if (kf > 0) {
-      cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
-      cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
-      cta_gemm_tiled(e, kf, e, 1.0, Li, e, OP_N, Dd + (size_t)e * b, b, OP_N, 0.0, Us, e, sm);
-      cta_gemm_tiled(kf, e, e, 1.0, Dd + e, b, OP_N, Ui, e, OP_N, 0.0, Ls, kf, sm);
-      cta_gemm_tiled(kf, kf, e, -1.0, Ls, kf, OP_N, Us, e, OP_N, 1.0, Dd + e + (size_t)e * b, b, sm);
-    }
-    for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
-      const int i = idx % b, j = idx / b;
-      if (i < e || j < e) Dd[i + (size_t)j * b] = (i == j) ? cone() : czero();
-    }
-    __syncthreads();
+}
+
+// Step 3a after the diagonal block was rotated (descriptor GEMMs between
+// k_head and this kernel): blocked unpivoted LU of the leading e x e block
+// with the 1e-13 relative pivot test (dense_kernels.hpp:70-93,
+// factorization.hpp:390-398), blocked triangular inverses, self panels and the
+// self Schur product (:409-420), head set to identity (:431-435).
+__global__ void __launch_bounds__(256) k_head2(DevLevel L, const int* batch_cl, cplx* gws) {
+  __shared__ cplx sm[kTileSmemCplx];
+  __shared__ double red[32];
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], kf = L.kfin[t], e = b - kf, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
+  const int cid = (1 << L.level) - 1 + t;
+  cplx* ws = gws + (size_t)q * 2 * bb;
+  cplx* LU = ws;        // e x e (ld e)
+  cplx* W = ws + bb;    // e x 32 scratch
+  cplx* Dd = blk(L.D, L.diag_blk[t], bm);  // rotated diagonal block (ld b)
+  if (e == 0) return;
+  cta_copy(e, e, Dd, b, LU, e);
+  __syncthreads();
+  double pmag = 0.0;
+  const int fail = cta_lu_blocked(e, LU, e, 1e-13, &pmag, red, sm);
+  if (fail >= 0) {
+    if (threadIdx.x == 0) raise_error(L.err, 4, cid, L.level, fail, pmag);
+    return;
   }
-  cta_copy(b, b, Dd, b, gD, b);
+  __syncthreads();
+  cplx* L11 = L.chain + L.L11_off[t];
+  cplx* U11 = L.chain + L.U11_off[t];
+  for (int idx = threadIdx.x; idx < e * e; idx += blockDim.x) {
+    const int i = idx % e, j = idx / e;
+    const cplx v = LU[idx];
+    L11[idx] = i > j ? v : (i == j ? cone() : czero());
+    U11[idx] = i <= j ? v : czero();
+  }
+  cplx* Li = L.chain + L.Linv_off[t];
+  cplx* Ui = L.chain + L.Uinv_off[t];
+  cta_inv_unit_lower(e, LU, e, Li, e, sm);
+  cta_inv_upper(e, LU, e, Ui, e, W, sm);
+  if (kf > 0) {
+    cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
+    cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
+    cta_gemm_tiled(e, kf, e, 1.0, Li, e, OP_N, Dd + (size_t)e * b, b, OP_N, 0.0, Us, e, sm);
+    cta_gemm_tiled(kf, e, e, 1.0, Dd + e, b, OP_N, Ui, e, OP_N, 0.0, Ls, kf, sm);
+    cta_gemm_tiled(kf, kf, e, -1.0, Ls, kf, OP_N, Us, e, OP_N, 1.0, Dd + e + (size_t)e * b, b, sm);
+  }
+  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    if (i < e || j < e) Dd[i + (size_t)j * b] = (i == j) ? cone() : czero();
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -855,6 +867,12 @@ void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStr
   cplx* ws = workspace(4 * (size_t)bm * bm * sizeof(cplx) * nb, s);
   k_head<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
   post_launch("k_head");
+}
+
+void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
+  cplx* ws = workspace(2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb, s);
+  k_head2<<<nb, 256, 0, s>>>(L, batch_cl, ws);
+  post_launch("k_head2");
 }
 
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {

@@ -109,6 +109,7 @@ void launch_complement(const DevLevel& L, cudaStream_t s);
 void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
+void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
 void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s);
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
