@@ -6,6 +6,8 @@
 //   k_panel  step 2 + step 3b: rotate row/column blocks, Lbar/Ubar panels
 //   k_schur  step 3c: Schur products scattered to dense / fill-in targets
 // Reference: proj/include/h2lu/factorization.hpp:260-440.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -84,34 +86,45 @@ __host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm 
 // is requested: the stack is re-projected on the pass-1 directions
 // (D1 = Vp U1) and eigendecomposed again (k_head), which resolves singular
 // values down to ~eps_mach * sigma_0 like the reference's QR + SVD.
-__global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+// Step 0, pass 1 on a 16-CTA thread-block cluster. The m x m Gram of the
+// projected fill stack is distributed column-cyclically over the CTAs' shared
+// memory (column c lives in CTA c % 16); the Householder tridiagonalization
+// (zhetd2 scheme) runs with two cluster barriers per column: the owner of
+// column k builds the reflector, every CTA forms its partial A v over its own
+// columns, the partials are reduced through distributed shared memory and
+// each CTA applies the rank-2 update to its own columns. CTA 0 then counts the
+// eigenvalues above thr^2 (Sturm) and bisects the retained ones; vectors are
+// formed by k_eigvec, the basis by k_eig1b. Threshold rule: factorization.hpp:
+// 295-298 / h2_matrix.hpp:287-290.
+constexpr int kHC = 16;
+
+__device__ inline size_t eig1c_smem(int m) {
+  const int ncl = (m + kHC - 1) / kHC;
+  return (size_t)m * ncl * sizeof(cplx) + (size_t)m * sizeof(cplx) * 6 + 256;
+}
+
+__global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ cplx tile_sm[kTileSmemCplx];
   __shared__ double red[32];
-  __shared__ int s_any, s_r, s_need;
-  __shared__ double s_s0, s_thr;
-  const long long Tstart = clock64();
-  const int q = blockIdx.x, p = p0 + q;
+  __shared__ int s_any;
+  __shared__ cplx s_tau[2];
+  __shared__ int s_skip[2];
+  const int rank = (int)cl.block_rank();
+  const int q = blockIdx.x / kHC, p = p0 + q;
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
   const size_t bb = (size_t)bm * bm;
-  cplx* ws = gws ? gws + (size_t)q * eig1_ws_cplx(bm) : reinterpret_cast<cplx*>(smraw);
-  cplx* H = ws;               // m x m
-  cplx* U = ws + bb;          // m x m (Jacobi vectors / retained eigenvectors)
-  double* wk = reinterpret_cast<double*>(ws + 2 * bb);  // 4 m r doubles (inverse iteration)
-  double* Z = wk + 8 * bb;    // m x r real eigenvectors of T (past the 4 bm^2 cplx of GEMM scratch)
-  unsigned char* sm = smraw + (gws ? 0 : eig1_ws_cplx(bm) * sizeof(cplx));
-  const int bm2 = (bm + 1) & ~1;  // keeps the complex arrays 16-byte aligned
-  double* lam = reinterpret_cast<double*>(sm);
-  double* dg = lam + bm2;
-  double* ed = dg + bm2;
-  cplx* tau = reinterpret_cast<cplx*>(ed + bm2);
-  cplx* pv = tau + bm;
-  cplx* wv = pv + bm;
-  int* ord = reinterpret_cast<int*>(wv + bm);
-  int* pr = ord + bm;
-  double* rot = reinterpret_cast<double*>(pr + bm + 2);
-
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  cplx* H = ws;  // reflectors out (m x m, ld m)
+  double* aux = reinterpret_cast<double*>(ws + 2 * bb);
+  const int ncl = (m + kHC - 1) / kHC;
+  cplx* Hl = reinterpret_cast<cplx*>(smraw);  // m x ncl local columns (col c = rank + kHC * jl)
+  cplx* vbuf = Hl + (size_t)m * ncl;          // [2][m] reflector broadcast (owner)
+  cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v
+  cplx* vv = pbuf + 2 * m;                    // local copy of v
+  cplx* wv = vv + m;                          // local w
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   {
@@ -120,27 +133,132 @@ __global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, i
     if (any) s_any = 1;
   }
   __syncthreads();
-  cplx* D1 = L.dir + (size_t)q * bb;
-  const cplx* Vp = L.Vp + (size_t)t * bb;
   if (!s_any || m == 0) {
     // no fill-in: the basis stays (factorization.hpp:276)
-    cta_copy(b, m, Vp, b, D1, b);
-    if (threadIdx.x == 0) L.pass2[q] = 0, L.rank1[q] = 0, L.cmax[q] = 0.0, L.lam[(size_t)q * bm] = 0.0;
-    return;
+    if (rank == 0 && threadIdx.x == 0) L.pass2[q] = 0, L.rank1[q] = 0, L.cmax[q] = 0.0, L.lam[(size_t)q * bm] = 0.0;
+    return;  // uniform over the cluster
   }
   const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
-  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
+    const int i = idx % m, jl = idx / m, c = rank + kHC * jl;
     cplx s = czero();
-    for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
-    H[idx] = s;
+    if (c < m)
+      for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + i + (size_t)c * m]);
+    Hl[idx] = s;
   }
+  cl.sync();
+  for (int kk = 0; kk + 1 < m; ++kk) {
+    const int owner = kk % kHC, buf = kk & 1;
+    const int nk = m - kk - 1;
+    if (rank == owner) {
+      cplx* x = Hl + (kk + 1) + (size_t)(kk / kHC) * m;
+      double part = 0.0;
+      for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) part += cabs2(x[i]);
+      const double xn2 = cta_sum(part, red);
+      __shared__ cplx s_scale;
+      __shared__ double s_beta;
+      if (threadIdx.x == 0) {
+        const cplx al = x[0];
+        if (xn2 == 0.0 && al.y == 0.0) {
+          s_skip[buf] = 1;
+          s_tau[buf] = czero();
+          s_beta = al.x;
+        } else {
+          double beta = sqrt(cabs2(al) + xn2);
+          if (al.x >= 0.0) beta = -beta;
+          s_skip[buf] = 0;
+          s_beta = beta;
+          s_tau[buf] = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
+          s_scale = cdiv(cone(), csub(al, cmk(beta, 0.0)));
+        }
+        aux[kk] = Hl[kk + (size_t)(kk / kHC) * m].x;  // d_k
+        aux[bm + kk] = s_beta;                         // e_k
+        reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = s_tau[buf];
+      }
+      __syncthreads();
+      if (!s_skip[buf])
+        for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) x[i] = cmul(x[i], s_scale);
+      __syncthreads();
+      cplx* vb = vbuf + (size_t)buf * m;
+      for (int i = threadIdx.x; i < nk; i += blockDim.x) vb[i] = i == 0 ? cone() : x[i];
+    }
+    cl.sync();  // S1: reflector published
+    const int* oskip = cl.map_shared_rank(s_skip, owner);
+    if (oskip[buf]) continue;  // uniform: every CTA reads the same flag
+    const cplx tk = cl.map_shared_rank(s_tau, owner)[buf];
+    const cplx* ovb = cl.map_shared_rank(vbuf, owner) + (size_t)buf * m;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) vv[i] = ovb[i];
+    __syncthreads();
+    // partial p over own columns c > kk (local rows kk+1 .. m-1)
+    cplx* pb = pbuf + (size_t)buf * m;
+    {
+      const int jl0 = (kk + 1 - rank + kHC - 1) / kHC;  // first local column with c > kk
+      for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+        cplx sacc = czero();
+        for (int jl = max(jl0, 0); jl < ncl; ++jl) {
+          const int c = rank + kHC * jl;
+          if (c >= m) break;
+          cfma(sacc, Hl[(kk + 1 + i) + (size_t)jl * m], vv[c - kk - 1]);
+        }
+        pb[i] = sacc;
+      }
+    }
+    cl.sync();  // S2: partials ready
+    // p = tau * sum of partials; c = v^H p; w = p - 1/2 conj(tau) c v (each CTA)
+    double cr = 0.0, ci = 0.0;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      cplx sacc = czero();
+      for (int rr = 0; rr < kHC; ++rr) sacc = cadd(sacc, cl.map_shared_rank(pbuf, rr)[(size_t)buf * m + i]);
+      sacc = cmul(tk, sacc);
+      wv[i] = sacc;
+      const cplx tt = cmul(cconj(vv[i]), sacc);
+      cr += tt.x;
+      ci += tt.y;
+    }
+    cr = cta_sum(cr, red);
+    ci = cta_sum(ci, red);
+    const cplx hc = cscale(cmul(cconj(tk), cmk(cr, ci)), 0.5);
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) wv[i] = csub(wv[i], cmul(hc, vv[i]));
+    __syncthreads();
+    // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
+    {
+      const int jl0 = max((kk + 1 - rank + kHC - 1) / kHC, 0);
+      const int ncols = ncl - jl0;
+      for (int idx = threadIdx.x; idx < nk * ncols; idx += blockDim.x) {
+        const int i = idx % nk, jl = jl0 + idx / nk;
+        const int c = rank + kHC * jl;
+        if (c >= m) continue;
+        const int jc = c - kk - 1;
+        cplx* a = Hl + (kk + 1 + i) + (size_t)jl * m;
+        cplx av = *a;
+        av = csub(av, cmul(vv[i], cconj(wv[jc])));
+        av = csub(av, cmul(wv[i], cconj(vv[jc])));
+        *a = av;
+      }
+    }
+    __syncthreads();
+  }
+  // last diagonal, reflectors to global memory
+  if (rank == (m - 1) % kHC && threadIdx.x == 0) {
+    aux[m - 1] = Hl[(m - 1) + (size_t)((m - 1) / kHC) * m].x;
+    aux[bm + m - 1] = 0.0;
+  }
+  for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
+    const int i = idx % m, c = rank + kHC * (idx / m);
+    if (c < m) H[i + (size_t)c * m] = Hl[idx];
+  }
+  cl.sync();
+  if (rank != 0) return;
+  // ---- CTA 0: spectrum edge, rank, retained eigenvalues
+  __shared__ double s_lo, s_hi, s_piv, s_s0, s_thr;
+  __shared__ int s_r, s_need;
   double cm = 0.0;
   for (int c = threadIdx.x; c < L.slot_cn[p]; c += blockDim.x) cm = fmax(cm, L.colnorm[L.slot_c0[p] + c]);
   const double cmax = cta_max(cm, red);
+  double* dg = reinterpret_cast<double*>(smraw);  // local columns no longer needed
+  double* ed = dg + m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) dg[i] = aux[i], ed[i] = aux[bm + i];
   __syncthreads();
-  const long long T0 = clock64();
-  // ---- tridiagonal reduction and the spectrum edge
-  cta_hetrd(m, H, dg, ed, tau, pv, wv, red);
   if (threadIdx.x == 0) {
     double lo = 0.0, hi = 0.0, emax = 0.0;
     for (int i = 0; i < m; ++i) {
@@ -153,80 +271,85 @@ __global__ void __launch_bounds__(256) k_eig1(DevLevel L, const int* batch_cl, i
     lo -= 1e-14 * span;
     hi += 1e-14 * span;
     const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
-    lam[0] = lo;  // scratch: bounds
-    lam[1] = hi;
-    lam[2] = pivmin;
     const double lmax = bisect_eig(m, dg, ed, m - 1, lo, hi, pivmin);
     const double s0 = sqrt(fmax(lmax, 0.0));
     const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
     int r = 0;
     if (s0 > 0.0) r = m - sturm_count(m, dg, ed, thr * thr, pivmin);
-    r = max(0, min(r, m));
-    s_s0 = s0;
-    s_thr = thr;
-    s_r = r;
+    s_r = max(0, min(r, m));
+    s_lo = lo, s_hi = hi, s_piv = pivmin, s_s0 = s0, s_thr = thr;
     // the Gram resolves eigenvalues to ~eps_mach * lmax: below ~1e-4 sigma_0
-    // the truncation needs the refinement pass
+    // the truncation needs the refinement pass (k_eig1_refine)
     s_need = s0 > 0.0 && thr < 1e-4 * s0;
   }
   __syncthreads();
-  const long long T1 = clock64();
-  const double lo = lam[0], hi = lam[1], pivmin = lam[2];
   const int r = s_r;
-  __syncthreads();
-  if (s_need) {
-    // rare (eps_fill < 1e-4): full Jacobi decomposition for the two-pass refinement
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      cplx s = czero();
-      for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
-      H[idx] = s;
-    }
-    double dmax = 0.0;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) dmax = fmax(dmax, H[i + i * m].x);
-    dmax = cta_max(dmax, red);
-    __syncthreads();
-    cta_jacobi_eig(m, H, U, rot, pr, red, 1e-17 * dmax);
-    for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(H[i + i * m].x, 0.0));
-    __syncthreads();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      int rk = 0;
-      for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
-      ord[rk] = i;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < b * m; idx += blockDim.x) {
-      const int i = idx % b, j = idx / b;
-      cplx v = czero();
-      const int col = ord[j];
-      for (int rr = 0; rr < m; ++rr) cfma(v, Vp[i + (size_t)rr * b], U[rr + col * m]);
-      D1[i + (size_t)j * b] = v;
-    }
-    double* lout = L.lam + (size_t)q * bm;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) lout[i] = lam[ord[i]];
-    if (threadIdx.x == 0) {
-      int rr = 0;
-      while (rr < m && lam[ord[rr]] > s_thr) ++rr;
-      L.pass2[q] = 1, L.rank1[q] = rr, L.cmax[q] = cmax;
-      if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d s0 %.3e thr %.3e r %d (refine)\n", L.level, t, m, s_s0, s_thr, rr);
-    }
-    return;
-  }
-  // ---- top-r eigenvalues by bisection; vectors in k_eigvec, basis in k_eig1b
-  double* aux = reinterpret_cast<double*>(ws + 2 * bb);  // dg, ed, lam (bm each), tau (bm cplx)
-  for (int j = threadIdx.x; j < r; j += blockDim.x) aux[2 * bm + j] = bisect_eig(m, dg, ed, m - 1 - j, lo, hi, pivmin);
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    aux[i] = dg[i];
-    aux[bm + i] = ed[i];
-    reinterpret_cast<cplx*>(aux + 4 * bm)[i] = tau[i];
-  }
+  if (!s_need)
+    for (int j = threadIdx.x; j < r; j += blockDim.x) aux[2 * bm + j] = bisect_eig(m, dg, ed, m - 1 - j, s_lo, s_hi, s_piv);
   if (threadIdx.x == 0) {
-    L.pass2[q] = 0;
+    L.pass2[q] = s_need ? 2 : 0;  // 2: refinement requested
     L.rank1[q] = r;
     L.cmax[q] = cmax;
     L.lam[(size_t)q * bm] = s_s0;
-    if (L.debug)
-      printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d | cycles gram %lld hetrd %lld\n", L.level, t, m, cmax, s_s0, s_thr,
-             r, T0 - Tstart, T1 - T0);
+    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d%s\n", L.level, t, m, cmax, s_s0, s_thr, r, s_need ? " (refine)" : "");
+  }
+}
+
+// Rare path (thr < 1e-4 sigma_0, e.g. eps_fill < 1e-4): full Jacobi
+// decomposition of the pass-1 Gram, D1 = Vp U1 sorted, then the
+// Rayleigh-Ritz refinement pass in k_head.
+__global__ void __launch_bounds__(256) k_eig1_refine(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[32];
+  const int q = blockIdx.x, p = p0 + q;
+  if (L.pass2[q] != 2) return;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  cplx* H = ws;
+  cplx* U = ws + bb;
+  double* lam = reinterpret_cast<double*>(smraw);
+  int* ord = reinterpret_cast<int*>(lam + bm);
+  int* pr = ord + bm;
+  double* rot = reinterpret_cast<double*>(pr + bm + 2);
+  cplx* D1 = L.dir + (size_t)q * bb;
+  const cplx* Vp = L.Vp + (size_t)t * bb;
+  const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+    cplx s = czero();
+    for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + idx]);
+    H[idx] = s;
+  }
+  double dmax = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) dmax = fmax(dmax, H[i + i * m].x);
+  dmax = cta_max(dmax, red);
+  __syncthreads();
+  cta_jacobi_eig(m, H, U, rot, pr, red, 1e-17 * dmax);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) lam[i] = sqrt(fmax(H[i + i * m].x, 0.0));
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    int rk = 0;
+    for (int j = 0; j < m; ++j) rk += (lam[j] > lam[i]) || (lam[j] == lam[i] && j < i);
+    ord[rk] = i;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < b * m; idx += blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    cplx v = czero();
+    const int col = ord[j];
+    for (int rr = 0; rr < m; ++rr) cfma(v, Vp[i + (size_t)rr * b], U[rr + col * m]);
+    D1[i + (size_t)j * b] = v;
+  }
+  double* lout = L.lam + (size_t)q * bm;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) lout[i] = lam[ord[i]];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double s0 = lam[ord[0]];
+    const double thr = fmax(fmax(L.eps * s0, L.eps * L.cmax[q]), 1e-300);
+    int rr = 0;
+    while (rr < m && lam[ord[rr]] > thr) ++rr;
+    L.pass2[q] = 1, L.rank1[q] = rr;
   }
 }
 
@@ -843,11 +966,39 @@ size_t eig1_small_bytes(int bm) { return (size_t)(bm + 1) * 8 * 3 + (size_t)bm *
 size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_small_bytes(bm); }
 
 void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase) {
-  const size_t small = eig1_small_bytes(L.bmax);
-  set_smem((const void*)k_eig1, small);
   cplx* ws = workspace(eig1_ws_cplx(L.bmax) * sizeof(cplx) * nb, s);
-  k_eig1<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
-  post_launch("k_eig1");
+  {
+    const int ncl = (L.bmax + kHC - 1) / kHC;
+    const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 6 + 256;
+    if (smem > kSmemCap) throw std::runtime_error("k_eig1c: block too large for the 16-CTA cluster");
+    set_smem((const void*)k_eig1c, smem);
+    static bool np = false;
+    if (!np) {
+      cudaFuncSetAttribute((const void*)k_eig1c, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      np = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb * kHC);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kHC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1c, L, batch_cl, p0, ws);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_eig1c failed: ") + cudaGetErrorString(e));
+    post_launch("k_eig1c");
+  }
+  {
+    const size_t small = (size_t)L.bmax * 8 + (size_t)L.bmax * 4 + (size_t)(L.bmax + 2) * 4 + 16 + (size_t)4 * (L.bmax / 2 + 1) * 8 + 64;
+    set_smem((const void*)k_eig1_refine, small);
+    k_eig1_refine<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
+    post_launch("k_eig1_refine");
+  }
   phase(1);
   if (mmax > 0) {
     const size_t vsm = (size_t)8 * L.bmax * sizeof(double) + 16 + (size_t)L.bmax * sizeof(cplx);
