@@ -829,3 +829,61 @@ __device__ inline void cta_inv_upper(int n, const cplx* LU, int ldu, cplx* Y, in
 }
 
 }  // namespace h2g
+
+namespace h2g {
+
+// ---------------------------------------------------------------------------
+// Blocked Householder QR (panels of 16 columns factored in shared memory,
+// trailing columns updated with the panel's compact-WY form through tiled
+// GEMMs). Same reflectors (Eigen convention) as cta_householder_qr.
+// P: shared scratch of m x 16 complex; Tb: shared 16 x 16; W: global scratch
+// of 16 x n complex (ld 16).
+__device__ inline void cta_householder_qr_blocked(int m, int n, cplx* A, int lda, cplx* tau, double* red, cplx* tile_sm, cplx* P, cplx* Tb,
+                                                  cplx* W, cplx* W2) {
+  const int s = min(m, n);
+  for (int j0 = 0; j0 < s; j0 += 16) {
+    const int kb = min(16, s - j0), mr = m - j0;
+    cta_copy(mr, kb, A + j0 + (size_t)j0 * lda, lda, P, mr);
+    __syncthreads();
+    cta_householder_qr(mr, kb, P, mr, tau + j0, red);
+    cta_copy(mr, kb, P, mr, A + j0 + (size_t)j0 * lda, lda);
+    __syncthreads();
+    const int nt = n - j0 - kb;
+    if (nt <= 0) continue;
+    // Y (mr x kb, unit lower trapezoidal) in P; T (kb x kb) of Qp = H_0^H..H_{kb-1}^H = I - Y T Y^H
+    for (int idx = threadIdx.x; idx < mr * kb; idx += blockDim.x) {
+      const int i = idx % mr, j = idx / mr;
+      if (i < j) P[idx] = czero();
+      else if (i == j) P[idx] = cone();
+    }
+    __syncthreads();
+    // S = Y^H Y (kb x kb) into Tb, then T in place column by column
+    for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+      const int i = idx % kb, j = idx / kb;
+      cplx v = czero();
+      for (int p = max(i, j); p < mr; ++p) cfma(v, cconj(P[p + (size_t)i * mr]), P[p + (size_t)j * mr]);
+      W2[idx] = v;  // S
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int kk = 0; kk < kb; ++kk) {
+        const cplx tk = cconj(tau[j0 + kk]);
+        for (int i = 0; i < kk; ++i) {
+          cplx v = czero();
+          for (int j = i; j < kk; ++j) cfma(v, Tb[i + j * 16], W2[j + kk * kb]);
+          Tb[i + kk * 16] = cmul(cmk(-tk.x, -tk.y), v);
+        }
+        Tb[kk + kk * 16] = tk;
+        for (int i = kk + 1; i < kb; ++i) Tb[i + kk * 16] = czero();
+      }
+    }
+    __syncthreads();
+    // A_trail <- Qp^H A_trail = A_trail - Y (T^H (Y^H A_trail))
+    cplx* At = A + j0 + (size_t)(j0 + kb) * lda;
+    cta_gemm_tiled(kb, nt, mr, 1.0, P, mr, OP_C, At, lda, OP_N, 0.0, W, 16, tile_sm);
+    cta_gemm_tiled(kb, nt, kb, 1.0, Tb, 16, OP_C, W, 16, OP_N, 0.0, W2, 16, tile_sm);
+    cta_gemm_tiled(mr, nt, kb, -1.0, P, mr, OP_N, W2, 16, OP_N, 1.0, At, lda, tile_sm);
+  }
+}
+
+}  // namespace h2g

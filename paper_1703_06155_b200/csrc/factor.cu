@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
 }
 
 // H, U, then 4.5 bm^2 of scratch (inverse iteration, then the compact-WY GEMMs)
-__host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 6 + (size_t)bm * 8 + 16; }
+// H, U, aux (8 bm), X1, X2, Tm, Sm (bm^2 each), tau (bm)
+__host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 6 + (size_t)bm * 9 + 16; }
 
 // --------------------------------------------------------------------------
 // Step 0, pass 1. The projected fill-in stack Y = Vp^H W (factorization.hpp:
@@ -430,12 +431,15 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
 }
 
 // D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H = I - Y T Y^H, the compact WY form
-// of a Householder QR of the retained eigenvectors U_r: [new | complement]
-// as three tiled GEMMs.
+// of a Householder QR of the retained eigenvectors U_r: [new | complement].
+// k_eig1b: blocked QR of U_r and the explicit Y; S = Y^H Y (descriptor GEMM);
+// k_eig1t: T recurrence and D1 = Vp; then X1 = Vp Y, X2 = X1 T and
+// D1 -= X2 Y^H as descriptor GEMMs with r resolved on the device.
 __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, cplx* gws) {
   __shared__ cplx tile_sm[kTileSmemCplx];
   __shared__ double red[32];
   __shared__ cplx tau[512];
+  extern __shared__ __align__(16) unsigned char qsm[];
   const int q = blockIdx.x;
   if (L.pass2[q]) return;
   const int r = L.rank1[q];
@@ -444,44 +448,52 @@ __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, 
   const size_t bb = (size_t)bm * bm;
   cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
   cplx* U = ws + bb;
-  cplx* D1 = L.dir + (size_t)q * bb;
-  const cplx* Vp = L.Vp + (size_t)t * bb;
-  if (r == 0 || m == 0) {
-    cta_copy(b, m, Vp, b, D1, b);
-    return;
-  }
-  cta_householder_qr(m, r, U, m, tau, red);
-  cplx* Y = ws;                    // m x r explicit reflectors (H no longer needed)
-  cplx* X1 = ws + 2 * bb + 4 * bm;  // b x r
-  cplx* X2 = X1 + bb;              // b x r
-  cplx* Tm = X2 + bb;              // r x r
-  cplx* Sm = Tm + bb;              // r x r: Y^H Y
+  if (r == 0 || m == 0) return;
+  cplx* P = reinterpret_cast<cplx*>(qsm);  // m x 16 panel
+  __shared__ cplx Tb[16 * 16];
+  cplx* Wq = ws + 2 * bb + 4 * bm;
+  cplx* Wq2 = Wq + (size_t)16 * r;
+  cta_householder_qr_blocked(m, r, U, m, tau, red, tile_sm, P, Tb, Wq, Wq2);
+  cplx* Y = ws;  // m x r explicit reflectors (H no longer needed)
   for (int idx = threadIdx.x; idx < m * r; idx += blockDim.x) {
     const int i = idx % m, jj = idx / m;
     Y[idx] = i < jj ? czero() : (i == jj ? cone() : U[i + (size_t)jj * m]);
   }
-  __syncthreads();
-  cta_gemm_tiled(r, r, m, 1.0, Y, m, OP_C, Y, m, OP_N, 0.0, Sm, r, tile_sm);
-  // T (upper, r x r): T_kk = conj(tau_k), T[0:k,k] = -conj(tau_k) T[0:k,0:k] S[0:k,k]
+  cplx* tau_g = ws + 2 * bb + 4 * bm + 4 * bb;  // after X1, X2, Tm, Sm
+  for (int i = threadIdx.x; i < r; i += blockDim.x) tau_g[i] = tau[i];
+}
+
+__global__ void __launch_bounds__(256) k_eig1t(DevLevel L, const int* batch_cl, cplx* gws) {
+  const int q = blockIdx.x;
+  if (L.pass2[q]) return;
+  const int r = L.rank1[q];
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  cplx* D1 = L.dir + (size_t)q * bb;
+  const cplx* Vp = L.Vp + (size_t)t * bb;
+  cta_copy(b, m, Vp, b, D1, b);
+  if (r == 0 || m == 0) return;
+  cplx* X1 = ws + 2 * bb + 4 * bm;
+  cplx* Tm = X1 + 2 * bb;
+  const cplx* Sm = Tm + bb;
+  const cplx* tau_g = X1 + 4 * bb;
+  // T (upper, r x r, ld bm): T_kk = conj(tau_k), T[0:k,k] = -conj(tau_k) T[0:k,0:k] S[0:k,k]
   for (int kk = 0; kk < r; ++kk) {
-    const cplx tk = cconj(tau[kk]);
+    const cplx tk = cconj(tau_g[kk]);
     for (int i = threadIdx.x; i < r; i += blockDim.x) {
       cplx v = czero();
       if (i < kk) {
-        for (int jj = i; jj < kk; ++jj) cfma(v, Tm[i + (size_t)jj * r], Sm[jj + (size_t)kk * r]);
+        for (int jj = i; jj < kk; ++jj) cfma(v, Tm[i + (size_t)jj * bm], Sm[jj + (size_t)kk * bm]);
         v = cmul(cmk(-tk.x, -tk.y), v);
       } else if (i == kk) {
         v = tk;
       }
-      Tm[i + (size_t)kk * r] = v;
+      Tm[i + (size_t)kk * bm] = v;
     }
     __syncthreads();
   }
-  cta_gemm_tiled(b, r, m, 1.0, Vp, b, OP_N, Y, m, OP_N, 0.0, X1, b, tile_sm);
-  cta_gemm_tiled(b, r, r, 1.0, X1, b, OP_N, Tm, r, OP_N, 0.0, X2, b, tile_sm);
-  cta_copy(b, m, Vp, b, D1, b);
-  __syncthreads();
-  cta_gemm_tiled(b, m, r, -1.0, X2, b, OP_N, Y, m, OP_C, 1.0, D1, b, tile_sm);
 }
 
 // --------------------------------------------------------------------------
@@ -772,7 +784,12 @@ __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
 
 __global__ void __launch_bounds__(128) k_gemm(const GemmDesc* descs) {
   __shared__ Tile128Smem S;
-  const GemmDesc d = descs[blockIdx.x];
+  GemmDesc d = descs[blockIdx.x];
+  if (d.skipnz && *d.skipnz) return;
+  if (d.dyn) {
+    const int v = *d.dyn;
+    d.m += d.mi * v, d.n += d.ni * v, d.k += d.ki * v;
+  }
   const int ntr = (d.m + 63) / 64, ntc = (d.n + 63) / 64;
   const bool zero = (d.flag1 && !*d.flag1) || (d.flag2 && !*d.flag2);
   const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
@@ -965,8 +982,11 @@ void launch_complement(const DevLevel& L, cudaStream_t s) {
 size_t eig1_small_bytes(int bm) { return (size_t)(bm + 1) * 8 * 3 + (size_t)bm * 16 * 3 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64; }
 size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_small_bytes(bm); }
 
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase) {
-  cplx* ws = workspace(eig1_ws_cplx(L.bmax) * sizeof(cplx) * nb, s);
+size_t eig1_ws_bytes(int bmax) { return eig1_ws_cplx(bmax) * sizeof(cplx); }
+
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int tiles, cudaStream_t s,
+                 const std::function<void(int)>& phase) {
+  cplx* ws = L.eigws;
   {
     const int ncl = (L.bmax + kHC - 1) / kHC;
     const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 6 + 256;
@@ -1007,8 +1027,15 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     post_launch("k_eigvec");
   }
   phase(2);
-  k_eig1b<<<nb, 256, 0, s>>>(L, batch_cl, ws);
+  set_smem((const void*)k_eig1b, (size_t)L.bmax * 16 * sizeof(cplx));
+  k_eig1b<<<nb, 256, (size_t)L.bmax * 16 * sizeof(cplx), s>>>(L, batch_cl, ws);
   post_launch("k_eig1b");
+  launch_gemm(wy, nb, s, tiles);              // S = Y^H Y
+  k_eig1t<<<nb, 256, 0, s>>>(L, batch_cl, ws);
+  post_launch("k_eig1t");
+  launch_gemm(wy + nb, nb, s, tiles);         // X1 = Vp Y
+  launch_gemm(wy + 2 * nb, nb, s, tiles);     // X2 = X1 T
+  launch_gemm(wy + 3 * nb, nb, s, tiles);     // D1 -= X2 Y^H
 }
 
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {

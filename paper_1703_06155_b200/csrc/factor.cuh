@@ -68,6 +68,7 @@ struct DevLevel {
   double* cmax;                // [q]
   DevError* err;
   int debug;
+  cplx* eigws;  // step-0 eigensolver workspace, eig1_ws_cplx(bmax) per batch slot
 };
 
 struct PanelItemD {
@@ -97,6 +98,10 @@ struct GemmDesc {
   double alpha, beta;
   const int* flag1;  // if set and *flag1 == 0 (or *flag2 == 0): op(A) op(B) counts as zero
   const int* flag2;
+  // device-resolved sizes: m += mi * *dyn, n += ni * *dyn, k += ki * *dyn
+  const int* dyn;
+  int mi, ni, ki, pad;
+  const int* skipnz;  // if set and *skipnz != 0: the descriptor is skipped (no write)
 };
 struct NormDesc {
   const cplx* F;
@@ -106,7 +111,9 @@ struct NormDesc {
 };
 
 void launch_complement(const DevLevel& L, cudaStream_t s);
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s, const std::function<void(int)>& phase);
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int tiles, cudaStream_t s,
+                 const std::function<void(int)>& phase);
+size_t eig1_ws_bytes(int bmax);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
 void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
