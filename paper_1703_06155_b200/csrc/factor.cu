@@ -97,12 +97,8 @@ __host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm 
 // eigenvalues above thr^2 (Sturm) and bisects the retained ones; vectors are
 // formed by k_eigvec, the basis by k_eig1b. Threshold rule: factorization.hpp:
 // 295-298 / h2_matrix.hpp:287-290.
-constexpr int kHC = 16;
+constexpr int kHCmax = 16;
 
-__device__ inline size_t eig1c_smem(int m) {
-  const int ncl = (m + kHC - 1) / kHC;
-  return (size_t)m * ncl * sizeof(cplx) + (size_t)m * sizeof(cplx) * 6 + 256;
-}
 
 __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   namespace cg = cooperative_groups;
@@ -112,6 +108,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   __shared__ int s_any;
   __shared__ cplx s_tau[2];
   __shared__ int s_skip[2];
+  const int kHC = (int)cl.num_blocks();  // 1, 4 or 16 CTAs per cluster
   const int rank = (int)cl.block_rank();
   const int q = blockIdx.x / kHC, p = p0 + q;
   const int t = batch_cl[q];
@@ -271,8 +268,46 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     const double span = fmax(hi - lo, 1e-300);
     lo -= 1e-14 * span;
     hi += 1e-14 * span;
-    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
-    const double lmax = bisect_eig(m, dg, ed, m - 1, lo, hi, pivmin);
+    s_lo = lo, s_hi = hi;
+    s_piv = 2.2250738585072014e-308 * fmax(1.0, emax);
+  }
+  __syncthreads();
+  // largest eigenvalue by multisection: every thread tests one point of the
+  // current bracket, so each round shrinks it blockDim.x-fold
+  {
+    __shared__ double s_a, s_b;
+    __shared__ int s_cnt[256];
+    if (threadIdx.x == 0) s_a = s_lo, s_b = s_hi;
+    __syncthreads();
+    for (int round = 0; round < 12; ++round) {
+      const double a = s_a, bnd = s_b;
+      if (bnd - a <= 2e-16 * fmax(fabs(a), fabs(bnd))) break;
+      const double x = a + (bnd - a) * (threadIdx.x + 1) / (blockDim.x + 1);
+      s_cnt[threadIdx.x] = sturm_count(m, dg, ed, x, s_piv);  // #eigenvalues below x
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        // smallest point below which all m eigenvalues lie -> new upper bound
+        double na = a, nb2 = bnd;
+        for (int j = 0; j < (int)blockDim.x; ++j) {
+          const double xj = a + (bnd - a) * (j + 1) / (blockDim.x + 1);
+          if (s_cnt[j] >= m) {
+            nb2 = xj;
+            break;
+          }
+          na = xj;
+        }
+        s_a = na, s_b = nb2;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s_s0 = 0.5 * (s_a + s_b);  // lmax (temporarily)
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double lo = s_lo, hi = s_hi, pivmin = s_piv;
+    (void)lo;
+    (void)hi;
+    const double lmax = s_s0;
     const double s0 = sqrt(fmax(lmax, 0.0));
     const double thr = fmax(fmax(L.eps * s0, L.eps * cmax), 1e-300);
     int r = 0;
@@ -682,7 +717,8 @@ __global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, 
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
 // 4 x 4 complex micro-tile per thread, K staged through shared memory.
 __global__ void __launch_bounds__(128) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
-  __shared__ Tile128Smem S;
+  extern __shared__ __align__(16) unsigned char tsm[];
+  Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
   const SchurTargetD tg = targets[blockIdx.x];
   const int bm = L.bmax;
   int rows, cols;
@@ -783,7 +819,8 @@ __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
 }
 
 __global__ void __launch_bounds__(128) k_gemm(const GemmDesc* descs) {
-  __shared__ Tile128Smem S;
+  extern __shared__ __align__(16) unsigned char tsm[];
+  Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
   GemmDesc d = descs[blockIdx.x];
   if (d.skipnz && *d.skipnz) return;
   if (d.dyn) {
@@ -988,6 +1025,9 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
                  const std::function<void(int)>& phase) {
   cplx* ws = L.eigws;
   {
+    // cluster size: small blocks fit one CTA's shared memory, large ones are
+    // spread over 4 or 16 CTAs
+    const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : kHCmax);
     const int ncl = (L.bmax + kHC - 1) / kHC;
     const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 6 + 256;
     if (smem > kSmemCap) throw std::runtime_error("k_eig1c: block too large for the 16-CTA cluster");
@@ -1069,7 +1109,8 @@ void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* item
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;
   const int t = (L.bmax + 63) / 64;
-  k_schur<<<dim3(ntargets, t * t), 128, 0, s>>>(L, targets, contrib);
+  set_smem((const void*)k_schur, sizeof(Tile128Smem));
+  k_schur<<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
   post_launch("k_schur");
 }
 
@@ -1078,7 +1119,8 @@ void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {
 }
 
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int tiles) {
-  if (n > 0) k_gemm<<<dim3(n, std::max(1, std::min(tiles, 16))), 128, 0, s>>>(d);
+  set_smem((const void*)k_gemm, sizeof(Tile128Smem));
+  if (n > 0) k_gemm<<<dim3(n, std::max(1, std::min(tiles, 16))), 128, sizeof(Tile128Smem), s>>>(d);
   post_launch("k_gemm");
 }
 

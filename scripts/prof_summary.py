@@ -1,0 +1,18 @@
+import sys
+sys.path.insert(0, ".")
+import paper_1703_06155_b200 as h2g
+from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+sched = sys.argv[2] if len(sys.argv) > 2 else "reference"
+c = BASELINE_CONFIGS[cfg]
+k0, scale, diag = vie_constants(c["cells"], c["side"])
+A = h2g.H2Matrix.build(vie_grid_points(c["cells"], c["side"]), c["leaf"], 1.0, h2g.helmholtz_kernel(k0, diag, scale), c["eps"])
+ch = h2g.factorize(A, c["eps"], schedule=sched)
+print("unprofiled", ch.timing())
+A.ctx.set_profiling(True)
+ch = h2g.factorize(A, c["eps"], schedule=sched)
+st = ch.kernel_stats()
+tot = sum(v["ms"] for v in st.values())
+for k, v in sorted(st.items(), key=lambda kv: -kv[1]["ms"]):
+    print(f"{k:<11} {v['ms']:9.1f} ms {v['ms']/tot:6.1%} launches {v['launches']}")
+print("profiled", ch.timing())

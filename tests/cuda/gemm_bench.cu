@@ -178,6 +178,67 @@ __global__ void __launch_bounds__(128) v5(int M, int N, int K, const cplx* A, co
       }
 }
 
+// V6: V4 + cp.async multi-stage (STG stages of K=8) staging, zero-fill via src-size 0.
+__device__ __forceinline__ void cp16(void* smem, const void* g, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(sz));
+}
+template <int STG>
+__global__ void __launch_bounds__(128) v6(int M, int N, int K, const cplx* A, const cplx* B, cplx* C) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  cplx(*sA)[8][64] = reinterpret_cast<cplx(*)[8][64]>(raw);
+  cplx(*sB)[8][64] = reinterpret_cast<cplx(*)[8][64]>(raw + STG * 8 * 64 * 16);
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+  cplx acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = czero();
+  const int nk = (K + 7) / 8;
+  auto load = [&](int st, int kc) {
+    const int k0 = kc * 8;
+    for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+      const int i = idx % 64, p = idx / 64;
+      const bool va = k0 + p < K;
+      cp16(&sA[st][p][i], A + r0 + i + (size_t)(va ? k0 + p : 0) * M, va);
+      const int q = idx % 8, j = idx / 8;
+      const bool vb = k0 + q < K;
+      cp16(&sB[st][q][j], B + (vb ? k0 + q : 0) + (size_t)(c0 + j) * K, vb);
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  for (int s = 0; s < STG - 1; ++s) {
+    if (s < nk) load(s, s);
+    else asm volatile("cp.async.commit_group;");
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STG - 2));
+    __syncthreads();
+    const int st = kc % STG;
+    const int nxt = kc + STG - 1;
+    if (nxt < nk) load(nxt % STG, nxt);
+    else asm volatile("cp.async.commit_group;");
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      cplx av[8], bv[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) av[a] = sA[st][p][tr + 8 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sB[st][p][tc * 4 + b];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) C[r0 + tr + 8 * a + (size_t)(c0 + tc * 4 + b) * M] = acc[a][b];
+}
+
 int main() {
   const int M = 4096, N = 4096, K = 512;
   cplx *A, *B, *C;
@@ -192,13 +253,19 @@ int main() {
   cudaFuncSetAttribute((const void*)v1, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   dim3 g(M / 64, N / 64);
   const double flops = 8.0 * M * N * K;
-  for (int v = 1; v <= 4; ++v) {
+  cudaFuncSetAttribute((const void*)v6<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 2 * 8 * 64 * 16);
+  cudaFuncSetAttribute((const void*)v6<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 8 * 64 * 16);
+  cudaFuncSetAttribute((const void*)v6<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 2 * 8 * 64 * 16);
+  for (int v = 1; v <= 7; ++v) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
       if (v == 1) v1<<<g, 256>>>(M, N, K, A, B, C);
       if (v == 2) v3<<<g, 128>>>(M, N, K, A, B, C);
       if (v == 3) v4<<<g, 128>>>(M, N, K, A, B, C);
       if (v == 4) v5<<<g, 128>>>(M, N, K, A, B, C);
+      if (v == 5) v6<3><<<g, 128, 3 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
+      if (v == 6) v6<4><<<g, 128, 4 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
+      if (v == 7) v6<6><<<g, 128, 6 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -216,13 +283,13 @@ int main() {
     cplx* C2;
     cudaMalloc(&C2, (size_t)M * N * 16);
     v4<<<g, 128>>>(M, N, K, A, B, C);
-    v5<<<g, 128>>>(M, N, K, A, B, C2);
+    v6<4><<<g, 128, 4 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C2);
     std::vector<double> c1((size_t)M * N * 2), c2((size_t)M * N * 2);
     cudaMemcpy(c1.data(), C, c1.size() * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(c2.data(), C2, c2.size() * 8, cudaMemcpyDeviceToHost);
     double md = 0, mx = 0;
     for (size_t i = 0; i < c1.size(); ++i) md = fmax(md, fabs(c1[i] - c2[i])), mx = fmax(mx, fabs(c1[i]));
-    printf("v5 vs v4 max abs diff %.3e (max %.3e)\n", md, mx);
+    printf("v6 vs v4 max abs diff %.3e (max %.3e)\n", md, mx);
   }
   return 0;
 }
