@@ -643,7 +643,6 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         size_t o_Qt = pk.add(Qt_off), o_L11 = pk.add(L11_off), o_U11 = pk.add(U11_off), o_Li = pk.add(Linv_off), o_Ui = pk.add(Uinv_off);
         size_t o_Lb = pk.add(Lbar_off), o_Ub = pk.add(Ubar_off), o_Ls = pk.add(Lself_off), o_Us = pk.add(Uself_off);
         size_t o_bat = pk.add(SC.batch_cl);
-        size_t o_pan = pk.add_raw(reinterpret_cast<const PanelItemD*>(W.panel.data()), W.panel.size());
         size_t o_sch = pk.add_raw(reinterpret_cast<const SchurTargetD*>(W.schur.data()), W.schur.size());
         size_t o_con = pk.add_raw(reinterpret_cast<const SchurContribD*>(W.contrib.data()), W.contrib.size());
         size_t o_fs = pk.add_raw(reinterpret_cast<const SolveTargetD*>(W.fsolve.data()), W.fsolve.size());
@@ -814,7 +813,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             for (int i = 0; i < 4; ++i) gW.insert(gW.end(), g[i].begin(), g[i].end());
           }
         }
-        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dW;
+        // step 2/3b panels as descriptor GEMMs (device-resolved e = b - kfin):
+        // column item D(t,c): T = Qt^H D, Ubar = L11^{-1} T[:e,:], lift = Ubar Qt_c^T, D = T (rows < e zeroed)
+        // row item    D(j,t): T = D conj(Qt), Lbar = T[:,:e] U11^{-1}, lift = Qt_j Lbar, D = T (cols < e zeroed)
+        std::vector<GemmDesc> gP1, gP2, gP3;
+        std::vector<MaskDesc> gPM;
+        std::vector<int> p3_ptr(1, 0);
+        size_t pmax = 1;
+        for (int bi = 0; bi < nbat0; ++bi) pmax = std::max<size_t>(pmax, W.panel_ptr[bi + 1] - W.panel_ptr[bi]);
+        DBuf panbuf;
+        panbuf.alloc(pmax * bb * 16, st);
+        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dW, dP1, dP2, dP3, dPM;
         upload(dW, gW, st);
         upload(dR1, gR1, st);
         upload(dR2, gR2, st);
@@ -881,6 +890,52 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.debug = std::getenv("H2G_DEBUG") ? std::atoi(std::getenv("H2G_DEBUG")) : 0;
         DL.eigws = eigws.as<cplx>();
 
+        {
+          cplx* chainb = CL->arena.as<cplx>();
+          cplx* liftb = lift.as<cplx>();
+          const int* kfd = DL.kfin;
+          for (int bi = 0; bi < nbat0; ++bi) {
+            for (int it = W.panel_ptr[bi]; it < W.panel_ptr[bi + 1]; ++it) {
+              const PanelItem& pi = W.panel[it];
+              const int t = SC.batch_cl[SC.batch_ptr[bi] + pi.q];
+              const int b = cur.bsz[t], bn = cur.bsz[pi.nb];
+              cplx* T = panbuf.as<cplx>() + (size_t)(it - W.panel_ptr[bi]) * bb;
+              cplx* Dblk = cur.D.as<cplx>() + (size_t)pi.blk * bb;
+              const cplx* Q = chainb + Qt_off[t];
+              const cplx* Qn = chainb + Qt_off[pi.nb];
+              GemmDesc r{}, pp{}, lf{};
+              if (pi.side == 0) {  // D(t, c): b x bn
+                r = {Q, Dblk, T, b, b, b, b, bn, b, OP_C, OP_N, 1.0, 0.0};
+                // Ubar (e x bn, ld e) = L11^{-1} (e x e, ld e) T[:e, :]
+                pp = {chainb + Linv_off[t], T, chainb + Ubar_off[pi.entry], b, b, b, b, bn, b, OP_N, OP_N, 1.0, 0.0};
+                pp.dyn = kfd + t, pp.mi = -1, pp.ki = -1, pp.ldneg = 1 | 4;
+                if (pi.lift) {
+                  lf = {chainb + Ubar_off[pi.entry], Qn, liftb + Ubar_off[pi.entry], b, bn, b, b, bn, bn, OP_N, OP_T, 1.0, 0.0};
+                  lf.dyn = kfd + t, lf.mi = -1, lf.ldneg = 1 | 4;
+                }
+                gPM.push_back({T, Dblk, b, b, bn, 0, b, 0, kfd + t});
+              } else {  // D(j, t): bn x b
+                r = {Dblk, Q, T, bn, b, bn, bn, b, b, OP_N, OP_R, 1.0, 0.0};
+                // Lbar (bn x e, ld bn) = T[:, :e] U11^{-1} (e x e, ld e)
+                pp = {T, chainb + Uinv_off[t], chainb + Lbar_off[pi.entry], bn, b, bn, bn, b, b, OP_N, OP_N, 1.0, 0.0};
+                pp.dyn = kfd + t, pp.ni = -1, pp.ki = -1, pp.ldneg = 2;
+                if (pi.lift) {
+                  lf = {Qn, chainb + Lbar_off[pi.entry], liftb + Lbar_off[pi.entry], bn, bn, bn, bn, b, bn, OP_N, OP_N, 1.0, 0.0};
+                  lf.dyn = kfd + t, lf.ni = -1;
+                }
+                gPM.push_back({T, Dblk, bn, bn, b, 1, b, 0, kfd + t});
+              }
+              gP1.push_back(r);
+              gP2.push_back(pp);
+              if (pi.lift) gP3.push_back(lf);
+            }
+            p3_ptr.push_back(static_cast<int>(gP3.size()));
+          }
+          upload(dP1, gP1, st);
+          upload(dP2, gP2, st);
+          upload(dP3, gP3, st);
+          upload(dPM, gPM, st);
+        }
         ctx->prof.cur_level = l;
         ctx->prof.begin(PC_COMPLEMENT, st);
         launch_complement(DL, st);
@@ -889,7 +944,6 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         ++C->klaunch[PC_COMPLEMENT];
         const int nbat = static_cast<int>(SC.batch_ptr.size()) - 1;
         const int* d_bat = at<int>(mt, o_bat);
-        const PanelItemD* d_pan = at<PanelItemD>(mt, o_pan);
         const SchurTargetD* d_sch = at<SchurTargetD>(mt, o_sch);
         const SchurContribD* d_con = at<SchurContribD>(mt, o_con);
         for (int bi = 0; bi < nbat; ++bi) {
@@ -923,7 +977,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           launch_head2(DL, d_bat + p0, nb, st);
           pf.end(st);
           pf.begin(PC_PANEL, st);
-          launch_panel(DL, d_bat + p0, d_pan + W.panel_ptr[bi], W.panel_ptr[bi + 1] - W.panel_ptr[bi], st);
+          {
+            const int i0 = W.panel_ptr[bi], ni = W.panel_ptr[bi + 1] - i0;
+            launch_gemm(dP1.as<GemmDesc>() + i0, ni, st, tl);
+            launch_gemm(dP2.as<GemmDesc>() + i0, ni, st, tl);
+            launch_gemm(dP3.as<GemmDesc>() + p3_ptr[bi], p3_ptr[bi + 1] - p3_ptr[bi], st, tl);
+            launch_mask(dPM.as<MaskDesc>() + i0, ni, st);
+          }
           pf.end(st);
           pf.begin(PC_SCHUR, st);
           launch_schur(DL, d_sch + W.schur_ptr[bi], W.schur_ptr[bi + 1] - W.schur_ptr[bi], d_con, st);
@@ -932,9 +992,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           C->klaunch[PC_COLNORM] += nn > 0;
           C->klaunch[PC_EIG1] += 3;
           C->klaunch[PC_HEAD] += 4;
-          C->klaunch[PC_PANEL] += W.panel_ptr[bi + 1] > W.panel_ptr[bi];
+          const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
+          C->klaunch[PC_PANEL] += npl;
           C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
-          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + (W.panel_ptr[bi + 1] > W.panel_ptr[bi]) + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
+          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
         }
         const double t_launched = wall();
         CK(cudaGetLastError());

@@ -3,7 +3,9 @@
 //   k_gram   step 0, part 1: Gram of the complement-projected fill-in stack
 //   k_head   step 0, part 2 + step 1 + step 3a: truncation (Jacobi), Qtilde,
 //            rotation of the diagonal block, unpivoted LU, self panels
-//   k_panel  step 2 + step 3b: rotate row/column blocks, Lbar/Ubar panels
+//   panels   step 2 + step 3b (rotations, Lbar/Ubar, lift to the entry frame,
+//            :359-362, :437-438) as k_gemm descriptors with e resolved on
+//            the device from kfin, then k_mask
 //   k_schur  step 3c: Schur products scattered to dense / fill-in targets
 // Reference: proj/include/h2lu/factorization.hpp:260-440.
 #include <cooperative_groups.h>
@@ -669,54 +671,11 @@ __global__ void __launch_bounds__(256) k_head2(DevLevel L, const int* batch_cl, 
 }
 
 // --------------------------------------------------------------------------
-// Step 2 for the off-diagonal blocks of row/column t and step 3b: column
-// item D(t,c) <- Qt^H D, Ubar = L11^{-1} D[:e,:]; row item D(j,t) <- D conj(Qt),
-// Lbar = D[:,:e] U11^{-1}; eliminated rows/columns zeroed (:437-438). For a
-// neighbour eliminated earlier the panel is also lifted back to its
-// level-entry frame (deposit_fill, :359-362).
-__global__ void __launch_bounds__(256) k_panel(DevLevel L, const int* batch_cl, const PanelItemD* items, cplx* gws) {
-  __shared__ cplx sm[kTileSmemCplx];
-  const PanelItemD it = items[blockIdx.x];
-  const int t = batch_cl[it.q];
-  const int bm = L.bmax;
-  const int b = L.bsz[t], e = b - L.kfin[t];
-  const int bn = L.bsz[it.nb];
-  cplx* T = gws + (size_t)blockIdx.x * bm * bm;
-  const cplx* Q = L.chain + L.Qt_off[t];
-  cplx* gD = blk(L.D, it.blk, bm);
-  const cplx* Li = L.chain + L.Linv_off[t];
-  const cplx* Ui = L.chain + L.Uinv_off[t];
-  if (it.side == 0) {  // D(t, c): b x bn
-    cta_gemm_tiled(b, bn, b, 1.0, Q, b, OP_C, gD, b, OP_N, 0.0, T, b, sm);
-    if (e > 0) {
-      cplx* Ub = L.chain + L.Ubar_off[it.entry];  // e x bn
-      cta_gemm_tiled(e, bn, e, 1.0, Li, e, OP_N, T, b, OP_N, 0.0, Ub, e, sm);
-      if (it.lift) cta_gemm_tiled(e, bn, bn, 1.0, Ub, e, OP_N, L.chain + L.Qt_off[it.nb], bn, OP_T, 0.0, L.lift + L.Ubar_off[it.entry], e, sm);
-    }
-    for (int idx = threadIdx.x; idx < b * bn; idx += blockDim.x) {
-      const int i = idx % b, j = idx / b;
-      gD[i + (size_t)j * b] = i < e ? czero() : T[i + (size_t)j * b];
-    }
-  } else {  // D(j, t): bn x b
-    cta_gemm_tiled(bn, b, b, 1.0, gD, bn, OP_N, Q, b, OP_R, 0.0, T, bn, sm);
-    if (e > 0) {
-      cplx* Lb = L.chain + L.Lbar_off[it.entry];  // bn x e
-      cta_gemm_tiled(bn, e, e, 1.0, T, bn, OP_N, Ui, e, OP_N, 0.0, Lb, bn, sm);
-      if (it.lift) cta_gemm_tiled(bn, e, bn, 1.0, L.chain + L.Qt_off[it.nb], bn, OP_N, Lb, bn, OP_N, 0.0, L.lift + L.Lbar_off[it.entry], bn, sm);
-    }
-    for (int idx = threadIdx.x; idx < bn * b; idx += blockDim.x) {
-      const int i = idx % bn, j = idx / bn;
-      gD[i + (size_t)j * bn] = j < e ? czero() : T[i + (size_t)j * bn];
-    }
-  }
-}
-
-// --------------------------------------------------------------------------
 // Step 3c: one CTA per target block (dense or fill-in); the contributions of
 // every cluster of the batch that hits it are summed in a fixed order, then
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
 // 4 x 4 complex micro-tile per thread, K staged through shared memory.
-__global__ void __launch_bounds__(128) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+__global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
   extern __shared__ __align__(16) unsigned char tsm[];
   Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
   const SchurTargetD tg = targets[blockIdx.x];
@@ -790,6 +749,16 @@ __global__ void __launch_bounds__(128) k_schur(DevLevel L, const SchurTargetD* t
 // --------------------------------------------------------------------------
 // Descriptor-driven copy / GEMM (level boundaries: finish_level, merge_permute,
 // root assembly, :445-584 and :637).
+__global__ void __launch_bounds__(256) k_mask(const MaskDesc* descs) {
+  const MaskDesc d = descs[blockIdx.x];
+  const int e = d.e0 - *d.kf;
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < d.m * d.n; idx += gridDim.y * blockDim.x) {
+    const int i = idx % d.m, j = idx / d.m;
+    const bool z = d.mode == 0 ? i < e : j < e;
+    d.dst[i + (size_t)j * d.ld] = z ? czero() : d.src[i + (size_t)j * d.ld];
+  }
+}
+
 // Largest column norm of a fill-in block as it enters W (F's columns, or
 // F's rows for a transposed key): the floor of factorization.hpp:295.
 __global__ void __launch_bounds__(256) k_colnorm(const NormDesc* descs) {
@@ -818,7 +787,7 @@ __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
   }
 }
 
-__global__ void __launch_bounds__(128) k_gemm(const GemmDesc* descs) {
+__global__ void __launch_bounds__(128, 3) k_gemm(const GemmDesc* descs) {
   extern __shared__ __align__(16) unsigned char tsm[];
   Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
   GemmDesc d = descs[blockIdx.x];
@@ -826,6 +795,9 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmDesc* descs) {
   if (d.dyn) {
     const int v = *d.dyn;
     d.m += d.mi * v, d.n += d.ni * v, d.k += d.ki * v;
+    if (d.ldneg & 1) d.lda -= v;
+    if (d.ldneg & 2) d.ldb -= v;
+    if (d.ldneg & 4) d.ldc -= v;
   }
   const int ntr = (d.m + 63) / 64, ntc = (d.n + 63) / 64;
   const bool zero = (d.flag1 && !*d.flag1) || (d.flag2 && !*d.flag2);
@@ -1093,18 +1065,18 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s
   post_launch("k_head2");
 }
 
+void launch_mask(const MaskDesc* d, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_mask<<<dim3(n, 8), 256, 0, s>>>(d);
+  post_launch("k_mask");
+}
+
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
   if (n <= 0) return;
   k_colnorm<<<n, 256, 0, s>>>(d);
   post_launch("k_colnorm");
 }
 
-void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s) {
-  if (nitems <= 0) return;
-  cplx* ws = workspace((size_t)L.bmax * L.bmax * sizeof(cplx) * nitems, s);
-  k_panel<<<nitems, 256, 0, s>>>(L, batch_cl, items, ws);
-  post_launch("k_panel");
-}
 
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;

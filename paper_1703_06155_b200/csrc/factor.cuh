@@ -100,8 +100,17 @@ struct GemmDesc {
   const int* flag2;
   // device-resolved sizes: m += mi * *dyn, n += ni * *dyn, k += ki * *dyn
   const int* dyn;
-  int mi, ni, ki, pad;
+  int mi, ni, ki;
+  int ldneg;  // bits 0/1/2: lda/ldb/ldc -= *dyn
   const int* skipnz;  // if set and *skipnz != 0: the descriptor is skipped (no write)
+};
+// Masked copy T -> D zeroing the eliminated rows (mode 0) or columns (mode
+// 1) of a rotated neighbour block: e = e0 - *kf (cleanup, factorization.hpp:437-438).
+struct MaskDesc {
+  const cplx* src;
+  cplx* dst;
+  int ld, m, n, mode, e0, pad;
+  const int* kf;
 };
 struct NormDesc {
   const cplx* F;
@@ -116,8 +125,8 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
 size_t eig1_ws_bytes(int bmax);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
+void launch_mask(const MaskDesc* d, int n, cudaStream_t s);
 void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
-void launch_panel(const DevLevel& L, const int* batch_cl, const PanelItemD* items, int nitems, cudaStream_t s);
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
