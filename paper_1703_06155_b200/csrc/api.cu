@@ -17,6 +17,8 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
+#include <unordered_map>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -83,6 +85,92 @@ int guarded(h2g_error* err, F&& f) {
 }
 
 // ------------------------------------------------------------ device buffers
+// Stream-ordered block cache in front of cudaMallocAsync. A factorize
+// allocates and frees the same few hundred buffers (per-level chain arenas,
+// Schur/fill pools, descriptor tables) every call; letting the driver pool
+// grow and re-map them measured up to ~0.6 s of host stall per level. Freed
+// blocks go back to a per-stream free list (reuse on the same stream is
+// ordered after every earlier use) and are handed out again best-fit.
+class BlockCache {
+ public:
+  static BlockCache& get() {
+    static BlockCache* c = new BlockCache();  // leaked: outlives static destructors
+    return *c;
+  }
+  static size_t round(size_t n) {
+    const size_t g = n < (1u << 20) ? 512 : (2u << 20);
+    return (n + g - 1) / g * g;
+  }
+  void add_stream(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu_);
+    live_.insert(s);
+  }
+  void remove_stream(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu_);
+    live_.erase(s);
+    auto& fl = free_[s];
+    for (auto& kv : fl) cudaFree(kv.second);
+    free_.erase(s);
+  }
+  void* alloc(size_t n, cudaStream_t s) {
+    const size_t r = round(n);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (live_.count(s)) {
+        auto& fl = free_[s];
+        auto it = fl.lower_bound(r);
+        if (it != fl.end() && it->first <= r + r / 4 + (4u << 20)) {
+          void* p = it->second;
+          fl.erase(it);
+          return p;
+        }
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, r, s);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim();
+      e = cudaMallocAsync(&p, r, s);
+    }
+    if (e != cudaSuccess) throw Error(H2G_ERR_CUDA, std::string("device allocation of ") + std::to_string(n) + " bytes: " + cudaGetErrorString(e));
+    std::lock_guard<std::mutex> g(mu_);
+    size_[p] = r;
+    return p;
+  }
+  void release(void* p, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = size_.find(p);
+    if (it != size_.end() && live_.count(s)) {
+      free_[s].emplace(it->second, p);
+      return;
+    }
+    if (it != size_.end()) size_.erase(it);
+    if (s)
+      cudaFree(p);  // owning stream already destroyed (context torn down first)
+    else
+      cudaFreeAsync(p, s);
+  }
+  // hand every cached block back to the driver (out-of-memory retry)
+  void trim() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto& fs : free_) {
+      for (auto& kv : fs.second) {
+        size_.erase(kv.second);
+        cudaFreeAsync(kv.second, fs.first);
+      }
+      fs.second.clear();
+      cudaStreamSynchronize(fs.first);
+    }
+  }
+
+ private:
+  std::mutex mu_;
+  std::set<cudaStream_t> live_;
+  std::map<cudaStream_t, std::multimap<size_t, void*>> free_;
+  std::unordered_map<void*, size_t> size_;
+};
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -101,7 +189,7 @@ struct DBuf {
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) BlockCache::get().release(p, s);
     p = nullptr;
     bytes = 0;
   }
@@ -110,7 +198,7 @@ struct DBuf {
     s = st;
     bytes = n;
     if (n) {
-      CK(cudaMallocAsync(&p, n, st));
+      p = BlockCache::get().alloc(n, st);
       if (zero) CK(cudaMemsetAsync(p, 0, n, st));
     }
   }
@@ -354,6 +442,7 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
     auto* c = new h2g_context();
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    BlockCache::get().add_stream(c->stream);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaMalloc(&c->d_err, sizeof(DevError)));
@@ -372,6 +461,7 @@ int h2g_context_destroy(h2g_context* ctx) {
   if (!ctx) return H2G_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  BlockCache::get().remove_stream(ctx->stream);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_flag);
   cudaEventDestroy(ctx->ev0);
@@ -600,6 +690,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     const int verbose = std::getenv("H2G_VERBOSE") ? std::atoi(std::getenv("H2G_VERBOSE")) : 0;
     auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     double tlev = wall();
+    auto mark = [&](const char* what) {
+      if (verbose >= 2) std::fprintf(stderr, "[h2g]   %-28s %.4f s\n", what, wall() - tlev);
+    };
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
         const LevelSym& Y = P->levels[li];
@@ -624,11 +717,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) Lbar_off[a] = top, top += (long long)cur.bsz[Y.R_nb[a]] * em;
           for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) Ubar_off[a] = top, top += (long long)cur.bsz[Y.C_nb[a]] * em;
         }
+        mark("offsets");
         auto CL = std::make_unique<ChainLevelHost>();
         CL->level = l;
         CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
         DBuf lift;
         lift.alloc(std::max<long long>(top, 1) * 16, st);
+        mark("chain allocated");
         // ---- per-level device metadata
         Packer pk;
         std::vector<int> posi(nl);
@@ -647,7 +742,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         size_t o_con = pk.add_raw(reinterpret_cast<const SchurContribD*>(W.contrib.data()), W.contrib.size());
         size_t o_fs = pk.add_raw(reinterpret_cast<const SolveTargetD*>(W.fsolve.data()), W.fsolve.size());
         size_t o_fc = pk.add_raw(reinterpret_cast<const SolveContribD*>(W.fcontrib.data()), W.fcontrib.size());
+        mark("meta packed");
         pk.upload(CL->meta, st);
+        mark("meta uploaded");
         const DBuf& mt = CL->meta;
         cur.Vp.alloc((size_t)nl * bb * 16, st, true);
         // ---- step-0 projection / Gram work (static sizes: descriptor GEMMs)
@@ -769,6 +866,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
         // step-0 eigensolver workspace and the compact-WY descriptor GEMMs
         // (sizes resolved on the device from the retained rank r)
+        mark("gram descriptors built");
         DBuf eigws;
         eigws.alloc((size_t)mb * eig1_ws_bytes(bm), st);
         std::vector<GemmDesc> gW;
@@ -936,6 +1034,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           upload(dP3, gP3, st);
           upload(dPM, gPM, st);
         }
+        mark("setup done");
         ctx->prof.cur_level = l;
         ctx->prof.begin(PC_COMPLEMENT, st);
         launch_complement(DL, st);
@@ -1009,6 +1108,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         if (!fex.empty()) CK(cudaMemcpyAsync(fex.data(), DL.fexists, fex.size() * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
 
+        mark("kfin read back");
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
         std::vector<int> rec_order;
@@ -1131,6 +1231,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         for (int t = 0; t < nl; ++t) C->solve_bytes += 16.0 * (double)cur.bsz[t] * cur.bsz[t];  // second Qtilde pass
         C->solve_bytes += 4.0 * 16.0 * (double)S.n;
 
+        mark("records done");
         // ---- merge to level lp (finish_level + merge_permute)
         const LevelSym& YP = P->levels[li + 1];
         LevelData nxt;
@@ -1231,6 +1332,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           if (k1) cd.push_back({T, dst, rows, nxt.bsz[P2], k1, kp, 0, 0});
           if (k2) cd.push_back({T + k1, dst + kfin[2 * P2], rows, nxt.bsz[P2], k2, kp, 0, 0});
         }
+        mark("merge descriptors built");
         DBuf dcd, dg1, dg2;
         upload(dcd, cd, st);
         upload(dg1, g1, st);
@@ -1246,6 +1348,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         if (!fexp.empty()) CK(cudaMemcpyAsync(nxt.fex.p, fexp.data(), fexp.size() * 4, cudaMemcpyHostToDevice, st));
         for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
         CK(cudaGetLastError());
+        mark("merge launched");
         CK(cudaStreamSynchronize(st));  // temporaries die here
 
         if (verbose) std::fprintf(stderr, "[h2g] level %d: merge done at %.3f s\n", l, wall() - tlev);
@@ -1306,6 +1409,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     }
     CK(cudaEventRecord(ctx->ev1, st));
     CK(cudaEventSynchronize(ctx->ev1));
+    if (verbose) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+        uint64_t a = 0, b = 0, c = 0, d = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &a);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &b);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &c);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &d);
+        std::fprintf(stderr, "[h2g] pool reserved %.2f GB (high %.2f), used %.2f GB (high %.2f)\n", a / 1e9, b / 1e9, c / 1e9, d / 1e9);
+      }
+    }
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     C->factor_ms = ms;
