@@ -265,6 +265,11 @@ enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SC
 struct h2g_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // Deferred Schur updates (targets not read by the next batch) run on a
+  // lower-priority side stream, overlapping the next batch's step 0-3b.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_crit = nullptr, ev_bulk = nullptr;
+  Prof prof_side;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevError* d_err = nullptr;
   int* d_flag = nullptr;
@@ -441,7 +446,12 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
     CK(cudaSetDevice(device));
     auto* c = new h2g_context();
     c->device = device;
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+    CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+    CK(cudaEventCreateWithFlags(&c->ev_crit, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_bulk, cudaEventDisableTiming));
     BlockCache::get().add_stream(c->stream);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
@@ -460,8 +470,12 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
 int h2g_context_destroy(h2g_context* ctx) {
   if (!ctx) return H2G_OK;
   cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->side);
   cudaStreamSynchronize(ctx->stream);
   BlockCache::get().remove_stream(ctx->stream);
+  cudaEventDestroy(ctx->ev_crit);
+  cudaEventDestroy(ctx->ev_bulk);
+  cudaStreamDestroy(ctx->side);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_flag);
   cudaEventDestroy(ctx->ev0);
@@ -647,6 +661,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->eps = eps;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), st));
     ctx->prof.reset();
+    ctx->prof_side.reset();
+    ctx->prof_side.on = ctx->prof.on;
     CK(cudaEventRecord(ctx->ev0, st));
     long long launches = 0;
     double flops = 0.0, sflops = 0.0, sbytes = 0.0;
@@ -1084,18 +1100,34 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             launch_mask(dPM.as<MaskDesc>() + i0, ni, st);
           }
           pf.end(st);
-          pf.begin(PC_SCHUR, st);
-          launch_schur(DL, d_sch + W.schur_ptr[bi], W.schur_ptr[bi + 1] - W.schur_ptr[bi], d_con, st);
-          pf.end(st);
+          {
+            // critical targets (rows/columns of the next batch) in-line, after
+            // the previous batch's deferred targets have landed; the rest on
+            // the side stream, overlapping the next batch
+            const int s0 = W.schur_ptr[bi], ncr = W.schur_crit[bi], nbulk = W.schur_ptr[bi + 1] - s0 - ncr;
+            if (bi > 0) CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));
+            pf.begin(PC_SCHUR, st);
+            launch_schur(DL, d_sch + s0, ncr, d_con, st);
+            pf.end(st);
+            CK(cudaEventRecord(ctx->ev_crit, st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->ev_crit, 0));
+            ctx->prof_side.cur_level = l;
+            ctx->prof_side.begin(PC_SCHUR, ctx->side);
+            launch_schur(DL, d_sch + s0 + ncr, nbulk, d_con, ctx->side);
+            ctx->prof_side.end(ctx->side);
+            CK(cudaEventRecord(ctx->ev_bulk, ctx->side));
+            C->klaunch[PC_SCHUR] += (ncr > 0) + (nbulk > 0);
+            launches += (ncr > 0) + (nbulk > 0);
+          }
           C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
           C->klaunch[PC_COLNORM] += nn > 0;
           C->klaunch[PC_EIG1] += 3;
           C->klaunch[PC_HEAD] += 4;
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
-          C->klaunch[PC_SCHUR] += W.schur_ptr[bi + 1] > W.schur_ptr[bi];
-          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl + (W.schur_ptr[bi + 1] > W.schur_ptr[bi]);
+          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
         }
+        CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();
         CK(cudaGetLastError());
         check_device_error(ctx, l);
@@ -1109,6 +1141,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaStreamSynchronize(st));
 
         mark("kfin read back");
+        const double sflops_lv0 = sflops, flops_lv0 = flops;
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
         std::vector<int> rec_order;
@@ -1232,6 +1265,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         C->solve_bytes += 4.0 * 16.0 * (double)S.n;
 
         mark("records done");
+        if (verbose) std::fprintf(stderr, "[h2g] level %d: algorithmic GFLOP total %.1f, Schur %.1f\n", l, (flops - flops_lv0) / 1e9, (sflops - sflops_lv0) / 1e9);
         // ---- merge to level lp (finish_level + merge_permute)
         const LevelSym& YP = P->levels[li + 1];
         LevelData nxt;
@@ -1426,7 +1460,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->factor_launches = launches;
     if (ctx->prof.on) {
       std::map<std::pair<int, int>, double> per;
-      for (const auto& r : ctx->prof.recs) {
+      std::vector<Prof::Rec> all(ctx->prof.recs);
+      all.insert(all.end(), ctx->prof_side.recs.begin(), ctx->prof_side.recs.end());
+      for (const auto& r : all) {
         float e = 0.f;
         cudaEventElapsedTime(&e, r.a, r.b);
         C->kms[r.cls] += e;

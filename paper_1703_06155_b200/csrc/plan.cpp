@@ -334,6 +334,15 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
     SolveContrib c;
   };
   std::vector<STmp> stmp;
+  std::vector<int> batch_of(static_cast<size_t>(L.nl), -1);
+  for (int b = 0; b < nbat; ++b)
+    for (int q = sch.batch_ptr[static_cast<size_t>(b)]; q < sch.batch_ptr[static_cast<size_t>(b) + 1]; ++q)
+      batch_of[static_cast<size_t>(sch.batch_cl[static_cast<size_t>(q)])] = b;
+  auto target_rc = [&](const SchurTarget& T) {
+    if (T.kind == 0) return std::make_pair(L.drow[static_cast<size_t>(T.idx)], L.dcol[static_cast<size_t>(T.idx)]);
+    return std::make_pair(L.frow[static_cast<size_t>(T.idx)], L.fcol[static_cast<size_t>(T.idx)]);
+  };
+  std::vector<SchurTarget> bulk;
   for (int b = 0; b < nbat; ++b) {
     const int p0 = sch.batch_ptr[static_cast<size_t>(b)], p1 = sch.batch_ptr[static_cast<size_t>(b) + 1];
     W.max_batch = std::max(W.max_batch, p1 - p0);
@@ -385,15 +394,25 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
       }
     }
     std::stable_sort(tmp.begin(), tmp.end(), [](const Tmp& x, const Tmp& y) { return x.key < y.key; });
+    bulk.clear();
+    int ncrit = 0;
     for (size_t i = 0; i < tmp.size();) {
       size_t j = i;
       while (j < tmp.size() && tmp[j].key == tmp[i].key) ++j;
       SchurTarget T{static_cast<int32_t>(tmp[i].key >> 40), static_cast<int32_t>(tmp[i].key & ((int64_t(1) << 40) - 1)),
                     static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
       for (size_t k = i; k < j; ++k) W.contrib.push_back(tmp[k].c);
-      W.schur.push_back(T);
+      const auto rc = target_rc(T);
+      if (batch_of[static_cast<size_t>(rc.first)] == b + 1 || batch_of[static_cast<size_t>(rc.second)] == b + 1) {
+        W.schur.push_back(T);
+        ++ncrit;
+      } else {
+        bulk.push_back(T);
+      }
       i = j;
     }
+    W.schur.insert(W.schur.end(), bulk.begin(), bulk.end());
+    W.schur_crit.push_back(ncrit);
     std::stable_sort(stmp.begin(), stmp.end(), [](const STmp& x, const STmp& y) { return x.seg < y.seg; });
     for (size_t i = 0; i < stmp.size();) {
       size_t j = i;

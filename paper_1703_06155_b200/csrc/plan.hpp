@@ -110,6 +110,10 @@ struct LevelWork {
   std::vector<int32_t> panel_ptr;  // per batch
   std::vector<PanelItem> panel;
   std::vector<int32_t> schur_ptr;  // per batch
+  // per batch: the first schur_crit[b] targets of batch b lie in a row or
+  // column of a cluster of batch b+1 (applied in-line on the main stream);
+  // the rest are deferred to the side stream, overlapping batch b+1
+  std::vector<int32_t> schur_crit;
   std::vector<SchurTarget> schur;
   std::vector<SchurContrib> contrib;
   std::vector<int32_t> fsolve_ptr;  // per batch
