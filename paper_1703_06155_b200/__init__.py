@@ -21,7 +21,7 @@ import numpy as np
 from . import geometry  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libh2g.so")
+LIB_PATH = os.environ.get("H2G_LIB", os.path.join(_HERE, "libh2g.so"))
 
 SCHEDULES = {"reference": 0, "colored": 1}
 KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2

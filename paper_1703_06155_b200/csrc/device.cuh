@@ -529,6 +529,84 @@ __device__ inline int sturm_count(int n, const double* d, const double* e, doubl
   return c;
 }
 
+// 1/q to ~1 ulp: hardware reciprocal seed + two Newton steps (a fraction of
+// the latency of a correctly rounded division on the FP64 pipe).
+__device__ __forceinline__ double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Sturm counts at P shifts at once: P independent recurrences interleaved so
+// the dependent FP64 chains overlap. e2[i] = e[i]^2.
+template <int P>
+__device__ __forceinline__ void sturm_count_p(int n, const double* d, const double* e2, const double* x, double pivmin, int* c) {
+  double q[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    q[p] = d[0] - x[p];
+    if (fabs(q[p]) < pivmin) q[p] = -pivmin;
+    c[p] = q[p] < 0.0;
+  }
+  for (int i = 1; i < n; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      q[p] = (di - x[p]) - ei * rcp_nr(q[p]);
+      if (fabs(q[p]) < pivmin) q[p] = -pivmin;
+      c[p] += q[p] < 0.0;
+    }
+  }
+}
+
+// Eigenvalues with descending index j = 0..r-1 (ascending index n-1-j) of T,
+// out[j], by multisection: G lanes of one warp per eigenvalue, 4 shifts per
+// lane, so every round shrinks the bracket (4G+1)-fold; stops at a relative
+// width of 1e-13 like bisect_eig. Whole CTA; no block barriers inside.
+__device__ inline void multisect_top(int n, const double* d, const double* e2, int r, double lo0, double hi0, double pivmin, double* out) {
+  constexpr int P = 4;
+  int G = 32;
+  while (G > 1 && G * r > (int)blockDim.x) G >>= 1;
+  const int slots = blockDim.x / G;
+  const int glane = (threadIdx.x & 31) % G, gid = threadIdx.x / G;
+  const int npts = G * P;
+  for (int j0 = 0; j0 < r; j0 += slots) {
+    const int j = j0 + gid;
+    const bool act = j < r;
+    const int J = n - 1 - j;
+    double lo = lo0, hi = hi0;
+    bool done = !act;
+    for (int it = 0; it < 200; ++it) {
+      if (!done && hi - lo <= 1e-13 * fmax(fabs(lo), fabs(hi))) done = true;
+      if (__all_sync(0xffffffffu, done)) break;
+      double x[P];
+      int c[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = lo + (hi - lo) * (double)(glane * P + p + 1) / (double)(npts + 1);
+      if (!done) {
+        sturm_count_p<P>(n, d, e2, x, pivmin, c);
+      } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p) c[p] = n;
+      }
+      int below = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) below += c[p] <= J;
+      for (int o = G / 2; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+      if (!done) {
+        const double nlo = below == 0 ? lo : lo + (hi - lo) * (double)below / (double)(npts + 1);
+        const double nhi = below == npts ? hi : lo + (hi - lo) * (double)(below + 1) / (double)(npts + 1);
+        if (nlo == lo && nhi == hi) done = true;
+        lo = fmax(lo, nlo), hi = fmin(hi, nhi);
+      }
+    }
+    if (act && glane == 0) out[j] = 0.5 * (lo + hi);
+  }
+}
+
 // Eigenvalue with ascending index j of T by bisection on [lo, hi].
 __device__ inline double bisect_eig(int n, const double* d, const double* e, int j, double lo, double hi, double pivmin) {
   for (int it = 0; it < 200; ++it) {
@@ -673,97 +751,81 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g, bool valid
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 
-__device__ __forceinline__ void tile128_load(Tile128Smem& S, int buf, const cplx* A, int lda, int opA, int ash, int am, const cplx* B, int ldb,
-                                             int opB, int bsh, int bn, int k, int k0) {
-  const bool a_rm = opA == OP_T || opA == OP_C;
-  const bool b_rm = opB == OP_N || opB == OP_R;
-  for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
-    int i, p;
-    if (a_rm) p = idx % 8, i = idx / 8;
-    else i = idx % 64, p = idx / 64;
-    const int ai = i + ash;
-    S.a[buf][p][i] = (k0 + p < k && ai >= 0 && ai < am) ? ld_op(A, lda, opA, ai, k0 + p) : czero();
-    int j, q;
-    if (b_rm) q = idx % 8, j = idx / 8;
-    else j = idx % 64, q = idx / 64;
-    const int bj = j + bsh;
-    S.b[buf][q][j] = (k0 + q < k && bj >= 0 && bj < bn) ? ld_op(B, ldb, opB, k0 + q, bj) : czero();
-  }
-}
-
 // acc[tile row i][tile col j] += sum_p op(A)[i + ash, p] op(B)[p, j + bsh]
 // (rows outside [0, am) / cols outside [0, bn) of op(A) / op(B) read as zero).
-// Plain (N, N) operands stream through a 3-stage cp.async pipeline (25.7
-// TFLOP/s in tests/cuda/gemm_bench.cu); other ops stage through registers.
-__device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B,
-                                            int ldb, int opB, int bsh, int bn, int k) {
+// Every operand form streams through a 3-stage cp.async pipeline (one 16-byte
+// complex per cp.async, so transposed operands need no register staging);
+// conjugation is applied when the k-slice is read from shared memory.
+template <bool CA, bool CB>
+__device__ __forceinline__ void tile128_pipe(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, bool at, int ash, int am, const cplx* B,
+                                             int ldb, bool bt, int bsh, int bn, int k) {
   const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
-  if (k <= 0) return;
   const int nk = (k + 7) / 8;
-  if (opA == OP_N && opB == OP_N) {
-    __syncthreads();
-    auto load = [&](int st, int kc) {
-      const int k0 = kc * 8;
-      for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
-        const int i = idx % 64, p = idx / 64;
-        const int ai = i + ash;
-        const bool va = k0 + p < k && ai >= 0 && ai < am;
-        cp_async16(&S.a[st][p][i], va ? A + ai + (size_t)(k0 + p) * lda : A, va);
-        const int q = idx % 8, j = idx / 8;
-        const int bj = j + bsh;
-        const bool vb = k0 + q < k && bj >= 0 && bj < bn;
-        cp_async16(&S.b[st][q][j], vb ? B + (k0 + q) + (size_t)bj * ldb : B, vb);
-      }
-      cp_async_commit();
-    };
-    for (int st = 0; st < 2; ++st) {
-      if (st < nk) load(st, st);
-      else cp_async_commit();
+  __syncthreads();
+  auto load = [&](int st, int kc) {
+    const int k0 = kc * 8;
+    for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+      // op(A)(i, p): column-major A[i + p lda] (N/R) or A[p + i lda] (T/C)
+      int i, p;
+      if (at) p = idx % 8, i = idx / 8;
+      else i = idx % 64, p = idx / 64;
+      const int ai = i + ash;
+      const bool va = k0 + p < k && ai >= 0 && ai < am;
+      const cplx* ga = at ? A + (k0 + p) + (size_t)ai * lda : A + ai + (size_t)(k0 + p) * lda;
+      cp_async16(&S.a[st][p][i], va ? ga : A, va);
+      // op(B)(q, j): B[q + j ldb] (N/R) or B[j + q ldb] (T/C)
+      int j, q;
+      if (bt) j = idx % 64, q = idx / 64;
+      else q = idx % 8, j = idx / 8;
+      const int bj = j + bsh;
+      const bool vb = k0 + q < k && bj >= 0 && bj < bn;
+      const cplx* gb = bt ? B + bj + (size_t)(k0 + q) * ldb : B + (k0 + q) + (size_t)bj * ldb;
+      cp_async16(&S.b[st][q][j], vb ? gb : B, vb);
     }
-    for (int kc = 0; kc < nk; ++kc) {
-      asm volatile("cp.async.wait_group 1;");
-      __syncthreads();
-      const int st = kc % 3;
-      if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
-      else cp_async_commit();
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        cplx av[8], bv[4];
-#pragma unroll
-        for (int a = 0; a < 8; ++a) av[a] = S.a[st][p][tr + 8 * a];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) bv[b] = S.b[st][p][tc * 4 + b];
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
-      }
-    }
-    asm volatile("cp.async.wait_group 0;");
-    __syncthreads();
-    return;
+    cp_async_commit();
+  };
+  for (int st = 0; st < 2; ++st) {
+    if (st < nk) load(st, st);
+    else cp_async_commit();
   }
-  __syncthreads();
-  tile128_load(S, 0, A, lda, opA, ash, am, B, ldb, opB, bsh, bn, k, 0);
-  __syncthreads();
-  int buf = 0;
-  for (int k0 = 0; k0 < k; k0 += 8) {
-    if (k0 + 8 < k) tile128_load(S, buf ^ 1, A, lda, opA, ash, am, B, ldb, opB, bsh, bn, k, k0 + 8);
-#pragma unroll 4
+  for (int kc = 0; kc < nk; ++kc) {
+    asm volatile("cp.async.wait_group 1;");
+    __syncthreads();
+    const int st = kc % 3;
+    if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
+    else cp_async_commit();
+#pragma unroll
     for (int p = 0; p < 8; ++p) {
       cplx av[8], bv[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) av[a] = S.a[buf][p][tr + 8 * a];
+      for (int a = 0; a < 8; ++a) {
+        av[a] = S.a[st][p][tr + 8 * a];
+        if (CA) av[a].y = -av[a].y;
+      }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = S.b[buf][p][tc * 4 + b];
+      for (int b = 0; b < 4; ++b) {
+        bv[b] = S.b[st][p][tc * 4 + b];
+        if (CB) bv[b].y = -bv[b].y;
+      }
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
     }
-    __syncthreads();
-    buf ^= 1;
   }
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B,
+                                            int ldb, int opB, int bsh, int bn, int k) {
+  if (k <= 0) return;
+  const bool at = opA == OP_T || opA == OP_C, bt = opB == OP_T || opB == OP_C;
+  const bool ca = opA == OP_C || opA == OP_R, cb = opB == OP_C || opB == OP_R;
+  if (!ca && !cb) tile128_pipe<false, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (ca && !cb) tile128_pipe<true, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (!ca && cb) tile128_pipe<false, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else tile128_pipe<true, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
 }
 
 }  // namespace h2g

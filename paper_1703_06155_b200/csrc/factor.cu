@@ -274,31 +274,31 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     s_piv = 2.2250738585072014e-308 * fmax(1.0, emax);
   }
   __syncthreads();
-  // largest eigenvalue by multisection: every thread tests one point of the
-  // current bracket, so each round shrinks it blockDim.x-fold
+  // largest eigenvalue by multisection: every thread tests 4 points of the
+  // current bracket, so each round shrinks it (4 blockDim.x + 1)-fold
+  double* e2 = ed + m;
+  for (int i = threadIdx.x; i + 1 < m; i += blockDim.x) e2[i] = ed[i] * ed[i];
   {
+    constexpr int P = 4;
     __shared__ double s_a, s_b;
-    __shared__ int s_cnt[256];
     if (threadIdx.x == 0) s_a = s_lo, s_b = s_hi;
     __syncthreads();
+    const int npts = blockDim.x * P;
     for (int round = 0; round < 12; ++round) {
       const double a = s_a, bnd = s_b;
       if (bnd - a <= 2e-16 * fmax(fabs(a), fabs(bnd))) break;
-      const double x = a + (bnd - a) * (threadIdx.x + 1) / (blockDim.x + 1);
-      s_cnt[threadIdx.x] = sturm_count(m, dg, ed, x, s_piv);  // #eigenvalues below x
-      __syncthreads();
+      double x[P];
+      int c[P];
+#pragma unroll
+      for (int pp = 0; pp < P; ++pp) x[pp] = a + (bnd - a) * (double)(threadIdx.x * P + pp + 1) / (double)(npts + 1);
+      sturm_count_p<P>(m, dg, e2, x, s_piv, c);  // #eigenvalues below x
+      // points below which fewer than m eigenvalues lie (monotone in x)
+      int below = 0;
+#pragma unroll
+      for (int pp = 0; pp < P; ++pp) below += __syncthreads_count(c[pp] < m);
       if (threadIdx.x == 0) {
-        // smallest point below which all m eigenvalues lie -> new upper bound
-        double na = a, nb2 = bnd;
-        for (int j = 0; j < (int)blockDim.x; ++j) {
-          const double xj = a + (bnd - a) * (j + 1) / (blockDim.x + 1);
-          if (s_cnt[j] >= m) {
-            nb2 = xj;
-            break;
-          }
-          na = xj;
-        }
-        s_a = na, s_b = nb2;
+        s_a = below == 0 ? a : a + (bnd - a) * (double)below / (double)(npts + 1);
+        s_b = below == npts ? bnd : a + (bnd - a) * (double)(below + 1) / (double)(npts + 1);
       }
       __syncthreads();
     }
@@ -318,18 +318,17 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     s_lo = lo, s_hi = hi, s_piv = pivmin, s_s0 = s0, s_thr = thr;
     // the Gram resolves eigenvalues to ~eps_mach * lmax: below ~1e-4 sigma_0
     // the truncation needs the refinement pass (k_eig1_refine)
-    s_need = s0 > 0.0 && thr < 1e-4 * s0;
+    s_need = s0 > 0.0 && (thr < 1e-4 * s0 || (L.debug & 4));  // debug bit 2: always refine
   }
   __syncthreads();
   const int r = s_r;
-  if (!s_need)
-    for (int j = threadIdx.x; j < r; j += blockDim.x) aux[2 * bm + j] = bisect_eig(m, dg, ed, m - 1 - j, s_lo, s_hi, s_piv);
+  if (!s_need) multisect_top(m, dg, e2, r, s_lo, s_hi, s_piv, aux + 2 * bm);
   if (threadIdx.x == 0) {
     L.pass2[q] = s_need ? 2 : 0;  // 2: refinement requested
     L.rank1[q] = r;
     L.cmax[q] = cmax;
     L.lam[(size_t)q * bm] = s_s0;
-    if (L.debug) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d%s\n", L.level, t, m, cmax, s_s0, s_thr, r, s_need ? " (refine)" : "");
+    if (L.debug & 1) printf("[h2g] eig1 level %d cluster %d m %d cmax %.3e s0 %.3e thr %.3e r %d%s\n", L.level, t, m, cmax, s_s0, s_thr, r, s_need ? " (refine)" : "");
   }
 }
 
@@ -592,7 +591,7 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
         while (r < m && lam[ord[r]] > thr) ++r;
       }
       s_r = r;
-      if (L.debug) printf("[h2g] pass2 level %d cluster %d m %d s0 %.3e r %d\n", L.level, t, m, s0, r);
+      if (L.debug & 1) printf("[h2g] pass2 level %d cluster %d m %d s0 %.3e r %d\n", L.level, t, m, s0, r);
     }
     __syncthreads();
     // directions D1 Uc (b x m) into T
