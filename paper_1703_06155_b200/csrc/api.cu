@@ -781,7 +781,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         std::vector<BDesc> bdesc;
         std::vector<int> ndesc_f;  // fill index per colnorm entry
         long long ymax = 1, gmax = 1;
-        const int kPartW = 512;
+        // Gram partials: K split so that small Grams still spread over many CTAs
+        const int kPartW = bm <= 32 ? 128 : (bm <= 64 ? 256 : 512);
         for (int bi = 0; bi < nbat0; ++bi) {
           long long ytop = 0, gtop = 0;
           for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) {
@@ -1066,7 +1067,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
           Prof& pf = ctx->prof;
           pf.begin(PC_GRAM, st);
-          const int tl = ((bm + 63) / 64) * ((bm + 63) / 64);
+          const int tl = bm;  // max GEMM dimension of this level's per-cluster products
           launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st, tl);
           launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
           pf.end(st);
@@ -1373,7 +1374,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         upload(dg2, g2, st);
         ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
-        const int tlm = ((std::max(bm, nxt.bmax) + 63) / 64) * ((std::max(bm, nxt.bmax) + 63) / 64);
+        const int tlm = std::max(bm, nxt.bmax);
         launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, tlm);
         launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, tlm);
         ctx->prof.end(st);

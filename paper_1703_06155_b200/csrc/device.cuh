@@ -739,10 +739,15 @@ namespace h2g {
 // 8 at a time, double-buffered. acc += op(A)[0:64, 0:k] op(B)[0:k, 0:64] with
 // rows >= mv / cols >= nv treated as zero. A/B point at the tile origin.
 // Measured 20 TFLOP/s on a 4096 x 4096 x 512 ZGEMM (tests/cuda/gemm_bench.cu).
-struct Tile128Smem {
-  cplx a[3][8][64];
-  cplx b[3][8][64];
+// 3-stage k-slices (8 deep) of a TM x TM output tile computed by 128 threads;
+// thread (tr, tc) = (tid % 8, tid / 8) owns rows tr + 8a (a < TM/8) and
+// columns tc * (TM/16) + b.
+template <int TM>
+struct TileSmem {
+  cplx a[3][8][TM];
+  cplx b[3][8][TM];
 };
+using Tile128Smem = TileSmem<64>;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -756,26 +761,27 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 // Every operand form streams through a 3-stage cp.async pipeline (one 16-byte
 // complex per cp.async, so transposed operands need no register staging);
 // conjugation is applied when the k-slice is read from shared memory.
-template <bool CA, bool CB>
-__device__ __forceinline__ void tile128_pipe(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, bool at, int ash, int am, const cplx* B,
-                                             int ldb, bool bt, int bsh, int bn, int k) {
+template <int TM, bool CA, bool CB>
+__device__ __forceinline__ void tile_pipe(cplx (&acc)[TM / 8][TM / 16], TileSmem<TM>& S, const cplx* A, int lda, bool at, int ash, int am,
+                                          const cplx* B, int ldb, bool bt, int bsh, int bn, int k) {
+  constexpr int RM = TM / 8, RN = TM / 16;
   const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
   const int nk = (k + 7) / 8;
   __syncthreads();
   auto load = [&](int st, int kc) {
     const int k0 = kc * 8;
-    for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+    for (int idx = threadIdx.x; idx < TM * 8; idx += 128) {
       // op(A)(i, p): column-major A[i + p lda] (N/R) or A[p + i lda] (T/C)
       int i, p;
       if (at) p = idx % 8, i = idx / 8;
-      else i = idx % 64, p = idx / 64;
+      else i = idx % TM, p = idx / TM;
       const int ai = i + ash;
       const bool va = k0 + p < k && ai >= 0 && ai < am;
       const cplx* ga = at ? A + (k0 + p) + (size_t)ai * lda : A + ai + (size_t)(k0 + p) * lda;
       cp_async16(&S.a[st][p][i], va ? ga : A, va);
       // op(B)(q, j): B[q + j ldb] (N/R) or B[j + q ldb] (T/C)
       int j, q;
-      if (bt) j = idx % 64, q = idx / 64;
+      if (bt) j = idx % TM, q = idx / TM;
       else q = idx % 8, j = idx / 8;
       const int bj = j + bsh;
       const bool vb = k0 + q < k && bj >= 0 && bj < bn;
@@ -796,36 +802,44 @@ __device__ __forceinline__ void tile128_pipe(cplx (&acc)[8][4], Tile128Smem& S, 
     else cp_async_commit();
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
-      cplx av[8], bv[4];
+      cplx av[RM], bv[RN];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
+      for (int a = 0; a < RM; ++a) {
         av[a] = S.a[st][p][tr + 8 * a];
         if (CA) av[a].y = -av[a].y;
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        bv[b] = S.b[st][p][tc * 4 + b];
+      for (int b = 0; b < RN; ++b) {
+        bv[b] = S.b[st][p][tc * RN + b];
         if (CB) bv[b].y = -bv[b].y;
       }
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < RM; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cfma(acc[a][b], av[a], bv[b]);
+        for (int b = 0; b < RN; ++b) cfma(acc[a][b], av[a], bv[b]);
     }
   }
   asm volatile("cp.async.wait_group 0;");
   __syncthreads();
 }
 
-__device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B,
-                                            int ldb, int opB, int bsh, int bn, int k) {
+// acc[tile row i][tile col j] += sum_p op(A)[i + ash, p] op(B)[p, j + bsh]
+// (rows outside [0, am) / cols outside [0, bn) of op(A) / op(B) read as zero).
+template <int TM>
+__device__ __forceinline__ void tile_acc(cplx (&acc)[TM / 8][TM / 16], TileSmem<TM>& S, const cplx* A, int lda, int opA, int ash, int am,
+                                         const cplx* B, int ldb, int opB, int bsh, int bn, int k) {
   if (k <= 0) return;
   const bool at = opA == OP_T || opA == OP_C, bt = opB == OP_T || opB == OP_C;
   const bool ca = opA == OP_C || opA == OP_R, cb = opB == OP_C || opB == OP_R;
-  if (!ca && !cb) tile128_pipe<false, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
-  else if (ca && !cb) tile128_pipe<true, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
-  else if (!ca && cb) tile128_pipe<false, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
-  else tile128_pipe<true, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  if (!ca && !cb) tile_pipe<TM, false, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (ca && !cb) tile_pipe<TM, true, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (!ca && cb) tile_pipe<TM, false, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else tile_pipe<TM, true, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+}
+
+__device__ __forceinline__ void tile128_acc(cplx (&acc)[8][4], Tile128Smem& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B,
+                                            int ldb, int opB, int bsh, int bn, int k) {
+  tile_acc<64>(acc, S, A, lda, opA, ash, am, B, ldb, opB, bsh, bn, k);
 }
 
 }  // namespace h2g

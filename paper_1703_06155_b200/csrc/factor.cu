@@ -786,9 +786,11 @@ __global__ void __launch_bounds__(256) k_copy(const CopyDesc* descs) {
   }
 }
 
+template <int TM>
 __global__ void __launch_bounds__(128, 3) k_gemm(const GemmDesc* descs) {
+  constexpr int RM = TM / 8, RN = TM / 16;
   extern __shared__ __align__(16) unsigned char tsm[];
-  Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
+  TileSmem<TM>& S = *reinterpret_cast<TileSmem<TM>*>(tsm);
   GemmDesc d = descs[blockIdx.x];
   if (d.skipnz && *d.skipnz) return;
   if (d.dyn) {
@@ -798,25 +800,23 @@ __global__ void __launch_bounds__(128, 3) k_gemm(const GemmDesc* descs) {
     if (d.ldneg & 2) d.ldb -= v;
     if (d.ldneg & 4) d.ldc -= v;
   }
-  const int ntr = (d.m + 63) / 64, ntc = (d.n + 63) / 64;
+  const int ntr = (d.m + TM - 1) / TM, ntc = (d.n + TM - 1) / TM;
   const bool zero = (d.flag1 && !*d.flag1) || (d.flag2 && !*d.flag2);
   const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
   // each CTA walks the tiles blockIdx.y, blockIdx.y + gridDim.y, ...
   for (int tile = blockIdx.y; tile < ntr * ntc; tile += gridDim.y) {
-    const int r0 = (tile % ntr) * 64, c0 = (tile / ntr) * 64;
-    cplx acc[8][4];
+    const int r0 = (tile % ntr) * TM, c0 = (tile / ntr) * TM;
+    cplx acc[RM][RN];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < RM; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = czero();
-    if (!zero) {
-      tile128_acc(acc, S, d.A, d.lda, d.opA, r0, d.m, d.B, d.ldb, d.opB, c0, d.n, d.k);
-    }
+      for (int b = 0; b < RN; ++b) acc[a][b] = czero();
+    if (!zero) tile_acc<TM>(acc, S, d.A, d.lda, d.opA, r0, d.m, d.B, d.ldb, d.opB, c0, d.n, d.k);
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < RM; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + b;
+      for (int b = 0; b < RN; ++b) {
+        const int i = r0 + tr + 8 * a, j = c0 + tc * RN + b;
         if (i < d.m && j < d.n) {
           cplx* o = d.C + i + (size_t)j * d.ldc;
           const cplx v = acc[a][b];
@@ -992,7 +992,7 @@ size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_s
 
 size_t eig1_ws_bytes(int bmax) { return eig1_ws_cplx(bmax) * sizeof(cplx); }
 
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int tiles, cudaStream_t s,
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int maxdim, cudaStream_t s,
                  const std::function<void(int)>& phase) {
   cplx* ws = L.eigws;
   {
@@ -1041,12 +1041,12 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   set_smem((const void*)k_eig1b, (size_t)L.bmax * 16 * sizeof(cplx));
   k_eig1b<<<nb, 256, (size_t)L.bmax * 16 * sizeof(cplx), s>>>(L, batch_cl, ws);
   post_launch("k_eig1b");
-  launch_gemm(wy, nb, s, tiles);              // S = Y^H Y
+  launch_gemm(wy, nb, s, maxdim);              // S = Y^H Y
   k_eig1t<<<nb, 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_eig1t");
-  launch_gemm(wy + nb, nb, s, tiles);         // X1 = Vp Y
-  launch_gemm(wy + 2 * nb, nb, s, tiles);     // X2 = X1 T
-  launch_gemm(wy + 3 * nb, nb, s, tiles);     // D1 -= X2 Y^H
+  launch_gemm(wy + nb, nb, s, maxdim);         // X1 = Vp Y
+  launch_gemm(wy + 2 * nb, nb, s, maxdim);     // X2 = X1 T
+  launch_gemm(wy + 3 * nb, nb, s, maxdim);     // D1 -= X2 Y^H
 }
 
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {
@@ -1089,10 +1089,24 @@ void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {
   if (n > 0) k_copy<<<n, 256, 0, s>>>(d); post_launch("k_copy");
 }
 
-void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int tiles) {
-  set_smem((const void*)k_gemm, sizeof(Tile128Smem));
-  if (n > 0) k_gemm<<<dim3(n, std::max(1, std::min(tiles, 16))), 128, sizeof(Tile128Smem), s>>>(d);
+// maxdim: upper bound of max(m, n) over the descriptors (0: unknown). Small
+// blocks run on 32 x 32 / 16 x 16 tiles instead of wasting a 64 x 64 tile.
+template <int TM>
+static void launch_gemm_tm(const GemmDesc* d, int n, cudaStream_t s, int maxdim) {
+  set_smem((const void*)k_gemm<TM>, sizeof(TileSmem<TM>));
+  const int t = maxdim > 0 ? (maxdim + TM - 1) / TM : 1;
+  k_gemm<TM><<<dim3(n, std::max(1, std::min(t * t, 16))), 128, sizeof(TileSmem<TM>), s>>>(d);
   post_launch("k_gemm");
+}
+
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim) {
+  if (n <= 0) return;
+  if (maxdim > 0 && maxdim <= 16)
+    launch_gemm_tm<16>(d, n, s, maxdim);
+  else if (maxdim > 0 && maxdim <= 32)
+    launch_gemm_tm<32>(d, n, s, maxdim);
+  else
+    launch_gemm_tm<64>(d, n, s, maxdim);
 }
 
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches) {

@@ -120,7 +120,7 @@ struct NormDesc {
 };
 
 void launch_complement(const DevLevel& L, cudaStream_t s);
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int tiles, cudaStream_t s,
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int maxdim, cudaStream_t s,
                  const std::function<void(int)>& phase);
 size_t eig1_ws_bytes(int bmax);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
@@ -130,7 +130,7 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
-void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int tiles = 1);
+void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim = 0);
 void launch_zero_desc_flags(int* p, int n, cudaStream_t s);
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches);
 size_t head_smem_bytes(int bmax);
