@@ -1090,7 +1090,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           launch_head(DL, d_bat + p0, p0, nb, st);
           launch_gemm(dR1.as<GemmDesc>() + p0, nb, st, tl);
           launch_gemm(dR2.as<GemmDesc>() + p0, nb, st, tl);
-          launch_head2(DL, d_bat + p0, nb, st);
+          launch_head2(DL, d_bat + p0, nb, mmax, st);
           pf.end(st);
           pf.begin(PC_PANEL, st);
           {
@@ -1122,11 +1122,14 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
           C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
           C->klaunch[PC_COLNORM] += nn > 0;
-          C->klaunch[PC_EIG1] += 3;
-          C->klaunch[PC_HEAD] += 4;
+          C->klaunch[PC_EIG1] += 2;
+          C->klaunch[PC_EIGVEC] += mmax > 0;
+          C->klaunch[PC_EIG1B] += 6;
+          const int nhead = 3 + (mmax > 64 ? 2 + 2 * ((mmax + 31) / 32) : 1);
+          C->klaunch[PC_HEAD] += nhead;
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
-          launches += 9 + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
+          launches += 8 + (mmax > 0) + nhead + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();

@@ -670,6 +670,188 @@ __global__ void __launch_bounds__(256) k_head2(DevLevel L, const int* batch_cl, 
 }
 
 // --------------------------------------------------------------------------
+// Step 3a for large heads (e > 64) as a multi-CTA blocked LU on the extended
+// matrix M = [[D, I_e], [I_e, 0]] (D the rotated b x b diagonal block, I_e
+// identities on the first e rows / columns). Eliminating only the first e
+// pivots right-looking gives, in place (factorization.hpp:390-420):
+//   M[:e, :e] = L11 \ U11 (1e-13 relative pivot test, dense_kernels.hpp:70-93)
+//   M[e:b, :e] = D21 U11^{-1} (Lself),   M[:e, e:b] = L11^{-1} D12 (Uself)
+//   M[e:b, e:b] = D22 - Lself Uself (self Schur),
+//   M[:e, b:b+e] = L11^{-1},            M[b:b+e, :e] = U11^{-1},
+// so the triangular inverses and self panels come out of the same trailing
+// GEMM updates. Per 32-wide panel: k_hlu_panel (diagonal block + row/column
+// triangular solves) and k_hlu_update (trailing GEMM over every CTA).
+__global__ void __launch_bounds__(256) k_hlu_prep(DevLevel L, const int* batch_cl, cplx* M0, int ldm, double* scale, int* fail) {
+  __shared__ double red[32];
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], e = b - L.kfin[t];
+  if (e == 0) return;
+  const int N = b + e;
+  cplx* M = M0 + (size_t)q * ldm * ldm;
+  const cplx* Dd = blk(L.D, L.diag_blk[t], L.bmax);
+  double mx = 0.0;
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.y * blockDim.x) {
+    const int i = idx % N, j = idx / N;
+    cplx v;
+    if (i < b && j < b) {
+      v = Dd[i + (size_t)j * b];
+      if (i < e && j < e) mx = fmax(mx, cabsd(v));
+    } else if (i < b) {
+      v = (i == j - b) ? cone() : czero();
+    } else {
+      v = (i - b == j) ? cone() : czero();
+    }
+    M[i + (size_t)j * ldm] = v;
+  }
+  mx = cta_max(mx, red);
+  if (threadIdx.x == 0) {
+    atomicMax(reinterpret_cast<unsigned long long*>(scale + q), __double_as_longlong(mx));
+    if (blockIdx.y == 0) fail[q] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const double* scale, int* fail, int j0) {
+  __shared__ cplx P[32][33];
+  __shared__ int s_fail;
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], e = b - L.kfin[t];
+  if (j0 >= e || fail[q]) return;
+  const int kb = min(32, e - j0), N = b + e;
+  cplx* M = M0 + (size_t)q * ldm * ldm;
+  const double tol = 1e-13 * scale[q];
+  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+    const int i = idx % kb, j = idx / kb;
+    P[i][j] = M[(j0 + i) + (size_t)(j0 + j) * ldm];
+  }
+  if (threadIdx.x == 0) s_fail = -1;
+  __syncthreads();
+  for (int k = 0; k < kb; ++k) {
+    const cplx piv = P[k][k];
+    const double pa = cabsd(piv);
+    if (pa < tol || (scale[q] == 0.0)) {
+      if (threadIdx.x == 0) {
+        raise_error(L.err, 4, (1 << L.level) - 1 + t, L.level, j0 + k, pa);
+        fail[q] = 1;
+      }
+      return;  // uniform
+    }
+    for (int i = k + 1 + threadIdx.x; i < kb; i += blockDim.x) P[i][k] = cdiv(P[i][k], piv);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (kb - k - 1) * (kb - k - 1); idx += blockDim.x) {
+      const int i = k + 1 + idx % (kb - k - 1), j = k + 1 + idx / (kb - k - 1);
+      P[i][j] = csub(P[i][j], cmul(P[i][k], P[k][j]));
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+    const int i = idx % kb, j = idx / kb;
+    M[(j0 + i) + (size_t)(j0 + j) * ldm] = P[i][j];
+  }
+  // rows below the panel: x U = a (L21); columns right of it: L y = c (U12)
+  const int rest = N - j0 - kb;
+  for (int it = threadIdx.x; it < 2 * rest; it += blockDim.x) {
+    cplx x[32];
+    if (it < rest) {
+      cplx* row = M + (j0 + kb + it) + (size_t)j0 * ldm;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k < kb) x[k] = row[(size_t)k * ldm];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k >= kb) break;
+        cplx a = x[k];
+        for (int l = 0; l < k; ++l) a = csub(a, cmul(x[l], P[l][k]));
+        x[k] = cdiv(a, P[k][k]);
+        row[(size_t)k * ldm] = x[k];
+      }
+    } else {
+      cplx* col = M + j0 + (size_t)(j0 + kb + it - rest) * ldm;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k < kb) x[k] = col[k];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k >= kb) break;
+        cplx a = x[k];
+        for (int l = 0; l < k; ++l) a = csub(a, cmul(P[k][l], x[l]));
+        x[k] = a;
+        col[k] = a;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 3) k_hlu_update(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const int* fail, int j0) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], e = b - L.kfin[t];
+  if (j0 >= e || fail[q]) return;
+  const int kb = min(32, e - j0), N = b + e, c = j0 + kb, rest = N - c;
+  const int nt = (rest + 63) / 64;
+  cplx* M = M0 + (size_t)q * ldm * ldm;
+  for (int tile = blockIdx.y; tile < nt * nt; tile += gridDim.y) {
+    const int r0 = (tile % nt) * 64, c0 = (tile / nt) * 64;
+    cplx acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
+    tile128_acc(acc, S, M + c + (size_t)j0 * ldm, ldm, OP_N, r0, rest, M + j0 + (size_t)c * ldm, ldm, OP_N, c0, rest, kb);
+    const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + bb;
+        if (i < rest && j < rest) {
+          cplx* o = M + (c + i) + (size_t)(c + j) * ldm;
+          *o = csub(*o, acc[a][bb]);
+        }
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch_cl, const cplx* M0, int ldm, const int* fail) {
+  const int q = blockIdx.x;
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], kf = L.kfin[t], e = b - kf;
+  if (e == 0 || fail[q]) return;
+  const cplx* M = M0 + (size_t)q * ldm * ldm;
+  cplx* L11 = L.chain + L.L11_off[t];
+  cplx* U11 = L.chain + L.U11_off[t];
+  cplx* Li = L.chain + L.Linv_off[t];
+  cplx* Ui = L.chain + L.Uinv_off[t];
+  cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
+  cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
+  cplx* Dd = blk(L.D, L.diag_blk[t], L.bmax);
+  const int stride = gridDim.y * blockDim.x;
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < e * e; idx += stride) {
+    const int i = idx % e, j = idx / e;
+    const cplx v = M[i + (size_t)j * ldm];
+    L11[idx] = i > j ? v : (i == j ? cone() : czero());
+    U11[idx] = i <= j ? v : czero();
+    Li[idx] = i >= j ? M[i + (size_t)(b + j) * ldm] : czero();
+    Ui[idx] = i <= j ? M[(b + i) + (size_t)j * ldm] : czero();
+  }
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < e * kf; idx += stride) {
+    const int i = idx % e, j = idx / e;
+    Us[idx] = M[i + (size_t)(e + j) * ldm];
+  }
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < kf * e; idx += stride) {
+    const int i = idx % kf, j = idx / kf;
+    Ls[idx] = M[(e + i) + (size_t)j * ldm];
+  }
+  for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < b * b; idx += stride) {
+    const int i = idx % b, j = idx / b;
+    Dd[i + (size_t)j * b] = (i < e || j < e) ? ((i == j) ? cone() : czero()) : M[i + (size_t)j * ldm];
+  }
+}
+
+// --------------------------------------------------------------------------
 // Step 3c: one CTA per target block (dense or fill-in); the contributions of
 // every cluster of the batch that hits it are summed in a fixed order, then
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
@@ -1058,7 +1240,30 @@ void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStr
   post_launch("k_head");
 }
 
-void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s) {
+void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cudaStream_t s) {
+  if (emax > 64) {
+    // multi-CTA extended LU (k_hlu_*); M per slot is (b + e)^2 <= (2 bmax)^2
+    const int ldm = 2 * L.bmax;
+    const size_t mbytes = (size_t)ldm * ldm * sizeof(cplx);
+    char* ws = reinterpret_cast<char*>(workspace(mbytes * nb + (size_t)nb * 16 + 64, s));
+    cplx* M0 = reinterpret_cast<cplx*>(ws);
+    double* scale = reinterpret_cast<double*>(ws + mbytes * nb);
+    int* fail = reinterpret_cast<int*>(scale + nb);
+    cudaMemsetAsync(scale, 0, (size_t)nb * sizeof(double), s);
+    k_hlu_prep<<<dim3(nb, 16), 256, 0, s>>>(L, batch_cl, M0, ldm, scale, fail);
+    post_launch("k_hlu_prep");
+    set_smem((const void*)k_hlu_update, sizeof(Tile128Smem));
+    const int nt = (ldm + 63) / 64;
+    for (int j0 = 0; j0 < emax; j0 += 32) {
+      k_hlu_panel<<<nb, 256, 0, s>>>(L, batch_cl, M0, ldm, scale, fail, j0);
+      post_launch("k_hlu_panel");
+      k_hlu_update<<<dim3(nb, std::min(nt * nt, 64)), 128, sizeof(Tile128Smem), s>>>(L, batch_cl, M0, ldm, fail, j0);
+      post_launch("k_hlu_update");
+    }
+    k_hlu_finish<<<dim3(nb, 16), 256, 0, s>>>(L, batch_cl, M0, ldm, fail);
+    post_launch("k_hlu_finish");
+    return;
+  }
   cplx* ws = workspace(2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb, s);
   k_head2<<<nb, 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_head2");

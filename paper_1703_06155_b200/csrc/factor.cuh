@@ -126,7 +126,9 @@ size_t eig1_ws_bytes(int bmax);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
 void launch_colnorm(const NormDesc* d, int n, cudaStream_t s);
 void launch_mask(const MaskDesc* d, int n, cudaStream_t s);
-void launch_head2(const DevLevel& L, const int* batch_cl, int nb, cudaStream_t s);
+// emax: upper bound of the batch's eliminated sizes (b - korig); > 64 takes
+// the multi-CTA extended LU
+void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cudaStream_t s);
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
