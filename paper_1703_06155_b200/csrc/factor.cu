@@ -101,6 +101,13 @@ __host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm 
 // 295-298 / h2_matrix.hpp:287-290.
 constexpr int kHCmax = 16;
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+
 
 __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
   namespace cg = cooperative_groups;
@@ -110,7 +117,9 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   __shared__ int s_any;
   __shared__ cplx s_tau[2];
   __shared__ int s_skip[2];
-  const int kHC = (int)cl.num_blocks();  // 1, 4 or 16 CTAs per cluster
+  const int kHC = (int)cl.num_blocks();  // 1, 4, 8 or 16 CTAs per cluster
+  const unsigned long long tm0 = (L.debug & 8) ? gtimer() : 0ull;
+  unsigned long long tm1 = 0, tm2 = 0, tm3 = 0;
   const int rank = (int)cl.block_rank();
   const int q = blockIdx.x / kHC, p = p0 + q;
   const int t = batch_cl[q];
@@ -122,9 +131,10 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   const int ncl = (m + kHC - 1) / kHC;
   cplx* Hl = reinterpret_cast<cplx*>(smraw);  // m x ncl local columns (col c = rank + kHC * jl)
   cplx* vbuf = Hl + (size_t)m * ncl;          // [2][m] reflector broadcast (owner)
-  cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v
-  cplx* vv = pbuf + 2 * m;                    // local copy of v
-  cplx* wv = vv + m;                          // local w
+  cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v over own columns
+  cplx* wfull = pbuf + 2 * m;                 // [2][m] reduced tau A v (written by the slice owners)
+  cplx* vv = wfull + 2 * m;                   // local copy of v
+  __shared__ cplx s_dots[2][kHCmax];          // per-slice partials of v^H w
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   {
@@ -146,7 +156,99 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
       for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + i + (size_t)c * m]);
     Hl[idx] = s;
   }
+  if (L.debug & 8) tm1 = gtimer();
+  // remote views of every CTA's partial / result buffers
+  const cplx* rp[kHCmax];
+  cplx* rw[kHCmax];
+  cplx* rd[kHCmax];
+#pragma unroll
+  for (int rr = 0; rr < kHCmax; ++rr) {
+    const int r2 = rr < kHC ? rr : 0;
+    rp[rr] = cl.map_shared_rank(pbuf, r2);
+    rw[rr] = cl.map_shared_rank(wfull, r2);
+    rd[rr] = cl.map_shared_rank(&s_dots[0][0], r2);
+  }
   cl.sync();
+  if (kHC == 1 && m <= 64) {
+    // small blocks: one warp runs the whole reduction (lane i owns rows i and
+    // i + 32 of the trailing block), no block barriers inside the column loop
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      cplx* vs = vbuf;  // v of the current column
+      cplx* wsv = pbuf; // w of the current column
+      for (int kk = 0; kk + 1 < m; ++kk) {
+        const int nk = m - kk - 1;
+        cplx* x = Hl + (kk + 1) + (size_t)kk * m;
+        const cplx x0 = lane < nk ? x[lane] : czero();
+        const cplx x1 = lane + 32 < nk ? x[lane + 32] : czero();
+        double part = (lane >= 1 ? cabs2(x0) : 0.0) + cabs2(x1);
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const double xn2 = part;
+        const cplx al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+        const bool skip = xn2 == 0.0 && al.y == 0.0;
+        double beta = al.x;
+        cplx tk = czero(), sc = czero();
+        if (!skip) {
+          beta = sqrt(cabs2(al) + xn2);
+          if (al.x >= 0.0) beta = -beta;
+          tk = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
+          sc = cdiv(cone(), csub(al, cmk(beta, 0.0)));
+        }
+        if (lane == 0) {
+          aux[kk] = Hl[kk + (size_t)kk * m].x;  // d_k
+          aux[bm + kk] = beta;                   // e_k
+          reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = tk;
+        }
+        if (skip) continue;  // warp-uniform
+        cplx v0 = lane == 0 ? cone() : cmul(x0, sc), v1 = cmul(x1, sc);
+        if (lane >= 1 && lane < nk) x[lane] = v0;
+        if (lane + 32 < nk) x[lane + 32] = v1;
+        if (lane < nk) vs[lane] = v0;
+        if (lane + 32 < nk) vs[lane + 32] = v1;
+        __syncwarp();
+        // p = tau A22 v (A22 = trailing nk x nk block, full storage)
+        const cplx* A22 = Hl + (kk + 1) + (size_t)(kk + 1) * m;
+        cplx p0 = czero(), p1 = czero();
+        for (int j = 0; j < nk; ++j) {
+          const cplx vj = vs[j];
+          if (lane < nk) cfma(p0, A22[lane + (size_t)j * m], vj);
+          if (lane + 32 < nk) cfma(p1, A22[lane + 32 + (size_t)j * m], vj);
+        }
+        p0 = cmul(tk, p0), p1 = cmul(tk, p1);
+        // c = v^H p; w = p - 1/2 conj(tau) c v
+        const cplx t0 = cmul(cconj(v0), p0), t1 = cmul(cconj(v1), p1);
+        double cr = (lane < nk ? t0.x : 0.0) + (lane + 32 < nk ? t1.x : 0.0);
+        double ci = (lane < nk ? t0.y : 0.0) + (lane + 32 < nk ? t1.y : 0.0);
+        for (int o = 16; o > 0; o >>= 1) {
+          cr += __shfl_xor_sync(0xffffffffu, cr, o);
+          ci += __shfl_xor_sync(0xffffffffu, ci, o);
+        }
+        const cplx hc = cscale(cmul(cconj(tk), cmk(cr, ci)), 0.5);
+        const cplx w0 = csub(p0, cmul(hc, v0)), w1 = csub(p1, cmul(hc, v1));
+        if (lane < nk) wsv[lane] = w0;
+        if (lane + 32 < nk) wsv[lane + 32] = w1;
+        __syncwarp();
+        // rank-2 update of own rows: A22[i, j] -= v_i conj(w_j) + w_i conj(v_j)
+        cplx* A22w = Hl + (kk + 1) + (size_t)(kk + 1) * m;
+        for (int j = 0; j < nk; ++j) {
+          const cplx vj = cconj(vs[j]), wj = cconj(wsv[j]);
+          if (lane < nk) {
+            cplx* a = A22w + lane + (size_t)j * m;
+            *a = csub(csub(*a, cmul(v0, wj)), cmul(w0, vj));
+          }
+          if (lane + 32 < nk) {
+            cplx* a = A22w + lane + 32 + (size_t)j * m;
+            *a = csub(csub(*a, cmul(v1, wj)), cmul(w1, vj));
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  } else {
+  // Per column: S1 (reflector published), S2 (partials A v ready), S3 (reduced
+  // w and the v^H w partials delivered): slice rank of the rows is reduced by
+  // CTA rank (warp 0) and pushed to every CTA, so each partial is read once.
   for (int kk = 0; kk + 1 < m; ++kk) {
     const int owner = kk % kHC, buf = kk & 1;
     const int nk = m - kk - 1;
@@ -204,22 +306,38 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
       }
     }
     cl.sync();  // S2: partials ready
-    // p = tau * sum of partials; c = v^H p; w = p - 1/2 conj(tau) c v (each CTA)
-    double cr = 0.0, ci = 0.0;
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-      cplx sacc = czero();
-      for (int rr = 0; rr < kHC; ++rr) sacc = cadd(sacc, cl.map_shared_rank(pbuf, rr)[(size_t)buf * m + i]);
-      sacc = cmul(tk, sacc);
-      wv[i] = sacc;
-      const cplx tt = cmul(cconj(vv[i]), sacc);
-      cr += tt.x;
-      ci += tt.y;
+    // slice rank: w_i = tau * sum_r p_r[i], pushed to every CTA; v^H w partial
+    if (threadIdx.x < 32) {
+      double dr = 0.0, di = 0.0;
+      for (int i = rank + kHC * (int)threadIdx.x; i < nk; i += 32 * kHC) {
+        cplx parts[kHCmax];
+#pragma unroll
+        for (int rr = 0; rr < kHCmax; ++rr)
+          if (rr < kHC) parts[rr] = rp[rr][(size_t)buf * m + i];
+        cplx sacc = czero();
+#pragma unroll
+        for (int rr = 0; rr < kHCmax; ++rr)
+          if (rr < kHC) sacc = cadd(sacc, parts[rr]);
+        sacc = cmul(tk, sacc);
+#pragma unroll
+        for (int rr = 0; rr < kHCmax; ++rr)
+          if (rr < kHC) rw[rr][(size_t)buf * m + i] = sacc;
+        const cplx tt = cmul(cconj(vv[i]), sacc);
+        dr += tt.x;
+        di += tt.y;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        dr += __shfl_xor_sync(0xffffffffu, dr, o);
+        di += __shfl_xor_sync(0xffffffffu, di, o);
+      }
+      if (threadIdx.x < kHC) rd[threadIdx.x][buf * kHCmax + rank] = cmk(dr, di);
     }
-    cr = cta_sum(cr, red);
-    ci = cta_sum(ci, red);
-    const cplx hc = cscale(cmul(cconj(tk), cmk(cr, ci)), 0.5);
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) wv[i] = csub(wv[i], cmul(hc, vv[i]));
-    __syncthreads();
+    cl.sync();  // S3: w and the v^H w partials delivered
+    // c = v^H w; w = w - 1/2 conj(tau) c v
+    cplx cdot = czero();
+    for (int rr = 0; rr < kHC; ++rr) cdot = cadd(cdot, s_dots[buf][rr]);
+    const cplx hc = cscale(cmul(cconj(tk), cdot), 0.5);
+    const cplx* wb = wfull + (size_t)buf * m;
     // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
     {
       const int jl0 = max((kk + 1 - rank + kHC - 1) / kHC, 0);
@@ -229,15 +347,18 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         const int c = rank + kHC * jl;
         if (c >= m) continue;
         const int jc = c - kk - 1;
+        const cplx wi = csub(wb[i], cmul(hc, vv[i])), wc = csub(wb[jc], cmul(hc, vv[jc]));
         cplx* a = Hl + (kk + 1 + i) + (size_t)jl * m;
         cplx av = *a;
-        av = csub(av, cmul(vv[i], cconj(wv[jc])));
-        av = csub(av, cmul(wv[i], cconj(vv[jc])));
+        av = csub(av, cmul(vv[i], cconj(wc)));
+        av = csub(av, cmul(wi, cconj(vv[jc])));
         *a = av;
       }
     }
     __syncthreads();
   }
+  }  // cluster path
+  if (L.debug & 8) tm2 = gtimer();
   // last diagonal, reflectors to global memory
   if (rank == (m - 1) % kHC && threadIdx.x == 0) {
     aux[m - 1] = Hl[(m - 1) + (size_t)((m - 1) / kHC) * m].x;
@@ -322,7 +443,11 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   }
   __syncthreads();
   const int r = s_r;
+  if (L.debug & 8) tm3 = gtimer();
   if (!s_need) multisect_top(m, dg, e2, r, s_lo, s_hi, s_piv, aux + 2 * bm);
+  if ((L.debug & 8) && threadIdx.x == 0)
+    printf("[h2g] eig1c-timing level %d cl %d kHC %d m %d r %d: gram %.1f us tridiag %.1f us lmax+rank %.1f us multisect %.1f us\n", L.level, t, kHC, m, r,
+           (tm1 - tm0) * 1e-3, (tm2 - tm1) * 1e-3, (tm3 - tm2) * 1e-3, (gtimer() - tm3) * 1e-3);
   if (threadIdx.x == 0) {
     L.pass2[q] = s_need ? 2 : 0;  // 2: refinement requested
     L.rank1[q] = r;
@@ -547,11 +672,9 @@ __global__ void __launch_bounds__(256) k_head(DevLevel L, const int* batch_cl, i
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
   const size_t bb = (size_t)bm * bm;
-  const int cid = (1 << L.level) - 1 + t;
   cplx* ws = gws + (size_t)q * 4 * bb;
-  cplx* Hc = ws;          // pass-2 Gram (m x m), later the LU workspace
+  cplx* Hc = ws;          // pass-2 Gram (m x m)
   cplx* Uc = ws + bb;     // pass-2 eigenvectors
-  cplx* Dd = ws + 2 * bb; // rotated diagonal block
   cplx* T = ws + 3 * bb;  // temporaries
   double* lam = reinterpret_cast<double*>(smraw);
   int* ord = reinterpret_cast<int*>(lam + bm);
@@ -713,7 +836,6 @@ __global__ void __launch_bounds__(256) k_hlu_prep(DevLevel L, const int* batch_c
 
 __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const double* scale, int* fail, int j0) {
   __shared__ cplx P[32][33];
-  __shared__ int s_fail;
   const int q = blockIdx.x;
   const int t = batch_cl[q];
   const int b = L.bsz[t], e = b - L.kfin[t];
@@ -725,7 +847,6 @@ __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_
     const int i = idx % kb, j = idx / kb;
     P[i][j] = M[(j0 + i) + (size_t)(j0 + j) * ldm];
   }
-  if (threadIdx.x == 0) s_fail = -1;
   __syncthreads();
   for (int k = 0; k < kb; ++k) {
     const cplx piv = P[k][k];
@@ -1180,9 +1301,9 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   {
     // cluster size: small blocks fit one CTA's shared memory, large ones are
     // spread over 4 or 16 CTAs
-    const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : kHCmax);
+    const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : (L.bmax <= 240 ? 8 : kHCmax));
     const int ncl = (L.bmax + kHC - 1) / kHC;
-    const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 6 + 256;
+    const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 8 + 256;
     if (smem > kSmemCap) throw std::runtime_error("k_eig1c: block too large for the 16-CTA cluster");
     set_smem((const void*)k_eig1c, smem);
     static bool np = false;
