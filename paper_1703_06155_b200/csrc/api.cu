@@ -309,6 +309,9 @@ struct ChainLevelHost {
   std::vector<int> fs_ptr;
   const SolveTargetD* d_fs = nullptr;
   const SolveContribD* d_fc = nullptr;
+  DBuf sched_buf;     // batch_ptr | batch_maxc | fs_ptr on the device
+  SolveSched sched{};
+  size_t part_need = 0;  // backward partials per rhs column (complex elements)
   DBuf d_src;
   // host copies of sizes/offsets for downloads
   std::vector<int> bsz, kfin, korig, R_ptr, R_nb, C_ptr, C_nb;
@@ -1245,6 +1248,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CL->fs_ptr = W.fsolve_ptr;
         CL->d_fs = at<SolveTargetD>(mt, o_fs);
         CL->d_fc = at<SolveContribD>(mt, o_fc);
+        {
+          std::vector<int> sv(CL->batch_ptr);
+          sv.insert(sv.end(), CL->batch_maxc.begin(), CL->batch_maxc.end());
+          sv.insert(sv.end(), CL->fs_ptr.begin(), CL->fs_ptr.end());
+          upload(CL->sched_buf, sv, st);
+          const int nb1 = static_cast<int>(CL->batch_ptr.size());
+          const int* base = CL->sched_buf.as<int>();
+          CL->sched = {nb1 - 1, base, d_bat, base + nb1, base + nb1 + (nb1 - 1), CL->d_fs, CL->d_fc};
+          for (int bi = 0; bi + 1 < nb1; ++bi)
+            CL->part_need = std::max(CL->part_need, (size_t)(CL->batch_ptr[bi + 1] - CL->batch_ptr[bi]) * (CL->batch_maxc[bi] + 1) * bm);
+        }
         SolveLevel& SL = CL->sl;
         SL.nl = nl;
         SL.bmax = bm;
@@ -1511,17 +1525,18 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   const bool fwd = mode != H2G_BACKWARD, bwd = mode != H2G_FORWARD;
   const int expl = mode == H2G_APPLY_INVERSE_EXPLICIT;
   long long launches = 1;
+  // right-hand sides per pass of the level kernels: 2 * bmax * rchunk
+  // complex of shared memory per CTA stays under ~96 KB
+  int bmax_all = 1;
+  for (auto& CLp : C->levels) bmax_all = std::max(bmax_all, CLp->sl.bmax);
+  const int rchunk = std::max(1, std::min(nrhs, (int)((96 * 1024) / (2 * 16 * (size_t)bmax_all))));
   CK(cudaEventRecord(ctx->ev0, st));
   if (fwd) {
     for (auto& CLp : C->levels) {
       ChainLevelHost& CL = *CLp;
-      const int nbat = static_cast<int>(CL.batch_ptr.size()) - 1;
-      for (int bi = 0; bi < nbat; ++bi) {
-        const int p0 = CL.batch_ptr[bi], nb = CL.batch_ptr[bi + 1] - p0;
-        launch_fwd_head(CL.sl, CL.d_batch + p0, nb, y, n, nrhs, expl, st);
-        const int f0 = CL.fs_ptr[bi], f1 = CL.fs_ptr[bi + 1];
-        launch_fwd_lbar(CL.sl, CL.d_fs + f0, f1 - f0, CL.d_fc, y, n, nrhs, st);
-        launches += 1 + (f1 > f0);
+      for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
+        launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
+        ++launches;
       }
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 0, st);
       launches += 2;
@@ -1540,13 +1555,11 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
       ChainLevelHost& CL = **it;
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 1, st);
       launches += 2;
-      const int nbat = static_cast<int>(CL.batch_ptr.size()) - 1;
-      for (int bi = nbat - 1; bi >= 0; --bi) {
-        const int p0 = CL.batch_ptr[bi], nb = CL.batch_ptr[bi + 1] - p0;
-        const size_t need = (size_t)nb * (CL.batch_maxc[bi] + 1) * CL.sl.bmax * nrhs * 16;
-        if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
-        launch_bwd(CL.sl, CL.d_batch + p0, nb, CL.batch_maxc[bi], y, n, nrhs, expl, C->partbuf.as<cplx>(), st);
-        launches += 2;
+      const size_t need = CL.part_need * rchunk * 16;
+      if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
+      for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
+        launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
+        ++launches;
       }
     }
   }

@@ -742,10 +742,12 @@ namespace h2g {
 // 3-stage k-slices (8 deep) of a TM x TM output tile computed by 128 threads;
 // thread (tr, tc) = (tid % 8, tid / 8) owns rows tr + 8a (a < TM/8) and
 // columns tc * (TM/16) + b.
+// Rows padded by one complex: the cp.async writes of a k-major operand hit
+// 8 consecutive k-rows, which would otherwise all start in the same bank.
 template <int TM>
 struct TileSmem {
-  cplx a[3][8][TM];
-  cplx b[3][8][TM];
+  cplx a[3][8][TM + 1];
+  cplx b[3][8][TM + 1];
 };
 using Tile128Smem = TileSmem<64>;
 

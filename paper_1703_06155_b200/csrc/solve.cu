@@ -1,6 +1,8 @@
 // Forward / backward substitution on the device (proj/include/h2lu/solve.hpp:
 // 43-83), batch by batch in the factorization's elimination order. Vectors
 // are n x nrhs column-major complex128 in tree order, updated in place.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <map>
 #include <mutex>
@@ -10,11 +12,9 @@
 
 namespace h2g {
 
-// seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50). One CTA per
-// record of the batch.
-__global__ void __launch_bounds__(256) k_fwd_head(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int t = batch_cl[blockIdx.x];
+// seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50); one CTA per
+// record.
+__device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, unsigned char* smraw) {
   const int b = S.bsz[t], e = b - S.kfin[t];
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);  // b x nrhs
@@ -51,8 +51,7 @@ __global__ void __launch_bounds__(256) k_fwd_head(SolveLevel S, const int* batch
 
 // y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51), contributions of a
 // target segment summed in a fixed order.
-__global__ void __launch_bounds__(256) k_fwd_lbar(SolveLevel S, const SolveTargetD* targets, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs) {
-  const SolveTargetD tg = targets[blockIdx.x];
+__device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs) {
   int rows;
   long long base;
   if (tg.seg >= 0) {
@@ -83,10 +82,8 @@ __global__ void __launch_bounds__(256) k_fwd_lbar(SolveLevel S, const SolveTarge
 // Backward gather (solve.hpp:77): partial[q][c] = Ubar(m, c) y[pos_c ...]
 // for one neighbour c of record m = batch[q] (the last slot is the self
 // block), spread over CTAs so the chain blocks stream at full bandwidth.
-__global__ void __launch_bounds__(256) k_bwd_gather(SolveLevel S, const int* batch_cl, const cplx* y, long long ldy, int nrhs, cplx* part,
-                                                    long long pstride) {
-  const int q = blockIdx.x, c = blockIdx.y;
-  const int t = batch_cl[q];
+__device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int nslot, const cplx* y, long long ldy, int nrhs, cplx* part,
+                                long long pstride) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
   if (e == 0 || c > nC || (c == nC && kf == 0)) return;
@@ -103,7 +100,7 @@ __global__ void __launch_bounds__(256) k_bwd_gather(SolveLevel S, const int* bat
     M = S.chain + S.Uself_off[t];
     x = y + S.pos[t] + e;
   }
-  cplx* out = part + ((size_t)q * gridDim.y + c) * pstride;
+  cplx* out = part + ((size_t)q * nslot + c) * pstride;
   for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
     const int i = idx % e, r = idx / e;
     cplx acc = czero();
@@ -115,10 +112,8 @@ __global__ void __launch_bounds__(256) k_bwd_gather(SolveLevel S, const int* bat
 
 // Backward record (solve.hpp:73-81): head -= sum of the gathered partials (in
 // neighbour order); U11 solve; seg <- conj(Qt) seg. One CTA per record.
-__global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part,
-                                             long long pstride, int nslot) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int t = batch_cl[blockIdx.x];
+__device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part, long long pstride,
+                         int nslot, unsigned char* smraw) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);
@@ -131,7 +126,7 @@ __global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, 
     for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
       const int i = idx % e, c = idx / e;
       cplx acc = czero();
-      for (int q = 0; q < nuse; ++q) acc = cadd(acc, part[((size_t)blockIdx.x * nslot + (q < nC ? q : nC)) * pstride + i + (size_t)c * e]);
+      for (int u = 0; u < nuse; ++u) acc = cadd(acc, part[((size_t)q * nslot + (u < nC ? u : nC)) * pstride + i + (size_t)c * e]);
       sS[i + c * b] = csub(sS[i + c * b], acc);
     }
     __syncthreads();
@@ -162,6 +157,45 @@ __global__ void __launch_bounds__(256) k_bwd(SolveLevel S, const int* batch_cl, 
   cta_gemm(b, nrhs, b, 1.0, Q, b, OP_R, sS, b, OP_N, 0.0, sO, b);
   __syncthreads();
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
+}
+
+// One persistent cooperative kernel per level and direction: the batches of
+// the elimination order run back to back with grid-wide barriers between the
+// record phase and the neighbour phase, instead of two launches per batch.
+__global__ void __launch_bounds__(256) k_fwd_level(SolveLevel S, SolveSched P, cplx* y, long long ldy, int nrhs, int explicit_inv) {
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  for (int bi = 0; bi < P.nbat; ++bi) {
+    const int p0 = P.batch_ptr[bi], nb = P.batch_ptr[bi + 1] - p0;
+    for (int q = blockIdx.x; q < nb; q += gridDim.x) {
+      fwd_head_body(S, P.batch_cl[p0 + q], y, ldy, nrhs, explicit_inv, smraw);
+      __syncthreads();
+    }
+    g.sync();
+    const int f0 = P.fs_ptr[bi], f1 = P.fs_ptr[bi + 1];
+    for (int f = f0 + blockIdx.x; f < f1; f += gridDim.x) fwd_lbar_body(S, P.fs[f], P.fc, y, ldy, nrhs);
+    g.sync();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bwd_level(SolveLevel S, SolveSched P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
+                                                   long long pstride) {
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  for (int bi = P.nbat - 1; bi >= 0; --bi) {
+    const int p0 = P.batch_ptr[bi], nb = P.batch_ptr[bi + 1] - p0;
+    const int nslot = P.batch_maxc[bi] + 1;
+    for (int it = blockIdx.x; it < nb * nslot; it += gridDim.x)
+      bwd_gather_body(S, P.batch_cl[p0 + it / nslot], it / nslot, it % nslot, nslot, y, ldy, nrhs, part, pstride);
+    g.sync();
+    for (int q = blockIdx.x; q < nb; q += gridDim.x) {
+      bwd_body(S, P.batch_cl[p0 + q], q, y, ldy, nrhs, explicit_inv, part, pstride, nslot, smraw);
+      __syncthreads();
+    }
+    g.sync();
+  }
 }
 
 // (P v)[j] = v[src[j]] (gather, solve.hpp:18-23) or its inverse (scatter, :25-30).
@@ -237,24 +271,48 @@ static void smem_attr(const void* fn, size_t bytes) {
   }
 }
 
-void launch_fwd_head(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
-  smem_attr((const void*)k_fwd_head, smem);
-  k_fwd_head<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv);
+// Co-resident grid for the cooperative level kernels (cached per kernel / smem).
+template <class K>
+static int coop_grid(K kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair((const void*)kernel, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, 256, smem);
+  const int g = std::max(1, std::min(per, 2)) * nsm;
+  if (per < 1) throw std::runtime_error("solve level kernel does not fit on an SM");
+  cache[key] = g;
+  return g;
 }
 
-void launch_fwd_lbar(const SolveLevel& S, const SolveTargetD* t, int nt, const SolveContribD* c, cplx* y, long long ldy, int nrhs, cudaStream_t s) {
-  if (nt > 0) k_fwd_lbar<<<nt, 256, 0, s>>>(S, t, c, y, ldy, nrhs);
+void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
+  if (P.nbat <= 0) return;
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
+  smem_attr((const void*)k_fwd_level, smem);
+  const int grid = coop_grid(k_fwd_level, smem);
+  SolveLevel Sv = S;
+  SolveSched Pv = P;
+  void* args[] = {&Sv, &Pv, &y, &ldy, &nrhs, &explicit_inv};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_fwd_level, grid, 256, args, smem, s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_fwd_level failed: ") + cudaGetErrorString(e));
 }
 
-void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, int maxc, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
-                cudaStream_t s) {
-  const long long pstride = (long long)S.bmax * nrhs;
-  const int nslot = maxc + 1;
-  k_bwd_gather<<<dim3(nb, nslot), 256, 0, s>>>(S, batch_cl, y, ldy, nrhs, part, pstride);
+void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s) {
+  if (P.nbat <= 0) return;
   const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
-  smem_attr((const void*)k_bwd, smem);
-  k_bwd<<<nb, 256, smem, s>>>(S, batch_cl, y, ldy, nrhs, explicit_inv, part, pstride, nslot);
+  smem_attr((const void*)k_bwd_level, smem);
+  const int grid = coop_grid(k_bwd_level, smem);
+  long long pstride = (long long)S.bmax * nrhs;
+  SolveLevel Sv = S;
+  SolveSched Pv = P;
+  void* args[] = {&Sv, &Pv, &y, &ldy, &nrhs, &explicit_inv, &part, &pstride};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_bwd_level, grid, 256, args, smem, s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_bwd_level failed: ") + cudaGetErrorString(e));
 }
 
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s) {

@@ -5,6 +5,13 @@
 
 namespace h2g {
 
+struct SolveTargetD {
+  int seg, c0, c1;
+};
+struct SolveContribD {
+  int m, entry;
+};
+
 struct SolveLevel {
   int nl;
   int bmax;
@@ -25,17 +32,22 @@ struct SolveLevel {
   const long long* Uself_off;
 };
 
-struct SolveTargetD {
-  int seg, c0, c1;
-};
-struct SolveContribD {
-  int m, entry;
+
+// Batch schedule of one level for the persistent substitution kernels.
+struct SolveSched {
+  int nbat;
+  const int* batch_ptr;   // [nbat + 1] into batch_cl
+  const int* batch_cl;
+  const int* batch_maxc;  // [nbat] max neighbour columns of a record
+  const int* fs_ptr;      // [nbat + 1] into fs
+  const SolveTargetD* fs;
+  const SolveContribD* fc;
 };
 
-void launch_fwd_head(const SolveLevel& S, const int* batch_cl, int nb, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
-void launch_fwd_lbar(const SolveLevel& S, const SolveTargetD* t, int nt, const SolveContribD* c, cplx* y, long long ldy, int nrhs, cudaStream_t s);
-void launch_bwd(const SolveLevel& S, const int* batch_cl, int nb, int maxc, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
-                cudaStream_t s);
+// Whole level, all batches, one cooperative launch per direction; part holds
+// max_b nb * (maxc_b + 1) * bmax * nrhs gathered backward partials.
+void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
+void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s);
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s);
 void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s);
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s);
