@@ -420,8 +420,18 @@ struct LevelData {
   std::vector<int> bsz, korig;
   std::vector<long long> pos;
   int bmax = 0;
+  // dense / fill blocks packed at their true sizes (bsz[row] x bsz[col])
+  std::vector<long long> doff, foff;
   DBuf D, F, fex, V0, Vp;
 };
+
+// Packed offsets of blocks (rows[i], cols[i]) with sizes bsz[.]; returns the total.
+long long pack_offsets(const std::vector<int>& rows, const std::vector<int>& cols, const std::vector<int>& bsz, std::vector<long long>& off) {
+  off.resize(rows.size());
+  long long top = 0;
+  for (size_t i = 0; i < rows.size(); ++i) off[i] = top, top += (long long)bsz[rows[i]] * bsz[cols[i]];
+  return top;
+}
 
 }  // namespace
 
@@ -685,12 +695,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       cur.bmax = std::max(1, *std::max_element(cur.bsz.begin(), cur.bsz.end()));
       const size_t bb = (size_t)cur.bmax * cur.bmax * 16;
       const LevelSym& Y = P->levels[0];
-      cur.D.alloc(std::max<size_t>(Y.drow.size(), 1) * bb, st, true);
+      const long long dtot = pack_offsets(Y.drow, Y.dcol, cur.bsz, cur.doff);
+      cur.D.alloc(std::max<long long>(dtot, 1) * 16, st, true);
       cur.V0.alloc((size_t)nl * bb, st, true);
       std::vector<CopyDesc> cd;
       for (size_t q = 0; q < Y.drow.size(); ++q) {
         const int r = Y.drow[q], c = Y.dcol[q];
-        cd.push_back({M->dense.as<cplx>() + M->dense_off[q], at<cplx>(cur.D, q * bb), cur.bsz[r], cur.bsz[r], cur.bsz[r], cur.bsz[c], 0, 0});
+        cd.push_back({M->dense.as<cplx>() + M->dense_off[q], cur.D.as<cplx>() + cur.doff[q], cur.bsz[r], cur.bsz[r], cur.bsz[r], cur.bsz[c], 0, 0});
       }
       for (int t = 0; t < nl; ++t)
         if (cur.korig[t] > 0)
@@ -699,7 +710,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       upload(dd, cd, st);
       launch_copy(dd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
       ++launches;
-      cur.F.alloc(std::max<size_t>(Y.frow.size(), 1) * bb, st, true);
+      const long long ftot = pack_offsets(Y.frow, Y.fcol, cur.bsz, cur.foff);
+      cur.F.alloc(std::max<long long>(ftot, 1) * 16, st, true);
       cur.fex.alloc(std::max<size_t>(Y.frow.size(), 1) * 4, st, true);
       CK(cudaStreamSynchronize(st));
     }
@@ -751,6 +763,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         std::vector<int> kfin0(cur.korig);
         size_t o_kfin = pk.add(kfin0);
         size_t o_drow = pk.add(Y.drow), o_dcol = pk.add(Y.dcol), o_diag = pk.add(Y.diag_blk);
+        size_t o_doff = pk.add(cur.doff), o_foff = pk.add(cur.foff);
         size_t o_frow = pk.add(Y.frow), o_fcol = pk.add(Y.fcol);
         size_t o_Rp = pk.add(Y.R_ptr), o_Rn = pk.add(Y.R_nb), o_Cp = pk.add(Y.C_ptr), o_Cn = pk.add(Y.C_nb);
         size_t o_Gp = pk.add(Y.G_ptr), o_Gf = pk.add(Y.G_fill), o_Gt = pk.add(Y.G_tr);
@@ -844,7 +857,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               const int t = SC.batch_cl[SC.batch_ptr[bi] + a.q];
               const int b = cur.bsz[t];
               const int fr = cur.bsz[Y.frow[a.fi]];
-              const cplx* F = cur.F.as<cplx>() + (size_t)a.fi * bb;
+              const cplx* F = cur.F.as<cplx>() + cur.foff[a.fi];
               cplx* Cp = ybuf.as<cplx>() + a.yoff + (long long)a.m * a.col;
               const int* fx = cur.fex.as<int>() + a.fi;
               gA1.push_back({cur.Vp.as<cplx>() + (size_t)t * bb, F, Cp, b, fr, a.m, a.m, a.bx, b, OP_C, a.tr ? OP_T : OP_N, 1.0, 0.0, fx, nullptr});
@@ -860,7 +873,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
           for (size_t c = 0; c < ndesc_f.size(); ++c) {
             const int fi = ndesc_f[c];
-            gN.push_back({cur.F.as<cplx>() + (size_t)fi * bb, cur.bsz[Y.frow[fi]], cur.bsz[Y.fcol[fi]], 0, 0, cur.fex.as<int>() + fi, cnbuf.as<double>() + c});
+            gN.push_back({cur.F.as<cplx>() + cur.foff[fi], cur.bsz[Y.frow[fi]], cur.bsz[Y.fcol[fi]], 0, 0, cur.fex.as<int>() + fi, cnbuf.as<double>() + c});
           }
           // transposition flag of each colnorm entry
           size_t c = 0;
@@ -879,7 +892,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             const int q = p - SC.batch_ptr[bi], t = SC.batch_cl[p];
             const int b = cur.bsz[t];
             cplx* Tq = rotbuf.as<cplx>() + (size_t)q * bb;
-            cplx* Dtt = cur.D.as<cplx>() + (size_t)Y.diag_blk[t] * bb;
+            cplx* Dtt = cur.D.as<cplx>() + cur.doff[Y.diag_blk[t]];
             const cplx* Qt = CL->arena.as<cplx>() + Qt_off[t];
             gR1.push_back({Qt, Dtt, Tq, b, b, b, b, b, b, OP_C, OP_N, 1.0, 0.0, nullptr, nullptr});
             gR2.push_back({Tq, Qt, Dtt, b, b, b, b, b, b, OP_N, OP_R, 1.0, 0.0, nullptr, nullptr});
@@ -965,6 +978,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.korig = at<int>(mt, o_korig);
         DL.kfin = at<int>(mt, o_kfin);
         DL.D = cur.D.as<cplx>();
+        DL.D_off = at<long long>(mt, o_doff);
+        DL.F_off = at<long long>(mt, o_foff);
         DL.drow = at<int>(mt, o_drow);
         DL.dcol = at<int>(mt, o_dcol);
         DL.diag_blk = at<int>(mt, o_diag);
@@ -1018,7 +1033,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               const int t = SC.batch_cl[SC.batch_ptr[bi] + pi.q];
               const int b = cur.bsz[t], bn = cur.bsz[pi.nb];
               cplx* T = panbuf.as<cplx>() + (size_t)(it - W.panel_ptr[bi]) * bb;
-              cplx* Dblk = cur.D.as<cplx>() + (size_t)pi.blk * bb;
+              cplx* Dblk = cur.D.as<cplx>() + cur.doff[pi.blk];
               const cplx* Q = chainb + Qt_off[t];
               const cplx* Qn = chainb + Qt_off[pi.nb];
               GemmDesc r{}, pp{}, lf{};
@@ -1139,8 +1154,11 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaGetLastError());
         check_device_error(ctx, l);
         if (verbose)
-          std::fprintf(stderr, "[h2g] level %d: nl %d bmax %d batches %d: host setup+launch %.3f s, device drain %.3f s\n", l, nl, bm, nbat,
-                       t_launched - tlev, wall() - t_launched);
+          std::fprintf(stderr,
+                       "[h2g] level %d: nl %d bmax %d batches %d: host setup+launch %.3f s, device drain %.3f s; D %zu blocks %.2f GB, F %zu blocks "
+                       "%.2f GB, chain %.2f GB\n",
+                       l, nl, bm, nbat, t_launched - tlev, wall() - t_launched, Y.drow.size(), cur.D.bytes / 1e9, Y.frow.size(), cur.F.bytes / 1e9,
+                       CL->arena.bytes / 1e9);
         // ---- read back final ranks and fill existence
         std::vector<int> kfin(nl), fex(Y.frow.size());
         CK(cudaMemcpyAsync(kfin.data(), DL.kfin, nl * 4, cudaMemcpyDeviceToHost, st));
@@ -1301,8 +1319,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         if (off != active_new) throw Error(H2G_ERR_INVALID_INPUT, "merge_permute: parent layout does not match the permutation");
         nxt.bmax = std::max(1, *std::max_element(nxt.bsz.begin(), nxt.bsz.end()));
         const size_t bbp = (size_t)nxt.bmax * nxt.bmax;
-        nxt.D.alloc(std::max<size_t>(YP.drow.size(), 1) * bbp * 16, st, true);
-        nxt.F.alloc(std::max<size_t>(YP.frow.size(), 1) * bbp * 16, st, true);
+        const long long ndtot = pack_offsets(YP.drow, YP.dcol, nxt.bsz, nxt.doff);
+        const long long nftot = pack_offsets(YP.frow, YP.fcol, nxt.bsz, nxt.foff);
+        nxt.D.alloc(std::max<long long>(ndtot, 1) * 16, st, true);
+        nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
         nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
         nxt.V0.alloc((size_t)nlp * bbp * 16, st, true);
         std::vector<CopyDesc> cd;
@@ -1322,7 +1342,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         const auto& admL = S.adm[l];
         for (size_t pq = 0; pq < YP.drow.size(); ++pq) {
           const int Pr = YP.drow[pq], Pc = YP.dcol[pq];
-          cplx* dst = Dp + pq * bbp;
+          cplx* dst = Dp + nxt.doff[pq];
           const int ldd = nxt.bsz[Pr];
           for (int ia = 0; ia < 2; ++ia)
             for (int ic = 0; ic < 2; ++ic) {
@@ -1332,7 +1352,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               if (di >= 0) {
                 const int ea = cur.bsz[a] - kfin[a], ec = cur.bsz[c] - kfin[c];
                 if (kfin[a] && kfin[c])
-                  cd.push_back({cur.D.as<cplx>() + di * bb + ea + (size_t)ec * cur.bsz[a], dst + ro + (size_t)co * ldd, cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
+                  cd.push_back({cur.D.as<cplx>() + cur.doff[di] + ea + (size_t)ec * cur.bsz[a], dst + ro + (size_t)co * ldd, cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
               } else {
                 const Pair hp{a + Y.first, c + Y.first};
                 auto it = std::lower_bound(admL.begin(), admL.end(), hp, [](const Pair& x, const Pair& y) { return x.row < y.row || (x.row == y.row && x.col < y.col); });
@@ -1356,7 +1376,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           if (!kfin[j] || !kfin[c]) continue;
           const int ro = (j & 1) ? kfin[j - 1] : 0, co = (c & 1) ? kfin[c - 1] : 0;
           const int ldd = nxt.bsz[YP.frow[pf]];
-          pend.push_back({j, c, static_cast<int>(f), Fp + (size_t)pf * bbp + ro + (size_t)co * ldd, ldd});
+          pend.push_back({j, c, static_cast<int>(f), Fp + nxt.foff[pf] + ro + (size_t)co * ldd, ldd});
         }
         for (const auto& pg : pend) {
           const int a = pg.a, c = pg.c;
@@ -1370,7 +1390,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int a = pg.a, c = pg.c;
           cplx* X = tmp.as<cplx>() + tmp_off[q];
           // X = V_a^H F (kfin_a x b_c);  dst += X conj(V_c)   (factorization.hpp:455, :540)
-          g1.push_back({Vptr(a), cur.F.as<cplx>() + (size_t)pg.fi * bb, X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
+          g1.push_back({Vptr(a), cur.F.as<cplx>() + cur.foff[pg.fi], X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
           g2.push_back({X, Vptr(c), pg.dst, kfin[a], cur.bsz[c], pg.ldd, kfin[a], kfin[c], cur.bsz[c], OP_N, OP_R, 1.0, 1.0});
         }
         // padded transfers (finish_level :464-474)
@@ -1437,7 +1457,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         for (size_t q = 0; q < YR->drow.size(); ++q) {
           const int r = YR->drow[q], c = YR->dcol[q];
           if (!cur.bsz[r] || !cur.bsz[c]) continue;
-          cd.push_back({cur.D.as<cplx>() + q * bb, C->root.as<cplx>() + cur.pos[r] + (size_t)cur.pos[c] * nroot, cur.bsz[r], (int)nroot, cur.bsz[r], cur.bsz[c], 0, 0});
+          cd.push_back({cur.D.as<cplx>() + cur.doff[q], C->root.as<cplx>() + cur.pos[r] + (size_t)cur.pos[c] * nroot, cur.bsz[r], (int)nroot, cur.bsz[r], cur.bsz[c], 0, 0});
         }
         DBuf dcd;
         upload(dcd, cd, st);

@@ -71,17 +71,29 @@ struct BuildLevel {
   KernelD K;
 };
 
-// One CTA per far item: Y = D^H Z(c, cols) (kloc x ncols), G_part += Y Y^H.
+// One CTA per (cluster slot, part, tile pair ta <= tb of the kloc x kloc
+// Gram): Y_x = D(:, tile x)^H Z(c, cols) for the item's columns, G[ta, tb] +=
+// Y_ta Y_tb^H; the mirrored tile is written as its conjugate transpose.
+__device__ __forceinline__ void tile_pair(int pr, int& ta, int& tb) {
+  ta = 0;
+  while (pr > ta) pr -= ta + 1, ++ta;  // pairs (0,0) (0,1) (1,1) (0,2) ...: tb-major
+  tb = ta;
+  ta = pr;
+}
+
 __global__ void __launch_bounds__(256) k_far_gram(BuildLevel B, const FarItem* items, const int* item_ptr) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx(*sZ)[65] = reinterpret_cast<cplx(*)[65]>(smraw);
   cplx(*sD)[65] = sZ + 64;
-  cplx(*sY)[65] = sZ + 128;
-  const int q = blockIdx.x;  // one CTA per (cluster slot, part)
+  const int q = blockIdx.x;  // one CTA per (cluster slot, part, tile pair)
   const int part = blockIdx.y;
+  int ta, tb;
+  tile_pair(blockIdx.z, ta, tb);
   const int kl = B.kloc[q], nr = B.csize[q];
+  if (tb * 64 >= kl) return;
   const long long r0 = B.cbeg[q];
   const bool leaf = B.D_off[q] < 0;
+  const bool same = ta == tb;
   const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
   cplx g[4][4];
 #pragma unroll
@@ -90,56 +102,73 @@ __global__ void __launch_bounds__(256) k_far_gram(BuildLevel B, const FarItem* i
     for (int b = 0; b < 4; ++b) g[a][b] = czero();
   for (int it = item_ptr[q] + part; it < item_ptr[q + 1]; it += B.nparts) {
     const FarItem fi = items[it];
-    cplx y[4][4];
+    cplx ya[4][4], yb[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) y[a][b] = czero();
+      for (int b = 0; b < 4; ++b) ya[a][b] = czero(), yb[a][b] = czero();
     for (int rc = 0; rc < nr; rc += 64) {
       const int rn = min(64, nr - rc);
       __syncthreads();
       for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
         const int i = idx % 64, j = idx / 64;
         sZ[i][j] = (i < rn && j < fi.ncols) ? kentry(B.K, B.px, B.py, B.pz, r0 + rc + i, fi.first_col + j) : czero();
-        if (!leaf) {
-          const cplx* D = B.Dbuf + B.D_off[q];
-          sD[i][j] = (i < rn && j < kl) ? D[rc + i + (size_t)j * nr] : czero();
-        }
       }
-      __syncthreads();
       if (leaf) {
-        // Y = Z directly (kloc = |c| <= 64)
+        // Y = Z directly (kloc = |c| <= 64, a single tile)
+        __syncthreads();
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) y[a][b] = sZ[tr * 4 + a][tc * 4 + b];
-      } else {
+          for (int b = 0; b < 4; ++b) ya[a][b] = sZ[tr * 4 + a][tc * 4 + b];
+        continue;
+      }
+      const cplx* D = B.Dbuf + B.D_off[q];
+      for (int pass = 0; pass < (same ? 1 : 2); ++pass) {
+        const int c0 = (pass == 0 ? ta : tb) * 64;
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+          const int i = idx % 64, j = idx / 64;
+          sD[i][j] = (i < rn && c0 + j < kl) ? D[rc + i + (size_t)(c0 + j) * nr] : czero();
+        }
+        __syncthreads();
         for (int p = 0; p < rn; ++p) {
           cplx dv[4], zv[4];
 #pragma unroll
           for (int a = 0; a < 4; ++a) dv[a] = cconj(sD[p][tr * 4 + a]);
 #pragma unroll
           for (int b = 0; b < 4; ++b) zv[b] = sZ[p][tc * 4 + b];
+          if (pass == 0) {
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) cfma(y[a][b], dv[a], zv[b]);
+              for (int b = 0; b < 4; ++b) cfma(ya[a][b], dv[a], zv[b]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) cfma(yb[a][b], dv[a], zv[b]);
+          }
         }
       }
     }
     __syncthreads();
+    // Y_ta into sZ, Y_tb into sD
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) sY[tr * 4 + a][tc * 4 + b] = y[a][b];
+      for (int b = 0; b < 4; ++b) {
+        sZ[tr * 4 + a][tc * 4 + b] = ya[a][b];
+        sD[tr * 4 + a][tc * 4 + b] = same ? ya[a][b] : yb[a][b];
+      }
     __syncthreads();
-    // G += Y Y^H over the chunk's columns
+    // G += Y_ta Y_tb^H over the chunk's columns
     for (int p = 0; p < fi.ncols; ++p) {
       cplx av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = sY[tr * 4 + a][p];
+      for (int a = 0; a < 4; ++a) av[a] = sZ[tr * 4 + a][p];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = cconj(sY[tc * 4 + b][p]);
+      for (int b = 0; b < 4; ++b) bv[b] = cconj(sD[tc * 4 + b][p]);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -151,21 +180,25 @@ __global__ void __launch_bounds__(256) k_far_gram(BuildLevel B, const FarItem* i
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int i = tr * 4 + a, j = tc * 4 + b;
-      if (i < kl && j < kl) out[i + (size_t)j * kl] = g[a][b];
+      const int i = ta * 64 + tr * 4 + a, j = tb * 64 + tc * 4 + b;
+      if (i < kl && j < kl) {
+        out[i + (size_t)j * kl] = g[a][b];
+        if (!same) out[j + (size_t)i * kl] = cconj(g[a][b]);
+      }
     }
 }
 
 // Per cluster: G = sum of parts (x mult), Jacobi eigendecomposition, eigen
 // vectors sorted by descending value into U (kloc x kloc) and the rank.
-__global__ void __launch_bounds__(256) k_far_eig(BuildLevel B, double mult, double eps, cplx* Uout, int* rank) {
+__global__ void __launch_bounds__(256) k_far_eig(BuildLevel B, double mult, double eps, cplx* Uout, int* rank, cplx* gws) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double red[32];
   const int q = blockIdx.x;
   const int n = B.kloc[q], bm = B.bm;
-  cplx* H = reinterpret_cast<cplx*>(smraw);
+  // H, U in shared memory for small clusters, else in the global workspace
+  cplx* H = gws ? gws + (size_t)q * 2 * bm * bm : reinterpret_cast<cplx*>(smraw);
   cplx* U = H + bm * bm;
-  double* lam = reinterpret_cast<double*>(U + bm * bm);
+  double* lam = gws ? reinterpret_cast<double*>(smraw) : reinterpret_cast<double*>(U + bm * bm);
   int* ord = reinterpret_cast<int*>(lam + bm);
   int* pr = ord + bm;
   double* rot = reinterpret_cast<double*>(pr + bm + 2);
@@ -224,20 +257,23 @@ struct CoupLevel {
   KernelD K;
 };
 
-// One CTA per (pair, 64-row chunk of t): X = Z(rows, s) conj(E_s) then
-// S_part = E_t(rows)^H X.
-__global__ void __launch_bounds__(256) k_coupling(CoupLevel C, const CoupItem* items) {
+// One CTA per (pair, 64-row chunk of t, 64 x 64 tile (a, b) of S): X =
+// Z(rows, s) conj(E_s(:, tile b)) then S_part(tile a, tile b) = E_t(rows, tile a)^H X.
+__global__ void __launch_bounds__(256) k_coupling(CoupLevel C, const CoupItem* items, int ntb) {
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx(*sZ)[65] = reinterpret_cast<cplx(*)[65]>(smraw);
   cplx(*sE)[65] = sZ + 64;
   cplx(*sX)[65] = sZ + 128;
   const CoupItem it = items[blockIdx.x];
   const int pq = it.pair;
-  const int tn = C.tn[pq], sn = C.sn[pq], kt = C.kt[pq], ks = C.ks[pq];
+  const int ta = blockIdx.y / ntb, tb = blockIdx.y % ntb;
+  const int tn = C.tn[pq], sn = C.sn[pq], kt0 = C.kt[pq], ks0 = C.ks[pq];
+  if (ta * 64 >= kt0 || tb * 64 >= ks0) return;
+  const int kt = min(64, kt0 - ta * 64), ks = min(64, ks0 - tb * 64);
   const int rn = min(64, tn - it.rc);
   const long long r0 = C.tb[pq] + it.rc, c0 = C.sb[pq];
-  const cplx* Et = C.E + C.Et_off[pq];
-  const cplx* Es = C.E + C.Es_off[pq];
+  const cplx* Et = C.E + C.Et_off[pq] + (size_t)ta * 64 * tn;
+  const cplx* Es = C.E + C.Es_off[pq] + (size_t)tb * 64 * sn;
   const int tr = threadIdx.x % 16, tc = threadIdx.x / 16;
   cplx x[4][4];
 #pragma unroll
@@ -297,7 +333,7 @@ __global__ void __launch_bounds__(256) k_coupling(CoupLevel C, const CoupItem* i
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = tr * 4 + a, j = tc * 4 + b;
-      if (i < kt && j < ks) out[i + (size_t)j * kt] = s[a][b];
+      if (i < kt && j < ks) out[ta * 64 + i + (size_t)(tb * 64 + j) * kt0] = s[a][b];
     }
 }
 
@@ -447,7 +483,8 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
         item_ptr[q + 1] = static_cast<int>(items.size());
       }
     }
-    if (bm > 64) throw std::runtime_error("build_h2_device: local basis dimension > 64 not supported yet");
+    if (l == L && bm > 64) throw std::runtime_error("build_h2_device: leaf size > 64 not supported");
+    const int T = (bm + 63) / 64;  // Gram tiles per side
     std::vector<int> rank(cnt, 0);
     cplx* Ubuf = nullptr;
     if (any_active) {
@@ -485,14 +522,21 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
       int* dip = dev_upload(item_ptr, st);
       BuildLevel BL{bm, dcb, dcs, dkl, ddo, Dbuf, part, nparts, px, py, pz, K};
       CKB(cudaFuncSetAttribute((const void*)k_far_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
-      k_far_gram<<<dim3(cnt, nparts), 256, kTileSmem, st>>>(BL, dit, dip);
+      k_far_gram<<<dim3(cnt, nparts, T * (T + 1) / 2), 256, kTileSmem, st>>>(BL, dit, dip);
       CKB(cudaGetLastError());
       CKB(cudaMallocAsync(&Ubuf, (size_t)cnt * bm * bm * 16, st));
       int* drank = nullptr;
       CKB(cudaMallocAsync(&drank, cnt * 4, st));
-      const size_t smem = 2 * (size_t)bm * bm * 16 + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
+      const size_t small = (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
+      cplx* eigws = nullptr;
+      size_t smem = 2 * (size_t)bm * bm * 16 + small;
+      if (bm > 64) {
+        CKB(cudaMallocAsync(&eigws, (size_t)cnt * 2 * bm * bm * 16, st));
+        smem = small;
+      }
       CKB(cudaFuncSetAttribute((const void*)k_far_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_far_eig<<<cnt, 256, smem, st>>>(BL, all_dup ? 2.0 : 1.0, eps_h2, Ubuf, drank);
+      k_far_eig<<<cnt, 256, smem, st>>>(BL, all_dup ? 2.0 : 1.0, eps_h2, Ubuf, drank, eigws);
+      if (eigws) cudaFreeAsync(eigws, st);
       CKB(cudaGetLastError());
       CKB(cudaMemcpyAsync(rank.data(), drank, cnt * 4, cudaMemcpyDeviceToHost, st));
       CKB(cudaStreamSynchronize(st));
@@ -575,7 +619,10 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
             for (int rc = 0; rc < tn.back(); rc += 64) items2.push_back({static_cast<int>(p), rc, 0});
           iptr.push_back(static_cast<int>(items2.size()));
         }
-        const long long pstride = 64 * 64;
+        int kmx = 1;
+        for (size_t p = 0; p < adm.size(); ++p) kmx = std::max(kmx, std::max(kt[p], ks[p]));
+        const int ntk = (kmx + 63) / 64;
+        const long long pstride = (long long)kmx * kmx;
         cplx* part = nullptr;
         CKB(cudaMallocAsync(&part, std::max<size_t>(items2.size(), 1) * pstride * 16, st));
         long long *dtb = dev_upload(tb, st), *dsb = dev_upload(sb, st), *dEt = dev_upload(Et, st), *dEs = dev_upload(Es, st);
@@ -583,7 +630,7 @@ BuildResult build_h2_device(const Structure& S, const double* points, const std:
         CoupItem* dit = dev_upload(items2, st);
         CoupLevel CLv{dtb, dsb, dtn, dsn, dkt, dks, dEt, dEs, Eprev, part, pstride, px, py, pz, K};
         CKB(cudaFuncSetAttribute((const void*)k_coupling, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
-        if (!items2.empty()) k_coupling<<<static_cast<int>(items2.size()), 256, kTileSmem, st>>>(CLv, dit);
+        if (!items2.empty()) k_coupling<<<dim3(static_cast<int>(items2.size()), ntk * ntk), 256, kTileSmem, st>>>(CLv, dit, ntk);
         // compact output offsets (temporary buffer, then host)
         long long top = 0;
         for (size_t p = 0; p < adm.size(); ++p) ooff.push_back(top), top += (long long)kt[p] * ks[p];

@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(256) k_head2(DevLevel L, const int* batch_cl, 
   cplx* ws = gws + (size_t)q * 2 * bb;
   cplx* LU = ws;        // e x e (ld e)
   cplx* W = ws + bb;    // e x 32 scratch
-  cplx* Dd = blk(L.D, L.diag_blk[t], bm);  // rotated diagonal block (ld b)
+  cplx* Dd = L.D + L.D_off[L.diag_blk[t]];  // rotated diagonal block (ld b)
   if (e == 0) return;
   cta_copy(e, e, Dd, b, LU, e);
   __syncthreads();
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(256) k_hlu_prep(DevLevel L, const int* batch_c
   if (e == 0) return;
   const int N = b + e;
   cplx* M = M0 + (size_t)q * ldm * ldm;
-  const cplx* Dd = blk(L.D, L.diag_blk[t], L.bmax);
+  const cplx* Dd = L.D + L.D_off[L.diag_blk[t]];
   double mx = 0.0;
   for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.y * blockDim.x) {
     const int i = idx % N, j = idx / N;
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch
   cplx* Ui = L.chain + L.Uinv_off[t];
   cplx* Us = L.chain + L.Uself_off[t];  // e x kf, ld e
   cplx* Ls = L.chain + L.Lself_off[t];  // kf x e, ld kf
-  cplx* Dd = blk(L.D, L.diag_blk[t], L.bmax);
+  cplx* Dd = L.D + L.D_off[L.diag_blk[t]];
   const int stride = gridDim.y * blockDim.x;
   for (int idx = blockIdx.y * blockDim.x + threadIdx.x; idx < e * e; idx += stride) {
     const int i = idx % e, j = idx / e;
@@ -987,11 +987,11 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
   if (tg.kind == 0) {
     rows = L.bsz[L.drow[tg.idx]];
     cols = L.bsz[L.dcol[tg.idx]];
-    out = blk(L.D, tg.idx, bm);
+    out = L.D + L.D_off[tg.idx];
   } else {
     rows = L.bsz[L.frow[tg.idx]];
     cols = L.bsz[L.fcol[tg.idx]];
-    out = blk(L.F, tg.idx, bm);
+    out = L.F + L.F_off[tg.idx];
   }
   const int ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
   if ((int)blockIdx.y >= ntr * ntc) return;

@@ -17,13 +17,15 @@ struct DevLevel {
   const int* pos;
   const int* korig;
   int* kfin;
-  // dense blocks (stride bmax^2, ld = rows)
+  // dense blocks, packed (offset D_off[i], rows x cols, ld = rows)
   cplx* D;
+  const long long* D_off;
   const int* drow;
   const int* dcol;
   const int* diag_blk;
-  // fills (stride bmax^2, ld = rows)
+  // fills, packed (offset F_off[i], ld = rows)
   cplx* F;
+  const long long* F_off;
   int* fexists;
   const int* frow;
   const int* fcol;
