@@ -279,10 +279,13 @@ class H2Matrix:
         a = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
         keep = a  # keep buffers alive during the call
         d = _Desc()
-        d.n = int(a["n"])
-        d.depth = int(a["depth"])
-        d.eta = float(a.get("eta", 1.0))
-        d.eps_h2 = float(a.get("eps_h2", 0.0))
+        def scalar(v):
+            return np.asarray(v).reshape(-1)[0]
+
+        d.n = int(scalar(a["n"]))
+        d.depth = int(scalar(a["depth"]))
+        d.eta = float(scalar(a.get("eta", 1.0)))
+        d.eps_h2 = float(scalar(a.get("eps_h2", 0.0)))
         d.cluster_begin = _i64(a["cluster_begin"].astype(np.int64, copy=False))
         d.cluster_end = _i64(a["cluster_end"].astype(np.int64, copy=False))
         d.adm_offsets = _i64(a["adm_offsets"])

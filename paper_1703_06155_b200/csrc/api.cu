@@ -1450,19 +1450,115 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       for (int la = std::max(l0, 0); la <= lv && l0 >= 0; ++la)
         if (!S.adm[la].empty()) needs_paint = true;
       if (nroot > 0) {
-        if (needs_paint) throw Error(H2G_ERR_INTERNAL, "root assembly with admissible blocks (stop-level override / early stop) not implemented yet");
         C->root.alloc((size_t)nroot * nroot * 16, st, true);
+        cplx* R0 = C->root.as<cplx>();
         const size_t bb = (size_t)cur.bmax * cur.bmax;
         std::vector<CopyDesc> cd;
         for (size_t q = 0; q < YR->drow.size(); ++q) {
           const int r = YR->drow[q], c = YR->dcol[q];
           if (!cur.bsz[r] || !cur.bsz[c]) continue;
-          cd.push_back({cur.D.as<cplx>() + cur.doff[q], C->root.as<cplx>() + cur.pos[r] + (size_t)cur.pos[c] * nroot, cur.bsz[r], (int)nroot, cur.bsz[r], cur.bsz[c], 0, 0});
+          cd.push_back({cur.D.as<cplx>() + cur.doff[q], R0 + cur.pos[r] + (size_t)cur.pos[c] * nroot, cur.bsz[r], (int)nroot, cur.bsz[r], cur.bsz[c], 0, 0});
         }
         DBuf dcd;
         upload(dcd, cd, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
         ++launches;
+        // paint (FactorState::paint, factorization.hpp:204-234): admissible
+        // blocks of this level and of every coarser level >= l0, expanded
+        // to this level's clusters (expand_to_level :191-201), plus the
+        // ledger / carried fill-in held in F
+        std::vector<DBuf> Ebuf;  // Ebuf[lv - la]: expanded bases per cluster at ancestor level la
+        std::vector<std::vector<long long>> Eoff;
+        if (needs_paint) {
+          const int nlv = static_cast<int>(cur.bsz.size());
+          const int flv = Structure::first(lv);
+          const int lmin = std::max(l0, 0);
+          auto anc = [&](int u, int la) { return ((flv + u + 1) >> (lv - la)) - 1; };  // heap id of u's ancestor at level la
+          auto kor = [&](int id) { return static_cast<int>(M->basis_rank[id]); };
+          Ebuf.resize(lv - lmin + 1);
+          Eoff.resize(lv - lmin + 1);
+          for (int la = lv - 1; la >= lmin; --la) {
+            const int d = lv - la;
+            long long top = 0;
+            Eoff[d].resize(nlv);
+            for (int u = 0; u < nlv; ++u) Eoff[d][u] = top, top += (long long)cur.bsz[u] * kor(anc(u, la));
+            Ebuf[d].alloc(std::max<long long>(top, 1) * 16, st, true);
+            std::vector<GemmDesc> ge;
+            for (int u = 0; u < nlv; ++u) {
+              const int a = anc(u, la), ch = anc(u, la + 1);
+              const int ka = kor(a), kc = kor(ch), b = cur.bsz[u];
+              if (!ka || !kc || !b) continue;
+              const int roff = (ch == 2 * a + 1) ? 0 : kor(2 * a + 1);
+              const cplx* T = M->basis.as<cplx>() + M->basis_off[a] + roff;
+              const cplx* Ein = d == 1 ? cur.V0.as<cplx>() + (size_t)u * bb : Ebuf[d - 1].as<cplx>() + Eoff[d - 1][u];
+              ge.push_back({Ein, T, Ebuf[d].as<cplx>() + Eoff[d][u], b, (int)M->basis_rows[a], b, b, ka, kc, OP_N, OP_N, 1.0, 0.0});
+            }
+            DBuf dge;
+            upload(dge, ge, st);
+            launch_gemm(dge.as<GemmDesc>(), static_cast<int>(ge.size()), st, 0);
+            launches += !ge.empty();
+          }
+          auto Eptr = [&](int u, int la) -> const cplx* {
+            return la == lv ? cur.V0.as<cplx>() + (size_t)u * bb : Ebuf[lv - la].as<cplx>() + Eoff[lv - la][u];
+          };
+          // X_u = E_u S (b_u x k_col), then root(u, v) = X_u E_v^T
+          std::vector<GemmDesc> gx, gm;
+          std::vector<long long> xoff;
+          long long xtop = 0;
+          struct Job {
+            int u, la, kc, c0, nv;
+            const cplx* S;
+            int kr;
+          };
+          std::vector<Job> jobs;
+          for (int la = lmin; la <= lv; ++la) {
+            for (size_t pq = 0; pq < S.adm[la].size(); ++pq) {
+              const int R = S.adm[la][pq].row, Cc = S.adm[la][pq].col;
+              const int kr = kor(R), kc = kor(Cc);
+              if (!kr || !kc) continue;
+              const cplx* Sm = M->coup.as<cplx>() + M->coup_off[S.adm_offset[la] + pq];
+              const int span = 1 << (lv - la);
+              const int u0 = ((R + 1) << (lv - la)) - 1 - flv, v0 = ((Cc + 1) << (lv - la)) - 1 - flv;
+              for (int u = u0; u < u0 + span; ++u) {
+                if (!cur.bsz[u]) continue;
+                jobs.push_back({u, la, kc, v0, span, Sm, kr});
+                xoff.push_back(xtop);
+                xtop += (long long)cur.bsz[u] * kc;
+              }
+            }
+          }
+          DBuf xbuf;
+          xbuf.alloc(std::max<long long>(xtop, 1) * 16, st);
+          for (size_t j = 0; j < jobs.size(); ++j) {
+            const Job& J = jobs[j];
+            const int b = cur.bsz[J.u];
+            cplx* X = xbuf.as<cplx>() + xoff[j];
+            gx.push_back({Eptr(J.u, J.la), J.S, X, b, J.kr, b, b, J.kc, J.kr, OP_N, OP_N, 1.0, 0.0});
+            for (int v = J.c0; v < J.c0 + J.nv; ++v) {
+              if (!cur.bsz[v]) continue;
+              gm.push_back({X, Eptr(v, J.la), R0 + cur.pos[J.u] + (size_t)cur.pos[v] * nroot, b, cur.bsz[v], (int)nroot, b, cur.bsz[v], J.kc, OP_N,
+                            OP_T, 1.0, 0.0});
+            }
+          }
+          DBuf dgx, dgm;
+          upload(dgx, gx, st);
+          upload(dgm, gm, st);
+          launch_gemm(dgx.as<GemmDesc>(), static_cast<int>(gx.size()), st, cur.bmax);
+          launch_gemm(dgm.as<GemmDesc>(), static_cast<int>(gm.size()), st, cur.bmax);
+          launches += (!gx.empty()) + (!gm.empty());
+          // fill-in deltas (zero where no fill was deposited)
+          std::vector<CopyDesc> cf;
+          for (size_t f = 0; f < YR->frow.size(); ++f) {
+            const int u = YR->frow[f], v = YR->fcol[f];
+            if (!cur.bsz[u] || !cur.bsz[v]) continue;
+            cf.push_back({cur.F.as<cplx>() + cur.foff[f], R0 + cur.pos[u] + (size_t)cur.pos[v] * nroot, cur.bsz[u], (int)nroot, cur.bsz[u], cur.bsz[v], 1, 0});
+          }
+          DBuf dcf;
+          upload(dcf, cf, st);
+          launch_copy(dcf.as<CopyDesc>(), static_cast<int>(cf.size()), st);
+          launches += !cf.empty();
+          CK(cudaStreamSynchronize(st));
+        }
         DBuf scratch;
         scratch.alloc(64, st);
         ctx->prof.begin(PC_ROOT, st);

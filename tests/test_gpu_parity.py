@@ -165,3 +165,39 @@ def test_gpu_matvec_matches_oracle():
     G = upload(A)
     x = O.rhs(A.n, 7)
     assert rel(G.matvec(x), A.matvec(x)) < 1e-12
+
+
+@pytest.mark.parametrize("extra", [1, 2, "depth"])
+def test_stop_level_override_paints_root(extra):
+    """factorize(A, eps, stop_level_override) above l0: the root is painted
+    from dense blocks, admissible couplings of this and coarser levels
+    expanded to the root level, and the ledger / carried fill-in
+    (factorization.hpp:204-234, 636-651); GPU against the oracle."""
+    A = rod_problem(400, 1e-10, leaf=25)
+    och_default = A.factorize(1e-10)
+    l0 = och_default.stop_level
+    stop = A.tree.depth if extra == "depth" else min(l0 + extra, A.tree.depth)
+    och = A.factorize(1e-10, stop_level=stop)
+    gch = h2g.factorize(upload(A), 1e-10, stop_level_override=stop)
+    assert gch.stop_level == och.stop_level == stop
+    assert gch.root_size == och.root_size > 0
+    compare_chains(och, gch, 0)
+    b = O.rhs(400, 21)
+    xo, xg = och.solve(b), gch.solve(b)
+    assert rel(xg, xo) < 1e-9
+    assert rel(xg, A.shadow_solve(b)) < 1e-8
+
+
+def test_vie_stop_override_matches_oracle():
+    A, K = vie_problem(16, 0.5, 32, 1e-4)
+    och0 = A.factorize(1e-4)
+    stop = och0.stop_level + 1
+    och = A.factorize(1e-4, stop_level=stop)
+    gch = h2g.factorize(upload(A), 1e-4, stop_level_override=stop)
+    assert gch.root_size == och.root_size
+    compare_chains(och, gch, rank_tol=1)
+    perm = A.tree.perm
+    b = O.rhs(A.n, 77)[perm]
+    xo, xg = och.solve(b), gch.solve(b)
+    assert rel(xg, xo) <= 10 * 1e-4
+    assert A.relative_residual(xg, b) <= 2 * A.relative_residual(xo, b) + 1e-14
