@@ -270,6 +270,10 @@ struct h2g_context {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_crit = nullptr, ev_bulk = nullptr;
   Prof prof_side;
+  // helper stream for small independent kernels of the main chain
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
+  Prof prof_aux;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevError* d_err = nullptr;
   int* d_flag = nullptr;
@@ -465,6 +469,9 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
     CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
     CK(cudaEventCreateWithFlags(&c->ev_crit, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_bulk, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_hi));
+    CK(cudaEventCreateWithFlags(&c->ev_aux0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_aux1, cudaEventDisableTiming));
     BlockCache::get().add_stream(c->stream);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
@@ -488,6 +495,10 @@ int h2g_context_destroy(h2g_context* ctx) {
   BlockCache::get().remove_stream(ctx->stream);
   cudaEventDestroy(ctx->ev_crit);
   cudaEventDestroy(ctx->ev_bulk);
+  cudaStreamSynchronize(ctx->aux);
+  cudaEventDestroy(ctx->ev_aux0);
+  cudaEventDestroy(ctx->ev_aux1);
+  cudaStreamDestroy(ctx->aux);
   cudaStreamDestroy(ctx->side);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_flag);
@@ -676,6 +687,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     ctx->prof.reset();
     ctx->prof_side.reset();
     ctx->prof_side.on = ctx->prof.on;
+    ctx->prof_aux.reset();
+    ctx->prof_aux.on = ctx->prof.on;
     CK(cudaEventRecord(ctx->ev0, st));
     long long launches = 0;
     double flops = 0.0, sflops = 0.0, sbytes = 0.0;
@@ -1084,14 +1097,21 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
           const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
           Prof& pf = ctx->prof;
-          pf.begin(PC_GRAM, st);
           const int tl = bm;  // max GEMM dimension of this level's per-cluster products
+          // column norms of the fill entering W on the helper stream, concurrent
+          // with the projection / Gram GEMMs
+          CK(cudaEventRecord(ctx->ev_aux0, st));
+          CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_aux0, 0));
+          ctx->prof_aux.cur_level = l;
+          ctx->prof_aux.begin(PC_COLNORM, ctx->aux);
+          launch_colnorm(dN.as<NormDesc>() + n_ptr[bi], nn, ctx->aux);
+          ctx->prof_aux.end(ctx->aux);
+          CK(cudaEventRecord(ctx->ev_aux1, ctx->aux));
+          pf.begin(PC_GRAM, st);
           launch_gemm(dA1.as<GemmDesc>() + a_ptr[bi], na, st, tl);
           launch_gemm(dB1.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
           pf.end(st);
-          pf.begin(PC_COLNORM, st);
-          launch_colnorm(dN.as<NormDesc>() + n_ptr[bi], nn, st);
-          pf.end(st);
+          CK(cudaStreamWaitEvent(st, ctx->ev_aux1, 0));
           pf.begin(PC_EIG1, st);
           int mmax = 0;
           for (int pq = p0; pq < p0 + nb; ++pq) mmax = std::max(mmax, cur.bsz[SC.batch_cl[pq]] - cur.korig[SC.batch_cl[pq]]);
@@ -1100,10 +1120,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             pf.begin(ph == 1 ? PC_EIGVEC : PC_EIG1B, st);
           });
           pf.end(st);
-          pf.begin(PC_GRAM, st);
-          launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st, tl);
-          launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
-          pf.end(st);
+          const bool pass2_possible = eig1_refine_possible(DL);
+          if (pass2_possible) {
+            pf.begin(PC_GRAM, st);
+            launch_gemm(dA2.as<GemmDesc>() + a_ptr[bi], na, st, tl);
+            launch_gemm(dB2.as<GemmDesc>() + b_ptr[bi], nbd, st, tl);
+            pf.end(st);
+          }
           pf.begin(PC_HEAD, st);
           launch_head(DL, d_bat + p0, p0, nb, st);
           launch_gemm(dR1.as<GemmDesc>() + p0, nb, st, tl);
@@ -1138,16 +1161,16 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             C->klaunch[PC_SCHUR] += (ncr > 0) + (nbulk > 0);
             launches += (ncr > 0) + (nbulk > 0);
           }
-          C->klaunch[PC_GRAM] += 2 * ((na > 0) + (nbd > 0));
+          C->klaunch[PC_GRAM] += (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0));
           C->klaunch[PC_COLNORM] += nn > 0;
-          C->klaunch[PC_EIG1] += 2;
+          C->klaunch[PC_EIG1] += 1 + pass2_possible;
           C->klaunch[PC_EIGVEC] += mmax > 0;
           C->klaunch[PC_EIG1B] += 6;
           const int nhead = 3 + (mmax > 64 ? 2 + 2 * ((mmax + 31) / 32) : 1);
           C->klaunch[PC_HEAD] += nhead;
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
-          launches += 8 + (mmax > 0) + nhead + 2 * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
+          launches += 7 + pass2_possible + (mmax > 0) + nhead + (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();
@@ -1596,6 +1619,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       std::map<std::pair<int, int>, double> per;
       std::vector<Prof::Rec> all(ctx->prof.recs);
       all.insert(all.end(), ctx->prof_side.recs.begin(), ctx->prof_side.recs.end());
+      all.insert(all.end(), ctx->prof_aux.recs.begin(), ctx->prof_aux.recs.end());
       for (const auto& r : all) {
         float e = 0.f;
         cudaEventElapsedTime(&e, r.a, r.b);

@@ -1329,9 +1329,13 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   }
   {
     const size_t small = (size_t)L.bmax * 8 + (size_t)L.bmax * 4 + (size_t)(L.bmax + 2) * 4 + 16 + (size_t)4 * (L.bmax / 2 + 1) * 8 + 64;
-    set_smem((const void*)k_eig1_refine, small);
-    k_eig1_refine<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
-    post_launch("k_eig1_refine");
+    // the refinement pass can only trigger when thr = eps max(s0, cmax) can
+    // fall below 1e-4 s0, i.e. for eps < 1e-4 (k_eig1c)
+    if (eig1_refine_possible(L)) {
+      set_smem((const void*)k_eig1_refine, small);
+      k_eig1_refine<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
+      post_launch("k_eig1_refine");
+    }
   }
   phase(1);
   if (mmax > 0) {

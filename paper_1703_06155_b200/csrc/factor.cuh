@@ -135,6 +135,8 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim = 0);
+// Step-0 refinement pass (k_eig1_refine, pass-2 Gram) reachable only for eps < 1e-4.
+inline bool eig1_refine_possible(const DevLevel& L) { return L.eps < 1e-4 || (L.debug & 4); }
 void launch_zero_desc_flags(int* p, int n, cudaStream_t s);
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches);
 size_t head_smem_bytes(int bmax);
