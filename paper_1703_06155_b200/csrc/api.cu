@@ -910,53 +910,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             gR1.push_back({Qt, Dtt, Tq, b, b, b, b, b, b, OP_C, OP_N, 1.0, 0.0, nullptr, nullptr});
             gR2.push_back({Tq, Qt, Dtt, b, b, b, b, b, b, OP_N, OP_R, 1.0, 0.0, nullptr, nullptr});
           }
-        // step-0 eigensolver workspace and the compact-WY descriptor GEMMs
-        // (sizes resolved on the device from the retained rank r)
+        // step-0 eigensolver workspace (per batch slot)
         mark("gram descriptors built");
         DBuf eigws;
         eigws.alloc((size_t)mb * eig1_ws_bytes(bm), st);
-        std::vector<GemmDesc> gW;
-        {
-          const size_t wsc = eig1_ws_bytes(bm) / 16;
-          std::vector<GemmDesc> w0, w1, w2, w3;
-          for (int q = 0; q < mb; ++q) {
-            cplx* ws = eigws.as<cplx>() + (size_t)q * wsc;
-            cplx* Yq = ws;
-            cplx* X1 = ws + 2 * bb + 4 * bm;
-            cplx* X2 = X1 + bb;
-            cplx* Tm = X2 + bb;
-            cplx* Sm = Tm + bb;
-            (void)Sm;
-            const int* dr = d_rank1 + q;
-            const int* skp = d_pass2 + q;
-            // placeholders: m/n/k below are patched per batch (b, m depend on the cluster)
-            w0.push_back({Yq, Yq, Sm, 0, 0, 0, 0, 0, 0, OP_C, OP_N, 1.0, 0.0, nullptr, nullptr, dr, 1, 1, 0, 0, skp});
-            w1.push_back({nullptr, Yq, X1, 0, 0, 0, 0, 0, 0, OP_N, OP_N, 1.0, 0.0, nullptr, nullptr, dr, 0, 1, 0, 0, skp});
-            w2.push_back({X1, Tm, X2, 0, 0, 0, 0, 0, 0, OP_N, OP_N, 1.0, 0.0, nullptr, nullptr, dr, 0, 1, 1, 0, skp});
-            w3.push_back({X2, Yq, nullptr, 0, 0, 0, 0, 0, 0, OP_N, OP_C, -1.0, 1.0, nullptr, nullptr, dr, 0, 0, 1, 0, skp});
-          }
-          // per batch: 4 groups of nb descriptors, patched with the slot's cluster sizes
-          for (int bi = 0; bi < nbat0; ++bi) {
-            const int p0b = SC.batch_ptr[bi], nbb = SC.batch_ptr[bi + 1] - p0b;
-            std::vector<GemmDesc> g[4];
-            for (int q = 0; q < nbb; ++q) {
-              const int t = SC.batch_cl[p0b + q];
-              const int b = cur.bsz[t], m = b - cur.korig[t];
-              const cplx* Vp = cur.Vp.as<cplx>() + (size_t)t * bb;
-              cplx* D1 = dirbuf.as<cplx>() + (size_t)q * bb;
-              GemmDesc a = w0[q];  // S = Y^H Y: r x r, k = m
-              a.lda = m, a.ldb = m, a.ldc = bm, a.k = m;
-              GemmDesc bq = w1[q];  // X1 = Vp Y: b x r, k = m
-              bq.A = Vp, bq.lda = b, bq.ldb = m, bq.ldc = b, bq.m = b, bq.k = m;
-              GemmDesc c = w2[q];  // X2 = X1 T: b x r, k = r (T stored with ld bm)
-              c.lda = b, c.ldb = bm, c.ldc = b, c.m = b;
-              GemmDesc d = w3[q];  // D1 -= X2 Y^H: b x m, k = r
-              d.C = D1, d.lda = b, d.ldb = m, d.ldc = b, d.m = b, d.n = m;
-              g[0].push_back(a), g[1].push_back(bq), g[2].push_back(c), g[3].push_back(d);
-            }
-            for (int i = 0; i < 4; ++i) gW.insert(gW.end(), g[i].begin(), g[i].end());
-          }
-        }
         // step 2/3b panels as descriptor GEMMs (device-resolved e = b - kfin):
         // column item D(t,c): T = Qt^H D, Ubar = L11^{-1} T[:e,:], lift = Ubar Qt_c^T, D = T (rows < e zeroed)
         // row item    D(j,t): T = D conj(Qt), Lbar = T[:,:e] U11^{-1}, lift = Qt_j Lbar, D = T (cols < e zeroed)
@@ -967,8 +924,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         for (int bi = 0; bi < nbat0; ++bi) pmax = std::max<size_t>(pmax, W.panel_ptr[bi + 1] - W.panel_ptr[bi]);
         DBuf panbuf;
         panbuf.alloc(pmax * bb * 16, st);
-        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dW, dP1, dP2, dP3, dPM;
-        upload(dW, gW, st);
+        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dP1, dP2, dP3, dPM;
         upload(dR1, gR1, st);
         upload(dR2, gR2, st);
         upload(dA1, gA1, st);
@@ -1115,7 +1071,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           pf.begin(PC_EIG1, st);
           int mmax = 0;
           for (int pq = p0; pq < p0 + nb; ++pq) mmax = std::max(mmax, cur.bsz[SC.batch_cl[pq]] - cur.korig[SC.batch_cl[pq]]);
-          launch_eig1(DL, d_bat + p0, p0, nb, mmax, dW.as<GemmDesc>() + 4 * p0, tl, st, [&](int ph) {
+          launch_eig1(DL, d_bat + p0, p0, nb, mmax, st, [&](int ph) {
             pf.end(st);
             pf.begin(ph == 1 ? PC_EIGVEC : PC_EIG1B, st);
           });
@@ -1165,12 +1121,12 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           C->klaunch[PC_COLNORM] += nn > 0;
           C->klaunch[PC_EIG1] += 1 + pass2_possible;
           C->klaunch[PC_EIGVEC] += mmax > 0;
-          C->klaunch[PC_EIG1B] += 6;
+          C->klaunch[PC_EIG1B] += 2;
           const int nhead = 3 + (mmax > 64 ? 2 + 2 * ((mmax + 31) / 32) : 1);
           C->klaunch[PC_HEAD] += nhead;
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
-          launches += 7 + pass2_possible + (mmax > 0) + nhead + (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
+          launches += 3 + pass2_possible + (mmax > 0) + nhead + (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_complement(DevLevel L, cplx* gws) {
   cta_copy(b, b - k, Q + (size_t)k * b, b, Vp, b);
 }
 
-// H, U, then 4.5 bm^2 of scratch (inverse iteration, then the compact-WY GEMMs)
+// H, U, then scratch for inverse iteration and the blocked QR
 // H, U, aux (8 bm), X1, X2, Tm, Sm (bm^2 each), tau (bm)
 __host__ __device__ inline size_t eig1_ws_cplx(int bm) { return (size_t)bm * bm * 6 + (size_t)bm * 9 + 16; }
 
@@ -591,11 +591,9 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
   for (int i = threadIdx.x; i < m; i += blockDim.x) U[i + (size_t)m * j] = y[i];
 }
 
-// D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H = I - Y T Y^H, the compact WY form
-// of a Householder QR of the retained eigenvectors U_r: [new | complement].
-// k_eig1b: blocked QR of U_r and the explicit Y; S = Y^H Y (descriptor GEMM);
-// k_eig1t: T recurrence and D1 = Vp; then X1 = Vp Y, X2 = X1 T and
-// D1 -= X2 Y^H as descriptor GEMMs with r resolved on the device.
+// D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H from a Householder QR of the
+// retained eigenvectors U_r: [new | complement]. k_eig1b: blocked QR of U_r,
+// the explicit reflectors Y and tau; k_eig1_apply: D1 row by row.
 __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, cplx* gws) {
   __shared__ cplx tile_sm[kTileSmemCplx];
   __shared__ double red[32];
@@ -624,36 +622,59 @@ __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, 
   for (int i = threadIdx.x; i < r; i += blockDim.x) tau_g[i] = tau[i];
 }
 
-__global__ void __launch_bounds__(256) k_eig1t(DevLevel L, const int* batch_cl, cplx* gws) {
+// D1 = Vp H_0^H H_1^H ... H_{r-1}^H applied row by row: every row of D1 is
+// transformed independently (d <- d - conj(tau_j) (d y_j) y_j^H), so one warp
+// per row streams through the r reflectors with no block-wide barrier. This
+// replaces the compact-WY chain (S = Y^H Y, T recurrence, three GEMMs).
+__global__ void __launch_bounds__(256) k_eig1_apply(DevLevel L, const int* batch_cl, const cplx* gws) {
+  constexpr int kMaxPer = 16;  // m <= 512
   const int q = blockIdx.x;
   if (L.pass2[q]) return;
-  const int r = L.rank1[q];
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int row = blockIdx.y * (blockDim.x / 32) + warp;
+  if (row >= b || m == 0) return;
   const size_t bb = (size_t)bm * bm;
-  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
-  cplx* D1 = L.dir + (size_t)q * bb;
+  const int r = L.rank1[q];
+  const cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  const cplx* Y = ws;                                    // m x r, unit lower trapezoidal
+  const cplx* tau_g = ws + 2 * bb + 4 * bm + 4 * bb;
   const cplx* Vp = L.Vp + (size_t)t * bb;
-  cta_copy(b, m, Vp, b, D1, b);
-  if (r == 0 || m == 0) return;
-  cplx* X1 = ws + 2 * bb + 4 * bm;
-  cplx* Tm = X1 + 2 * bb;
-  const cplx* Sm = Tm + bb;
-  const cplx* tau_g = X1 + 4 * bb;
-  // T (upper, r x r, ld bm): T_kk = conj(tau_k), T[0:k,k] = -conj(tau_k) T[0:k,0:k] S[0:k,k]
-  for (int kk = 0; kk < r; ++kk) {
-    const cplx tk = cconj(tau_g[kk]);
-    for (int i = threadIdx.x; i < r; i += blockDim.x) {
-      cplx v = czero();
-      if (i < kk) {
-        for (int jj = i; jj < kk; ++jj) cfma(v, Tm[i + (size_t)jj * bm], Sm[jj + (size_t)kk * bm]);
-        v = cmul(cmk(-tk.x, -tk.y), v);
-      } else if (i == kk) {
-        v = tk;
+  cplx* D1 = L.dir + (size_t)q * bb;
+  cplx d[kMaxPer];
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int c = lane + 32 * u;
+    d[u] = c < m ? Vp[row + (size_t)c * b] : czero();
+  }
+  for (int j = 0; j < r; ++j) {
+    const cplx* y = Y + (size_t)j * m;
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxPer; ++u) {
+      const int c = lane + 32 * u;
+      if (c < m && c >= j) {
+        const cplx yv = y[c];
+        sr += d[u].x * yv.x - d[u].y * yv.y;
+        si += d[u].x * yv.y + d[u].y * yv.x;
       }
-      Tm[i + (size_t)kk * bm] = v;
     }
-    __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
+    const cplx f = cmul(cconj(tau_g[j]), cmk(sr, si));
+#pragma unroll
+    for (int u = 0; u < kMaxPer; ++u) {
+      const int c = lane + 32 * u;
+      if (c < m && c >= j) d[u] = csub(d[u], cmul(f, cconj(y[c])));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int c = lane + 32 * u;
+    if (c < m) D1[row + (size_t)c * b] = d[u];
   }
 }
 
@@ -1295,7 +1316,7 @@ size_t eig1_smem_bytes(int bm) { return eig1_ws_cplx(bm) * sizeof(cplx) + eig1_s
 
 size_t eig1_ws_bytes(int bmax) { return eig1_ws_cplx(bmax) * sizeof(cplx); }
 
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int maxdim, cudaStream_t s,
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s,
                  const std::function<void(int)>& phase) {
   cplx* ws = L.eigws;
   {
@@ -1348,12 +1369,9 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   set_smem((const void*)k_eig1b, (size_t)L.bmax * 16 * sizeof(cplx));
   k_eig1b<<<nb, 256, (size_t)L.bmax * 16 * sizeof(cplx), s>>>(L, batch_cl, ws);
   post_launch("k_eig1b");
-  launch_gemm(wy, nb, s, maxdim);              // S = Y^H Y
-  k_eig1t<<<nb, 256, 0, s>>>(L, batch_cl, ws);
-  post_launch("k_eig1t");
-  launch_gemm(wy + nb, nb, s, maxdim);         // X1 = Vp Y
-  launch_gemm(wy + 2 * nb, nb, s, maxdim);     // X2 = X1 T
-  launch_gemm(wy + 3 * nb, nb, s, maxdim);     // D1 -= X2 Y^H
+  if (mmax > 512) throw std::runtime_error("k_eig1_apply: complement dimension > 512");
+  k_eig1_apply<<<dim3(nb, (L.bmax + 7) / 8), 256, 0, s>>>(L, batch_cl, ws);
+  post_launch("k_eig1_apply");
 }
 
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s) {

@@ -122,7 +122,7 @@ struct NormDesc {
 };
 
 void launch_complement(const DevLevel& L, cudaStream_t s);
-void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, const GemmDesc* wy, int maxdim, cudaStream_t s,
+void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s,
                  const std::function<void(int)>& phase);
 size_t eig1_ws_bytes(int bmax);
 void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStream_t s);
