@@ -245,7 +245,9 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     fms, sms, flaunch, slaunch = [], [], [], []
+    ch = None
     for _ in range(args.steps):
+        ch = None  # release the previous chain first: its device blocks are reused
         ch = h2g.factorize(A, eps, schedule=args.schedule)
         x = ch.solve(b)
         tm = ch.timing()

@@ -192,7 +192,8 @@ __device__ inline void cta_householder_qr(int m, int n, cplx* A, int lda, cplx* 
     __syncthreads();
     const int triv = s_triv;
     const cplx denom = s_denom, tk = s_tau;
-    for (int i = 1 + threadIdx.x; i < m - k; i += blockDim.x) x[i] = triv ? czero() : cdiv(x[i], denom);
+    const cplx rden = triv ? czero() : cdiv(cone(), denom);
+    for (int i = 1 + threadIdx.x; i < m - k; i += blockDim.x) x[i] = triv ? czero() : cmul(x[i], rden);
     __syncthreads();
     // apply H to A[k:, k+1:]: one warp per column
     if (!triv) {
@@ -996,19 +997,21 @@ __device__ inline void cta_householder_qr_blocked(int m, int n, cplx* A, int lda
       W2[idx] = v;  // S
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int kk = 0; kk < kb; ++kk) {
-        const cplx tk = cconj(tau[j0 + kk]);
-        for (int i = 0; i < kk; ++i) {
-          cplx v = czero();
-          for (int j = i; j < kk; ++j) cfma(v, Tb[i + j * 16], W2[j + kk * kb]);
-          Tb[i + kk * 16] = cmul(cmk(-tk.x, -tk.y), v);
-        }
+    // T column by column, rows of a column in parallel
+    for (int kk = 0; kk < kb; ++kk) {
+      const cplx tk = cconj(tau[j0 + kk]);
+      const int i = threadIdx.x;
+      if (i < kk) {
+        cplx v = czero();
+        for (int j = i; j < kk; ++j) cfma(v, Tb[i + j * 16], W2[j + kk * kb]);
+        Tb[i + kk * 16] = cmul(cmk(-tk.x, -tk.y), v);
+      } else if (i == kk) {
         Tb[kk + kk * 16] = tk;
-        for (int i = kk + 1; i < kb; ++i) Tb[i + kk * 16] = czero();
+      } else if (i < kb) {
+        Tb[i + kk * 16] = czero();
       }
+      __syncthreads();
     }
-    __syncthreads();
     // A_trail <- Qp^H A_trail = A_trail - Y (T^H (Y^H A_trail))
     cplx* At = A + j0 + (size_t)(j0 + kb) * lda;
     cta_gemm_tiled(kb, nt, mr, 1.0, P, mr, OP_C, At, lda, OP_N, 0.0, W, 16, tile_sm);
