@@ -149,12 +149,28 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     return;  // uniform over the cluster
   }
   const int g0 = L.slot_g0[p], gn = L.slot_gn[p];
-  for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
-    const int i = idx % m, jl = idx / m, c = rank + kHC * jl;
-    cplx s = czero();
-    if (c < m)
-      for (int g = 0; g < gn; ++g) s = cadd(s, L.gram[L.gram_off[g0 + g] + i + (size_t)c * m]);
-    Hl[idx] = s;
+  __shared__ long long s_goff[128];
+  for (int gb = 0; gb < gn; gb += 128) {
+    const int gc = min(128, gn - gb);
+    __syncthreads();
+    for (int g = threadIdx.x; g < gc; g += blockDim.x) s_goff[g] = L.gram_off[g0 + gb + g];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
+      const int i = idx % m, jl = idx / m, c = rank + kHC * jl;
+      cplx s0 = gb ? Hl[idx] : czero(), s1 = czero(), s2 = czero(), s3 = czero();
+      if (c < m) {
+        const size_t e = i + (size_t)c * m;
+        int g = 0;
+        for (; g + 4 <= gc; g += 4) {
+          s0 = cadd(s0, L.gram[s_goff[g] + e]);
+          s1 = cadd(s1, L.gram[s_goff[g + 1] + e]);
+          s2 = cadd(s2, L.gram[s_goff[g + 2] + e]);
+          s3 = cadd(s3, L.gram[s_goff[g + 3] + e]);
+        }
+        for (; g < gc; ++g) s0 = cadd(s0, L.gram[s_goff[g] + e]);
+      }
+      Hl[idx] = cadd(cadd(s0, s1), cadd(s2, s3));
+    }
   }
   if (L.debug & 8) tm1 = gtimer();
   // remote views of every CTA's partial / result buffers
