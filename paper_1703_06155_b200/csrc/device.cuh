@@ -826,6 +826,115 @@ __device__ __forceinline__ void tile_pipe(cplx (&acc)[TM / 8][TM / 16], TileSmem
   __syncthreads();
 }
 
+// 64 x 64 complex tile on the FP64 tensor cores (DMMA m8n8k4): 4 warps, each
+// a 32 x 32 warp tile of 4 x 4 m8n8 tiles with separate real / imaginary
+// accumulators; the k-slices are the same cp.async stages as tile_pipe.
+// Thread (g, tq) = (lane / 4, lane % 4) holds rows wr + 8 mi + g and columns
+// wc + 8 ni + 2 tq + h of its warp tile.
+struct Acc64 {
+  double re[4][4][2], im[4][4][2];
+};
+
+__device__ __forceinline__ void acc64_zero(Acc64& c) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) c.re[a][b][0] = c.re[a][b][1] = c.im[a][b][0] = c.im[a][b][1] = 0.0;
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};" : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// f(i, j, v) for every accumulator element (i, j tile-local)
+template <class F>
+__device__ __forceinline__ void acc64_each(const Acc64& c, F&& f) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wr = (warp % 2) * 32, wc = (warp / 2) * 32, g = lane / 4, tq = lane % 4;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) f(wr + mi * 8 + g, wc + ni * 8 + tq * 2 + h, make_double2(c.re[mi][ni][h], c.im[mi][ni][h]));
+}
+
+template <bool CA, bool CB>
+__device__ __forceinline__ void tile_pipe_dmma(Acc64& acc, TileSmem<64>& S, const cplx* A, int lda, bool at, int ash, int am, const cplx* B,
+                                               int ldb, bool bt, int bsh, int bn, int k) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wr = (warp % 2) * 32, wc = (warp / 2) * 32, g = lane / 4, tq = lane % 4;
+  const int nk = (k + 7) / 8;
+  __syncthreads();
+  auto load = [&](int st, int kc) {
+    const int k0 = kc * 8;
+    for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+      int i, p;
+      if (at) p = idx % 8, i = idx / 8;
+      else i = idx % 64, p = idx / 64;
+      const int ai = i + ash;
+      const bool va = k0 + p < k && ai >= 0 && ai < am;
+      const cplx* ga = at ? A + (k0 + p) + (size_t)ai * lda : A + ai + (size_t)(k0 + p) * lda;
+      cp_async16(&S.a[st][p][i], va ? ga : A, va);
+      int j, q;
+      if (bt) j = idx % 64, q = idx / 64;
+      else q = idx % 8, j = idx / 8;
+      const int bj = j + bsh;
+      const bool vb = k0 + q < k && bj >= 0 && bj < bn;
+      const cplx* gb = bt ? B + bj + (size_t)(k0 + q) * ldb : B + (k0 + q) + (size_t)bj * ldb;
+      cp_async16(&S.b[st][q][j], vb ? gb : B, vb);
+    }
+    cp_async_commit();
+  };
+  for (int st = 0; st < 2; ++st) {
+    if (st < nk) load(st, st);
+    else cp_async_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    asm volatile("cp.async.wait_group 1;");
+    __syncthreads();
+    const int st = kc % 3;
+    if (kc + 2 < nk) load((kc + 2) % 3, kc + 2);
+    else cp_async_commit();
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+      cplx af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        af[mi] = S.a[st][kk + tq][wr + mi * 8 + g];
+        if (CA) af[mi].y = -af[mi].y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        bf[ni] = S.b[st][kk + tq][wc + ni * 8 + g];
+        if (CB) bf[ni].y = -bf[ni].y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma884(acc.re[mi][ni][0], acc.re[mi][ni][1], af[mi].x, bf[ni].x);
+          dmma884(acc.re[mi][ni][0], acc.re[mi][ni][1], -af[mi].y, bf[ni].y);
+          dmma884(acc.im[mi][ni][0], acc.im[mi][ni][1], af[mi].x, bf[ni].y);
+          dmma884(acc.im[mi][ni][0], acc.im[mi][ni][1], af[mi].y, bf[ni].x);
+        }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tile_acc_dmma(Acc64& acc, TileSmem<64>& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B, int ldb,
+                                              int opB, int bsh, int bn, int k) {
+  if (k <= 0) return;
+  const bool at = opA == OP_T || opA == OP_C, bt = opB == OP_T || opB == OP_C;
+  const bool ca = opA == OP_C || opA == OP_R, cb = opB == OP_C || opB == OP_R;
+  if (!ca && !cb) tile_pipe_dmma<false, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (ca && !cb) tile_pipe_dmma<true, false>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else if (!ca && cb) tile_pipe_dmma<false, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+  else tile_pipe_dmma<true, true>(acc, S, A, lda, at, ash, am, B, ldb, bt, bsh, bn, k);
+}
+
 // acc[tile row i][tile col j] += sum_p op(A)[i + ash, p] op(B)[p, j + bsh]
 // (rows outside [0, am) / cols outside [0, bn) of op(A) / op(B) read as zero).
 template <int TM>

@@ -953,23 +953,16 @@ __global__ void __launch_bounds__(128, 3) k_hlu_update(DevLevel L, const int* ba
   cplx* M = M0 + (size_t)q * ldm * ldm;
   for (int tile = blockIdx.y; tile < nt * nt; tile += gridDim.y) {
     const int r0 = (tile % nt) * 64, c0 = (tile / nt) * 64;
-    cplx acc[8][4];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb) acc[a][bb] = czero();
-    tile128_acc(acc, S, M + c + (size_t)j0 * ldm, ldm, OP_N, r0, rest, M + j0 + (size_t)c * ldm, ldm, OP_N, c0, rest, kb);
-    const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb) {
-        const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + bb;
-        if (i < rest && j < rest) {
-          cplx* o = M + (c + i) + (size_t)(c + j) * ldm;
-          *o = csub(*o, acc[a][bb]);
-        }
+    Acc64 acc;
+    acc64_zero(acc);
+    tile_acc_dmma(acc, S, M + c + (size_t)j0 * ldm, ldm, OP_N, r0, rest, M + j0 + (size_t)c * ldm, ldm, OP_N, c0, rest, kb);
+    acc64_each(acc, [&](int ii, int jj, cplx v) {
+      const int i = r0 + ii, j = c0 + jj;
+      if (i < rest && j < rest) {
+        cplx* o = M + (c + i) + (size_t)(c + j) * ldm;
+        *o = csub(*o, v);
       }
+    });
   }
 }
 
@@ -1033,11 +1026,8 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
   const int ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
   if ((int)blockIdx.y >= ntr * ntc) return;
   const int r0 = (blockIdx.y % ntr) * 64, c0 = (blockIdx.y / ntr) * 64;
-  cplx acc[8][4];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = czero();
+  Acc64 acc;
+  acc64_zero(acc);
   bool touched = false;
   for (int ci = tg.c0; ci < tg.c1; ++ci) {
     const SchurContribD cb = contrib[ci];
@@ -1069,19 +1059,15 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     // the contribution covers target rows [ro, ro+arows) x cols [co, co+bcols)
     const int ash = r0 - ro, bsh = c0 - co;
     if (ash >= arows || bsh >= bcols || ash + 64 <= 0 || bsh + 64 <= 0) continue;
-    tile128_acc(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
+    tile_acc_dmma(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
   }
-  const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = r0 + tr + 8 * a, j = c0 + tc * 4 + b;
-      if (i < rows && j < cols && (acc[a][b].x != 0.0 || acc[a][b].y != 0.0)) {
-        cplx* o = out + i + (size_t)j * rows;
-        *o = csub(*o, acc[a][b]);
-      }
+  acc64_each(acc, [&](int ii, int jj, cplx v) {
+    const int i = r0 + ii, j = c0 + jj;
+    if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
+      cplx* o = out + i + (size_t)j * rows;
+      *o = csub(*o, v);
     }
+  });
   if (tg.kind == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
 }
 
@@ -1146,6 +1132,19 @@ __global__ void __launch_bounds__(128, 3) k_gemm(const GemmDesc* descs) {
   // each CTA walks the tiles blockIdx.y, blockIdx.y + gridDim.y, ...
   for (int tile = blockIdx.y; tile < ntr * ntc; tile += gridDim.y) {
     const int r0 = (tile % ntr) * TM, c0 = (tile / ntr) * TM;
+    if constexpr (TM == 64) {
+      Acc64 acc;
+      acc64_zero(acc);
+      if (!zero) tile_acc_dmma(acc, S, d.A, d.lda, d.opA, r0, d.m, d.B, d.ldb, d.opB, c0, d.n, d.k);
+      acc64_each(acc, [&](int ii, int jj, cplx v) {
+        const int i = r0 + ii, j = c0 + jj;
+        if (i < d.m && j < d.n) {
+          cplx* o = d.C + i + (size_t)j * d.ldc;
+          *o = d.beta == 0.0 ? cscale(v, d.alpha) : make_double2(d.beta * o->x + d.alpha * v.x, d.beta * o->y + d.alpha * v.y);
+        }
+      });
+      continue;
+    }
     cplx acc[RM][RN];
 #pragma unroll
     for (int a = 0; a < RM; ++a)

@@ -239,6 +239,76 @@ __global__ void __launch_bounds__(128) v6(int M, int N, int K, const cplx* A, co
     for (int b = 0; b < 4; ++b) C[r0 + tr + 8 * a + (size_t)(c0 + tc * 4 + b) * M] = acc[a][b];
 }
 
+// V7: DMMA m8n8k4 on interleaved complex k-slices staged by a 3-stage cp.async
+// pipeline (padded rows); 4 warps, each a 32x32 complex warp tile (4x4 m8n8
+// tiles, re/im accumulators).
+template <int STG>
+__global__ void __launch_bounds__(128) v7(int M, int N, int K, const cplx* A, const cplx* B, cplx* C) {
+  extern __shared__ __align__(16) unsigned char raw[];
+  cplx(*sA)[8][65] = reinterpret_cast<cplx(*)[8][65]>(raw);
+  cplx(*sB)[8][65] = reinterpret_cast<cplx(*)[8][65]>(raw + STG * 8 * 65 * 16);
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wr = (warp % 2) * 32, wc = (warp / 2) * 32;
+  const int g = lane / 4, tq = lane % 4;
+  double re[4][4][2], im[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) re[a][b][0] = re[a][b][1] = im[a][b][0] = im[a][b][1] = 0.0;
+  const int nk = (K + 7) / 8;
+  auto load = [&](int st, int kc) {
+    const int k0 = kc * 8;
+    for (int idx = threadIdx.x; idx < 64 * 8; idx += 128) {
+      const int i = idx % 64, p = idx / 64;
+      const bool va = k0 + p < K;
+      cp16(&sA[st][p][i], A + r0 + i + (size_t)(va ? k0 + p : 0) * M, va);
+      const int q = idx % 8, j = idx / 8;
+      const bool vb = k0 + q < K;
+      cp16(&sB[st][q][j], B + (vb ? k0 + q : 0) + (size_t)(c0 + j) * K, vb);
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  for (int s = 0; s < STG - 1; ++s) {
+    if (s < nk) load(s, s);
+    else asm volatile("cp.async.commit_group;");
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STG - 2));
+    __syncthreads();
+    const int st = kc % STG;
+    const int nxt = kc + STG - 1;
+    if (nxt < nk) load(nxt % STG, nxt);
+    else asm volatile("cp.async.commit_group;");
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4) {
+      cplx af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = sA[st][kk + tq][wr + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = sB[st][kk + tq][wc + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          dmma(re[mi][ni][0], re[mi][ni][1], af[mi].x, bf[ni].x);
+          dmma(re[mi][ni][0], re[mi][ni][1], -af[mi].y, bf[ni].y);
+          dmma(im[mi][ni][0], im[mi][ni][1], af[mi].x, bf[ni].y);
+          dmma(im[mi][ni][0], im[mi][ni][1], af[mi].y, bf[ni].x);
+        }
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = r0 + wr + mi * 8 + g, col = c0 + wc + ni * 8 + tq * 2 + h;
+        C[row + (size_t)col * M] = make_double2(re[mi][ni][h], im[mi][ni][h]);
+      }
+}
+
 int main() {
   const int M = 4096, N = 4096, K = 512;
   cplx *A, *B, *C;
@@ -256,7 +326,9 @@ int main() {
   cudaFuncSetAttribute((const void*)v6<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 2 * 8 * 64 * 16);
   cudaFuncSetAttribute((const void*)v6<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 8 * 64 * 16);
   cudaFuncSetAttribute((const void*)v6<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 2 * 8 * 64 * 16);
-  for (int v = 1; v <= 7; ++v) {
+  cudaFuncSetAttribute((const void*)v7<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 2 * 8 * 65 * 16);
+  cudaFuncSetAttribute((const void*)v7<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 2 * 8 * 65 * 16);
+  for (int v = 1; v <= 9; ++v) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
       if (v == 1) v1<<<g, 256>>>(M, N, K, A, B, C);
@@ -266,6 +338,8 @@ int main() {
       if (v == 5) v6<3><<<g, 128, 3 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
       if (v == 6) v6<4><<<g, 128, 4 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
       if (v == 7) v6<6><<<g, 128, 6 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C);
+      if (v == 8) v7<3><<<g, 128, 3 * 2 * 8 * 65 * 16>>>(M, N, K, A, B, C);
+      if (v == 9) v7<4><<<g, 128, 4 * 2 * 8 * 65 * 16>>>(M, N, K, A, B, C);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -283,13 +357,13 @@ int main() {
     cplx* C2;
     cudaMalloc(&C2, (size_t)M * N * 16);
     v4<<<g, 128>>>(M, N, K, A, B, C);
-    v6<4><<<g, 128, 4 * 2 * 8 * 64 * 16>>>(M, N, K, A, B, C2);
+    v7<3><<<g, 128, 3 * 2 * 8 * 65 * 16>>>(M, N, K, A, B, C2);
     std::vector<double> c1((size_t)M * N * 2), c2((size_t)M * N * 2);
     cudaMemcpy(c1.data(), C, c1.size() * 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(c2.data(), C2, c2.size() * 8, cudaMemcpyDeviceToHost);
     double md = 0, mx = 0;
     for (size_t i = 0; i < c1.size(); ++i) md = fmax(md, fabs(c1[i] - c2[i])), mx = fmax(mx, fabs(c1[i]));
-    printf("v6 vs v4 max abs diff %.3e (max %.3e)\n", md, mx);
+    printf("v7 vs v4 max abs diff %.3e (max %.3e)\n", md, mx);
   }
   return 0;
 }
