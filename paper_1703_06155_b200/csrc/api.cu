@@ -1619,7 +1619,13 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   if ((size_t)n * nrhs * 16 > C->tmpbuf.bytes) C->tmpbuf.alloc((size_t)n * nrhs * 16, st);
   cplx* tmp = C->tmpbuf.as<cplx>();
   const bool fwd = mode != H2G_BACKWARD, bwd = mode != H2G_FORWARD;
-  const int expl = mode == H2G_APPLY_INVERSE_EXPLICIT;
+  // The record heads apply the factorization's stored L11^{-1} / U11^{-1}
+  // (GEMVs over the chain data) in every mode: the sequential triangular
+  // substitution (solve.hpp:47-50, :73-81) costs one block barrier per
+  // eliminated row on the critical path. Set H2G_SOLVE_TRIANGULAR=1 for the
+  // substitution form.
+  static const bool tri = std::getenv("H2G_SOLVE_TRIANGULAR") && std::atoi(std::getenv("H2G_SOLVE_TRIANGULAR"));
+  const int expl = (mode == H2G_APPLY_INVERSE_EXPLICIT || !tri) ? 1 : 0;
   long long launches = 1;
   // right-hand sides per pass of the level kernels: 2 * bmax * rchunk
   // complex of shared memory per CTA stays under ~96 KB

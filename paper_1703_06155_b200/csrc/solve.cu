@@ -12,6 +12,41 @@
 
 namespace h2g {
 
+// out = op(A) x for an n x n matrix A in global memory (op: N, R = conj, or
+// C = conj-transpose), x / out n x nrhs in shared memory: one warp per output
+// row with the lanes spread over the row's k range (many independent loads in
+// flight), up to 8 right-hand sides per pass over A.
+__device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const cplx* x, int ldx, cplx* out, int ldo) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int c0 = 0; c0 < nrhs; c0 += 8) {
+    const int nc = min(8, nrhs - c0);
+    for (int i = warp; i < n; i += nw) {
+      cplx acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = czero();
+      for (int p = lane; p < n; p += 32) {
+        cplx av;
+        if (op == OP_C) av = cconj(A[p + (size_t)i * lda]);
+        else if (op == OP_R) av = cconj(A[i + (size_t)p * lda]);
+        else av = A[i + (size_t)p * lda];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < nc) cfma(acc[c], av, x[p + (size_t)(c0 + c) * ldx]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c >= nc) break;
+        double re = acc[c].x, im = acc[c].y;
+        for (int o = 16; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0) out[i + (size_t)(c0 + c) * ldo] = make_double2(re, im);
+      }
+    }
+  }
+}
+
 // seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50); one CTA per
 // record.
 __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, unsigned char* smraw) {
@@ -22,7 +57,7 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
   __syncthreads();
   const cplx* Q = S.chain + S.Qt_off[t];
-  cta_gemm(b, nrhs, b, 1.0, Q, b, OP_C, sS, b, OP_N, 0.0, sO, b);
+  warp_gemv(b, nrhs, Q, b, OP_C, sS, b, sO, b);
   __syncthreads();
   if (e > 0) {
     if (explicit_inv) {
