@@ -324,7 +324,17 @@ def main():
         else:
             roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        roof.update({"traffic": None, "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / max(sch["launches"], 1),
+        traffic, tsrc = None, None
+        import glob
+        for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_schur_traffic.json"))):
+            try:
+                tj = json.load(open(f))
+            except Exception:
+                continue
+            if tj.get("config") == args.config and tj.get("launches") == sch["launches"]:
+                traffic, tsrc = tj["traffic_per_launch"], os.path.relpath(f, ROOT) + " (ncu dram__bytes_read+write per k_schur launch, same launch list)"
+        roof.update({"traffic": traffic, "traffic_source": tsrc, "algorithmic_bytes_per_launch": sch["bytes"] / max(sch["launches"], 1),
+                     "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / max(sch["launches"], 1),
                      "algorithmic_flops": sch["flops"], "algorithmic_bytes": sch["bytes"], "share_of_factorize": sch["ms"] / max(prof_total, 1e-9),
                      "tflops": tf, "gbs": gbs})
     breakdown = {k: {"ms": round(v["ms"], 3), "launches": v["launches"]} for k, v in stats.items()}
