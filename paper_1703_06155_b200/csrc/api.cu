@@ -6,6 +6,7 @@
 // to the parent (finish_level :445-475, merge_permute :483-584) with
 // descriptor-driven batched copies/GEMMs; the remainder is LU-factored on the
 // device (:637-651). There is no CPU fallback.
+#include <functional>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -109,7 +110,7 @@ class BlockCache {
     std::lock_guard<std::mutex> g(mu_);
     live_.erase(s);
     auto& fl = free_[s];
-    for (auto& kv : fl) cudaFree(kv.second);
+    for (auto& kv : fl) cudaFree(kv.second), cached_ -= kv.first;
     free_.erase(s);
   }
   void* alloc(size_t n, cudaStream_t s) {
@@ -121,6 +122,7 @@ class BlockCache {
         auto it = fl.lower_bound(r);
         if (it != fl.end() && it->first <= r + r / 4 + (4u << 20)) {
           void* p = it->second;
+          cached_ -= it->first;
           fl.erase(it);
           return p;
         }
@@ -132,6 +134,13 @@ class BlockCache {
       cudaGetLastError();
       trim();
       e = cudaMallocAsync(&p, r, s);
+      // still short: let the running factorization move finished chain
+      // levels to host memory, one at a time
+      while (e == cudaErrorMemoryAllocation && spill && spill()) {
+        cudaGetLastError();
+        trim();
+        e = cudaMallocAsync(&p, r, s);
+      }
     }
     if (e != cudaSuccess) throw Error(H2G_ERR_CUDA, std::string("device allocation of ") + std::to_string(n) + " bytes: " + cudaGetErrorString(e));
     std::lock_guard<std::mutex> g(mu_);
@@ -143,6 +152,7 @@ class BlockCache {
     auto it = size_.find(p);
     if (it != size_.end() && live_.count(s)) {
       free_[s].emplace(it->second, p);
+      cached_ += it->second;
       return;
     }
     if (it != size_.end()) size_.erase(it);
@@ -157,15 +167,41 @@ class BlockCache {
     for (auto& fs : free_) {
       for (auto& kv : fs.second) {
         size_.erase(kv.second);
+        cached_ -= kv.first;
         cudaFreeAsync(kv.second, fs.first);
       }
       fs.second.clear();
       cudaStreamSynchronize(fs.first);
     }
+    // and the pool's own reserve (release threshold is "keep everything")
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   }
+
+  // device bytes a new allocation can still obtain: driver-free memory, the
+  // pool's reserve and the blocks parked in this cache
+  size_t headroom() {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    size_t pool_spare = 0;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t res = 0, used = 0;
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      pool_spare = res > used ? res - used : 0;
+    }
+    std::lock_guard<std::mutex> g(mu_);
+    return fr + pool_spare + cached_;
+  }
+
+  std::function<bool()> spill;  // set by h2g_factorize while it runs
 
  private:
   std::mutex mu_;
+  size_t cached_ = 0;
   std::set<cudaStream_t> live_;
   std::map<cudaStream_t, std::multimap<size_t, void*>> free_;
   std::unordered_map<void*, size_t> size_;
@@ -201,6 +237,36 @@ struct DBuf {
       p = BlockCache::get().alloc(n, st);
       if (zero) CK(cudaMemsetAsync(p, 0, n, st));
     }
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Pinned, device-mapped host memory. Used only when a configuration does not
+// fit in HBM (config 3: the level-12 -> 11 merge cores and the chains of
+// finished levels); kernels read / write it in place over the host link.
+struct HBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() { release(); }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n) {
+    release();
+    if (cudaHostAlloc(&p, std::max<size_t>(n, 16), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw Error(H2G_ERR_CUDA, std::string("pinned host allocation of ") + std::to_string(n) + " bytes failed");
+    }
+    bytes = n;
   }
   template <class T>
   T* as() const {
@@ -295,6 +361,8 @@ struct h2g_matrix {
   std::vector<int64_t> basis_rows, basis_rank, basis_off, coup_off, dense_off;
   int64_t basis_elems = 0, coup_elems = 0, dense_elems = 0;
   DBuf basis, coup, dense;
+  HBuf hdense;  // the dense blocks, moved to pinned host memory when HBM runs short (config 3)
+  const cplx* dense_ptr() const { return hdense.p ? hdense.as<cplx>() : dense.as<cplx>(); }
   std::vector<std::unique_ptr<PlanCache>> plans;
   std::mutex mu;
 };
@@ -306,6 +374,9 @@ struct ChainLevelHost {
   std::vector<int64_t> src;  // permutation
   // device-resident solve data
   DBuf arena;                // chain numeric data of this level
+  HBuf harena;               // ... or here, once offloaded to pinned host memory
+  const cplx* chain_ptr() const { return harena.p ? harena.as<cplx>() : arena.as<cplx>(); }
+  size_t chain_bytes() const { return harena.p ? harena.bytes : arena.bytes; }
   DBuf meta;                 // packed int / offset arrays
   SolveLevel sl{};
   std::vector<int> batch_ptr, batch_maxc;
@@ -640,7 +711,7 @@ int h2g_matrix_download(const h2g_matrix* m, int64_t* cb, int64_t* ce, int64_t* 
     if (dense_offset) std::copy(m->dense_off.begin(), m->dense_off.end(), dense_offset);
     if (basis_data && m->basis_elems) CK(cudaMemcpyAsync(basis_data, m->basis.p, m->basis_elems * 16, cudaMemcpyDeviceToHost, s));
     if (coupling_data && m->coup_elems) CK(cudaMemcpyAsync(coupling_data, m->coup.p, m->coup_elems * 16, cudaMemcpyDeviceToHost, s));
-    if (dense_data && m->dense_elems) CK(cudaMemcpyAsync(dense_data, m->dense.p, m->dense_elems * 16, cudaMemcpyDeviceToHost, s));
+    if (dense_data && m->dense_elems) CK(cudaMemcpyAsync(dense_data, m->dense_ptr(), m->dense_elems * 16, cudaMemcpyDefault, s));
     CK(cudaStreamSynchronize(s));
   });
 }
@@ -650,7 +721,7 @@ int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y
     if (!ctx || !m || !x || !y || nrhs < 1) throw Error(H2G_ERR_INVALID_INPUT, "matvec: bad arguments");
     CK(cudaSetDevice(ctx->device));
     matvec_device(m->S, m->basis_rows, m->basis_rank, m->basis_off, m->coup_off, m->dense_off, m->basis.as<cplx>(), m->coup.as<cplx>(),
-                  m->dense.as<cplx>(), x, y, nrhs, ctx->stream);
+                  m->dense_ptr(), x, y, nrhs, ctx->stream);
   });
 }
 
@@ -714,7 +785,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       std::vector<CopyDesc> cd;
       for (size_t q = 0; q < Y.drow.size(); ++q) {
         const int r = Y.drow[q], c = Y.dcol[q];
-        cd.push_back({M->dense.as<cplx>() + M->dense_off[q], cur.D.as<cplx>() + cur.doff[q], cur.bsz[r], cur.bsz[r], cur.bsz[r], cur.bsz[c], 0, 0});
+        cd.push_back({M->dense_ptr() + M->dense_off[q], cur.D.as<cplx>() + cur.doff[q], cur.bsz[r], cur.bsz[r], cur.bsz[r], cur.bsz[c], 0, 0});
       }
       for (int t = 0; t < nl; ++t)
         if (cur.korig[t] > 0)
@@ -731,6 +802,51 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
 
     int li = 0;
     int last_level = L;  // level whose state is "cur" at the root
+    // HBM budget: when the next allocation would not fit, finished levels'
+    // chains move to pinned host memory (oldest first); the solve then reads
+    // them over the host link (config 3 only; configs 1-2 never trigger this)
+    const size_t kMargin = size_t(8) << 30;
+    size_t offloaded = 0;
+    auto offload_chain = [&](ChainLevelHost& X) {
+      X.harena.alloc(X.arena.bytes);
+      CK(cudaMemcpyAsync(X.harena.p, X.arena.p, X.arena.bytes, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      offloaded += X.arena.bytes;
+      X.arena.release();
+      X.sl.chain = X.harena.as<cplx>();
+    };
+    struct SpillGuard {
+      ~SpillGuard() { BlockCache::get().spill = nullptr; }
+    } spill_guard;
+    // the input's dense blocks are only read at the leaf-level entry (and by
+    // the matvec); they are the second thing to leave HBM
+    auto offload_dense = [&]() -> bool {
+      if (M->hdense.p || !M->dense.p || M->dense_elems == 0) return false;
+      M->hdense.alloc(M->dense_elems * 16);
+      CK(cudaMemcpyAsync(M->hdense.p, M->dense.p, M->dense_elems * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      M->dense.release();
+      return true;
+    };
+    BlockCache::get().spill = [&]() -> bool {
+      for (auto& X : C->levels)
+        if (X->arena.p) {
+          offload_chain(*X);
+          return true;
+        }
+      return offload_dense();
+    };
+    auto ensure = [&](size_t need, ChainLevelHost* extra) {
+      if (BlockCache::get().headroom() >= need + kMargin) return;
+      CK(cudaStreamSynchronize(st));
+      BlockCache::get().trim();
+      for (auto& X : C->levels) {
+        if (BlockCache::get().headroom() >= need + kMargin) return;
+        if (X->arena.p) offload_chain(*X), BlockCache::get().trim();
+      }
+      if (extra && extra->arena.p && BlockCache::get().headroom() < need + kMargin) offload_chain(*extra), BlockCache::get().trim();
+      if (BlockCache::get().headroom() < need + kMargin && offload_dense()) BlockCache::get().trim();
+    };
     const int verbose = std::getenv("H2G_VERBOSE") ? std::atoi(std::getenv("H2G_VERBOSE")) : 0;
     auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     double tlev = wall();
@@ -764,9 +880,30 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         mark("offsets");
         auto CL = std::make_unique<ChainLevelHost>();
         CL->level = l;
+        // lifted panels (Qt_n Lbar / Ubar Qt_n^T for neighbours n eliminated
+        // earlier, deposit_fill :359-366): packed, only the lifted entries
+        std::vector<long long> liftL_off(Y.R_nb.size(), -1), liftU_off(Y.C_nb.size(), -1);
+        // only panels that feed a fill-in target are lifted
+        std::vector<char> needL(Y.R_nb.size(), 0), needU(Y.C_nb.size(), 0);
+        for (const SchurContrib& cb : W.contrib) {
+          if (cb.flags & 1) needL[cb.r] = 1;
+          if (cb.flags & 2) needU[cb.c] = 1;
+        }
+        auto lifted = [&](const PanelItem& pi) { return pi.lift && (pi.side == 0 ? needU[pi.entry] : needL[pi.entry]); };
+        long long ltop = 0;
+        for (size_t bi = 0; bi + 1 < SC.batch_ptr.size(); ++bi)
+          for (int it = W.panel_ptr[bi]; it < W.panel_ptr[bi + 1]; ++it) {
+            const PanelItem& pi = W.panel[it];
+            if (!lifted(pi)) continue;
+            const int t = SC.batch_cl[SC.batch_ptr[bi] + pi.q];
+            const long long em = cur.bsz[t] - cur.korig[t];
+            (pi.side == 0 ? liftU_off : liftL_off)[pi.entry] = ltop;
+            ltop += em * cur.bsz[pi.nb];
+          }
+        ensure((size_t)(std::max<long long>(top, 1) + std::max<long long>(ltop, 1) + (long long)nl * bb) * 16 + (size_t(4) << 30), nullptr);
         CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
         DBuf lift;
-        lift.alloc(std::max<long long>(top, 1) * 16, st);
+        lift.alloc(std::max<long long>(ltop, 1) * 16, st);
         mark("chain allocated");
         // ---- per-level device metadata
         Packer pk;
@@ -782,6 +919,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         size_t o_Gp = pk.add(Y.G_ptr), o_Gf = pk.add(Y.G_fill), o_Gt = pk.add(Y.G_tr);
         size_t o_Qt = pk.add(Qt_off), o_L11 = pk.add(L11_off), o_U11 = pk.add(U11_off), o_Li = pk.add(Linv_off), o_Ui = pk.add(Uinv_off);
         size_t o_Lb = pk.add(Lbar_off), o_Ub = pk.add(Ubar_off), o_Ls = pk.add(Lself_off), o_Us = pk.add(Uself_off);
+        size_t o_lL = pk.add(liftL_off), o_lU = pk.add(liftU_off);
         size_t o_bat = pk.add(SC.batch_cl);
         size_t o_sch = pk.add_raw(reinterpret_cast<const SchurTargetD*>(W.schur.data()), W.schur.size());
         size_t o_con = pk.add_raw(reinterpret_cast<const SchurContribD*>(W.contrib.data()), W.contrib.size());
@@ -974,6 +1112,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.Lself_off = at<long long>(mt, o_Ls);
         DL.Uself_off = at<long long>(mt, o_Us);
         DL.lift = lift.as<cplx>();
+        DL.liftL_off = at<long long>(mt, o_lL);
+        DL.liftU_off = at<long long>(mt, o_lU);
         DL.Linv_off = at<long long>(mt, o_Li);
         DL.Uinv_off = at<long long>(mt, o_Ui);
         DL.slot_g0 = at<int>(meta2, o_sg0);
@@ -1011,8 +1151,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                 // Ubar (e x bn, ld e) = L11^{-1} (e x e, ld e) T[:e, :]
                 pp = {chainb + Linv_off[t], T, chainb + Ubar_off[pi.entry], b, b, b, b, bn, b, OP_N, OP_N, 1.0, 0.0};
                 pp.dyn = kfd + t, pp.mi = -1, pp.ki = -1, pp.ldneg = 1 | 4;
-                if (pi.lift) {
-                  lf = {chainb + Ubar_off[pi.entry], Qn, liftb + Ubar_off[pi.entry], b, bn, b, b, bn, bn, OP_N, OP_T, 1.0, 0.0};
+                if (lifted(pi)) {
+                  lf = {chainb + Ubar_off[pi.entry], Qn, liftb + liftU_off[pi.entry], b, bn, b, b, bn, bn, OP_N, OP_T, 1.0, 0.0};
                   lf.dyn = kfd + t, lf.mi = -1, lf.ldneg = 1 | 4;
                 }
                 gPM.push_back({T, Dblk, b, b, bn, 0, b, 0, kfd + t});
@@ -1021,15 +1161,15 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                 // Lbar (bn x e, ld bn) = T[:, :e] U11^{-1} (e x e, ld e)
                 pp = {T, chainb + Uinv_off[t], chainb + Lbar_off[pi.entry], bn, b, bn, bn, b, b, OP_N, OP_N, 1.0, 0.0};
                 pp.dyn = kfd + t, pp.ni = -1, pp.ki = -1, pp.ldneg = 2;
-                if (pi.lift) {
-                  lf = {Qn, chainb + Lbar_off[pi.entry], liftb + Lbar_off[pi.entry], bn, bn, bn, bn, b, bn, OP_N, OP_N, 1.0, 0.0};
+                if (lifted(pi)) {
+                  lf = {Qn, chainb + Lbar_off[pi.entry], liftb + liftL_off[pi.entry], bn, bn, bn, bn, b, bn, OP_N, OP_N, 1.0, 0.0};
                   lf.dyn = kfd + t, lf.ni = -1;
                 }
                 gPM.push_back({T, Dblk, bn, bn, b, 1, b, 0, kfd + t});
               }
               gP1.push_back(r);
               gP2.push_back(pp);
-              if (pi.lift) gP3.push_back(lf);
+              if (lifted(pi)) gP3.push_back(lf);
             }
             p3_ptr.push_back(static_cast<int>(gP3.size()));
           }
@@ -1145,6 +1285,15 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaStreamSynchronize(st));
 
         mark("kfin read back");
+        // level scratch is dead once the last batch has drained (keeps the
+        // merge's peak memory down at config 3)
+        lift.release();
+        panbuf.release();
+        ybuf.release();
+        gbuf.release();
+        dirbuf.release();
+        rotbuf.release();
+        eigws.release();
         const double sflops_lv0 = sflops, flops_lv0 = flops;
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
@@ -1300,38 +1449,38 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         const size_t bbp = (size_t)nxt.bmax * nxt.bmax;
         const long long ndtot = pack_offsets(YP.drow, YP.dcol, nxt.bsz, nxt.doff);
         const long long nftot = pack_offsets(YP.frow, YP.fcol, nxt.bsz, nxt.foff);
-        nxt.D.alloc(std::max<long long>(ndtot, 1) * 16, st, true);
-        nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
-        nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
-        nxt.V0.alloc((size_t)nlp * bbp * 16, st, true);
-        std::vector<CopyDesc> cd;
-        std::vector<GemmDesc> g1, g2;
-        long long tmp_top = 0;
-        std::vector<long long> tmp_off;
-        cplx* Dp = nxt.D.as<cplx>();
-        cplx* Fp = nxt.F.as<cplx>();
+        // Merge in two phases so that the level-l fill pool and the level-(l-1)
+        // pools never coexist: (1) project every fill that survives the merge
+        // to its compact kfin_a x kfin_c core Z = V_a^H F conj(V_c)
+        // (factorization.hpp:455, :540), (2) release the level-l fill pool and
+        // the level scratch, allocate level l-1 and assemble it.
+        std::vector<CopyDesc> cd;  // dst pointers relative to nxt.D (dst_kind 0) / nxt.F (1), fixed up after allocation
+        std::vector<int> cd_kind;
         const cplx* chainp = CL->arena.as<cplx>();
         auto Vptr = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kfin[t]) * cur.bsz[t]; };
         struct PendingG {
-          int a, c, fi;
-          cplx* dst;
+          int a, c, fi, kind;
+          long long doff;  // element offset of the destination in nxt.D / nxt.F
           int ldd;
         };
         std::vector<PendingG> pend;
         const auto& admL = S.adm[l];
         for (size_t pq = 0; pq < YP.drow.size(); ++pq) {
           const int Pr = YP.drow[pq], Pc = YP.dcol[pq];
-          cplx* dst = Dp + nxt.doff[pq];
+          const long long dbase = nxt.doff[pq];
           const int ldd = nxt.bsz[Pr];
           for (int ia = 0; ia < 2; ++ia)
             for (int ic = 0; ic < 2; ++ic) {
               const int a = 2 * Pr + ia, c = 2 * Pc + ic;
               const int ro = ia ? kfin[2 * Pr] : 0, co = ic ? kfin[2 * Pc] : 0;
+              const long long doff = dbase + ro + (long long)co * ldd;
               const int di = Y.dense_index(a, c);
               if (di >= 0) {
                 const int ea = cur.bsz[a] - kfin[a], ec = cur.bsz[c] - kfin[c];
-                if (kfin[a] && kfin[c])
-                  cd.push_back({cur.D.as<cplx>() + cur.doff[di] + ea + (size_t)ec * cur.bsz[a], dst + ro + (size_t)co * ldd, cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
+                if (kfin[a] && kfin[c]) {
+                  cd.push_back({cur.D.as<cplx>() + cur.doff[di] + ea + (size_t)ec * cur.bsz[a], reinterpret_cast<cplx*>(doff * 16), cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
+                  cd_kind.push_back(0);
+                }
               } else {
                 const Pair hp{a + Y.first, c + Y.first};
                 auto it = std::lower_bound(admL.begin(), admL.end(), hp, [](const Pair& x, const Pair& y) { return x.row < y.row || (x.row == y.row && x.col < y.col); });
@@ -1339,9 +1488,12 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                   throw Error(H2G_ERR_INVALID_INPUT, "merge_permute: child block is neither dense nor admissible");
                 const int64_t gi = S.adm_offset[l] + (it - admL.begin());
                 const int ka = cur.korig[a], kc = cur.korig[c];
-                if (ka && kc) cd.push_back({M->coup.as<cplx>() + M->coup_off[gi], dst + ro + (size_t)co * ldd, ka, ldd, ka, kc, 0, 0});
+                if (ka && kc) {
+                  cd.push_back({M->coup.as<cplx>() + M->coup_off[gi], reinterpret_cast<cplx*>(doff * 16), ka, ldd, ka, kc, 0, 0});
+                  cd_kind.push_back(0);
+                }
                 const int fi = Y.fill_index(a, c);
-                if (fi >= 0 && fex[fi] && kfin[a] && kfin[c]) pend.push_back({a, c, fi, dst + ro + (size_t)co * ldd, ldd});
+                if (fi >= 0 && fex[fi] && kfin[a] && kfin[c]) pend.push_back({a, c, fi, 0, doff, ldd});
               }
             }
         }
@@ -1355,23 +1507,96 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           if (!kfin[j] || !kfin[c]) continue;
           const int ro = (j & 1) ? kfin[j - 1] : 0, co = (c & 1) ? kfin[c - 1] : 0;
           const int ldd = nxt.bsz[YP.frow[pf]];
-          pend.push_back({j, c, static_cast<int>(f), Fp + nxt.foff[pf] + ro + (size_t)co * ldd, ldd});
+          pend.push_back({j, c, static_cast<int>(f), 1, nxt.foff[pf] + ro + (long long)co * ldd, ldd});
         }
-        for (const auto& pg : pend) {
-          const int a = pg.a, c = pg.c;
-          tmp_off.push_back(tmp_top);
-          tmp_top += (long long)kfin[a] * cur.bsz[c];
+        // phase 1: compact cores Z (chunked X = V_a^H F temporaries)
+        std::vector<long long> zoff(pend.size());
+        long long ztop = 0;
+        for (size_t q = 0; q < pend.size(); ++q) zoff[q] = ztop, ztop += (long long)kfin[pend[q].a] * kfin[pend[q].c];
+        // chunks bounded by 2 GB of X and 2 GB of Z; when Z does not fit in
+        // HBM next to the level-l fill pool it is staged through pinned host
+        // memory chunk by chunk (bulk copies, config 3)
+        const long long kChunk = (2LL << 30) / 16;
+        std::vector<size_t> chunk_q(1, 0);
+        {
+          long long xt = 0, zt = 0;
+          for (size_t q = 0; q < pend.size(); ++q) {
+            const long long xn = (long long)kfin[pend[q].a] * cur.bsz[pend[q].c], zn = (long long)kfin[pend[q].a] * kfin[pend[q].c];
+            if (q > chunk_q.back() && (xt + xn > kChunk || zt + zn > kChunk)) chunk_q.push_back(q), xt = 0, zt = 0;
+            xt += xn, zt += zn;
+          }
+          chunk_q.push_back(pend.size());
         }
-        DBuf tmp;
-        tmp.alloc(std::max<long long>(tmp_top, 1) * 16, st);
-        for (size_t q = 0; q < pend.size(); ++q) {
-          const auto& pg = pend[q];
-          const int a = pg.a, c = pg.c;
-          cplx* X = tmp.as<cplx>() + tmp_off[q];
-          // X = V_a^H F (kfin_a x b_c);  dst += X conj(V_c)   (factorization.hpp:455, :540)
-          g1.push_back({Vptr(a), cur.F.as<cplx>() + cur.foff[pg.fi], X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
-          g2.push_back({X, Vptr(c), pg.dst, kfin[a], cur.bsz[c], pg.ldd, kfin[a], kfin[c], cur.bsz[c], OP_N, OP_R, 1.0, 1.0});
+        const int nchunk = static_cast<int>(chunk_q.size()) - 1;
+        DBuf zdev;  // all of Z (in HBM) or one chunk (host-staged)
+        HBuf zhost;
+        const bool zstaged = BlockCache::get().headroom() < (size_t)ztop * 16 + (size_t(4) << 30) + kMargin;
+        long long zchunk_max = 1;
+        for (int ck = 0; ck < nchunk; ++ck)
+          if (chunk_q[ck + 1] > chunk_q[ck])
+            zchunk_max = std::max(zchunk_max, (chunk_q[ck + 1] < pend.size() ? zoff[chunk_q[ck + 1]] : ztop) - zoff[chunk_q[ck]]);
+        if (zstaged) {
+          zhost.alloc((size_t)std::max<long long>(ztop, 1) * 16);
+          zdev.alloc(zchunk_max * 16, st);
+          mark("merge: pinned Z allocated");
+        } else {
+          zdev.alloc(std::max<long long>(ztop, 1) * 16, st);
         }
+        auto zdst = [&](size_t q, int ck) { return zdev.as<cplx>() + (zstaged ? zoff[q] - zoff[chunk_q[ck]] : zoff[q]); };
+        auto zlen = [&](int ck) { return (chunk_q[ck + 1] < pend.size() ? zoff[chunk_q[ck + 1]] : ztop) - zoff[chunk_q[ck]]; };
+        {
+          DBuf tmp, dg1, dg2;
+          for (int ck = 0; ck < nchunk; ++ck) {
+            const size_t q0 = chunk_q[ck], q1 = chunk_q[ck + 1];
+            if (q1 == q0) continue;
+            std::vector<long long> xoff;
+            long long xtop = 0;
+            for (size_t q = q0; q < q1; ++q) xoff.push_back(xtop), xtop += (long long)kfin[pend[q].a] * cur.bsz[pend[q].c];
+            tmp.alloc(std::max<long long>(xtop, 1) * 16, st);
+            std::vector<GemmDesc> g1, g2;
+            for (size_t q = q0; q < q1; ++q) {
+              const auto& pg = pend[q];
+              const int a = pg.a, c = pg.c;
+              cplx* X = tmp.as<cplx>() + xoff[q - q0];
+              // X = V_a^H F (kfin_a x b_c);  Z = X conj(V_c)   (factorization.hpp:455, :540)
+              g1.push_back({Vptr(a), cur.F.as<cplx>() + cur.foff[pg.fi], X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
+              g2.push_back({X, Vptr(c), zdst(q, ck), kfin[a], cur.bsz[c], kfin[a], kfin[a], kfin[c], cur.bsz[c], OP_N, OP_R, 1.0, 0.0});
+            }
+            upload(dg1, g1, st);
+            upload(dg2, g2, st);
+            ctx->prof.begin(PC_MERGE, st);
+            const int tlm = std::max(bm, nxt.bmax);
+            launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, tlm);
+            launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, tlm);
+            ctx->prof.end(st);
+            if (zstaged) CK(cudaMemcpyAsync(zhost.as<cplx>() + zoff[q0], zdev.p, zlen(ck) * 16, cudaMemcpyDeviceToHost, st));
+            C->klaunch[PC_MERGE] += 2;
+            launches += 2;
+          }
+        }
+        for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
+        mark("merge: phase 1 launched");
+        // phase 2: the level-l fill pool and scratch are dead
+        cur.F.release();
+        cur.fex.release();
+        cur.Vp.release();
+        if (zstaged) offload_chain(*CL), BlockCache::get().trim();  // memory is tight: this level's chain goes to the host too
+        mark("merge: phase 1 done");
+        ensure((size_t)(std::max<long long>(ndtot, 1) + std::max<long long>(nftot, 1) + (long long)nlp * bbp) * 16, CL.get());
+        nxt.D.alloc(std::max<long long>(ndtot, 1) * 16, st, true);
+        nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
+        nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
+        nxt.V0.alloc((size_t)nlp * bbp * 16, st, true);
+        cplx* Dp = nxt.D.as<cplx>();
+        cplx* Fp = nxt.F.as<cplx>();
+        for (size_t q = 0; q < cd.size(); ++q) cd[q].dst = (cd_kind[q] ? Fp : Dp) + reinterpret_cast<long long>(cd[q].dst) / 16;
+        // cores accumulate after the coupling / dense-corner copies (dst = S + Z)
+        std::vector<CopyDesc> cz;
+        for (int ck = 0; ck < nchunk; ++ck)
+          for (size_t q = chunk_q[ck]; q < chunk_q[ck + 1]; ++q) {
+            const auto& pg = pend[q];
+            cz.push_back({zdst(q, ck), (pg.kind ? Fp : Dp) + pg.doff, kfin[pg.a], pg.ldd, kfin[pg.a], kfin[pg.c], 1, 0});
+          }
         // padded transfers (finish_level :464-474)
         for (int P2 = 0; P2 < nlp; ++P2) {
           const int id = firstp + P2;
@@ -1384,25 +1609,35 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           if (k2) cd.push_back({T + k1, dst + kfin[2 * P2], rows, nxt.bsz[P2], k2, kp, 0, 0});
         }
         mark("merge descriptors built");
-        DBuf dcd, dg1, dg2;
+        DBuf dcd, dcz;
         upload(dcd, cd, st);
-        upload(dg1, g1, st);
-        upload(dg2, g2, st);
+        upload(dcz, cz, st);
         ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
-        const int tlm = std::max(bm, nxt.bmax);
-        launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, tlm);
-        launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, tlm);
+        if (!zstaged) {
+          launch_copy(dcz.as<CopyDesc>(), static_cast<int>(cz.size()), st);
+        } else {
+          for (int ck = 0; ck < nchunk; ++ck) {
+            if (chunk_q[ck + 1] == chunk_q[ck]) continue;
+            CK(cudaMemcpyAsync(zdev.p, zhost.as<cplx>() + zoff[chunk_q[ck]], zlen(ck) * 16, cudaMemcpyHostToDevice, st));
+            launch_copy(dcz.as<CopyDesc>() + chunk_q[ck], static_cast<int>(chunk_q[ck + 1] - chunk_q[ck]), st);
+          }
+        }
         ctx->prof.end(st);
-        C->klaunch[PC_MERGE] += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
-        launches += (!cd.empty()) + (!g1.empty()) + (!g2.empty());
+        C->klaunch[PC_MERGE] += (!cd.empty()) + (!cz.empty());
+        launches += (!cd.empty()) + (!cz.empty());
         if (!fexp.empty()) CK(cudaMemcpyAsync(nxt.fex.p, fexp.data(), fexp.size() * 4, cudaMemcpyHostToDevice, st));
-        for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
         CK(cudaGetLastError());
         mark("merge launched");
         CK(cudaStreamSynchronize(st));  // temporaries die here
 
-        if (verbose) std::fprintf(stderr, "[h2g] level %d: merge done at %.3f s\n", l, wall() - tlev);
+        if (verbose) {
+          size_t fr = 0, tot = 0;
+          cudaMemGetInfo(&fr, &tot);
+          std::fprintf(stderr, "[h2g] level %d: merge done at %.3f s; Z %.2f GB%s, next D %.2f GB, next F %.2f GB; device free %.2f of %.2f GB\n", l, wall() - tlev,
+                       (zdev.bytes + zhost.bytes) / 1e9, zstaged ? " (host-staged)" : "", nxt.D.bytes / 1e9, nxt.F.bytes / 1e9, fr / 1e9, tot / 1e9);
+          std::fprintf(stderr, "[h2g] chains offloaded to host so far: %.2f GB\n", offloaded / 1e9);
+        }
         tlev = wall();
         C->levels.push_back(std::move(CL));
         cur = std::move(nxt);
@@ -1736,10 +1971,10 @@ int h2g_chain_record_mats(const h2g_chain* c, int32_t li, int32_t ri, double* q,
     const int t = CL.rec_cluster[ri];
     const int b = CL.bsz[t], e = b - CL.kfin[t];
     cudaStream_t st = c->ctx->stream;
-    const cplx* base = CL.arena.as<cplx>();
-    if (q) CK(cudaMemcpyAsync(q, base + CL.Qt_off[t], (size_t)b * b * 16, cudaMemcpyDeviceToHost, st));
-    if (l11 && e) CK(cudaMemcpyAsync(l11, base + CL.L11_off[t], (size_t)e * e * 16, cudaMemcpyDeviceToHost, st));
-    if (u11 && e) CK(cudaMemcpyAsync(u11, base + CL.U11_off[t], (size_t)e * e * 16, cudaMemcpyDeviceToHost, st));
+    const cplx* base = CL.chain_ptr();
+    if (q) CK(cudaMemcpyAsync(q, base + CL.Qt_off[t], (size_t)b * b * 16, cudaMemcpyDefault, st));
+    if (l11 && e) CK(cudaMemcpyAsync(l11, base + CL.L11_off[t], (size_t)e * e * 16, cudaMemcpyDefault, st));
+    if (u11 && e) CK(cudaMemcpyAsync(u11, base + CL.U11_off[t], (size_t)e * e * 16, cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
   });
 }
@@ -1770,32 +2005,32 @@ int h2g_chain_record_blocks(const h2g_chain* c, int32_t li, int32_t ri, int64_t*
     const int kf = CL.kfin[t], e = CL.bsz[t] - kf;
     if (e == 0) return;
     cudaStream_t st = c->ctx->stream;
-    const cplx* base = CL.arena.as<cplx>();
+    const cplx* base = CL.chain_ptr();
     size_t q = 0, off = 0;
     for (int a = CL.R_ptr[t]; a < CL.R_ptr[t + 1]; ++a, ++q) {
       const int j = CL.R_nb[a];
       lpos[q] = CL.pos[j];
       lrows[q] = CL.bsz[j];
-      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lbar_off[a], (size_t)CL.bsz[j] * e * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lbar_off[a], (size_t)CL.bsz[j] * e * 16, cudaMemcpyDefault, st));
       off += (size_t)CL.bsz[j] * e;
     }
     if (kf > 0) {
       lpos[q] = CL.pos[t] + e;
       lrows[q] = kf;
-      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lself_off[t], (size_t)kf * e * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ldata + 2 * off, base + CL.Lself_off[t], (size_t)kf * e * 16, cudaMemcpyDefault, st));
     }
     q = 0, off = 0;
     for (int a = CL.C_ptr[t]; a < CL.C_ptr[t + 1]; ++a, ++q) {
       const int cc = CL.C_nb[a];
       upos[q] = CL.pos[cc];
       ucols[q] = CL.bsz[cc];
-      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Ubar_off[a], (size_t)CL.bsz[cc] * e * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Ubar_off[a], (size_t)CL.bsz[cc] * e * 16, cudaMemcpyDefault, st));
       off += (size_t)CL.bsz[cc] * e;
     }
     if (kf > 0) {
       upos[q] = CL.pos[t] + e;
       ucols[q] = kf;
-      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Uself_off[t], (size_t)kf * e * 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(udata + 2 * off, base + CL.Uself_off[t], (size_t)kf * e * 16, cudaMemcpyDefault, st));
     }
     CK(cudaStreamSynchronize(st));
   });
@@ -1830,8 +2065,8 @@ uint64_t h2g_chain_hash(const h2g_chain* c) {
   for (const auto& CL : c->levels) {
     mix(CL->src.data(), CL->src.size() * 8);
     mix(CL->rec.data(), CL->rec.size() * 8);
-    std::vector<char> buf(CL->arena.bytes);
-    if (cudaMemcpyAsync(buf.data(), CL->arena.p, buf.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess) return 0;
+    std::vector<char> buf(CL->chain_bytes());
+    if (cudaMemcpyAsync(buf.data(), CL->chain_ptr(), buf.size(), cudaMemcpyDefault, st) != cudaSuccess) return 0;
     cudaStreamSynchronize(st);
     // hash only the live parts of every record
     for (int t : CL->rec_cluster) {

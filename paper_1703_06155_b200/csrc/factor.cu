@@ -1040,7 +1040,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     int arows, bcols, ro, co;
     if (cb.r >= 0) {
       arows = L.bsz[L.R_nb[cb.r]];
-      A = ((cb.flags & 1) ? L.lift : L.chain) + L.Lbar_off[cb.r];
+      A = (cb.flags & 1) ? L.lift + L.liftL_off[cb.r] : L.chain + L.Lbar_off[cb.r];
       ro = 0;
     } else {
       arows = kf;
@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     }
     if (cb.c >= 0) {
       bcols = L.bsz[L.C_nb[cb.c]];
-      B = ((cb.flags & 2) ? L.lift : L.chain) + L.Ubar_off[cb.c];
+      B = (cb.flags & 2) ? L.lift + L.liftU_off[cb.c] : L.chain + L.Ubar_off[cb.c];
       co = 0;
     } else {
       bcols = kf;

@@ -51,7 +51,9 @@ struct DevLevel {
   const long long* Lself_off;
   const long long* Uself_off;
   // scratch
-  cplx* lift;                 // lifted panels, same offsets as Lbar/Ubar (pool base)
+  cplx* lift;                 // lifted panels (packed: only entries whose neighbour was eliminated earlier)
+  const long long* liftL_off; // per R entry, offset into lift (-1: not lifted)
+  const long long* liftU_off; // per C entry
   const long long* Linv_off;  // L11^{-1}, U11^{-1} (e x e) in the chain
   const long long* Uinv_off;
   // step-0 per batch-slot data (indexed by the slot's global position p in
