@@ -567,16 +567,21 @@ __device__ __forceinline__ void sturm_count_p(int n, const double* d, const doub
 // out[j], by multisection: G lanes of one warp per eigenvalue, 4 shifts per
 // lane, so every round shrinks the bracket (4G+1)-fold; stops at a relative
 // width of 1e-13 like bisect_eig. Whole CTA; no block barriers inside.
-__device__ inline void multisect_top(int n, const double* d, const double* e2, int r, double lo0, double hi0, double pivmin, double* out) {
+// part / nparts: this CTA computes the eigenvalues j = part, part + nparts, ...
+// (the CTAs of a cluster share the work).
+__device__ inline void multisect_top(int n, const double* d, const double* e2, int r, double lo0, double hi0, double pivmin, double* out,
+                                     int part = 0, int nparts = 1) {
   constexpr int P = 4;
+  const int cnt = r > part ? (r - part + nparts - 1) / nparts : 0;
   int G = 32;
-  while (G > 1 && G * r > (int)blockDim.x) G >>= 1;
+  while (G > 1 && G * cnt > (int)blockDim.x) G >>= 1;
   const int slots = blockDim.x / G;
   const int glane = (threadIdx.x & 31) % G, gid = threadIdx.x / G;
   const int npts = G * P;
-  for (int j0 = 0; j0 < r; j0 += slots) {
-    const int j = j0 + gid;
-    const bool act = j < r;
+  for (int j0 = 0; j0 < cnt; j0 += slots) {
+    const int jl = j0 + gid;
+    const bool act = jl < cnt;
+    const int j = part + nparts * jl;
     const int J = n - 1 - j;
     double lo = lo0, hi = hi0;
     bool done = !act;

@@ -132,9 +132,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   cplx* Hl = reinterpret_cast<cplx*>(smraw);  // m x ncl local columns (col c = rank + kHC * jl)
   cplx* vbuf = Hl + (size_t)m * ncl;          // [2][m] reflector broadcast (owner)
   cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v over own columns
-  cplx* wfull = pbuf + 2 * m;                 // [2][m] reduced tau A v (written by the slice owners)
+  cplx* wfull = pbuf + 2 * m;                 // [2][m] reduced tau A v (each CTA its own copy)
   cplx* vv = wfull + 2 * m;                   // local copy of v
-  __shared__ cplx s_dots[2][kHCmax];          // per-slice partials of v^H w
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   {
@@ -175,14 +174,10 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   if (L.debug & 8) tm1 = gtimer();
   // remote views of every CTA's partial / result buffers
   const cplx* rp[kHCmax];
-  cplx* rw[kHCmax];
-  cplx* rd[kHCmax];
 #pragma unroll
   for (int rr = 0; rr < kHCmax; ++rr) {
     const int r2 = rr < kHC ? rr : 0;
     rp[rr] = cl.map_shared_rank(pbuf, r2);
-    rw[rr] = cl.map_shared_rank(wfull, r2);
-    rd[rr] = cl.map_shared_rank(&s_dots[0][0], r2);
   }
   cl.sync();
   if (kHC == 1 && m <= 64) {
@@ -262,9 +257,9 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     }
     __syncthreads();
   } else {
-  // Per column: S1 (reflector published), S2 (partials A v ready), S3 (reduced
-  // w and the v^H w partials delivered): slice rank of the rows is reduced by
-  // CTA rank (warp 0) and pushed to every CTA, so each partial is read once.
+  // Per column two cluster barriers: S1 (reflector published by the column's
+  // owner), S2 (partials A v over each CTA's columns ready); then every CTA
+  // reduces w and v^H w from the partials itself and updates its columns.
   for (int kk = 0; kk + 1 < m; ++kk) {
     const int owner = kk % kHC, buf = kk & 1;
     const int nk = m - kk - 1;
@@ -322,10 +317,13 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
       }
     }
     cl.sync();  // S2: partials ready
-    // slice rank: w_i = tau * sum_r p_r[i], pushed to every CTA; v^H w partial
-    if (threadIdx.x < 32) {
+    // every CTA reduces the full w = tau * sum_r p_r (rank order) from the
+    // partials in distributed shared memory and forms v^H w itself: one
+    // cluster barrier less per column than pushing reduced slices around
+    cplx* wb = wfull + (size_t)buf * m;
+    {
       double dr = 0.0, di = 0.0;
-      for (int i = rank + kHC * (int)threadIdx.x; i < nk; i += 32 * kHC) {
+      for (int i = threadIdx.x; i < nk; i += blockDim.x) {
         cplx parts[kHCmax];
 #pragma unroll
         for (int rr = 0; rr < kHCmax; ++rr)
@@ -335,9 +333,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         for (int rr = 0; rr < kHCmax; ++rr)
           if (rr < kHC) sacc = cadd(sacc, parts[rr]);
         sacc = cmul(tk, sacc);
-#pragma unroll
-        for (int rr = 0; rr < kHCmax; ++rr)
-          if (rr < kHC) rw[rr][(size_t)buf * m + i] = sacc;
+        wb[i] = sacc;
         const cplx tt = cmul(cconj(vv[i]), sacc);
         dr += tt.x;
         di += tt.y;
@@ -346,16 +342,14 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         dr += __shfl_xor_sync(0xffffffffu, dr, o);
         di += __shfl_xor_sync(0xffffffffu, di, o);
       }
-      if (threadIdx.x < kHC) rd[threadIdx.x][buf * kHCmax + rank] = cmk(dr, di);
-    }
-    cl.sync();  // S3: w and the v^H w partials delivered
-    // c = v^H w; w = w - 1/2 conj(tau) c v
-    cplx cdot = czero();
-    for (int rr = 0; rr < kHC; ++rr) cdot = cadd(cdot, s_dots[buf][rr]);
-    const cplx hc = cscale(cmul(cconj(tk), cdot), 0.5);
-    const cplx* wb = wfull + (size_t)buf * m;
-    // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
-    {
+      const int wi = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+      if ((threadIdx.x & 31) == 0) red[wi] = dr, red[16 + wi] = di;
+      __syncthreads();
+      dr = 0.0, di = 0.0;
+      for (int u = 0; u < nw; ++u) dr += red[u], di += red[16 + u];
+      // c = v^H w; w = w - 1/2 conj(tau) c v
+      const cplx hc = cscale(cmul(cconj(tk), cmk(dr, di)), 0.5);
+      // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
       const int jl0 = max((kk + 1 - rank + kHC - 1) / kHC, 0);
       const int ncols = ncl - jl0;
       for (int idx = threadIdx.x; idx < nk * ncols; idx += blockDim.x) {
@@ -363,11 +357,11 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         const int c = rank + kHC * jl;
         if (c >= m) continue;
         const int jc = c - kk - 1;
-        const cplx wi = csub(wb[i], cmul(hc, vv[i])), wc = csub(wb[jc], cmul(hc, vv[jc]));
+        const cplx wi2 = csub(wb[i], cmul(hc, vv[i])), wc = csub(wb[jc], cmul(hc, vv[jc]));
         cplx* a = Hl + (kk + 1 + i) + (size_t)jl * m;
         cplx av = *a;
         av = csub(av, cmul(vv[i], cconj(wc)));
-        av = csub(av, cmul(wi, cconj(vv[jc])));
+        av = csub(av, cmul(wi2, cconj(vv[jc])));
         *a = av;
       }
     }
@@ -385,8 +379,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     if (c < m) H[i + (size_t)c * m] = Hl[idx];
   }
   cl.sync();
-  if (rank != 0) return;
-  // ---- CTA 0: spectrum edge, rank, retained eigenvalues
+  // ---- every CTA (redundantly, identical results): spectrum edge and rank;
+  // the retained eigenvalues are split over the CTAs of the cluster
   __shared__ double s_lo, s_hi, s_piv, s_s0, s_thr;
   __shared__ int s_r, s_need;
   double cm = 0.0;
@@ -460,7 +454,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   __syncthreads();
   const int r = s_r;
   if (L.debug & 8) tm3 = gtimer();
-  if (!s_need) multisect_top(m, dg, e2, r, s_lo, s_hi, s_piv, aux + 2 * bm);
+  if (!s_need) multisect_top(m, dg, e2, r, s_lo, s_hi, s_piv, aux + 2 * bm, rank, kHC);
+  if (rank != 0) return;
   if ((L.debug & 8) && threadIdx.x == 0)
     printf("[h2g] eig1c-timing level %d cl %d kHC %d m %d r %d: gram %.1f us tridiag %.1f us lmax+rank %.1f us multisect %.1f us\n", L.level, t, kHC, m, r,
            (tm1 - tm0) * 1e-3, (tm2 - tm1) * 1e-3, (tm3 - tm2) * 1e-3, (gtimer() - tm3) * 1e-3);
@@ -1007,11 +1002,12 @@ __global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch
 // every cluster of the batch that hits it are summed in a fixed order, then
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
 // 4 x 4 complex micro-tile per thread, K staged through shared memory.
+template <int TM>
 __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+  constexpr int RM = TM / 8, RN = TM / 16;  // DFMA micro-tile (TM < 64)
   extern __shared__ __align__(16) unsigned char tsm[];
-  Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
+  TileSmem<TM>& S = *reinterpret_cast<TileSmem<TM>*>(tsm);
   const SchurTargetD tg = targets[blockIdx.x];
-  const int bm = L.bmax;
   int rows, cols;
   cplx* out;
   if (tg.kind == 0) {
@@ -1023,11 +1019,19 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     cols = L.bsz[L.fcol[tg.idx]];
     out = L.F + L.F_off[tg.idx];
   }
-  const int ntr = (rows + 63) / 64, ntc = (cols + 63) / 64;
+  const int ntr = (rows + TM - 1) / TM, ntc = (cols + TM - 1) / TM;
   if ((int)blockIdx.y >= ntr * ntc) return;
-  const int r0 = (blockIdx.y % ntr) * 64, c0 = (blockIdx.y / ntr) * 64;
+  const int r0 = (blockIdx.y % ntr) * TM, c0 = (blockIdx.y / ntr) * TM;
   Acc64 acc;
-  acc64_zero(acc);
+  cplx accs[TM == 64 ? 1 : RM][TM == 64 ? 1 : RN];
+  if constexpr (TM == 64) {
+    acc64_zero(acc);
+  } else {
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+#pragma unroll
+      for (int b = 0; b < RN; ++b) accs[a][b] = czero();
+  }
   bool touched = false;
   for (int ci = tg.c0; ci < tg.c1; ++ci) {
     const SchurContribD cb = contrib[ci];
@@ -1058,16 +1062,34 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     }
     // the contribution covers target rows [ro, ro+arows) x cols [co, co+bcols)
     const int ash = r0 - ro, bsh = c0 - co;
-    if (ash >= arows || bsh >= bcols || ash + 64 <= 0 || bsh + 64 <= 0) continue;
-    tile_acc_dmma(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
+    if (ash >= arows || bsh >= bcols || ash + TM <= 0 || bsh + TM <= 0) continue;
+    if constexpr (TM == 64)
+      tile_acc_dmma(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
+    else
+      tile_acc<TM>(accs, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
   }
-  acc64_each(acc, [&](int ii, int jj, cplx v) {
-    const int i = r0 + ii, j = c0 + jj;
-    if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
-      cplx* o = out + i + (size_t)j * rows;
-      *o = csub(*o, v);
-    }
-  });
+  if constexpr (TM == 64) {
+    acc64_each(acc, [&](int ii, int jj, cplx v) {
+      const int i = r0 + ii, j = c0 + jj;
+      if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
+        cplx* o = out + i + (size_t)j * rows;
+        *o = csub(*o, v);
+      }
+    });
+  } else {
+    const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+#pragma unroll
+      for (int b = 0; b < RN; ++b) {
+        const int i = r0 + tr + 8 * a, j = c0 + tc * RN + b;
+        const cplx v = accs[a][b];
+        if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
+          cplx* o = out + i + (size_t)j * rows;
+          *o = csub(*o, v);
+        }
+      }
+  }
   if (tg.kind == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
 }
 
@@ -1442,9 +1464,17 @@ void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
 
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;
+  if (L.bmax <= 32) {
+    // small blocks (leaf levels, e of a few columns): 32 x 32 DFMA tiles, the
+    // target read-modify-write dominates and a 64 x 64 tensor tile would be 3/4 padding
+    set_smem((const void*)k_schur<32>, sizeof(TileSmem<32>));
+    k_schur<32><<<dim3(ntargets, 1), 128, sizeof(TileSmem<32>), s>>>(L, targets, contrib);
+    post_launch("k_schur");
+    return;
+  }
   const int t = (L.bmax + 63) / 64;
-  set_smem((const void*)k_schur, sizeof(Tile128Smem));
-  k_schur<<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
+  set_smem((const void*)k_schur<64>, sizeof(Tile128Smem));
+  k_schur<64><<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
   post_launch("k_schur");
 }
 
