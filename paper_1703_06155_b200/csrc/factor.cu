@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   cplx* vbuf = Hl + (size_t)m * ncl;          // [2][m] reflector broadcast (owner)
   cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v over own columns
   cplx* wfull = pbuf + 2 * m;                 // [2][m] reduced tau A v (each CTA its own copy)
-  cplx* vv = wfull + 2 * m;                   // local copy of v
+  cplx* vv = wfull + 2 * m;                   // local copy of v (+ [m] next v, cluster path)
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   {
@@ -257,51 +257,71 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     }
     __syncthreads();
   } else {
-  // Per column two cluster barriers: S1 (reflector published by the column's
-  // owner), S2 (partials A v over each CTA's columns ready); then every CTA
-  // reduces w and v^H w from the partials itself and updates its columns.
-  for (int kk = 0; kk + 1 < m; ++kk) {
-    const int owner = kk % kHC, buf = kk & 1;
+  // One cluster barrier per column. Every CTA keeps the current reflector v
+  // (and tau) itself: after the barrier that delivers the partials A v of
+  // column kk, each CTA reduces w and v^H w, takes column kk+1 as its owner
+  // published it before the barrier (pre-update copy), applies the rank-2
+  // update of column kk to it and forms reflector kk+1 redundantly; the
+  // owner also keeps it in its columns (the reflector output).
+  cplx* pub = vbuf;            // [2][m] published next column (owner), rows kk+1..
+  cplx* wb = wfull;            // [m] w (local)
+  cplx* colb = wfull + m;      // [m] next column after the update (local)
+  cplx* vn = vv + m;           // [m] next reflector (local)
+  __shared__ cplx s_tl, s_sc;
+  __shared__ double s_bt;
+  __shared__ int s_sk;
+  // reflector of column kk from col[0 .. m-kk-1] = A[kk.., kk] (updated);
+  // writes vn, s_tl, s_sk (aux from rank 0)
+  auto reflector = [&](int kk, const cplx* col) {
     const int nk = m - kk - 1;
-    if (rank == owner) {
-      cplx* x = Hl + (kk + 1) + (size_t)(kk / kHC) * m;
-      double part = 0.0;
-      for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) part += cabs2(x[i]);
-      const double xn2 = cta_sum(part, red);
-      __shared__ cplx s_scale;
-      __shared__ double s_beta;
-      if (threadIdx.x == 0) {
-        const cplx al = x[0];
-        if (xn2 == 0.0 && al.y == 0.0) {
-          s_skip[buf] = 1;
-          s_tau[buf] = czero();
-          s_beta = al.x;
-        } else {
-          double beta = sqrt(cabs2(al) + xn2);
-          if (al.x >= 0.0) beta = -beta;
-          s_skip[buf] = 0;
-          s_beta = beta;
-          s_tau[buf] = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
-          s_scale = cdiv(cone(), csub(al, cmk(beta, 0.0)));
-        }
-        aux[kk] = Hl[kk + (size_t)(kk / kHC) * m].x;  // d_k
-        aux[bm + kk] = s_beta;                         // e_k
-        reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = s_tau[buf];
+    double part = 0.0;
+    for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) part += cabs2(col[1 + i]);
+    const double xn2 = cta_sum(part, red);
+    if (threadIdx.x == 0) {
+      const cplx al = col[1];
+      if (xn2 == 0.0 && al.y == 0.0) {
+        s_sk = 1;
+        s_tl = czero();
+        s_bt = al.x;
+      } else {
+        double beta = sqrt(cabs2(al) + xn2);
+        if (al.x >= 0.0) beta = -beta;
+        s_sk = 0;
+        s_bt = beta;
+        s_tl = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
+        s_sc = cdiv(cone(), csub(al, cmk(beta, 0.0)));
       }
-      __syncthreads();
-      if (!s_skip[buf])
-        for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) x[i] = cmul(x[i], s_scale);
-      __syncthreads();
-      cplx* vb = vbuf + (size_t)buf * m;
-      for (int i = threadIdx.x; i < nk; i += blockDim.x) vb[i] = i == 0 ? cone() : x[i];
+      if (rank == 0) {
+        aux[kk] = col[0].x;  // d_k
+        aux[bm + kk] = s_bt; // e_k
+        reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = s_tl;
+      }
     }
-    cl.sync();  // S1: reflector published
-    const int* oskip = cl.map_shared_rank(s_skip, owner);
-    if (oskip[buf]) continue;  // uniform: every CTA reads the same flag
-    const cplx tk = cl.map_shared_rank(s_tau, owner)[buf];
-    const cplx* ovb = cl.map_shared_rank(vbuf, owner) + (size_t)buf * m;
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) vv[i] = ovb[i];
     __syncthreads();
+    // skipped columns (tau = 0) use v = e_1: the update then subtracts zeros
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) vn[i] = i == 0 ? cone() : (s_sk ? czero() : cmul(col[1 + i], s_sc));
+  };
+  if (m > 1) {
+    // column 0 lives in CTA 0 (Gram reduced and the cluster synchronised above)
+    const cplx* c0 = cl.map_shared_rank(Hl, 0);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) colb[i] = c0[i];
+    __syncthreads();
+    reflector(0, colb);
+    __syncthreads();
+  }
+  for (int kk = 0; kk + 1 < m; ++kk) {
+    const int buf = kk & 1;
+    const int nk = m - kk - 1;
+    // current reflector
+    const cplx tk = s_tl;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) vv[i] = vn[i];
+    __syncthreads();
+    // publish column kk+1 (rows kk+1..) before its update by column kk
+    const int own1 = (kk + 1) % kHC;
+    if (kk + 2 < m && rank == own1) {
+      const cplx* src = Hl + (kk + 1) + (size_t)((kk + 1) / kHC) * m;
+      for (int i = threadIdx.x; i < nk; i += blockDim.x) pub[(size_t)buf * m + i] = src[i];
+    }
     // partial p over own columns c > kk (local rows kk+1 .. m-1)
     cplx* pb = pbuf + (size_t)buf * m;
     {
@@ -316,40 +336,59 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         pb[i] = sacc;
       }
     }
-    cl.sync();  // S2: partials ready
-    // every CTA reduces the full w = tau * sum_r p_r (rank order) from the
-    // partials in distributed shared memory and forms v^H w itself: one
-    // cluster barrier less per column than pushing reduced slices around
-    cplx* wb = wfull + (size_t)buf * m;
+    cl.sync();  // partials of column kk and the published column kk+1 ready
+    // the owner stores reflector kk below the subdiagonal of its column kk
+    // (nobody reads that column any more; earlier, other CTAs may still have
+    // been copying it)
+    if (rank == kk % kHC) {
+      cplx* x = Hl + (kk + 1) + (size_t)(kk / kHC) * m;
+      for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) x[i] = vv[i];
+    }
+    // w = tau * sum_r p_r (rank order), c = v^H w
+    double dr = 0.0, di = 0.0;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      cplx parts[kHCmax];
+#pragma unroll
+      for (int rr = 0; rr < kHCmax; ++rr)
+        if (rr < kHC) parts[rr] = rp[rr][(size_t)buf * m + i];
+      cplx sacc = czero();
+#pragma unroll
+      for (int rr = 0; rr < kHCmax; ++rr)
+        if (rr < kHC) sacc = cadd(sacc, parts[rr]);
+      sacc = cmul(tk, sacc);
+      wb[i] = sacc;
+      const cplx tt = cmul(cconj(vv[i]), sacc);
+      dr += tt.x;
+      di += tt.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      dr += __shfl_xor_sync(0xffffffffu, dr, o);
+      di += __shfl_xor_sync(0xffffffffu, di, o);
+    }
     {
-      double dr = 0.0, di = 0.0;
-      for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-        cplx parts[kHCmax];
-#pragma unroll
-        for (int rr = 0; rr < kHCmax; ++rr)
-          if (rr < kHC) parts[rr] = rp[rr][(size_t)buf * m + i];
-        cplx sacc = czero();
-#pragma unroll
-        for (int rr = 0; rr < kHCmax; ++rr)
-          if (rr < kHC) sacc = cadd(sacc, parts[rr]);
-        sacc = cmul(tk, sacc);
-        wb[i] = sacc;
-        const cplx tt = cmul(cconj(vv[i]), sacc);
-        dr += tt.x;
-        di += tt.y;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        dr += __shfl_xor_sync(0xffffffffu, dr, o);
-        di += __shfl_xor_sync(0xffffffffu, di, o);
-      }
       const int wi = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
       if ((threadIdx.x & 31) == 0) red[wi] = dr, red[16 + wi] = di;
       __syncthreads();
       dr = 0.0, di = 0.0;
       for (int u = 0; u < nw; ++u) dr += red[u], di += red[16 + u];
-      // c = v^H w; w = w - 1/2 conj(tau) c v
-      const cplx hc = cscale(cmul(cconj(tk), cmk(dr, di)), 0.5);
-      // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
+    }
+    // w = w - 1/2 conj(tau) c v
+    const cplx hc = cscale(cmul(cconj(tk), cmk(dr, di)), 0.5);
+    // next column: the published copy with this column's update (same
+    // expression as the owner's own update below, so the copies agree)
+    if (kk + 2 < m) {
+      const cplx* pc = cl.map_shared_rank(pub, own1) + (size_t)buf * m;
+      const cplx wc = csub(wb[0], cmul(hc, vv[0]));
+      for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+        const cplx wi2 = csub(wb[i], cmul(hc, vv[i]));
+        cplx av = pc[i];
+        av = csub(av, cmul(vv[i], cconj(wc)));
+        av = csub(av, cmul(wi2, cconj(vv[0])));
+        colb[i] = av;
+      }
+    }
+    // rank-2 update of own columns c > kk: A[i, c] -= v_i conj(w_c) + w_i conj(v_c)
+    {
       const int jl0 = max((kk + 1 - rank + kHC - 1) / kHC, 0);
       const int ncols = ncl - jl0;
       for (int idx = threadIdx.x; idx < nk * ncols; idx += blockDim.x) {
@@ -365,6 +404,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
         *a = av;
       }
     }
+    __syncthreads();
+    if (kk + 2 < m) reflector(kk + 1, colb);
     __syncthreads();
   }
   }  // cluster path
