@@ -571,13 +571,14 @@ __global__ void __launch_bounds__(256) k_eig1_refine(DevLevel L, const int* batc
 // work arrays in shared memory; eigenvalues closer than 1e-8 ||T|| form a
 // cluster handled by one CTA and Gram-Schmidt'ed against each other), then
 // the back-transformation by the tridiagonalisation reflectors (whole CTA).
-__global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl, cplx* gws) {
+__global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl, cplx* gws, int wpc) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ double red[32];
-  const int q = blockIdx.x, j = blockIdx.y;
+  const int q = blockIdx.x;
   if (L.pass2[q]) return;
   const int r = L.rank1[q];
-  if (j >= r) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.y * wpc + warp;  // one warp per retained eigenvector
+  if ((int)blockIdx.y * wpc >= r) return;  // uniform over the CTA
   const int t = batch_cl[q];
   const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
   const size_t bb = (size_t)bm * bm;
@@ -585,24 +586,55 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
   const cplx* H = ws;
   cplx* U = ws + bb;
   const double* aux = reinterpret_cast<const double*>(ws + 2 * bb);
-  const double* gd = aux;
-  const double* ge = aux + bm;
   const double* glam = aux + 2 * bm;
   const cplx* tau = reinterpret_cast<const cplx*>(aux + 4 * bm);
   double* dg = reinterpret_cast<double*>(smraw);
   double* ed = dg + m;
-  double* wk = ed + m;  // 4m
-  double* z = wk + 4 * m;
-  cplx* y = reinterpret_cast<cplx*>(z + m + (m & 1));
-  for (int i = threadIdx.x; i < m; i += blockDim.x) dg[i] = gd[i], ed[i] = ge[i];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) dg[i] = aux[i], ed[i] = aux[bm + i];
   __syncthreads();
-  // inverse iteration from a per-eigenvalue pseudo-random start: (near-)
-  // degenerate eigenvalues get independent vectors of their invariant
-  // subspace; k_eig1b orthonormalises the retained set as a whole
-  if (threadIdx.x == 0) {
+  if (j >= r || warp >= wpc) return;
+  // per-warp work arrays: U factor (dd, du, du2, 1/dd), multipliers, pivots, z
+  double* wk = ed + m + (size_t)warp * 7 * m;
+  double* dd = wk;
+  double* du = wk + m;
+  double* du2 = wk + 2 * m;
+  double* rdd = wk + 3 * m;
+  double* fl = wk + 4 * m;
+  double* z = wk + 5 * m;
+  unsigned char* pv = reinterpret_cast<unsigned char*>(wk + 6 * m);
+  if (lane == 0) {
+    // inverse iteration from a per-eigenvalue pseudo-random start: (near-)
+    // degenerate eigenvalues get independent vectors of their invariant
+    // subspace; k_eig1b orthonormalises the retained set as a whole.
+    // T - lam I = P L U is factored once (partial pivoting, tiny pivots
+    // replaced as in tri_shift_solve) and reused for the three solves.
     double emax = 0.0;
     for (int i = 0; i + 1 < m; ++i) emax = fmax(emax, ed[i] * ed[i]);
-    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax);
+    const double tiny = 2.2250738585072014e-308 * fmax(1.0, emax) * 1e10 + 1e-300;
+    const double lam = glam[j];
+    double dcur = dg[0] - lam;  // dd[i] while eliminating row i+1
+    double dnext_e = m > 1 ? ed[0] : 0.0;  // du[i] (may be modified by a swap)
+    for (int i = 0; i + 1 < m; ++i) {
+      const double sub = ed[i];                     // dl[i]
+      const double dn = dg[i + 1] - lam;            // dd[i+1] before elimination
+      const double un = i + 2 < m ? ed[i + 1] : 0.0; // du[i+1]
+      if (fabs(dcur) >= fabs(sub)) {
+        if (fabs(dcur) < tiny) dcur = dcur >= 0 ? tiny : -tiny;
+        const double f = sub / dcur;
+        dd[i] = dcur, du[i] = dnext_e, du2[i] = 0.0, fl[i] = f, pv[i] = 0;
+        dcur = dn - f * dnext_e;
+        dnext_e = un;
+      } else {
+        const double f = dcur / sub;
+        dd[i] = sub, du[i] = dn, du2[i] = un, fl[i] = f, pv[i] = 1;
+        dcur = dnext_e - f * dn;
+        dnext_e = -f * un;
+      }
+      rdd[i] = 1.0 / dd[i];
+    }
+    if (fabs(dcur) < tiny) dcur = dcur >= 0 ? tiny : -tiny;
+    dd[m - 1] = dcur;
+    rdd[m - 1] = 1.0 / dcur;
     for (int i = 0; i < m; ++i) {
       unsigned h = (unsigned)(i * 2654435761u) ^ (unsigned)((j + 1) * 40503u);
       h ^= h >> 13;
@@ -611,36 +643,76 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
       z[i] = 1.0 + 0.5 * ((double)(h & 0xffff) / 65535.0 - 0.5);
     }
     for (int it = 0; it < 3; ++it) {
-      tri_shift_solve(m, dg, ed, glam[j], z, wk, pivmin * 1e10 + 1e-300);
-      double nrm = 0.0;
-      for (int i = 0; i < m; ++i) nrm += z[i] * z[i];
+      // forward: the row operations of the factorization
+      double zi = z[0];
+      for (int i = 0; i + 1 < m; ++i) {
+        const double zn = z[i + 1];
+        if (!pv[i]) {
+          z[i] = zi;
+          zi = zn - fl[i] * zi;
+        } else {
+          z[i] = zn;
+          zi = zi - fl[i] * zn;
+        }
+      }
+      z[m - 1] = zi;
+      // back substitution with U (two superdiagonals)
+      double z1 = z[m - 1] * rdd[m - 1], z2 = 0.0;
+      z[m - 1] = z1;
+      double nrm = z1 * z1;
+      for (int i = m - 2; i >= 0; --i) {
+        const double zi2 = (z[i] - du[i] * z1 - du2[i] * z2) * rdd[i];
+        z[i] = zi2;
+        z2 = z1, z1 = zi2;
+        nrm += zi2 * zi2;
+      }
       const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
       for (int i = 0; i < m; ++i) z[i] *= inv;
     }
   }
-  __syncthreads();
-  // back-transform y = Q z, Q = H_0 ... H_{m-2}
-  for (int i = threadIdx.x; i < m; i += blockDim.x) y[i] = cmk(z[i], 0.0);
-  __syncthreads();
+  __syncwarp();
+  // back-transform y = Q z, Q = H_0 ... H_{m-2}: the warp streams through the
+  // reflectors (lane owns entries lane, lane + 32, ...), no block barriers
+  constexpr int kPer = 16;  // m <= 512
+  cplx y[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = lane + 32 * u;
+    y[u] = i < m ? cmk(z[i], 0.0) : czero();
+  }
   for (int kk = m - 2; kk >= 0; --kk) {
     const cplx tk = tau[kk];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
-    const cplx* v = H + (kk + 1) + (size_t)kk * m;  // v[0] = 1
-    const int nk = m - kk - 1;
+    const cplx* v = H + (kk + 1) + (size_t)kk * m;  // rows kk+1.., v[0] = 1
     double sr = 0.0, si = 0.0;
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-      const cplx vv = i == 0 ? cone() : cconj(v[i]);
-      const cplx yy = y[kk + 1 + i];
-      sr += vv.x * yy.x - vv.y * yy.y;
-      si += vv.x * yy.y + vv.y * yy.x;
+    cplx vr[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = lane + 32 * u;  // global row
+      vr[u] = czero();
+      if (i > kk && i < m) {
+        vr[u] = i == kk + 1 ? cone() : __ldg(v + (i - kk - 1));
+        const cplx vc = cconj(vr[u]);
+        sr += vc.x * y[u].x - vc.y * y[u].y;
+        si += vc.x * y[u].y + vc.y * y[u].x;
+      }
     }
-    sr = cta_sum(sr, red);
-    si = cta_sum(si, red);
+    for (int o = 16; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
     const cplx sc = cmul(tk, cmk(sr, si));
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) y[kk + 1 + i] = csub(y[kk + 1 + i], cmul(i == 0 ? cone() : v[i], sc));
-    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = lane + 32 * u;
+      if (i > kk && i < m) y[u] = csub(y[u], cmul(vr[u], sc));
+    }
   }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) U[i + (size_t)m * j] = y[i];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = lane + 32 * u;
+    if (i < m) U[i + (size_t)m * j] = y[u];
+  }
 }
 
 // D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H from a Householder QR of the
@@ -1438,9 +1510,13 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   }
   phase(1);
   if (mmax > 0) {
-    const size_t vsm = (size_t)8 * L.bmax * sizeof(double) + 16 + (size_t)L.bmax * sizeof(cplx);
+    if (mmax > 512) throw std::runtime_error("k_eigvec: complement dimension > 512");
+    // one warp per eigenvector; shared: d, e (2 bmax) + 7 bmax doubles per warp
+    int wpc = 8;
+    while (wpc > 1 && (size_t)(2 + 7 * wpc) * L.bmax * sizeof(double) > kSmemCap) --wpc;
+    const size_t vsm = (size_t)(2 + 7 * wpc) * L.bmax * sizeof(double) + 64;
     set_smem((const void*)k_eigvec, vsm);
-    k_eigvec<<<dim3(nb, mmax), 256, vsm, s>>>(L, batch_cl, ws);
+    k_eigvec<<<dim3(nb, (mmax + wpc - 1) / wpc), 256, vsm, s>>>(L, batch_cl, ws, wpc);
     post_launch("k_eigvec");
   }
   phase(2);
