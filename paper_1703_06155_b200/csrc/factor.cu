@@ -592,9 +592,12 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
   double* ed = dg + m;
   for (int i = threadIdx.x; i < m; i += blockDim.x) dg[i] = aux[i], ed[i] = aux[bm + i];
   __syncthreads();
-  if (j >= r || warp >= wpc) return;
+  // every warp stays for the staged back-transformation below; idle ones
+  // (j >= r or beyond wpc) only help staging
+  const bool act = j < r && warp < wpc;
+  const unsigned long long tv0 = (L.debug & 8) ? gtimer() : 0ull;
   // per-warp work arrays: U factor (dd, du, du2, 1/dd), multipliers, pivots, z
-  double* wk = ed + m + (size_t)warp * 7 * m;
+  double* wk = ed + m + (size_t)min(warp, wpc - 1) * 7 * m;
   double* dd = wk;
   double* du = wk + m;
   double* du2 = wk + 2 * m;
@@ -602,7 +605,7 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
   double* fl = wk + 4 * m;
   double* z = wk + 5 * m;
   unsigned char* pv = reinterpret_cast<unsigned char*>(wk + 6 * m);
-  if (lane == 0) {
+  if (act && lane == 0) {
     // inverse iteration from a per-eigenvalue pseudo-random start: (near-)
     // degenerate eigenvalues get independent vectors of their invariant
     // subspace; k_eig1b orthonormalises the retained set as a whole.
@@ -620,17 +623,17 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
       const double un = i + 2 < m ? ed[i + 1] : 0.0; // du[i+1]
       if (fabs(dcur) >= fabs(sub)) {
         if (fabs(dcur) < tiny) dcur = dcur >= 0 ? tiny : -tiny;
-        const double f = sub / dcur;
+        const double f = sub * rcp_nr(dcur);
         dd[i] = dcur, du[i] = dnext_e, du2[i] = 0.0, fl[i] = f, pv[i] = 0;
         dcur = dn - f * dnext_e;
         dnext_e = un;
       } else {
-        const double f = dcur / sub;
+        const double f = dcur * rcp_nr(sub);
         dd[i] = sub, du[i] = dn, du2[i] = un, fl[i] = f, pv[i] = 1;
         dcur = dnext_e - f * dn;
         dnext_e = -f * un;
       }
-      rdd[i] = 1.0 / dd[i];
+      rdd[i] = rcp_nr(dd[i]);
     }
     if (fabs(dcur) < tiny) dcur = dcur >= 0 ? tiny : -tiny;
     dd[m - 1] = dcur;
@@ -671,48 +674,89 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
     }
   }
   __syncwarp();
-  // back-transform y = Q z, Q = H_0 ... H_{m-2}: the warp streams through the
-  // reflectors (lane owns entries lane, lane + 32, ...), no block barriers
+  const unsigned long long tv1 = (L.debug & 8) ? gtimer() : 0ull;
+  // back-transform y = Q z, Q = H_0 ... H_{m-2}: reflectors staged CH at a
+  // time in shared memory by the whole CTA (coalesced), then every warp
+  // streams its vector through them (lane owns entries lane, lane + 32, ...)
   constexpr int kPer = 16;  // m <= 512
+  constexpr int CH = 8;
+  cplx* Hs = reinterpret_cast<cplx*>(dg + (size_t)(2 + 7 * wpc) * m + (((2 + 7 * wpc) * m) & 1));  // [CH][m]
+  __shared__ cplx ts[CH];
   cplx y[kPer];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int i = lane + 32 * u;
-    y[u] = i < m ? cmk(z[i], 0.0) : czero();
+    y[u] = (act && i < m) ? cmk(z[i], 0.0) : czero();
   }
-  for (int kk = m - 2; kk >= 0; --kk) {
-    const cplx tk = tau[kk];
-    if (tk.x == 0.0 && tk.y == 0.0) continue;
-    const cplx* v = H + (kk + 1) + (size_t)kk * m;  // rows kk+1.., v[0] = 1
-    double sr = 0.0, si = 0.0;
-    cplx vr[kPer];
+  for (int k1 = m - 2; k1 >= 0; k1 -= CH) {
+    const int k0 = max(0, k1 - CH + 1);
+    __syncthreads();  // previous chunk consumed
+    {
+      // flattened (column, row) index so each thread has its loads in flight at once
+      const int tot = (k1 - k0 + 1) * m;
+      for (int base = 0; base < tot; base += 8 * (int)blockDim.x) {
+        cplx tmp[8];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int i = lane + 32 * u;  // global row
-      vr[u] = czero();
-      if (i > kk && i < m) {
-        vr[u] = i == kk + 1 ? cone() : __ldg(v + (i - kk - 1));
-        const cplx vc = cconj(vr[u]);
-        sr += vc.x * y[u].x - vc.y * y[u].y;
-        si += vc.x * y[u].y + vc.y * y[u].x;
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * (int)blockDim.x + (int)threadIdx.x;
+          const int c = k0 + idx / m, i = idx % m;
+          tmp[u] = (idx < tot && i > 0 && i < m - c - 1) ? H[(c + 1) + i + (size_t)c * m] : cone();
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + u * (int)blockDim.x + (int)threadIdx.x;
+          if (idx < tot) Hs[idx] = tmp[u];
+        }
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      sr += __shfl_xor_sync(0xffffffffu, sr, o);
-      si += __shfl_xor_sync(0xffffffffu, si, o);
-    }
-    const cplx sc = cmul(tk, cmk(sr, si));
+    if (threadIdx.x <= k1 - k0) ts[threadIdx.x] = tau[k0 + threadIdx.x];
+    __syncthreads();
+    if (!act) continue;
+    for (int kk = k1; kk >= k0; --kk) {
+      const cplx tk = ts[kk - k0];
+      if (tk.x == 0.0 && tk.y == 0.0) continue;
+      const cplx* v = Hs + (size_t)(kk - k0) * m - (kk + 1);  // v[i] for global row i > kk
+      double sr = 0.0, si = 0.0, sr2 = 0.0, si2 = 0.0;
+      const int u0 = ((kk + 1) / 32) & ~1, u1 = (m + 31) / 32;  // warp-uniform live range
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int i = lane + 32 * u;
-      if (i > kk && i < m) y[u] = csub(y[u], cmul(vr[u], sc));
+      for (int u = 0; u < kPer; u += 2) {
+        if (u >= u1) break;
+        if (u + 2 <= u0) continue;
+        const int i = lane + 32 * u, i2 = i + 32;
+        if (i > kk && i < m) {
+          const cplx vc = cconj(v[i]);
+          sr += vc.x * y[u].x - vc.y * y[u].y;
+          si += vc.x * y[u].y + vc.y * y[u].x;
+        }
+        if (i2 > kk && i2 < m) {
+          const cplx vc = cconj(v[i2]);
+          sr2 += vc.x * y[u + 1].x - vc.y * y[u + 1].y;
+          si2 += vc.x * y[u + 1].y + vc.y * y[u + 1].x;
+        }
+      }
+      sr += sr2, si += si2;
+      for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        si += __shfl_xor_sync(0xffffffffu, si, o);
+      }
+      const cplx sc = cmul(tk, cmk(sr, si));
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        if (u >= u1) break;
+        if (u < u0) continue;
+        const int i = lane + 32 * u;
+        if (i > kk && i < m) y[u] = csub(y[u], cmul(v[i], sc));
+      }
     }
   }
+  if (!act) return;
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int i = lane + 32 * u;
     if (i < m) U[i + (size_t)m * j] = y[u];
   }
+  if ((L.debug & 8) && lane == 0 && j == 0)
+    printf("[h2g] eigvec-timing level %d m %d r %d: inverse iteration %.1f us back-transform %.1f us\n", L.level, m, r, (tv1 - tv0) * 1e-3, (gtimer() - tv1) * 1e-3);
 }
 
 // D1 = Vp Qm with Qm = H_0^H ... H_{r-1}^H from a Householder QR of the
@@ -772,11 +816,15 @@ __global__ void __launch_bounds__(256) k_eig1_apply(DevLevel L, const int* batch
     const int c = lane + 32 * u;
     d[u] = c < m ? Vp[row + (size_t)c * b] : czero();
   }
+  const int u1 = (m + 31) / 32;
   for (int j = 0; j < r; ++j) {
     const cplx* y = Y + (size_t)j * m;
     double sr = 0.0, si = 0.0;
+    const int u0 = j / 32;  // warp-uniform live range of the reflector
 #pragma unroll
     for (int u = 0; u < kMaxPer; ++u) {
+      if (u >= u1) break;
+      if (u < u0) continue;
       const int c = lane + 32 * u;
       if (c < m && c >= j) {
         const cplx yv = y[c];
@@ -791,6 +839,8 @@ __global__ void __launch_bounds__(256) k_eig1_apply(DevLevel L, const int* batch
     const cplx f = cmul(cconj(tau_g[j]), cmk(sr, si));
 #pragma unroll
     for (int u = 0; u < kMaxPer; ++u) {
+      if (u >= u1) break;
+      if (u < u0) continue;
       const int c = lane + 32 * u;
       if (c < m && c >= j) d[u] = csub(d[u], cmul(f, cconj(y[c])));
     }
@@ -1512,9 +1562,11 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   if (mmax > 0) {
     if (mmax > 512) throw std::runtime_error("k_eigvec: complement dimension > 512");
     // one warp per eigenvector; shared: d, e (2 bmax) + 7 bmax doubles per warp
+    // + the staged reflector chunk (8 x bmax complex)
     int wpc = 8;
-    while (wpc > 1 && (size_t)(2 + 7 * wpc) * L.bmax * sizeof(double) > kSmemCap) --wpc;
-    const size_t vsm = (size_t)(2 + 7 * wpc) * L.bmax * sizeof(double) + 64;
+    auto need = [&](int w) { return (size_t)(2 + 7 * w) * L.bmax * sizeof(double) + 8 * (size_t)L.bmax * sizeof(cplx) + 64; };
+    while (wpc > 1 && need(wpc) > kSmemCap) --wpc;
+    const size_t vsm = need(wpc);
     set_smem((const void*)k_eigvec, vsm);
     k_eigvec<<<dim3(nb, (mmax + wpc - 1) / wpc), 256, vsm, s>>>(L, batch_cl, ws, wpc);
     post_launch("k_eigvec");

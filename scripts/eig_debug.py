@@ -18,3 +18,15 @@ print("level  n   mmax   gram_us  tridiag_us  lmax+rank_us  multisect_us (averag
 for lv in sorted(agg, reverse=True):
     a = agg[lv]
     print("%5d %4d %5d %9.1f %11.1f %13.1f %13.1f" % (lv, a[0], a[5], a[1] / a[0], a[2] / a[0], a[3] / a[0], a[4] / a[0]))
+pat2 = re.compile(r"eigvec-timing level (\d+) m (\d+) r (\d+): inverse iteration ([\d.]+) us back-transform ([\d.]+) us")
+agg2 = collections.defaultdict(lambda: [0, 0.0, 0.0, 0])
+for m in pat2.finditer(txt):
+    a = agg2[int(m.group(1))]
+    a[0] += 1
+    a[1] += float(m.group(4))
+    a[2] += float(m.group(5))
+    a[3] = max(a[3], int(m.group(2)))
+print("level  n   mmax  invit_us  backtransform_us (k_eigvec, vector 0)")
+for lv in sorted(agg2, reverse=True):
+    a = agg2[lv]
+    print("%5d %4d %5d %9.1f %9.1f" % (lv, a[0], a[3], a[1] / a[0], a[2] / a[0]))

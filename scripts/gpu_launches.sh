@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_once.py 2 > gpurun_out/ncu_launch.log 2>&1
+python scripts/launch_table.py gpurun_out/launches.csv > gpurun_out/launch_table.txt 2>&1
