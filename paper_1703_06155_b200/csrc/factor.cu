@@ -790,6 +790,104 @@ __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, 
   for (int i = threadIdx.x; i < r; i += blockDim.x) tau_g[i] = tau[i];
 }
 
+// The same QR on a thread-block cluster: the columns of U_r are spread
+// column-cyclically over the CTAs' shared memory; per column the owner forms
+// the reflector (one warp), publishes it, one cluster barrier, and every CTA
+// applies it to its own later columns (a warp per column). Same reflector
+// convention and outputs as k_eig1b (Y unit lower trapezoidal, tau).
+__global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_cl, cplx* gws) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int kHC = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int q = blockIdx.x / kHC;
+  if (L.pass2[q]) return;  // uniform over the cluster
+  const int r = L.rank1[q];
+  const int t = batch_cl[q];
+  const int b = L.bsz[t], k = L.korig[t], m = b - k, bm = L.bmax;
+  if (r == 0 || m == 0) return;
+  const size_t bb = (size_t)bm * bm;
+  cplx* ws = gws + (size_t)q * eig1_ws_cplx(bm);
+  const cplx* U = ws + bb;
+  cplx* Y = ws;
+  cplx* tau_g = ws + 2 * bb + 4 * bm + 4 * bb;
+  const int ncl = (r + kHC - 1) / kHC;
+  cplx* Ul = reinterpret_cast<cplx*>(smraw);  // m x ncl, local column jl = global rank + kHC jl
+  cplx* pubw = Ul + (size_t)m * ncl;          // [2][m] published reflector (owner), w[0] = 1
+  cplx* wv = pubw + 2 * m;                    // local copy
+  __shared__ cplx pubt[2];
+  __shared__ cplx s_tk;
+  for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
+    const int i = idx % m, jl = idx / m, c = rank + kHC * jl;
+    Ul[idx] = c < r ? U[i + (size_t)c * m] : czero();
+  }
+  cl.sync();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int s = min(m, r);
+  for (int j = 0; j < s; ++j) {
+    const int owner = j % kHC, buf = j & 1, mr = m - j;
+    if (rank == owner && warp == 0) {
+      cplx* x = Ul + j + (size_t)(j / kHC) * m;
+      double part = 0.0;
+      for (int i = 1 + lane; i < mr; i += 32) part += cabs2(x[i]);
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double tail = part;
+      const cplx c0 = x[0];
+      const double tiny = 2.2250738585072014e-308;
+      const bool triv = tail <= tiny && c0.y * c0.y <= tiny;
+      cplx tk = czero(), rden = czero();
+      if (!triv) {
+        double beta = sqrt(cabs2(c0) + tail);
+        if (c0.x >= 0.0) beta = -beta;
+        const cplx denom = csub(c0, cmk(beta, 0.0));
+        tk = cconj(cdiv(csub(cmk(beta, 0.0), c0), cmk(beta, 0.0)));
+        rden = cdiv(cone(), denom);
+      }
+      cplx* pw = pubw + (size_t)buf * m;
+      for (int i = lane; i < mr; i += 32) {
+        const cplx v = i == 0 ? cone() : (triv ? czero() : cmul(x[i], rden));
+        if (i > 0) x[i] = v;
+        pw[i] = v;
+      }
+      if (lane == 0) pubt[buf] = tk, tau_g[j] = tk;
+    }
+    cl.sync();  // reflector j published
+    const cplx* ow = cl.map_shared_rank(pubw, owner) + (size_t)buf * m;
+    if (threadIdx.x == 0) s_tk = cl.map_shared_rank(pubt, owner)[buf];
+    for (int i = threadIdx.x; i < mr; i += blockDim.x) wv[i] = ow[i];
+    __syncthreads();
+    const cplx tk = s_tk;
+    if (tk.x != 0.0 || tk.y != 0.0) {
+      // own columns c > j, a warp per column
+      const int jl0 = (j + 1 - rank + kHC - 1) / kHC;
+      for (int jl = max(jl0, 0) + warp; jl < ncl; jl += nw) {
+        const int c = rank + kHC * jl;
+        if (c >= r) break;
+        cplx* a = Ul + j + (size_t)jl * m;
+        cplx tt = czero();
+        for (int i = 1 + lane; i < mr; i += 32) cfma(tt, cconj(wv[i]), a[i]);
+        for (int o = 16; o > 0; o >>= 1) {
+          tt.x += __shfl_xor_sync(0xffffffffu, tt.x, o);
+          tt.y += __shfl_xor_sync(0xffffffffu, tt.y, o);
+        }
+        tt = cmul(tk, cadd(tt, a[0]));
+        __syncwarp();
+        if (lane == 0) a[0] = csub(a[0], tt);
+        for (int i = 1 + lane; i < mr; i += 32) a[i] = csub(a[i], cmul(wv[i], tt));
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();  // nobody reads this CTA's published reflectors any more
+  // Y (m x r): unit lower trapezoidal reflectors
+  for (int idx = threadIdx.x; idx < m * ncl; idx += blockDim.x) {
+    const int i = idx % m, jl = idx / m, c = rank + kHC * jl;
+    if (c < r) Y[i + (size_t)c * m] = i < c ? czero() : (i == c ? cone() : Ul[idx]);
+  }
+}
+
 // D1 = Vp H_0^H H_1^H ... H_{r-1}^H applied row by row: every row of D1 is
 // transformed independently (d <- d - conj(tau_j) (d y_j) y_j^H), so one warp
 // per row streams through the r reflectors with no block-wide barrier. This
@@ -1572,9 +1670,34 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     post_launch("k_eigvec");
   }
   phase(2);
-  set_smem((const void*)k_eig1b, (size_t)L.bmax * 16 * sizeof(cplx));
-  k_eig1b<<<nb, 256, (size_t)L.bmax * 16 * sizeof(cplx), s>>>(L, batch_cl, ws);
-  post_launch("k_eig1b");
+  {
+    // QR of the retained vectors on a cluster (columns in distributed shared memory)
+    const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : (L.bmax <= 240 ? 8 : kHCmax));
+    const int ncl = (L.bmax + kHC - 1) / kHC;
+    const size_t smem = ((size_t)L.bmax * ncl + 3 * (size_t)L.bmax) * sizeof(cplx) + 64;
+    if (smem > kSmemCap) throw std::runtime_error("k_eig1b_cl: block too large for the cluster");
+    set_smem((const void*)k_eig1b_cl, smem);
+    static bool np = false;
+    if (!np) {
+      cudaFuncSetAttribute((const void*)k_eig1b_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      np = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb * kHC);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kHC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1b_cl, L, batch_cl, ws);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_eig1b_cl failed: ") + cudaGetErrorString(e));
+    post_launch("k_eig1b_cl");
+  }
   if (mmax > 512) throw std::runtime_error("k_eig1_apply: complement dimension > 512");
   k_eig1_apply<<<dim3(nb, (L.bmax + 7) / 8), 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_eig1_apply");
