@@ -1251,7 +1251,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_crit, 0));
             ctx->prof_side.cur_level = l;
             ctx->prof_side.begin(PC_SCHUR, ctx->side);
-            launch_schur(DL, d_sch + s0 + ncr, nbulk, d_con, ctx->side);
+            if (!(DL.debug & 16)) launch_schur(DL, d_sch + s0 + ncr, nbulk, d_con, ctx->side);  // debug 16: timing experiment only (wrong results)
             ctx->prof_side.end(ctx->side);
             CK(cudaEventRecord(ctx->ev_bulk, ctx->side));
             C->klaunch[PC_SCHUR] += (ncr > 0) + (nbulk > 0);

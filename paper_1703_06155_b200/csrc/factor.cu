@@ -892,8 +892,8 @@ __global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_c
 // transformed independently (d <- d - conj(tau_j) (d y_j) y_j^H), so one warp
 // per row streams through the r reflectors with no block-wide barrier. This
 // replaces the compact-WY chain (S = Y^H Y, T recurrence, three GEMMs).
+template <int KP>  // columns per lane: m <= 32 KP
 __global__ void __launch_bounds__(256) k_eig1_apply(DevLevel L, const int* batch_cl, const cplx* gws) {
-  constexpr int kMaxPer = 16;  // m <= 512
   const int q = blockIdx.x;
   if (L.pass2[q]) return;
   const int t = batch_cl[q];
@@ -908,43 +908,54 @@ __global__ void __launch_bounds__(256) k_eig1_apply(DevLevel L, const int* batch
   const cplx* tau_g = ws + 2 * bb + 4 * bm + 4 * bb;
   const cplx* Vp = L.Vp + (size_t)t * bb;
   cplx* D1 = L.dir + (size_t)q * bb;
-  cplx d[kMaxPer];
+  cplx d[KP];
 #pragma unroll
-  for (int u = 0; u < kMaxPer; ++u) {
+  for (int u = 0; u < KP; ++u) {
     const int c = lane + 32 * u;
     d[u] = c < m ? Vp[row + (size_t)c * b] : czero();
   }
+  // reflector j + 1 is loaded (predicated, all loads in flight together)
+  // while reflector j is applied
+  cplx yn[KP];
+  auto load = [&](int j) {
+    const cplx* y = Y + (size_t)j * m;
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
+      const int c = lane + 32 * u;
+      yn[u] = (c < m && c >= j) ? y[c] : czero();
+    }
+  };
+  if (r > 0) load(0);
   const int u1 = (m + 31) / 32;
   for (int j = 0; j < r; ++j) {
-    const cplx* y = Y + (size_t)j * m;
-    double sr = 0.0, si = 0.0;
-    const int u0 = j / 32;  // warp-uniform live range of the reflector
+    cplx yv[KP];
 #pragma unroll
-    for (int u = 0; u < kMaxPer; ++u) {
+    for (int u = 0; u < KP; ++u) yv[u] = yn[u];
+    const cplx tj = tau_g[j];
+    if (j + 1 < r) load(j + 1);
+    const int u0 = j / 32;  // warp-uniform live range of the reflector
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int u = 0; u < KP; ++u) {
       if (u >= u1) break;
       if (u < u0) continue;
-      const int c = lane + 32 * u;
-      if (c < m && c >= j) {
-        const cplx yv = y[c];
-        sr += d[u].x * yv.x - d[u].y * yv.y;
-        si += d[u].x * yv.y + d[u].y * yv.x;
-      }
+      sr += d[u].x * yv[u].x - d[u].y * yv[u].y;
+      si += d[u].x * yv[u].y + d[u].y * yv[u].x;
     }
     for (int o = 16; o > 0; o >>= 1) {
       sr += __shfl_xor_sync(0xffffffffu, sr, o);
       si += __shfl_xor_sync(0xffffffffu, si, o);
     }
-    const cplx f = cmul(cconj(tau_g[j]), cmk(sr, si));
+    const cplx f = cmul(cconj(tj), cmk(sr, si));
 #pragma unroll
-    for (int u = 0; u < kMaxPer; ++u) {
+    for (int u = 0; u < KP; ++u) {
       if (u >= u1) break;
       if (u < u0) continue;
-      const int c = lane + 32 * u;
-      if (c < m && c >= j) d[u] = csub(d[u], cmul(f, cconj(y[c])));
+      d[u] = csub(d[u], cmul(f, cconj(yv[u])));
     }
   }
 #pragma unroll
-  for (int u = 0; u < kMaxPer; ++u) {
+  for (int u = 0; u < KP; ++u) {
     const int c = lane + 32 * u;
     if (c < m) D1[row + (size_t)c * b] = d[u];
   }
@@ -1699,7 +1710,15 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     post_launch("k_eig1b_cl");
   }
   if (mmax > 512) throw std::runtime_error("k_eig1_apply: complement dimension > 512");
-  k_eig1_apply<<<dim3(nb, (L.bmax + 7) / 8), 256, 0, s>>>(L, batch_cl, ws);
+  const dim3 ga(nb, (L.bmax + 7) / 8);
+  if (L.bmax <= 128)
+    k_eig1_apply<4><<<ga, 256, 0, s>>>(L, batch_cl, ws);
+  else if (L.bmax <= 256)
+    k_eig1_apply<8><<<ga, 256, 0, s>>>(L, batch_cl, ws);
+  else if (L.bmax <= 384)
+    k_eig1_apply<12><<<ga, 256, 0, s>>>(L, batch_cl, ws);
+  else
+    k_eig1_apply<16><<<ga, 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_eig1_apply");
 }
 
