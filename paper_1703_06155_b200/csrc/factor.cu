@@ -1138,8 +1138,14 @@ __global__ void __launch_bounds__(256) k_hlu_prep(DevLevel L, const int* batch_c
   }
 }
 
-__global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const double* scale, int* fail, int j0) {
+__global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const double* scale, int* fail, int j0,
+                                                   cplx* Dg) {
+  // grid (nb, NY): every CTA factors the 32 x 32 diagonal block itself
+  // (identical results) and takes a share of the row / column triangular
+  // solves; the factored block goes to Dg (k_hlu_update stores it into M, so
+  // no CTA here can see it half-written)
   __shared__ cplx P[32][33];
+  __shared__ cplx rinv[32];
   const int q = blockIdx.x;
   const int t = batch_cl[q];
   const int b = L.bsz[t], e = b - L.kfin[t];
@@ -1156,13 +1162,15 @@ __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_
     const cplx piv = P[k][k];
     const double pa = cabsd(piv);
     if (pa < tol || (scale[q] == 0.0)) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && blockIdx.y == 0) {
         raise_error(L.err, 4, (1 << L.level) - 1 + t, L.level, j0 + k, pa);
         fail[q] = 1;
       }
       return;  // uniform
     }
-    for (int i = k + 1 + threadIdx.x; i < kb; i += blockDim.x) P[i][k] = cdiv(P[i][k], piv);
+    const cplx rp = cdiv(cone(), piv);
+    if (threadIdx.x == 0) rinv[k] = rp;
+    for (int i = k + 1 + threadIdx.x; i < kb; i += blockDim.x) P[i][k] = cmul(P[i][k], rp);
     __syncthreads();
     for (int idx = threadIdx.x; idx < (kb - k - 1) * (kb - k - 1); idx += blockDim.x) {
       const int i = k + 1 + idx % (kb - k - 1), j = k + 1 + idx / (kb - k - 1);
@@ -1170,13 +1178,14 @@ __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_
     }
     __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
-    const int i = idx % kb, j = idx / kb;
-    M[(j0 + i) + (size_t)(j0 + j) * ldm] = P[i][j];
-  }
+  if (blockIdx.y == 0)
+    for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+      const int i = idx % kb, j = idx / kb;
+      Dg[(size_t)q * 1024 + i + 32 * j] = P[i][j];
+    }
   // rows below the panel: x U = a (L21); columns right of it: L y = c (U12)
   const int rest = N - j0 - kb;
-  for (int it = threadIdx.x; it < 2 * rest; it += blockDim.x) {
+  for (int it = blockIdx.y * blockDim.x + threadIdx.x; it < 2 * rest; it += gridDim.y * blockDim.x) {
     cplx x[32];
     if (it < rest) {
       cplx* row = M + (j0 + kb + it) + (size_t)j0 * ldm;
@@ -1186,9 +1195,14 @@ __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (k >= kb) break;
-        cplx a = x[k];
-        for (int l = 0; l < k; ++l) a = csub(a, cmul(x[l], P[l][k]));
-        x[k] = cdiv(a, P[k][k]);
+        cplx a0 = x[k], a1 = czero();
+        int l = 0;
+        for (; l + 1 < k; l += 2) {
+          a0 = csub(a0, cmul(x[l], P[l][k]));
+          a1 = csub(a1, cmul(x[l + 1], P[l + 1][k]));
+        }
+        if (l < k) a0 = csub(a0, cmul(x[l], P[l][k]));
+        x[k] = cmul(cadd(a0, a1), rinv[k]);
         row[(size_t)k * ldm] = x[k];
       }
     } else {
@@ -1199,16 +1213,21 @@ __global__ void __launch_bounds__(256) k_hlu_panel(DevLevel L, const int* batch_
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         if (k >= kb) break;
-        cplx a = x[k];
-        for (int l = 0; l < k; ++l) a = csub(a, cmul(P[k][l], x[l]));
-        x[k] = a;
-        col[k] = a;
+        cplx a0 = x[k], a1 = czero();
+        int l = 0;
+        for (; l + 1 < k; l += 2) {
+          a0 = csub(a0, cmul(P[k][l], x[l]));
+          a1 = csub(a1, cmul(P[k][l + 1], x[l + 1]));
+        }
+        if (l < k) a0 = csub(a0, cmul(P[k][l], x[l]));
+        x[k] = cadd(a0, a1);
+        col[k] = x[k];
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(128, 3) k_hlu_update(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const int* fail, int j0) {
+__global__ void __launch_bounds__(128, 3) k_hlu_update(DevLevel L, const int* batch_cl, cplx* M0, int ldm, const int* fail, int j0, const cplx* Dg) {
   extern __shared__ __align__(16) unsigned char tsm[];
   Tile128Smem& S = *reinterpret_cast<Tile128Smem*>(tsm);
   const int q = blockIdx.x;
@@ -1218,6 +1237,11 @@ __global__ void __launch_bounds__(128, 3) k_hlu_update(DevLevel L, const int* ba
   const int kb = min(32, e - j0), N = b + e, c = j0 + kb, rest = N - c;
   const int nt = (rest + 63) / 64;
   cplx* M = M0 + (size_t)q * ldm * ldm;
+  if (blockIdx.y == 0)  // the panel's factored diagonal block (read by nobody in this launch)
+    for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+      const int i = idx % kb, j = idx / kb;
+      M[(j0 + i) + (size_t)(j0 + j) * ldm] = Dg[(size_t)q * 1024 + i + 32 * j];
+    }
   for (int tile = blockIdx.y; tile < nt * nt; tile += gridDim.y) {
     const int r0 = (tile % nt) * 64, c0 = (tile / nt) * 64;
     Acc64 acc;
@@ -1736,9 +1760,10 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cuda
     // multi-CTA extended LU (k_hlu_*); M per slot is (b + e)^2 <= (2 bmax)^2
     const int ldm = 2 * L.bmax;
     const size_t mbytes = (size_t)ldm * ldm * sizeof(cplx);
-    char* ws = reinterpret_cast<char*>(workspace(mbytes * nb + (size_t)nb * 16 + 64, s));
+    char* ws = reinterpret_cast<char*>(workspace(mbytes * nb + (size_t)nb * 1024 * sizeof(cplx) + (size_t)nb * 16 + 64, s));
     cplx* M0 = reinterpret_cast<cplx*>(ws);
-    double* scale = reinterpret_cast<double*>(ws + mbytes * nb);
+    cplx* Dg = reinterpret_cast<cplx*>(ws + mbytes * nb);  // factored 32 x 32 diagonal blocks
+    double* scale = reinterpret_cast<double*>(Dg + (size_t)nb * 1024);
     int* fail = reinterpret_cast<int*>(scale + nb);
     cudaMemsetAsync(scale, 0, (size_t)nb * sizeof(double), s);
     k_hlu_prep<<<dim3(nb, 16), 256, 0, s>>>(L, batch_cl, M0, ldm, scale, fail);
@@ -1746,9 +1771,9 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cuda
     set_smem((const void*)k_hlu_update, sizeof(Tile128Smem));
     const int nt = (ldm + 63) / 64;
     for (int j0 = 0; j0 < emax; j0 += 32) {
-      k_hlu_panel<<<nb, 256, 0, s>>>(L, batch_cl, M0, ldm, scale, fail, j0);
+      k_hlu_panel<<<dim3(nb, (2 * ldm + 255) / 256), 256, 0, s>>>(L, batch_cl, M0, ldm, scale, fail, j0, Dg);
       post_launch("k_hlu_panel");
-      k_hlu_update<<<dim3(nb, std::min(nt * nt, 64)), 128, sizeof(Tile128Smem), s>>>(L, batch_cl, M0, ldm, fail, j0);
+      k_hlu_update<<<dim3(nb, std::min(nt * nt, 64)), 128, sizeof(Tile128Smem), s>>>(L, batch_cl, M0, ldm, fail, j0, Dg);
       post_launch("k_hlu_update");
     }
     k_hlu_finish<<<dim3(nb, 16), 256, 0, s>>>(L, batch_cl, M0, ldm, fail);
