@@ -181,20 +181,24 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   }
   cl.sync();
   if (kHC == 1 && m <= 64) {
-    // small blocks: one warp runs the whole reduction (lane i owns rows i and
-    // i + 32 of the trailing block), no block barriers inside the column loop
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      cplx* vs = vbuf;  // v of the current column
-      cplx* wsv = pbuf; // w of the current column
-      for (int kk = 0; kk + 1 < m; ++kk) {
-        const int nk = m - kk - 1;
-        cplx* x = Hl + (kk + 1) + (size_t)kk * m;
+    // small blocks, one CTA: warp 0 forms the reflector; the matvec runs as
+    // (row, column-group) partials over all 256 threads, the rank-2 update
+    // over all threads; four block barriers per column
+    __shared__ int s_sk1[2];  // by column parity: a skipped column has no closing barrier
+    __shared__ cplx s_tk1[2];
+    cplx* vs = vbuf;       // v of the current column
+    cplx* wsv = vbuf + m;  // w of the current column
+    cplx* part = pbuf;     // [4][m] matvec partials (pbuf + wfull: 4m)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int kk = 0; kk + 1 < m; ++kk) {
+      const int nk = m - kk - 1;
+      cplx* x = Hl + (kk + 1) + (size_t)kk * m;
+      if (warp == 0) {
         const cplx x0 = lane < nk ? x[lane] : czero();
         const cplx x1 = lane + 32 < nk ? x[lane + 32] : czero();
-        double part = (lane >= 1 ? cabs2(x0) : 0.0) + cabs2(x1);
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        const double xn2 = part;
+        double part2 = (lane >= 1 ? cabs2(x0) : 0.0) + cabs2(x1);
+        for (int o = 16; o > 0; o >>= 1) part2 += __shfl_xor_sync(0xffffffffu, part2, o);
+        const double xn2 = part2;
         const cplx al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
         const bool skip = xn2 == 0.0 && al.y == 0.0;
         double beta = al.x;
@@ -209,51 +213,60 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
           aux[kk] = Hl[kk + (size_t)kk * m].x;  // d_k
           aux[bm + kk] = beta;                   // e_k
           reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = tk;
+          s_sk1[kk & 1] = skip;
+          s_tk1[kk & 1] = tk;
         }
-        if (skip) continue;  // warp-uniform
-        cplx v0 = lane == 0 ? cone() : cmul(x0, sc), v1 = cmul(x1, sc);
-        if (lane >= 1 && lane < nk) x[lane] = v0;
-        if (lane + 32 < nk) x[lane + 32] = v1;
-        if (lane < nk) vs[lane] = v0;
-        if (lane + 32 < nk) vs[lane + 32] = v1;
-        __syncwarp();
-        // p = tau A22 v (A22 = trailing nk x nk block, full storage)
-        const cplx* A22 = Hl + (kk + 1) + (size_t)(kk + 1) * m;
-        cplx p0 = czero(), p1 = czero();
-        for (int j = 0; j < nk; ++j) {
-          const cplx vj = vs[j];
-          if (lane < nk) cfma(p0, A22[lane + (size_t)j * m], vj);
-          if (lane + 32 < nk) cfma(p1, A22[lane + 32 + (size_t)j * m], vj);
+        if (!skip) {
+          const cplx v0 = lane == 0 ? cone() : cmul(x0, sc), v1 = cmul(x1, sc);
+          if (lane >= 1 && lane < nk) x[lane] = v0;
+          if (lane + 32 < nk) x[lane + 32] = v1;
+          if (lane < nk) vs[lane] = v0;
+          if (lane + 32 < nk) vs[lane + 32] = v1;
         }
-        p0 = cmul(tk, p0), p1 = cmul(tk, p1);
-        // c = v^H p; w = p - 1/2 conj(tau) c v
-        const cplx t0 = cmul(cconj(v0), p0), t1 = cmul(cconj(v1), p1);
-        double cr = (lane < nk ? t0.x : 0.0) + (lane + 32 < nk ? t1.x : 0.0);
-        double ci = (lane < nk ? t0.y : 0.0) + (lane + 32 < nk ? t1.y : 0.0);
+      }
+      __syncthreads();
+      if (s_sk1[kk & 1]) continue;  // uniform
+      const cplx tk = s_tk1[kk & 1];
+      const cplx* A22 = Hl + (kk + 1) + (size_t)(kk + 1) * m;
+      {
+        const int i = threadIdx.x & 63, g = threadIdx.x >> 6;
+        if (i < nk) {
+          cplx acc = czero();
+          for (int j = g; j < nk; j += 4) cfma(acc, A22[i + (size_t)j * m], vs[j]);
+          part[g * m + i] = acc;
+        }
+      }
+      __syncthreads();
+      // p = tau A22 v, c = v^H p (rows over the first two warps)
+      cplx pi = czero();
+      double cr = 0.0, ci = 0.0;
+      if (threadIdx.x < 64) {
+        const int i = threadIdx.x;
+        if (i < nk) {
+          pi = cmul(tk, cadd(cadd(part[i], part[m + i]), cadd(part[2 * m + i], part[3 * m + i])));
+          const cplx tt = cmul(cconj(vs[i]), pi);
+          cr = tt.x, ci = tt.y;
+        }
         for (int o = 16; o > 0; o >>= 1) {
           cr += __shfl_xor_sync(0xffffffffu, cr, o);
           ci += __shfl_xor_sync(0xffffffffu, ci, o);
         }
-        const cplx hc = cscale(cmul(cconj(tk), cmk(cr, ci)), 0.5);
-        const cplx w0 = csub(p0, cmul(hc, v0)), w1 = csub(p1, cmul(hc, v1));
-        if (lane < nk) wsv[lane] = w0;
-        if (lane + 32 < nk) wsv[lane + 32] = w1;
-        __syncwarp();
-        // rank-2 update of own rows: A22[i, j] -= v_i conj(w_j) + w_i conj(v_j)
-        cplx* A22w = Hl + (kk + 1) + (size_t)(kk + 1) * m;
-        for (int j = 0; j < nk; ++j) {
-          const cplx vj = cconj(vs[j]), wj = cconj(wsv[j]);
-          if (lane < nk) {
-            cplx* a = A22w + lane + (size_t)j * m;
-            *a = csub(csub(*a, cmul(v0, wj)), cmul(w0, vj));
-          }
-          if (lane + 32 < nk) {
-            cplx* a = A22w + lane + 32 + (size_t)j * m;
-            *a = csub(csub(*a, cmul(v1, wj)), cmul(w1, vj));
-          }
-        }
-        __syncwarp();
+        if (lane == 0) red[2 * warp] = cr, red[2 * warp + 1] = ci;
       }
+      __syncthreads();
+      if (threadIdx.x < 64 && (int)threadIdx.x < nk) {
+        const cplx hc = cscale(cmul(cconj(tk), cmk(red[0] + red[2], red[1] + red[3])), 0.5);
+        wsv[threadIdx.x] = csub(pi, cmul(hc, vs[threadIdx.x]));
+      }
+      __syncthreads();
+      // rank-2 update of the trailing block: A22[i, j] -= v_i conj(w_j) + w_i conj(v_j)
+      cplx* A22w = Hl + (kk + 1) + (size_t)(kk + 1) * m;
+      for (int idx = threadIdx.x; idx < nk * nk; idx += blockDim.x) {
+        const int i = idx % nk, j = idx / nk;
+        cplx* a = A22w + i + (size_t)j * m;
+        *a = csub(csub(*a, cmul(vs[i], cconj(wsv[j]))), cmul(wsv[i], cconj(vs[j])));
+      }
+      __syncthreads();
     }
     __syncthreads();
   } else {
