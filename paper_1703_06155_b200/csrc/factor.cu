@@ -459,12 +459,13 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     s_piv = 2.2250738585072014e-308 * fmax(1.0, emax);
   }
   __syncthreads();
-  // largest eigenvalue by multisection: every thread tests 4 points of the
-  // current bracket, so each round shrinks it (4 blockDim.x + 1)-fold
+  // largest eigenvalue by multisection: every thread tests one point of the
+  // current bracket, so each round shrinks it (blockDim.x + 1)-fold (more
+  // points per thread saturate the FP64 pipe without saving a round)
   double* e2 = ed + m;
   for (int i = threadIdx.x; i + 1 < m; i += blockDim.x) e2[i] = ed[i] * ed[i];
   {
-    constexpr int P = 4;
+    constexpr int P = 1;
     __shared__ double s_a, s_b;
     if (threadIdx.x == 0) s_a = s_lo, s_b = s_hi;
     __syncthreads();
