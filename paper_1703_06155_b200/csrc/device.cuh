@@ -571,7 +571,7 @@ __device__ __forceinline__ void sturm_count_p(int n, const double* d, const doub
 // (the CTAs of a cluster share the work).
 __device__ inline void multisect_top(int n, const double* d, const double* e2, int r, double lo0, double hi0, double pivmin, double* out,
                                      int part = 0, int nparts = 1) {
-  constexpr int P = 4;
+  constexpr int P = 2;  // 2 shifts per lane: latency and FP64 throughput of the counts balance
   const int cnt = r > part ? (r - part + nparts - 1) / nparts : 0;
   int G = 32;
   while (G > 1 && G * cnt > (int)blockDim.x) G >>= 1;
