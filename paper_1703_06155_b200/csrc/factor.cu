@@ -280,39 +280,43 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   cplx* wb = wfull;            // [m] w (local)
   cplx* colb = wfull + m;      // [m] next column after the update (local)
   cplx* vn = vv + m;           // [m] next reflector (local)
-  __shared__ cplx s_tl, s_sc;
-  __shared__ double s_bt;
-  __shared__ int s_sk;
   // reflector of column kk from col[0 .. m-kk-1] = A[kk.., kk] (updated);
   // writes vn, s_tl, s_sk (aux from rank 0)
+  // every thread forms the scalars itself from one block reduction (no
+  // broadcast barrier); the partial sums alternate between two halves of red2
+  __shared__ double red2[64];
+  cplx r_tl = czero();
   auto reflector = [&](int kk, const cplx* col) {
     const int nk = m - kk - 1;
     double part = 0.0;
     for (int i = 1 + threadIdx.x; i < nk; i += blockDim.x) part += cabs2(col[1 + i]);
-    const double xn2 = cta_sum(part, red);
-    if (threadIdx.x == 0) {
-      const cplx al = col[1];
-      if (xn2 == 0.0 && al.y == 0.0) {
-        s_sk = 1;
-        s_tl = czero();
-        s_bt = al.x;
-      } else {
-        double beta = sqrt(cabs2(al) + xn2);
-        if (al.x >= 0.0) beta = -beta;
-        s_sk = 0;
-        s_bt = beta;
-        s_tl = cdiv(csub(cmk(beta, 0.0), al), cmk(beta, 0.0));
-        s_sc = cdiv(cone(), csub(al, cmk(beta, 0.0)));
-      }
-      if (rank == 0) {
-        aux[kk] = col[0].x;  // d_k
-        aux[bm + kk] = s_bt; // e_k
-        reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = s_tl;
-      }
-    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    double* rb = red2 + 32 * (kk & 1);
+    if ((threadIdx.x & 31) == 0) rb[threadIdx.x >> 5] = part;
     __syncthreads();
+    double xn2 = 0.0;
+    for (int u = 0; u < (int)(blockDim.x >> 5); ++u) xn2 += rb[u];
+    const cplx al = col[1];
+    const bool sk = xn2 == 0.0 && al.y == 0.0;
+    double beta = al.x;
+    cplx sc = czero();
+    r_tl = czero();
+    if (!sk) {
+      beta = sqrt(cabs2(al) + xn2);
+      if (al.x >= 0.0) beta = -beta;
+      // tau = (beta - al) / beta, scale = 1 / (al - beta) (beta real)
+      const double ib = 1.0 / beta;
+      r_tl = cmk((beta - al.x) * ib, -al.y * ib);
+      const double zx = al.x - beta, zy = al.y, iz = 1.0 / (zx * zx + zy * zy);
+      sc = cmk(zx * iz, -zy * iz);
+    }
+    if (rank == 0 && threadIdx.x == 0) {
+      aux[kk] = col[0].x;  // d_k
+      aux[bm + kk] = beta; // e_k
+      reinterpret_cast<cplx*>(aux + 4 * bm)[kk] = r_tl;
+    }
     // skipped columns (tau = 0) use v = e_1: the update then subtracts zeros
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) vn[i] = i == 0 ? cone() : (s_sk ? czero() : cmul(col[1 + i], s_sc));
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) vn[i] = i == 0 ? cone() : (sk ? czero() : cmul(col[1 + i], sc));
   };
   if (m > 1) {
     // column 0 lives in CTA 0 (Gram reduced and the cluster synchronised above)
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     const int buf = kk & 1;
     const int nk = m - kk - 1;
     // current reflector
-    const cplx tk = s_tl;
+    const cplx tk = r_tl;
     for (int i = threadIdx.x; i < nk; i += blockDim.x) vv[i] = vn[i];
     __syncthreads();
     // publish column kk+1 (rows kk+1..) before its update by column kk
