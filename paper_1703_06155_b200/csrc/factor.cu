@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   cplx* pub = vbuf;            // [2][m] published next column (owner), rows kk+1..
   cplx* wb = wfull;            // [m] w (local)
   cplx* colb = wfull + m;      // [m] next column after the update (local)
-  cplx* vn = vv + m;           // [m] next reflector (local)
+  cplx* const vbase = vv;      // [2][m] reflectors by column parity (local)
+  cplx* vn = vbase;            // where the next reflector goes
   // reflector of column kk from col[0 .. m-kk-1] = A[kk.., kk] (updated);
   // writes vn, s_tl, s_sk (aux from rank 0)
   // every thread forms the scalars itself from one block reduction (no
@@ -331,8 +332,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     const int nk = m - kk - 1;
     // current reflector
     const cplx tk = r_tl;
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) vv[i] = vn[i];
-    __syncthreads();
+    vv = vbase + (size_t)(kk & 1) * m;  // written by reflector(kk), visible since the last barrier
+    vn = vbase + (size_t)((kk + 1) & 1) * m;
     // publish column kk+1 (rows kk+1..) before its update by column kk
     const int own1 = (kk + 1) % kHC;
     if (kk + 2 < m && rank == own1) {
