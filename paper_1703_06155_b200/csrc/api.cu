@@ -1333,16 +1333,40 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           flops += 8.0 * bd * bd * rot;  // step 2 on off-diagonal blocks
           if (e > 0) {
             flops += 8.0 / 3.0 * ed * ed * ed + 4.0 * ed * ed * (rot + 2.0 * kf);  // LU + TRSMs
-            // Schur: sum_j b_j * e * sum_c b_c (incl. self rows/cols of kf)
-            double rows = kf, cols = kf;
-            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) rows += cur.bsz[Y.R_nb[a]];
-            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) cols += cur.bsz[Y.C_nb[a]];
-            const double sch = 8.0 * rows * ed * cols;
+            flops += 8.0 * kf * ed * kf;  // self Schur block (head kernels)
+          }
+        }
+        // Schur products actually executed by k_schur: per
+        // target and contribution; rows / columns of a dense target whose
+        // cluster was eliminated in an earlier batch receive exact zeros and
+        // are not computed. Bytes: every target read + written once, panels
+        // read once per target they feed.
+        for (const SchurTarget& T : W.schur) {
+          int rws, cls, rs = 0, cs = 0;
+          if ((T.kind & 1) == 0) {
+            const int j = Y.drow[T.idx], c = Y.dcol[T.idx];
+            rws = cur.bsz[j], cls = cur.bsz[c];
+            if (T.kind & 2) rs = cur.bsz[j] - kfin[j];
+            if (T.kind & 4) cs = cur.bsz[c] - kfin[c];
+          } else {
+            rws = cur.bsz[Y.frow[T.idx]], cls = cur.bsz[Y.fcol[T.idx]];
+          }
+          bool any = false;
+          for (int k = T.c0; k < T.c1; ++k) {
+            const SchurContrib& cb = W.contrib[k];
+            const int tc = cb.t, ec = cur.bsz[tc] - kfin[tc];
+            if (ec == 0) continue;
+            any = true;
+            const int ro = cb.r >= 0 ? 0 : ec, ar = cb.r >= 0 ? cur.bsz[Y.R_nb[cb.r]] : kfin[tc];
+            const int co = cb.c >= 0 ? 0 : ec, bc = cb.c >= 0 ? cur.bsz[Y.C_nb[cb.c]] : kfin[tc];
+            const double rr = std::max(0, std::min(ro + ar, rws) - std::max(ro, rs));
+            const double cc = std::max(0, std::min(co + bc, cls) - std::max(co, cs));
+            const double sch = 8.0 * rr * ec * cc;
             flops += sch;
             sflops += sch;
-            // every target entry read + written once, panels read once
-            sbytes += 16.0 * 2.0 * rows * cols + 16.0 * ed * (rows + cols);
+            sbytes += 16.0 * ec * (rr + cc);
           }
+          if (any) sbytes += 32.0 * (double)(rws - rs) * (double)(cls - cs);
         }
         for (size_t f = 0; f < Y.frow.size(); ++f)
           if (Y.fadm[f] >= 0 && fex[f]) ++ledger;

@@ -1323,20 +1323,24 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
   extern __shared__ __align__(16) unsigned char tsm[];
   TileSmem<TM>& S = *reinterpret_cast<TileSmem<TM>*>(tsm);
   const SchurTargetD tg = targets[blockIdx.x];
-  int rows, cols;
+  int rows, cols, rs = 0, cs = 0;
   cplx* out;
-  if (tg.kind == 0) {
-    rows = L.bsz[L.drow[tg.idx]];
-    cols = L.bsz[L.dcol[tg.idx]];
+  if ((tg.kind & 1) == 0) {
+    const int j = L.drow[tg.idx], c = L.dcol[tg.idx];
+    rows = L.bsz[j];
+    cols = L.bsz[c];
     out = L.D + L.D_off[tg.idx];
+    // rows / columns eliminated by an earlier batch receive exact zeros
+    if (tg.kind & 2) rs = rows - L.kfin[j];
+    if (tg.kind & 4) cs = cols - L.kfin[c];
   } else {
     rows = L.bsz[L.frow[tg.idx]];
     cols = L.bsz[L.fcol[tg.idx]];
     out = L.F + L.F_off[tg.idx];
   }
-  const int ntr = (rows + TM - 1) / TM, ntc = (cols + TM - 1) / TM;
+  const int ntr = (rows - rs + TM - 1) / TM, ntc = (cols - cs + TM - 1) / TM;
   if ((int)blockIdx.y >= ntr * ntc) return;
-  const int r0 = (blockIdx.y % ntr) * TM, c0 = (blockIdx.y / ntr) * TM;
+  const int r0 = rs + (blockIdx.y % ntr) * TM, c0 = cs + (blockIdx.y / ntr) * TM;
   Acc64 acc;
   cplx accs[TM == 64 ? 1 : RM][TM == 64 ? 1 : RN];
   if constexpr (TM == 64) {
@@ -1405,7 +1409,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
         }
       }
   }
-  if (tg.kind == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
+  if ((tg.kind & 1) == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
 }
 
 // --------------------------------------------------------------------------

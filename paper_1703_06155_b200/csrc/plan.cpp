@@ -339,7 +339,7 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
     for (int q = sch.batch_ptr[static_cast<size_t>(b)]; q < sch.batch_ptr[static_cast<size_t>(b) + 1]; ++q)
       batch_of[static_cast<size_t>(sch.batch_cl[static_cast<size_t>(q)])] = b;
   auto target_rc = [&](const SchurTarget& T) {
-    if (T.kind == 0) return std::make_pair(L.drow[static_cast<size_t>(T.idx)], L.dcol[static_cast<size_t>(T.idx)]);
+    if ((T.kind & 1) == 0) return std::make_pair(L.drow[static_cast<size_t>(T.idx)], L.dcol[static_cast<size_t>(T.idx)]);
     return std::make_pair(L.frow[static_cast<size_t>(T.idx)], L.fcol[static_cast<size_t>(T.idx)]);
   };
   std::vector<SchurTarget> bulk;
@@ -403,6 +403,14 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
                     static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
       for (size_t k = i; k < j; ++k) W.contrib.push_back(tmp[k].c);
       const auto rc = target_rc(T);
+      // dense target whose row (column) cluster was eliminated in an earlier
+      // batch: its first e rows (columns) are zero and stay zero (cleanup,
+      // factorization.hpp:431-439), so the update there is exactly zero and
+      // the kernel starts its tiles at e (bit 1: rows, bit 2: columns)
+      if (T.kind == 0) {
+        if (batch_of[static_cast<size_t>(rc.first)] < b) T.kind |= 2;
+        if (batch_of[static_cast<size_t>(rc.second)] < b) T.kind |= 4;
+      }
       if (batch_of[static_cast<size_t>(rc.first)] == b + 1 || batch_of[static_cast<size_t>(rc.second)] == b + 1) {
         W.schur.push_back(T);
         ++ncrit;

@@ -85,7 +85,7 @@ struct PanelItem {
 };
 
 struct SchurTarget {
-  int32_t kind;   // 0 dense, 1 fill
+  int32_t kind;   // bit 0: 0 dense, 1 fill; bits 1/2 (dense): row / column cluster eliminated in an earlier batch
   int32_t idx;    // dense block / fill index
   int32_t c0, c1; // contribution range
 };
