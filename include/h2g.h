@@ -190,6 +190,12 @@ int h2g_chain_kernel_stats(const h2g_chain* c, int32_t cls, double* out);
  * out[4]: factor_flops, schur_flops, solve_bytes, schur_bytes */
 int h2g_chain_work(const h2g_chain* c, double* out);
 
+/* The Schur products k_schur actually executed: rows / columns of a dense
+ * target whose cluster was eliminated in an earlier batch are exact zeros
+ * (cleanup, factorization.hpp:431-439) and are skipped.
+ * out[2]: flops, bytes (targets read + written once, panels once per target) */
+int h2g_chain_schur_executed(const h2g_chain* c, double* out);
+
 /* Seeded complex-normal vector: mt19937_64(seed) + std::normal_distribution,
  * cxd(g(rng), g(rng)) (tools/h2lu_cli.cpp:181-191), ORIGINAL order. */
 void h2g_random_rhs(int64_t n, uint64_t seed, double* out);

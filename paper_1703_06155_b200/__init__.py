@@ -151,6 +151,7 @@ SYMBOLS = {
     "h2g_chain_hash": (C.c_uint64, [_P]),
     "h2g_chain_timing": (C.c_int, [_P, _D, _D, _I64, _I64]),
     "h2g_chain_work": (C.c_int, [_P, _D]),
+    "h2g_chain_schur_executed": (C.c_int, [_P, _D]),
     "h2g_random_rhs": (None, [C.c_int64, C.c_uint64, _D]),
     "h2g_set_profiling": (C.c_int, [_P, C.c_int32]),
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
@@ -486,7 +487,10 @@ class FactorChain:
     def work(self):
         out = np.zeros(4)
         lib().h2g_chain_work(self.h, _d(out))
-        return dict(factor_flops=out[0], schur_flops=out[1], solve_bytes=out[2], schur_bytes=out[3])
+        ex = np.zeros(2)
+        lib().h2g_chain_schur_executed(self.h, _d(ex))
+        return dict(factor_flops=out[0], schur_flops=out[1], solve_bytes=out[2], schur_bytes=out[3],
+                    schur_flops_executed=ex[0], schur_bytes_executed=ex[1])
 
     def _solve(self, b, mode):
         b = np.asarray(b)

@@ -409,6 +409,7 @@ struct h2g_chain {
   double factor_ms = 0.0, solve_ms = 0.0;
   long long factor_launches = 0, solve_launches = 0;
   double factor_flops = 0.0, schur_flops = 0.0, solve_bytes = 0.0, schur_bytes = 0.0;
+  double schur_flops_exec = 0.0, schur_bytes_exec = 0.0;  // k_schur work after the exact-zero skip
   double kms[PC_N] = {0}, kflops[PC_N] = {0}, kbytes[PC_N] = {0};
   long long klaunch[PC_N] = {0};
 };
@@ -1333,14 +1334,24 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           flops += 8.0 * bd * bd * rot;  // step 2 on off-diagonal blocks
           if (e > 0) {
             flops += 8.0 / 3.0 * ed * ed * ed + 4.0 * ed * ed * (rot + 2.0 * kf);  // LU + TRSMs
-            flops += 8.0 * kf * ed * kf;  // self Schur block (head kernels)
+            // Schur, SURVEY §8d algorithmic count: sum_j b_j * e * sum_c b_c
+            // (incl. self rows/cols of kf), as the reference's GEMMs
+            // (factorization.hpp:416-420) execute them
+            double rows = kf, cols = kf;
+            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) rows += cur.bsz[Y.R_nb[a]];
+            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) cols += cur.bsz[Y.C_nb[a]];
+            const double sch = 8.0 * rows * ed * cols;
+            flops += sch;
+            sflops += sch;
+            // every target entry read + written once, panels read once
+            sbytes += 16.0 * 2.0 * rows * cols + 16.0 * ed * (rows + cols);
           }
         }
-        // Schur products actually executed by k_schur: per
-        // target and contribution; rows / columns of a dense target whose
-        // cluster was eliminated in an earlier batch receive exact zeros and
-        // are not computed. Bytes: every target read + written once, panels
-        // read once per target they feed.
+        // Schur products actually executed by k_schur: per target and
+        // contribution; rows / columns of a dense target whose cluster was
+        // eliminated in an earlier batch receive exact zeros and are not
+        // computed. Bytes: every target read + written once, panels read
+        // once per target they feed.
         for (const SchurTarget& T : W.schur) {
           int rws, cls, rs = 0, cs = 0;
           if ((T.kind & 1) == 0) {
@@ -1361,12 +1372,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             const int co = cb.c >= 0 ? 0 : ec, bc = cb.c >= 0 ? cur.bsz[Y.C_nb[cb.c]] : kfin[tc];
             const double rr = std::max(0, std::min(ro + ar, rws) - std::max(ro, rs));
             const double cc = std::max(0, std::min(co + bc, cls) - std::max(co, cs));
-            const double sch = 8.0 * rr * ec * cc;
-            flops += sch;
-            sflops += sch;
-            sbytes += 16.0 * ec * (rr + cc);
+            C->schur_flops_exec += 8.0 * rr * ec * cc;
+            C->schur_bytes_exec += 16.0 * ec * (rr + cc);
           }
-          if (any) sbytes += 32.0 * (double)(rws - rs) * (double)(cls - cs);
+          if (any) C->schur_bytes_exec += 32.0 * (double)(rws - rs) * (double)(cls - cs);
         }
         for (size_t f = 0; f < Y.frow.size(); ++f)
           if (Y.fadm[f] >= 0 && fex[f]) ++ledger;
@@ -2144,6 +2153,13 @@ int h2g_chain_work(const h2g_chain* c, double* out) {
   out[1] = c->schur_flops;
   out[2] = c->solve_bytes;
   out[3] = c->schur_bytes;
+  return H2G_OK;
+}
+
+int h2g_chain_schur_executed(const h2g_chain* c, double* out) {
+  if (!c || !out) return H2G_ERR_INVALID_INPUT;
+  out[0] = c->schur_flops_exec;
+  out[1] = c->schur_bytes_exec;
   return H2G_OK;
 }
 
