@@ -328,8 +328,20 @@ struct Prof {
 };
 enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SCHUR, PC_MERGE, PC_ROOT, PC_OTHER, PC_EIGVEC, PC_EIG1B, PC_N };
 
+struct PlanCache {
+  int stop = 0, schedule = 0;
+  std::vector<LevelSym> levels;
+  std::vector<LevelSchedule> sched;
+  std::vector<LevelWork> work;
+};
+
 struct h2g_context {
   int device = 0;
+  // symbolic plans keyed by a fingerprint of the block structure, stop level
+  // and schedule: a new matrix with the structure of an earlier one (same
+  // geometry, new entries) reuses the plan (the two most recent are kept)
+  std::mutex plan_mu;
+  std::vector<std::pair<uint64_t, std::shared_ptr<PlanCache>>> plan_lru;
   cudaStream_t stream = nullptr;
   // Deferred Schur updates (targets not read by the next batch) run on a
   // lower-priority side stream, overlapping the next batch's step 0-3b.
@@ -346,13 +358,6 @@ struct h2g_context {
   Prof prof;
 };
 
-struct PlanCache {
-  int stop = 0, schedule = 0;
-  std::vector<LevelSym> levels;
-  std::vector<LevelSchedule> sched;
-  std::vector<LevelWork> work;
-};
-
 struct h2g_matrix {
   h2g_context* ctx = nullptr;
   Structure S;
@@ -363,7 +368,7 @@ struct h2g_matrix {
   DBuf basis, coup, dense;
   HBuf hdense;  // the dense blocks, moved to pinned host memory when HBM runs short (config 3)
   const cplx* dense_ptr() const { return hdense.p ? hdense.as<cplx>() : dense.as<cplx>(); }
-  std::vector<std::unique_ptr<PlanCache>> plans;
+  std::vector<std::shared_ptr<PlanCache>> plans;
   std::mutex mu;
 };
 
@@ -444,11 +449,45 @@ void check_device_error(h2g_context* ctx, int level_fallback) {
   throw x;
 }
 
+uint64_t structure_fingerprint(const Structure& S, int stop, int schedule) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  const int64_t hdr[5] = {S.n, S.depth, S.l0, stop, schedule};
+  mix(hdr, sizeof(hdr));
+  mix(&S.eta, sizeof(S.eta));
+  mix(S.begin.data(), S.begin.size() * 8);
+  mix(S.end.data(), S.end.size() * 8);
+  for (const auto& v : S.adm) {
+    const int64_t k = (int64_t)v.size();
+    mix(&k, 8);
+    mix(v.data(), v.size() * sizeof(Pair));
+  }
+  for (const auto& v : S.split) {
+    const int64_t k = (int64_t)v.size();
+    mix(&k, 8);
+    mix(v.data(), v.size() * sizeof(Pair));
+  }
+  mix(S.leaf.data(), S.leaf.size() * sizeof(Pair));
+  return h;
+}
+
 PlanCache* get_plan(h2g_matrix* M, int stop, int schedule) {
   std::lock_guard<std::mutex> g(M->mu);
   for (auto& p : M->plans)
     if (p->stop == stop && p->schedule == schedule) return p.get();
-  auto P = std::make_unique<PlanCache>();
+  const uint64_t fp = structure_fingerprint(M->S, stop, schedule);
+  {
+    std::lock_guard<std::mutex> g2(M->ctx->plan_mu);
+    for (auto& e : M->ctx->plan_lru)
+      if (e.first == fp && e.second->stop == stop && e.second->schedule == schedule) {
+        M->plans.push_back(e.second);
+        return M->plans.back().get();
+      }
+  }
+  auto P = std::make_shared<PlanCache>();
   P->stop = stop;
   P->schedule = schedule;
   P->levels = build_levels(M->S, stop);
@@ -457,6 +496,12 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule) {
       P->sched.push_back(build_schedule(L, schedule));
       P->work.push_back(build_work(L, P->sched.back()));
     }
+  }
+  {
+    std::lock_guard<std::mutex> g2(M->ctx->plan_mu);
+    auto& lru = M->ctx->plan_lru;
+    lru.insert(lru.begin(), {fp, P});
+    if (lru.size() > 2) lru.pop_back();
   }
   M->plans.push_back(std::move(P));
   return M->plans.back().get();
