@@ -871,7 +871,8 @@ __global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_c
       }
       if (lane == 0) pubt[buf] = tk, tau_g[j] = tk;
     }
-    cl.sync();  // reflector j published
+    if (kHC == 1) __syncthreads();  // single CTA: a block barrier suffices
+    else cl.sync();                  // reflector j published
     const cplx* ow = cl.map_shared_rank(pubw, owner) + (size_t)buf * m;
     if (threadIdx.x == 0) s_tk = cl.map_shared_rank(pubt, owner)[buf];
     for (int i = threadIdx.x; i < mr; i += blockDim.x) wv[i] = ow[i];
