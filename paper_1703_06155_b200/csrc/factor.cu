@@ -1854,19 +1854,12 @@ static void launch_gemm_tm(const GemmDesc* d, int n, cudaStream_t s, int maxdim,
 
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim) {
   if (n <= 0) return;
-  if (maxdim > 0 && maxdim <= 16) {
+  if (maxdim > 0 && maxdim <= 16)
     launch_gemm_tm<16>(d, n, s, maxdim);
-  } else if (maxdim > 0 && maxdim <= 32) {
+  else if (maxdim > 0 && maxdim <= 32)
     launch_gemm_tm<32>(d, n, s, maxdim);
-  } else {
-    // a handful of large products (the per-cluster rotations of D(t,t)):
-    // 64 x 64 tiles would leave most SMs idle, 32 x 32 tiles spread them
-    const int t64 = maxdim > 0 ? (maxdim + 63) / 64 : 1, t32 = maxdim > 0 ? (maxdim + 31) / 32 : 1;
-    if (maxdim > 0 && (long long)n * std::min(t64 * t64, 16) < 148 && maxdim <= 512)
-      launch_gemm_tm<32>(d, n, s, maxdim, t32 * t32);
-    else
-      launch_gemm_tm<64>(d, n, s, maxdim);
-  }
+  else
+    launch_gemm_tm<64>(d, n, s, maxdim);
 }
 
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches) {
