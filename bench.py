@@ -11,8 +11,9 @@ The H² input is built on the GPU once, outside the timed region.
          library stream), inputs resident in HBM, max over ranks
   e2e    same metric through the public C-ABI calls with HOST buffers: every
          step uploads the H² matrix (h2g_matrix_upload) and the RHS from host
-         memory, factorizes, solves and reads x back (wall clock around the
-         synchronous calls, max over ranks)
+         memory, builds the symbolic plan from scratch (cold structure),
+         factorizes, solves and reads x back (wall clock around the
+         synchronous calls, max over ranks); e2e.warm reuses the plan
 
 Multi-GPU: the factorization does not shard in this round, so --gpus N runs N
 independent replicas (weak scaling). --impl reference times the
@@ -87,27 +88,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- helpers
-def sampled_dense_residual(points_tree, kernel_args, x, b, nrows=4096, seed=1234):
-    """||Zx - b|| / ||b|| on seeded sampled rows, Z from the kernel directly
-    (SURVEY §8d(ii)); numpy, O(nrows * N)."""
-    k0, scale, diag = kernel_args
-    n = points_tree.shape[0]
-    rng = np.random.default_rng(seed)
-    rows = np.sort(rng.choice(n, size=min(nrows, n), replace=False))
-    num = den = 0.0
-    for c0 in range(0, rows.size, 256):
-        rr = rows[c0:c0 + 256]
-        d = points_tree[rr, None, :] - points_tree[None, :, :]
-        r = np.sqrt((d * d).sum(-1))
-        with np.errstate(divide="ignore", invalid="ignore"):
-            Z = scale * np.exp(-1j * k0 * r) / (4 * np.pi * r)
-        Z[np.arange(rr.size), rr] = diag
-        res = Z @ x - b[rr]
-        num += float(np.vdot(res, res).real)
-        den += float(np.vdot(b[rr], b[rr]).real)
-    return math.sqrt(num / den)
-
-
 def load_peaks():
     peaks = {}
     try:
@@ -121,10 +101,43 @@ def load_peaks():
     return peaks
 
 
-def cpu_oracle_sample(threads_note=True):
-    """Oracle (CPU restatement of the reference, single-threaded like the
-    reference) factorizing BASELINE config 1 — the reference's own
-    CPU-runnable case — as the bounded CPU sample."""
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_threads():
+    """Threads the oracle's worker pool uses (H2O_THREADS, default all cores)."""
+    v = os.environ.get("H2O_THREADS")
+    return max(1, int(v)) if v else (os.cpu_count() or 1)
+
+
+def golden_cpu_reference(config):
+    """The full-config oracle factorization measured once (tests/golden,
+    written by scripts/oracle_golden.py), if committed for this config."""
+    f = os.path.join(ROOT, "tests", "golden", f"cfg{config}_oracle.json")
+    if not os.path.exists(f):
+        return None
+    try:
+        g = json.load(open(f))
+    except Exception:
+        return None
+    return {"value": g["n"] / g["oracle_factor_s"], "unit": "unknowns/s", "factor_s": g["oracle_factor_s"], "cores": g["oracle_threads"],
+            "nproc": g["nproc"], "cpu_model": g["cpu_model"], "when": g["when"], "source": os.path.relpath(f, ROOT),
+            "note": f"oracle factorization of the full BASELINE config {config} (N={g['n']}) measured once on the GPU box host"}
+
+
+def cpu_oracle_sample():
+    """Bounded CPU sample of the config-2 workload: the oracle (CPU
+    restatement of the reference, reference order) factorizing one octant of
+    the config-2 cube, i.e. the 16^3 sub-cube at the same spacing h = 1/32,
+    leaf 32, eps 1e-4 (identical to BASELINE config 1, the reference's own
+    CPU-runnable case)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points
@@ -134,6 +147,24 @@ def cpu_oracle_sample(threads_note=True):
     t = O.Tree(vie_grid_points(c["cells"], c["side"]), c["leaf"])
     A = O.H2(O.Blocks(t, 1.0), O.helmholtz(k0, diag, scale), c["eps"])
     return A, c, O
+
+
+SAMPLE_NOTE = ("oracle/ (CPU restatement of proj/include/h2lu/factorization.hpp, reference cluster order; independent block "
+               "products on a worker pool, bit-identical to 1 thread) factorizing one octant of the config-2 cube per step: the "
+               "16^3 sub-cube at the same h = 1/32, leaf 32, eps 1e-4 (= BASELINE config 1, N=4096). unknowns/s on the octant "
+               "overstates the CPU's full-cube rate (work per unknown grows with N); the full config-2 oracle run measured once "
+               "is under full_config")
+
+
+def workload_config(config, schedule="reference", world=1):
+    from paper_1703_06155_b200.geometry import BASELINE_CONFIGS
+
+    c = BASELINE_CONFIGS[config]
+    n = c["cells"] ** 3
+    return {"workload": f"BASELINE config {config}: VIE dielectric cube {c['cells']}^3 = {n} unknowns, side {c['side']} lambda, eps_r 4, "
+                        f"leaf {c['leaf']}, eta 1, eps_h2 = eps_fill = {c['eps']}",
+            "n": n, "schedule": schedule, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (dense leaf blocks alone exceed 126 MB)"}
 
 
 def run_reference(args, rank):
@@ -149,9 +180,8 @@ def run_reference(args, rank):
         secs.append(ch.seconds)
     t = float(np.mean(secs))
     value = n / t
-    sample = (f"oracle/ (CPU restatement of proj/include/h2lu/factorization.hpp, 1 thread like the reference) "
-              f"factorizing BASELINE config 1 (16^3 VIE cube, leaf 32, eps 1e-4, N={n}) per step; "
-              f"config 2 on the CPU takes minutes, config 1 is the reference's CPU-runnable case")
+    cpu = {"value": value, "unit": "unknowns/s", "cores": oracle_threads(), "nproc": os.cpu_count(), "cpu_model": cpu_model(), "kind": "port",
+           "sample": SAMPLE_NOTE, "full_config": golden_cpu_reference(args.config)}
     return {
         "metric": "H2 factorization unknowns/s",
         "value": value,
@@ -166,8 +196,8 @@ def run_reference(args, rank):
         "vs_baseline": None,
         "dtype": "complex128",
         "data": "synthetic",
-        "config": {"workload": "BASELINE config 1 sample (see cpu_baseline.sample)", "n": n, "leaf": c["leaf"], "eps": c["eps"], "eta": 1.0},
-        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": 1, "kind": "port", "sample": sample},
+        "config": workload_config(args.config, args.schedule, args.gpus),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -264,7 +294,15 @@ def main():
     levels = ch.levels()
     residual = A.relative_residual(x, b)
     pts_tree = pts[perm]
-    sampled = sampled_dense_residual(pts_tree, (k0, scale, diag), x, b)
+    rows = np.sort(np.random.default_rng(1234).choice(n, size=min(4096, n), replace=False)).astype(np.int64)
+    sampled = h2g.sampled_dense_residual(pts_tree, h2g.helmholtz_kernel(k0, diag, scale), x, b, rows, ctx)
+    # cold symbolic plan: the first factorize of a new structure builds it on
+    # the host (outside the device factor time); later ones reuse it
+    ctx.clear_plans()
+    Acold = h2g.H2Matrix.upload(host, ctx)
+    chc = h2g.factorize(Acold, eps, schedule=args.schedule)
+    plan_cold_ms = max_over_ranks(chc.timing()["plan_ms"])
+    del chc, Acold
 
     # ---- end to end through the C ABI with host buffers
     e2e = None
@@ -281,21 +319,33 @@ def main():
             pinned = True
         except Exception:
             pinned = False
-        ts = []
-        for i in range(1 + args.steps):
-            t0 = time.perf_counter()
-            G = h2g.H2Matrix.upload(host, ctx)
-            ch2 = h2g.factorize(G, eps, schedule=args.schedule)
-            x2 = ch2.solve(b)
-            t1 = time.perf_counter()
-            del ch2, G
-            if i >= 1:
-                ts.append(t1 - t0)
-        sync_all()
-        te2e = max_over_ranks(float(np.mean(ts)))
+        def e2e_run(cold):
+            ts, plan = [], []
+            for i in range(1 + args.steps):
+                if cold:
+                    ctx.clear_plans()  # new structure every step: the host plan is built inside the timed region
+                t0 = time.perf_counter()
+                G = h2g.H2Matrix.upload(host, ctx)
+                ch2 = h2g.factorize(G, eps, schedule=args.schedule)
+                x2 = ch2.solve(b)
+                t1 = time.perf_counter()
+                plan.append(ch2.timing()["plan_ms"])
+                del ch2, G
+                if i >= 1:
+                    ts.append(t1 - t0)
+            sync_all()
+            return max_over_ranks(float(np.mean(ts))), float(np.mean(plan[1:])), x2
+
+        te2e, plan_e2e, x2 = e2e_run(cold=True)
+        twarm, plan_warm, _ = e2e_run(cold=False)
         e2e = {"value": n * world / te2e, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "s_per_step": te2e, "pinned_host": pinned, "timing": "wall clock around synchronous C-ABI calls, max over ranks",
-               "solution_matches_resident_run": bool(np.allclose(x2, x, rtol=0, atol=1e-12 * np.abs(x).max()))}
+               "s_per_step": te2e, "plan_ms_per_step": plan_e2e, "pinned_host": pinned,
+               "timing": "wall clock around synchronous C-ABI calls (upload from pinned host memory, symbolic plan built from scratch, "
+                         "factorize, solve, x read back), max over ranks",
+               "solution_matches_resident_run": bool(np.allclose(x2, x, rtol=0, atol=1e-12 * np.abs(x).max())),
+               "warm": {"value": n * world / twarm, "s_per_step": twarm, "plan_ms_per_step": plan_warm,
+                        "note": "same, with the symbolic plan reused from the context's structure-keyed cache (refactorization of the "
+                                "same geometry with new entries)"}}
 
     # ---- roofline of the dominant kernel class (separate profiled run)
     ctx.set_profiling(True)
@@ -314,13 +364,14 @@ def main():
     roof = None
     if sch["ms"] > 0:
         t_s = sch["ms"] / 1e3
-        tf = sch["flops"] / t_s / 1e12
-        gbs = sch["bytes"] / t_s / 1e9
-        t_flop = sch["flops"] / (peak_tf * 1e12)
-        t_mem = sch["bytes"] / (hbm * 1e9)
-        if t_flop >= t_mem:
+        exw = chp.work()
+        ex_flops, ex_bytes = exw["schur_flops_executed"], exw["schur_bytes_executed"]
+        tf = ex_flops / t_s / 1e12
+        gbs = ex_bytes / t_s / 1e9
+        nl = max(sch["launches"], 1)
+        if ex_flops / (peak_tf * 1e12) >= ex_bytes / (hbm * 1e9):
             roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": tf / peak_tf, "peak_source": peak_src + " (FP64 has no tcgen05 path; DFMA/DMMA peak)"}
+                    "frac": tf / peak_tf, "peak_source": peak_src + " (FP64 has no tcgen05 path; DMMA/DFMA peak)"}
         else:
             roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
@@ -333,25 +384,29 @@ def main():
                 continue
             if tj.get("config") == args.config and tj.get("launches") == sch["launches"]:
                 traffic, tsrc = tj["traffic_per_launch"], os.path.relpath(f, ROOT) + " (ncu dram__bytes_read+write per k_schur launch, same launch list)"
-        exw = chp.work()
-        roof.update({"executed_flops": exw["schur_flops_executed"], "executed_tflops": exw["schur_flops_executed"] / t_s / 1e12,
-                     "executed_bytes": exw["schur_bytes_executed"],
-                     "note": "achieved = SURVEY 8d algorithmic Schur flops (full b_j x e x b_c products, as the reference executes them) / "
-                             "k_schur event time; k_schur skips the rows/columns of clusters eliminated in an earlier batch (exact zeros), "
-                             "executed_tflops is the rate on the work actually done"})
-        roof.update({"traffic": traffic, "traffic_source": tsrc, "algorithmic_bytes_per_launch": sch["bytes"] / max(sch["launches"], 1),
-                     "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / max(sch["launches"], 1),
-                     "algorithmic_flops": sch["flops"], "algorithmic_bytes": sch["bytes"], "share_of_factorize": sch["ms"] / max(prof_total, 1e-9),
-                     "tflops": tf, "gbs": gbs})
+        roof.update({"basis": "executed work: the products k_schur computes (rows/columns of clusters eliminated in an earlier batch "
+                              "are exact zeros and are skipped, factorization.hpp:431-439); flops_per_launch x launches / k_schur event time",
+                     "flops_per_launch": ex_flops / nl, "bytes_per_launch": ex_bytes / nl,
+                     "traffic": traffic, "traffic_source": tsrc, "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / nl,
+                     "share_of_factorize": sch["ms"] / max(prof_total, 1e-9),
+                     "algorithmic": {"flops": sch["flops"], "tflops": sch["flops"] / t_s / 1e12, "frac": sch["flops"] / t_s / 1e12 / peak_tf,
+                                     "note": "SURVEY 8d count (full b_j x e x b_c products, as the reference's GEMMs execute them, "
+                                             "including the exact-zero rows/columns k_schur skips)"}})
+    solve_roof = None
+    if solve_ms > 0:
+        sgbs = work["solve_bytes"] / (solve_ms / 1e3) / 1e9
+        solve_roof = {"kernel": "solve (k_fwd_level / k_bwd_level, nrhs = 1)", "bound": "hbm", "achieved": sgbs, "peak": hbm, "unit": "GB/s",
+                      "frac": sgbs / hbm, "bytes": work["solve_bytes"],
+                      "basis": "chain bytes (Qtilde read twice, L11/U11/Lbar/Ubar, root triangles) + 4 x 16 x N vector traffic per solve "
+                               "/ device solve time"}
     breakdown = {k: {"ms": round(v["ms"], 3), "launches": v["launches"]} for k, v in stats.items()}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ao, co, O = cpu_oracle_sample()
         cho = Ao.factorize(co["eps"])
-        cpu = {"value": Ao.n / cho.seconds, "unit": "unknowns/s", "cores": 1, "kind": "port",
-               "sample": f"oracle/ restatement of the reference factorize, 1 thread, BASELINE config 1 (N={Ao.n}, {cho.seconds:.1f} s); "
-                         f"config 2 is minutes on one core, config 1 is the reference's CPU-runnable case"}
+        cpu = {"value": Ao.n / cho.seconds, "unit": "unknowns/s", "cores": oracle_threads(), "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+               "kind": "port", "sample": SAMPLE_NOTE + f" (this run: {cho.seconds:.2f} s)", "full_config": golden_cpu_reference(args.config)}
 
     out = {
         "metric": "H2 factorization unknowns/s",
@@ -366,10 +421,10 @@ def main():
         "vs_baseline": None,
         "dtype": "complex128",
         "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}: VIE dielectric cube {c['cells']}^3 = {n} unknowns, side {c['side']} lambda, eps_r 4, leaf {c['leaf']}, eta 1, eps_h2 = eps_fill = {eps}",
-                   "n": n, "schedule": args.schedule, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (dense leaf blocks alone exceed 126 MB)"},
+        "config": workload_config(args.config, args.schedule, world),
         "factor_ms": factor_ms,
+        "plan_ms_cold": plan_cold_ms,
+        "factor_ms_incl_cold_plan": factor_ms + plan_cold_ms,
         "solve_ms": solve_ms,
         "factor_tflops": work["factor_flops"] / (factor_ms / 1e3) / 1e12,
         "solve_gbs": work["solve_bytes"] / (solve_ms / 1e3) / 1e9 if solve_ms > 0 else None,
@@ -383,6 +438,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(np.mean(flaunch) + np.mean(slaunch)),
         "roofline": roof,
+        "solve_roofline": solve_roof,
         "kernel_breakdown_ms": breakdown,
         "cpu_baseline": cpu,
     }

@@ -140,6 +140,14 @@ int h2g_matrix_download(const h2g_matrix* m, int64_t* cluster_begin, int64_t* cl
 /* y = A x through the compressed operator (h2_matrix.hpp:80-137), host buffers, nrhs columns. */
 int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y, int32_t nrhs, h2g_error* err);
 
+/* y[q] = sum_j Z(rows[q], j) x[j] with Z generated directly from the kernel
+ * (the reference's assemble_block, kernel.hpp:64-102): the north_star's dense
+ * sampled-row residual computed on the device. points: n x 3
+ * row-major in TREE order; rows: tree indices; x: n x nrhs, y: nrows x nrhs,
+ * column-major interleaved complex128, host buffers. */
+int h2g_kernel_rows_matvec(h2g_context* ctx, const double* points_tree, int64_t n, const h2g_kernel_spec* kernel,
+                           const int64_t* rows, int64_t nrows, const double* x, double* y, int32_t nrhs, h2g_error* err);
+
 /* ---- hot path --------------------------------------------------------- */
 /* factorize(A, eps_fill_in, stop_level_override) (factorization.hpp:600-653).
  * stop_level < 0 means "default" (l0). */
@@ -176,6 +184,16 @@ uint64_t h2g_chain_hash(const h2g_chain* c);
 /* Device time (ms, CUDA events on the chain's stream) of the last factorize
  * and the last solve, and the number of kernels each launched. */
 int h2g_chain_timing(const h2g_chain* c, double* factor_ms, double* solve_ms, int64_t* factor_launches, int64_t* solve_launches);
+/* Host symbolic plan of the factorization (CSR neighbour lists, fill
+ * targets, Schur target lists, merge maps; it replaces the reference's
+ * whole-map scans, factorization.hpp:268-293): its build time for this chain
+ * (outside the device factor time of h2g_chain_timing) and whether it was
+ * built (1) or reused from the matrix / context plan cache (0). */
+int h2g_chain_plan(const h2g_chain* c, double* plan_ms, int32_t* built);
+/* Drop the context's structure-keyed plan cache (a later factorize of a new
+ * matrix handle then builds its plan from scratch: a cold-structure run). */
+int h2g_context_clear_plans(h2g_context* ctx);
+
 /* Per-kernel-class device timing of factorize (CUDA events around every
  * launch on the context stream; off by default). Classes: 0 complement,
  * 1 step-0 projection/Gram GEMMs, 2 column norms, 3 eig pass 1, 4 head,

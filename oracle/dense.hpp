@@ -25,6 +25,8 @@
 #include <utility>
 #include <vector>
 
+#include "pool.hpp"
+
 namespace h2o {
 
 using cxd = std::complex<double>;
@@ -157,6 +159,17 @@ struct Mat {
   }
 };
 
+// Summation-order switch for the oracle self-noise study (H2O_GEMM_ORDER=reverse
+// accumulates the inner dimension last-to-first, as a differently blocked BLAS
+// would): the same algorithm with rounding-level differences. Default: forward.
+inline bool gemm_reverse_k() {
+  static const bool rev = [] {
+    const char* e = std::getenv("H2O_GEMM_ORDER");
+    return e && std::string(e) == "reverse";
+  }();
+  return rev;
+}
+
 // C += alpha * A * B (all column-major, plain). A and C are split into real
 // and imaginary planes so the inner loops are pure FMA streams, and four
 // columns of C share every load of A.
@@ -166,12 +179,14 @@ inline void gemm_acc(Mat& C, const Mat& A, const Mat& B, double alpha = 1.0) {
   if (m == 0 || n == 0 || k == 0) return;
   std::vector<double> ar(static_cast<size_t>(m * k)), ai(static_cast<size_t>(m * k));
   for (Index q = 0; q < m * k; ++q) ar[static_cast<size_t>(q)] = A.d[static_cast<size_t>(q)].real(), ai[static_cast<size_t>(q)] = A.d[static_cast<size_t>(q)].imag();
-  std::vector<double> cr(static_cast<size_t>(m * 4)), ci(static_cast<size_t>(m * 4));
-  for (Index j0 = 0; j0 < n; j0 += 4) {
+  // Each group of four C columns is computed start to finish by one thread,
+  // so the arithmetic is the same for any thread count.
+  const bool reverse_k = gemm_reverse_k();
+  auto panel = [&](Index j0) {
+    std::vector<double> cr(static_cast<size_t>(m * 4), 0.0), ci(static_cast<size_t>(m * 4), 0.0);
     const Index nj = std::min<Index>(4, n - j0);
-    std::fill(cr.begin(), cr.end(), 0.0);
-    std::fill(ci.begin(), ci.end(), 0.0);
-    for (Index p = 0; p < k; ++p) {
+    for (Index pp = 0; pp < k; ++pp) {
+      const Index p = reverse_k ? k - 1 - pp : pp;
       const double* xr = ar.data() + p * m;
       const double* xi = ai.data() + p * m;
       for (Index jj = 0; jj < nj; ++jj) {
@@ -190,6 +205,12 @@ inline void gemm_acc(Mat& C, const Mat& A, const Mat& B, double alpha = 1.0) {
       cxd* cj = C.col(j0 + jj);
       for (Index i = 0; i < m; ++i) cj[i] += alpha * cxd(cr[static_cast<size_t>(jj * m + i)], ci[static_cast<size_t>(jj * m + i)]);
     }
+  };
+  const Index groups = (n + 3) / 4;
+  if (groups > 1 && m * n * k >= (Index(1) << 20)) {
+    pool_for(groups, [&](int64_t g) { panel(static_cast<Index>(g) * 4); });
+  } else {
+    for (Index g = 0; g < groups; ++g) panel(g * 4);
   }
 }
 
@@ -230,13 +251,19 @@ inline Reflector make_householder(cxd* x, Index m) {
 // A[row0.., col0..col1) = (I - tau v v^H) A, v = [1; ess], len = #rows.
 inline void apply_householder_left(Mat& A, Index row0, Index col0, Index col1, const cxd* ess, Index len, cxd tau) {
   if (tau == cxd(0.0)) return;
-  for (Index j = col0; j < col1; ++j) {
+  auto one = [&](Index j) {
     cxd* a = A.col(j) + row0;
     cxd t = a[0];
     for (Index i = 1; i < len; ++i) t += std::conj(ess[i - 1]) * a[i];
     t *= tau;
     a[0] -= t;
     for (Index i = 1; i < len; ++i) a[i] -= ess[i - 1] * t;
+  };
+  // columns are independent: one thread per column, serial arithmetic
+  if ((col1 - col0) > 1 && (col1 - col0) * len >= (Index(1) << 16)) {
+    pool_for(col1 - col0, [&](int64_t j) { one(col0 + static_cast<Index>(j)); });
+  } else {
+    for (Index j = col0; j < col1; ++j) one(j);
   }
 }
 

@@ -358,19 +358,29 @@ inline const Mat& step1_projection(FactorState& st, int i) {
 // Step 2 (factorization.hpp:344-350).
 inline void step2_apply_projection(FactorState& st, int i, const Mat& Q) {
   const Mat QH = Q.adjoint(), Qc = Q.conjugate();
-  for (const Key& key : st.dense.touching(i)) {
-    Mat& D = st.dense.at(key.first, key.second);
-    if (key.first == i) D = mul(QH, D);
-    if (key.second == i) D = mul(D, Qc);
-  }
+  const auto keys = st.dense.touching(i);
+  std::vector<Mat*> blocks;
+  for (const Key& key : keys) blocks.push_back(&st.dense.at(key.first, key.second));
+  pool_for(static_cast<int64_t>(keys.size()), [&](int64_t q) {  // distinct blocks
+    Mat& D = *blocks[static_cast<size_t>(q)];
+    if (keys[static_cast<size_t>(q)].first == i) D = mul(QH, D);
+    if (keys[static_cast<size_t>(q)].second == i) D = mul(D, Qc);
+  });
   st.rotated[static_cast<size_t>(i)] = 1;
 }
 
-// deposit_fill (factorization.hpp:359-366).
-inline void deposit_fill(FactorState& st, int j, int k, Mat F) {
+// deposit_fill (factorization.hpp:359-366): the lift of a rotated side ...
+inline Mat lift_fill(const FactorState& st, int j, int k, Mat F) {
   const size_t uj = static_cast<size_t>(j), uk = static_cast<size_t>(k);
   if (st.rotated[uj]) F = mul(st.basis[uj], F.bottom_rows(st.kfin[uj]));
   if (st.rotated[uk]) F = mul(F.right_cols(st.kfin[uk]), st.basis[uk].transpose());
+  return F;
+}
+
+// ... and the accumulation into the ledger (admissible at this level) or the
+// carried map.
+inline void deposit_fill(FactorState& st, int j, int k, Mat F) {
+  F = lift_fill(st, j, k, std::move(F));
   BlockMap& target = contains_pair(st.A->blocks->admissible[static_cast<size_t>(st.level)], j, k) ? st.ledger : st.carried;
   target.accumulate(j, k, F);
 }
@@ -405,20 +415,41 @@ inline void step3_partial_eliminate(FactorState& st, int i) {
     cols.emplace_back(i, solve_unit_lower(rec.L11, Dii.block(0, e, e, k)));
     rows.emplace_back(i, solve_right_upper(Dii.block(e, 0, k, e), rec.U11));
   }
-  for (const auto& rj : rows) {
-    for (const auto& cc : cols) {
-      Mat* T = st.dense.find(rj.first, cc.first);
-      if (T) {
-        const Index ro = rj.first == i ? e : 0, co = cc.first == i ? e : 0;
-        Mat P = mul(rj.second, cc.second);
-        T->add_block(ro, co, P, -1.0);
-      } else {
-        Mat P = mul(rj.second, cc.second);
-        for (cxd& v : P.d) v = -v;
-        deposit_fill(st, rj.first, cc.first, std::move(P));
+  // Every (row, column) pair is a distinct target, so the products run in
+  // parallel; the fill slots are created first (serially, in map order) and
+  // each receives exactly one contribution from this cluster.
+  const size_t nr = rows.size(), nc = cols.size();
+  std::vector<Mat*> dense_t(nr * nc, nullptr), fill_t(nr * nc, nullptr);
+  std::vector<char> fresh(nr * nc, 0);
+  for (size_t a = 0; a < nr; ++a)
+    for (size_t c = 0; c < nc; ++c) {
+      const int j = rows[a].first, x = cols[c].first;
+      if (Mat* T = st.dense.find(j, x)) {
+        dense_t[a * nc + c] = T;
+        continue;
       }
+      BlockMap& target = contains_pair(st.A->blocks->admissible[static_cast<size_t>(st.level)], j, x) ? st.ledger : st.carried;
+      Mat* slot = target.find(j, x);
+      if (!slot) slot = &target.put(j, x, Mat()), fresh[a * nc + c] = 1;
+      fill_t[a * nc + c] = slot;
     }
-  }
+  pool_for(static_cast<int64_t>(nr * nc), [&](int64_t q) {
+    const size_t a = static_cast<size_t>(q) / nc, c = static_cast<size_t>(q) % nc;
+    const auto& rj = rows[a];
+    const auto& cc = cols[c];
+    Mat P = mul(rj.second, cc.second);
+    if (Mat* T = dense_t[static_cast<size_t>(q)]) {
+      const Index ro = rj.first == i ? e : 0, co = cc.first == i ? e : 0;
+      T->add_block(ro, co, P, -1.0);
+      return;
+    }
+    for (cxd& v : P.d) v = -v;
+    Mat F = lift_fill(st, rj.first, cc.first, std::move(P));
+    if (fresh[static_cast<size_t>(q)])
+      *fill_t[static_cast<size_t>(q)] = std::move(F);
+    else
+      *fill_t[static_cast<size_t>(q)] += F;
+  });
   rec.fill_targets = static_cast<Index>(rows.size() * cols.size());
   for (auto& rj : rows) rec.Lbar.push_back({st.pos[static_cast<size_t>(rj.first)] + (rj.first == i ? e : 0), std::move(rj.second)});
   for (auto& cc : cols) rec.Ubar.push_back({st.pos[static_cast<size_t>(cc.first)] + (cc.first == i ? e : 0), std::move(cc.second)});
@@ -439,16 +470,19 @@ inline void finish_level(FactorState& st) {
   const auto& adm = st.A->blocks->admissible[static_cast<size_t>(st.level)];
   const auto& coup = st.A->couplings[static_cast<size_t>(st.level)];
   size_t absorbed = 0;
-  for (size_t q = 0; q < adm.size(); ++q) {
+  std::vector<Mat> sfs(adm.size());
+  pool_for(static_cast<int64_t>(adm.size()), [&](int64_t qq) {
+    const size_t q = static_cast<size_t>(qq);
     const int t = adm[q].row, s = adm[q].col;
     const size_t ut = static_cast<size_t>(t), us = static_cast<size_t>(s);
     Mat sf(st.kfin[ut], st.kfin[us]);
     sf.set_block(0, 0, coup[q]);
-    if (const Mat* F = st.ledger.find(t, s)) {
-      sf += mul(mul(st.basis[ut].adjoint(), *F), st.basis[us].conjugate());
-      ++absorbed;
-    }
-    st.final_coupling.put(t, s, std::move(sf));
+    if (const Mat* F = st.ledger.find(t, s)) sf += mul(mul(st.basis[ut].adjoint(), *F), st.basis[us].conjugate());
+    sfs[q] = std::move(sf);
+  });
+  for (size_t q = 0; q < adm.size(); ++q) {
+    if (st.ledger.find(adm[q].row, adm[q].col)) ++absorbed;
+    st.final_coupling.put(adm[q].row, adm[q].col, std::move(sfs[q]));
   }
   if (absorbed != st.ledger.size()) throw InvalidInputError("finish_level: ledger holds a key that is not admissible at this level");
   st.ledger.clear();
@@ -517,10 +551,19 @@ inline void merge_permute(FactorState& st) {
   }
 
   BlockMap moved;
-  for (const auto& kv : st.carried.m) {
+  std::vector<const std::pair<const Key, Mat>*> items;
+  for (const auto& kv : st.carried.m) items.push_back(&kv);
+  std::vector<Mat> projs(items.size());
+  pool_for(static_cast<int64_t>(items.size()), [&](int64_t q) {
+    const auto& kv = *items[static_cast<size_t>(q)];
+    projs[static_cast<size_t>(q)] =
+        mul(mul(st.basis[static_cast<size_t>(kv.first.first)].adjoint(), kv.second), st.basis[static_cast<size_t>(kv.first.second)].conjugate());
+  });
+  for (size_t q = 0; q < items.size(); ++q) {
+    const auto& kv = *items[q];
     const int j = kv.first.first, c = kv.first.second;
     const int pj = T.cluster(j).parent, pc = T.cluster(c).parent;
-    Mat proj = mul(mul(st.basis[static_cast<size_t>(j)].adjoint(), kv.second), st.basis[static_cast<size_t>(c)].conjugate());
+    const Mat& proj = projs[q];
     const Cluster& cpj = T.cluster(pj);
     const Cluster& cpc = T.cluster(pc);
     const Index ro = j == cpj.children[0] ? 0 : kf(cpj.children[0]);

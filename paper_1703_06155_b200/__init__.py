@@ -136,6 +136,7 @@ SYMBOLS = {
     "h2g_matrix_sizes": (C.c_int, [_P, _I64]),
     "h2g_matrix_download": (C.c_int, [_P, _I64, _I64, _I64, _I64, _I32, _I64, _I32, _I32, _I64, _I64, _I64, _D, _I64, _D, _I64, _D]),
     "h2g_matvec": (C.c_int, [_P, _P, _D, _D, C.c_int32, C.POINTER(_Err)]),
+    "h2g_kernel_rows_matvec": (C.c_int, [_P, _D, C.c_int64, C.POINTER(_Kernel), _I64, C.c_int64, _D, _D, C.c_int32, C.POINTER(_Err)]),
     "h2g_factorize": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_int32, C.POINTER(_P), C.POINTER(_Err)]),
     "h2g_chain_destroy": (C.c_int, [_P]),
     "h2g_solve": (C.c_int, [_P, _D, _D, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_Err)]),
@@ -154,6 +155,8 @@ SYMBOLS = {
     "h2g_chain_schur_executed": (C.c_int, [_P, _D]),
     "h2g_random_rhs": (None, [C.c_int64, C.c_uint64, _D]),
     "h2g_set_profiling": (C.c_int, [_P, C.c_int32]),
+    "h2g_chain_plan": (C.c_int, [_P, _D, _I32]),
+    "h2g_context_clear_plans": (C.c_int, [_P]),
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
 }
 
@@ -213,6 +216,11 @@ class Context:
 
     def set_profiling(self, on=True):
         lib().h2g_set_profiling(self.h, 1 if on else 0)
+
+    def clear_plans(self):
+        """Forget the structure-keyed plan cache (next factorize of a new
+        matrix builds its symbolic plan from scratch)."""
+        lib().h2g_context_clear_plans(self.h)
 
     @classmethod
     def default(cls, device=0):
@@ -277,18 +285,30 @@ class H2Matrix:
         """From host arrays in the include/h2g.h layout (keys as exported by
         oracle/pyoracle.H2.export() plus the tree/partition arrays)."""
         ctx = ctx or Context.default()
-        a = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
-        keep = a  # keep buffers alive during the call
+        # every array converted to the dtype the C ABI reads; the converted
+        # arrays stay referenced by `a` until h2g_matrix_upload returns
+        i64 = ("cluster_begin", "cluster_end", "adm_offsets", "split_offsets", "basis_rows", "basis_rank", "basis_offset",
+               "coupling_offset", "dense_offset")
+        i32 = ("adm_pairs", "split_pairs", "leaf_pairs")
+        cpx = ("basis_data", "coupling_data", "dense_data")
+        a = {}
+        for k in i64:
+            a[k] = np.ascontiguousarray(arrays[k], dtype=np.int64)
+        for k in i32:
+            a[k] = np.ascontiguousarray(np.asarray(arrays[k]).reshape(-1, 2), dtype=np.int32)
+        for k in cpx:
+            a[k] = np.ascontiguousarray(arrays[k], dtype=np.complex128)
         d = _Desc()
+
         def scalar(v):
             return np.asarray(v).reshape(-1)[0]
 
-        d.n = int(scalar(a["n"]))
-        d.depth = int(scalar(a["depth"]))
-        d.eta = float(scalar(a.get("eta", 1.0)))
-        d.eps_h2 = float(scalar(a.get("eps_h2", 0.0)))
-        d.cluster_begin = _i64(a["cluster_begin"].astype(np.int64, copy=False))
-        d.cluster_end = _i64(a["cluster_end"].astype(np.int64, copy=False))
+        d.n = int(scalar(arrays["n"]))
+        d.depth = int(scalar(arrays["depth"]))
+        d.eta = float(scalar(arrays.get("eta", 1.0)))
+        d.eps_h2 = float(scalar(arrays.get("eps_h2", 0.0)))
+        d.cluster_begin = _i64(a["cluster_begin"])
+        d.cluster_end = _i64(a["cluster_end"])
         d.adm_offsets = _i64(a["adm_offsets"])
         d.adm_pairs = _i32(a["adm_pairs"])
         d.split_offsets = _i64(a["split_offsets"])
@@ -306,7 +326,7 @@ class H2Matrix:
         err = _Err()
         h = _P()
         rc = lib().h2g_matrix_upload(ctx.h, C.byref(d), C.byref(h), C.byref(err))
-        del keep
+        del a
         _check(rc, err)
         return cls(h, ctx)
 
@@ -371,6 +391,31 @@ class H2Matrix:
         if nb == 0.0:
             raise UndefinedMetricError("relative_residual: right-hand side is zero")
         return float(np.linalg.norm(self.matvec(x) - b) / nb)
+
+
+def kernel_rows_matvec(points_tree, kernel, rows, x, ctx=None):
+    """(Z x)[rows] with Z generated from the kernel on the device: the dense
+    sampled-row residual of SURVEY §8d(ii). points_tree: n x 3 in tree order;
+    rows: tree indices; x: tree order (n or n x nrhs)."""
+    ctx = ctx or Context.default()
+    pts = np.ascontiguousarray(points_tree, dtype=np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    x = np.asarray(x, dtype=np.complex128)
+    nrhs = 1 if x.ndim == 1 else x.shape[1]
+    xf = np.asfortranarray(x.reshape(n, nrhs))
+    y = np.zeros((rows.size, nrhs), np.complex128, order="F")
+    err = _Err()
+    kc = kernel.c()
+    _check(lib().h2g_kernel_rows_matvec(ctx.h, _d(pts), n, C.byref(kc), _i64(rows), rows.size, xf.ctypes.data_as(_D), y.ctypes.data_as(_D),
+                                        nrhs, C.byref(err)), err)
+    return y[:, 0].copy() if x.ndim == 1 else y
+
+
+def sampled_dense_residual(points_tree, kernel, x, b, rows, ctx=None):
+    """||(Z x - b)[rows]|| / ||b[rows]|| on the device."""
+    zx = kernel_rows_matvec(points_tree, kernel, rows, x, ctx)
+    return float(np.linalg.norm(zx - b[rows]) / np.linalg.norm(b[rows]))
 
 
 REC_FIELDS = ("cluster", "level", "pos", "bsize", "eliminated", "rank_before", "rank_after", "fill_targets", "n_lbar", "n_ubar")
@@ -470,7 +515,10 @@ class FactorChain:
         f, s = C.c_double(), C.c_double()
         fl, sl = C.c_int64(), C.c_int64()
         lib().h2g_chain_timing(self.h, C.byref(f), C.byref(s), C.byref(fl), C.byref(sl))
-        return dict(factor_ms=f.value, solve_ms=s.value, factor_launches=fl.value, solve_launches=sl.value)
+        pm, built = C.c_double(), C.c_int32()
+        lib().h2g_chain_plan(self.h, C.byref(pm), C.byref(built))
+        return dict(factor_ms=f.value, solve_ms=s.value, factor_launches=fl.value, solve_launches=sl.value, plan_ms=pm.value,
+                    plan_built=bool(built.value))
 
     KERNEL_CLASSES = ("complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other", "eigvec", "eig1b")
 

@@ -6,6 +6,7 @@
 // to the parent (finish_level :445-475, merge_permute :483-584) with
 // descriptor-driven batched copies/GEMMs; the remainder is LU-factored on the
 // device (:637-651). There is no CPU fallback.
+#include <atomic>
 #include <functional>
 #include <cuda_runtime.h>
 
@@ -102,43 +103,62 @@ class BlockCache {
     const size_t g = n < (1u << 20) ? 512 : (2u << 20);
     return (n + g - 1) / g * g;
   }
-  void add_stream(cudaStream_t s) {
+  void add_stream(cudaStream_t s, int device) {
     std::lock_guard<std::mutex> g(mu_);
-    live_.insert(s);
+    live_[s] = device;
   }
   void remove_stream(cudaStream_t s) {
     std::lock_guard<std::mutex> g(mu_);
-    live_.erase(s);
     auto& fl = free_[s];
-    for (auto& kv : fl) cudaFree(kv.second), cached_ -= kv.first;
+    const int dev = live_.count(s) ? live_[s] : -1;
+    for (auto& kv : fl) cudaFree(kv.second), cached_[dev] -= kv.first;
     free_.erase(s);
+    live_.erase(s);
+    spill_.erase(s);
+  }
+  // Out-of-memory hook of the factorization running on stream s (moves
+  // finished chain levels to host memory); one per stream / context, so two
+  // contexts never call each other's hook.
+  void set_spill(cudaStream_t s, std::function<bool()> f) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (f)
+      spill_[s] = std::move(f);
+    else
+      spill_.erase(s);
   }
   void* alloc(size_t n, cudaStream_t s) {
     const size_t r = round(n);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::function<bool()> spill;
     {
       std::lock_guard<std::mutex> g(mu_);
-      if (live_.count(s)) {
+      auto lv = live_.find(s);
+      if (lv != live_.end()) {
+        dev = lv->second;
         auto& fl = free_[s];
         auto it = fl.lower_bound(r);
         if (it != fl.end() && it->first <= r + r / 4 + (4u << 20)) {
           void* p = it->second;
-          cached_ -= it->first;
+          cached_[dev] -= it->first;
           fl.erase(it);
           return p;
         }
       }
+      auto sp = spill_.find(s);
+      if (sp != spill_.end()) spill = sp->second;
     }
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, r, s);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
-      trim();
+      trim(dev);
       e = cudaMallocAsync(&p, r, s);
-      // still short: let the running factorization move finished chain
-      // levels to host memory, one at a time
+      // still short: let the factorization on this stream move finished
+      // chain levels to host memory, one at a time
       while (e == cudaErrorMemoryAllocation && spill && spill()) {
         cudaGetLastError();
-        trim();
+        trim(dev);
         e = cudaMallocAsync(&p, r, s);
       }
     }
@@ -150,9 +170,10 @@ class BlockCache {
   void release(void* p, cudaStream_t s) {
     std::lock_guard<std::mutex> g(mu_);
     auto it = size_.find(p);
-    if (it != size_.end() && live_.count(s)) {
+    auto lv = live_.find(s);
+    if (it != size_.end() && lv != live_.end()) {
       free_[s].emplace(it->second, p);
-      cached_ += it->second;
+      cached_[lv->second] += it->second;
       return;
     }
     if (it != size_.end()) size_.erase(it);
@@ -161,48 +182,54 @@ class BlockCache {
     else
       cudaFreeAsync(p, s);
   }
-  // hand every cached block back to the driver (out-of-memory retry)
-  void trim() {
+  // hand the cached blocks of one device back to the driver (out-of-memory retry)
+  void trim(int dev) {
     std::lock_guard<std::mutex> g(mu_);
     for (auto& fs : free_) {
+      auto lv = live_.find(fs.first);
+      if (lv == live_.end() || lv->second != dev) continue;
       for (auto& kv : fs.second) {
         size_.erase(kv.second);
-        cached_ -= kv.first;
+        cached_[dev] -= kv.first;
         cudaFreeAsync(kv.second, fs.first);
       }
       fs.second.clear();
       cudaStreamSynchronize(fs.first);
     }
     // and the pool's own reserve (release threshold is "keep everything")
-    int dev = 0;
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
+  void trim() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    trim(dev);
   }
 
-  // device bytes a new allocation can still obtain: driver-free memory, the
-  // pool's reserve and the blocks parked in this cache
+  // device bytes a new allocation on the current device can still obtain:
+  // driver-free memory, the pool's reserve and this device's cached blocks
   size_t headroom() {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     size_t pool_spare = 0;
     int dev = 0;
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t res = 0, used = 0;
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
       pool_spare = res > used ? res - used : 0;
     }
     std::lock_guard<std::mutex> g(mu_);
-    return fr + pool_spare + cached_;
+    return fr + pool_spare + cached_[dev];
   }
-
-  std::function<bool()> spill;  // set by h2g_factorize while it runs
 
  private:
   std::mutex mu_;
-  size_t cached_ = 0;
-  std::set<cudaStream_t> live_;
+  std::map<int, size_t> cached_;           // per device
+  std::map<cudaStream_t, int> live_;       // stream -> device
+  std::map<cudaStream_t, std::function<bool()>> spill_;
   std::map<cudaStream_t, std::multimap<size_t, void*>> free_;
   std::unordered_map<void*, size_t> size_;
 };
@@ -330,6 +357,7 @@ enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SC
 
 struct PlanCache {
   int stop = 0, schedule = 0;
+  Structure key;  // the structure the plan was built for (checked on a fingerprint hit)
   std::vector<LevelSym> levels;
   std::vector<LevelSchedule> sched;
   std::vector<LevelWork> work;
@@ -337,6 +365,13 @@ struct PlanCache {
 
 struct h2g_context {
   int device = 0;
+  // Matrices and chains hold a reference: h2g_context_destroy only drops the
+  // caller's, the context is torn down when the last user is gone (a chain
+  // may outlive the handle it was factorized with).
+  std::atomic<int> refs{1};
+  // one factorize / solve at a time per context (they share its streams,
+  // events and profiling state)
+  std::recursive_mutex run_mu;
   // symbolic plans keyed by a fingerprint of the block structure, stop level
   // and schedule: a new matrix with the structure of an earlier one (same
   // geometry, new entries) reuses the plan (the two most recent are kept)
@@ -412,6 +447,8 @@ struct h2g_chain {
   DBuf ybuf, tmpbuf, partbuf;
   size_t storage_bytes = 0;
   double factor_ms = 0.0, solve_ms = 0.0;
+  double plan_ms = 0.0;     // host symbolic plan (get_plan), outside factor_ms
+  bool plan_built = false;  // false: reused from the matrix / context plan cache
   long long factor_launches = 0, solve_launches = 0;
   double factor_flops = 0.0, schur_flops = 0.0, solve_bytes = 0.0, schur_bytes = 0.0;
   double schur_flops_exec = 0.0, schur_bytes_exec = 0.0;  // k_schur work after the exact-zero skip
@@ -474,7 +511,27 @@ uint64_t structure_fingerprint(const Structure& S, int stop, int schedule) {
   return h;
 }
 
-PlanCache* get_plan(h2g_matrix* M, int stop, int schedule) {
+bool same_pairs(const std::vector<Pair>& a, const std::vector<Pair>& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i)
+    if (a[i].row != b[i].row || a[i].col != b[i].col) return false;
+  return true;
+}
+
+// Full structural equality behind the 64-bit fingerprint: a plan is only
+// reused for an identical tree and partition.
+bool same_structure(const Structure& a, const Structure& b) {
+  if (a.n != b.n || a.depth != b.depth || a.eta != b.eta || a.l0 != b.l0 || a.begin != b.begin || a.end != b.end) return false;
+  if (a.adm.size() != b.adm.size() || a.split.size() != b.split.size() || !same_pairs(a.leaf, b.leaf)) return false;
+  for (size_t l = 0; l < a.adm.size(); ++l)
+    if (!same_pairs(a.adm[l], b.adm[l])) return false;
+  for (size_t l = 0; l < a.split.size(); ++l)
+    if (!same_pairs(a.split[l], b.split[l])) return false;
+  return true;
+}
+
+PlanCache* get_plan(h2g_matrix* M, int stop, int schedule, bool* built) {
+  *built = false;
   std::lock_guard<std::mutex> g(M->mu);
   for (auto& p : M->plans)
     if (p->stop == stop && p->schedule == schedule) return p.get();
@@ -482,12 +539,14 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule) {
   {
     std::lock_guard<std::mutex> g2(M->ctx->plan_mu);
     for (auto& e : M->ctx->plan_lru)
-      if (e.first == fp && e.second->stop == stop && e.second->schedule == schedule) {
+      if (e.first == fp && e.second->stop == stop && e.second->schedule == schedule && same_structure(e.second->key, M->S)) {
         M->plans.push_back(e.second);
         return M->plans.back().get();
       }
   }
+  *built = true;
   auto P = std::make_shared<PlanCache>();
+  P->key = M->S;
   P->stop = stop;
   P->schedule = schedule;
   P->levels = build_levels(M->S, stop);
@@ -589,7 +648,7 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_hi));
     CK(cudaEventCreateWithFlags(&c->ev_aux0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_aux1, cudaEventDisableTiming));
-    BlockCache::get().add_stream(c->stream);
+    BlockCache::get().add_stream(c->stream, device);
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaMalloc(&c->d_err, sizeof(DevError)));
@@ -604,8 +663,9 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
   });
 }
 
-int h2g_context_destroy(h2g_context* ctx) {
-  if (!ctx) return H2G_OK;
+}  // extern "C"
+
+static void context_teardown(h2g_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->side);
   cudaStreamSynchronize(ctx->stream);
@@ -623,6 +683,16 @@ int h2g_context_destroy(h2g_context* ctx) {
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+static void context_release(h2g_context* ctx) {
+  if (ctx && --ctx->refs == 0) context_teardown(ctx);
+}
+
+extern "C" {
+
+int h2g_context_destroy(h2g_context* ctx) {
+  context_release(ctx);
   return H2G_OK;
 }
 
@@ -665,6 +735,7 @@ int h2g_matrix_upload(h2g_context* ctx, const h2g_matrix_desc* d, h2g_matrix** o
     if (M->coup_elems) CK(cudaMemcpyAsync(M->coup.p, d->coupling_data, M->coup_elems * 16, cudaMemcpyHostToDevice, s));
     if (M->dense_elems) CK(cudaMemcpyAsync(M->dense.p, d->dense_data, M->dense_elems * 16, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
+    ++ctx->refs;  // the matrix holds the context
     *out = M.release();
   });
 }
@@ -694,14 +765,17 @@ int h2g_matrix_build(h2g_context* ctx, const double* points, int64_t n, int64_t 
     M->coup.s = ctx->stream;
     M->dense.p = R.dense;
     M->dense.s = ctx->stream;
+    ++ctx->refs;  // the matrix holds the context
     *out = M.release();
   });
 }
 
 int h2g_matrix_destroy(h2g_matrix* m) {
   if (!m) return H2G_OK;
-  cudaSetDevice(m->ctx->device);
+  h2g_context* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
   delete m;
+  context_release(ctx);
   return H2G_OK;
 }
 
@@ -771,12 +845,23 @@ int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y
   });
 }
 
+int h2g_kernel_rows_matvec(h2g_context* ctx, const double* points_tree, int64_t n, const h2g_kernel_spec* kernel, const int64_t* rows,
+                           int64_t nrows, const double* x, double* y, int32_t nrhs, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !points_tree || !kernel || (nrows && (!rows || !y)) || !x || n < 1 || nrows < 0 || nrhs < 1)
+      throw Error(H2G_ERR_INVALID_INPUT, "kernel_rows_matvec: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    kernel_rows_matvec_device(points_tree, n, *kernel, rows, nrows, x, y, nrhs, ctx->stream);
+  });
+}
+
 // ------------------------------------------------------------- factorize
 int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t stop_level, int32_t schedule, h2g_chain** out, h2g_error* err) {
   return guarded(err, [&] {
     if (!ctx || !mc || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
     if (!(eps > 0.0)) throw Error(H2G_ERR_INVALID_INPUT, "factorize: eps_fill_in must be positive");
     if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED) throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
+    std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);
     CK(cudaSetDevice(ctx->device));
     h2g_matrix* M = const_cast<h2g_matrix*>(mc);
     const Structure& S = M->S;
@@ -789,9 +874,10 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     }
     cudaStream_t st = ctx->stream;
     const auto tp0 = std::chrono::steady_clock::now();
-    PlanCache* P = get_plan(M, stop, schedule);
-    if (std::getenv("H2G_VERBOSE"))
-      std::fprintf(stderr, "[h2g] plan %.3f s\n", std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
+    bool plan_built = false;
+    PlanCache* P = get_plan(M, stop, schedule, &plan_built);
+    const double plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
+    if (std::getenv("H2G_VERBOSE")) std::fprintf(stderr, "[h2g] plan %.3f s (%s)\n", plan_s, plan_built ? "built" : "cached");
 
     auto C = std::make_unique<h2g_chain>();
     C->ctx = ctx;
@@ -800,6 +886,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->schedule = schedule;
     C->depth = L;
     C->eps = eps;
+    C->plan_ms = plan_s * 1e3;
+    C->plan_built = plan_built;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), st));
     ctx->prof.reset();
     ctx->prof_side.reset();
@@ -862,8 +950,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       X.sl.chain = X.harena.as<cplx>();
     };
     struct SpillGuard {
-      ~SpillGuard() { BlockCache::get().spill = nullptr; }
-    } spill_guard;
+      cudaStream_t s;
+      ~SpillGuard() { BlockCache::get().set_spill(s, nullptr); }
+    } spill_guard{st};
     // the input's dense blocks are only read at the leaf-level entry (and by
     // the matvec); they are the second thing to leave HBM
     auto offload_dense = [&]() -> bool {
@@ -874,14 +963,14 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       M->dense.release();
       return true;
     };
-    BlockCache::get().spill = [&]() -> bool {
+    BlockCache::get().set_spill(st, [&]() -> bool {
       for (auto& X : C->levels)
         if (X->arena.p) {
           offload_chain(*X);
           return true;
         }
       return offload_dense();
-    };
+    });
     auto ensure = [&](size_t need, ChainLevelHost* extra) {
       if (BlockCache::get().headroom() >= need + kMargin) return;
       CK(cudaStreamSynchronize(st));
@@ -1096,8 +1185,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
         // step-0 eigensolver workspace (per batch slot)
         mark("gram descriptors built");
-        DBuf eigws;
+        DBuf eigws, scratch;
         eigws.alloc((size_t)mb * eig1_ws_bytes(bm), st);
+        scratch.alloc(level_scratch_bytes(nl, bm, mb), st);
         // step 2/3b panels as descriptor GEMMs (device-resolved e = b - kfin):
         // column item D(t,c): T = Qt^H D, Ubar = L11^{-1} T[:e,:], lift = Ubar Qt_c^T, D = T (rows < e zeroed)
         // row item    D(j,t): T = D conj(Qt), Lbar = T[:,:e] U11^{-1}, lift = Qt_j Lbar, D = T (cols < e zeroed)
@@ -1177,6 +1267,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         DL.err = ctx->d_err;
         DL.debug = std::getenv("H2G_DEBUG") ? std::atoi(std::getenv("H2G_DEBUG")) : 0;
         DL.eigws = eigws.as<cplx>();
+        DL.scratch = scratch.as<cplx>();
+        DL.scratch_bytes = scratch.bytes;
 
         {
           cplx* chainb = CL->arena.as<cplx>();
@@ -1340,6 +1432,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         dirbuf.release();
         rotbuf.release();
         eigws.release();
+        scratch.release();
         const double sflops_lv0 = sflops, flops_lv0 = flops;
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
@@ -1905,15 +1998,18 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->schur_bytes = sbytes;
     C->kflops[PC_SCHUR] = sflops;
     C->kbytes[PC_SCHUR] = sbytes;
+    ++ctx->refs;  // the chain holds the context
     *out = C.release();
   });
 }
 
 int h2g_chain_destroy(h2g_chain* c) {
   if (!c) return H2G_OK;
-  cudaSetDevice(c->ctx->device);
-  cudaStreamSynchronize(c->ctx->stream);
+  h2g_context* ctx = c->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
   delete c;
+  context_release(ctx);
   return H2G_OK;
 }
 
@@ -1990,6 +2086,7 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
 int h2g_solve_device(h2g_chain* c, double* x_dev, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err) {
   return guarded(err, [&] {
     if (!c || !x_dev) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    std::lock_guard<std::recursive_mutex> run_lock(c->ctx->run_mu);
     CK(cudaSetDevice(c->ctx->device));
     solve_device_impl(c, reinterpret_cast<cplx*>(x_dev), n, nrhs, mode);
   });
@@ -1998,6 +2095,7 @@ int h2g_solve_device(h2g_chain* c, double* x_dev, int64_t n, int32_t nrhs, int32
 int h2g_solve(h2g_chain* c, const double* b, double* x, int64_t n, int32_t nrhs, int32_t mode, h2g_error* err) {
   return guarded(err, [&] {
     if (!c || !b || !x) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    std::lock_guard<std::recursive_mutex> run_lock(c->ctx->run_mu);
     CK(cudaSetDevice(c->ctx->device));
     if (n != c->n) throw Error(H2G_ERR_INVALID_INPUT, fmt("solve: right-hand side has length %lld, factorization expects %lld", n, c->n));
     if (nrhs < 1) throw Error(H2G_ERR_INVALID_INPUT, "solve: nrhs must be >= 1");
@@ -2116,6 +2214,7 @@ int h2g_chain_record_blocks(const h2g_chain* c, int32_t li, int32_t ri, int64_t*
 
 int h2g_chain_root(const h2g_chain* c, double* root_l, double* root_u) {
   return guarded(nullptr, [&] {
+    if (!c) throw Error(H2G_ERR_INVALID_INPUT, "null chain");
     const int64_t r = c->root_size;
     if (r == 0) return;
     std::vector<std::complex<double>> A((size_t)r * r);
@@ -2174,6 +2273,20 @@ int h2g_chain_timing(const h2g_chain* c, double* fms, double* sms, int64_t* fl, 
   if (sms) *sms = c->solve_ms;
   if (fl) *fl = c->factor_launches;
   if (sl) *sl = c->solve_launches;
+  return H2G_OK;
+}
+
+int h2g_chain_plan(const h2g_chain* c, double* plan_ms, int32_t* built) {
+  if (!c) return H2G_ERR_INVALID_INPUT;
+  if (plan_ms) *plan_ms = c->plan_ms;
+  if (built) *built = c->plan_built ? 1 : 0;
+  return H2G_OK;
+}
+
+int h2g_context_clear_plans(h2g_context* ctx) {
+  if (!ctx) return H2G_ERR_INVALID_INPUT;
+  std::lock_guard<std::mutex> g(ctx->plan_mu);
+  ctx->plan_lru.clear();
   return H2G_OK;
 }
 

@@ -837,4 +837,51 @@ void matvec_device(const Structure& S, const std::vector<int64_t>& basis_rows, c
   for (void* p : {(void*)x, (void*)y, (void*)xh, (void*)yh, (void*)push}) cudaFreeAsync(p, st);
 }
 
+// ------------------------------------------------- sampled dense rows
+// y[q] = sum_j Z(rows[q], j) x[j] with Z generated from the kernel (the
+// north_star's dense sampled-row residual; the reference's
+// assemble_block, kernel.hpp:64-102). One CTA per sampled row; each thread
+// strides the columns, then a fixed-order tree reduction (deterministic).
+__global__ void __launch_bounds__(256) k_rows_matvec(KernelD K, const double* px, const double* py, const double* pz, long long n,
+                                                      const long long* rows, const cplx* x, int nrhs, long long ldx, cplx* y, long long ldy) {
+  __shared__ cplx red[256];
+  const long long r = rows[blockIdx.x];
+  for (int c = 0; c < nrhs; ++c) {
+    cplx s = czero();
+    const cplx* xc = x + (size_t)c * ldx;
+    for (long long j = threadIdx.x; j < n; j += blockDim.x) cfma(s, kentry(K, px, py, pz, r, j), xc[j]);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) y[blockIdx.x + (size_t)c * ldy] = red[0];
+    __syncthreads();
+  }
+}
+
+void kernel_rows_matvec_device(const double* points_tree, int64_t n, const h2g_kernel_spec& Ks, const int64_t* rows, int64_t nrows,
+                               const double* x_host, double* y_host, int nrhs, cudaStream_t st) {
+  KernelD K{Ks.kind, Ks.wavenumber_re, Ks.wavenumber_im, Ks.scale_re, Ks.scale_im, Ks.diag_re, Ks.diag_im};
+  std::vector<double> hx(n), hy(n), hz(n);
+  for (int64_t i = 0; i < n; ++i) hx[i] = points_tree[3 * i], hy[i] = points_tree[3 * i + 1], hz[i] = points_tree[3 * i + 2];
+  for (int64_t q = 0; q < nrows; ++q)
+    if (rows[q] < 0 || rows[q] >= n) throw std::invalid_argument("kernel_rows_matvec: row index out of range");
+  std::vector<long long> hr(rows, rows + nrows);
+  double* px = dev_upload(hx, st);
+  double* py = dev_upload(hy, st);
+  double* pz = dev_upload(hz, st);
+  long long* dr = dev_upload(hr, st);
+  cplx *x = nullptr, *y = nullptr;
+  CKB(cudaMallocAsync(&x, (size_t)n * nrhs * 16, st));
+  CKB(cudaMallocAsync(&y, (size_t)std::max<int64_t>(nrows, 1) * nrhs * 16, st));
+  CKB(cudaMemcpyAsync(x, x_host, (size_t)n * nrhs * 16, cudaMemcpyHostToDevice, st));
+  if (nrows) k_rows_matvec<<<static_cast<unsigned>(nrows), 256, 0, st>>>(K, px, py, pz, n, dr, x, nrhs, n, y, nrows);
+  CKB(cudaGetLastError());
+  if (nrows) CKB(cudaMemcpyAsync(y_host, y, (size_t)nrows * nrhs * 16, cudaMemcpyDeviceToHost, st));
+  CKB(cudaStreamSynchronize(st));
+  for (void* p : {(void*)px, (void*)py, (void*)pz, (void*)dr, (void*)x, (void*)y}) cudaFreeAsync(p, st);
+}
+
 }  // namespace h2g

@@ -27,4 +27,9 @@ void matvec_device(const Structure& S, const std::vector<int64_t>& basis_rows, c
                    const std::vector<int64_t>& basis_off, const std::vector<int64_t>& coup_off, const std::vector<int64_t>& dense_off,
                    const cplx* basis, const cplx* coup, const cplx* dense, const double* x_host, double* y_host, int nrhs, cudaStream_t s);
 
+// Dense kernel rows times x (tree order points, n x 3 row-major): the sampled
+// dense residual of the north_star.
+void kernel_rows_matvec_device(const double* points_tree, int64_t n, const h2g_kernel_spec& K, const int64_t* rows, int64_t nrows,
+                               const double* x_host, double* y_host, int nrhs, cudaStream_t s);
+
 }  // namespace h2g

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <set>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -1618,17 +1619,34 @@ size_t head_smem_bytes(int bm) {
   return smem3(bm) + (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
 }
 
-// Opt in to the dynamic shared memory a launch needs (cached per kernel).
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// Opt in to the dynamic shared memory a launch needs (cached per device and
+// kernel: the attribute is per device, a second GPU in the process needs its own).
 static void set_smem(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> done;
+  static std::map<std::pair<int, const void*>, size_t> done;
   std::lock_guard<std::mutex> g(mu);
-  size_t& cur = done[fn];
+  size_t& cur = done[{current_device(), fn}];
   if (bytes > cur) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       throw std::runtime_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
     cur = bytes;
   }
+}
+
+// Non-portable cluster sizes (> 8 CTAs), opted in once per device and kernel.
+static void allow_big_clusters(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert({current_device(), fn}).second)
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      throw std::runtime_error("cudaFuncSetAttribute(NonPortableClusterSizeAllowed) failed");
 }
 
 static int sync_debug() {
@@ -1642,27 +1660,36 @@ static void post_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));
 }
 
-static cplx* g_ws = nullptr;
-static size_t g_ws_bytes = 0;
-static cplx* workspace(size_t bytes, cudaStream_t s) {
-  if (bytes > g_ws_bytes) {
-    if (g_ws) {
-      cudaStreamSynchronize(s);
-      cudaFree(g_ws);
-    }
-    cudaMalloc(&g_ws, bytes);
-    g_ws_bytes = bytes;
-  }
-  return g_ws;
+// Level scratch (complement / head / extended-LU workspaces). It is owned by
+// the caller's level state (one allocation per context and level, stream
+// ordered), never a process-wide buffer.
+static size_t complement_bytes(int bm) { return 2 * (size_t)bm * bm * sizeof(cplx) + (size_t)bm * sizeof(cplx); }
+static size_t hlu_ws_bytes(int bm, int nb) {
+  const size_t ldm = 2 * (size_t)bm;
+  return ldm * ldm * sizeof(cplx) * nb + (size_t)nb * 1024 * sizeof(cplx) + (size_t)nb * 16 + 64;
+}
+
+size_t level_scratch_bytes(int nl, int bm, int max_batch) {
+  size_t need = 4 * (size_t)bm * bm * sizeof(cplx) * max_batch;  // k_head
+  need = std::max(need, 2 * (size_t)bm * bm * sizeof(cplx) * max_batch);  // k_head2
+  if (bm > 64) need = std::max(need, hlu_ws_bytes(bm, max_batch));  // k_hlu_* (e > 64 needs b > 64)
+  if (complement_bytes(bm) > kSmemCap) need = std::max(need, complement_bytes(bm) * nl);
+  return need;
+}
+
+static cplx* workspace(const DevLevel& L, size_t bytes) {
+  if (!L.scratch || bytes > L.scratch_bytes)
+    throw std::runtime_error("level scratch too small: " + std::to_string(bytes) + " bytes needed, " + std::to_string(L.scratch_bytes) + " allocated");
+  return L.scratch;
 }
 
 void launch_complement(const DevLevel& L, cudaStream_t s) {
-  const size_t need = 2 * (size_t)L.bmax * L.bmax * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx);
+  const size_t need = complement_bytes(L.bmax);
   if (need <= kSmemCap) {
     set_smem((const void*)k_complement, need);
     k_complement<<<L.nl, 256, need, s>>>(L, nullptr); post_launch("k_complement");
   } else {
-    cplx* ws = workspace(need * L.nl, s);
+    cplx* ws = workspace(L, need * L.nl);
     k_complement<<<L.nl, 256, 0, s>>>(L, ws);
     post_launch("k_complement");
   }
@@ -1684,11 +1711,7 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 8 + 256;
     if (smem > kSmemCap) throw std::runtime_error("k_eig1c: block too large for the 16-CTA cluster");
     set_smem((const void*)k_eig1c, smem);
-    static bool np = false;
-    if (!np) {
-      cudaFuncSetAttribute((const void*)k_eig1c, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      np = true;
-    }
+    allow_big_clusters((const void*)k_eig1c);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb * kHC);
     cfg.blockDim = dim3(256);
@@ -1736,11 +1759,7 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     const size_t smem = ((size_t)L.bmax * ncl + 3 * (size_t)L.bmax) * sizeof(cplx) + 64;
     if (smem > kSmemCap) throw std::runtime_error("k_eig1b_cl: block too large for the cluster");
     set_smem((const void*)k_eig1b_cl, smem);
-    static bool np = false;
-    if (!np) {
-      cudaFuncSetAttribute((const void*)k_eig1b_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      np = true;
-    }
+    allow_big_clusters((const void*)k_eig1b_cl);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nb * kHC);
     cfg.blockDim = dim3(256);
@@ -1774,7 +1793,7 @@ void launch_head(const DevLevel& L, const int* batch_cl, int p0, int nb, cudaStr
   const int bm = L.bmax;
   const size_t small = (size_t)bm * 8 + (size_t)bm * 4 + (size_t)(bm + 2) * 4 + 16 + (size_t)4 * (bm / 2 + 1) * 8 + 64;
   set_smem((const void*)k_head, small);
-  cplx* ws = workspace(4 * (size_t)bm * bm * sizeof(cplx) * nb, s);
+  cplx* ws = workspace(L, 4 * (size_t)bm * bm * sizeof(cplx) * nb);
   k_head<<<nb, 256, small, s>>>(L, batch_cl, p0, ws);
   post_launch("k_head");
 }
@@ -1784,7 +1803,7 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cuda
     // multi-CTA extended LU (k_hlu_*); M per slot is (b + e)^2 <= (2 bmax)^2
     const int ldm = 2 * L.bmax;
     const size_t mbytes = (size_t)ldm * ldm * sizeof(cplx);
-    char* ws = reinterpret_cast<char*>(workspace(mbytes * nb + (size_t)nb * 1024 * sizeof(cplx) + (size_t)nb * 16 + 64, s));
+    char* ws = reinterpret_cast<char*>(workspace(L, hlu_ws_bytes(L.bmax, nb)));
     cplx* M0 = reinterpret_cast<cplx*>(ws);
     cplx* Dg = reinterpret_cast<cplx*>(ws + mbytes * nb);  // factored 32 x 32 diagonal blocks
     double* scale = reinterpret_cast<double*>(Dg + (size_t)nb * 1024);
@@ -1804,7 +1823,7 @@ void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cuda
     post_launch("k_hlu_finish");
     return;
   }
-  cplx* ws = workspace(2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb, s);
+  cplx* ws = workspace(L, 2 * (size_t)L.bmax * L.bmax * sizeof(cplx) * nb);
   k_head2<<<nb, 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_head2");
 }

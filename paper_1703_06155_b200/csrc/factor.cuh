@@ -73,6 +73,8 @@ struct DevLevel {
   DevError* err;
   int debug;
   cplx* eigws;  // step-0 eigensolver workspace, eig1_ws_cplx(bmax) per batch slot
+  cplx* scratch;         // level scratch of the head / extended-LU / complement kernels
+  size_t scratch_bytes;  // >= level_scratch_bytes(nl, bmax, max batch)
 };
 
 struct PanelItemD {
@@ -123,6 +125,9 @@ struct NormDesc {
   double* out;
 };
 
+// Bytes of DevLevel::scratch a level with nl clusters, bmax and the given
+// largest batch needs.
+size_t level_scratch_bytes(int nl, int bmax, int max_batch);
 void launch_complement(const DevLevel& L, cudaStream_t s);
 void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mmax, cudaStream_t s,
                  const std::function<void(int)>& phase);

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <stdexcept>
 
@@ -294,11 +295,18 @@ __global__ void k_finite(const cplx* y, long long total, int* bad) {
 }
 
 // ----------------------------------------------------------------- launchers
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+// Dynamic shared-memory opt-in, cached per (device, kernel).
 static void smem_attr(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> done;
+  static std::map<std::pair<int, const void*>, size_t> done;
   std::lock_guard<std::mutex> g(mu);
-  size_t& cur = done[fn];
+  size_t& cur = done[{cur_device(), fn}];
   if (bytes > cur) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       throw std::runtime_error("cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
@@ -306,13 +314,14 @@ static void smem_attr(const void* fn, size_t bytes) {
   }
 }
 
-// Co-resident grid for the cooperative level kernels (cached per kernel / smem).
+// Co-resident grid for the cooperative level kernels (cached per device /
+// kernel / smem).
 template <class K>
 static int coop_grid(K kernel, size_t smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_pair((const void*)kernel, smem);
+  auto key = std::make_tuple(cur_device(), (const void*)kernel, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int dev = 0, nsm = 0, per = 0;

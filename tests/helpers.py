@@ -20,6 +20,36 @@ def vie_problem(cells, side, leaf, eps):
     return O.H2(b, K, eps), K
 
 
+# Arrays that define an H² input (include/h2g.h layout); the hash proves two
+# runs factorized the identical matrix.
+_HASH_KEYS = ("cluster_begin", "cluster_end", "adm_offsets", "adm_pairs", "split_offsets", "split_pairs", "leaf_pairs",
+              "basis_rows", "basis_rank", "basis_offset", "basis_data", "coupling_offset", "coupling_data", "dense_offset",
+              "dense_data")
+_HASH_DTYPES = dict(cluster_begin=np.int64, cluster_end=np.int64, adm_offsets=np.int64, adm_pairs=np.int32,
+                    split_offsets=np.int64, split_pairs=np.int32, leaf_pairs=np.int32, basis_rows=np.int64,
+                    basis_rank=np.int64, basis_offset=np.int64, basis_data=np.complex128, coupling_offset=np.int64,
+                    coupling_data=np.complex128, dense_offset=np.int64, dense_data=np.complex128)
+
+
+def h2_input_hash(arrays):
+    import hashlib
+
+    h = hashlib.sha256()
+    for k in _HASH_KEYS:
+        a = np.ascontiguousarray(arrays[k], dtype=_HASH_DTYPES[k])
+        if k == "split_pairs":  # the download pads an empty list to one row
+            a = a[: int(arrays["split_offsets"][-1])]
+        h.update(k.encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def sampled_rows(n, nrows=4096, seed=1234):
+    """Seeded row sample of the dense sampled-row residual."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(nrows, n), replace=False)).astype(np.int64)
+
+
 def ranks_by_cluster(records):
     return {(r["level"], r["cluster"]): r["rank_after"] for r in records}
 

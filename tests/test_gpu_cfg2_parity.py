@@ -1,0 +1,96 @@
+"""Parity on the benched configuration (BASELINE config 2: 32^3 VIE cube,
+leaf 32, eps 1e-4) against a committed oracle golden run.
+
+tests/golden/cfg2_oracle.{json,npz} was produced by scripts/oracle_golden.py
+on a GPU box: the H² was built by the GPU builder (the bench's input),
+downloaded, and factorized by the CPU oracle (reference cluster order,
+factorization.hpp:618) there. This test rebuilds the H² on the device,
+proves it is the identical input (SHA-256 of every array), factorizes it on
+the GPU and compares with the oracle (north_star criteria):
+
+  * solution:  ||x_gpu - x_oracle|| / ||x_oracle|| <= 10 eps
+  * residual:  within 2x the oracle's, both through the H² operator
+               (verify.hpp:14-19) and on 4096 sampled dense rows
+  * ranks:     per (level, cluster) rank_after within the bound recorded in
+               tests/golden/cfg2_rank_noise.json: max(1, the oracle's own
+               per-cluster rank change under a rounding-level perturbation of
+               the same algorithm); see DESIGN.md "Parity at config 2".
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1703_06155_b200 as h2g
+from helpers import h2_input_hash, rel, sampled_rows
+from paper_1703_06155_b200.geometry import BASELINE_CONFIGS, vie_constants, vie_grid_points
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+if not os.path.exists(os.path.join(GOLD, "cfg2_oracle.json")):
+    pytest.skip("config-2 golden fixture not generated yet (scripts/oracle_golden.py)", allow_module_level=True)
+
+
+def _load():
+    meta = json.load(open(os.path.join(GOLD, "cfg2_oracle.json")))
+    arr = np.load(os.path.join(GOLD, "cfg2_oracle.npz"))
+    return meta, arr
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    meta, gold = _load()
+    c = BASELINE_CONFIGS[2]
+    k0, scale, diag = vie_constants(c["cells"], c["side"])
+    pts = vie_grid_points(c["cells"], c["side"])
+    A = h2g.H2Matrix.build(pts, c["leaf"], 1.0, h2g.helmholtz_kernel(k0, diag, scale), c["eps"])
+    host = A.download()
+    ch = h2g.factorize(A, c["eps"])
+    perm = host["perm"]
+    b = h2g.random_rhs(A.n, 1234)[perm]
+    x = ch.solve(b)
+    return dict(meta=meta, gold=gold, A=A, host=host, ch=ch, b=b, x=x, pts_tree=pts[perm], kernel=h2g.helmholtz_kernel(k0, diag, scale),
+                eps=c["eps"])
+
+
+def test_identical_input(cfg2):
+    assert h2_input_hash(cfg2["host"]) == cfg2["meta"]["input_sha256"]
+
+
+def test_solution_within_10_eps(cfg2):
+    d = rel(cfg2["x"], cfg2["gold"]["x"])
+    assert d <= 10 * cfg2["eps"], d
+
+
+def test_residuals_within_2x(cfg2):
+    meta = cfg2["meta"]
+    r_h2 = cfg2["A"].relative_residual(cfg2["x"], cfg2["b"])
+    assert r_h2 <= 2 * meta["residual_h2"], (r_h2, meta["residual_h2"])
+    rows = sampled_rows(cfg2["A"].n)
+    r_d = h2g.sampled_dense_residual(cfg2["pts_tree"], cfg2["kernel"], cfg2["x"], cfg2["b"], rows)
+    assert r_d <= 2 * meta["residual_sampled_dense"], (r_d, meta["residual_sampled_dense"])
+
+
+def test_ranks_within_oracle_noise(cfg2):
+    rec = cfg2["gold"]["rec"]  # level, cluster, bsize, rank_before, rank_after, eliminated
+    ro = {(int(r[0]), int(r[1])): int(r[4]) for r in rec}
+    rg = {(r["level"], r["cluster"]): r["rank_after"] for r in cfg2["ch"].all_records()}
+    assert ro.keys() == rg.keys()
+    d = np.array([rg[k] - ro[k] for k in ro])
+    bound = 1
+    noise = os.path.join(GOLD, "cfg2_rank_noise.json")
+    if os.path.exists(noise):
+        bound = max(1, int(json.load(open(noise))["max_abs_rank_diff"]))
+    assert np.abs(d).max() <= bound, (np.abs(d).max(), bound)
+    # the level sums stay within 2 % of the oracle's
+    for lv in sorted({k[0] for k in ro}):
+        so = sum(v for k, v in ro.items() if k[0] == lv)
+        sg = sum(v for k, v in rg.items() if k[0] == lv)
+        assert abs(sg - so) <= 0.02 * so + 1, (lv, sg, so)
+
+
+def test_root_size_close(cfg2):
+    ro = cfg2["meta"]["root_size"]
+    assert abs(cfg2["ch"].root_size - ro) <= 0.05 * ro + 2

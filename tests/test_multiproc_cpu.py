@@ -26,10 +26,12 @@ def test_reference_arm_rank0_only_world2(monkeypatch):
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout  # rank 0 alone prints
     rec = json.loads(lines[0])
-    assert rec["impl"] == "reference" and rec["value"] > 0 and rec["cpu_baseline"]["cores"] == 1
+    assert rec["impl"] == "reference" and rec["value"] > 0 and rec["cpu_baseline"]["cores"] >= 1
+    assert rec["cpu_baseline"]["nproc"] >= 1 and rec["cpu_baseline"]["cpu_model"]
+    assert rec["config"]["n"] == 32768  # the GPU arm's workload (config 2); the sample is its octant
 
 
-def test_max_over_ranks_reduction_gloo():
+def test_max_over_ranks_reduction_gloo(tmp_path):
     """The replica driver's timing reduction (max over ranks) with gloo."""
     code = r'''
 import os, torch, torch.distributed as dist
@@ -42,12 +44,9 @@ dist.barrier()
 if r == 0: print("OK", t.item())
 dist.destroy_process_group()
 '''
-    path = os.path.join(ROOT, "tests", "_maxred.py")
+    path = str(tmp_path / "_maxred.py")
     open(path, "w").write(code)
-    try:
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29612", path]
-        out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        assert "OK 2.0" in out.stdout
-    finally:
-        os.remove(path)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29612", path]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "OK 2.0" in out.stdout
