@@ -274,6 +274,18 @@ struct DBuf {
 // Pinned, device-mapped host memory. Used only when a configuration does not
 // fit in HBM (config 3: the level-12 -> 11 merge cores and the chains of
 // finished levels); kernels read / write it in place over the host link.
+// Process-wide cap on pinned staging memory (H2G_HOST_STAGING_GB, default
+// 96 GB): past it a staging request fails as a device out-of-memory instead
+// of exhausting the host.
+std::atomic<size_t> g_pinned_bytes{0};
+size_t pinned_cap() {
+  static const size_t cap = [] {
+    const char* e = std::getenv("H2G_HOST_STAGING_GB");
+    return (size_t)((e ? std::atof(e) : 96.0) * 1e9);
+  }();
+  return cap;
+}
+
 struct HBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -282,18 +294,22 @@ struct HBuf {
   HBuf& operator=(const HBuf&) = delete;
   ~HBuf() { release(); }
   void release() {
-    if (p) cudaFreeHost(p);
+    if (p) cudaFreeHost(p), g_pinned_bytes -= bytes;
     p = nullptr;
     bytes = 0;
   }
   void alloc(size_t n) {
     release();
+    if (g_pinned_bytes + n > pinned_cap())
+      throw Error(H2G_ERR_CUDA, std::string("out of memory: staging ") + std::to_string(n) + " bytes in pinned host memory would exceed the " +
+                                    std::to_string(pinned_cap()) + "-byte cap (H2G_HOST_STAGING_GB)");
     if (cudaHostAlloc(&p, std::max<size_t>(n, 16), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
       throw Error(H2G_ERR_CUDA, std::string("pinned host allocation of ") + std::to_string(n) + " bytes failed");
     }
     bytes = n;
+    g_pinned_bytes += n;
   }
   template <class T>
   T* as() const {
@@ -600,9 +616,15 @@ struct LevelData {
   std::vector<int> bsz, korig;
   std::vector<long long> pos;
   int bmax = 0;
-  // dense / fill blocks packed at their true sizes (bsz[row] x bsz[col])
+  // dense blocks packed at their true sizes (bsz[row] x bsz[col]); fill
+  // blocks in the segmented front pool (foff from the FrontPlan, -1 = never
+  // held in full) or, for the root level, packed like the dense blocks
   std::vector<long long> doff, foff;
+  FrontPlan front;
+  bool has_front = false;
+  std::vector<int> fex_host;  // fill blocks holding content at level entry
   DBuf D, F, fex, V0, Vp;
+  long long foff_safe(size_t f) const { return foff[f] < 0 ? 0 : foff[f]; }
 };
 
 // Packed offsets of blocks (rows[i], cols[i]) with sizes bsz[.]; returns the total.
@@ -928,8 +950,16 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
       upload(dd, cd, st);
       launch_copy(dd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
       ++launches;
-      const long long ftot = pack_offsets(Y.frow, Y.fcol, cur.bsz, cur.foff);
-      cur.F.alloc(std::max<long long>(ftot, 1) * 16, st, true);
+      cur.fex_host.assign(Y.frow.size(), 0);
+      if (stop <= L) {
+        cur.front = build_front(Y, P->sched[0], P->work[0], cur.bsz, {});
+        cur.has_front = true;
+        cur.foff = cur.front.foff;
+        cur.F.alloc(std::max<long long>(cur.front.pool_elems, 1) * 16, st, true);
+      } else {
+        const long long ftot = pack_offsets(Y.frow, Y.fcol, cur.bsz, cur.foff);
+        cur.F.alloc(std::max<long long>(ftot, 1) * 16, st, true);
+      }
       cur.fex.alloc(std::max<size_t>(Y.frow.size(), 1) * 4, st, true);
       CK(cudaStreamSynchronize(st));
     }
@@ -988,6 +1018,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     auto mark = [&](const char* what) {
       if (verbose >= 2) std::fprintf(stderr, "[h2g]   %-28s %.4f s\n", what, wall() - tlev);
     };
+    std::vector<cplx*> core_ptr_h;  // per fill of the running level: its compact core (host copy of DevLevel::core_ptr)
+    std::vector<DBuf> core_chunks;   // the cores, one chunk per segment; released after the merge
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
         const LevelSym& Y = P->levels[li];
@@ -1048,7 +1080,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         std::vector<int> kfin0(cur.korig);
         size_t o_kfin = pk.add(kfin0);
         size_t o_drow = pk.add(Y.drow), o_dcol = pk.add(Y.dcol), o_diag = pk.add(Y.diag_blk);
-        size_t o_doff = pk.add(cur.doff), o_foff = pk.add(cur.foff);
+        std::vector<long long> foff_dev(cur.foff.size());
+        for (size_t f = 0; f < foff_dev.size(); ++f) foff_dev[f] = cur.foff_safe(f);
+        size_t o_doff = pk.add(cur.doff), o_foff = pk.add(foff_dev);
         size_t o_frow = pk.add(Y.frow), o_fcol = pk.add(Y.fcol);
         size_t o_Rp = pk.add(Y.R_ptr), o_Rn = pk.add(Y.R_nb), o_Cp = pk.add(Y.C_ptr), o_Cn = pk.add(Y.C_nb);
         size_t o_Gp = pk.add(Y.G_ptr), o_Gf = pk.add(Y.G_fill), o_Gt = pk.add(Y.G_tr);
@@ -1143,7 +1177,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               const int t = SC.batch_cl[SC.batch_ptr[bi] + a.q];
               const int b = cur.bsz[t];
               const int fr = cur.bsz[Y.frow[a.fi]];
-              const cplx* F = cur.F.as<cplx>() + cur.foff[a.fi];
+              const cplx* F = cur.F.as<cplx>() + cur.foff_safe(a.fi);
               cplx* Cp = ybuf.as<cplx>() + a.yoff + (long long)a.m * a.col;
               const int* fx = cur.fex.as<int>() + a.fi;
               gA1.push_back({cur.Vp.as<cplx>() + (size_t)t * bb, F, Cp, b, fr, a.m, a.m, a.bx, b, OP_C, a.tr ? OP_T : OP_N, 1.0, 0.0, fx, nullptr});
@@ -1159,7 +1193,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
           for (size_t c = 0; c < ndesc_f.size(); ++c) {
             const int fi = ndesc_f[c];
-            gN.push_back({cur.F.as<cplx>() + cur.foff[fi], cur.bsz[Y.frow[fi]], cur.bsz[Y.fcol[fi]], 0, 0, cur.fex.as<int>() + fi, cnbuf.as<double>() + c});
+            gN.push_back({cur.F.as<cplx>() + cur.foff_safe(fi), cur.bsz[Y.frow[fi]], cur.bsz[Y.fcol[fi]], 0, 0, cur.fex.as<int>() + fi, cnbuf.as<double>() + c});
           }
           // transposition flag of each colnorm entry
           size_t c = 0;
@@ -1327,8 +1361,90 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         const int* d_bat = at<int>(mt, o_bat);
         const SchurTargetD* d_sch = at<SchurTargetD>(mt, o_sch);
         const SchurContribD* d_con = at<SchurContribD>(mt, o_con);
+        // ---- segmented fill storage (plan.hpp FrontPlan): full blocks are
+        // zeroed when their storage interval starts and projected to their
+        // compact cores Z = V_j^H F conj(V_c) (factorization.hpp:455, :540) at
+        // the end of the segment in which the later side passed step 0
+        const FrontPlan& FP = cur.front;
+        const size_t nfill = Y.frow.size();
+        core_ptr_h.assign(nfill, nullptr);
+        core_chunks.clear();
+        DBuf core_tab, dzero;
+        core_tab.alloc(std::max<size_t>(nfill, 1) * sizeof(cplx*), st, true);
+        DL.core_ptr = core_tab.as<cplx*>();
+        std::vector<int> zptr(1, 0);
+        {
+          std::vector<CopyDesc> zd;
+          for (int sg = 0; sg < FP.K; ++sg) {
+            for (int f : FP.zero_at[sg]) {
+              const int rj = cur.bsz[Y.frow[f]], cc = cur.bsz[Y.fcol[f]];
+              zd.push_back({nullptr, cur.F.as<cplx>() + cur.foff[f], rj, rj, rj, cc, 0, 0});
+            }
+            zptr.push_back(static_cast<int>(zd.size()));
+          }
+          upload(dzero, zd, st);
+        }
+        auto segment_end = [&](int sg) {
+          CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates land first
+          std::vector<int> kf(nl);
+          CK(cudaMemcpyAsync(kf.data(), DL.kfin, nl * 4, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          const auto& cores = FP.core_at[sg];
+          std::vector<long long> coff(cores.size());
+          long long ctop = 0;
+          for (size_t q = 0; q < cores.size(); ++q) coff[q] = ctop, ctop += (long long)kf[Y.frow[cores[q]]] * kf[Y.fcol[cores[q]]];
+          if (ctop > 0) {
+            ensure((size_t)ctop * 16, nullptr);
+            core_chunks.emplace_back();
+            core_chunks.back().alloc((size_t)ctop * 16, st, true);
+            for (size_t q = 0; q < cores.size(); ++q) core_ptr_h[cores[q]] = core_chunks.back().as<cplx>() + coff[q];
+          }
+          const cplx* chainp = CL->arena.as<cplx>();
+          auto V = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kf[t]) * cur.bsz[t]; };
+          const auto& col = FP.collapse_at[sg];
+          const long long kChunkX = (1LL << 30) / 16;
+          DBuf xb, dg1, dg2;
+          for (size_t q0 = 0; q0 < col.size();) {
+            std::vector<GemmDesc> g1, g2;
+            long long xt = 0;
+            std::vector<long long> xo;
+            size_t q1 = q0;
+            for (; q1 < col.size(); ++q1) {
+              const int f = col[q1], j = Y.frow[f], c = Y.fcol[f];
+              const long long xn = (long long)kf[j] * cur.bsz[c];
+              if (q1 > q0 && xt + xn > kChunkX) break;
+              xo.push_back(xt);
+              xt += xn;
+            }
+            xb.alloc((size_t)std::max<long long>(xt, 1) * 16, st);
+            for (size_t q = q0; q < q1; ++q) {
+              const int f = col[q], j = Y.frow[f], c = Y.fcol[f];
+              if (!kf[j] || !kf[c]) continue;
+              cplx* X = xb.as<cplx>() + xo[q - q0];
+              const int* fx = cur.fex.as<int>() + f;
+              g1.push_back({V(j), cur.F.as<cplx>() + cur.foff[f], X, cur.bsz[j], cur.bsz[j], kf[j], kf[j], cur.bsz[c], cur.bsz[j], OP_C, OP_N, 1.0, 0.0, fx, nullptr});
+              g2.push_back({X, V(c), core_ptr_h[f], kf[j], cur.bsz[c], kf[j], kf[j], kf[c], cur.bsz[c], OP_N, OP_R, 1.0, 0.0, fx, nullptr});
+            }
+            upload(dg1, g1, st);
+            upload(dg2, g2, st);
+            ctx->prof.begin(PC_MERGE, st);
+            launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, bm);
+            launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, bm);
+            ctx->prof.end(st);
+            C->klaunch[PC_MERGE] += (!g1.empty()) + (!g2.empty());
+            launches += (!g1.empty()) + (!g2.empty());
+            q0 = q1;
+          }
+          CK(cudaMemcpyAsync(core_tab.p, core_ptr_h.data(), nfill * sizeof(cplx*), cudaMemcpyHostToDevice, st));
+          CK(cudaStreamSynchronize(st));  // core_ptr_h is rewritten at the next segment end
+        };
         for (int bi = 0; bi < nbat; ++bi) {
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
+          const int sgi = fill_segment(bi, nbat, FP.K);
+          if (sgi > 0 && bi == FP.seg_first_batch[sgi] && zptr[sgi + 1] > zptr[sgi]) {
+            launch_copy(dzero.as<CopyDesc>() + zptr[sgi], zptr[sgi + 1] - zptr[sgi], st);
+            ++launches;
+          }
           const int na = a_ptr[bi + 1] - a_ptr[bi], nbd = b_ptr[bi + 1] - b_ptr[bi], nn = n_ptr[bi + 1] - n_ptr[bi];
           Prof& pf = ctx->prof;
           const int tl = bm;  // max GEMM dimension of this level's per-cluster products
@@ -1405,6 +1521,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
           launches += 3 + pass2_possible + (mmax > 0) + nhead + (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
+          if (bi + 1 == FP.seg_first_batch[sgi + 1]) segment_end(sgi);
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();
@@ -1498,7 +1615,9 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
             if (T.kind & 2) rs = cur.bsz[j] - kfin[j];
             if (T.kind & 4) cs = cur.bsz[c] - kfin[c];
           } else {
-            rws = cur.bsz[Y.frow[T.idx]], cls = cur.bsz[Y.fcol[T.idx]];
+            const int j = Y.frow[T.idx], c = Y.fcol[T.idx];
+            rws = cur.bsz[j], cls = cur.bsz[c];
+            if (T.kind & 8) rs = cur.bsz[j] - kfin[j], cs = cur.bsz[c] - kfin[c];  // core deposit
           }
           bool any = false;
           for (int k = T.c0; k < T.c1; ++k) {
@@ -1517,6 +1636,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         }
         for (size_t f = 0; f < Y.frow.size(); ++f)
           if (Y.fadm[f] >= 0 && fex[f]) ++ledger;
+        // collapse projections (segment ends)
+        for (const auto& col : cur.front.collapse_at)
+          for (int f : col)
+            if (fex[f]) {
+              const int a = Y.frow[f], c = Y.fcol[f];
+              flops += 8.0 * kfin[a] * cur.bsz[a] * cur.bsz[c] + 8.0 * kfin[a] * cur.bsz[c] * kfin[c];
+            }
         // ---- permutation (merge_permute :492-509)
         const int lp = l - 1;
         const int nlp = nl / 2;
@@ -1619,22 +1745,19 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         nxt.bmax = std::max(1, *std::max_element(nxt.bsz.begin(), nxt.bsz.end()));
         const size_t bbp = (size_t)nxt.bmax * nxt.bmax;
         const long long ndtot = pack_offsets(YP.drow, YP.dcol, nxt.bsz, nxt.doff);
-        const long long nftot = pack_offsets(YP.frow, YP.fcol, nxt.bsz, nxt.foff);
-        // Merge in two phases so that the level-l fill pool and the level-(l-1)
-        // pools never coexist: (1) project every fill that survives the merge
-        // to its compact kfin_a x kfin_c core Z = V_a^H F conj(V_c)
-        // (factorization.hpp:455, :540), (2) release the level-l fill pool and
-        // the level scratch, allocate level l-1 and assemble it.
+        // Merge (finish_level :445-475 + merge_permute :483-584). Every fill
+        // block that survives already sits in its compact core
+        // Z = V_a^H F conj(V_c) (segment ends above), so the parent blocks are
+        // assembled by copies: couplings / dense corners first, cores
+        // accumulated on top (dst = pad(S) + Z).
         std::vector<CopyDesc> cd;  // dst pointers relative to nxt.D (dst_kind 0) / nxt.F (1), fixed up after allocation
         std::vector<int> cd_kind;
-        const cplx* chainp = CL->arena.as<cplx>();
-        auto Vptr = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kfin[t]) * cur.bsz[t]; };
-        struct PendingG {
+        struct PendingZ {
           int a, c, fi, kind;
           long long doff;  // element offset of the destination in nxt.D / nxt.F
           int ldd;
         };
-        std::vector<PendingG> pend;
+        std::vector<PendingZ> pend;
         const auto& admL = S.adm[l];
         for (size_t pq = 0; pq < YP.drow.size(); ++pq) {
           const int Pr = YP.drow[pq], Pc = YP.dcol[pq];
@@ -1668,91 +1791,40 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
               }
             }
         }
+        // carried fill-in moves to the parent pair (content flags first: they
+        // seed the next level's segment plan)
         std::vector<int> fexp(YP.frow.size(), 0);
         for (size_t f = 0; f < Y.frow.size(); ++f) {
           if (Y.fadm[f] >= 0 || !fex[f]) continue;
           const int pf = Y.carried_parent[f];
           if (pf < 0) throw Error(H2G_ERR_INTERNAL, "carried fill without a parent target");
           fexp[pf] = 1;
+        }
+        const bool next_factorized = lp >= stop;
+        if (next_factorized) {
+          nxt.front = build_front(YP, P->sched[li + 1], P->work[li + 1], nxt.bsz, fexp);
+          nxt.has_front = true;
+          nxt.foff = nxt.front.foff;
+        }
+        const long long nftot = next_factorized ? nxt.front.pool_elems : pack_offsets(YP.frow, YP.fcol, nxt.bsz, nxt.foff);
+        for (size_t f = 0; f < Y.frow.size(); ++f) {
+          if (Y.fadm[f] >= 0 || !fex[f]) continue;
+          const int pf = Y.carried_parent[f];
           const int j = Y.frow[f], c = Y.fcol[f];
           if (!kfin[j] || !kfin[c]) continue;
+          if (nxt.foff[pf] < 0) throw Error(H2G_ERR_INTERNAL, "carried fill has no storage at the next level");
           const int ro = (j & 1) ? kfin[j - 1] : 0, co = (c & 1) ? kfin[c - 1] : 0;
           const int ldd = nxt.bsz[YP.frow[pf]];
           pend.push_back({j, c, static_cast<int>(f), 1, nxt.foff[pf] + ro + (long long)co * ldd, ldd});
         }
-        // phase 1: compact cores Z (chunked X = V_a^H F temporaries)
-        std::vector<long long> zoff(pend.size());
-        long long ztop = 0;
-        for (size_t q = 0; q < pend.size(); ++q) zoff[q] = ztop, ztop += (long long)kfin[pend[q].a] * kfin[pend[q].c];
-        // chunks bounded by 2 GB of X and 2 GB of Z; when Z does not fit in
-        // HBM next to the level-l fill pool it is staged through pinned host
-        // memory chunk by chunk (bulk copies, config 3)
-        const long long kChunk = (2LL << 30) / 16;
-        std::vector<size_t> chunk_q(1, 0);
-        {
-          long long xt = 0, zt = 0;
-          for (size_t q = 0; q < pend.size(); ++q) {
-            const long long xn = (long long)kfin[pend[q].a] * cur.bsz[pend[q].c], zn = (long long)kfin[pend[q].a] * kfin[pend[q].c];
-            if (q > chunk_q.back() && (xt + xn > kChunk || zt + zn > kChunk)) chunk_q.push_back(q), xt = 0, zt = 0;
-            xt += xn, zt += zn;
-          }
-          chunk_q.push_back(pend.size());
-        }
-        const int nchunk = static_cast<int>(chunk_q.size()) - 1;
-        DBuf zdev;  // all of Z (in HBM) or one chunk (host-staged)
-        HBuf zhost;
-        const bool zstaged = BlockCache::get().headroom() < (size_t)ztop * 16 + (size_t(4) << 30) + kMargin;
-        long long zchunk_max = 1;
-        for (int ck = 0; ck < nchunk; ++ck)
-          if (chunk_q[ck + 1] > chunk_q[ck])
-            zchunk_max = std::max(zchunk_max, (chunk_q[ck + 1] < pend.size() ? zoff[chunk_q[ck + 1]] : ztop) - zoff[chunk_q[ck]]);
-        if (zstaged) {
-          zhost.alloc((size_t)std::max<long long>(ztop, 1) * 16);
-          zdev.alloc(zchunk_max * 16, st);
-          mark("merge: pinned Z allocated");
-        } else {
-          zdev.alloc(std::max<long long>(ztop, 1) * 16, st);
-        }
-        auto zdst = [&](size_t q, int ck) { return zdev.as<cplx>() + (zstaged ? zoff[q] - zoff[chunk_q[ck]] : zoff[q]); };
-        auto zlen = [&](int ck) { return (chunk_q[ck + 1] < pend.size() ? zoff[chunk_q[ck + 1]] : ztop) - zoff[chunk_q[ck]]; };
-        {
-          DBuf tmp, dg1, dg2;
-          for (int ck = 0; ck < nchunk; ++ck) {
-            const size_t q0 = chunk_q[ck], q1 = chunk_q[ck + 1];
-            if (q1 == q0) continue;
-            std::vector<long long> xoff;
-            long long xtop = 0;
-            for (size_t q = q0; q < q1; ++q) xoff.push_back(xtop), xtop += (long long)kfin[pend[q].a] * cur.bsz[pend[q].c];
-            tmp.alloc(std::max<long long>(xtop, 1) * 16, st);
-            std::vector<GemmDesc> g1, g2;
-            for (size_t q = q0; q < q1; ++q) {
-              const auto& pg = pend[q];
-              const int a = pg.a, c = pg.c;
-              cplx* X = tmp.as<cplx>() + xoff[q - q0];
-              // X = V_a^H F (kfin_a x b_c);  Z = X conj(V_c)   (factorization.hpp:455, :540)
-              g1.push_back({Vptr(a), cur.F.as<cplx>() + cur.foff[pg.fi], X, cur.bsz[a], cur.bsz[a], kfin[a], kfin[a], cur.bsz[c], cur.bsz[a], OP_C, OP_N, 1.0, 0.0});
-              g2.push_back({X, Vptr(c), zdst(q, ck), kfin[a], cur.bsz[c], kfin[a], kfin[a], kfin[c], cur.bsz[c], OP_N, OP_R, 1.0, 0.0});
-            }
-            upload(dg1, g1, st);
-            upload(dg2, g2, st);
-            ctx->prof.begin(PC_MERGE, st);
-            const int tlm = std::max(bm, nxt.bmax);
-            launch_gemm(dg1.as<GemmDesc>(), static_cast<int>(g1.size()), st, tlm);
-            launch_gemm(dg2.as<GemmDesc>(), static_cast<int>(g2.size()), st, tlm);
-            ctx->prof.end(st);
-            if (zstaged) CK(cudaMemcpyAsync(zhost.as<cplx>() + zoff[q0], zdev.p, zlen(ck) * 16, cudaMemcpyDeviceToHost, st));
-            C->klaunch[PC_MERGE] += 2;
-            launches += 2;
-          }
-        }
-        for (const auto& pg : pend) flops += 8.0 * kfin[pg.a] * cur.bsz[pg.a] * cur.bsz[pg.c] + 8.0 * kfin[pg.a] * cur.bsz[pg.c] * kfin[pg.c];
-        mark("merge: phase 1 launched");
-        // phase 2: the level-l fill pool and scratch are dead
+        nxt.fex_host = fexp;
+        for (const auto& pg : pend)
+          if (!core_ptr_h[pg.fi]) throw Error(H2G_ERR_INTERNAL, "fill block with content has no core");
+        // the level-l fill pool and scratch are dead
         cur.F.release();
         cur.fex.release();
         cur.Vp.release();
-        if (zstaged) offload_chain(*CL), BlockCache::get().trim();  // memory is tight: this level's chain goes to the host too
-        mark("merge: phase 1 done");
+        mark("merge: fill pool released");
         ensure((size_t)(std::max<long long>(ndtot, 1) + std::max<long long>(nftot, 1) + (long long)nlp * bbp) * 16, CL.get());
         nxt.D.alloc(std::max<long long>(ndtot, 1) * 16, st, true);
         nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
@@ -1763,11 +1835,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         for (size_t q = 0; q < cd.size(); ++q) cd[q].dst = (cd_kind[q] ? Fp : Dp) + reinterpret_cast<long long>(cd[q].dst) / 16;
         // cores accumulate after the coupling / dense-corner copies (dst = S + Z)
         std::vector<CopyDesc> cz;
-        for (int ck = 0; ck < nchunk; ++ck)
-          for (size_t q = chunk_q[ck]; q < chunk_q[ck + 1]; ++q) {
-            const auto& pg = pend[q];
-            cz.push_back({zdst(q, ck), (pg.kind ? Fp : Dp) + pg.doff, kfin[pg.a], pg.ldd, kfin[pg.a], kfin[pg.c], 1, 0});
-          }
+        for (const auto& pg : pend) cz.push_back({core_ptr_h[pg.fi], (pg.kind ? Fp : Dp) + pg.doff, kfin[pg.a], pg.ldd, kfin[pg.a], kfin[pg.c], 1, 0});
         // padded transfers (finish_level :464-474)
         for (int P2 = 0; P2 < nlp; ++P2) {
           const int id = firstp + P2;
@@ -1785,15 +1853,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         upload(dcz, cz, st);
         ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
-        if (!zstaged) {
-          launch_copy(dcz.as<CopyDesc>(), static_cast<int>(cz.size()), st);
-        } else {
-          for (int ck = 0; ck < nchunk; ++ck) {
-            if (chunk_q[ck + 1] == chunk_q[ck]) continue;
-            CK(cudaMemcpyAsync(zdev.p, zhost.as<cplx>() + zoff[chunk_q[ck]], zlen(ck) * 16, cudaMemcpyHostToDevice, st));
-            launch_copy(dcz.as<CopyDesc>() + chunk_q[ck], static_cast<int>(chunk_q[ck + 1] - chunk_q[ck]), st);
-          }
-        }
+        launch_copy(dcz.as<CopyDesc>(), static_cast<int>(cz.size()), st);
         ctx->prof.end(st);
         C->klaunch[PC_MERGE] += (!cd.empty()) + (!cz.empty());
         launches += (!cd.empty()) + (!cz.empty());
@@ -1801,12 +1861,18 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaGetLastError());
         mark("merge launched");
         CK(cudaStreamSynchronize(st));  // temporaries die here
+        size_t core_bytes = 0;
+        for (auto& ch : core_chunks) core_bytes += ch.bytes;
+        core_chunks.clear();
 
         if (verbose) {
           size_t fr = 0, tot = 0;
           cudaMemGetInfo(&fr, &tot);
-          std::fprintf(stderr, "[h2g] level %d: merge done at %.3f s; Z %.2f GB%s, next D %.2f GB, next F %.2f GB; device free %.2f of %.2f GB\n", l, wall() - tlev,
-                       (zdev.bytes + zhost.bytes) / 1e9, zstaged ? " (host-staged)" : "", nxt.D.bytes / 1e9, nxt.F.bytes / 1e9, fr / 1e9, tot / 1e9);
+          std::fprintf(stderr,
+                       "[h2g] level %d: merge done at %.3f s; fill front pool %.2f GB (all full blocks %.2f GB, %d segments), cores %.2f GB, next D %.2f GB, "
+                       "next F %.2f GB; device free %.2f of %.2f GB\n",
+                       l, wall() - tlev, cur.front.pool_elems * 16.0 / 1e9, cur.front.full_elems_total * 16.0 / 1e9, cur.front.K, core_bytes / 1e9,
+                       nxt.D.bytes / 1e9, nxt.F.bytes / 1e9, fr / 1e9, tot / 1e9);
           std::fprintf(stderr, "[h2g] chains offloaded to host so far: %.2f GB\n", offloaded / 1e9);
         }
         tlev = wall();
@@ -1936,6 +2002,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           for (size_t f = 0; f < YR->frow.size(); ++f) {
             const int u = YR->frow[f], v = YR->fcol[f];
             if (!cur.bsz[u] || !cur.bsz[v]) continue;
+            if (cur.foff[f] < 0 || (f < cur.fex_host.size() && !cur.fex_host[f])) continue;  // no content (segmented storage may be shared)
             cf.push_back({cur.F.as<cplx>() + cur.foff[f], R0 + cur.pos[u] + (size_t)cur.pos[v] * nroot, cur.bsz[u], (int)nroot, cur.bsz[u], cur.bsz[v], 1, 0});
           }
           DBuf dcf;

@@ -1325,7 +1325,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
   extern __shared__ __align__(16) unsigned char tsm[];
   TileSmem<TM>& S = *reinterpret_cast<TileSmem<TM>*>(tsm);
   const SchurTargetD tg = targets[blockIdx.x];
-  int rows, cols, rs = 0, cs = 0;
+  int rows, cols, rs = 0, cs = 0, ldo = -1;
   cplx* out;
   if ((tg.kind & 1) == 0) {
     const int j = L.drow[tg.idx], c = L.dcol[tg.idx];
@@ -1336,10 +1336,21 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     if (tg.kind & 2) rs = rows - L.kfin[j];
     if (tg.kind & 4) cs = cols - L.kfin[c];
   } else {
-    rows = L.bsz[L.frow[tg.idx]];
-    cols = L.bsz[L.fcol[tg.idx]];
-    out = L.F + L.F_off[tg.idx];
+    const int j = L.frow[tg.idx], c = L.fcol[tg.idx];
+    rows = L.bsz[j];
+    cols = L.bsz[c];
+    if (tg.kind & 8) {
+      // compact core of a collapsed block: target rows / columns [e, b) of
+      // the (rotated) panels land at [0, kfin) of the kfin_j x kfin_c core
+      rs = rows - L.kfin[j];
+      cs = cols - L.kfin[c];
+      ldo = L.kfin[j];
+      out = L.core_ptr[tg.idx] - rs - (size_t)cs * ldo;
+    } else {
+      out = L.F + L.F_off[tg.idx];
+    }
   }
+  if (ldo < 0) ldo = rows;
   const int ntr = (rows - rs + TM - 1) / TM, ntc = (cols - cs + TM - 1) / TM;
   if ((int)blockIdx.y >= ntr * ntc) return;
   const int r0 = rs + (blockIdx.y % ntr) * TM, c0 = cs + (blockIdx.y / ntr) * TM;
@@ -1393,7 +1404,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     acc64_each(acc, [&](int ii, int jj, cplx v) {
       const int i = r0 + ii, j = c0 + jj;
       if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
-        cplx* o = out + i + (size_t)j * rows;
+        cplx* o = out + i + (size_t)j * ldo;
         *o = csub(*o, v);
       }
     });
@@ -1406,7 +1417,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
         const int i = r0 + tr + 8 * a, j = c0 + tc * RN + b;
         const cplx v = accs[a][b];
         if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
-          cplx* o = out + i + (size_t)j * rows;
+          cplx* o = out + i + (size_t)j * ldo;
           *o = csub(*o, v);
         }
       }

@@ -73,6 +73,7 @@ struct DevLevel {
   DevError* err;
   int debug;
   cplx* eigws;  // step-0 eigensolver workspace, eig1_ws_cplx(bmax) per batch slot
+  cplx* const* core_ptr; // per fill: its compact core (kfin_j x kfin_c) once collapsed (SchurTarget kind bit 3)
   cplx* scratch;         // level scratch of the head / extended-LU / complement kernels
   size_t scratch_bytes;  // >= level_scratch_bytes(nl, bmax, max batch)
 };

@@ -1,6 +1,10 @@
 // Host symbolic analysis, see plan.hpp.
 #include "plan.hpp"
 
+#include <climits>
+#include <cstdlib>
+#include <map>
+
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -317,9 +321,135 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
   return S;
 }
 
+int fill_segments(int nbat) {
+  static const int k = [] {
+    const char* e = std::getenv("H2G_FILL_SEGMENTS");
+    return e ? std::max(1, std::atoi(e)) : 16;
+  }();
+  return std::max(1, std::min(k, nbat));
+}
+
+namespace {
+
+// Best-fit interval allocator over one contiguous pool (element units).
+class FrontAllocator {
+ public:
+  long long alloc(long long n) {
+    auto it = by_size_.lower_bound(n);
+    if (it == by_size_.end()) {
+      const long long o = top_;
+      top_ += n;
+      return o;
+    }
+    const long long o = it->second, sz = it->first;
+    by_size_.erase(it);
+    by_off_.erase(o);
+    if (sz > n) insert(o + n, sz - n);
+    return o;
+  }
+  void release(long long o, long long n) {
+    // coalesce with the neighbours
+    auto nx = by_off_.lower_bound(o);
+    if (nx != by_off_.end() && nx->first == o + n) {
+      n += nx->second;
+      erase(nx->first, nx->second);
+    }
+    auto pv = by_off_.lower_bound(o);
+    if (pv != by_off_.begin()) {
+      --pv;
+      if (pv->first + pv->second == o) {
+        o = pv->first;
+        n += pv->second;
+        erase(pv->first, pv->second);
+      }
+    }
+    if (o + n == top_) {
+      top_ = o;  // give the tail back
+      return;
+    }
+    insert(o, n);
+  }
+  long long high() const { return high_; }
+  void note() { high_ = std::max(high_, top_); }
+
+ private:
+  void insert(long long o, long long n) {
+    by_off_[o] = n;
+    by_size_.emplace(n, o);
+  }
+  void erase(long long o, long long n) {
+    by_off_.erase(o);
+    auto r = by_size_.equal_range(n);
+    for (auto it = r.first; it != r.second; ++it)
+      if (it->second == o) {
+        by_size_.erase(it);
+        break;
+      }
+  }
+  long long top_ = 0, high_ = 0;
+  std::map<long long, long long> by_off_;
+  std::multimap<long long, long long> by_size_;
+};
+
+}  // namespace
+
+FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W, const std::vector<int>& bsz, const std::vector<int>& init) {
+  FrontPlan F;
+  const int nbat = static_cast<int>(sch.batch_ptr.size()) - 1;
+  const int K = fill_segments(nbat);
+  F.K = K;
+  F.seg_first_batch.assign(static_cast<size_t>(K) + 1, nbat);
+  for (int b = nbat - 1; b >= 0; --b) F.seg_first_batch[static_cast<size_t>(fill_segment(b, nbat, K))] = b;
+  const size_t nf = L.frow.size();
+  // first / last batch depositing into each fill block
+  std::vector<int> fd(nf, INT32_MAX), ld(nf, -1);
+  for (int b = 0; b < nbat; ++b)
+    for (int q = W.schur_ptr[static_cast<size_t>(b)]; q < W.schur_ptr[static_cast<size_t>(b) + 1]; ++q) {
+      const SchurTarget& T = W.schur[static_cast<size_t>(q)];
+      if ((T.kind & 1) == 0) continue;
+      fd[static_cast<size_t>(T.idx)] = std::min(fd[static_cast<size_t>(T.idx)], b);
+      ld[static_cast<size_t>(T.idx)] = std::max(ld[static_cast<size_t>(T.idx)], b);
+    }
+  F.foff.assign(nf, -1);
+  F.zero_at.assign(static_cast<size_t>(K), {});
+  F.collapse_at.assign(static_cast<size_t>(K), {});
+  F.core_at.assign(static_cast<size_t>(K), {});
+  std::vector<std::vector<int>> start(static_cast<size_t>(K)), stop(static_cast<size_t>(K));
+  for (size_t f = 0; f < nf; ++f) {
+    const int bc = std::max(sch.order[static_cast<size_t>(L.frow[f])], sch.order[static_cast<size_t>(L.fcol[f])]);
+    const int s1 = fill_segment(bc, nbat, K);
+    const bool in = !init.empty() && init[f];
+    const bool full = in || (ld[f] >= 0 && fill_segment(fd[f], nbat, K) <= s1);
+    const bool core_dep = ld[f] >= 0 && fill_segment(ld[f], nbat, K) > s1;
+    if (full) {
+      const int s0 = in ? 0 : fill_segment(fd[f], nbat, K);
+      start[static_cast<size_t>(s0)].push_back(static_cast<int>(f));
+      stop[static_cast<size_t>(s1)].push_back(static_cast<int>(f));
+      F.collapse_at[static_cast<size_t>(s1)].push_back(static_cast<int>(f));
+      F.full_elems_total += static_cast<long long>(bsz[static_cast<size_t>(L.frow[f])]) * bsz[static_cast<size_t>(L.fcol[f])];
+    }
+    if (full || core_dep) F.core_at[static_cast<size_t>(s1)].push_back(static_cast<int>(f));
+  }
+  FrontAllocator A;
+  auto size_of = [&](int f) {
+    return static_cast<long long>(bsz[static_cast<size_t>(L.frow[static_cast<size_t>(f)])]) * bsz[static_cast<size_t>(L.fcol[static_cast<size_t>(f)])];
+  };
+  for (int s = 0; s < K; ++s) {
+    for (int f : start[static_cast<size_t>(s)]) {
+      F.foff[static_cast<size_t>(f)] = A.alloc(size_of(f));
+      if (s > 0) F.zero_at[static_cast<size_t>(s)].push_back(f);
+    }
+    A.note();
+    for (int f : stop[static_cast<size_t>(s)]) A.release(F.foff[static_cast<size_t>(f)], size_of(f));
+  }
+  F.pool_elems = A.high();
+  return F;
+}
+
 LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
   LevelWork W;
   const int nbat = static_cast<int>(sch.batch_ptr.size()) - 1;
+  const int K = fill_segments(nbat);
   const auto& ord = sch.order;
   W.panel_ptr.assign(1, 0);
   W.schur_ptr.assign(1, 0);
@@ -401,8 +531,20 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
       while (j < tmp.size() && tmp[j].key == tmp[i].key) ++j;
       SchurTarget T{static_cast<int32_t>(tmp[i].key >> 40), static_cast<int32_t>(tmp[i].key & ((int64_t(1) << 40) - 1)),
                     static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
-      for (size_t k = i; k < j; ++k) W.contrib.push_back(tmp[k].c);
       const auto rc = target_rc(T);
+      // fill target whose core already exists (both sides collapsed in an
+      // earlier segment): deposit into the core, unlifted panels
+      bool core = false;
+      if (T.kind == 1) {
+        const int bc = std::max(ord[static_cast<size_t>(rc.first)], ord[static_cast<size_t>(rc.second)]);
+        core = fill_segment(b, nbat, K) > fill_segment(bc, nbat, K);
+        if (core) T.kind |= 8;
+      }
+      for (size_t k = i; k < j; ++k) {
+        SchurContrib cb = tmp[k].c;
+        if (core) cb.flags = 0;
+        W.contrib.push_back(cb);
+      }
       // dense target whose row (column) cluster was eliminated in an earlier
       // batch: its first e rows (columns) are zero and stay zero (cleanup,
       // factorization.hpp:431-439), so the update there is exactly zero and

@@ -84,8 +84,20 @@ struct PanelItem {
   int32_t lift;   // neighbour eliminated earlier: also store the lifted panel
 };
 
+// Fill-in storage by segments (compact fill). A level's batches
+// are cut into K contiguous segments. A fill block (j, c) is held in full
+// (bsz_j x bsz_c, level-entry frames, as deposit_fill keeps it,
+// factorization.hpp:359-366) only while a side still has its step 0 ahead:
+// at the end of the segment holding max(batch(j), batch(c)) it is projected to
+// its core V_j^H F conj(V_c) (kfin_j x kfin_c, the only form its later
+// consumers read, :455 and :540), and deposits of later segments go straight
+// to the core (the lifts through V_j / V_c cancel against the projection).
+int fill_segments(int nbat);
+inline int fill_segment(int b, int nbat, int K) { return nbat > 0 ? static_cast<int>(static_cast<int64_t>(b) * K / nbat) : 0; }
+
 struct SchurTarget {
-  int32_t kind;   // bit 0: 0 dense, 1 fill; bits 1/2 (dense): row / column cluster eliminated in an earlier batch
+  int32_t kind;   // bit 0: 0 dense, 1 fill; bits 1/2 (dense): row / column cluster eliminated in an earlier batch;
+                  // bit 3 (fill): deposit into the compact core (both sides already collapsed)
   int32_t idx;    // dense block / fill index
   int32_t c0, c1; // contribution range
 };
@@ -122,6 +134,23 @@ struct LevelWork {
   int max_batch = 0;
   int64_t schur_products = 0;  // structural count (upper bound)
 };
+
+// Segment plan of one level's fill storage (see fill_segments): full-block
+// offsets in a reused "front" pool (interval allocation over segments) and
+// the per-segment lists the driver acts on.
+struct FrontPlan {
+  int K = 1;
+  std::vector<int> seg_first_batch;             // [K + 1]
+  std::vector<long long> foff;                  // per fill: element offset in the front pool, -1 = never held in full
+  long long pool_elems = 0;
+  std::vector<std::vector<int>> zero_at;        // per segment: full blocks whose storage starts there (zeroed first; s > 0)
+  std::vector<std::vector<int>> collapse_at;    // per segment: full blocks projected to cores at its end
+  std::vector<std::vector<int>> core_at;        // per segment: every core created at its end (collapsed + core-only)
+  long long full_elems_total = 0;               // sum of all full blocks (what a non-segmented pool would hold)
+};
+// init[f] != 0: the block holds content at level entry (carried fill-in
+// deposited by the merge of the finer level); may be empty.
+FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W, const std::vector<int>& bsz, const std::vector<int>& init);
 
 Structure structure_from_desc(const h2g_matrix_desc* d);
 Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm);

@@ -63,7 +63,7 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   if (e > 0) {
     if (explicit_inv) {
       const cplx* Li = S.chain + S.Linv_off[t];
-      cta_gemm(e, nrhs, e, 1.0, Li, e, OP_N, sO, b, OP_N, 0.0, sS, b);
+      warp_gemv(e, nrhs, Li, e, OP_N, sO, b, sS, b);
       __syncthreads();
       for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sO[(idx % e) + (idx / e) * b] = sS[(idx % e) + (idx / e) * b];
       __syncthreads();
@@ -85,8 +85,10 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
 }
 
-// y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51), contributions of a
-// target segment summed in a fixed order.
+// y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51). One warp per target
+// row; the lanes stride over the flattened (contribution, p) index space so
+// every lane has independent loads in flight, then a fixed shuffle tree
+// (deterministic summation order).
 __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs) {
   int rows;
   long long base;
@@ -98,20 +100,46 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
     rows = S.kfin[m];
     base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
   }
-  for (int idx = threadIdx.x; idx < rows * nrhs; idx += blockDim.x) {
-    const int i = idx % rows, c = idx / rows;
-    cplx acc = czero();
-    for (int ci = tg.c0; ci < tg.c1; ++ci) {
-      const SolveContribD cb = contrib[ci];
-      const int m = cb.m;
-      const int e = S.bsz[m] - S.kfin[m];
-      if (e == 0) continue;
-      const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[m]);
-      const cplx* h = y + S.pos[m] + c * ldy;
-      for (int p = 0; p < e; ++p) cfma(acc, M[i + (size_t)p * rows], h[p]);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int c0 = 0; c0 < nrhs; c0 += 4) {
+    const int nc = min(4, nrhs - c0);
+    for (int i = warp; i < rows; i += nw) {
+      cplx acc[4] = {czero(), czero(), czero(), czero()};
+      int ci = tg.c0, off = 0, e = 0;
+      const cplx* M = nullptr;
+      const cplx* h = nullptr;
+      auto open = [&](int c) {
+        const SolveContribD cb = contrib[c];
+        e = S.bsz[cb.m] - S.kfin[cb.m];
+        M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]);
+        h = y + S.pos[cb.m];
+      };
+      if (ci < tg.c1) open(ci);
+      for (int u = lane;; u += 32) {
+        while (ci < tg.c1 && u >= off + e) {
+          off += e;
+          if (++ci < tg.c1) open(ci);
+        }
+        if (ci >= tg.c1) break;
+        const int p = u - off;
+        const cplx mv = M[i + (size_t)p * rows];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nc) cfma(acc[c], mv, h[p + (size_t)(c0 + c) * ldy]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double re = acc[c].x, im = acc[c].y;
+        for (int o = 16; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0 && c < nc) {
+          cplx* o = y + base + i + (size_t)(c0 + c) * ldy;
+          *o = csub(*o, make_double2(re, im));
+        }
+      }
     }
-    cplx* o = y + base + i + c * ldy;
-    *o = csub(*o, acc);
   }
 }
 
@@ -137,12 +165,28 @@ __device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int ns
     x = y + S.pos[t] + e;
   }
   cplx* out = part + ((size_t)q * nslot + c) * pstride;
-  for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
-    const int i = idx % e, r = idx / e;
-    cplx acc = czero();
-    const cplx* xr = x + r * ldy;
-    for (int p = 0; p < cols; ++p) cfma(acc, M[i + (size_t)p * e], xr[p]);
-    out[i + (size_t)r * e] = acc;
+  // one warp per row of Ubar, lanes over its columns (independent loads)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int r0 = 0; r0 < nrhs; r0 += 4) {
+    const int nc = min(4, nrhs - r0);
+    for (int i = warp; i < e; i += nw) {
+      cplx acc[4] = {czero(), czero(), czero(), czero()};
+      for (int p = lane; p < cols; p += 32) {
+        const cplx mv = M[i + (size_t)p * e];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r < nc) cfma(acc[r], mv, x[p + (size_t)(r0 + r) * ldy]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double re = acc[r].x, im = acc[r].y;
+        for (int o = 16; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0 && r < nc) out[i + (size_t)(r0 + r) * e] = make_double2(re, im);
+      }
+    }
   }
 }
 
@@ -159,16 +203,24 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
   if (e > 0) {
     const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
     const int nuse = nC + (kf > 0 ? 1 : 0);
-    for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) {
+    // head -= sum of the gathered partials: one warp per (row, rhs), lanes
+    // over the neighbour slots, fixed shuffle tree
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+    for (int idx = warp; idx < e * nrhs; idx += nw) {
       const int i = idx % e, c = idx / e;
       cplx acc = czero();
-      for (int u = 0; u < nuse; ++u) acc = cadd(acc, part[((size_t)q * nslot + (u < nC ? u : nC)) * pstride + i + (size_t)c * e]);
-      sS[i + c * b] = csub(sS[i + c * b], acc);
+      for (int u = lane; u < nuse; u += 32) acc = cadd(acc, part[((size_t)q * nslot + (u < nC ? u : nC)) * pstride + i + (size_t)c * e]);
+      double re = acc.x, im = acc.y;
+      for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+      }
+      if (lane == 0) sS[i + c * b] = csub(sS[i + c * b], make_double2(re, im));
     }
     __syncthreads();
     if (explicit_inv) {
       const cplx* Ui = S.chain + S.Uinv_off[t];
-      cta_gemm(e, nrhs, e, 1.0, Ui, e, OP_N, sS, b, OP_N, 0.0, sO, b);
+      warp_gemv(e, nrhs, Ui, e, OP_N, sS, b, sO, b);
       __syncthreads();
       for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sS[(idx % e) + (idx / e) * b] = sO[(idx % e) + (idx / e) * b];
       __syncthreads();
@@ -190,7 +242,7 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
     }
   }
   const cplx* Q = S.chain + S.Qt_off[t];
-  cta_gemm(b, nrhs, b, 1.0, Q, b, OP_R, sS, b, OP_N, 0.0, sO, b);
+  warp_gemv(b, nrhs, Q, b, OP_R, sS, b, sO, b);
   __syncthreads();
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
 }

@@ -16,7 +16,7 @@ def test_rows_matvec_matches_oracle():
     k0, scale, diag = vie_constants(16, 0.5)
     pts = vie_grid_points(16, 0.5)
     t = O.Tree(pts, 32)
-    pts_tree = t.points()
+    pts_tree = t.points
     n = pts.shape[0]
     rng = np.random.default_rng(5)
     x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
