@@ -104,6 +104,12 @@ typedef struct h2g_matrix_desc {
   const double* coupling_data;
   const int64_t* dense_offset;    /* [num_leaf_pairs]; |t| x |s| */
   const double* dense_data;
+  /* optional (needed only by h2g_matrix_save / h2g_chain_save, which write
+   * the tree like serialize.hpp:121-132): points n x 3 in TREE order, the
+   * tree permutation (tree index -> original index) and the leaf size */
+  const double* points_tree;
+  const int64_t* perm;
+  int64_t leafsize;
 } h2g_matrix_desc;
 
 typedef struct h2g_context h2g_context;
@@ -139,6 +145,31 @@ int h2g_matrix_download(const h2g_matrix* m, int64_t* cluster_begin, int64_t* cl
                         double* dense_data);
 /* y = A x through the compressed operator (h2_matrix.hpp:80-137), host buffers, nrhs columns. */
 int h2g_matvec(h2g_context* ctx, const h2g_matrix* m, const double* x, double* y, int32_t nrhs, h2g_error* err);
+
+/* ---- H2LU v1 container (serialize.hpp:27-343) ----------------------------
+ * The reference's on-disk format, byte compatible: little-endian, header
+ * "H2LU" / version 1 / kind (1 matrix, 2 chain, 3 vector), column-major
+ * complex128 matrices. Loads validate like the reference loaders and fail
+ * with H2G_ERR_INVALID_INPUT (SerializationError) on malformed files. */
+/* save_h2 (:186-196); the matrix must know its points (h2g_matrix_build, or
+ * points_tree / perm / leafsize in the upload desc) */
+int h2g_matrix_save(const h2g_matrix* m, const char* path, h2g_error* err);
+/* load_h2 (:198-243): the block partition is recomputed from the stored
+ * tree, the data uploaded to the device */
+int h2g_matrix_load(h2g_context* ctx, const char* path, h2g_matrix** out, h2g_error* err);
+/* save_chain (:245-284): the chain of a factorization of `source` (whose
+ * tree the file carries) downloaded into the reference's record layout */
+int h2g_chain_save(const h2g_chain* c, const h2g_matrix* source, const char* path, h2g_error* err);
+/* load_chain (:286-343) into a device chain that h2g_solve can apply (the
+ * records' elimination order is kept; triangular inverses formed on load) */
+int h2g_chain_load(h2g_context* ctx, const char* path, h2g_chain** out, h2g_error* err);
+/* The tree permutation (tree index -> original index) of the chain's matrix
+ * (the CLI applies it to vectors on the way in and out, h2lu_cli.cpp:47-57) */
+int h2g_chain_perm_tree(const h2g_chain* c, int64_t* perm);
+/* save_vector / load_vector (:345-353), host only. load: call with
+ * data == NULL to get the length in *n, then again with a buffer of 2 n doubles */
+int h2g_vector_save(const char* path, const double* data, int64_t n, h2g_error* err);
+int h2g_vector_load(const char* path, double* data, int64_t* n, h2g_error* err);
 
 /* y[q] = sum_j Z(rows[q], j) x[j] with Z generated directly from the kernel
  * (the reference's assemble_block, kernel.hpp:64-102): the north_star's dense

@@ -8,6 +8,7 @@
 #include <random>
 
 #include "factor.hpp"
+#include "serialize.hpp"
 
 using namespace h2o;
 
@@ -57,6 +58,8 @@ int guarded(F&& f) {
     return fail(3, e.what());
   } catch (const UndefinedMetricError& e) {
     return fail(5, e.what());
+  } catch (const ser::SerializationError& e) {
+    return fail(6, e.what());
   } catch (const std::exception& e) {
     return fail(9, e.what());
   }
@@ -589,3 +592,43 @@ int orc_test_carried_embed(void* h, double* out) {
 }
 
 }  // extern "C"
+
+// ----------------------------------------------- H2LU v1 container (tests)
+extern "C" {
+// self-noise study: 1 = accumulate GEMM inner products last-to-first
+void orc_set_gemm_order(int reverse) { gemm_order_flag() = reverse ? 1 : 0; }
+int64_t orc_h2_n(void* h) { return static_cast<H2H*>(h)->A.n(); }
+int orc_h2_save(void* h, const char* path) {
+  return guarded([&] { ser::save_h2(path, static_cast<H2H*>(h)->A); });
+}
+void* orc_h2_load(const char* path) {
+  H2H* out = nullptr;
+  guarded([&] { out = new H2H{ser::load_h2(path), KernelSpec{}}; });
+  return out;
+}
+int orc_chain_save(void* c, const char* path) {
+  return guarded([&] { ser::save_chain(path, static_cast<ChainH*>(c)->c); });
+}
+void* orc_chain_load(const char* path) {
+  ChainH* out = nullptr;
+  guarded([&] { out = new ChainH{ser::load_chain(path)}; });
+  return out;
+}
+int orc_vector_save(const char* path, const double* x, int64_t n) {
+  return guarded([&] {
+    std::vector<cxd> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) v[static_cast<size_t>(i)] = cxd(x[2 * i], x[2 * i + 1]);
+    ser::save_vector(path, v);
+  });
+}
+int orc_vector_load(const char* path, double* x, int64_t* n) {
+  return guarded([&] {
+    const auto v = ser::load_vector(path);
+    if (x) {
+      if (*n < static_cast<int64_t>(v.size())) throw InvalidInputError("vector_load: buffer too short");
+      for (size_t i = 0; i < v.size(); ++i) x[2 * i] = v[i].real(), x[2 * i + 1] = v[i].imag();
+    }
+    *n = static_cast<int64_t>(v.size());
+  });
+}
+}

@@ -162,13 +162,14 @@ struct Mat {
 // Summation-order switch for the oracle self-noise study (H2O_GEMM_ORDER=reverse
 // accumulates the inner dimension last-to-first, as a differently blocked BLAS
 // would): the same algorithm with rounding-level differences. Default: forward.
-inline bool gemm_reverse_k() {
-  static const bool rev = [] {
+inline int& gemm_order_flag() {
+  static int flag = [] {
     const char* e = std::getenv("H2O_GEMM_ORDER");
-    return e && std::string(e) == "reverse";
+    return e && std::string(e) == "reverse" ? 1 : 0;
   }();
-  return rev;
+  return flag;
 }
+inline bool gemm_reverse_k() { return gemm_order_flag() != 0; }
 
 // C += alpha * A * B (all column-major, plain). A and C are split into real
 // and imaginary planes so the inner loops are pure FMA streams, and four

@@ -114,6 +114,14 @@ def lib():
             "orc_test_stepwise": (C.c_int, [P, C.c_double, C.c_int, D]),
             "orc_test_fill_free_bits": (C.c_int, [P, C.c_double, D]),
             "orc_test_carried_embed": (C.c_int, [P, D]),
+            "orc_h2_save": (C.c_int, [P, C.c_char_p]),
+            "orc_h2_n": (C.c_int64, [P]),
+            "orc_set_gemm_order": (None, [C.c_int]),
+            "orc_h2_load": (P, [C.c_char_p]),
+            "orc_chain_save": (C.c_int, [P, C.c_char_p]),
+            "orc_chain_load": (P, [C.c_char_p]),
+            "orc_vector_save": (C.c_int, [C.c_char_p, D, C.c_int64]),
+            "orc_vector_load": (C.c_int, [C.c_char_p, D, I64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -536,3 +544,52 @@ def truncated_row_basis(B, eps, floor=0.0):
     r = np.zeros(1, np.int64)
     _check(lib().orc_truncated_row_basis(B.ctypes.data_as(D), m, f, eps, floor, U.ctypes.data_as(D), _i64(r)))
     return U[:, : int(r[0])]
+
+
+# ------------------------------------------- H2LU v1 container (serialize.hpp)
+def save_h2(A, path):
+    _check(lib().orc_h2_save(A.h, os.fsencode(path)))
+
+
+def load_h2(path):
+    """load_h2: tree from the file, partition recomputed (serialize.hpp:198-243)."""
+    h = lib().orc_h2_load(os.fsencode(path))
+    if not h:
+        _raise()
+    A = H2.__new__(H2)
+    A.h = h
+    A.kernel = None
+    A.eps_h2 = None
+    A.blocks = None
+    A.tree = None
+    A.n = int(lib().orc_h2_n(h))
+    return A
+
+
+def save_chain(ch, path):
+    _check(lib().orc_chain_save(ch.h, os.fsencode(path)))
+
+
+def load_chain(path):
+    h = lib().orc_chain_load(os.fsencode(path))
+    if not h:
+        _raise()
+    return Chain(h)
+
+
+def save_vector(path, v):
+    v = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
+    _check(lib().orc_vector_save(os.fsencode(path), _d(v.view(np.float64)), v.size))
+
+
+def load_vector(path):
+    n = np.zeros(1, np.int64)
+    _check(lib().orc_vector_load(os.fsencode(path), None, _i64(n)))
+    v = np.zeros(int(n[0]), np.complex128)
+    _check(lib().orc_vector_load(os.fsencode(path), _d(v.view(np.float64)), _i64(n)))
+    return v
+
+
+def set_gemm_order(reverse):
+    """Oracle self-noise switch: GEMM inner products accumulated last-to-first."""
+    lib().orc_set_gemm_order(1 if reverse else 0)

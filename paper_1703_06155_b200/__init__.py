@@ -120,6 +120,9 @@ class _Desc(C.Structure):
         ("coupling_data", _D),
         ("dense_offset", _I64),
         ("dense_data", _D),
+        ("points_tree", _D),
+        ("perm", _I64),
+        ("leafsize", C.c_int64),
     ]
 
 
@@ -156,6 +159,13 @@ SYMBOLS = {
     "h2g_random_rhs": (None, [C.c_int64, C.c_uint64, _D]),
     "h2g_set_profiling": (C.c_int, [_P, C.c_int32]),
     "h2g_chain_plan": (C.c_int, [_P, _D, _I32]),
+    "h2g_matrix_save": (C.c_int, [_P, C.c_char_p, C.POINTER(_Err)]),
+    "h2g_matrix_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_chain_save": (C.c_int, [_P, _P, C.c_char_p, C.POINTER(_Err)]),
+    "h2g_chain_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_vector_save": (C.c_int, [C.c_char_p, _D, C.c_int64, C.POINTER(_Err)]),
+    "h2g_chain_perm_tree": (C.c_int, [_P, _I64]),
+    "h2g_vector_load": (C.c_int, [C.c_char_p, _D, _I64, C.POINTER(_Err)]),
     "h2g_context_clear_plans": (C.c_int, [_P]),
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
 }
@@ -323,6 +333,12 @@ class H2Matrix:
         d.coupling_data = _d(a["coupling_data"].view(np.float64))
         d.dense_offset = _i64(a["dense_offset"])
         d.dense_data = _d(a["dense_data"].view(np.float64))
+        if arrays.get("points_tree") is not None and arrays.get("perm") is not None:
+            a["points_tree"] = np.ascontiguousarray(arrays["points_tree"], dtype=np.float64).reshape(-1, 3)
+            a["perm"] = np.ascontiguousarray(arrays["perm"], dtype=np.int64)
+            d.points_tree = _d(a["points_tree"])
+            d.perm = _i64(a["perm"])
+            d.leafsize = int(scalar(arrays.get("leafsize", 0)))
         err = _Err()
         h = _P()
         rc = lib().h2g_matrix_upload(ctx.h, C.byref(d), C.byref(h), C.byref(err))
@@ -340,6 +356,27 @@ class H2Matrix:
         kc = kernel.c()
         _check(lib().h2g_matrix_build(ctx.h, _d(pts), pts.shape[0], leafsize, eta, C.byref(kc), eps_h2, C.byref(h), C.byref(err)), err)
         return cls(h, ctx)
+
+    def save(self, path):
+        """save_h2 (serialize.hpp:186-196): the H2LU v1 container."""
+        err = _Err()
+        _check(lib().h2g_matrix_save(self.h, os.fsencode(path), C.byref(err)), err)
+
+    @classmethod
+    def load(cls, path, ctx=None):
+        """load_h2 (serialize.hpp:198-243) onto the device."""
+        ctx = ctx or Context.default()
+        err = _Err()
+        h = _P()
+        _check(lib().h2g_matrix_load(ctx.h, os.fsencode(path), C.byref(h), C.byref(err)), err)
+        return cls(h, ctx)
+
+    def perm(self):
+        """Tree permutation (tree index -> original index) without the data."""
+        out = np.zeros(self.n, np.int64)
+        if lib().h2g_matrix_download(self.h, None, None, _i64(out), *([None] * 13)):
+            raise H2GError("download failed")
+        return out
 
     def download(self):
         nc, L = self.num_clusters, self.depth
@@ -425,9 +462,10 @@ LEVEL_FIELDS = ("level", "nrecs", "rank_sum_before", "rank_sum_after", "eliminat
 class FactorChain:
     """Device-resident factorization (FactorChain, factorization.hpp:76-98)."""
 
-    def __init__(self, handle, matrix):
+    def __init__(self, handle, matrix, ctx=None):
         self.h = handle
-        self.matrix = matrix  # keep the context alive
+        self.matrix = matrix  # the factorized matrix (None for a chain loaded from a file)
+        self.ctx = ctx or (matrix.ctx if matrix is not None else None)
         info = np.zeros(6, np.int64)
         lib().h2g_chain_info(self.h, _i64(info))
         self.n, self.stop_level, self.root_size, self.num_levels, self.storage_bytes, sch = (int(v) for v in info)
@@ -437,6 +475,12 @@ class FactorChain:
         if getattr(self, "h", None) and _lib is not None:
             _lib.h2g_chain_destroy(self.h)
             self.h = None
+
+    def tree_perm(self):
+        """Tree permutation of the factorized matrix (tree index -> original index)."""
+        out = np.zeros(self.n, np.int64)
+        lib().h2g_chain_perm_tree(self.h, _i64(out))
+        return out
 
     def level(self, li):
         out = np.zeros(9, np.int64)
@@ -569,6 +613,41 @@ class FactorChain:
         """In-place solve on device memory (pointer from e.g. torch.Tensor.data_ptr())."""
         err = _Err()
         _check(lib().h2g_solve_device(self.h, C.cast(C.c_void_p(ptr), _D), n, nrhs, mode, C.byref(err)), err)
+
+
+def save_chain(chain, path, matrix=None):
+    """save_chain (serialize.hpp:245-284); the tree comes from the factorized matrix."""
+    m = matrix or chain.matrix
+    if m is None:
+        raise InvalidInputError("save_chain: the source matrix is needed for the tree")
+    err = _Err()
+    _check(lib().h2g_chain_save(chain.h, m.h, os.fsencode(path), C.byref(err)), err)
+
+
+def load_chain(path, ctx=None):
+    """load_chain (serialize.hpp:286-343) into a device chain h2g_solve applies."""
+    ctx = ctx or Context.default()
+    err = _Err()
+    h = _P()
+    _check(lib().h2g_chain_load(ctx.h, os.fsencode(path), C.byref(h), C.byref(err)), err)
+    return FactorChain(h, None, ctx)
+
+
+def save_vector(path, v):
+    """save_vector (serialize.hpp:345-348)."""
+    v = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
+    err = _Err()
+    _check(lib().h2g_vector_save(os.fsencode(path), _d(v.view(np.float64)), v.size, C.byref(err)), err)
+
+
+def load_vector(path):
+    """load_vector (serialize.hpp:350-353)."""
+    err = _Err()
+    n = C.c_int64(0)
+    _check(lib().h2g_vector_load(os.fsencode(path), None, C.byref(n), C.byref(err)), err)
+    v = np.zeros(n.value, np.complex128)
+    _check(lib().h2g_vector_load(os.fsencode(path), _d(v.view(np.float64)), C.byref(n), C.byref(err)), err)
+    return v
 
 
 def factorize(A, eps_fill_in, stop_level_override=None, schedule="reference"):

@@ -7,6 +7,7 @@
 // descriptor-driven batched copies/GEMMs; the remainder is LU-factored on the
 // device (:637-651). There is no CPU fallback.
 #include <atomic>
+#include <unistd.h>
 #include <functional>
 #include <cuda_runtime.h>
 
@@ -30,6 +31,7 @@
 #include "build.cuh"
 #include "factor.cuh"
 #include "plan.hpp"
+#include "serialize.hpp"
 #include "solve.cuh"
 
 using namespace h2g;
@@ -280,8 +282,9 @@ struct DBuf {
 std::atomic<size_t> g_pinned_bytes{0};
 size_t pinned_cap() {
   static const size_t cap = [] {
-    const char* e = std::getenv("H2G_HOST_STAGING_GB");
-    return (size_t)((e ? std::atof(e) : 96.0) * 1e9);
+    if (const char* e = std::getenv("H2G_HOST_STAGING_GB")) return (size_t)(std::atof(e) * 1e9);
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    return pages > 0 && psz > 0 ? (size_t)(0.6 * (double)pages * (double)psz) : (size_t)96e9;  // 60 % of host RAM
   }();
   return cap;
 }
@@ -292,6 +295,7 @@ struct HBuf {
   HBuf() = default;
   HBuf(const HBuf&) = delete;
   HBuf& operator=(const HBuf&) = delete;
+  HBuf(HBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
   ~HBuf() { release(); }
   void release() {
     if (p) cudaFreeHost(p), g_pinned_bytes -= bytes;
@@ -373,6 +377,7 @@ enum { PC_COMPLEMENT = 0, PC_GRAM, PC_COLNORM, PC_EIG1, PC_HEAD, PC_PANEL, PC_SC
 
 struct PlanCache {
   int stop = 0, schedule = 0;
+  int segments = 1;  // fill storage segments K the work lists were built for
   Structure key;  // the structure the plan was built for (checked on a fingerprint hit)
   std::vector<LevelSym> levels;
   std::vector<LevelSchedule> sched;
@@ -413,6 +418,9 @@ struct h2g_matrix {
   h2g_context* ctx = nullptr;
   Structure S;
   std::vector<int64_t> perm;
+  std::vector<double> points_tree;  // n x 3, tree order (for the H2LU container); empty if unknown
+  int64_t leafsize = 0;
+  int64_t shadow_guard = 4000;      // carried through the H2LU container (h2_matrix.hpp:38)
   double eps_h2 = 0.0;
   std::vector<int64_t> basis_rows, basis_rank, basis_off, coup_off, dense_off;
   int64_t basis_elems = 0, coup_elems = 0, dense_elems = 0;
@@ -462,6 +470,7 @@ struct h2g_chain {
   DBuf root;  // LU packed (n_root^2)
   DBuf ybuf, tmpbuf, partbuf;
   size_t storage_bytes = 0;
+  std::vector<int64_t> tree_perm;  // tree index -> original index of the factorized matrix (empty: identity)
   double factor_ms = 0.0, solve_ms = 0.0;
   double plan_ms = 0.0;     // host symbolic plan (get_plan), outside factor_ms
   bool plan_built = false;  // false: reused from the matrix / context plan cache
@@ -566,10 +575,28 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule, bool* built) {
   P->stop = stop;
   P->schedule = schedule;
   P->levels = build_levels(M->S, stop);
+  // fill storage: whole-level full blocks when the leaf level's fill pool
+  // is small next to HBM (no segment syncs), else 16 segments (compact cores
+  // once both sides have passed step 0); H2G_FILL_SEGMENTS overrides
+  int segments = 1;
+  if (const char* e = std::getenv("H2G_FILL_SEGMENTS")) {
+    segments = std::max(1, std::atoi(e));
+  } else if (!P->levels.empty()) {
+    const LevelSym& Y0 = P->levels[0];
+    const int first = Structure::first(Y0.level);
+    double fill = 0.0;
+    for (size_t f = 0; f < Y0.frow.size(); ++f)
+      fill += 16.0 * (double)(M->S.end[first + Y0.frow[f]] - M->S.begin[first + Y0.frow[f]]) *
+              (double)(M->S.end[first + Y0.fcol[f]] - M->S.begin[first + Y0.fcol[f]]);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    if (fill > 0.15 * (double)tot) segments = 16;
+  }
+  P->segments = segments;
   for (const auto& L : P->levels) {
     if (L.level >= stop && stop <= M->S.depth) {
       P->sched.push_back(build_schedule(L, schedule));
-      P->work.push_back(build_work(L, P->sched.back()));
+      P->work.push_back(build_work(L, P->sched.back(), segments));
     }
   }
   {
@@ -756,6 +783,9 @@ int h2g_matrix_upload(h2g_context* ctx, const h2g_matrix_desc* d, h2g_matrix** o
     if (M->basis_elems) CK(cudaMemcpyAsync(M->basis.p, d->basis_data, M->basis_elems * 16, cudaMemcpyHostToDevice, s));
     if (M->coup_elems) CK(cudaMemcpyAsync(M->coup.p, d->coupling_data, M->coup_elems * 16, cudaMemcpyHostToDevice, s));
     if (M->dense_elems) CK(cudaMemcpyAsync(M->dense.p, d->dense_data, M->dense_elems * 16, cudaMemcpyHostToDevice, s));
+    if (d->points_tree) M->points_tree.assign(d->points_tree, d->points_tree + 3 * S.n);
+    if (d->perm) M->perm.assign(d->perm, d->perm + S.n);
+    M->leafsize = d->leafsize;
     CK(cudaStreamSynchronize(s));
     ++ctx->refs;  // the matrix holds the context
     *out = M.release();
@@ -772,6 +802,10 @@ int h2g_matrix_build(h2g_context* ctx, const double* points, int64_t n, int64_t 
     M->ctx = ctx;
     M->S = build_structure(points, n, leafsize, eta, &M->perm);
     M->eps_h2 = eps_h2;
+    M->leafsize = leafsize;
+    M->points_tree.resize(3 * (size_t)n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) M->points_tree[3 * i + a] = points[3 * M->perm[i] + a];
     BuildResult R = build_h2_device(M->S, points, M->perm, *kernel, eps_h2, ctx->stream);
     M->basis_rows = std::move(R.basis_rows);
     M->basis_rank = std::move(R.basis_rank);
@@ -909,6 +943,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     C->depth = L;
     C->eps = eps;
     C->plan_ms = plan_s * 1e3;
+    C->tree_perm = M->perm;
     C->plan_built = plan_built;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevError), st));
     ctx->prof.reset();
@@ -1020,6 +1055,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     };
     std::vector<cplx*> core_ptr_h;  // per fill of the running level: its compact core (host copy of DevLevel::core_ptr)
     std::vector<DBuf> core_chunks;   // the cores, one chunk per segment; released after the merge
+    std::vector<HBuf> core_hchunks;  // ... or in pinned host memory when HBM is short
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
         const LevelSym& Y = P->levels[li];
@@ -1395,9 +1431,21 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           for (size_t q = 0; q < cores.size(); ++q) coff[q] = ctop, ctop += (long long)kf[Y.frow[cores[q]]] * kf[Y.fcol[cores[q]]];
           if (ctop > 0) {
             ensure((size_t)ctop * 16, nullptr);
-            core_chunks.emplace_back();
-            core_chunks.back().alloc((size_t)ctop * 16, st, true);
-            for (size_t q = 0; q < cores.size(); ++q) core_ptr_h[cores[q]] = core_chunks.back().as<cplx>() + coff[q];
+            cplx* base = nullptr;
+            if (BlockCache::get().headroom() >= (size_t)ctop * 16 + kMargin) {
+              core_chunks.emplace_back();
+              core_chunks.back().alloc((size_t)ctop * 16, st, true);
+              base = core_chunks.back().as<cplx>();
+            } else {
+              // HBM is short: this segment's cores live in pinned, device-mapped
+              // host memory (written by the collapse and the later core
+              // deposits, read once by the merge)
+              core_hchunks.emplace_back();
+              core_hchunks.back().alloc((size_t)ctop * 16);
+              CK(cudaMemsetAsync(core_hchunks.back().p, 0, (size_t)ctop * 16, st));
+              base = core_hchunks.back().as<cplx>();
+            }
+            for (size_t q = 0; q < cores.size(); ++q) core_ptr_h[cores[q]] = base + coff[q];
           }
           const cplx* chainp = CL->arena.as<cplx>();
           auto V = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kf[t]) * cur.bsz[t]; };
@@ -1861,17 +1909,20 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         CK(cudaGetLastError());
         mark("merge launched");
         CK(cudaStreamSynchronize(st));  // temporaries die here
-        size_t core_bytes = 0;
+        size_t core_bytes = 0, core_host_bytes = 0;
         for (auto& ch : core_chunks) core_bytes += ch.bytes;
+        for (auto& ch : core_hchunks) core_host_bytes += ch.bytes;
         core_chunks.clear();
+        core_hchunks.clear();
 
         if (verbose) {
           size_t fr = 0, tot = 0;
           cudaMemGetInfo(&fr, &tot);
           std::fprintf(stderr,
-                       "[h2g] level %d: merge done at %.3f s; fill front pool %.2f GB (all full blocks %.2f GB, %d segments), cores %.2f GB, next D %.2f GB, "
-                       "next F %.2f GB; device free %.2f of %.2f GB\n",
+                       "[h2g] level %d: merge done at %.3f s; fill front pool %.2f GB (all full blocks %.2f GB, %d segments), cores %.2f GB "
+                       "(+ %.2f GB host-staged), next D %.2f GB, next F %.2f GB; device free %.2f of %.2f GB\n",
                        l, wall() - tlev, cur.front.pool_elems * 16.0 / 1e9, cur.front.full_elems_total * 16.0 / 1e9, cur.front.K, core_bytes / 1e9,
+                       core_host_bytes / 1e9,
                        nxt.D.bytes / 1e9, nxt.F.bytes / 1e9, fr / 1e9, tot / 1e9);
           std::fprintf(stderr, "[h2g] chains offloaded to host so far: %.2f GB\n", offloaded / 1e9);
         }
@@ -2386,6 +2437,533 @@ int h2g_chain_schur_executed(const h2g_chain* c, double* out) {
   out[0] = c->schur_flops_exec;
   out[1] = c->schur_bytes_exec;
   return H2G_OK;
+}
+
+}  // extern "C"
+
+// =================================================== H2LU v1 container
+namespace {
+
+template <class F>
+void io_guard(F&& f) {
+  try {
+    f();
+  } catch (const Error&) {
+    throw;
+  } catch (const std::runtime_error& e) {  // serialize: malformed file (SerializationError)
+    throw Error(H2G_ERR_INVALID_INPUT, e.what());
+  }
+}
+
+io::TreeData tree_of(const h2g_matrix* m) {
+  if (m->points_tree.empty() || m->leafsize < 1)
+    throw Error(H2G_ERR_INVALID_INPUT, "save: the matrix does not know its points / leaf size (build it with h2g_matrix_build, or pass points_tree, "
+                                       "perm and leafsize in the upload desc)");
+  io::TreeData t;
+  t.n = m->S.n;
+  t.depth = m->S.depth;
+  t.leafsize = m->leafsize;
+  if (m->perm.empty()) {
+    t.perm.resize(t.n);
+    for (int64_t i = 0; i < t.n; ++i) t.perm[i] = i;
+  } else {
+    t.perm = m->perm;
+  }
+  t.points = m->points_tree;
+  t.begin = m->S.begin;
+  t.end = m->S.end;
+  return t;
+}
+
+io::HMat hmat(int64_t r, int64_t c, const cplx* src_host) {
+  io::HMat M;
+  M.rows = r, M.cols = c;
+  M.data.resize((size_t)(r * c));
+  if (r * c) std::memcpy(M.data.data(), src_host, (size_t)(r * c) * 16);
+  return M;
+}
+
+// Inverse of a unit-lower (lower = true) or upper e x e matrix, column-major.
+std::vector<std::complex<double>> tri_inverse(const std::vector<std::complex<double>>& A, int e, bool lower) {
+  std::vector<std::complex<double>> X((size_t)e * e, 0.0);
+  for (int j = 0; j < e; ++j) {
+    // solve A x = e_j
+    std::vector<std::complex<double>> x(e, 0.0);
+    x[j] = 1.0;
+    if (lower) {
+      for (int p = 0; p < e; ++p)
+        for (int i = p + 1; i < e; ++i) x[i] -= A[i + (size_t)p * e] * x[p];
+    } else {
+      for (int p = e - 1; p >= 0; --p) {
+        x[p] /= A[p + (size_t)p * e];
+        for (int i = 0; i < p; ++i) x[i] -= A[i + (size_t)p * e] * x[p];
+      }
+    }
+    for (int i = 0; i < e; ++i) X[i + (size_t)j * e] = x[i];
+  }
+  return X;
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2g_matrix_save(const h2g_matrix* m, const char* path, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!m || !path) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    CK(cudaSetDevice(m->ctx->device));
+    io_guard([&] {
+      const Structure& S = m->S;
+      io::MatrixFile F;
+      F.tree = tree_of(m);
+      F.eta = S.eta;
+      F.eps_h2 = m->eps_h2;
+      F.shadow_guard = m->shadow_guard;
+      cudaStream_t st = m->ctx->stream;
+      std::vector<std::complex<double>> basis(m->basis_elems), coup(m->coup_elems), dense(m->dense_elems);
+      if (m->basis_elems) CK(cudaMemcpyAsync(basis.data(), m->basis.p, m->basis_elems * 16, cudaMemcpyDeviceToHost, st));
+      if (m->coup_elems) CK(cudaMemcpyAsync(coup.data(), m->coup.p, m->coup_elems * 16, cudaMemcpyDeviceToHost, st));
+      if (m->dense_elems) CK(cudaMemcpyAsync(dense.data(), m->dense_ptr(), m->dense_elems * 16, cudaMemcpyDefault, st));
+      CK(cudaStreamSynchronize(st));
+      const int nc = S.num_clusters();
+      F.bases.resize(nc);
+      for (int id = 0; id < nc; ++id)
+        F.bases[id] = hmat(m->basis_rows[id], m->basis_rank[id], reinterpret_cast<const cplx*>(basis.data() + m->basis_off[id]));
+      F.couplings.resize(S.depth + 1);
+      for (int l = 0; l <= S.depth; ++l)
+        for (size_t q = 0; q < S.adm[l].size(); ++q) {
+          const int64_t g = S.adm_offset[l] + (int64_t)q;
+          F.couplings[l].push_back(hmat(m->basis_rank[S.adm[l][q].row], m->basis_rank[S.adm[l][q].col],
+                                        reinterpret_cast<const cplx*>(coup.data() + m->coup_off[g])));
+        }
+      for (size_t q = 0; q < S.leaf.size(); ++q) {
+        const auto& pr = S.leaf[q];
+        F.dense.push_back(hmat(S.end[pr.row] - S.begin[pr.row], S.end[pr.col] - S.begin[pr.col], reinterpret_cast<const cplx*>(dense.data() + m->dense_off[q])));
+      }
+      io::save_matrix(path, F);
+    });
+  });
+}
+
+int h2g_matrix_load(h2g_context* ctx, const char* path, h2g_matrix** out, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !path || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    io_guard([&] {
+      io::MatrixReader R(path);
+      io::MatrixFile& H = R.head();
+      Structure S = structure_from_tree(H.tree.points.data(), H.tree.n, H.tree.depth, H.tree.begin, H.tree.end, H.eta);
+      std::vector<int64_t> adm_count(S.depth + 1);
+      for (int l = 0; l <= S.depth; ++l) adm_count[l] = (int64_t)S.adm[l].size();
+      R.read_rest(adm_count, (int64_t)S.leaf.size());
+      io::MatrixFile F = R.take();
+      const int nc = S.num_clusters();
+      // flatten into an upload descriptor
+      std::vector<int64_t> brows(nc), brank(nc), boff(nc), coff, doff, aoff(S.depth + 2, 0), soff(S.depth + 2, 0);
+      std::vector<int32_t> apairs, spairs, lpairs;
+      std::vector<std::complex<double>> bdata, cdata, ddata;
+      for (int id = 0; id < nc; ++id) {
+        brows[id] = F.bases[id].rows;
+        brank[id] = F.bases[id].cols;
+        boff[id] = (int64_t)bdata.size();
+        bdata.insert(bdata.end(), F.bases[id].data.begin(), F.bases[id].data.end());
+      }
+      for (int l = 0; l <= S.depth; ++l) {
+        aoff[l + 1] = aoff[l] + (int64_t)S.adm[l].size();
+        soff[l + 1] = soff[l] + (int64_t)S.split[l].size();
+        for (size_t q = 0; q < S.adm[l].size(); ++q) {
+          const auto& pr = S.adm[l][q];
+          const io::HMat& C = F.couplings[l][q];
+          if (C.rows != brank[pr.row] || C.cols != brank[pr.col]) throw std::runtime_error("serialize: coupling dims inconsistent with basis ranks");
+          apairs.push_back(pr.row), apairs.push_back(pr.col);
+          coff.push_back((int64_t)cdata.size());
+          cdata.insert(cdata.end(), C.data.begin(), C.data.end());
+        }
+        for (const auto& pr : S.split[l]) spairs.push_back(pr.row), spairs.push_back(pr.col);
+      }
+      for (size_t q = 0; q < S.leaf.size(); ++q) {
+        const auto& pr = S.leaf[q];
+        const io::HMat& D = F.dense[q];
+        if (D.rows != S.end[pr.row] - S.begin[pr.row] || D.cols != S.end[pr.col] - S.begin[pr.col])
+          throw std::runtime_error("serialize: dense block dims inconsistent with tree");
+        lpairs.push_back(pr.row), lpairs.push_back(pr.col);
+        doff.push_back((int64_t)ddata.size());
+        ddata.insert(ddata.end(), D.data.begin(), D.data.end());
+      }
+      h2g_matrix_desc d{};
+      d.n = S.n;
+      d.depth = S.depth;
+      d.eta = S.eta;
+      d.eps_h2 = F.eps_h2;
+      d.cluster_begin = S.begin.data();
+      d.cluster_end = S.end.data();
+      d.adm_offsets = aoff.data();
+      d.adm_pairs = apairs.data();
+      d.split_offsets = soff.data();
+      d.split_pairs = spairs.data();
+      d.num_leaf_pairs = (int64_t)S.leaf.size();
+      d.leaf_pairs = lpairs.data();
+      d.basis_rows = brows.data();
+      d.basis_rank = brank.data();
+      d.basis_offset = boff.data();
+      d.basis_data = reinterpret_cast<const double*>(bdata.data());
+      d.coupling_offset = coff.data();
+      d.coupling_data = reinterpret_cast<const double*>(cdata.data());
+      d.dense_offset = doff.data();
+      d.dense_data = reinterpret_cast<const double*>(ddata.data());
+      d.points_tree = F.tree.points.data();
+      d.perm = F.tree.perm.data();
+      d.leafsize = F.tree.leafsize;
+      h2g_error e2{};
+      const int rc = h2g_matrix_upload(ctx, &d, out, &e2);
+      if (rc) throw Error(rc, e2.msg);
+      (*out)->shadow_guard = F.shadow_guard;
+    });
+  });
+}
+
+int h2g_chain_save(const h2g_chain* c, const h2g_matrix* source, const char* path, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!c || !source || !path) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    if (source->S.n != c->n) throw Error(H2G_ERR_INVALID_INPUT, "save_chain: the chain and the matrix differ in size");
+    CK(cudaSetDevice(c->ctx->device));
+    io_guard([&] {
+      io::ChainFile F;
+      F.tree = tree_of(source);
+      F.n = c->n;
+      F.stop_level = c->stop_level;
+      F.eps_fill_in = c->eps;
+      cudaStream_t st = c->ctx->stream;
+      for (const auto& CLp : c->levels) {
+        const ChainLevelHost& CL = *CLp;
+        std::vector<cplx> arena(CL.chain_bytes() / 16);
+        if (!arena.empty()) CK(cudaMemcpyAsync(arena.data(), CL.chain_ptr(), arena.size() * 16, cudaMemcpyDefault, st));
+        CK(cudaStreamSynchronize(st));
+        io::LevelFile LF;
+        LF.level = CL.level;
+        const size_t nrec = CL.rec_cluster.size();
+        for (size_t ri = 0; ri < nrec; ++ri) {
+          const int64_t* r = CL.rec.data() + 10 * ri;
+          const int t = CL.rec_cluster[ri];
+          const int b = CL.bsz[t], kf = CL.kfin[t], e = b - kf;
+          io::RecordData R;
+          R.cluster = (int32_t)r[0];
+          R.level = (int32_t)r[1];
+          R.pos = r[2], R.bsize = r[3], R.eliminated = r[4], R.rank_before = r[5], R.rank_after = r[6], R.fill_targets = r[7];
+          R.Qtilde = hmat(b, b, arena.data() + CL.Qt_off[t]);
+          R.L11 = hmat(e, e, arena.data() + CL.L11_off[t]);
+          R.U11 = hmat(e, e, arena.data() + CL.U11_off[t]);
+          if (e > 0) {
+            for (int a = CL.R_ptr[t]; a < CL.R_ptr[t + 1]; ++a)
+              R.Lbar.push_back({CL.pos[CL.R_nb[a]], hmat(CL.bsz[CL.R_nb[a]], e, arena.data() + CL.Lbar_off[a])});
+            if (kf > 0) R.Lbar.push_back({CL.pos[t] + e, hmat(kf, e, arena.data() + CL.Lself_off[t])});
+            for (int a = CL.C_ptr[t]; a < CL.C_ptr[t + 1]; ++a)
+              R.Ubar.push_back({CL.pos[CL.C_nb[a]], hmat(e, CL.bsz[CL.C_nb[a]], arena.data() + CL.Ubar_off[a])});
+            if (kf > 0) R.Ubar.push_back({CL.pos[t] + e, hmat(e, kf, arena.data() + CL.Uself_off[t])});
+          }
+          LF.recs.push_back(std::move(R));
+        }
+        LF.perm_level = CL.level;
+        LF.src = CL.src;
+        LF.active_after = CL.diag[8];
+        LF.diag_level = CL.level;
+        LF.rank_sum_before = CL.diag[2], LF.rank_sum_after = CL.diag[3], LF.eliminated = CL.diag[4], LF.ledger_blocks = CL.diag[5];
+        LF.chain_bytes = (uint64_t)CL.diag[6];
+        F.levels.push_back(std::move(LF));
+      }
+      const int64_t r = c->root_size;
+      F.root_size = r;
+      F.root_l.rows = F.root_l.cols = F.root_u.rows = F.root_u.cols = r;
+      if (r > 0) {
+        std::vector<std::complex<double>> A((size_t)r * r);
+        CK(cudaMemcpyAsync(A.data(), c->root.p, (size_t)r * r * 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        F.root_l.data.assign((size_t)r * r, 0.0);
+        F.root_u.data.assign((size_t)r * r, 0.0);
+        for (int64_t j = 0; j < r; ++j)
+          for (int64_t i = 0; i < r; ++i) {
+            const auto v = A[i + j * r];
+            if (i > j) F.root_l.data[i + j * r] = v;
+            else F.root_u.data[i + j * r] = v;
+            if (i == j) F.root_l.data[i + j * r] = 1.0;
+          }
+      }
+      io::save_chain(path, F);
+    });
+  });
+}
+
+int h2g_chain_load(h2g_context* ctx, const char* path, h2g_chain** out, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!ctx || !path || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);
+    CK(cudaSetDevice(ctx->device));
+    io_guard([&] {
+      io::ChainFile F = io::load_chain(path);
+      cudaStream_t st = ctx->stream;
+      auto C = std::make_unique<h2g_chain>();
+      C->ctx = ctx;
+      C->n = F.n;
+      C->stop_level = F.stop_level;
+      C->schedule = H2G_SCHEDULE_REFERENCE;
+      C->depth = F.tree.depth;
+      C->eps = F.eps_fill_in;
+      C->tree_perm = F.tree.perm;
+      for (const io::LevelFile& LF : F.levels) {
+        const int l = LF.level;
+        if (l < 0 || l > F.tree.depth) throw std::runtime_error("serialize: level out of range");
+        const int nl = 1 << l, first = Structure::first(l);
+        auto CL = std::make_unique<ChainLevelHost>();
+        CL->level = l;
+        CL->bsz.assign(nl, 0);
+        CL->kfin.assign(nl, 0);
+        CL->korig.assign(nl, 0);
+        CL->pos.assign(nl, 0);
+        std::vector<int> rec_of(nl, -1);
+        for (size_t ri = 0; ri < LF.recs.size(); ++ri) {
+          const io::RecordData& R = LF.recs[ri];
+          const int t = R.cluster - first;
+          if (R.level != l || t < 0 || t >= nl || rec_of[t] >= 0) throw std::runtime_error("serialize: record cluster does not belong to its level");
+          rec_of[t] = (int)ri;
+          CL->bsz[t] = (int)R.bsize;
+          CL->kfin[t] = (int)(R.bsize - R.eliminated);
+          CL->korig[t] = (int)R.rank_before;
+          CL->pos[t] = R.pos;
+        }
+        for (int t = 0; t < nl; ++t)
+          if (rec_of[t] < 0) throw std::runtime_error("serialize: level block misses a cluster record");
+        // segment start -> cluster (neighbour identification of the off-diagonal blocks)
+        std::unordered_map<long long, int> seg_at;
+        for (int t = 0; t < nl; ++t)
+          if (CL->bsz[t] > 0) seg_at[CL->pos[t]] = t;
+        auto seg_of = [&](int64_t pos) {
+          auto it = seg_at.find(pos);
+          if (it == seg_at.end()) throw std::runtime_error("serialize: off-diagonal block does not start a cluster segment");
+          return it->second;
+        };
+        // neighbour lists (record order of the file = ascending cluster within
+        // a block list, self last) and chain offsets
+        CL->R_ptr.assign(1, 0);
+        CL->C_ptr.assign(1, 0);
+        std::vector<std::vector<int>> nbg(nl);
+        for (int t = 0; t < nl; ++t) {
+          const io::RecordData& R = LF.recs[rec_of[t]];
+          const int b = CL->bsz[t], e = b - CL->kfin[t];
+          for (const auto& blk : R.Lbar) {
+            if (blk.pos >= R.pos && blk.pos < R.pos + b) continue;  // self block
+            const int j = seg_of(blk.pos);
+            if (blk.M.rows != CL->bsz[j] || blk.M.cols != e) throw std::runtime_error("serialize: Lbar block dims inconsistent");
+            CL->R_nb.push_back(j);
+            nbg[t].push_back(j), nbg[j].push_back(t);
+          }
+          CL->R_ptr.push_back((int)CL->R_nb.size());
+          for (const auto& blk : R.Ubar) {
+            if (blk.pos >= R.pos && blk.pos < R.pos + b) continue;
+            const int c2 = seg_of(blk.pos);
+            if (blk.M.cols != CL->bsz[c2] || blk.M.rows != e) throw std::runtime_error("serialize: Ubar block dims inconsistent");
+            CL->C_nb.push_back(c2);
+            nbg[t].push_back(c2), nbg[c2].push_back(t);
+          }
+          CL->C_ptr.push_back((int)CL->C_nb.size());
+        }
+        int bm = 1;
+        for (int t = 0; t < nl; ++t) bm = std::max(bm, CL->bsz[t]);
+        std::vector<long long> Qt(nl), L11(nl), U11(nl), Li(nl), Ui(nl), Ls(nl), Us(nl), Lb(CL->R_nb.size()), Ub(CL->C_nb.size());
+        long long top = 0;
+        for (int t = 0; t < nl; ++t) {
+          const long long b = CL->bsz[t], kf = CL->kfin[t], e = b - kf;
+          Qt[t] = top, top += b * b;
+          L11[t] = top, top += e * e;
+          U11[t] = top, top += e * e;
+          Li[t] = top, top += e * e;
+          Ui[t] = top, top += e * e;
+          Ls[t] = top, top += kf * e;
+          Us[t] = top, top += kf * e;
+          for (int a = CL->R_ptr[t]; a < CL->R_ptr[t + 1]; ++a) Lb[a] = top, top += (long long)CL->bsz[CL->R_nb[a]] * e;
+          for (int a = CL->C_ptr[t]; a < CL->C_ptr[t + 1]; ++a) Ub[a] = top, top += (long long)CL->bsz[CL->C_nb[a]] * e;
+        }
+        std::vector<std::complex<double>> arena((size_t)std::max<long long>(top, 1), 0.0);
+        auto put = [&](long long off, const io::HMat& M) { std::copy(M.data.begin(), M.data.end(), arena.begin() + off); };
+        for (int t = 0; t < nl; ++t) {
+          const io::RecordData& R = LF.recs[rec_of[t]];
+          const int b = CL->bsz[t], kf = CL->kfin[t], e = b - kf;
+          put(Qt[t], R.Qtilde);
+          if (e == 0) continue;
+          put(L11[t], R.L11);
+          put(U11[t], R.U11);
+          const auto li = tri_inverse(R.L11.data, e, true), ui = tri_inverse(R.U11.data, e, false);
+          std::copy(li.begin(), li.end(), arena.begin() + Li[t]);
+          std::copy(ui.begin(), ui.end(), arena.begin() + Ui[t]);
+          int ar = CL->R_ptr[t], ac = CL->C_ptr[t];
+          for (const auto& blk : R.Lbar) {
+            if (blk.pos >= R.pos && blk.pos < R.pos + b) {
+              if (blk.M.rows != kf || blk.M.cols != e) throw std::runtime_error("serialize: self Lbar block dims inconsistent");
+              put(Ls[t], blk.M);
+            } else {
+              put(Lb[ar++], blk.M);
+            }
+          }
+          for (const auto& blk : R.Ubar) {
+            if (blk.pos >= R.pos && blk.pos < R.pos + b) {
+              if (blk.M.cols != kf || blk.M.rows != e) throw std::runtime_error("serialize: self Ubar block dims inconsistent");
+              put(Us[t], blk.M);
+            } else {
+              put(Ub[ac++], blk.M);
+            }
+          }
+        }
+        // solve schedule: dependency wavefronts of the file's record order
+        // over the neighbour graph (as build_schedule's reference mode)
+        std::vector<int> key(nl, 0), order;
+        for (const auto& R : LF.recs) order.push_back(R.cluster - first);
+        std::vector<int> rank_in(nl);
+        for (int q = 0; q < nl; ++q) rank_in[order[q]] = q;
+        int nb_batches = 0;
+        for (int t : order) {
+          int w = 0;
+          for (int x : nbg[t])
+            if (rank_in[x] < rank_in[t]) w = std::max(w, key[x] + 1);
+          key[t] = w;
+          nb_batches = std::max(nb_batches, w + 1);
+        }
+        std::vector<std::vector<int>> bat(nb_batches);
+        for (int t : order) bat[key[t]].push_back(t);
+        std::vector<int> batch_ptr(1, 0), batch_cl, batch_maxc, fs_ptr(1, 0);
+        std::vector<SolveTargetD> fs;
+        std::vector<SolveContribD> fc;
+        for (auto& bv : bat) {
+          struct T2 {
+            long long seg;
+            SolveContribD c;
+          };
+          std::vector<T2> tmp;
+          int mc = 0;
+          for (int t : bv) {
+            batch_cl.push_back(t);
+            mc = std::max(mc, CL->C_ptr[t + 1] - CL->C_ptr[t]);
+            for (int a = CL->R_ptr[t]; a < CL->R_ptr[t + 1]; ++a) tmp.push_back({CL->R_nb[a], {t, a}});
+            tmp.push_back({-1 - (long long)t, {t, -1 - t}});
+          }
+          batch_ptr.push_back((int)batch_cl.size());
+          batch_maxc.push_back(mc);
+          std::stable_sort(tmp.begin(), tmp.end(), [](const T2& x, const T2& y) { return x.seg < y.seg; });
+          for (size_t i = 0; i < tmp.size();) {
+            size_t j = i;
+            while (j < tmp.size() && tmp[j].seg == tmp[i].seg) ++j;
+            fs.push_back({(int)tmp[i].seg, (int)fc.size(), (int)(fc.size() + (j - i))});
+            for (size_t k = i; k < j; ++k) fc.push_back(tmp[k].c);
+            i = j;
+          }
+          fs_ptr.push_back((int)fs.size());
+        }
+        // device data
+        CL->arena.alloc((size_t)std::max<long long>(top, 1) * 16, st);
+        CK(cudaMemcpyAsync(CL->arena.p, arena.data(), (size_t)std::max<long long>(top, 1) * 16, cudaMemcpyHostToDevice, st));
+        Packer pk;
+        size_t o_bsz = pk.add(CL->bsz), o_pos = pk.add(CL->pos), o_kfin = pk.add(CL->kfin), o_Cp = pk.add(CL->C_ptr), o_Cn = pk.add(CL->C_nb);
+        size_t o_Qt = pk.add(Qt), o_L11 = pk.add(L11), o_U11 = pk.add(U11), o_Li = pk.add(Li), o_Ui = pk.add(Ui), o_Lb = pk.add(Lb), o_Ub = pk.add(Ub),
+               o_Ls = pk.add(Ls), o_Us = pk.add(Us), o_bat = pk.add(batch_cl);
+        size_t o_fs = pk.add_raw(fs.data(), fs.size()), o_fc = pk.add_raw(fc.data(), fc.size());
+        pk.upload(CL->meta, st);
+        const DBuf& mt = CL->meta;
+        SolveLevel& SL = CL->sl;
+        SL.nl = nl;
+        SL.bmax = bm;
+        SL.bsz = at<int>(mt, o_bsz);
+        SL.pos = at<long long>(mt, o_pos);
+        SL.kfin = at<int>(mt, o_kfin);
+        SL.C_ptr = at<int>(mt, o_Cp);
+        SL.C_nb = at<int>(mt, o_Cn);
+        SL.chain = CL->arena.as<cplx>();
+        SL.Qt_off = at<long long>(mt, o_Qt);
+        SL.L11_off = at<long long>(mt, o_L11);
+        SL.U11_off = at<long long>(mt, o_U11);
+        SL.Linv_off = at<long long>(mt, o_Li);
+        SL.Uinv_off = at<long long>(mt, o_Ui);
+        SL.Lbar_off = at<long long>(mt, o_Lb);
+        SL.Ubar_off = at<long long>(mt, o_Ub);
+        SL.Lself_off = at<long long>(mt, o_Ls);
+        SL.Uself_off = at<long long>(mt, o_Us);
+        CL->batch_ptr = batch_ptr;
+        CL->batch_maxc = batch_maxc;
+        CL->d_batch = at<int>(mt, o_bat);
+        CL->fs_ptr = fs_ptr;
+        CL->d_fs = at<SolveTargetD>(mt, o_fs);
+        CL->d_fc = at<SolveContribD>(mt, o_fc);
+        {
+          std::vector<int> sv(batch_ptr);
+          sv.insert(sv.end(), batch_maxc.begin(), batch_maxc.end());
+          sv.insert(sv.end(), fs_ptr.begin(), fs_ptr.end());
+          upload(CL->sched_buf, sv, st);
+          const int nb1 = (int)batch_ptr.size();
+          const int* base = CL->sched_buf.as<int>();
+          CL->sched = {nb1 - 1, base, CL->d_batch, base + nb1, base + nb1 + (nb1 - 1), CL->d_fs, CL->d_fc};
+          for (int bi = 0; bi + 1 < nb1; ++bi)
+            CL->part_need = std::max(CL->part_need, (size_t)(batch_ptr[bi + 1] - batch_ptr[bi]) * (batch_maxc[bi] + 1) * bm);
+        }
+        // host inspection copies
+        CL->Qt_off = Qt, CL->L11_off = L11, CL->U11_off = U11, CL->Lbar_off = Lb, CL->Ubar_off = Ub, CL->Lself_off = Ls, CL->Uself_off = Us;
+        for (size_t ri = 0; ri < LF.recs.size(); ++ri) {
+          const io::RecordData& R = LF.recs[ri];
+          const int t = R.cluster - first;
+          const int e = (int)R.eliminated;
+          const int nlb = e > 0 ? (CL->R_ptr[t + 1] - CL->R_ptr[t]) + (CL->kfin[t] > 0) : 0;
+          const int nub = e > 0 ? (CL->C_ptr[t + 1] - CL->C_ptr[t]) + (CL->kfin[t] > 0) : 0;
+          const int64_t rr[10] = {R.cluster, R.level, R.pos, R.bsize, R.eliminated, R.rank_before, R.rank_after, R.fill_targets, nlb, nub};
+          CL->rec.insert(CL->rec.end(), rr, rr + 10);
+          CL->rec_cluster.push_back(t);
+        }
+        CL->diag = {l, (int64_t)LF.recs.size(), LF.rank_sum_before, LF.rank_sum_after, LF.eliminated, LF.ledger_blocks, (int64_t)LF.chain_bytes,
+                    (int64_t)LF.src.size(), LF.active_after};
+        CL->src = LF.src;
+        upload(CL->d_src, CL->src, st);
+        C->storage_bytes = (size_t)LF.chain_bytes;
+        C->levels.push_back(std::move(CL));
+      }
+      C->root_size = F.root_size;
+      if (F.root_size > 0) {
+        const int64_t r = F.root_size;
+        std::vector<std::complex<double>> A((size_t)r * r);
+        for (int64_t j = 0; j < r; ++j)
+          for (int64_t i = 0; i < r; ++i) A[i + j * r] = i > j ? F.root_l.data[i + j * r] : F.root_u.data[i + j * r];
+        C->root.alloc((size_t)r * r * 16, st);
+        CK(cudaMemcpyAsync(C->root.p, A.data(), (size_t)r * r * 16, cudaMemcpyHostToDevice, st));
+      }
+      CK(cudaStreamSynchronize(st));
+      ++ctx->refs;  // the chain holds the context
+      *out = C.release();
+    });
+  });
+}
+
+int h2g_chain_perm_tree(const h2g_chain* c, int64_t* perm) {
+  if (!c || !perm) return H2G_ERR_INVALID_INPUT;
+  for (int64_t i = 0; i < c->n; ++i) perm[i] = c->tree_perm.empty() ? i : c->tree_perm[i];
+  return H2G_OK;
+}
+
+int h2g_vector_save(const char* path, const double* data, int64_t n, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!path || (n > 0 && !data) || n < 0) throw Error(H2G_ERR_INVALID_INPUT, "vector_save: bad arguments");
+    io_guard([&] {
+      std::vector<std::complex<double>> v((size_t)n);
+      if (n) std::memcpy(v.data(), data, (size_t)n * 16);
+      io::save_vector(path, v);
+    });
+  });
+}
+
+int h2g_vector_load(const char* path, double* data, int64_t* n, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!path || !n) throw Error(H2G_ERR_INVALID_INPUT, "vector_load: bad arguments");
+    io_guard([&] {
+      const auto v = io::load_vector(path);
+      if (data) {
+        if (*n < (int64_t)v.size()) throw Error(H2G_ERR_INVALID_INPUT, "vector_load: buffer too short");
+        std::memcpy(data, v.data(), v.size() * 16);
+      }
+      *n = (int64_t)v.size();
+    });
+  });
 }
 
 }  // extern "C"

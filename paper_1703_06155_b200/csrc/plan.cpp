@@ -74,6 +74,8 @@ double box_distance(const Box& a, const Box& b) {
 }
 }  // namespace
 
+static void partition(Structure& S, const std::vector<Box>& box);
+
 Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm_out) {
   if (n <= 0) throw std::invalid_argument("build: empty point cloud");
   if (leafsize < 1) throw std::invalid_argument("build: leafsize must be >= 1");
@@ -125,8 +127,19 @@ Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double
     stack.push_back({2 * it.id + 1, it.level + 1, it.b, mid});
     stack.push_back({2 * it.id + 2, it.level + 1, mid, it.e});
   }
-  S.adm.resize(static_cast<size_t>(depth) + 1);
-  S.split.resize(static_cast<size_t>(depth) + 1);
+  partition(S, box);
+  if (perm_out) *perm_out = std::move(perm);
+  return S;
+}
+
+// Block partition of an existing tree (block_tree.hpp:15-73): strict
+// admissibility max(diam) < eta * dist on the cluster bounding boxes.
+static void partition(Structure& S, const std::vector<Box>& box) {
+  const int depth = S.depth;
+  const double eta = S.eta;
+  S.adm.assign(static_cast<size_t>(depth) + 1, {});
+  S.split.assign(static_cast<size_t>(depth) + 1, {});
+  S.leaf.clear();
   auto level_of = [](int id) {
     int l = 0;
     while ((2 << l) - 1 <= id) ++l;
@@ -154,12 +167,40 @@ Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double
   std::sort(S.leaf.begin(), S.leaf.end(), pair_less);
   S.adm_offset.assign(static_cast<size_t>(depth) + 2, 0);
   for (int l = 0; l <= depth; ++l) S.adm_offset[static_cast<size_t>(l) + 1] = S.adm_offset[static_cast<size_t>(l)] + static_cast<int64_t>(S.adm[static_cast<size_t>(l)].size());
+  S.l0 = -1;
   for (int l = 0; l <= depth; ++l)
     if (!S.adm[static_cast<size_t>(l)].empty()) {
       S.l0 = l;
       break;
     }
-  if (perm_out) *perm_out = std::move(perm);
+}
+
+// Tree given (loaded from an H2LU file: ranges + tree-order points), partition
+// recomputed exactly as load_h2 does (serialize.hpp:204-206).
+Structure structure_from_tree(const double* pts_tree, int64_t n, int depth, const std::vector<int64_t>& begin, const std::vector<int64_t>& end,
+                              double eta) {
+  Structure S;
+  S.n = n;
+  S.depth = depth;
+  S.eta = eta;
+  S.begin = begin;
+  S.end = end;
+  const int nc = S.num_clusters();
+  if ((int)begin.size() != nc || (int)end.size() != nc) throw std::invalid_argument("structure_from_tree: range arrays do not match the depth");
+  std::vector<Box> box(static_cast<size_t>(nc));
+  for (int id = 0; id < nc; ++id) {
+    Box& bx = box[static_cast<size_t>(id)];
+    for (int a = 0; a < 3; ++a) bx.lo[a] = bx.hi[a] = 0.0;
+    const int64_t b = begin[static_cast<size_t>(id)], e = end[static_cast<size_t>(id)];
+    if (b >= e) continue;
+    for (int a = 0; a < 3; ++a) bx.lo[a] = bx.hi[a] = pts_tree[3 * b + a];
+    for (int64_t i = b + 1; i < e; ++i)
+      for (int a = 0; a < 3; ++a) {
+        bx.lo[a] = std::min(bx.lo[a], pts_tree[3 * i + a]);
+        bx.hi[a] = std::max(bx.hi[a], pts_tree[3 * i + a]);
+      }
+  }
+  partition(S, box);
   return S;
 }
 
@@ -321,13 +362,7 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
   return S;
 }
 
-int fill_segments(int nbat) {
-  static const int k = [] {
-    const char* e = std::getenv("H2G_FILL_SEGMENTS");
-    return e ? std::max(1, std::atoi(e)) : 16;
-  }();
-  return std::max(1, std::min(k, nbat));
-}
+int fill_segments(int nbat, int requested) { return std::max(1, std::min(requested, nbat)); }
 
 namespace {
 
@@ -396,7 +431,7 @@ class FrontAllocator {
 FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W, const std::vector<int>& bsz, const std::vector<int>& init) {
   FrontPlan F;
   const int nbat = static_cast<int>(sch.batch_ptr.size()) - 1;
-  const int K = fill_segments(nbat);
+  const int K = W.fill_segments;
   F.K = K;
   F.seg_first_batch.assign(static_cast<size_t>(K) + 1, nbat);
   for (int b = nbat - 1; b >= 0; --b) F.seg_first_batch[static_cast<size_t>(fill_segment(b, nbat, K))] = b;
@@ -446,10 +481,11 @@ FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWo
   return F;
 }
 
-LevelWork build_work(const LevelSym& L, const LevelSchedule& sch) {
+LevelWork build_work(const LevelSym& L, const LevelSchedule& sch, int segments) {
   LevelWork W;
   const int nbat = static_cast<int>(sch.batch_ptr.size()) - 1;
-  const int K = fill_segments(nbat);
+  const int K = fill_segments(nbat, segments);
+  W.fill_segments = K;
   const auto& ord = sch.order;
   W.panel_ptr.assign(1, 0);
   W.schur_ptr.assign(1, 0);

@@ -92,7 +92,7 @@ struct PanelItem {
 // its core V_j^H F conj(V_c) (kfin_j x kfin_c, the only form its later
 // consumers read, :455 and :540), and deposits of later segments go straight
 // to the core (the lifts through V_j / V_c cancel against the projection).
-int fill_segments(int nbat);
+int fill_segments(int nbat, int requested);
 inline int fill_segment(int b, int nbat, int K) { return nbat > 0 ? static_cast<int>(static_cast<int64_t>(b) * K / nbat) : 0; }
 
 struct SchurTarget {
@@ -132,6 +132,7 @@ struct LevelWork {
   std::vector<SolveTarget> fsolve;
   std::vector<SolveContrib> fcontrib;
   int max_batch = 0;
+  int fill_segments = 1;       // K of the fill storage plan (fill_segments)
   int64_t schur_products = 0;  // structural count (upper bound)
 };
 
@@ -154,10 +155,15 @@ FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWo
 
 Structure structure_from_desc(const h2g_matrix_desc* d);
 Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm);
+// Partition of a given tree (tree-order points and heap-order ranges).
+Structure structure_from_tree(const double* pts_tree, int64_t n, int depth, const std::vector<int64_t>& begin, const std::vector<int64_t>& end,
+                              double eta);
 
 // Levels from depth down to (and including) `stop`.
 std::vector<LevelSym> build_levels(const Structure& S, int stop);
 LevelSchedule build_schedule(const LevelSym& L, int kind);
-LevelWork build_work(const LevelSym& L, const LevelSchedule& sch);
+// segments: requested fill-storage segments K (1 = whole-level full blocks,
+// collapsed at the level end)
+LevelWork build_work(const LevelSym& L, const LevelSchedule& sch, int segments);
 
 }  // namespace h2g

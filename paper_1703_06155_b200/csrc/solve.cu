@@ -48,6 +48,43 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
   }
 }
 
+// out = op(A) x for a column-major m x k matrix A (op: A or conj(A), no
+// transpose), x k x nrhs (global or shared). Coalesced: thread t owns row
+// i = t % m' of a chunk of m' <= blockDim rows and the k-slice p = g, g + G,
+// ... with g = t / m', G = blockDim / m' groups; the G partial sums are
+// reduced through shared memory in a fixed order (deterministic). subtract:
+// out -= result instead of out = result. red: blockDim complex of shared.
+__device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool conjA, const cplx* x, long long ldx, cplx* out, long long ldo,
+                           bool subtract, cplx* red) {
+  for (int i0 = 0; i0 < m; i0 += blockDim.x) {
+    const int mm = min(m - i0, (int)blockDim.x);
+    const int G = max(1, (int)blockDim.x / mm);
+    const int t = threadIdx.x, i = t % mm, g = t / mm;
+    for (int c = 0; c < nrhs; ++c) {
+      cplx acc = czero();
+      if (g < G) {
+        const cplx* xc = x + (size_t)c * ldx;
+#pragma unroll 4
+        for (int p = g; p < k; p += G) {
+          cplx a = A[(i0 + i) + (size_t)p * lda];
+          if (conjA) a.y = -a.y;
+          cfma(acc, a, xc[p]);
+        }
+      }
+      __syncthreads();
+      if (g < G) red[g * mm + i] = acc;
+      __syncthreads();
+      if (t < mm) {
+        cplx s = red[t];
+        for (int q = 1; q < G; ++q) s = cadd(s, red[q * mm + t]);
+        cplx* o = out + (i0 + t) + (size_t)c * ldo;
+        *o = subtract ? csub(*o, s) : s;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50); one CTA per
 // record.
 __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, unsigned char* smraw) {
@@ -55,6 +92,7 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);  // b x nrhs
   cplx* sO = sS + (size_t)b * nrhs;           // b x nrhs
+  cplx* sR = sO + (size_t)b * nrhs;           // reduction scratch (blockDim)
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
   __syncthreads();
   const cplx* Q = S.chain + S.Qt_off[t];
@@ -63,8 +101,7 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   if (e > 0) {
     if (explicit_inv) {
       const cplx* Li = S.chain + S.Linv_off[t];
-      warp_gemv(e, nrhs, Li, e, OP_N, sO, b, sS, b);
-      __syncthreads();
+      cta_gemv_n(e, e, nrhs, Li, e, false, sO, b, sS, b, false, sR);
       for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sO[(idx % e) + (idx / e) * b] = sS[(idx % e) + (idx / e) * b];
       __syncthreads();
     } else {
@@ -85,11 +122,12 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
 }
 
-// y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51). One warp per target
-// row; the lanes stride over the flattened (contribution, p) index space so
-// every lane has independent loads in flight, then a fixed shuffle tree
-// (deterministic summation order).
-__device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs) {
+// y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51). Thread (i, g):
+// row i of the target, slice g of every contribution's columns (coalesced
+// column reads); contributions accumulate per thread, one fixed-order
+// reduction at the end (deterministic).
+__device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const SolveContribD* contrib, cplx* y, long long ldy, int nrhs,
+                              cplx* red) {
   int rows;
   long long base;
   if (tg.seg >= 0) {
@@ -100,54 +138,41 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
     rows = S.kfin[m];
     base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
   }
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int c0 = 0; c0 < nrhs; c0 += 4) {
-    const int nc = min(4, nrhs - c0);
-    for (int i = warp; i < rows; i += nw) {
-      cplx acc[4] = {czero(), czero(), czero(), czero()};
-      int ci = tg.c0, off = 0, e = 0;
-      const cplx* M = nullptr;
-      const cplx* h = nullptr;
-      auto open = [&](int c) {
-        const SolveContribD cb = contrib[c];
-        e = S.bsz[cb.m] - S.kfin[cb.m];
-        M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]);
-        h = y + S.pos[cb.m];
-      };
-      if (ci < tg.c1) open(ci);
-      for (int u = lane;; u += 32) {
-        while (ci < tg.c1 && u >= off + e) {
-          off += e;
-          if (++ci < tg.c1) open(ci);
+  for (int i0 = 0; i0 < rows; i0 += blockDim.x) {
+    const int mm = min(rows - i0, (int)blockDim.x);
+    const int G = max(1, (int)blockDim.x / mm);
+    const int t = threadIdx.x, i = t % mm, g = t / mm;
+    for (int c = 0; c < nrhs; ++c) {
+      cplx acc = czero();
+      if (g < G) {
+        for (int ci = tg.c0; ci < tg.c1; ++ci) {
+          const SolveContribD cb = contrib[ci];
+          const int e = S.bsz[cb.m] - S.kfin[cb.m];
+          const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i0 + i;
+          const cplx* h = y + S.pos[cb.m] + (size_t)c * ldy;
+#pragma unroll 4
+          for (int p = g; p < e; p += G) cfma(acc, M[(size_t)p * rows], h[p]);
         }
-        if (ci >= tg.c1) break;
-        const int p = u - off;
-        const cplx mv = M[i + (size_t)p * rows];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < nc) cfma(acc[c], mv, h[p + (size_t)(c0 + c) * ldy]);
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double re = acc[c].x, im = acc[c].y;
-        for (int o = 16; o > 0; o >>= 1) {
-          re += __shfl_xor_sync(0xffffffffu, re, o);
-          im += __shfl_xor_sync(0xffffffffu, im, o);
-        }
-        if (lane == 0 && c < nc) {
-          cplx* o = y + base + i + (size_t)(c0 + c) * ldy;
-          *o = csub(*o, make_double2(re, im));
-        }
+      __syncthreads();
+      if (g < G) red[g * mm + i] = acc;
+      __syncthreads();
+      if (t < mm) {
+        cplx s2 = red[t];
+        for (int q = 1; q < G; ++q) s2 = cadd(s2, red[q * mm + t]);
+        cplx* o = y + base + i0 + t + (size_t)c * ldy;
+        *o = csub(*o, s2);
       }
     }
   }
+  __syncthreads();
 }
 
 // Backward gather (solve.hpp:77): partial[q][c] = Ubar(m, c) y[pos_c ...]
 // for one neighbour c of record m = batch[q] (the last slot is the self
 // block), spread over CTAs so the chain blocks stream at full bandwidth.
 __device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int nslot, const cplx* y, long long ldy, int nrhs, cplx* part,
-                                long long pstride) {
+                                long long pstride, cplx* red) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
   if (e == 0 || c > nC || (c == nC && kf == 0)) return;
@@ -165,29 +190,7 @@ __device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int ns
     x = y + S.pos[t] + e;
   }
   cplx* out = part + ((size_t)q * nslot + c) * pstride;
-  // one warp per row of Ubar, lanes over its columns (independent loads)
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  for (int r0 = 0; r0 < nrhs; r0 += 4) {
-    const int nc = min(4, nrhs - r0);
-    for (int i = warp; i < e; i += nw) {
-      cplx acc[4] = {czero(), czero(), czero(), czero()};
-      for (int p = lane; p < cols; p += 32) {
-        const cplx mv = M[i + (size_t)p * e];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < nc) cfma(acc[r], mv, x[p + (size_t)(r0 + r) * ldy]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        double re = acc[r].x, im = acc[r].y;
-        for (int o = 16; o > 0; o >>= 1) {
-          re += __shfl_xor_sync(0xffffffffu, re, o);
-          im += __shfl_xor_sync(0xffffffffu, im, o);
-        }
-        if (lane == 0 && r < nc) out[i + (size_t)(r0 + r) * e] = make_double2(re, im);
-      }
-    }
-  }
+  cta_gemv_n(e, cols, nrhs, M, e, false, x, ldy, out, e, false, red);
 }
 
 // Backward record (solve.hpp:73-81): head -= sum of the gathered partials (in
@@ -198,6 +201,7 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);
   cplx* sO = sS + (size_t)b * nrhs;
+  cplx* sR = sO + (size_t)b * nrhs;  // reduction scratch (blockDim)
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
   __syncthreads();
   if (e > 0) {
@@ -220,7 +224,7 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
     __syncthreads();
     if (explicit_inv) {
       const cplx* Ui = S.chain + S.Uinv_off[t];
-      warp_gemv(e, nrhs, Ui, e, OP_N, sS, b, sO, b);
+      cta_gemv_n(e, e, nrhs, Ui, e, false, sS, b, sO, b, false, sR);
       __syncthreads();
       for (int idx = threadIdx.x; idx < e * nrhs; idx += blockDim.x) sS[(idx % e) + (idx / e) * b] = sO[(idx % e) + (idx / e) * b];
       __syncthreads();
@@ -242,8 +246,7 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
     }
   }
   const cplx* Q = S.chain + S.Qt_off[t];
-  warp_gemv(b, nrhs, Q, b, OP_R, sS, b, sO, b);
-  __syncthreads();
+  cta_gemv_n(b, b, nrhs, Q, b, true, sS, b, sO, b, false, sR);
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
 }
 
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(256) k_fwd_level(SolveLevel S, SolveSched P, c
     }
     g.sync();
     const int f0 = P.fs_ptr[bi], f1 = P.fs_ptr[bi + 1];
-    for (int f = f0 + blockIdx.x; f < f1; f += gridDim.x) fwd_lbar_body(S, P.fs[f], P.fc, y, ldy, nrhs);
+    for (int f = f0 + blockIdx.x; f < f1; f += gridDim.x) fwd_lbar_body(S, P.fs[f], P.fc, y, ldy, nrhs, reinterpret_cast<cplx*>(smraw));
     g.sync();
   }
 }
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(256) k_bwd_level(SolveLevel S, SolveSched P, c
     const int p0 = P.batch_ptr[bi], nb = P.batch_ptr[bi + 1] - p0;
     const int nslot = P.batch_maxc[bi] + 1;
     for (int it = blockIdx.x; it < nb * nslot; it += gridDim.x)
-      bwd_gather_body(S, P.batch_cl[p0 + it / nslot], it / nslot, it % nslot, nslot, y, ldy, nrhs, part, pstride);
+      bwd_gather_body(S, P.batch_cl[p0 + it / nslot], it / nslot, it % nslot, nslot, y, ldy, nrhs, part, pstride, reinterpret_cast<cplx*>(smraw));
     g.sync();
     for (int q = blockIdx.x; q < nb; q += gridDim.x) {
       bwd_body(S, P.batch_cl[p0 + q], q, y, ldy, nrhs, explicit_inv, part, pstride, nslot, smraw);
@@ -388,7 +391,7 @@ static int coop_grid(K kernel, size_t smem) {
 
 void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s) {
   if (P.nbat <= 0) return;
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
   smem_attr((const void*)k_fwd_level, smem);
   const int grid = coop_grid(k_fwd_level, smem);
   SolveLevel Sv = S;
@@ -400,7 +403,7 @@ void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long lo
 
 void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s) {
   if (P.nbat <= 0) return;
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx);
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
   smem_attr((const void*)k_bwd_level, smem);
   const int grid = coop_grid(k_bwd_level, smem);
   long long pstride = (long long)S.bmax * nrhs;

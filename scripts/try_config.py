@@ -29,7 +29,7 @@ t0 = time.time()
 A = h2g.H2Matrix.build(pts, c["leaf"], 1.0, K, c["eps"])
 build_s = time.time() - t0
 print("config %d eps %.0e: N %d, build %.1f s" % (cfg, c["eps"], A.n, build_s), flush=True)
-perm = A.download()["perm"] if A.n <= 300000 else None
+perm = A.perm()
 os.environ.setdefault("H2G_VERBOSE", "1")
 t0 = time.time()
 ch = h2g.factorize(A, c["eps"], schedule=sched)
