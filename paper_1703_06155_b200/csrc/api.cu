@@ -7,6 +7,7 @@
 // descriptor-driven batched copies/GEMMs; the remainder is LU-factored on the
 // device (:637-651). There is no CPU fallback.
 #include <atomic>
+#include <thread>
 #include <unistd.h>
 #include <functional>
 #include <cuda_runtime.h>
@@ -593,11 +594,28 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule, bool* built) {
     if (fill > 0.15 * (double)tot) segments = 16;
   }
   P->segments = segments;
-  for (const auto& L : P->levels) {
-    if (L.level >= stop && stop <= M->S.depth) {
-      P->sched.push_back(build_schedule(L, schedule));
-      P->work.push_back(build_work(L, P->sched.back(), segments));
-    }
+  // schedules and work lists are independent per level: one host thread each
+  size_t nfact = 0;
+  for (const auto& L : P->levels)
+    if (L.level >= stop && stop <= M->S.depth) ++nfact;
+  P->sched.resize(nfact);
+  P->work.resize(nfact);
+  {
+    std::vector<std::thread> th;
+    std::exception_ptr failed;
+    std::mutex fm;
+    for (size_t i = 0; i < nfact; ++i)
+      th.emplace_back([&, i] {
+        try {
+          P->sched[i] = build_schedule(P->levels[i], schedule);
+          P->work[i] = build_work(P->levels[i], P->sched[i], segments);
+        } catch (...) {
+          std::lock_guard<std::mutex> g(fm);
+          if (!failed) failed = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    if (failed) std::rethrow_exception(failed);
   }
   {
     std::lock_guard<std::mutex> g2(M->ctx->plan_mu);
@@ -1798,8 +1816,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         // Z = V_a^H F conj(V_c) (segment ends above), so the parent blocks are
         // assembled by copies: couplings / dense corners first, cores
         // accumulated on top (dst = pad(S) + Z).
-        std::vector<CopyDesc> cd;  // dst pointers relative to nxt.D (dst_kind 0) / nxt.F (1), fixed up after allocation
-        std::vector<int> cd_kind;
+        std::vector<CopyDesc> cd;  // dst pointers relative to nxt.D, fixed up after allocation
         struct PendingZ {
           int a, c, fi, kind;
           long long doff;  // element offset of the destination in nxt.D / nxt.F
@@ -1821,7 +1838,6 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                 const int ea = cur.bsz[a] - kfin[a], ec = cur.bsz[c] - kfin[c];
                 if (kfin[a] && kfin[c]) {
                   cd.push_back({cur.D.as<cplx>() + cur.doff[di] + ea + (size_t)ec * cur.bsz[a], reinterpret_cast<cplx*>(doff * 16), cur.bsz[a], ldd, kfin[a], kfin[c], 0, 0});
-                  cd_kind.push_back(0);
                 }
               } else {
                 const Pair hp{a + Y.first, c + Y.first};
@@ -1832,7 +1848,6 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                 const int ka = cur.korig[a], kc = cur.korig[c];
                 if (ka && kc) {
                   cd.push_back({M->coup.as<cplx>() + M->coup_off[gi], reinterpret_cast<cplx*>(doff * 16), ka, ldd, ka, kc, 0, 0});
-                  cd_kind.push_back(0);
                 }
                 const int fi = Y.fill_index(a, c);
                 if (fi >= 0 && fex[fi] && kfin[a] && kfin[c]) pend.push_back({a, c, fi, 0, doff, ldd});
@@ -1873,17 +1888,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         cur.fex.release();
         cur.Vp.release();
         mark("merge: fill pool released");
-        ensure((size_t)(std::max<long long>(ndtot, 1) + std::max<long long>(nftot, 1) + (long long)nlp * bbp) * 16, CL.get());
+        // (1) parent dense blocks and padded transfers from the level-l dense
+        // pool, which is then released before the parent fill pool exists
+        ensure((size_t)(std::max<long long>(ndtot, 1) + (long long)nlp * bbp) * 16, CL.get());
         nxt.D.alloc(std::max<long long>(ndtot, 1) * 16, st, true);
-        nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
-        nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
         nxt.V0.alloc((size_t)nlp * bbp * 16, st, true);
         cplx* Dp = nxt.D.as<cplx>();
-        cplx* Fp = nxt.F.as<cplx>();
-        for (size_t q = 0; q < cd.size(); ++q) cd[q].dst = (cd_kind[q] ? Fp : Dp) + reinterpret_cast<long long>(cd[q].dst) / 16;
-        // cores accumulate after the coupling / dense-corner copies (dst = S + Z)
-        std::vector<CopyDesc> cz;
-        for (const auto& pg : pend) cz.push_back({core_ptr_h[pg.fi], (pg.kind ? Fp : Dp) + pg.doff, kfin[pg.a], pg.ldd, kfin[pg.a], kfin[pg.c], 1, 0});
+        for (size_t q = 0; q < cd.size(); ++q) cd[q].dst = Dp + reinterpret_cast<long long>(cd[q].dst) / 16;
         // padded transfers (finish_level :464-474)
         for (int P2 = 0; P2 < nlp; ++P2) {
           const int id = firstp + P2;
@@ -1895,12 +1906,24 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           if (k1) cd.push_back({T, dst, rows, nxt.bsz[P2], k1, kp, 0, 0});
           if (k2) cd.push_back({T + k1, dst + kfin[2 * P2], rows, nxt.bsz[P2], k2, kp, 0, 0});
         }
-        mark("merge descriptors built");
         DBuf dcd, dcz;
         upload(dcd, cd, st);
-        upload(dcz, cz, st);
         ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcd.as<CopyDesc>(), static_cast<int>(cd.size()), st);
+        ctx->prof.end(st);
+        cur.D.release();  // stream-ordered: reused only after the copies above
+        mark("merge: dense blocks assembled");
+        // (2) the parent fill pool; cores accumulate on top of the copies
+        // (dst = pad(S) + Z)
+        ensure((size_t)(std::max<long long>(nftot, 1) + YP.frow.size() * 4) + 16, CL.get());
+        nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
+        nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
+        cplx* Fp = nxt.F.as<cplx>();
+        std::vector<CopyDesc> cz;
+        for (const auto& pg : pend) cz.push_back({core_ptr_h[pg.fi], (pg.kind ? Fp : Dp) + pg.doff, kfin[pg.a], pg.ldd, kfin[pg.a], kfin[pg.c], 1, 0});
+        mark("merge descriptors built");
+        upload(dcz, cz, st);
+        ctx->prof.begin(PC_MERGE, st);
         launch_copy(dcz.as<CopyDesc>(), static_cast<int>(cz.size()), st);
         ctx->prof.end(st);
         C->klaunch[PC_MERGE] += (!cd.empty()) + (!cz.empty());

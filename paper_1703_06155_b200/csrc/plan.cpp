@@ -2,6 +2,8 @@
 #include "plan.hpp"
 
 #include <climits>
+#include <mutex>
+#include <thread>
 #include <cstdlib>
 #include <map>
 
@@ -253,12 +255,26 @@ std::vector<LevelSym> build_levels(const Structure& S, int stop) {
     // fill targets
     std::vector<int64_t> keys;
     if (processed) {
-      for (int m = 0; m < nl; ++m)
-        for (int a = Y.R_ptr[static_cast<size_t>(m)]; a < Y.R_ptr[static_cast<size_t>(m) + 1]; ++a)
-          for (int b = Y.C_ptr[static_cast<size_t>(m)]; b < Y.C_ptr[static_cast<size_t>(m) + 1]; ++b) {
-            const int j = Y.R_nb[static_cast<size_t>(a)], c = Y.C_nb[static_cast<size_t>(b)];
-            if (Y.dense_index(j, c) < 0) keys.push_back(int64_t(j) * nl + c);
-          }
+      // every (row, column) neighbour pair of a cluster that is not dense;
+      // clusters split over host threads (read-only lookups), merged below
+      const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), nl / 64));
+      std::vector<std::vector<int64_t>> part(static_cast<size_t>(nt));
+      auto work = [&](int w) {
+        std::vector<int64_t>& out_keys = part[static_cast<size_t>(w)];
+        for (int m = w; m < nl; m += nt)
+          for (int a = Y.R_ptr[static_cast<size_t>(m)]; a < Y.R_ptr[static_cast<size_t>(m) + 1]; ++a)
+            for (int b = Y.C_ptr[static_cast<size_t>(m)]; b < Y.C_ptr[static_cast<size_t>(m) + 1]; ++b) {
+              const int j = Y.R_nb[static_cast<size_t>(a)], c = Y.C_nb[static_cast<size_t>(b)];
+              if (Y.dense_index(j, c) < 0) out_keys.push_back(int64_t(j) * nl + c);
+            }
+        std::sort(out_keys.begin(), out_keys.end());
+        out_keys.erase(std::unique(out_keys.begin(), out_keys.end()), out_keys.end());
+      };
+      std::vector<std::thread> th;
+      for (int w = 1; w < nt; ++w) th.emplace_back(work, w);
+      work(0);
+      for (auto& t : th) t.join();
+      for (auto& v : part) keys.insert(keys.end(), v.begin(), v.end());
     }
     if (!out.empty()) {
       const LevelSym& P = out.back();  // level l+1
@@ -487,19 +503,14 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch, int segments) 
   const int K = fill_segments(nbat, segments);
   W.fill_segments = K;
   const auto& ord = sch.order;
-  W.panel_ptr.assign(1, 0);
-  W.schur_ptr.assign(1, 0);
-  W.fsolve_ptr.assign(1, 0);
   struct Tmp {
     int64_t key;  // kind, idx
     SchurContrib c;
   };
-  std::vector<Tmp> tmp;
   struct STmp {
     int64_t seg;
     SolveContrib c;
   };
-  std::vector<STmp> stmp;
   std::vector<int> batch_of(static_cast<size_t>(L.nl), -1);
   for (int b = 0; b < nbat; ++b)
     for (int q = sch.batch_ptr[static_cast<size_t>(b)]; q < sch.batch_ptr[static_cast<size_t>(b) + 1]; ++q)
@@ -508,109 +519,161 @@ LevelWork build_work(const LevelSym& L, const LevelSchedule& sch, int segments) 
     if ((T.kind & 1) == 0) return std::make_pair(L.drow[static_cast<size_t>(T.idx)], L.dcol[static_cast<size_t>(T.idx)]);
     return std::make_pair(L.frow[static_cast<size_t>(T.idx)], L.fcol[static_cast<size_t>(T.idx)]);
   };
-  std::vector<SchurTarget> bulk;
-  for (int b = 0; b < nbat; ++b) {
-    const int p0 = sch.batch_ptr[static_cast<size_t>(b)], p1 = sch.batch_ptr[static_cast<size_t>(b) + 1];
-    W.max_batch = std::max(W.max_batch, p1 - p0);
-    tmp.clear();
-    stmp.clear();
-    for (int q = p0; q < p1; ++q) {
-      const int t = sch.batch_cl[static_cast<size_t>(q)];
-      const int ot = ord[static_cast<size_t>(t)];
-      for (int e = L.C_ptr[static_cast<size_t>(t)]; e < L.C_ptr[static_cast<size_t>(t) + 1]; ++e) {
-        const int c = L.C_nb[static_cast<size_t>(e)];
-        W.panel.push_back({q - p0, 0, c, L.C_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(c)] < ot ? 1 : 0});
-      }
-      for (int e = L.R_ptr[static_cast<size_t>(t)]; e < L.R_ptr[static_cast<size_t>(t) + 1]; ++e) {
-        const int j = L.R_nb[static_cast<size_t>(e)];
-        W.panel.push_back({q - p0, 1, j, L.R_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(j)] < ot ? 1 : 0});
-      }
-      // Schur products rows x cols, self last (factorization.hpp:403-425)
-      const int r0 = L.R_ptr[static_cast<size_t>(t)], r1 = L.R_ptr[static_cast<size_t>(t) + 1];
-      const int c0 = L.C_ptr[static_cast<size_t>(t)], c1 = L.C_ptr[static_cast<size_t>(t) + 1];
-      for (int a = r0; a <= r1; ++a) {
-        const bool rself = a == r1;
-        const int j = rself ? t : L.R_nb[static_cast<size_t>(a)];
-        for (int e = c0; e <= c1; ++e) {
-          const bool cself = e == c1;
-          if (rself && cself) continue;  // D(t,t) corner: head kernel
-          const int c = cself ? t : L.C_nb[static_cast<size_t>(e)];
-          SchurContrib sc{t, rself ? -1 - t : a, cself ? -1 - t : e, 0};
-          int kind, idx;
-          if (rself) {
-            kind = 0, idx = L.C_blk[static_cast<size_t>(e)];
-          } else if (cself) {
-            kind = 0, idx = L.R_blk[static_cast<size_t>(a)];
-          } else {
-            idx = L.dense_index(j, c);
-            kind = 0;
-            if (idx < 0) {
-              kind = 1;
-              idx = L.fill_index(j, c);
-              if (idx < 0) throw std::logic_error("plan: Schur target neither dense nor fill");
-              if (ord[static_cast<size_t>(j)] < ot) sc.flags |= 1;
-              if (ord[static_cast<size_t>(c)] < ot) sc.flags |= 2;
-            }
-          }
-          tmp.push_back({(int64_t(kind) << 40) | int64_t(idx), sc});
-          ++W.schur_products;
+  // Batches are independent: ranges of batches are built on host threads and
+  // concatenated in batch order (indices into the contribution lists shifted).
+  auto build_range = [&](int b0, int b1, LevelWork& W) {
+    W.panel_ptr.assign(1, 0);
+    W.schur_ptr.assign(1, 0);
+    W.fsolve_ptr.assign(1, 0);
+    std::vector<Tmp> tmp;
+    std::vector<STmp> stmp;
+    std::vector<SchurTarget> bulk;
+    for (int b = b0; b < b1; ++b) {
+      const int p0 = sch.batch_ptr[static_cast<size_t>(b)], p1 = sch.batch_ptr[static_cast<size_t>(b) + 1];
+      W.max_batch = std::max(W.max_batch, p1 - p0);
+      tmp.clear();
+      stmp.clear();
+      for (int q = p0; q < p1; ++q) {
+        const int t = sch.batch_cl[static_cast<size_t>(q)];
+        const int ot = ord[static_cast<size_t>(t)];
+        for (int e = L.C_ptr[static_cast<size_t>(t)]; e < L.C_ptr[static_cast<size_t>(t) + 1]; ++e) {
+          const int c = L.C_nb[static_cast<size_t>(e)];
+          W.panel.push_back({q - p0, 0, c, L.C_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(c)] < ot ? 1 : 0});
         }
-        // forward-solve Lbar targets (solve.hpp:51)
-        stmp.push_back({rself ? -1 - int64_t(t) : int64_t(j), {t, rself ? -1 - t : a}});
+        for (int e = L.R_ptr[static_cast<size_t>(t)]; e < L.R_ptr[static_cast<size_t>(t) + 1]; ++e) {
+          const int j = L.R_nb[static_cast<size_t>(e)];
+          W.panel.push_back({q - p0, 1, j, L.R_blk[static_cast<size_t>(e)], e, ord[static_cast<size_t>(j)] < ot ? 1 : 0});
+        }
+        // Schur products rows x cols, self last (factorization.hpp:403-425)
+        const int r0 = L.R_ptr[static_cast<size_t>(t)], r1 = L.R_ptr[static_cast<size_t>(t) + 1];
+        const int c0 = L.C_ptr[static_cast<size_t>(t)], c1 = L.C_ptr[static_cast<size_t>(t) + 1];
+        for (int a = r0; a <= r1; ++a) {
+          const bool rself = a == r1;
+          const int j = rself ? t : L.R_nb[static_cast<size_t>(a)];
+          for (int e = c0; e <= c1; ++e) {
+            const bool cself = e == c1;
+            if (rself && cself) continue;  // D(t,t) corner: head kernel
+            const int c = cself ? t : L.C_nb[static_cast<size_t>(e)];
+            SchurContrib sc{t, rself ? -1 - t : a, cself ? -1 - t : e, 0};
+            int kind, idx;
+            if (rself) {
+              kind = 0, idx = L.C_blk[static_cast<size_t>(e)];
+            } else if (cself) {
+              kind = 0, idx = L.R_blk[static_cast<size_t>(a)];
+            } else {
+              idx = L.dense_index(j, c);
+              kind = 0;
+              if (idx < 0) {
+                kind = 1;
+                idx = L.fill_index(j, c);
+                if (idx < 0) throw std::logic_error("plan: Schur target neither dense nor fill");
+                if (ord[static_cast<size_t>(j)] < ot) sc.flags |= 1;
+                if (ord[static_cast<size_t>(c)] < ot) sc.flags |= 2;
+              }
+            }
+            tmp.push_back({(int64_t(kind) << 40) | int64_t(idx), sc});
+            ++W.schur_products;
+          }
+          // forward-solve Lbar targets (solve.hpp:51)
+          stmp.push_back({rself ? -1 - int64_t(t) : int64_t(j), {t, rself ? -1 - t : a}});
+        }
       }
+      std::stable_sort(tmp.begin(), tmp.end(), [](const Tmp& x, const Tmp& y) { return x.key < y.key; });
+      bulk.clear();
+      int ncrit = 0;
+      for (size_t i = 0; i < tmp.size();) {
+        size_t j = i;
+        while (j < tmp.size() && tmp[j].key == tmp[i].key) ++j;
+        SchurTarget T{static_cast<int32_t>(tmp[i].key >> 40), static_cast<int32_t>(tmp[i].key & ((int64_t(1) << 40) - 1)),
+                      static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
+        const auto rc = target_rc(T);
+        // fill target whose core already exists (both sides collapsed in an
+        // earlier segment): deposit into the core, unlifted panels
+        bool core = false;
+        if (T.kind == 1) {
+          const int bc = std::max(ord[static_cast<size_t>(rc.first)], ord[static_cast<size_t>(rc.second)]);
+          core = fill_segment(b, nbat, K) > fill_segment(bc, nbat, K);
+          if (core) T.kind |= 8;
+        }
+        for (size_t k = i; k < j; ++k) {
+          SchurContrib cb = tmp[k].c;
+          if (core) cb.flags = 0;
+          W.contrib.push_back(cb);
+        }
+        // dense target whose row (column) cluster was eliminated in an earlier
+        // batch: its first e rows (columns) are zero and stay zero (cleanup,
+        // factorization.hpp:431-439), so the update there is exactly zero and
+        // the kernel starts its tiles at e (bit 1: rows, bit 2: columns)
+        if (T.kind == 0) {
+          if (batch_of[static_cast<size_t>(rc.first)] < b) T.kind |= 2;
+          if (batch_of[static_cast<size_t>(rc.second)] < b) T.kind |= 4;
+        }
+        if (batch_of[static_cast<size_t>(rc.first)] == b + 1 || batch_of[static_cast<size_t>(rc.second)] == b + 1) {
+          W.schur.push_back(T);
+          ++ncrit;
+        } else {
+          bulk.push_back(T);
+        }
+        i = j;
+      }
+      W.schur.insert(W.schur.end(), bulk.begin(), bulk.end());
+      W.schur_crit.push_back(ncrit);
+      std::stable_sort(stmp.begin(), stmp.end(), [](const STmp& x, const STmp& y) { return x.seg < y.seg; });
+      for (size_t i = 0; i < stmp.size();) {
+        size_t j = i;
+        while (j < stmp.size() && stmp[j].seg == stmp[i].seg) ++j;
+        SolveTarget T{static_cast<int32_t>(stmp[i].seg), static_cast<int32_t>(W.fcontrib.size()), static_cast<int32_t>(W.fcontrib.size() + (j - i))};
+        for (size_t k = i; k < j; ++k) W.fcontrib.push_back(stmp[k].c);
+        W.fsolve.push_back(T);
+        i = j;
+      }
+      W.panel_ptr.push_back(static_cast<int32_t>(W.panel.size()));
+      W.schur_ptr.push_back(static_cast<int32_t>(W.schur.size()));
+      W.fsolve_ptr.push_back(static_cast<int32_t>(W.fsolve.size()));
     }
-    std::stable_sort(tmp.begin(), tmp.end(), [](const Tmp& x, const Tmp& y) { return x.key < y.key; });
-    bulk.clear();
-    int ncrit = 0;
-    for (size_t i = 0; i < tmp.size();) {
-      size_t j = i;
-      while (j < tmp.size() && tmp[j].key == tmp[i].key) ++j;
-      SchurTarget T{static_cast<int32_t>(tmp[i].key >> 40), static_cast<int32_t>(tmp[i].key & ((int64_t(1) << 40) - 1)),
-                    static_cast<int32_t>(W.contrib.size()), static_cast<int32_t>(W.contrib.size() + (j - i))};
-      const auto rc = target_rc(T);
-      // fill target whose core already exists (both sides collapsed in an
-      // earlier segment): deposit into the core, unlifted panels
-      bool core = false;
-      if (T.kind == 1) {
-        const int bc = std::max(ord[static_cast<size_t>(rc.first)], ord[static_cast<size_t>(rc.second)]);
-        core = fill_segment(b, nbat, K) > fill_segment(bc, nbat, K);
-        if (core) T.kind |= 8;
-      }
-      for (size_t k = i; k < j; ++k) {
-        SchurContrib cb = tmp[k].c;
-        if (core) cb.flags = 0;
-        W.contrib.push_back(cb);
-      }
-      // dense target whose row (column) cluster was eliminated in an earlier
-      // batch: its first e rows (columns) are zero and stay zero (cleanup,
-      // factorization.hpp:431-439), so the update there is exactly zero and
-      // the kernel starts its tiles at e (bit 1: rows, bit 2: columns)
-      if (T.kind == 0) {
-        if (batch_of[static_cast<size_t>(rc.first)] < b) T.kind |= 2;
-        if (batch_of[static_cast<size_t>(rc.second)] < b) T.kind |= 4;
-      }
-      if (batch_of[static_cast<size_t>(rc.first)] == b + 1 || batch_of[static_cast<size_t>(rc.second)] == b + 1) {
-        W.schur.push_back(T);
-        ++ncrit;
-      } else {
-        bulk.push_back(T);
-      }
-      i = j;
+  };
+  const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()), nbat / 16));
+  std::vector<LevelWork> part(static_cast<size_t>(nt));
+  {
+    std::vector<std::thread> th;
+    std::exception_ptr failed;
+    std::mutex fm;
+    for (int w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        try {
+          build_range(static_cast<int>(static_cast<int64_t>(nbat) * w / nt), static_cast<int>(static_cast<int64_t>(nbat) * (w + 1) / nt),
+                      part[static_cast<size_t>(w)]);
+        } catch (...) {
+          std::lock_guard<std::mutex> g(fm);
+          if (!failed) failed = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    if (failed) std::rethrow_exception(failed);
+  }
+  W.panel_ptr.assign(1, 0);
+  W.schur_ptr.assign(1, 0);
+  W.fsolve_ptr.assign(1, 0);
+  for (LevelWork& P : part) {
+    const int32_t po = static_cast<int32_t>(W.panel.size()), so = static_cast<int32_t>(W.schur.size()), co = static_cast<int32_t>(W.contrib.size());
+    const int32_t fo = static_cast<int32_t>(W.fsolve.size()), fco = static_cast<int32_t>(W.fcontrib.size());
+    for (size_t i = 1; i < P.panel_ptr.size(); ++i) W.panel_ptr.push_back(po + P.panel_ptr[i]);
+    for (size_t i = 1; i < P.schur_ptr.size(); ++i) W.schur_ptr.push_back(so + P.schur_ptr[i]);
+    for (size_t i = 1; i < P.fsolve_ptr.size(); ++i) W.fsolve_ptr.push_back(fo + P.fsolve_ptr[i]);
+    W.panel.insert(W.panel.end(), P.panel.begin(), P.panel.end());
+    for (SchurTarget T : P.schur) {
+      T.c0 += co, T.c1 += co;
+      W.schur.push_back(T);
     }
-    W.schur.insert(W.schur.end(), bulk.begin(), bulk.end());
-    W.schur_crit.push_back(ncrit);
-    std::stable_sort(stmp.begin(), stmp.end(), [](const STmp& x, const STmp& y) { return x.seg < y.seg; });
-    for (size_t i = 0; i < stmp.size();) {
-      size_t j = i;
-      while (j < stmp.size() && stmp[j].seg == stmp[i].seg) ++j;
-      SolveTarget T{static_cast<int32_t>(stmp[i].seg), static_cast<int32_t>(W.fcontrib.size()), static_cast<int32_t>(W.fcontrib.size() + (j - i))};
-      for (size_t k = i; k < j; ++k) W.fcontrib.push_back(stmp[k].c);
+    W.contrib.insert(W.contrib.end(), P.contrib.begin(), P.contrib.end());
+    W.schur_crit.insert(W.schur_crit.end(), P.schur_crit.begin(), P.schur_crit.end());
+    for (SolveTarget T : P.fsolve) {
+      T.c0 += fco, T.c1 += fco;
       W.fsolve.push_back(T);
-      i = j;
     }
-    W.panel_ptr.push_back(static_cast<int32_t>(W.panel.size()));
-    W.schur_ptr.push_back(static_cast<int32_t>(W.schur.size()));
-    W.fsolve_ptr.push_back(static_cast<int32_t>(W.fsolve.size()));
+    W.fcontrib.insert(W.fcontrib.end(), P.fcontrib.begin(), P.fcontrib.end());
+    W.max_batch = std::max(W.max_batch, P.max_batch);
+    W.schur_products += P.schur_products;
   }
   return W;
 }

@@ -56,6 +56,31 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
 // out -= result instead of out = result. red: blockDim complex of shared.
 __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool conjA, const cplx* x, long long ldx, cplx* out, long long ldo,
                            bool subtract, cplx* red) {
+  if (nrhs >= 4) {
+    // many right-hand sides: thread (row, group of 4 columns), the k loop
+    // serial with 4 independent accumulators per A element (A read once per
+    // column group, coalesced across rows)
+    const int ng = (nrhs + 3) / 4;
+    for (int idx = threadIdx.x; idx < m * ng; idx += blockDim.x) {
+      const int i = idx % m, c0 = (idx / m) * 4, nc = min(4, nrhs - c0);
+      cplx acc[4] = {czero(), czero(), czero(), czero()};
+      for (int p = 0; p < k; ++p) {
+        cplx a = A[i + (size_t)p * lda];
+        if (conjA) a.y = -a.y;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nc) cfma(acc[c], a, x[p + (size_t)(c0 + c) * ldx]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < nc) {
+          cplx* o = out + i + (size_t)(c0 + c) * ldo;
+          *o = subtract ? csub(*o, acc[c]) : acc[c];
+        }
+    }
+    __syncthreads();
+    return;
+  }
   for (int i0 = 0; i0 < m; i0 += blockDim.x) {
     const int mm = min(m - i0, (int)blockDim.x);
     const int G = max(1, (int)blockDim.x / mm);
@@ -137,6 +162,35 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
     const int m = -1 - tg.seg;
     rows = S.kfin[m];
     base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
+  }
+  if (nrhs >= 4) {
+    // many right-hand sides: thread (row, group of 4 columns), contributions
+    // and their columns serial, 4 accumulators per Lbar element
+    const int ng = (nrhs + 3) / 4;
+    for (int idx = threadIdx.x; idx < rows * ng; idx += blockDim.x) {
+      const int i = idx % rows, c0 = (idx / rows) * 4, nc = min(4, nrhs - c0);
+      cplx acc[4] = {czero(), czero(), czero(), czero()};
+      for (int ci = tg.c0; ci < tg.c1; ++ci) {
+        const SolveContribD cb = contrib[ci];
+        const int e = S.bsz[cb.m] - S.kfin[cb.m];
+        const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i;
+        const cplx* h = y + S.pos[cb.m];
+        for (int p = 0; p < e; ++p) {
+          const cplx mv = M[(size_t)p * rows];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < nc) cfma(acc[c], mv, h[p + (size_t)(c0 + c) * ldy]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < nc) {
+          cplx* o = y + base + i + (size_t)(c0 + c) * ldy;
+          *o = csub(*o, acc[c]);
+        }
+    }
+    __syncthreads();
+    return;
   }
   for (int i0 = 0; i0 < rows; i0 += blockDim.x) {
     const int mm = min(rows - i0, (int)blockDim.x);
