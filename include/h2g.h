@@ -50,7 +50,8 @@ typedef struct h2g_error {
  * ascending-heap-id order (factorization.hpp:618) exactly, executed as
  * dependency wavefronts; COLORED runs a greedy distance-1 colouring, one
  * colour per batch (a different, equally valid elimination order). */
-enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1 };
+enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1, H2G_SCHEDULE_SERIAL = 2 };
+/* SERIAL: the reference order one cluster per batch (the hooks' debug mode). */
 
 /* Solve modes: solve.hpp:105 solve, :43 forward, :65 backward, :113
  * apply_inverse (alias of solve), plus the explicit-inverse application
@@ -224,6 +225,37 @@ int h2g_chain_plan(const h2g_chain* c, double* plan_ms, int32_t* built);
 /* Drop the context's structure-keyed plan cache (a later factorize of a new
  * matrix handle then builds its plan from scratch: a cold-structure run). */
 int h2g_context_clear_plans(h2g_context* ctx);
+
+/* ---- FactorizeHooks debug mode (factorization.hpp:588-593) -------------
+ * factorize with callbacks after every cluster's basis update (step 0),
+ * projection (step 2) and elimination (step 3) and after every level merge,
+ * in the reference order: the run uses the SERIAL schedule and synchronises
+ * at every step; inside a callback the h2g_state_* calls inspect the device
+ * state (FactorState, :115-251). */
+typedef struct h2g_state h2g_state;
+typedef struct h2g_factorize_hooks {
+  void* user;
+  void (*after_basis_update)(void* user, const h2g_state* st, int32_t cluster);
+  void (*after_projection)(void* user, const h2g_state* st, int32_t cluster);
+  void (*after_elimination)(void* user, const h2g_state* st, int32_t cluster);
+  void (*after_merge)(void* user, const h2g_state* st);
+} h2g_factorize_hooks;
+int h2g_factorize_hooked(h2g_context* ctx, const h2g_matrix* m, double eps_fill_in, int32_t stop_level, const h2g_factorize_hooks* hooks,
+                         h2g_chain** out, h2g_error* err);
+/* info[3]: level, active length, n */
+int h2g_state_info(const h2g_state* st, int64_t* info);
+/* out[5] for a cluster of the current level (heap id): pos, bsize, rank
+ * (kfin once its basis was updated, else the level-entry rank), rotated
+ * (projected) flag, eliminated count (0 until eliminated) */
+int h2g_state_cluster(const h2g_state* st, int32_t cluster, int64_t* out);
+/* Qtilde (bsize x bsize) of a cluster whose basis was updated */
+int h2g_state_qtilde(const h2g_state* st, int32_t cluster, double* out);
+/* FactorState::shadow() (:240-245): the dense n x n matrix the state
+ * represents (painted on the host from the device blocks; SizeGuardError
+ * above n = 4096) */
+int h2g_state_shadow(const h2g_state* st, double* out);
+/* inside after_merge: the permutation src of the level just merged */
+int h2g_state_perm(const h2g_state* st, int64_t* src, int64_t* len);
 
 /* Per-kernel-class device timing of factorize (CUDA events around every
  * launch on the context stream; off by default). Classes: 0 complement,

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <complex>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -76,6 +77,11 @@ class Context {
 // Device-resident H2Matrix (immutable input of factorize).
 class H2Matrix {
  public:
+  H2Matrix(const Context& ctx, h2g_matrix* m) : ctx_(ctx), m_(m, [](h2g_matrix* p) { h2g_matrix_destroy(p); }) {
+    int64_t s[8];
+    h2g_matrix_sizes(m, s);
+    n_ = s[0];
+  }
   H2Matrix(const Context& ctx, const h2g_matrix_desc& d) : ctx_(ctx) {
     h2g_error e{};
     h2g_matrix* m = nullptr;
@@ -84,6 +90,13 @@ class H2Matrix {
     int64_t s[8];
     h2g_matrix_sizes(m, s);
     n_ = s[0];
+  }
+  // load_h2 (serialize.hpp:198-243) onto the device
+  static H2Matrix load(const Context& ctx, const std::string& path) {
+    h2g_error e{};
+    h2g_matrix* m = nullptr;
+    check(h2g_matrix_load(ctx.get(), path.c_str(), &m, &e), e);
+    return H2Matrix(ctx, m);
   }
   int64_t n() const { return n_; }
   const h2g_matrix* get() const { return m_.get(); }
@@ -97,7 +110,8 @@ class H2Matrix {
 
 class FactorChain {
  public:
-  FactorChain(h2g_chain* c, int64_t n) : c_(c, [](h2g_chain* p) { h2g_chain_destroy(p); }), n_(n) {}
+  // The chain keeps its context alive (the C ABI reference-counts it too).
+  FactorChain(h2g_chain* c, int64_t n, Context ctx) : ctx_(std::move(ctx)), c_(c, [](h2g_chain* p) { h2g_chain_destroy(p); }), n_(n) {}
   int64_t n() const { return n_; }
   h2g_chain* get() const { return c_.get(); }
   int stop_level() const { return info()[1]; }
@@ -110,8 +124,47 @@ class FactorChain {
     h2g_chain_info(c_.get(), v.data());
     return v;
   }
+  Context ctx_;
   std::shared_ptr<h2g_chain> c_;
   int64_t n_;
+};
+
+// FactorState as a hook sees it (factorization.hpp:115-251).
+class FactorState {
+ public:
+  explicit FactorState(const h2g_state* s) : s_(s) {}
+  struct ClusterInfo {
+    int64_t pos, bsize, rank, rotated, eliminated;
+  };
+  ClusterInfo cluster(int id) const {
+    int64_t o[5];
+    h2g_error e{};
+    check(h2g_state_cluster(s_, id, o), e);
+    return {o[0], o[1], o[2], o[3], o[4]};
+  }
+  // FactorState::shadow() (:240-245), n x n column-major
+  std::vector<cxd> shadow() const {
+    int64_t info[3];
+    h2g_state_info(s_, info);
+    std::vector<cxd> Z(static_cast<size_t>(info[2] * info[2]));
+    h2g_error e{};
+    const int rc = h2g_state_shadow(s_, reinterpret_cast<double*>(Z.data()));
+    if (rc) {
+      h2g_last_error(&e);
+      check(rc, e);
+    }
+    return Z;
+  }
+  const h2g_state* get() const { return s_; }
+
+ private:
+  const h2g_state* s_;
+};
+
+// FactorizeHooks (factorization.hpp:588-593)
+struct FactorizeHooks {
+  std::function<void(const FactorState&, int)> after_basis_update, after_projection, after_elimination;
+  std::function<void(const FactorState&)> after_merge;
 };
 
 inline FactorChain factorize(const H2Matrix& A, double eps_fill_in, std::optional<int> stop_level_override = std::nullopt,
@@ -119,7 +172,65 @@ inline FactorChain factorize(const H2Matrix& A, double eps_fill_in, std::optiona
   h2g_error e{};
   h2g_chain* c = nullptr;
   check(h2g_factorize(A.ctx().get(), A.get(), eps_fill_in, stop_level_override.value_or(-1), schedule, &c, &e), e);
-  return FactorChain(c, A.n());
+  return FactorChain(c, A.n(), A.ctx());
+}
+
+// factorize(A, eps, stop, hooks) (factorization.hpp:600-601): the device in
+// debug mode (reference order, one cluster per step).
+inline FactorChain factorize(const H2Matrix& A, double eps_fill_in, std::optional<int> stop_level_override, const FactorizeHooks* hooks) {
+  if (!hooks) return factorize(A, eps_fill_in, stop_level_override);
+  h2g_factorize_hooks h{};
+  h.user = const_cast<FactorizeHooks*>(hooks);
+  h.after_basis_update = [](void* u, const h2g_state* st, int32_t i) {
+    auto* k = static_cast<FactorizeHooks*>(u);
+    if (k->after_basis_update) k->after_basis_update(FactorState(st), i);
+  };
+  h.after_projection = [](void* u, const h2g_state* st, int32_t i) {
+    auto* k = static_cast<FactorizeHooks*>(u);
+    if (k->after_projection) k->after_projection(FactorState(st), i);
+  };
+  h.after_elimination = [](void* u, const h2g_state* st, int32_t i) {
+    auto* k = static_cast<FactorizeHooks*>(u);
+    if (k->after_elimination) k->after_elimination(FactorState(st), i);
+  };
+  h.after_merge = [](void* u, const h2g_state* st) {
+    auto* k = static_cast<FactorizeHooks*>(u);
+    if (k->after_merge) k->after_merge(FactorState(st));
+  };
+  h2g_error e{};
+  h2g_chain* c = nullptr;
+  check(h2g_factorize_hooked(A.ctx().get(), A.get(), eps_fill_in, stop_level_override.value_or(-1), &h, &c, &e), e);
+  return FactorChain(c, A.n(), A.ctx());
+}
+
+// ---- H2LU v1 container (serialize.hpp:186-353)
+inline void save_h2(const std::string& path, const H2Matrix& A) {
+  h2g_error e{};
+  check(h2g_matrix_save(A.get(), path.c_str(), &e), e);
+}
+inline void save_chain(const std::string& path, const FactorChain& c, const H2Matrix& source) {
+  h2g_error e{};
+  check(h2g_chain_save(c.get(), source.get(), path.c_str(), &e), e);
+}
+inline FactorChain load_chain(const Context& ctx, const std::string& path) {
+  h2g_error e{};
+  h2g_chain* c = nullptr;
+  check(h2g_chain_load(ctx.get(), path.c_str(), &c, &e), e);
+  int64_t info[6];
+  h2g_chain_info(c, info);
+  return FactorChain(c, info[0], ctx);
+}
+inline void save_vector(const std::string& path, const Vec& v) {
+  h2g_error e{};
+  check(h2g_vector_save(path.c_str(), reinterpret_cast<const double*>(v.data()), static_cast<int64_t>(v.size()), &e), e);
+}
+inline Vec load_vector(const std::string& path) {
+  h2g_error e{};
+  int64_t n = 0;
+  check(h2g_vector_load(path.c_str(), nullptr, &n, &e), e);
+  Vec v(static_cast<size_t>(n));
+  check(h2g_vector_load(path.c_str(), reinterpret_cast<double*>(v.data()), &n, &e), e);
+  return v;
 }
 
 inline Vec run(const FactorChain& ch, const Vec& b, int mode) {

@@ -23,7 +23,7 @@ from . import geometry  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("H2G_LIB", os.path.join(_HERE, "libh2g.so"))
 
-SCHEDULES = {"reference": 0, "colored": 1}
+SCHEDULES = {"reference": 0, "colored": 1, "serial": 2}
 KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2
 _SOLVE, _FORWARD, _BACKWARD, _APPLY_INVERSE, _APPLY_INVERSE_EXPLICIT = 0, 1, 2, 3, 4
 
@@ -165,6 +165,12 @@ SYMBOLS = {
     "h2g_chain_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_P), C.POINTER(_Err)]),
     "h2g_vector_save": (C.c_int, [C.c_char_p, _D, C.c_int64, C.POINTER(_Err)]),
     "h2g_chain_perm_tree": (C.c_int, [_P, _I64]),
+    "h2g_factorize_hooked": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_void_p, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_state_info": (C.c_int, [_P, _I64]),
+    "h2g_state_cluster": (C.c_int, [_P, C.c_int32, _I64]),
+    "h2g_state_qtilde": (C.c_int, [_P, C.c_int32, _D]),
+    "h2g_state_shadow": (C.c_int, [_P, _D]),
+    "h2g_state_perm": (C.c_int, [_P, _I64, _I64]),
     "h2g_vector_load": (C.c_int, [C.c_char_p, _D, _I64, C.POINTER(_Err)]),
     "h2g_context_clear_plans": (C.c_int, [_P]),
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
@@ -648,6 +654,103 @@ def load_vector(path):
     v = np.zeros(n.value, np.complex128)
     _check(lib().h2g_vector_load(os.fsencode(path), _d(v.view(np.float64)), C.byref(n), C.byref(err)), err)
     return v
+
+
+_STEP_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int32)
+_MERGE_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+class _Hooks(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("after_basis_update", _STEP_CB), ("after_projection", _STEP_CB), ("after_elimination", _STEP_CB),
+                ("after_merge", _MERGE_CB)]
+
+
+class FactorState:
+    """What a FactorizeHooks callback sees (FactorState, factorization.hpp:115-251);
+    valid only inside the callback."""
+
+    def __init__(self, ptr):
+        self.p = ptr
+
+    def info(self):
+        out = np.zeros(3, np.int64)
+        lib().h2g_state_info(self.p, _i64(out))
+        return dict(level=int(out[0]), active_len=int(out[1]), n=int(out[2]))
+
+    def cluster(self, cid):
+        out = np.zeros(5, np.int64)
+        err = _Err()
+        if lib().h2g_state_cluster(self.p, cid, _i64(out)):
+            lib().h2g_last_error(C.byref(err))
+            _raise(err)
+        return dict(pos=int(out[0]), bsize=int(out[1]), rank=int(out[2]), rotated=bool(out[3]), eliminated=int(out[4]))
+
+    def qtilde(self, cid):
+        b = self.cluster(cid)["bsize"]
+        Q = np.zeros((b, b), np.complex128, order="F")
+        err = _Err()
+        if lib().h2g_state_qtilde(self.p, cid, Q.ctypes.data_as(_D)):
+            lib().h2g_last_error(C.byref(err))
+            _raise(err)
+        return Q
+
+    def shadow(self):
+        """FactorState::shadow() (factorization.hpp:240-245) of the device state."""
+        n = self.info()["n"]
+        Z = np.zeros((n, n), np.complex128, order="F")
+        err = _Err()
+        if lib().h2g_state_shadow(self.p, Z.ctypes.data_as(_D)):
+            lib().h2g_last_error(C.byref(err))
+            _raise(err)
+        return Z
+
+    def perm(self):
+        n = C.c_int64(0)
+        lib().h2g_state_perm(self.p, None, C.byref(n))
+        out = np.zeros(n.value, np.int64)
+        lib().h2g_state_perm(self.p, _i64(out), C.byref(n))
+        return out
+
+
+def factorize_hooked(A, eps_fill_in, after_basis_update=None, after_projection=None, after_elimination=None, after_merge=None,
+                     stop_level_override=None):
+    """factorize(A, eps, stop, hooks) (factorization.hpp:588-601): the GPU path in
+    debug mode (reference order one cluster at a time, synchronised at every
+    step); each callback gets (FactorState, cluster heap id) or (FactorState,).
+    Exceptions raised inside callbacks are re-raised after the factorization."""
+    errors = []
+
+    def wrap_step(f):
+        def cb(user, st, cl):
+            if f is None or errors:
+                return
+            try:
+                f(FactorState(st), int(cl))
+            except BaseException as e:  # noqa: BLE001 - re-raised below
+                errors.append(e)
+        return _STEP_CB(cb)
+
+    def wrap_merge(f):
+        def cb(user, st):
+            if f is None or errors:
+                return
+            try:
+                f(FactorState(st))
+            except BaseException as e:  # noqa: BLE001
+                errors.append(e)
+        return _MERGE_CB(cb)
+
+    hk = _Hooks(None, wrap_step(after_basis_update), wrap_step(after_projection), wrap_step(after_elimination), wrap_merge(after_merge))
+    err = _Err()
+    h = _P()
+    stop = -1 if stop_level_override is None else int(stop_level_override)
+    rc = lib().h2g_factorize_hooked(A.ctx.h, A.h, float(eps_fill_in), stop, C.cast(C.pointer(hk), C.c_void_p), C.byref(h), C.byref(err))
+    if errors:
+        if rc == 0:
+            FactorChain(h, A)  # released
+        raise errors[0]
+    _check(rc, err)
+    return FactorChain(h, A)
 
 
 def factorize(A, eps_fill_in, stop_level_override=None, schedule="reference"):

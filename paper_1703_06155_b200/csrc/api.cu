@@ -285,7 +285,7 @@ size_t pinned_cap() {
   static const size_t cap = [] {
     if (const char* e = std::getenv("H2G_HOST_STAGING_GB")) return (size_t)(std::atof(e) * 1e9);
     const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
-    return pages > 0 && psz > 0 ? (size_t)(0.6 * (double)pages * (double)psz) : (size_t)96e9;  // 60 % of host RAM
+    return pages > 0 && psz > 0 ? (size_t)(0.75 * (double)pages * (double)psz) : (size_t)96e9;  // 75 % of host RAM
   }();
   return cap;
 }
@@ -682,6 +682,165 @@ long long pack_offsets(const std::vector<int>& rows, const std::vector<int>& col
 
 }  // namespace
 
+// ============================================== FactorizeHooks debug state
+// What a hook sees (FactorState, factorization.hpp:115-251): the current
+// level's device pools and the host bookkeeping of the driver.
+struct h2g_state {
+  h2g_context* ctx = nullptr;
+  const h2g_matrix* M = nullptr;
+  const LevelData* cur = nullptr;       // level pools (dense D, fill F, V0)
+  const LevelSym* Y = nullptr;          // level structure
+  int level = 0;
+  const int* d_kfin = nullptr;          // device kfin (nullptr after a merge: kfin = korig)
+  const std::vector<char>* rotated = nullptr;
+  const std::vector<int>* elim = nullptr;  // eliminated count per cluster (0 until eliminated)
+  const cplx* chain = nullptr;          // level chain arena (Qtilde)
+  const std::vector<long long>* Qt_off = nullptr;
+  const std::vector<int64_t>* perm_src = nullptr;  // after_merge: the permutation just applied
+};
+
+namespace {
+
+using cx = std::complex<double>;
+
+std::vector<cx> dl(const void* dev, size_t elems, cudaStream_t st) {
+  std::vector<cx> h(elems);
+  if (elems) CK(cudaMemcpyAsync(h.data(), dev, elems * 16, cudaMemcpyDefault, st));
+  return h;
+}
+
+// FactorState::paint / shadow (factorization.hpp:177-245) from device blocks.
+std::vector<cx> state_shadow(const h2g_state& S) {
+  const h2g_matrix& M = *S.M;
+  const Structure& T = M.S;
+  const LevelData& cur = *S.cur;
+  const LevelSym& Y = *S.Y;
+  const int64_t n = T.n;
+  if (n > 4096) throw Error(H2G_ERR_SIZE_GUARD, fmt("shadow: n = %lld exceeds the guard 4096", n));
+  cudaStream_t st = S.ctx->stream;
+  const int nl = Y.nl, l = S.level, first = Y.first;
+  std::vector<int> kf(cur.korig);
+  if (S.d_kfin) CK(cudaMemcpyAsync(kf.data(), S.d_kfin, nl * 4, cudaMemcpyDeviceToHost, st));
+  const auto D = dl(cur.D.p, cur.D.bytes / 16, st);
+  const auto F = dl(cur.F.p, cur.F.bytes / 16, st);
+  std::vector<int> fex(Y.frow.size(), 0);
+  if (!fex.empty()) CK(cudaMemcpyAsync(fex.data(), cur.fex.p, fex.size() * 4, cudaMemcpyDeviceToHost, st));
+  const size_t bb = (size_t)cur.bmax * cur.bmax;
+  const auto V0 = dl(cur.V0.p, cur.V0.bytes / 16, st);
+  const auto B = dl(M.basis.p, M.basis_elems, st);
+  const auto Cp = dl(M.coup.p, M.coup_elems, st);
+  CK(cudaStreamSynchronize(st));
+  std::vector<std::vector<cx>> Q(nl);
+  for (int t = 0; t < nl; ++t)
+    if ((*S.rotated)[t]) {
+      Q[t] = dl(S.chain + (*S.Qt_off)[t], (size_t)cur.bsz[t] * cur.bsz[t], st);
+      CK(cudaStreamSynchronize(st));
+    }
+  int64_t active = 0;
+  for (int t = 0; t < nl; ++t) active = std::max<int64_t>(active, cur.pos[t] + cur.bsz[t]);
+  std::vector<cx> Z((size_t)n * n, 0.0);
+  for (int64_t p = active; p < n; ++p) Z[p + p * n] = 1.0;
+  auto kor = [&](int id) { return (int)M.basis_rank[id]; };
+  // place_block (:177-188): rotate a projected side and zero its eliminated part
+  auto place = [&](int t, int s2, std::vector<cx> Mb) {
+    const int bt = cur.bsz[t], bs = cur.bsz[s2];
+    if ((*S.rotated)[t]) {
+      std::vector<cx> R((size_t)bt * bs, 0.0);
+      for (int j = 0; j < bs; ++j)
+        for (int i = 0; i < bt; ++i) {
+          cx a = 0.0;
+          for (int p = 0; p < bt; ++p) a += std::conj(Q[t][p + (size_t)i * bt]) * Mb[p + (size_t)j * bt];
+          R[i + (size_t)j * bt] = i < bt - kf[t] ? cx(0.0) : a;
+        }
+      Mb.swap(R);
+    }
+    if ((*S.rotated)[s2]) {
+      std::vector<cx> R((size_t)bt * bs, 0.0);
+      for (int j = 0; j < bs; ++j)
+        for (int i = 0; i < bt; ++i) {
+          cx a = 0.0;
+          for (int p = 0; p < bs; ++p) a += Mb[i + (size_t)p * bt] * std::conj(Q[s2][p + (size_t)j * bs]);
+          R[i + (size_t)j * bt] = j < bs - kf[s2] ? cx(0.0) : a;
+        }
+      Mb.swap(R);
+    }
+    for (int j = 0; j < bs; ++j)
+      for (int i = 0; i < bt; ++i) Z[(cur.pos[t] + i) + (size_t)(cur.pos[s2] + j) * n] = Mb[i + (size_t)j * bt];
+  };
+  // dense blocks (in place on the device, already in their current frames)
+  for (size_t q = 0; q < Y.drow.size(); ++q) {
+    const int r = Y.drow[q], c = Y.dcol[q];
+    for (int j = 0; j < cur.bsz[c]; ++j)
+      for (int i = 0; i < cur.bsz[r]; ++i) Z[(cur.pos[r] + i) + (size_t)(cur.pos[c] + j) * n] = D[cur.doff[q] + i + (size_t)j * cur.bsz[r]];
+  }
+  // expanded level-entry bases of this level's clusters to an ancestor
+  // level la (expand_to_level, :191-201): E (bsz_u x k_anc)
+  auto expand = [&](int u, int la) {
+    const int b = cur.bsz[u];
+    std::vector<cx> E((size_t)b * kor(first + u));
+    const int k0 = kor(first + u);
+    for (int j = 0; j < k0; ++j)
+      for (int i = 0; i < b; ++i) E[i + (size_t)j * b] = V0[u * bb + i + (size_t)j * b];
+    int id = first + u, kc = k0;
+    for (int lv = l; lv > la; --lv) {
+      const int par = (id - 1) / 2, kp = kor(par);
+      const int roff = (id == 2 * par + 1) ? 0 : kor(2 * par + 1);
+      const int rows = (int)M.basis_rows[par];
+      std::vector<cx> E2((size_t)b * kp, 0.0);
+      for (int j = 0; j < kp; ++j)
+        for (int p = 0; p < kc; ++p) {
+          const cx tv = B[M.basis_off[par] + roff + p + (size_t)j * rows];
+          for (int i = 0; i < b; ++i) E2[i + (size_t)j * b] += E[i + (size_t)p * b] * tv;
+        }
+      E.swap(E2);
+      id = par, kc = kp;
+    }
+    return E;
+  };
+  auto fill_of = [&](int r, int c) {
+    const int f = Y.fill_index(r, c);
+    return (f >= 0 && fex[f] && cur.foff[f] >= 0) ? f : -1;
+  };
+  const int lmin = T.l0 >= 0 ? T.l0 : l + 1;
+  for (int la = lmin; la <= l; ++la) {
+    for (size_t pq = 0; pq < T.adm[la].size(); ++pq) {
+      const int R = T.adm[la][pq].row, Cc = T.adm[la][pq].col;
+      const int kr = kor(R), kc2 = kor(Cc);
+      const cx* Sm = reinterpret_cast<const cx*>(Cp.data()) + M.coup_off[T.adm_offset[la] + pq];
+      const int span = 1 << (l - la);
+      const int u0 = ((R + 1) << (l - la)) - 1 - first, v0 = ((Cc + 1) << (l - la)) - 1 - first;
+      for (int u = u0; u < u0 + span; ++u) {
+        const auto Eu = expand(u, la);
+        // X = Eu S (bsz_u x kc2)
+        std::vector<cx> X((size_t)cur.bsz[u] * kc2, 0.0);
+        for (int j = 0; j < kc2; ++j)
+          for (int p = 0; p < kr; ++p) {
+            const cx sv = Sm[p + (size_t)j * kr];
+            for (int i = 0; i < cur.bsz[u]; ++i) X[i + (size_t)j * cur.bsz[u]] += Eu[i + (size_t)p * cur.bsz[u]] * sv;
+          }
+        for (int v = v0; v < v0 + span; ++v) {
+          const auto Ev = expand(v, la);
+          const int bu = cur.bsz[u], bv = cur.bsz[v];
+          std::vector<cx> Mb((size_t)bu * bv, 0.0);
+          for (int j = 0; j < bv; ++j)
+            for (int p = 0; p < kc2; ++p) {
+              const cx ev = Ev[j + (size_t)p * bv];
+              for (int i = 0; i < bu; ++i) Mb[i + (size_t)j * bu] += X[i + (size_t)p * bu] * ev;
+            }
+          const int f = fill_of(u, v);
+          if (f >= 0)
+            for (int j = 0; j < bv; ++j)
+              for (int i = 0; i < bu; ++i) Mb[i + (size_t)j * bu] += F[cur.foff[f] + i + (size_t)j * bu];
+          place(u, v, std::move(Mb));
+        }
+      }
+    }
+  }
+  return Z;
+}
+
+}  // namespace
+
 // ================================================================ C ABI
 extern "C" {
 
@@ -930,11 +1089,16 @@ int h2g_kernel_rows_matvec(h2g_context* ctx, const double* points_tree, int64_t 
 }
 
 // ------------------------------------------------------------- factorize
-int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t stop_level, int32_t schedule, h2g_chain** out, h2g_error* err) {
+}  // extern "C"
+
+static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t stop_level, int32_t schedule, const h2g_factorize_hooks* hooks,
+                          h2g_chain** out, h2g_error* err) {
   return guarded(err, [&] {
     if (!ctx || !mc || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
     if (!(eps > 0.0)) throw Error(H2G_ERR_INVALID_INPUT, "factorize: eps_fill_in must be positive");
-    if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED) throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
+    if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED && schedule != H2G_SCHEDULE_SERIAL)
+      throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
+    if (hooks) schedule = H2G_SCHEDULE_SERIAL;  // debug mode: one cluster per step, reference order
     std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);
     CK(cudaSetDevice(ctx->device));
     h2g_matrix* M = const_cast<h2g_matrix*>(mc);
@@ -1280,13 +1444,13 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         // column item D(t,c): T = Qt^H D, Ubar = L11^{-1} T[:e,:], lift = Ubar Qt_c^T, D = T (rows < e zeroed)
         // row item    D(j,t): T = D conj(Qt), Lbar = T[:,:e] U11^{-1}, lift = Qt_j Lbar, D = T (cols < e zeroed)
         std::vector<GemmDesc> gP1, gP2, gP3;
-        std::vector<MaskDesc> gPM;
+        std::vector<MaskDesc> gPM, gPC;
         std::vector<int> p3_ptr(1, 0);
         size_t pmax = 1;
         for (int bi = 0; bi < nbat0; ++bi) pmax = std::max<size_t>(pmax, W.panel_ptr[bi + 1] - W.panel_ptr[bi]);
         DBuf panbuf;
         panbuf.alloc(pmax * bb * 16, st);
-        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dP1, dP2, dP3, dPM;
+        DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dP1, dP2, dP3, dPM, dPC;
         upload(dR1, gR1, st);
         upload(dR2, gR2, st);
         upload(dA1, gA1, st);
@@ -1393,6 +1557,8 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
                 }
                 gPM.push_back({T, Dblk, bn, bn, b, 1, b, 0, kfd + t});
               }
+              gPC.push_back(gPM.back());
+              gPC.back().e0 = 0;  // e = 0 - kfin <= 0: a plain copy (debug mode, after projection)
               gP1.push_back(r);
               gP2.push_back(pp);
               if (lifted(pi)) gP3.push_back(lf);
@@ -1403,6 +1569,7 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           upload(dP2, gP2, st);
           upload(dP3, gP3, st);
           upload(dPM, gPM, st);
+          if (hooks) upload(dPC, gPC, st);
         }
         mark("setup done");
         ctx->prof.cur_level = l;
@@ -1504,6 +1671,23 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           CK(cudaMemcpyAsync(core_tab.p, core_ptr_h.data(), nfill * sizeof(cplx*), cudaMemcpyHostToDevice, st));
           CK(cudaStreamSynchronize(st));  // core_ptr_h is rewritten at the next segment end
         };
+        std::vector<char> rotated(nl, 0);
+        std::vector<int> elimv(nl, 0);
+        h2g_state hstate;
+        hstate.ctx = ctx;
+        hstate.M = M;
+        hstate.cur = &cur;
+        hstate.Y = &Y;
+        hstate.level = l;
+        hstate.d_kfin = nullptr;
+        hstate.rotated = &rotated;
+        hstate.elim = &elimv;
+        hstate.chain = CL->arena.as<cplx>();
+        hstate.Qt_off = &Qt_off;
+        auto hook_sync = [&] {
+          CK(cudaStreamSynchronize(st));
+          check_device_error(ctx, l);
+        };
         for (int bi = 0; bi < nbat; ++bi) {
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
           const int sgi = fill_segment(bi, nbat, FP.K);
@@ -1545,14 +1729,29 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           }
           pf.begin(PC_HEAD, st);
           launch_head(DL, d_bat + p0, p0, nb, st);
+          if (hooks) {  // debug mode (SERIAL schedule: the batch is one cluster)
+            hook_sync();
+            hstate.d_kfin = DL.kfin;
+            if (hooks->after_basis_update) hooks->after_basis_update(hooks->user, &hstate, Y.first + SC.batch_cl[p0]);
+          }
           launch_gemm(dR1.as<GemmDesc>() + p0, nb, st, tl);
           launch_gemm(dR2.as<GemmDesc>() + p0, nb, st, tl);
+          if (hooks) {
+            // step 2 in full before step 3: the rotated row / column blocks
+            // land in D unmasked (the reference's state after projection)
+            const int i0 = W.panel_ptr[bi], ni = W.panel_ptr[bi + 1] - i0;
+            launch_gemm(dP1.as<GemmDesc>() + i0, ni, st, tl);
+            launch_mask(dPC.as<MaskDesc>() + i0, ni, st);
+            hook_sync();
+            rotated[SC.batch_cl[p0]] = 1;
+            if (hooks->after_projection) hooks->after_projection(hooks->user, &hstate, Y.first + SC.batch_cl[p0]);
+          }
           launch_head2(DL, d_bat + p0, nb, mmax, st);
           pf.end(st);
           pf.begin(PC_PANEL, st);
           {
             const int i0 = W.panel_ptr[bi], ni = W.panel_ptr[bi + 1] - i0;
-            launch_gemm(dP1.as<GemmDesc>() + i0, ni, st, tl);
+            if (!hooks) launch_gemm(dP1.as<GemmDesc>() + i0, ni, st, tl);
             launch_gemm(dP2.as<GemmDesc>() + i0, ni, st, tl);
             launch_gemm(dP3.as<GemmDesc>() + p3_ptr[bi], p3_ptr[bi + 1] - p3_ptr[bi], st, tl);
             launch_mask(dPM.as<MaskDesc>() + i0, ni, st);
@@ -1587,6 +1786,15 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
           const int npl = W.panel_ptr[bi + 1] > W.panel_ptr[bi] ? 3 + (p3_ptr[bi + 1] > p3_ptr[bi]) : 0;
           C->klaunch[PC_PANEL] += npl;
           launches += 3 + pass2_possible + (mmax > 0) + nhead + (pass2_possible ? 2 : 1) * ((na > 0) + (nbd > 0)) + (nn > 0) + npl;
+          if (hooks) {
+            CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));
+            hook_sync();
+            const int tcl = SC.batch_cl[p0];
+            int kft = 0;
+            CK(cudaMemcpy(&kft, DL.kfin + tcl, 4, cudaMemcpyDeviceToHost));
+            elimv[tcl] = cur.bsz[tcl] - kft;
+            if (hooks->after_elimination) hooks->after_elimination(hooks->user, &hstate, Y.first + tcl);
+          }
           if (bi + 1 == FP.seg_first_batch[sgi + 1]) segment_end(sgi);
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
@@ -1914,8 +2122,28 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         cur.D.release();  // stream-ordered: reused only after the copies above
         mark("merge: dense blocks assembled");
         // (2) the parent fill pool; cores accumulate on top of the copies
-        // (dst = pad(S) + Z)
-        ensure((size_t)(std::max<long long>(nftot, 1) + YP.frow.size() * 4) + 16, CL.get());
+        // (dst = pad(S) + Z). When HBM is short the device-resident cores
+        // move to pinned host memory first (they are read once, below).
+        {
+          const size_t need = (size_t)std::max<long long>(nftot, 1) * 16 + YP.frow.size() * 4 + 16;
+          ensure(need, CL.get());
+          for (size_t ci = 0; ci < core_chunks.size() && BlockCache::get().headroom() < need + kMargin; ++ci) {
+            DBuf& dch = core_chunks[ci];
+            if (!dch.p) continue;
+            core_hchunks.emplace_back();
+            HBuf& hch = core_hchunks.back();
+            hch.alloc(dch.bytes);
+            CK(cudaMemcpyAsync(hch.p, dch.p, dch.bytes, cudaMemcpyDeviceToHost, st));
+            const char* d0 = static_cast<const char*>(dch.p);
+            for (auto& cp : core_ptr_h) {
+              const char* q = reinterpret_cast<const char*>(cp);
+              if (q >= d0 && q < d0 + dch.bytes) cp = reinterpret_cast<cplx*>(static_cast<char*>(hch.p) + (q - d0));
+            }
+            CK(cudaStreamSynchronize(st));
+            dch.release();
+            BlockCache::get().trim();
+          }
+        }
         nxt.F.alloc(std::max<long long>(nftot, 1) * 16, st, true);
         nxt.fex.alloc(std::max<size_t>(YP.frow.size(), 1) * 4, st, true);
         cplx* Fp = nxt.F.as<cplx>();
@@ -1953,6 +2181,25 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
         C->levels.push_back(std::move(CL));
         cur = std::move(nxt);
         last_level = lp;
+        if (hooks && hooks->after_merge) {
+          // the parent level's state (nothing projected yet); its structure
+          // is the next plan level
+          std::vector<char> rot0(cur.bsz.size(), 0);
+          std::vector<int> el0(cur.bsz.size(), 0);
+          std::vector<int64_t> src_used(C->levels.back()->src.begin(), C->levels.back()->src.end());
+          h2g_state ms;
+          ms.ctx = ctx;
+          ms.M = M;
+          ms.cur = &cur;
+          ms.Y = &P->levels[li + 1];
+          ms.level = lp;
+          ms.d_kfin = nullptr;
+          ms.rotated = &rot0;
+          ms.elim = &el0;
+          ms.perm_src = &src_used;
+          CK(cudaStreamSynchronize(st));
+          hooks->after_merge(hooks->user, &ms);
+        }
         if (elim == 0 && l > stop) {
           C->stop_level = l;
           ++li;
@@ -2142,6 +2389,17 @@ int h2g_factorize(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t st
     ++ctx->refs;  // the chain holds the context
     *out = C.release();
   });
+}
+
+extern "C" {
+
+int h2g_factorize(h2g_context* ctx, const h2g_matrix* m, double eps, int32_t stop_level, int32_t schedule, h2g_chain** out, h2g_error* err) {
+  return factorize_impl(ctx, m, eps, stop_level, schedule, nullptr, out, err);
+}
+
+int h2g_factorize_hooked(h2g_context* ctx, const h2g_matrix* m, double eps, int32_t stop_level, const h2g_factorize_hooks* hooks, h2g_chain** out,
+                         h2g_error* err) {
+  return factorize_impl(ctx, m, eps, stop_level, H2G_SCHEDULE_SERIAL, hooks, out, err);
 }
 
 int h2g_chain_destroy(h2g_chain* c) {
@@ -2987,6 +3245,60 @@ int h2g_vector_load(const char* path, double* data, int64_t* n, h2g_error* err) 
       *n = (int64_t)v.size();
     });
   });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int h2g_state_info(const h2g_state* st, int64_t* info) {
+  if (!st || !info) return H2G_ERR_INVALID_INPUT;
+  int64_t active = 0;
+  for (size_t t = 0; t < st->cur->bsz.size(); ++t) active = std::max<int64_t>(active, st->cur->pos[t] + st->cur->bsz[t]);
+  info[0] = st->level;
+  info[1] = active;
+  info[2] = st->M->S.n;
+  return H2G_OK;
+}
+
+int h2g_state_cluster(const h2g_state* st, int32_t cluster, int64_t* out) {
+  return guarded(nullptr, [&] {
+    if (!st || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    const int t = cluster - st->Y->first;
+    if (t < 0 || t >= st->Y->nl) throw Error(H2G_ERR_INVALID_INPUT, "state_cluster: cluster not on the current level");
+    int kf = st->cur->korig[t];
+    if (st->d_kfin) CK(cudaMemcpy(&kf, st->d_kfin + t, 4, cudaMemcpyDeviceToHost));
+    out[0] = st->cur->pos[t];
+    out[1] = st->cur->bsz[t];
+    out[2] = kf;
+    out[3] = (*st->rotated)[t];
+    out[4] = (*st->elim)[t];
+  });
+}
+
+int h2g_state_qtilde(const h2g_state* st, int32_t cluster, double* out) {
+  return guarded(nullptr, [&] {
+    if (!st || !out || !st->chain || !st->Qt_off) throw Error(H2G_ERR_INVALID_INPUT, "state_qtilde: no projection on this state");
+    const int t = cluster - st->Y->first;
+    if (t < 0 || t >= st->Y->nl) throw Error(H2G_ERR_INVALID_INPUT, "state_qtilde: cluster not on the current level");
+    const int b = st->cur->bsz[t];
+    CK(cudaMemcpy(out, st->chain + (*st->Qt_off)[t], (size_t)b * b * 16, cudaMemcpyDeviceToHost));
+  });
+}
+
+int h2g_state_shadow(const h2g_state* st, double* out) {
+  return guarded(nullptr, [&] {
+    if (!st || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    const auto Z = state_shadow(*st);
+    std::memcpy(out, Z.data(), Z.size() * 16);
+  });
+}
+
+int h2g_state_perm(const h2g_state* st, int64_t* src, int64_t* len) {
+  if (!st || !len || !st->perm_src) return H2G_ERR_INVALID_INPUT;
+  if (src) std::copy(st->perm_src->begin(), st->perm_src->end(), src);
+  *len = (int64_t)st->perm_src->size();
+  return H2G_OK;
 }
 
 }  // extern "C"

@@ -355,6 +355,8 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
       while (mark[static_cast<size_t>(c)] == t) ++c;
       key[static_cast<size_t>(t)] = c;
     }
+  } else if (kind == H2G_SCHEDULE_SERIAL) {
+    for (int t = 0; t < nl; ++t) key[static_cast<size_t>(t)] = t;  // one cluster per batch, ascending id
   } else {
     // dependency wavefronts of the ascending-id order: every lower-id
     // neighbour completes before t starts, no higher-id neighbour does.

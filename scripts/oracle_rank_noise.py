@@ -42,9 +42,15 @@ per_level = {}
 for lv in sorted({k[0] for k in rf}, reverse=True):
     dl = np.array([v for k, v in d.items() if k[0] == lv])
     per_level[str(lv)] = dict(max_abs=int(np.abs(dl).max()), nonzero=int(np.count_nonzero(dl)), clusters=int(dl.size))
-res = dict(config=cfg, eps=c["eps"], perturbation="GEMM inner-product order reversed (oracle/dense.hpp gemm_acc); same H2 input",
+mean_abs = {}
+for lv in sorted({k[0] for k in rf}, reverse=True):
+    mean_abs[str(lv)] = float(np.mean([abs(v) for k, v in d.items() if k[0] == lv]))
+res = dict(config=cfg, eps=c["eps"], mean_abs_per_level=mean_abs, perturbation="GEMM inner-product order reversed (oracle/dense.hpp gemm_acc); same H2 input",
            max_abs_rank_diff=int(max(abs(v) for v in d.values())), nonzero=int(sum(1 for v in d.values() if v)), clusters=len(d),
            per_level=per_level, rank_sum_after_forward=runs["forward"][1], rank_sum_after_reverse=runs["reverse"][1],
            root_forward=runs["forward"][2], root_reverse=runs["reverse"][2])
 json.dump(res, open(out, "w"), indent=1)
+keys = sorted(rf)
+np.savez_compressed(os.path.splitext(out)[0] + ".npz", level_cluster=np.array(keys, np.int64), forward=np.array([rf[k] for k in keys], np.int64),
+                    reverse=np.array([rr[k] for k in keys], np.int64))
 print(json.dumps(res))

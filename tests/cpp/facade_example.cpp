@@ -35,6 +35,20 @@ int main() {
     Vec y = apply_inverse(ch, b);
     bool same = y == x;
     std::printf("facade: root %lld residual %.3e apply_inverse==solve %d\n", (long long)ch.root_size(), err, (int)same);
+    // the chain outlives the Context / H2Matrix handles it came from
+    FactorChain kept = [&] {
+      Context c2(0);
+      H2Matrix A2(c2, d);
+      return factorize(A2, 1e-8);
+    }();
+    const bool kept_ok = solve(kept, b) == x;
+    // hooks (debug mode; a single leaf goes straight to the root: no steps)
+    FactorizeHooks hk;
+    int steps = 0;
+    hk.after_projection = [&](const FactorState&, int) { ++steps; };
+    FactorChain ch2 = factorize(A, 1e-8, std::nullopt, &hk);
+    std::printf("facade: kept chain solves %d, hooked steps %d\n", (int)kept_ok, steps);
+    if (!kept_ok || solve(ch2, b) != x) return 4;
     // singular pivot -> SingularPivotError with the root's cluster -1
     std::vector<cxd> Z(n * n, cxd(0.0));
     d.dense_data = reinterpret_cast<const double*>(Z.data());
