@@ -50,8 +50,12 @@ typedef struct h2g_error {
  * ascending-heap-id order (factorization.hpp:618) exactly, executed as
  * dependency wavefronts; COLORED runs a greedy distance-1 colouring, one
  * colour per batch (a different, equally valid elimination order). */
-enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1, H2G_SCHEDULE_SERIAL = 2 };
-/* SERIAL: the reference order one cluster per batch (the hooks' debug mode). */
+enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1, H2G_SCHEDULE_SERIAL = 2, H2G_SCHEDULE_INTERIOR_FIRST = 3 };
+/* SERIAL: the reference order one cluster per batch (the hooks' debug mode).
+ * INTERIOR_FIRST: the north_star's 8-way subtree split as an order (SURVEY
+ * §8e option 2): per level with >= 8 clusters, the clusters whose dense
+ * neighbours all lie in their own level-3 subtree first, then the boundary
+ * clusters (each group ascending id); coarser levels in reference order. */
 
 /* Solve modes: solve.hpp:105 solve, :43 forward, :65 backward, :113
  * apply_inverse (alias of solve), plus the explicit-inverse application

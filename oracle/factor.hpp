@@ -134,7 +134,8 @@ struct BlockMap {
 };
 
 // ------------------------------------------------------------- schedules
-enum ScheduleKind { SCHEDULE_REFERENCE = 0, SCHEDULE_COLORED = 1 };
+enum ScheduleKind { SCHEDULE_REFERENCE = 0, SCHEDULE_COLORED = 1, SCHEDULE_INTERIOR_FIRST = 3 };
+constexpr int kInteriorParts = 8;  // the north_star's 8-GPU subtree split
 
 // Greedy distance-1 colouring in ascending id over the dense-neighbour graph
 // of one level; returns the cluster order (colour, id).
@@ -621,6 +622,24 @@ inline std::vector<int> level_order(const FactorState& st, int l, int schedule) 
     std::vector<Key> keys;
     for (const auto& kv : st.dense.m) keys.push_back(kv.first);
     return colored_order(ids, keys);
+  }
+  if (schedule == SCHEDULE_INTERIOR_FIRST && T.level_count(l) >= kInteriorParts) {
+    // interior clusters of the level-3 subtrees (all dense neighbours in the
+    // same subtree) first, then the boundary clusters, each ascending
+    int lp = 0;
+    while ((1 << lp) < kInteriorParts) ++lp;
+    const int first = T.level_begin(l), shift = l - lp;
+    std::set<int> boundary;
+    for (const auto& kv : st.dense.m) {
+      const int a = kv.first.first - first, b = kv.first.second - first;
+      if ((a >> shift) != (b >> shift)) boundary.insert(kv.first.first), boundary.insert(kv.first.second);
+    }
+    std::vector<int> order;
+    for (int i : ids)
+      if (!boundary.count(i)) order.push_back(i);
+    for (int i : ids)
+      if (boundary.count(i)) order.push_back(i);
+    return order;
   }
   return ids;
 }

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2
-SCHEDULE_REFERENCE, SCHEDULE_COLORED = 0, 1
+SCHEDULE_REFERENCE, SCHEDULE_COLORED, SCHEDULE_INTERIOR_FIRST = 0, 1, 3
 
 
 class OracleError(RuntimeError):

@@ -23,7 +23,7 @@ from . import geometry  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("H2G_LIB", os.path.join(_HERE, "libh2g.so"))
 
-SCHEDULES = {"reference": 0, "colored": 1, "serial": 2}
+SCHEDULES = {"reference": 0, "colored": 1, "serial": 2, "interior-first": 3}
 KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2
 _SOLVE, _FORWARD, _BACKWARD, _APPLY_INVERSE, _APPLY_INVERSE_EXPLICIT = 0, 1, 2, 3, 4
 

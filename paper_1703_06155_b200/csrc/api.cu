@@ -1096,7 +1096,8 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
   return guarded(err, [&] {
     if (!ctx || !mc || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
     if (!(eps > 0.0)) throw Error(H2G_ERR_INVALID_INPUT, "factorize: eps_fill_in must be positive");
-    if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED && schedule != H2G_SCHEDULE_SERIAL)
+    if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED && schedule != H2G_SCHEDULE_SERIAL &&
+        schedule != H2G_SCHEDULE_INTERIOR_FIRST)
       throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
     if (hooks) schedule = H2G_SCHEDULE_SERIAL;  // debug mode: one cluster per step, reference order
     std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);

@@ -357,6 +357,29 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
     }
   } else if (kind == H2G_SCHEDULE_SERIAL) {
     for (int t = 0; t < nl; ++t) key[static_cast<size_t>(t)] = t;  // one cluster per batch, ascending id
+  } else if (kind == H2G_SCHEDULE_INTERIOR_FIRST && nl >= kInteriorParts) {
+    // the north_star's subtree split (SURVEY §8e option 2): the level-3
+    // subtrees are the parts; clusters whose dense neighbours all lie in
+    // their own part go first (ascending id), the boundary clusters after
+    // them (ascending id); batches are the dependency wavefronts of that order
+    int lp = 0;
+    while ((1 << lp) < kInteriorParts) ++lp;
+    const int shift = L.level - lp;
+    std::vector<int> pos(static_cast<size_t>(nl));
+    std::vector<int> order;
+    std::vector<char> interior(static_cast<size_t>(nl), 1);
+    for (int t = 0; t < nl; ++t)
+      for (int x : nb[static_cast<size_t>(t)])
+        if ((x >> shift) != (t >> shift)) interior[static_cast<size_t>(t)] = 0;
+    for (int pass = 1; pass >= 0; --pass)
+      for (int t = 0; t < nl; ++t)
+        if (interior[static_cast<size_t>(t)] == pass) pos[static_cast<size_t>(t)] = static_cast<int>(order.size()), order.push_back(t);
+    for (int t : order) {
+      int w = 0;
+      for (int x : nb[static_cast<size_t>(t)])
+        if (pos[static_cast<size_t>(x)] < pos[static_cast<size_t>(t)]) w = std::max(w, key[static_cast<size_t>(x)] + 1);
+      key[static_cast<size_t>(t)] = w;
+    }
   } else {
     // dependency wavefronts of the ascending-id order: every lower-id
     // neighbour completes before t starts, no higher-id neighbour does.

@@ -68,6 +68,9 @@ struct LevelSym {
   }
 };
 
+// Parts of the interior-first schedule (the north_star's 8-GPU subtree split).
+constexpr int kInteriorParts = 8;
+
 // Processing order of one level: batches of mutually non-adjacent clusters.
 struct LevelSchedule {
   std::vector<int> batch_ptr, batch_cl;  // local ids, ascending within a batch

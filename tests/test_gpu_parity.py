@@ -88,13 +88,13 @@ def test_helmholtz_rod():
     assert rel(gch.solve(b), A.shadow_solve(b)) < 1e-9
 
 
-@pytest.mark.parametrize("schedule", ["reference", "colored"])
+@pytest.mark.parametrize("schedule", ["reference", "colored", "interior-first"])
 def test_vie_config1_parity(schedule):
     """BASELINE config 1 (16^3 VIE cube, leaf 32, eps 1e-4) against the oracle
     run in the same elimination order."""
     A, K = vie_problem(16, 0.5, 32, 1e-4)
     eps = 1e-4
-    sched = O.SCHEDULE_REFERENCE if schedule == "reference" else O.SCHEDULE_COLORED
+    sched = {"reference": O.SCHEDULE_REFERENCE, "colored": O.SCHEDULE_COLORED, "interior-first": O.SCHEDULE_INTERIOR_FIRST}[schedule]
     och = A.factorize(eps, schedule=sched)
     gch = h2g.factorize(upload(A), eps, schedule=schedule)
     compare_chains(och, gch, rank_tol=1)

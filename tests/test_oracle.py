@@ -89,6 +89,20 @@ def test_stepwise_colored_schedule_is_exact_too():
     assert r["worst"] < 1e-10
 
 
+def test_stepwise_interior_first_schedule_is_exact_too():
+    """The north_star's subtree split as an elimination order (interior
+    clusters of the 8 level-3 subtrees first, then the boundary): still an
+    exact factorization of the represented matrix (stepwise dense oracle)."""
+    from paper_1703_06155_b200.geometry import cube_points
+
+    A = O.H2(O.Blocks(O.Tree(cube_points(512), 8)), O.laplace(2.0), 1e-10)
+    r = A.test_stepwise(1e-12, O.SCHEDULE_INTERIOR_FIRST)
+    assert r["worst"] < 1e-10
+    ch_ref, ch_if = A.factorize(1e-12), A.factorize(1e-12, schedule=O.SCHEDULE_INTERIOR_FIRST)
+    b = O.rhs(512, 4)
+    assert np.linalg.norm(ch_if.solve(b) - ch_ref.solve(b)) / np.linalg.norm(ch_ref.solve(b)) < 1e-8
+
+
 def test_replay_reproduces_matrix():  # :97-104
     A = rod_h2(128, 1e-8, 1.0, 16)
     for eps in (1e-6, 1e-10):
