@@ -28,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/h2g.h"
 #include "build.cuh"
 #include "factor.cuh"
@@ -49,6 +51,13 @@ struct Error : std::runtime_error {
 };
 
 thread_local h2g_error g_last{};
+
+// NVTX range (header-only NVTX v3): factorize / level / merge / solve phases
+// show up by name in Nsight timelines.
+struct NvtxRange {
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 void set_error(h2g_error* out, int code, const char* msg, int cluster = -1, int level = -1, long long piv = -1, double mag = 0.0) {
   h2g_error e{};
@@ -451,6 +460,9 @@ struct ChainLevelHost {
   const SolveContribD* d_fc = nullptr;
   DBuf sched_buf;     // batch_ptr | batch_maxc | fs_ptr on the device
   SolveSched sched{};
+  DBuf flow_meta;     // dataflow solve schedule (k_fwd_flow / k_bwd_flow)
+  SolveFlow flow{};
+  size_t flow_part = 0;  // backward partials per rhs column (complex elements)
   size_t part_need = 0;  // backward partials per rhs column (complex elements)
   DBuf d_src;
   // host copies of sizes/offsets for downloads
@@ -469,7 +481,7 @@ struct h2g_chain {
   std::vector<std::unique_ptr<ChainLevelHost>> levels;
   int64_t root_size = 0;
   DBuf root;  // LU packed (n_root^2)
-  DBuf ybuf, tmpbuf, partbuf;
+  DBuf ybuf, tmpbuf, partbuf, flowcnt;
   size_t storage_bytes = 0;
   std::vector<int64_t> tree_perm;  // tree index -> original index of the factorized matrix (empty: identity)
   double factor_ms = 0.0, solve_ms = 0.0;
@@ -681,6 +693,71 @@ long long pack_offsets(const std::vector<int>& rows, const std::vector<int>& col
 }
 
 }  // namespace
+
+// Dataflow schedule of one level's substitutions (solve.cuh SolveFlow) from
+// the batch schedule: items in the elimination order, writer indices per
+// segment, gather slots per record. fs / fc: the per-batch forward targets.
+void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, const std::vector<int>& batch_cl, const std::vector<int>& fs_ptr,
+                const std::vector<SolveTargetD>& fs, const std::vector<SolveContribD>& fc, cudaStream_t st) {
+  const int nbat = (int)batch_ptr.size() - 1;
+  std::vector<int> bat(nl, 0);
+  for (int b = 0; b < nbat; ++b)
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) bat[batch_cl[q]] = b;
+  // forward
+  std::vector<int> f_items, rec_widx(nl, 0), fs_widx(fs.size(), 0), wcount(nl, 0);
+  for (int b = 0; b < nbat; ++b) {
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) {
+      const int t = batch_cl[q];
+      rec_widx[t] = wcount[t]++;
+      f_items.push_back(t);
+    }
+    for (int f = fs_ptr[b]; f < fs_ptr[b + 1]; ++f) {
+      const int sg = fs[f].seg >= 0 ? fs[f].seg : -1 - fs[f].seg;
+      fs_widx[f] = wcount[sg]++;
+      f_items.push_back(-1 - f);
+    }
+  }
+  // backward: per record its C entries then the self block
+  std::vector<int> b_items, slot_m, slot_c, rec_slot0(nl, 0), rec_nslot(nl, 0), reader_need(nl, 0);
+  std::vector<unsigned char> slot_final;
+  std::vector<long long> slot_off;
+  std::vector<int> slot_of_rec(nl, 0);
+  long long poff = 0;
+  for (int t = 0; t < nl; ++t) {
+    const int e = CL.bsz[t] - CL.kfin[t];
+    rec_slot0[t] = (int)slot_m.size();
+    if (e > 0) {
+      for (int a = CL.C_ptr[t]; a < CL.C_ptr[t + 1]; ++a) {
+        const int c = CL.C_nb[a];
+        slot_m.push_back(t), slot_c.push_back(a);
+        const bool fin = bat[c] > bat[t];
+        slot_final.push_back(fin ? 1 : 0);
+        if (!fin) ++reader_need[c];
+        slot_off.push_back(poff), poff += e;
+      }
+      if (CL.kfin[t] > 0) slot_m.push_back(t), slot_c.push_back(-1), slot_final.push_back(0), slot_off.push_back(poff), poff += e;
+    }
+    rec_nslot[t] = (int)slot_m.size() - rec_slot0[t];
+  }
+  for (int b = nbat - 1; b >= 0; --b) {
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) {
+      const int t = batch_cl[q];
+      for (int u = 0; u < rec_nslot[t]; ++u) b_items.push_back(-1 - (rec_slot0[t] + u));
+    }
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) b_items.push_back(batch_cl[q]);
+  }
+  if (slot_off.empty()) slot_off.push_back(0);
+  Packer pk;
+  const size_t o_fi = pk.add(f_items), o_rw = pk.add(rec_widx), o_fw = pk.add(fs_widx), o_bi = pk.add(b_items), o_sm = pk.add(slot_m),
+               o_sc = pk.add(slot_c), o_sf = pk.add(slot_final), o_so = pk.add(slot_off), o_r0 = pk.add(rec_slot0), o_rn = pk.add(rec_nslot),
+               o_rd = pk.add(reader_need);
+  pk.upload(CL.flow_meta, st);
+  const DBuf& m = CL.flow_meta;
+  CL.flow = SolveFlow{(int)f_items.size(), at<int>(m, o_fi), at<int>(m, o_rw), at<int>(m, o_fw), (int)b_items.size(), at<int>(m, o_bi),
+                      at<int>(m, o_sm), at<int>(m, o_sc), at<unsigned char>(m, o_sf), at<long long>(m, o_so), at<int>(m, o_r0), at<int>(m, o_rn),
+                      at<int>(m, o_rd)};
+  CL.flow_part = (size_t)std::max<long long>(poff, 1);
+}
 
 // ============================================== FactorizeHooks debug state
 // What a hook sees (FactorState, factorization.hpp:115-251): the current
@@ -1102,6 +1179,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
     if (hooks) schedule = H2G_SCHEDULE_SERIAL;  // debug mode: one cluster per step, reference order
     std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);
     CK(cudaSetDevice(ctx->device));
+    NvtxRange nv_factor("h2g factorize");
     h2g_matrix* M = const_cast<h2g_matrix*>(mc);
     const Structure& S = M->S;
     const int L = S.depth, l0 = S.l0;
@@ -1241,6 +1319,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
     std::vector<HBuf> core_hchunks;  // ... or in pinned host memory when HBM is short
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
+        NvtxRange nv_level("h2g level " + std::to_string(l));
         const LevelSym& Y = P->levels[li];
         const LevelSchedule& SC = P->sched[li];
         const LevelWork& W = P->work[li];
@@ -1977,6 +2056,17 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           for (int bi = 0; bi + 1 < nb1; ++bi)
             CL->part_need = std::max(CL->part_need, (size_t)(CL->batch_ptr[bi + 1] - CL->batch_ptr[bi]) * (CL->batch_maxc[bi] + 1) * bm);
         }
+        CL->C_ptr = Y.C_ptr;
+        CL->C_nb = Y.C_nb;
+        CL->bsz = cur.bsz;
+        CL->kfin = kfin;
+        {
+          std::vector<SolveTargetD> fsd(W.fsolve.size());
+          std::vector<SolveContribD> fcd(W.fcontrib.size());
+          for (size_t i = 0; i < fsd.size(); ++i) fsd[i] = {W.fsolve[i].seg, W.fsolve[i].c0, W.fsolve[i].c1};
+          for (size_t i = 0; i < fcd.size(); ++i) fcd[i] = {W.fcontrib[i].m, W.fcontrib[i].entry};
+          build_flow(*CL, nl, SC.batch_ptr, SC.batch_cl, W.fsolve_ptr, fsd, fcd, st);
+        }
         SolveLevel& SL = CL->sl;
         SL.nl = nl;
         SL.bmax = bm;
@@ -2415,6 +2505,7 @@ int h2g_chain_destroy(h2g_chain* c) {
 
 // ------------------------------------------------------------------ solve
 static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mode) {
+  NvtxRange nv_solve("h2g solve");
   h2g_context* ctx = C->ctx;
   cudaStream_t st = ctx->stream;
   if (n != C->n) throw Error(H2G_ERR_INVALID_INPUT, fmt("solve: right-hand side has length %lld, factorization expects %lld", n, C->n));
@@ -2441,12 +2532,26 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   int bmax_all = 1;
   for (auto& CLp : C->levels) bmax_all = std::max(bmax_all, CLp->sl.bmax);
   const int rchunk = std::max(1, std::min(nrhs, (int)((96 * 1024) / (2 * 16 * (size_t)bmax_all))));
+  // dataflow level kernels (per-item dependency counters) by default; the
+  // batch-synchronous cooperative kernels with H2G_SOLVE_BATCHED=1
+  static const bool batched = std::getenv("H2G_SOLVE_BATCHED") && std::atoi(std::getenv("H2G_SOLVE_BATCHED"));
+  {
+    int nlmax = 1;
+    for (auto& CLp : C->levels) nlmax = std::max(nlmax, CLp->sl.nl);
+    const size_t cb = (size_t)(3 * nlmax + 2) * sizeof(int);  // [0] stall flag, [1..] counters
+    if (cb > C->flowcnt.bytes) C->flowcnt.alloc(cb, st);
+    CK(cudaMemsetAsync(C->flowcnt.p, 0, sizeof(int), st));
+  }
   CK(cudaEventRecord(ctx->ev0, st));
   if (fwd) {
     for (auto& CLp : C->levels) {
       ChainLevelHost& CL = *CLp;
       for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
-        launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
+        if (batched)
+          launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
+        else
+          launch_fwd_flow(CL.sl, CL.sched, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->flowcnt.as<int>() + 1,
+                          C->flowcnt.as<int>(), st);
         ++launches;
       }
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 0, st);
@@ -2466,10 +2571,14 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
       ChainLevelHost& CL = **it;
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 1, st);
       launches += 2;
-      const size_t need = CL.part_need * rchunk * 16;
+      const size_t need = (batched ? CL.part_need : CL.flow_part) * rchunk * 16;
       if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
       for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
-        launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
+        if (batched)
+          launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
+        else
+          launch_bwd_flow(CL.sl, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1,
+                          C->flowcnt.as<int>(), st);
         ++launches;
       }
     }
@@ -2477,6 +2586,11 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev1, st));
   CK(cudaEventSynchronize(ctx->ev1));
+  if (!batched) {
+    int stalled = 0;
+    CK(cudaMemcpy(&stalled, C->flowcnt.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (stalled) throw Error(H2G_ERR_INTERNAL, "solve: a dataflow dependency wait stalled (schedule inconsistent with the chain)");
+  }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   C->solve_ms = ms;
@@ -3182,6 +3296,7 @@ int h2g_chain_load(h2g_context* ctx, const char* path, h2g_chain** out, h2g_erro
           for (int bi = 0; bi + 1 < nb1; ++bi)
             CL->part_need = std::max(CL->part_need, (size_t)(batch_ptr[bi + 1] - batch_ptr[bi]) * (batch_maxc[bi] + 1) * bm);
         }
+        build_flow(*CL, nl, batch_ptr, batch_cl, fs_ptr, fs, fc, st);
         // host inspection copies
         CL->Qt_off = Qt, CL->L11_off = L11, CL->U11_off = U11, CL->Lbar_off = Lb, CL->Ubar_off = Ub, CL->Lself_off = Ls, CL->Uself_off = Us;
         for (size_t ri = 0; ri < LF.recs.size(); ++ri) {

@@ -225,8 +225,7 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
 // Backward gather (solve.hpp:77): partial[q][c] = Ubar(m, c) y[pos_c ...]
 // for one neighbour c of record m = batch[q] (the last slot is the self
 // block), spread over CTAs so the chain blocks stream at full bandwidth.
-__device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int nslot, const cplx* y, long long ldy, int nrhs, cplx* part,
-                                long long pstride, cplx* red) {
+__device__ void bwd_gather_to(const SolveLevel& S, int t, int c, const cplx* y, long long ldy, int nrhs, cplx* out, cplx* red) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const int nC = S.C_ptr[t + 1] - S.C_ptr[t];
   if (e == 0 || c > nC || (c == nC && kf == 0)) return;
@@ -243,14 +242,18 @@ __device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int ns
     M = S.chain + S.Uself_off[t];
     x = y + S.pos[t] + e;
   }
-  cplx* out = part + ((size_t)q * nslot + c) * pstride;
   cta_gemv_n(e, cols, nrhs, M, e, false, x, ldy, out, e, false, red);
+}
+
+__device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int nslot, const cplx* y, long long ldy, int nrhs, cplx* part,
+                                long long pstride, cplx* red) {
+  bwd_gather_to(S, t, c, y, ldy, nrhs, part + ((size_t)q * nslot + c) * pstride, red);
 }
 
 // Backward record (solve.hpp:73-81): head -= sum of the gathered partials (in
 // neighbour order); U11 solve; seg <- conj(Qt) seg. One CTA per record.
-__device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part, long long pstride,
-                         int nslot, unsigned char* smraw) {
+__device__ void bwd_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part0, long long slot_stride,
+                         unsigned char* smraw) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);
@@ -267,7 +270,7 @@ __device__ void bwd_body(const SolveLevel& S, int t, int q, cplx* y, long long l
     for (int idx = warp; idx < e * nrhs; idx += nw) {
       const int i = idx % e, c = idx / e;
       cplx acc = czero();
-      for (int u = lane; u < nuse; u += 32) acc = cadd(acc, part[((size_t)q * nslot + (u < nC ? u : nC)) * pstride + i + (size_t)c * e]);
+      for (int u = lane; u < nuse; u += 32) acc = cadd(acc, part0[(size_t)u * slot_stride + i + (size_t)c * e]);
       double re = acc.x, im = acc.y;
       for (int o = 16; o > 0; o >>= 1) {
         re += __shfl_xor_sync(0xffffffffu, re, o);
@@ -336,10 +339,141 @@ __global__ void __launch_bounds__(256) k_bwd_level(SolveLevel S, SolveSched P, c
       bwd_gather_body(S, P.batch_cl[p0 + it / nslot], it / nslot, it % nslot, nslot, y, ldy, nrhs, part, pstride, reinterpret_cast<cplx*>(smraw));
     g.sync();
     for (int q = blockIdx.x; q < nb; q += gridDim.x) {
-      bwd_body(S, P.batch_cl[p0 + q], q, y, ldy, nrhs, explicit_inv, part, pstride, nslot, smraw);
+      bwd_body(S, P.batch_cl[p0 + q], y, ldy, nrhs, explicit_inv, part + (size_t)q * nslot * pstride, pstride, smraw);
       __syncthreads();
     }
     g.sync();
+  }
+}
+
+// ------------------------------------------------------------ dataflow
+// The substitutions as a dependency graph instead of batch-wide barriers:
+// work items (records, neighbour targets / gather slots) are handed out in
+// the elimination order by a global ticket, and every item waits only on the
+// items it reads from (per-segment writer counters, record-done flags). An
+// item depends only on items with smaller tickets, which are held by running
+// CTAs, so the wait cannot deadlock; per-segment writers are serialised in a
+// fixed order, so results are deterministic.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+// Spin until *p >= v; a wait longer than ~2 s means a broken schedule: the
+// stall is reported through *fail (and the host raises) instead of hanging.
+__device__ __forceinline__ bool wait_ge(const int* p, int v, int* fail) {
+  if (ld_acquire(p) >= v) return true;
+  const long long t0 = clock64();
+  while (ld_acquire(p) < v) {
+    __nanosleep(64);
+    if (clock64() - t0 > 4000000000LL || *(volatile int*)fail) {
+      atomicExch(fail, 1);
+      return false;
+    }
+  }
+  return true;
+}
+// after a wait by thread 0: every thread acquires too (fresh view of the data)
+__device__ __forceinline__ void acquire_all(const int* p) {
+  __syncthreads();
+  (void)ld_acquire(p);
+}
+// publish: the block's stores are visible before the counter moves
+__device__ __forceinline__ void publish(int* p, int v) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(p, v);
+}
+
+// Forward (solve.hpp:43-59). items: >= 0 record cluster t, < 0 target -1-f.
+// cnt: [0] ticket, [1 + s] writers of segment s done.
+__global__ void __launch_bounds__(256) k_fwd_flow(SolveLevel S, SolveSched P, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv,
+                                                  int* cnt, int* fail) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int s_item, s_ok;
+  int* seg = cnt + 1;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(cnt, 1), s_ok = 1;
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= F.nf) return;
+    const int code = F.f_items[it];
+    if (code >= 0) {
+      const int t = code, w = F.rec_widx[t];
+      if (threadIdx.x == 0) s_ok = wait_ge(seg + t, w, fail);
+      acquire_all(seg + t);
+      if (!s_ok) return;
+      fwd_head_body(S, t, y, ldy, nrhs, explicit_inv, smraw);
+      publish(seg + t, w + 1);
+    } else {
+      const int f = -1 - code;
+      const SolveTargetD tg = P.fs[f];
+      const int sg = tg.seg >= 0 ? tg.seg : -1 - tg.seg;
+      if (threadIdx.x == 0) {
+        for (int ci = tg.c0; ci < tg.c1 && s_ok; ++ci) {
+          const int m = P.fc[ci].m;
+          s_ok = wait_ge(seg + m, F.rec_widx[m] + 1, fail);  // head of record m final
+        }
+        if (s_ok) s_ok = wait_ge(seg + sg, F.fs_widx[f], fail);  // earlier writers of the segment
+      }
+      acquire_all(seg + sg);
+      if (!s_ok) return;
+      fwd_lbar_body(S, tg, P.fc, y, ldy, nrhs, reinterpret_cast<cplx*>(smraw));
+      publish(seg + sg, F.fs_widx[f] + 1);
+    }
+    __syncthreads();
+  }
+}
+
+// Backward (solve.hpp:65-83). items: >= 0 record cluster m, < 0 gather slot
+// -1-s. cnt: [0] ticket, [1 + m] slots of m done, [1 + nl + c] reads of c's
+// retained part done, [1 + 2 nl + c] record c done.
+__global__ void __launch_bounds__(256) k_bwd_flow(SolveLevel S, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
+                                                  int* cnt, int* fail) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int s_item, s_ok;
+  const int nl = S.nl;
+  int* slots_done = cnt + 1;
+  int* reads_done = cnt + 1 + nl;
+  int* rec_done = cnt + 1 + 2 * nl;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(cnt, 1), s_ok = 1;
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= F.nb) return;
+    const int code = F.b_items[it];
+    if (code >= 0) {
+      const int m = code;
+      if (threadIdx.x == 0) {
+        s_ok = wait_ge(slots_done + m, F.rec_nslot[m], fail);
+        if (s_ok) s_ok = wait_ge(reads_done + m, F.reader_need[m], fail);  // nobody still reads the retained part
+      }
+      acquire_all(slots_done + m);
+      if (!s_ok) return;
+      const int e = S.bsz[m] - S.kfin[m];
+      bwd_body(S, m, y, ldy, nrhs, explicit_inv, part + (size_t)F.slot_off[F.rec_slot0[m]] * nrhs, (long long)e * nrhs, smraw);
+      publish(rec_done + m, 1);
+    } else {
+      const int sl = -1 - code;
+      const int m = F.slot_m[sl], a = F.slot_c[sl];
+      const int nC = S.C_ptr[m + 1] - S.C_ptr[m];
+      const int c = a >= 0 ? S.C_nb[a] : -1;
+      if (threadIdx.x == 0 && c >= 0 && F.slot_final[sl]) s_ok = wait_ge(rec_done + c, 1, fail);
+      acquire_all(rec_done + (c >= 0 ? c : m));
+      if (!s_ok) return;
+      bwd_gather_to(S, m, a >= 0 ? a - S.C_ptr[m] : nC, y, ldy, nrhs, part + (size_t)F.slot_off[sl] * nrhs, reinterpret_cast<cplx*>(smraw));
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(slots_done + m, 1);
+        if (c >= 0 && !F.slot_final[sl]) atomicAdd(reads_done + c, 1);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -482,6 +616,48 @@ void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, in
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s) {
   const int grid = (int)std::min<long long>(4096, (total + 255) / 256);
   if (total > 0) k_finite<<<grid, 256, 0, s>>>(y, total, bad);
+}
+
+
+static int flow_grid(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(cur_device(), fn, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem);
+  if (per < 1) throw std::runtime_error("solve flow kernel does not fit on an SM");
+  const int g = std::max(1, std::min(per, 2)) * nsm;
+  cache[key] = g;
+  return g;
+}
+
+void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
+                     int* fail, cudaStream_t s) {
+  if (F.nf <= 0) return;
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
+  smem_attr((const void*)k_fwd_flow, smem);
+  cudaMemsetAsync(cnt, 0, (size_t)(S.nl + 1) * sizeof(int), s);
+  const int grid = std::min(flow_grid((const void*)k_fwd_flow, smem), F.nf);
+  k_fwd_flow<<<grid, 256, smem, s>>>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_fwd_flow failed: ") + cudaGetErrorString(e));
+}
+
+void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
+                     cudaStream_t s) {
+  if (F.nb <= 0) return;
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
+  smem_attr((const void*)k_bwd_flow, smem);
+  cudaMemsetAsync(cnt, 0, (size_t)(3 * S.nl + 1) * sizeof(int), s);
+  const int grid = std::min(flow_grid((const void*)k_bwd_flow, smem), F.nb);
+  k_bwd_flow<<<grid, 256, smem, s>>>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_bwd_flow failed: ") + cudaGetErrorString(e));
 }
 
 }  // namespace h2g

@@ -44,10 +44,36 @@ struct SolveSched {
   const SolveContribD* fc;
 };
 
+// Dataflow schedule of one level's substitutions (k_fwd_flow / k_bwd_flow).
+struct SolveFlow {
+  // forward: items in elimination order (>= 0 record, < 0 target -1-f),
+  // writer index of every record / target on its segment
+  int nf;
+  const int* f_items;
+  const int* rec_widx;
+  const int* fs_widx;
+  // backward: items (>= 0 record, < 0 gather slot -1-s)
+  int nb;
+  const int* b_items;
+  const int* slot_m;             // record of the slot
+  const int* slot_c;             // C entry (global index) or -1: self block
+  const unsigned char* slot_final;  // neighbour processed later in the forward order: wait for its backward record
+  const long long* slot_off;     // partial offset (complex per rhs)
+  const int* rec_slot0;          // first slot of a record
+  const int* rec_nslot;
+  const int* reader_need;        // slots that read the record's retained part before it rotates it
+};
+
 // Whole level, all batches, one cooperative launch per direction; part holds
 // max_b nb * (maxc_b + 1) * bmax * nrhs gathered backward partials.
 void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
 void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s);
+// Dataflow versions (no grid-wide barriers). cnt: >= 3 nl + 1 ints (reset by
+// the launch); *fail is set when a dependency wait stalls (never reset here).
+void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
+                     int* fail, cudaStream_t s);
+void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
+                     cudaStream_t s);
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s);
 void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s);
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s);
