@@ -1904,7 +1904,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         rotbuf.release();
         eigws.release();
         scratch.release();
-        const double sflops_lv0 = sflops, flops_lv0 = flops;
+        const double sflops_lv0 = sflops, flops_lv0 = flops, sexec_lv0 = C->schur_flops_exec;
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
         std::vector<int> rec_order;
@@ -2091,7 +2091,9 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         C->solve_bytes += 4.0 * 16.0 * (double)S.n;
 
         mark("records done");
-        if (verbose) std::fprintf(stderr, "[h2g] level %d: algorithmic GFLOP total %.1f, Schur %.1f\n", l, (flops - flops_lv0) / 1e9, (sflops - sflops_lv0) / 1e9);
+        if (verbose)
+          std::fprintf(stderr, "[h2g] level %d: algorithmic GFLOP total %.1f, Schur %.1f (executed %.1f)\n", l, (flops - flops_lv0) / 1e9,
+                       (sflops - sflops_lv0) / 1e9, (C->schur_flops_exec - sexec_lv0) / 1e9);
         // ---- merge to level lp (finish_level + merge_permute)
         const LevelSym& YP = P->levels[li + 1];
         LevelData nxt;

@@ -56,8 +56,14 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--h2", choices=["gpu", "oracle"], default="gpu")
     ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--cells", type=int, default=None, help="override: cells per side (a scaled analog of the config)")
+    ap.add_argument("--side", type=float, default=None, help="override: cube side in wavelengths")
     args = ap.parse_args()
-    c = BASELINE_CONFIGS[args.config]
+    c = dict(BASELINE_CONFIGS[args.config])
+    if args.cells:
+        c["cells"] = args.cells
+    if args.side:
+        c["side"] = args.side
     eps = args.eps or c["eps"]
     k0, scale, diag = vie_constants(c["cells"], c["side"])
     pts = vie_grid_points(c["cells"], c["side"])
@@ -104,6 +110,8 @@ def main():
     )
     meta = dict(
         config=args.config,
+        cells=c["cells"],
+        side=c["side"],
         n=n,
         leaf=c["leaf"],
         eps=eps,
