@@ -1400,27 +1400,56 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
     else
       tile_acc<TM>(accs, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
   }
+  // Epilogue: target -= acc. The target values of a row group are loaded
+  // together before any store (the stores may alias later loads, so loads
+  // interleaved with stores would serialise into one round trip each).
   if constexpr (TM == 64) {
-    acc64_each(acc, [&](int ii, int jj, cplx v) {
-      const int i = r0 + ii, j = c0 + jj;
-      if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
-        cplx* o = out + i + (size_t)j * ldo;
-        *o = csub(*o, v);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int wr = (warp % 2) * 32, wc = (warp / 2) * 32, g = lane / 4, tq = lane % 4;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int n0 = 0; n0 < 4; n0 += 2) {  // groups of 4 targets: bounded registers
+        cplx old[2][2];
+        bool ok[2][2];
+        const int i = r0 + wr + mi * 8 + g;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ni = n0 + u, j = c0 + wc + ni * 8 + tq * 2 + h;
+            ok[u][h] = i < rows && j < cols && (acc.re[mi][ni][h] != 0.0 || acc.im[mi][ni][h] != 0.0);
+            if (ok[u][h]) old[u][h] = out[i + (size_t)j * ldo];
+          }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (ok[u][h]) {
+              const int ni = n0 + u, j = c0 + wc + ni * 8 + tq * 2 + h;
+              out[i + (size_t)j * ldo] = make_double2(old[u][h].x - acc.re[mi][ni][h], old[u][h].y - acc.im[mi][ni][h]);
+            }
       }
-    });
   } else {
     const int tr = threadIdx.x % 8, tc = threadIdx.x / 8;
+    cplx old[RM][RN];
+    bool ok[RM][RN];
 #pragma unroll
     for (int a = 0; a < RM; ++a)
 #pragma unroll
       for (int b = 0; b < RN; ++b) {
         const int i = r0 + tr + 8 * a, j = c0 + tc * RN + b;
-        const cplx v = accs[a][b];
-        if (i < rows && j < cols && (v.x != 0.0 || v.y != 0.0)) {
-          cplx* o = out + i + (size_t)j * ldo;
-          *o = csub(*o, v);
-        }
+        ok[a][b] = i < rows && j < cols && (accs[a][b].x != 0.0 || accs[a][b].y != 0.0);
+        if (ok[a][b]) old[a][b] = out[i + (size_t)j * ldo];
       }
+#pragma unroll
+    for (int a = 0; a < RM; ++a)
+#pragma unroll
+      for (int b = 0; b < RN; ++b)
+        if (ok[a][b]) {
+          const int i = r0 + tr + 8 * a, j = c0 + tc * RN + b;
+          out[i + (size_t)j * ldo] = csub(old[a][b], accs[a][b]);
+        }
   }
   if ((tg.kind & 1) == 1 && touched && threadIdx.x == 0 && blockIdx.y == 0) L.fexists[tg.idx] = 1;
 }

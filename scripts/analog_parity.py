@@ -7,7 +7,7 @@ usage: python scripts/analog_parity.py GOLDEN_PREFIX"""
 import json
 import sys
 
-sys.path[:0] = [".", "tests"]
+sys.path[:0] = [".", "tests", "oracle"]
 import numpy as np
 
 import paper_1703_06155_b200 as h2g
