@@ -5,7 +5,7 @@ same reference algorithm, proj/include/h2lu/factorization.hpp), comparing the
 per-(level, cluster) rank_after. The result bounds how closely ANY
 implementation can match the reference's ranks at this configuration.
 
-usage: python scripts/oracle_rank_noise.py CONFIG OUT_JSON [H2_FILE]
+usage: python scripts/oracle_rank_noise.py CONFIG OUT_JSON [H2_FILE [EPS]]
 (H2_FILE: an H2LU matrix to factorize, e.g. the GPU-built input; default:
 built by the oracle)"""
 import json
@@ -22,7 +22,9 @@ from helpers import vie_problem  # noqa: E402
 from paper_1703_06155_b200.geometry import BASELINE_CONFIGS  # noqa: E402
 
 cfg, out = int(sys.argv[1]), sys.argv[2]
-c = BASELINE_CONFIGS[cfg]
+c = dict(BASELINE_CONFIGS[cfg])
+if len(sys.argv) > 4:
+    c["eps"] = float(sys.argv[4])
 if len(sys.argv) > 3:
     A = O.load_h2(sys.argv[3])
 else:
