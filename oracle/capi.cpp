@@ -597,6 +597,8 @@ int orc_test_carried_embed(void* h, double* out) {
 extern "C" {
 // self-noise study: 1 = accumulate GEMM inner products last-to-first
 void orc_set_gemm_order(int reverse) { gemm_order_flag() = reverse ? 1 : 0; }
+// self-noise study: 1 = step-0 truncation through the Gram (Eq. 16-18)
+void orc_set_truncation(int mode) { truncation_mode() = mode; }
 int64_t orc_h2_n(void* h) { return static_cast<H2H*>(h)->A.n(); }
 int orc_h2_save(void* h, const char* path) {
   return guarded([&] { ser::save_h2(path, static_cast<H2H*>(h)->A); });

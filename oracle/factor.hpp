@@ -280,6 +280,28 @@ struct FactorState {  // factorization.hpp:115-251
   }
 };
 
+// Self-noise study only: the step-0 truncation through the Gram of the
+// projected fill stack (the paper's Eq. 16-18 formulation, the one the GPU
+// path uses) instead of QR(W^H) + Jacobi SVD (h2_matrix.hpp:279-285); same
+// rule sigma > max(eps sigma_0, floor, 1e-300). 0 = reference form (default).
+inline int& truncation_mode() {
+  static int mode = 0;
+  return mode;
+}
+
+inline Mat truncated_row_basis_gram(const Mat& W, double eps, double floor) {
+  const Index m = W.r;
+  if (m == 0 || W.c == 0) return Mat(m, 0);
+  Mat G = mul(W, W.adjoint());
+  SVDResult svd = jacobi_svd_left(G);  // PSD: singular values = eigenvalues
+  if (svd.sigma.empty() || svd.sigma[0] <= 0.0) return Mat(m, 0);
+  const double s0 = std::sqrt(svd.sigma[0]);
+  const double thr = std::max({eps * s0, floor, 1e-300});
+  Index r = 0;
+  while (r < static_cast<Index>(svd.sigma.size()) && std::sqrt(std::max(svd.sigma[static_cast<size_t>(r)], 0.0)) > thr) ++r;
+  return svd.U.left_cols(r);
+}
+
 // Step 0 (factorization.hpp:260-312).
 inline Index step0_update_basis(FactorState& st, int i) {
   const size_t ui = static_cast<size_t>(i);
@@ -315,7 +337,7 @@ inline Index step0_update_basis(FactorState& st, int i) {
   }
   const double floor = st.eps_fill_in * cmax;
   if (k > 0) W -= mul(V, mul(V.adjoint(), W));
-  Mat add = truncated_row_basis(W, st.eps_fill_in, floor);
+  Mat add = truncation_mode() == 1 ? truncated_row_basis_gram(W, st.eps_fill_in, floor) : truncated_row_basis(W, st.eps_fill_in, floor);
   const Index r = std::min<Index>(add.c, b - k);
   if (r == 0) return 0;
   Mat vnew(b, k + r);

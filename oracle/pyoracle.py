@@ -117,6 +117,7 @@ def lib():
             "orc_h2_save": (C.c_int, [P, C.c_char_p]),
             "orc_h2_n": (C.c_int64, [P]),
             "orc_set_gemm_order": (None, [C.c_int]),
+            "orc_set_truncation": (None, [C.c_int]),
             "orc_h2_load": (P, [C.c_char_p]),
             "orc_chain_save": (C.c_int, [P, C.c_char_p]),
             "orc_chain_load": (P, [C.c_char_p]),
@@ -593,3 +594,9 @@ def load_vector(path):
 def set_gemm_order(reverse):
     """Oracle self-noise switch: GEMM inner products accumulated last-to-first."""
     lib().orc_set_gemm_order(1 if reverse else 0)
+
+
+def set_truncation(mode):
+    """Oracle self-noise switch: 1 = step-0 truncation through the Gram of the
+    projected fill (the paper's Eq. 16-18, as the GPU does), 0 = QR + SVD."""
+    lib().orc_set_truncation(int(mode))

@@ -30,14 +30,19 @@ if len(sys.argv) > 3:
 else:
     A, K = vie_problem(c["cells"], c["side"], c["leaf"], c["eps"])
 runs = {}
-for name, rev in (("forward", False), ("reverse", True)):
+variants = [("forward", False, 0), ("reverse", True, 0)]
+if os.environ.get("NOISE_GRAM"):
+    variants.append(("gram", False, 1))  # the step-0 truncation through the Gram (paper Eq. 16-18)
+for name, rev, mode in variants:
     O.set_gemm_order(rev)
+    O.set_truncation(mode)
     t0 = time.time()
     ch = A.factorize(c["eps"])
     runs[name] = ({(r["level"], r["cluster"]): r["rank_after"] for r in ch.all_records()}, [l["rank_sum_after"] for l in ch.levels()],
                   ch.root_size, time.time() - t0)
     print(name, runs[name][1], runs[name][2], "%.0f s" % runs[name][3], flush=True)
 O.set_gemm_order(False)
+O.set_truncation(0)
 rf, rr = runs["forward"][0], runs["reverse"][0]
 d = {k: rr[k] - rf[k] for k in rf}
 per_level = {}
@@ -51,6 +56,15 @@ res = dict(config=cfg, eps=c["eps"], mean_abs_per_level=mean_abs, perturbation="
            max_abs_rank_diff=int(max(abs(v) for v in d.values())), nonzero=int(sum(1 for v in d.values() if v)), clusters=len(d),
            per_level=per_level, rank_sum_after_forward=runs["forward"][1], rank_sum_after_reverse=runs["reverse"][1],
            root_forward=runs["forward"][2], root_reverse=runs["reverse"][2])
+if "gram" in runs:
+    rgm = runs["gram"][0]
+    dg = {k: rgm[k] - rf[k] for k in rf}
+    res["gram_variant"] = dict(perturbation="step-0 truncation through the Gram of the projected fill (paper Eq. 16-18) instead of QR + SVD",
+                               max_abs_rank_diff=int(max(abs(v) for v in dg.values())),
+                               per_level={str(lv): dict(max_abs=int(max(abs(v) for k, v in dg.items() if k[0] == lv)),
+                                                       mean_abs=float(np.mean([abs(v) for k, v in dg.items() if k[0] == lv])))
+                                          for lv in sorted({k[0] for k in rf}, reverse=True)},
+                               rank_sum_after=runs["gram"][1], root=runs["gram"][2])
 json.dump(res, open(out, "w"), indent=1)
 keys = sorted(rf)
 np.savez_compressed(os.path.splitext(out)[0] + ".npz", level_cluster=np.array(keys, np.int64), forward=np.array([rf[k] for k in keys], np.int64),
