@@ -50,12 +50,22 @@ typedef struct h2g_error {
  * ascending-heap-id order (factorization.hpp:618) exactly, executed as
  * dependency wavefronts; COLORED runs a greedy distance-1 colouring, one
  * colour per batch (a different, equally valid elimination order). */
-enum h2g_schedule { H2G_SCHEDULE_REFERENCE = 0, H2G_SCHEDULE_COLORED = 1, H2G_SCHEDULE_SERIAL = 2, H2G_SCHEDULE_INTERIOR_FIRST = 3 };
+enum h2g_schedule {
+  H2G_SCHEDULE_REFERENCE = 0,
+  H2G_SCHEDULE_COLORED = 1,
+  H2G_SCHEDULE_SERIAL = 2,
+  H2G_SCHEDULE_INTERIOR_FIRST = 3,
+  H2G_SCHEDULE_SUBTREE = 4
+};
 /* SERIAL: the reference order one cluster per batch (the hooks' debug mode).
  * INTERIOR_FIRST: the north_star's 8-way subtree split as an order (SURVEY
  * §8e option 2): per level with >= 8 clusters, the clusters whose dense
  * neighbours all lie in their own level-3 subtree first, then the boundary
- * clusters (each group ascending id); coarser levels in reference order. */
+ * clusters (each group ascending id); coarser levels in reference order.
+ * SUBTREE: the same split with the interior clusters grouped subtree by
+ * subtree (subtree 0's interior wavefronts, then subtree 1's, ..., then the
+ * boundary clusters): every interior batch belongs to one subtree, which is
+ * what the multi-GPU partition (h2g_factorize_dist) hands to the ranks. */
 
 /* Solve modes: solve.hpp:105 solve, :43 forward, :65 backward, :113
  * apply_inverse (alias of solve), plus the explicit-inverse application
@@ -190,6 +200,49 @@ int h2g_kernel_rows_matvec(h2g_context* ctx, const double* points_tree, int64_t 
 int h2g_factorize(h2g_context* ctx, const h2g_matrix* m, double eps_fill_in, int32_t stop_level, int32_t schedule,
                   h2g_chain** out, h2g_error* err);
 int h2g_chain_destroy(h2g_chain* c);
+
+/* ---- multi-GPU subtree partition (north_star, SURVEY §8e option 2) --------
+ * One process per GPU, every rank holding the same matrix. Per level with
+ * >= 8 clusters the 8 level-3 subtrees are dealt to the ranks (subtree s to
+ * rank s * nranks / 8, nranks in {1, 2, 4, 8}); under the SUBTREE order the
+ * eliminations of a subtree's interior clusters (all dense neighbours inside
+ * the subtree) touch only blocks of that subtree, so every rank runs the
+ * interior batches of its own subtrees and skips the others'. At the level's
+ * interior / boundary border the ranks exchange what their interior phase
+ * produced - final ranks, factor records, the updated dense blocks and the
+ * fill-in blocks of their subtrees - through `exchange`, an all-gather with
+ * per-rank sizes over NCCL (NVLink); the boundary clusters, the merge and the
+ * coarse levels (< 8 clusters) then run replicated on every rank, so each
+ * rank ends with the complete chain. The result is bitwise the single-GPU
+ * factorization in the SUBTREE order.
+ * exchange(user, buf, offsets, nranks): buf is a DEVICE buffer of
+ * offsets[nranks] bytes; on entry this rank's part [offsets[rank],
+ * offsets[rank + 1]) is filled, on return every part must hold the owning
+ * rank's bytes on every rank (ncclBroadcast per part inside one group, or
+ * torch.distributed.broadcast; all work complete on return). Nonzero return
+ * = failure. */
+typedef int (*h2g_exchange_fn)(void* user, void* device_buf, const int64_t* offsets, int32_t nranks);
+typedef struct h2g_dist {
+  int32_t rank, nranks;
+  h2g_exchange_fn exchange;
+  void* user;
+} h2g_dist;
+int h2g_factorize_dist(h2g_context* ctx, const h2g_matrix* m, double eps_fill_in, int32_t stop_level, const h2g_dist* dist, h2g_chain** out,
+                       h2g_error* err);
+/* Host-only view of the partition of one factorized level (no device needed):
+ * counts[4] = clusters, batches, dense blocks, fill blocks of the level;
+ * batch_of[nl] = batch of every cluster under the SUBTREE order;
+ * part_batch[9]: batches [part_batch[s], part_batch[s+1]) are subtree s's
+ * interior, batches from part_batch[8] on the boundary; dense_part[ndense] /
+ * fill_part[nfill] = the subtree whose interior phase writes the block, -1 =
+ * none (only the boundary phase does), -2 = two subtrees (never happens; the
+ * CPU tests assert it); dense_rc[2 ndense] / fill_rc[2 nfill] = (row, column)
+ * cluster (level-local ids) of every block. Output arrays may be null. */
+int h2g_partition_plan(const h2g_matrix_desc* d, int32_t stop_level, int32_t level, int64_t* counts, int32_t* batch_of, int32_t* part_batch,
+                       int32_t* dense_part, int32_t* fill_part, int32_t* dense_rc, int32_t* fill_rc, h2g_error* err);
+/* Bytes this rank sent / all ranks exchanged and the seconds spent inside
+ * `exchange` during the factorization that produced c (0 for h2g_factorize). */
+int h2g_chain_dist_stats(const h2g_chain* c, double* out3);
 
 /* solve / forward_substitute / backward_substitute / apply_inverse
  * (solve.hpp:43-113) with host buffers: b, x are n x nrhs column-major

@@ -23,7 +23,7 @@ from . import geometry  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("H2G_LIB", os.path.join(_HERE, "libh2g.so"))
 
-SCHEDULES = {"reference": 0, "colored": 1, "serial": 2, "interior-first": 3}
+SCHEDULES = {"reference": 0, "colored": 1, "serial": 2, "interior-first": 3, "subtree": 4}
 KERNEL_LAPLACE, KERNEL_HELMHOLTZ, KERNEL_ZERO = 0, 1, 2
 _SOLVE, _FORWARD, _BACKWARD, _APPLY_INVERSE, _APPLY_INVERSE_EXPLICIT = 0, 1, 2, 3, 4
 
@@ -174,6 +174,9 @@ SYMBOLS = {
     "h2g_vector_load": (C.c_int, [C.c_char_p, _D, _I64, C.POINTER(_Err)]),
     "h2g_context_clear_plans": (C.c_int, [_P]),
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
+    "h2g_factorize_dist": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_void_p, C.POINTER(_P), C.POINTER(_Err)]),
+    "h2g_chain_dist_stats": (C.c_int, [_P, _D]),
+    "h2g_partition_plan": (C.c_int, [C.POINTER(_Desc), C.c_int32, C.c_int32, _I64, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_Err)]),
 }
 
 _lib = None
@@ -216,6 +219,57 @@ def _i64(a):
 
 def _i32(a):
     return a.ctypes.data_as(_I32)
+
+
+def _desc_from_arrays(arrays, keep):
+    """h2g_matrix_desc over host arrays; the converted arrays are appended to
+    `keep`, which must outlive the C call."""
+    # every array converted to the dtype the C ABI reads; the converted
+    # arrays stay referenced by `a` until h2g_matrix_upload returns
+    i64 = ("cluster_begin", "cluster_end", "adm_offsets", "split_offsets", "basis_rows", "basis_rank", "basis_offset",
+           "coupling_offset", "dense_offset")
+    i32 = ("adm_pairs", "split_pairs", "leaf_pairs")
+    cpx = ("basis_data", "coupling_data", "dense_data")
+    a = {}
+    keep.append(a)
+    for k in i64:
+        a[k] = np.ascontiguousarray(arrays[k], dtype=np.int64)
+    for k in i32:
+        a[k] = np.ascontiguousarray(np.asarray(arrays[k]).reshape(-1, 2), dtype=np.int32)
+    for k in cpx:
+        a[k] = np.ascontiguousarray(arrays[k], dtype=np.complex128)
+    d = _Desc()
+
+    def scalar(v):
+        return np.asarray(v).reshape(-1)[0]
+
+    d.n = int(scalar(arrays["n"]))
+    d.depth = int(scalar(arrays["depth"]))
+    d.eta = float(scalar(arrays.get("eta", 1.0)))
+    d.eps_h2 = float(scalar(arrays.get("eps_h2", 0.0)))
+    d.cluster_begin = _i64(a["cluster_begin"])
+    d.cluster_end = _i64(a["cluster_end"])
+    d.adm_offsets = _i64(a["adm_offsets"])
+    d.adm_pairs = _i32(a["adm_pairs"])
+    d.split_offsets = _i64(a["split_offsets"])
+    d.split_pairs = _i32(a["split_pairs"])
+    d.num_leaf_pairs = int(a["leaf_pairs"].shape[0])
+    d.leaf_pairs = _i32(a["leaf_pairs"])
+    d.basis_rows = _i64(a["basis_rows"])
+    d.basis_rank = _i64(a["basis_rank"])
+    d.basis_offset = _i64(a["basis_offset"])
+    d.basis_data = _d(a["basis_data"].view(np.float64))
+    d.coupling_offset = _i64(a["coupling_offset"])
+    d.coupling_data = _d(a["coupling_data"].view(np.float64))
+    d.dense_offset = _i64(a["dense_offset"])
+    d.dense_data = _d(a["dense_data"].view(np.float64))
+    if arrays.get("points_tree") is not None and arrays.get("perm") is not None:
+        a["points_tree"] = np.ascontiguousarray(arrays["points_tree"], dtype=np.float64).reshape(-1, 3)
+        a["perm"] = np.ascontiguousarray(arrays["perm"], dtype=np.int64)
+        d.points_tree = _d(a["points_tree"])
+        d.perm = _i64(a["perm"])
+        d.leafsize = int(scalar(arrays.get("leafsize", 0)))
+    return d
 
 
 class Context:
@@ -301,50 +355,8 @@ class H2Matrix:
         """From host arrays in the include/h2g.h layout (keys as exported by
         oracle/pyoracle.H2.export() plus the tree/partition arrays)."""
         ctx = ctx or Context.default()
-        # every array converted to the dtype the C ABI reads; the converted
-        # arrays stay referenced by `a` until h2g_matrix_upload returns
-        i64 = ("cluster_begin", "cluster_end", "adm_offsets", "split_offsets", "basis_rows", "basis_rank", "basis_offset",
-               "coupling_offset", "dense_offset")
-        i32 = ("adm_pairs", "split_pairs", "leaf_pairs")
-        cpx = ("basis_data", "coupling_data", "dense_data")
-        a = {}
-        for k in i64:
-            a[k] = np.ascontiguousarray(arrays[k], dtype=np.int64)
-        for k in i32:
-            a[k] = np.ascontiguousarray(np.asarray(arrays[k]).reshape(-1, 2), dtype=np.int32)
-        for k in cpx:
-            a[k] = np.ascontiguousarray(arrays[k], dtype=np.complex128)
-        d = _Desc()
-
-        def scalar(v):
-            return np.asarray(v).reshape(-1)[0]
-
-        d.n = int(scalar(arrays["n"]))
-        d.depth = int(scalar(arrays["depth"]))
-        d.eta = float(scalar(arrays.get("eta", 1.0)))
-        d.eps_h2 = float(scalar(arrays.get("eps_h2", 0.0)))
-        d.cluster_begin = _i64(a["cluster_begin"])
-        d.cluster_end = _i64(a["cluster_end"])
-        d.adm_offsets = _i64(a["adm_offsets"])
-        d.adm_pairs = _i32(a["adm_pairs"])
-        d.split_offsets = _i64(a["split_offsets"])
-        d.split_pairs = _i32(a["split_pairs"])
-        d.num_leaf_pairs = int(a["leaf_pairs"].shape[0])
-        d.leaf_pairs = _i32(a["leaf_pairs"])
-        d.basis_rows = _i64(a["basis_rows"])
-        d.basis_rank = _i64(a["basis_rank"])
-        d.basis_offset = _i64(a["basis_offset"])
-        d.basis_data = _d(a["basis_data"].view(np.float64))
-        d.coupling_offset = _i64(a["coupling_offset"])
-        d.coupling_data = _d(a["coupling_data"].view(np.float64))
-        d.dense_offset = _i64(a["dense_offset"])
-        d.dense_data = _d(a["dense_data"].view(np.float64))
-        if arrays.get("points_tree") is not None and arrays.get("perm") is not None:
-            a["points_tree"] = np.ascontiguousarray(arrays["points_tree"], dtype=np.float64).reshape(-1, 3)
-            a["perm"] = np.ascontiguousarray(arrays["perm"], dtype=np.int64)
-            d.points_tree = _d(a["points_tree"])
-            d.perm = _i64(a["perm"])
-            d.leafsize = int(scalar(arrays.get("leafsize", 0)))
+        a = []
+        d = _desc_from_arrays(arrays, a)
         err = _Err()
         h = _P()
         rc = lib().h2g_matrix_upload(ctx.h, C.byref(d), C.byref(h), C.byref(err))
@@ -561,6 +573,13 @@ class FactorChain:
     def hash(self):
         return int(lib().h2g_chain_hash(self.h))
 
+    def dist_stats(self):
+        """factorize_dist: bytes this rank contributed / bytes exchanged by all
+        ranks / seconds inside the exchange callback."""
+        out = np.zeros(3)
+        lib().h2g_chain_dist_stats(self.h, _d(out))
+        return dict(sent_bytes=out[0], total_bytes=out[1], exchange_s=out[2])
+
     def timing(self):
         f, s = C.c_double(), C.c_double()
         fl, sl = C.c_int64(), C.c_int64()
@@ -751,6 +770,124 @@ def factorize_hooked(A, eps_fill_in, after_basis_update=None, after_projection=N
         raise errors[0]
     _check(rc, err)
     return FactorChain(h, A)
+
+
+# ---- multi-GPU subtree partition (h2g_factorize_dist) ---------------------
+_XCHG_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_int32)
+
+
+class _Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("exchange", _XCHG_CB), ("user", C.c_void_p)]
+
+
+class _RawBuffer:
+    """A (device or host) pointer as an array-interface object torch can wrap
+    without a copy."""
+
+    def __init__(self, ptr, nbytes, device):
+        iface = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False), "version": 2}
+        if device:
+            self.__cuda_array_interface__ = iface
+        else:
+            self.__array_interface__ = iface
+
+
+def torch_exchange(group=None, device_buffers=True, errors=None):
+    """The `exchange` callback of h2g_dist over torch.distributed: part r of the
+    buffer is broadcast from rank r (an all-gather with per-rank sizes). With
+    the NCCL backend the parts move GPU to GPU over NVLink; with gloo (tests)
+    they are staged through host memory. Returns a Python callable
+    (buf_ptr, offsets, nranks) -> 0 / 1."""
+    import torch
+    import torch.distributed as dist
+
+    def run(buf, offsets, nranks):
+        try:
+            offs = [int(offsets[i]) for i in range(nranks + 1)]
+            me = dist.get_rank(group)
+            if dist.get_world_size(group) != nranks:
+                raise InvalidInputError(f"exchange: process group has {dist.get_world_size(group)} ranks, the factorization {nranks}")
+            if device_buffers:
+                t = torch.as_tensor(_RawBuffer(buf, offs[-1], True), device="cuda")
+            else:
+                t = torch.from_numpy(np.asarray(_RawBuffer(buf, offs[-1], False)))
+            direct = dist.get_backend(group) == "nccl" or not device_buffers
+            for r in range(nranks):
+                part = t[offs[r]:offs[r + 1]]
+                if part.numel() == 0:
+                    continue
+                src = dist.get_global_rank(group, r) if group is not None else r
+                if direct:
+                    dist.broadcast(part, src=src, group=group)
+                else:
+                    h = part.cpu() if r == me else torch.empty(part.numel(), dtype=torch.uint8)
+                    dist.broadcast(h, src=src, group=group)
+                    if r != me:
+                        part.copy_(h)
+            if device_buffers:
+                torch.cuda.synchronize()
+            return 0
+        except BaseException as e:  # noqa: BLE001 - reported to the C side as a failure, re-raised by factorize_dist
+            if errors is not None:
+                errors.append(e)
+            return 1
+
+    return run
+
+
+def factorize_dist(A, eps_fill_in, stop_level_override=None, group=None, rank=None, nranks=None, exchange=None):
+    """The north_star's multi-GPU factorization (h2g_factorize_dist): every
+    rank holds the same H2Matrix on its own GPU; the level-3 subtrees are dealt
+    to the ranks, each rank eliminates the interior clusters of its subtrees,
+    the ranks exchange the results at every level's interior / boundary border
+    and run the boundary clusters replicated. Every rank returns the complete
+    FactorChain (bitwise the single-GPU factorization with schedule="subtree").
+    Default: rank / nranks / exchange from torch.distributed (`group`)."""
+    errors = []
+    if exchange is None:
+        import torch.distributed as dist
+
+        if rank is None:
+            rank = dist.get_rank(group)
+        if nranks is None:
+            nranks = dist.get_world_size(group)
+        exchange = torch_exchange(group, True, errors) if nranks > 1 else None
+
+    def cb(user, buf, offsets, n):
+        return int(exchange(buf, offsets, n))
+
+    ccb = _XCHG_CB(cb) if exchange is not None else _XCHG_CB()
+    d = _Dist(int(rank), int(nranks), ccb, None)
+    err = _Err()
+    h = _P()
+    stop = -1 if stop_level_override is None else int(stop_level_override)
+    rc = lib().h2g_factorize_dist(A.ctx.h, A.h, float(eps_fill_in), stop, C.byref(d), C.byref(h), C.byref(err))
+    if errors:
+        raise errors[0]
+    _check(rc, err)
+    return FactorChain(h, A)
+
+
+def partition_plan(arrays, level, stop_level_override=None):
+    """Host-only view of one level's subtree partition (h2g_partition_plan):
+    dict(nl, batches, batch_of, part_batch, dense_part, fill_part)."""
+    keep = []
+    d = _desc_from_arrays(arrays, keep)
+    err = _Err()
+    counts = np.zeros(4, np.int64)
+    stop = -1 if stop_level_override is None else int(stop_level_override)
+    _check(lib().h2g_partition_plan(C.byref(d), stop, int(level), _i64(counts), None, None, None, None, None, None, C.byref(err)), err)
+    nl, nbat, nd, nf = (int(v) for v in counts)
+    batch_of = np.zeros(max(nl, 1), np.int32)
+    part_batch = np.zeros(9, np.int32)
+    dense_part = np.zeros(max(nd, 1), np.int32)
+    fill_part = np.zeros(max(nf, 1), np.int32)
+    dense_rc = np.zeros((max(nd, 1), 2), np.int32)
+    fill_rc = np.zeros((max(nf, 1), 2), np.int32)
+    _check(lib().h2g_partition_plan(C.byref(d), stop, int(level), _i64(counts), _i32(batch_of), _i32(part_batch), _i32(dense_part), _i32(fill_part),
+                                    _i32(dense_rc), _i32(fill_rc), C.byref(err)), err)
+    return dict(nl=nl, batches=nbat, batch_of=batch_of[:nl], part_batch=part_batch, dense_part=dense_part[:nd], fill_part=fill_part[:nf],
+                dense_rc=dense_rc[:nd], fill_rc=fill_rc[:nf])
 
 
 def factorize(A, eps_fill_in, stop_level_override=None, schedule="reference"):

@@ -485,6 +485,7 @@ struct h2g_chain {
   size_t storage_bytes = 0;
   std::vector<int64_t> tree_perm;  // tree index -> original index of the factorized matrix (empty: identity)
   double factor_ms = 0.0, solve_ms = 0.0;
+  double dist_sent_bytes = 0.0, dist_total_bytes = 0.0, dist_exchange_s = 0.0;  // h2g_factorize_dist
   double plan_ms = 0.0;     // host symbolic plan (get_plan), outside factor_ms
   bool plan_built = false;  // false: reused from the matrix / context plan cache
   long long factor_launches = 0, solve_launches = 0;
@@ -605,6 +606,9 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule, bool* built) {
     cudaMemGetInfo(&fr, &tot);
     if (fill > 0.15 * (double)tot) segments = 16;
   }
+  // the subtree partition exchanges whole fill blocks at the interior /
+  // boundary border: whole-level storage (one collapse at the level end)
+  if (schedule == H2G_SCHEDULE_SUBTREE) segments = 1;
   P->segments = segments;
   // schedules and work lists are independent per level: one host thread each
   size_t nfact = 0;
@@ -703,9 +707,24 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
   std::vector<int> bat(nl, 0);
   for (int b = 0; b < nbat; ++b)
     for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) bat[batch_cl[q]] = b;
+  // records with large blocks: the rotation is cut into row slabs (32 rows of
+  // Qt^H forward, 64 rows of conj(Qt) backward), each its own work item
+  static const int split_min = std::getenv("H2G_SOLVE_SPLIT") ? std::atoi(std::getenv("H2G_SOLVE_SPLIT")) : 128;
+  const int kSlabBase = 1 << 30;
+  std::vector<int> rec_ns_f(nl, 0), rec_ns_b(nl, 0);
+  if (split_min > 0)
+    for (int t = 0; t < nl; ++t)
+      if (CL.bsz[t] >= split_min) {
+        rec_ns_f[t] = std::min(64, (CL.bsz[t] + 31) / 32);
+        rec_ns_b[t] = std::min(64, (CL.bsz[t] + 63) / 64);
+      }
   // forward
   std::vector<int> f_items, rec_widx(nl, 0), fs_widx(fs.size(), 0), wcount(nl, 0);
   for (int b = 0; b < nbat; ++b) {
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) {
+      const int t = batch_cl[q];
+      for (int sl = 0; sl < rec_ns_f[t]; ++sl) f_items.push_back(kSlabBase + t * 64 + sl);
+    }
     for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) {
       const int t = batch_cl[q];
       rec_widx[t] = wcount[t]++;
@@ -745,17 +764,19 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
       for (int u = 0; u < rec_nslot[t]; ++u) b_items.push_back(-1 - (rec_slot0[t] + u));
     }
     for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) b_items.push_back(batch_cl[q]);
+    for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q)
+      for (int sl = 0; sl < rec_ns_b[batch_cl[q]]; ++sl) b_items.push_back(kSlabBase + batch_cl[q] * 64 + sl);
   }
   if (slot_off.empty()) slot_off.push_back(0);
   Packer pk;
   const size_t o_fi = pk.add(f_items), o_rw = pk.add(rec_widx), o_fw = pk.add(fs_widx), o_bi = pk.add(b_items), o_sm = pk.add(slot_m),
                o_sc = pk.add(slot_c), o_sf = pk.add(slot_final), o_so = pk.add(slot_off), o_r0 = pk.add(rec_slot0), o_rn = pk.add(rec_nslot),
-               o_rd = pk.add(reader_need);
+               o_rd = pk.add(reader_need), o_nf = pk.add(rec_ns_f), o_nb = pk.add(rec_ns_b);
   pk.upload(CL.flow_meta, st);
   const DBuf& m = CL.flow_meta;
   CL.flow = SolveFlow{(int)f_items.size(), at<int>(m, o_fi), at<int>(m, o_rw), at<int>(m, o_fw), (int)b_items.size(), at<int>(m, o_bi),
                       at<int>(m, o_sm), at<int>(m, o_sc), at<unsigned char>(m, o_sf), at<long long>(m, o_so), at<int>(m, o_r0), at<int>(m, o_rn),
-                      at<int>(m, o_rd)};
+                      at<int>(m, o_rd), at<int>(m, o_nf), at<int>(m, o_nb)};
   CL.flow_part = (size_t)std::max<long long>(poff, 1);
 }
 
@@ -1169,14 +1190,21 @@ int h2g_kernel_rows_matvec(h2g_context* ctx, const double* points_tree, int64_t 
 }  // extern "C"
 
 static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, int32_t stop_level, int32_t schedule, const h2g_factorize_hooks* hooks,
-                          h2g_chain** out, h2g_error* err) {
+                          h2g_chain** out, h2g_error* err, const h2g_dist* dist = nullptr) {
   return guarded(err, [&] {
     if (!ctx || !mc || !out) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
     if (!(eps > 0.0)) throw Error(H2G_ERR_INVALID_INPUT, "factorize: eps_fill_in must be positive");
     if (schedule != H2G_SCHEDULE_REFERENCE && schedule != H2G_SCHEDULE_COLORED && schedule != H2G_SCHEDULE_SERIAL &&
-        schedule != H2G_SCHEDULE_INTERIOR_FIRST)
+        schedule != H2G_SCHEDULE_INTERIOR_FIRST && schedule != H2G_SCHEDULE_SUBTREE)
       throw Error(H2G_ERR_INVALID_INPUT, "factorize: unknown schedule");
     if (hooks) schedule = H2G_SCHEDULE_SERIAL;  // debug mode: one cluster per step, reference order
+    if (dist) {
+      if (dist->nranks != 1 && dist->nranks != 2 && dist->nranks != 4 && dist->nranks != 8)
+        throw Error(H2G_ERR_INVALID_INPUT, "factorize_dist: nranks must be 1, 2, 4 or 8 (the 8 level-3 subtrees are dealt to the ranks)");
+      if (dist->rank < 0 || dist->rank >= dist->nranks) throw Error(H2G_ERR_INVALID_INPUT, "factorize_dist: rank outside [0, nranks)");
+      if (dist->nranks > 1 && !dist->exchange) throw Error(H2G_ERR_INVALID_INPUT, "factorize_dist: exchange callback missing");
+      schedule = H2G_SCHEDULE_SUBTREE;
+    }
     std::lock_guard<std::recursive_mutex> run_lock(ctx->run_mu);
     CK(cudaSetDevice(ctx->device));
     NvtxRange nv_factor("h2g factorize");
@@ -1751,6 +1779,116 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           CK(cudaMemcpyAsync(core_tab.p, core_ptr_h.data(), nfill * sizeof(cplx*), cudaMemcpyHostToDevice, st));
           CK(cudaStreamSynchronize(st));  // core_ptr_h is rewritten at the next segment end
         };
+        // ---- multi-GPU subtree partition (h2g_factorize_dist): what the
+        // interior phase of every subtree writes, derived from the work lists
+        // of its batches: final ranks and chain records of its clusters, the
+        // dense blocks it rotates / updates, the fill blocks it deposits into
+        std::vector<PartList> parts;
+        const bool partitioned = dist && dist->nranks > 1;
+        const int bnd0 = partitioned ? SC.part_batch[kInteriorParts] : 0;  // first boundary batch
+        auto part_owner = [&](int sp) { return sp * dist->nranks / kInteriorParts; };
+        auto batch_part = [&](int bi) {
+          int sp = 0;
+          while (sp + 1 < kInteriorParts && bi >= SC.part_batch[sp + 1]) ++sp;
+          return sp;
+        };
+        if (partitioned && bnd0 > 0) {
+          if (FP.K != 1) throw Error(H2G_ERR_INTERNAL, "factorize_dist: segmented fill storage in a partitioned level");
+          parts = build_parts(Y, SC, W);
+          for (const PartList& PL : parts)
+            for (int q : PL.fblk)
+              if (cur.foff[q] < 0) throw Error(H2G_ERR_INTERNAL, "factorize_dist: deposited fill block without storage");
+        }
+        bool exchanged = !(partitioned && bnd0 > 0);
+        auto do_exchange = [&] {
+          NvtxRange nv_x("h2g exchange level " + std::to_string(l));
+          CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));
+          CK(cudaStreamSynchronize(ctx->side));
+          CK(cudaStreamSynchronize(ctx->aux));
+          // layout per rank: its subtrees in order, each [ints | pad to 16 B | complex regions]
+          auto chain_end = [&](int t) { return t + 1 < nl ? Qt_off[t + 1] : top; };
+          std::vector<int64_t> offs(dist->nranks + 1, 0);
+          std::vector<size_t> part_off(kInteriorParts, 0);
+          {
+            size_t o = 0;
+            int r = 0;
+            for (int sp = 0; sp < kInteriorParts; ++sp) {
+              while (r < part_owner(sp)) offs[++r] = static_cast<int64_t>(o);
+              part_off[sp] = o;
+              const PartList& PL = parts[sp];
+              o += (PL.ints() * 4 + 15) / 16 * 16;
+              for (int t : PL.cl) o += (size_t)(chain_end(t) - Qt_off[t]) * 16;
+              for (int q : PL.dblk) o += (size_t)cur.bsz[Y.drow[q]] * cur.bsz[Y.dcol[q]] * 16;
+              for (int q : PL.fblk) o += (size_t)cur.bsz[Y.frow[q]] * cur.bsz[Y.fcol[q]] * 16;
+            }
+            while (r < dist->nranks) offs[++r] = static_cast<int64_t>(o);
+          }
+          const size_t total = static_cast<size_t>(offs[dist->nranks]);
+          if (total == 0) return;
+          ensure(total, nullptr);
+          DBuf xbuf, dmv, didx;
+          xbuf.alloc(total, st);
+          // descriptors: own subtrees pack (pool -> buffer), the others unpack
+          std::vector<MoveDesc> mv_pack, mv_unpack;
+          std::vector<int> idx_all;
+          struct IntJob {
+            int sp, which, i0, n;  // which: 0 kfin, 1 fexists
+            size_t boff;
+          };
+          std::vector<IntJob> jobs;
+          cplx* chainp = CL->arena.as<cplx>();
+          for (int sp = 0; sp < kInteriorParts; ++sp) {
+            const PartList& PL = parts[sp];
+            const bool mine = part_owner(sp) == dist->rank;
+            char* base = static_cast<char*>(xbuf.p) + part_off[sp];
+            jobs.push_back({sp, 0, static_cast<int>(idx_all.size()), static_cast<int>(PL.cl.size()), part_off[sp]});
+            idx_all.insert(idx_all.end(), PL.cl.begin(), PL.cl.end());
+            jobs.push_back({sp, 1, static_cast<int>(idx_all.size()), static_cast<int>(PL.fblk.size()), part_off[sp] + PL.cl.size() * 4});
+            idx_all.insert(idx_all.end(), PL.fblk.begin(), PL.fblk.end());
+            cplx* bc = reinterpret_cast<cplx*>(base + (PL.ints() * 4 + 15) / 16 * 16);
+            auto region = [&](cplx* pool, long long len) {
+              if (len > 0) (mine ? mv_pack : mv_unpack).push_back(mine ? MoveDesc{pool, bc, len} : MoveDesc{bc, pool, len});
+              bc += len;
+            };
+            for (int t : PL.cl) region(chainp + Qt_off[t], chain_end(t) - Qt_off[t]);
+            for (int q : PL.dblk) region(cur.D.as<cplx>() + cur.doff[q], (long long)cur.bsz[Y.drow[q]] * cur.bsz[Y.dcol[q]]);
+            for (int q : PL.fblk) region(cur.F.as<cplx>() + cur.foff[q], (long long)cur.bsz[Y.frow[q]] * cur.bsz[Y.fcol[q]]);
+          }
+          std::vector<MoveDesc> mv_all(mv_pack);
+          mv_all.insert(mv_all.end(), mv_unpack.begin(), mv_unpack.end());
+          upload(dmv, mv_all, st);
+          upload(didx, idx_all, st);
+          auto int_moves = [&](bool own, int scatter) {
+            for (const IntJob& j : jobs) {
+              if ((part_owner(j.sp) == dist->rank) != own) continue;
+              int* basep = j.which == 0 ? DL.kfin : DL.fexists;
+              launch_int_move(basep, didx.as<int>() + j.i0, j.n, reinterpret_cast<int*>(static_cast<char*>(xbuf.p) + j.boff), scatter, st);
+            }
+          };
+          int_moves(true, 0);
+          launch_move(dmv.as<MoveDesc>(), static_cast<int>(mv_pack.size()), st);
+          CK(cudaStreamSynchronize(st));
+          const double tx0 = wall();
+          const int rc = dist->exchange(dist->user, xbuf.p, offs.data(), dist->nranks);
+          if (rc != 0) throw Error(H2G_ERR_INTERNAL, fmt("factorize_dist: the exchange callback failed (code %lld) at level %lld", rc, l));
+          C->dist_exchange_s += wall() - tx0;
+          C->dist_sent_bytes += static_cast<double>(offs[dist->rank + 1] - offs[dist->rank]);
+          C->dist_total_bytes += static_cast<double>(total);
+          int_moves(false, 1);
+          launch_move(dmv.as<MoveDesc>() + mv_pack.size(), static_cast<int>(mv_unpack.size()), st);
+          CK(cudaStreamSynchronize(st));
+          launches += 2 * kInteriorParts + 2;
+          if (verbose)
+            std::fprintf(stderr, "[h2g] level %d: rank %d/%d exchanged %.3f GB (own part %.3f GB), interior batches %d of %d\n", l, dist->rank,
+                         dist->nranks, total / 1e9, (offs[dist->rank + 1] - offs[dist->rank]) / 1e9, bnd0, nbat);
+        };
+        auto maybe_exchange = [&](int next_bi) {
+          if (!exchanged && next_bi >= bnd0) {
+            exchanged = true;
+            do_exchange();
+          }
+        };
+        int prev_exec = -1;
         std::vector<char> rotated(nl, 0);
         std::vector<int> elimv(nl, 0);
         h2g_state hstate;
@@ -1769,6 +1907,17 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           check_device_error(ctx, l);
         };
         for (int bi = 0; bi < nbat; ++bi) {
+          maybe_exchange(bi);
+          if (partitioned && bi < bnd0 && part_owner(batch_part(bi)) != dist->rank) {
+            // another rank's subtree: its results arrive with the exchange
+            if (bi + 1 == nbat) {
+              maybe_exchange(nbat);
+              segment_end(0);
+            }
+            continue;
+          }
+          if (partitioned && prev_exec >= 0 && prev_exec != bi - 1) CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));
+          prev_exec = bi;
           const int p0 = SC.batch_ptr[bi], nb = SC.batch_ptr[bi + 1] - p0;
           const int sgi = fill_segment(bi, nbat, FP.K);
           if (sgi > 0 && bi == FP.seg_first_batch[sgi] && zptr[sgi + 1] > zptr[sgi]) {
@@ -1875,7 +2024,10 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
             elimv[tcl] = cur.bsz[tcl] - kft;
             if (hooks->after_elimination) hooks->after_elimination(hooks->user, &hstate, Y.first + tcl);
           }
-          if (bi + 1 == FP.seg_first_batch[sgi + 1]) segment_end(sgi);
+          if (bi + 1 == FP.seg_first_batch[sgi + 1]) {
+            maybe_exchange(bi + 1);
+            segment_end(sgi);
+          }
         }
         CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));  // deferred Schur updates of the last batch
         const double t_launched = wall();
@@ -2495,6 +2647,60 @@ int h2g_factorize_hooked(h2g_context* ctx, const h2g_matrix* m, double eps, int3
   return factorize_impl(ctx, m, eps, stop_level, H2G_SCHEDULE_SERIAL, hooks, out, err);
 }
 
+int h2g_factorize_dist(h2g_context* ctx, const h2g_matrix* m, double eps, int32_t stop_level, const h2g_dist* dist, h2g_chain** out, h2g_error* err) {
+  if (!dist) {
+    set_error(err, H2G_ERR_INVALID_INPUT, "factorize_dist: null dist");
+    return H2G_ERR_INVALID_INPUT;
+  }
+  return factorize_impl(ctx, m, eps, stop_level, H2G_SCHEDULE_SUBTREE, nullptr, out, err, dist);
+}
+
+int h2g_partition_plan(const h2g_matrix_desc* d, int32_t stop_level, int32_t level, int64_t* counts, int32_t* batch_of, int32_t* part_batch,
+                       int32_t* dense_part, int32_t* fill_part, int32_t* dense_rc, int32_t* fill_rc, h2g_error* err) {
+  return guarded(err, [&] {
+    if (!d || !counts) throw Error(H2G_ERR_INVALID_INPUT, "null argument");
+    const Structure S = structure_from_desc(d);
+    int stop = S.depth + 1;
+    if (S.l0 >= 0) stop = stop_level >= 0 ? stop_level : S.l0;
+    const std::vector<LevelSym> levels = build_levels(S, stop);
+    const LevelSym* Y = nullptr;
+    for (const auto& L : levels)
+      if (L.level == level && L.level >= stop) Y = &L;
+    if (!Y) throw Error(H2G_ERR_INVALID_INPUT, "partition_plan: level is not factorized");
+    const LevelSchedule SC = build_schedule(*Y, H2G_SCHEDULE_SUBTREE);
+    const LevelWork W = build_work(*Y, SC, 1);
+    counts[0] = Y->nl;
+    counts[1] = static_cast<int64_t>(SC.batch_ptr.size()) - 1;
+    counts[2] = static_cast<int64_t>(Y->drow.size());
+    counts[3] = static_cast<int64_t>(Y->frow.size());
+    if (batch_of)
+      for (int t = 0; t < Y->nl; ++t) batch_of[t] = SC.order[t];
+    if (part_batch)
+      for (int q = 0; q <= kInteriorParts; ++q) part_batch[q] = SC.part_batch[q];
+    const std::vector<PartList> parts = build_parts(*Y, SC, W);
+    auto mark = [&](int32_t* out, size_t n, bool fill) {
+      if (!out) return;
+      for (size_t q = 0; q < n; ++q) out[q] = -1;
+      for (int sp = 0; sp < kInteriorParts; ++sp)
+        for (int q : (fill ? parts[sp].fblk : parts[sp].dblk)) out[q] = out[q] == -1 ? sp : -2;  // -2: written by two subtrees (never)
+    };
+    mark(dense_part, Y->drow.size(), false);
+    mark(fill_part, Y->frow.size(), true);
+    if (dense_rc)
+      for (size_t q = 0; q < Y->drow.size(); ++q) dense_rc[2 * q] = Y->drow[q], dense_rc[2 * q + 1] = Y->dcol[q];
+    if (fill_rc)
+      for (size_t q = 0; q < Y->frow.size(); ++q) fill_rc[2 * q] = Y->frow[q], fill_rc[2 * q + 1] = Y->fcol[q];
+  });
+}
+
+int h2g_chain_dist_stats(const h2g_chain* c, double* out3) {
+  if (!c || !out3) return H2G_ERR_INVALID_INPUT;
+  out3[0] = c->dist_sent_bytes;
+  out3[1] = c->dist_total_bytes;
+  out3[2] = c->dist_exchange_s;
+  return H2G_OK;
+}
+
 int h2g_chain_destroy(h2g_chain* c) {
   if (!c) return H2G_OK;
   h2g_context* ctx = c->ctx;
@@ -2540,7 +2746,7 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   {
     int nlmax = 1;
     for (auto& CLp : C->levels) nlmax = std::max(nlmax, CLp->sl.nl);
-    const size_t cb = (size_t)(3 * nlmax + 2) * sizeof(int);  // [0] stall flag, [1..] counters
+    const size_t cb = (size_t)(4 * nlmax + 2) * sizeof(int);  // [0] stall flag, [1..] counters
     if (cb > C->flowcnt.bytes) C->flowcnt.alloc(cb, st);
     CK(cudaMemsetAsync(C->flowcnt.p, 0, sizeof(int), st));
   }
@@ -2553,7 +2759,7 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
           launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
         else
           launch_fwd_flow(CL.sl, CL.sched, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->flowcnt.as<int>() + 1,
-                          C->flowcnt.as<int>(), st);
+                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, st);
         ++launches;
       }
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 0, st);
@@ -2580,7 +2786,7 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
           launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
         else
           launch_bwd_flow(CL.sl, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1,
-                          C->flowcnt.as<int>(), st);
+                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, st);
         ++launches;
       }
     }

@@ -929,6 +929,93 @@ __device__ __forceinline__ void tile_pipe_dmma(Acc64& acc, TileSmem<64>& S, cons
   __syncthreads();
 }
 
+// One Schur contribution as the concatenated pipeline sees it: the tile's
+// rows / columns of op(A) = A (arows x e, ld arows) and op(B) = B (e x bcols,
+// ld e), shifted by ash / bsh; e = 0 marks a contribution that misses the tile.
+struct SchurPanel {
+  const cplx* A;
+  const cplx* B;
+  int arows, bcols, ash, bsh, e, pad;
+};
+
+// acc += sum over panels tab[0..n) of A_p B_p on the tile: ONE cp.async
+// pipeline runs through the k-slices of all panels back to back (no ramp,
+// drain or extra barrier per contribution; the loads of the next panel are in
+// flight while the current one is multiplied). Slices are 8 deep, zero padded;
+// the upper half of a slice is skipped when it holds no data (e <= 4 at the
+// fine levels). kv: 3 ints of shared memory.
+// mlim / nlim: rows / columns of the tile inside the target; a warp skips the
+// 8 x 8 blocks of its 32 x 32 share that lie outside (targets of ~100 rows
+// would otherwise pay for 128).
+__device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64>& S, const SchurPanel* tab, int n, int* kv, int mlim, int nlim) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wr = (warp % 2) * 32, wc = (warp / 2) * 32, g = lane / 4, tq = lane % 4;
+  const int mi_n = min(4, max(0, (mlim - wr + 7) / 8)), ni_n = min(4, max(0, (nlim - wc + 7) / 8));
+  int total = 0;
+  for (int p = 0; p < n; ++p) total += (tab[p].e + 7) / 8;
+  if (total == 0) return;
+  int li = 0, lk = 0, issued = 0;
+  while (li < n && tab[li].e == 0) ++li;
+  auto issue = [&]() {
+    if (li < n) {
+      const SchurPanel P = tab[li];
+      const int st = issued % 3;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = threadIdx.x + u * 128;
+        const int i = idx % 64, p = idx / 64;
+        const int ai = i + P.ash;
+        const bool va = lk + p < P.e && ai >= 0 && ai < P.arows;
+        cp_async16(&S.a[st][p][i], va ? P.A + ai + (size_t)(lk + p) * P.arows : P.A, va);
+        const int q = idx % 8, j = idx / 8;
+        const int bj = j + P.bsh;
+        const bool vb = lk + q < P.e && bj >= 0 && bj < P.bcols;
+        cp_async16(&S.b[st][q][j], vb ? P.B + (lk + q) + (size_t)bj * P.e : P.B, vb);
+      }
+      if (threadIdx.x == 0) kv[st] = P.e - lk;
+      lk += 8;
+      if (lk >= P.e) {
+        lk = 0;
+        ++li;
+        while (li < n && tab[li].e == 0) ++li;
+      }
+      ++issued;
+    }
+    cp_async_commit();
+  };
+  issue();
+  issue();
+  for (int s = 0; s < total; ++s) {
+    asm volatile("cp.async.wait_group 1;");
+    __syncthreads();
+    issue();
+    const int st = s % 3;
+    const int nh = kv[st] > 4 ? 8 : 4;
+    if (mi_n == 0 || ni_n == 0) continue;
+    for (int kk = 0; kk < nh; kk += 4) {
+      cplx af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = S.a[st][kk + tq][wr + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = S.b[st][kk + tq][wc + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        if (mi >= mi_n) break;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          if (ni >= ni_n) break;
+          dmma884(acc.re[mi][ni][0], acc.re[mi][ni][1], af[mi].x, bf[ni].x);
+          dmma884(acc.re[mi][ni][0], acc.re[mi][ni][1], -af[mi].y, bf[ni].y);
+          dmma884(acc.im[mi][ni][0], acc.im[mi][ni][1], af[mi].x, bf[ni].y);
+          dmma884(acc.im[mi][ni][0], acc.im[mi][ni][1], af[mi].y, bf[ni].x);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();
+}
+
 __device__ __forceinline__ void tile_acc_dmma(Acc64& acc, TileSmem<64>& S, const cplx* A, int lda, int opA, int ash, int am, const cplx* B, int ldb,
                                               int opB, int bsh, int bn, int k) {
   if (k <= 0) return;

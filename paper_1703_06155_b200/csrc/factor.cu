@@ -1365,40 +1365,72 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
       for (int b = 0; b < RN; ++b) accs[a][b] = czero();
   }
   bool touched = false;
-  for (int ci = tg.c0; ci < tg.c1; ++ci) {
+  // one contribution resolved against this tile; returns its e (0: the
+  // cluster eliminated nothing), use = false when it misses the tile
+  auto resolve = [&](int ci, SchurPanel& P, bool& use) {
     const SchurContribD cb = contrib[ci];
     const int t = cb.t;
     const int kf = L.kfin[t], e = L.bsz[t] - kf;
-    if (e == 0) continue;
-    touched = true;
-    const cplx* A;
-    const cplx* B;
-    int arows, bcols, ro, co;
+    use = false;
+    if (e == 0) return 0;
+    int ro, co;
     if (cb.r >= 0) {
-      arows = L.bsz[L.R_nb[cb.r]];
-      A = (cb.flags & 1) ? L.lift + L.liftL_off[cb.r] : L.chain + L.Lbar_off[cb.r];
+      P.arows = L.bsz[L.R_nb[cb.r]];
+      P.A = (cb.flags & 1) ? L.lift + L.liftL_off[cb.r] : L.chain + L.Lbar_off[cb.r];
       ro = 0;
     } else {
-      arows = kf;
-      A = L.chain + L.Lself_off[t];
+      P.arows = kf;
+      P.A = L.chain + L.Lself_off[t];
       ro = e;
     }
     if (cb.c >= 0) {
-      bcols = L.bsz[L.C_nb[cb.c]];
-      B = (cb.flags & 2) ? L.lift + L.liftU_off[cb.c] : L.chain + L.Ubar_off[cb.c];
+      P.bcols = L.bsz[L.C_nb[cb.c]];
+      P.B = (cb.flags & 2) ? L.lift + L.liftU_off[cb.c] : L.chain + L.Ubar_off[cb.c];
       co = 0;
     } else {
-      bcols = kf;
-      B = L.chain + L.Uself_off[t];
+      P.bcols = kf;
+      P.B = L.chain + L.Uself_off[t];
       co = e;
     }
     // the contribution covers target rows [ro, ro+arows) x cols [co, co+bcols)
-    const int ash = r0 - ro, bsh = c0 - co;
-    if (ash >= arows || bsh >= bcols || ash + TM <= 0 || bsh + TM <= 0) continue;
-    if constexpr (TM == 64)
-      tile_acc_dmma(acc, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
-    else
-      tile_acc<TM>(accs, S, A, arows, OP_N, ash, arows, B, e, OP_N, bsh, bcols, e);
+    P.ash = r0 - ro;
+    P.bsh = c0 - co;
+    P.e = e;
+    use = !(P.ash >= P.arows || P.bsh >= P.bcols || P.ash + TM <= 0 || P.bsh + TM <= 0);
+    return e;
+  };
+  if constexpr (TM == 64) {
+    // all contributions of the target through one load pipeline (tables of
+    // 16 panels resolved by 16 threads in parallel)
+    __shared__ SchurPanel tab[16];
+    __shared__ int s_kv[3], s_touched;
+    if (threadIdx.x == 0) s_touched = 0;
+    for (int cbase = tg.c0; cbase < tg.c1; cbase += 16) {
+      const int nc = min(16, tg.c1 - cbase);
+      __syncthreads();
+      if ((int)threadIdx.x < nc) {
+        SchurPanel P;
+        bool use;
+        const int e = resolve(cbase + threadIdx.x, P, use);
+        if (e > 0) s_touched = 1;
+        if (!use) P.A = nullptr, P.B = nullptr, P.arows = P.bcols = P.ash = P.bsh = 0, P.e = 0;
+        P.pad = 0;
+        tab[threadIdx.x] = P;
+      }
+      __syncthreads();
+      schur_pipe_dmma(acc, S, tab, nc, s_kv, rows - r0, cols - c0);
+    }
+    __syncthreads();
+    touched = s_touched != 0;
+  } else {
+    for (int ci = tg.c0; ci < tg.c1; ++ci) {
+      SchurPanel P;
+      bool use;
+      if (resolve(ci, P, use) == 0) continue;
+      touched = true;
+      if (!use) continue;
+      tile_acc<TM>(accs, S, P.A, P.arows, OP_N, P.ash, P.arows, P.B, P.e, OP_N, P.bsh, P.bcols, P.e);
+    }
   }
   // Epilogue: target -= acc. The target values of a row group are loaded
   // together before any store (the stores may alias later loads, so loads
@@ -1895,6 +1927,23 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
   set_smem((const void*)k_schur<64>, sizeof(Tile128Smem));
   k_schur<64><<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
   post_launch("k_schur");
+}
+
+__global__ void __launch_bounds__(256) k_move(const MoveDesc* descs) {
+  const MoveDesc d = descs[blockIdx.x];
+  for (long long i = (long long)blockIdx.y * blockDim.x + threadIdx.x; i < d.len; i += (long long)gridDim.y * blockDim.x) d.dst[i] = d.src[i];
+}
+__global__ void k_int_move(int* base, const int* idx, int n, int* packed, int scatter) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (scatter) base[idx[i]] = packed[i];
+  else packed[i] = base[idx[i]];
+}
+void launch_move(const MoveDesc* d, int n, cudaStream_t s) {
+  if (n > 0) k_move<<<dim3(n, 8), 256, 0, s>>>(d); post_launch("k_move");
+}
+void launch_int_move(int* base, const int* idx, int n, int* packed, int scatter, cudaStream_t s) {
+  if (n > 0) k_int_move<<<(n + 255) / 256, 256, 0, s>>>(base, idx, n, packed, scatter); post_launch("k_int_move");
 }
 
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s) {

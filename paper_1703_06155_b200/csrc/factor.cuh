@@ -126,6 +126,17 @@ struct NormDesc {
   double* out;
 };
 
+// Multi-GPU exchange (h2g_factorize_dist): contiguous regions moved between
+// the level pools and the exchange buffer, and indexed ints (kfin, fexists).
+struct MoveDesc {
+  const cplx* src;
+  cplx* dst;
+  long long len;
+};
+void launch_move(const MoveDesc* d, int n, cudaStream_t s);
+// scatter = 0: packed[i] = base[idx[i]]; 1: base[idx[i]] = packed[i]
+void launch_int_move(int* base, const int* idx, int n, int* packed, int scatter, cudaStream_t s);
+
 // Bytes of DevLevel::scratch a level with nl clusters, bmax and the given
 // largest batch needs.
 size_t level_scratch_bytes(int nl, int bmax, int max_batch);

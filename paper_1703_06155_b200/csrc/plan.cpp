@@ -346,6 +346,7 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
     nb[static_cast<size_t>(c)].push_back(r);
   }
   std::vector<int> key(static_cast<size_t>(nl), 0);
+  std::vector<int> part_batch(static_cast<size_t>(kInteriorParts) + 1, 0);
   if (kind == H2G_SCHEDULE_COLORED) {
     std::vector<int> mark(static_cast<size_t>(nl) + 1, -1);
     for (int t = 0; t < nl; ++t) {
@@ -380,6 +381,37 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
         if (pos[static_cast<size_t>(x)] < pos[static_cast<size_t>(t)]) w = std::max(w, key[static_cast<size_t>(x)] + 1);
       key[static_cast<size_t>(t)] = w;
     }
+  } else if (kind == H2G_SCHEDULE_SUBTREE && nl >= kInteriorParts) {
+    // the interior-first split with subtree-pure batches: the interior
+    // clusters of subtree 0 (wavefronts of their ascending-id order), then
+    // subtree 1's, ..., then the boundary clusters (wavefronts again)
+    int lp = 0;
+    while ((1 << lp) < kInteriorParts) ++lp;
+    const int shift = L.level - lp;
+    std::vector<char> interior(static_cast<size_t>(nl), 1);
+    for (int t = 0; t < nl; ++t)
+      for (int x : nb[static_cast<size_t>(t)])
+        if ((x >> shift) != (t >> shift)) interior[static_cast<size_t>(t)] = 0;
+    int base = 0;
+    for (int s = 0; s <= kInteriorParts; ++s) {
+      part_batch[static_cast<size_t>(s)] = base;
+      int top = base;
+      for (int t = 0; t < nl; ++t) {
+        const bool mine = s < kInteriorParts ? (interior[static_cast<size_t>(t)] && (t >> shift) == s) : !interior[static_cast<size_t>(t)];
+        if (!mine) continue;
+        int w = base;
+        // earlier members of the same group with a lower id (interior
+        // clusters of other subtrees are never neighbours; for the boundary
+        // group every interior neighbour lies in an earlier batch already)
+        for (int x : nb[static_cast<size_t>(t)]) {
+          const bool same = s < kInteriorParts ? (interior[static_cast<size_t>(x)] && (x >> shift) == s) : !interior[static_cast<size_t>(x)];
+          if (same && x < t) w = std::max(w, key[static_cast<size_t>(x)] + 1);
+        }
+        key[static_cast<size_t>(t)] = w;
+        top = std::max(top, w + 1);
+      }
+      base = top;
+    }
   } else {
     // dependency wavefronts of the ascending-id order: every lower-id
     // neighbour completes before t starts, no higher-id neighbour does.
@@ -393,6 +425,7 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
   const int nb_batches = nl ? *std::max_element(key.begin(), key.end()) + 1 : 0;
   LevelSchedule S;
   S.order = key;
+  S.part_batch = part_batch;
   std::vector<std::vector<int>> bat(static_cast<size_t>(nb_batches));
   for (int t = 0; t < nl; ++t) bat[static_cast<size_t>(key[static_cast<size_t>(t)])].push_back(t);
   S.batch_ptr.assign(1, 0);
@@ -401,6 +434,33 @@ LevelSchedule build_schedule(const LevelSym& L, int kind) {
     S.batch_ptr.push_back(static_cast<int>(S.batch_cl.size()));
   }
   return S;
+}
+
+std::vector<PartList> build_parts(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W) {
+  std::vector<PartList> parts(static_cast<size_t>(kInteriorParts));
+  if (sch.part_batch.size() != static_cast<size_t>(kInteriorParts) + 1) return parts;
+  for (int sp = 0; sp < kInteriorParts; ++sp) {
+    PartList& PL = parts[static_cast<size_t>(sp)];
+    std::vector<char> dm(L.drow.size(), 0), fm(L.frow.size(), 0);
+    for (int bi = sch.part_batch[static_cast<size_t>(sp)]; bi < sch.part_batch[static_cast<size_t>(sp) + 1]; ++bi) {
+      for (int p = sch.batch_ptr[static_cast<size_t>(bi)]; p < sch.batch_ptr[static_cast<size_t>(bi) + 1]; ++p) {
+        const int t = sch.batch_cl[static_cast<size_t>(p)];
+        PL.cl.push_back(t);
+        dm[static_cast<size_t>(L.diag_blk[static_cast<size_t>(t)])] = 1;
+      }
+      for (int it = W.panel_ptr[static_cast<size_t>(bi)]; it < W.panel_ptr[static_cast<size_t>(bi) + 1]; ++it)
+        dm[static_cast<size_t>(W.panel[static_cast<size_t>(it)].blk)] = 1;
+      for (int q = W.schur_ptr[static_cast<size_t>(bi)]; q < W.schur_ptr[static_cast<size_t>(bi) + 1]; ++q) {
+        const SchurTarget& T = W.schur[static_cast<size_t>(q)];
+        ((T.kind & 1) ? fm : dm)[static_cast<size_t>(T.idx)] = 1;
+      }
+    }
+    for (size_t q = 0; q < dm.size(); ++q)
+      if (dm[q]) PL.dblk.push_back(static_cast<int>(q));
+    for (size_t q = 0; q < fm.size(); ++q)
+      if (fm[q]) PL.fblk.push_back(static_cast<int>(q));
+  }
+  return parts;
 }
 
 int fill_segments(int nbat, int requested) { return std::max(1, std::min(requested, nbat)); }

@@ -75,6 +75,10 @@ constexpr int kInteriorParts = 8;
 struct LevelSchedule {
   std::vector<int> batch_ptr, batch_cl;  // local ids, ascending within a batch
   std::vector<int> order;                // [nl] batch index of each cluster
+  // SUBTREE schedule: batches [part_batch[s], part_batch[s + 1]) eliminate
+  // interior clusters of subtree s only; batches from part_batch[parts] on are
+  // the boundary clusters (all batches, for the other schedules)
+  std::vector<int> part_batch;           // [kInteriorParts + 1]
 };
 
 // Per-batch work lists (static for a schedule; sizes resolved on device).
@@ -155,6 +159,18 @@ struct FrontPlan {
 // init[f] != 0: the block holds content at level entry (carried fill-in
 // deposited by the merge of the finer level); may be empty.
 FrontPlan build_front(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W, const std::vector<int>& bsz, const std::vector<int>& init);
+
+// Multi-GPU subtree partition (h2g_factorize_dist): what the interior phase of
+// each of the kInteriorParts subtrees writes under the SUBTREE schedule - the
+// clusters it eliminates (final ranks, chain records), the dense blocks it
+// rotates / updates and the fill blocks it deposits into - read off the work
+// lists of the subtree's batches. Lists of different subtrees are disjoint
+// (an interior cluster's dense neighbours all lie in its own subtree).
+struct PartList {
+  std::vector<int> cl, dblk, fblk;
+  size_t ints() const { return cl.size() + fblk.size(); }
+};
+std::vector<PartList> build_parts(const LevelSym& L, const LevelSchedule& sch, const LevelWork& W);
 
 Structure structure_from_desc(const h2g_matrix_desc* d);
 Structure build_structure(const double* pts, int64_t n, int64_t leafsize, double eta, std::vector<int64_t>* perm);

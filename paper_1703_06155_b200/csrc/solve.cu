@@ -17,11 +17,13 @@ namespace h2g {
 // C = conj-transpose), x / out n x nrhs in shared memory: one warp per output
 // row with the lanes spread over the row's k range (many independent loads in
 // flight), up to 8 right-hand sides per pass over A.
-__device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const cplx* x, int ldx, cplx* out, int ldo) {
+__device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const cplx* x, int ldx, cplx* out, long long ldo, int r0 = 0,
+                          int r1 = -1) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  if (r1 < 0) r1 = n;  // output rows [r0, r1) only (a slab of the product)
   for (int c0 = 0; c0 < nrhs; c0 += 8) {
     const int nc = min(8, nrhs - c0);
-    for (int i = warp; i < n; i += nw) {
+    for (int i = r0 + warp; i < r1; i += nw) {
       cplx acc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[c] = czero();
@@ -112,16 +114,23 @@ __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool 
 
 // seg <- Qt^H seg, then head <- L11^{-1} head (solve.hpp:47-50); one CTA per
 // record.
-__device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, unsigned char* smraw) {
+__device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, unsigned char* smraw,
+                              const cplx* pre = nullptr) {
   const int b = S.bsz[t], e = b - S.kfin[t];
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);  // b x nrhs
   cplx* sO = sS + (size_t)b * nrhs;           // b x nrhs
   cplx* sR = sO + (size_t)b * nrhs;           // reduction scratch (blockDim)
-  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
-  __syncthreads();
-  const cplx* Q = S.chain + S.Qt_off[t];
-  warp_gemv(b, nrhs, Q, b, OP_C, sS, b, sO, b);
+  // pre == nullptr: rotate the segment here; else pre holds Qt^H seg already
+  // (computed by the record's slab items, split records)
+  if (pre) {
+    for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sO[idx] = pre[p0 + (idx % b) + (idx / b) * ldy];
+  } else {
+    for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
+    __syncthreads();
+    const cplx* Q = S.chain + S.Qt_off[t];
+    warp_gemv(b, nrhs, Q, b, OP_C, sS, b, sO, b);
+  }
   __syncthreads();
   if (e > 0) {
     if (explicit_inv) {
@@ -145,6 +154,18 @@ __device__ void fwd_head_body(const SolveLevel& S, int t, cplx* y, long long ldy
     }
   }
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
+}
+
+// Slab sl of ns of a split record's rotation: rows [r0, r1) of Qt^H seg into
+// pre (the record's head item applies L11^{-1} once every slab has landed).
+__device__ void fwd_slab_body(const SolveLevel& S, int t, int sl, int ns, const cplx* y, long long ldy, int nrhs, cplx* pre, unsigned char* smraw) {
+  const int b = S.bsz[t];
+  const long long p0 = S.pos[t];
+  cplx* sS = reinterpret_cast<cplx*>(smraw);  // b x nrhs
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = y[p0 + (idx % b) + (idx / b) * ldy];
+  __syncthreads();
+  const int rows = (b + ns - 1) / ns, r0 = sl * rows, r1 = min(b, r0 + rows);
+  warp_gemv(b, nrhs, S.chain + S.Qt_off[t], b, OP_C, sS, b, pre + p0, ldy, r0, r1);
 }
 
 // y[pos_j ...] -= sum_m Lbar(m, j) head_m (solve.hpp:51). Thread (i, g):
@@ -252,8 +273,10 @@ __device__ void bwd_gather_body(const SolveLevel& S, int t, int q, int c, int ns
 
 // Backward record (solve.hpp:73-81): head -= sum of the gathered partials (in
 // neighbour order); U11 solve; seg <- conj(Qt) seg. One CTA per record.
+// post != nullptr (split record): the segment before its rotation goes to
+// post and the record's slab items apply conj(Qt).
 __device__ void bwd_body(const SolveLevel& S, int t, cplx* y, long long ldy, int nrhs, int explicit_inv, const cplx* part0, long long slot_stride,
-                         unsigned char* smraw) {
+                         unsigned char* smraw, cplx* post = nullptr) {
   const int b = S.bsz[t], kf = S.kfin[t], e = b - kf;
   const long long p0 = S.pos[t];
   cplx* sS = reinterpret_cast<cplx*>(smraw);
@@ -302,9 +325,26 @@ __device__ void bwd_body(const SolveLevel& S, int t, cplx* y, long long ldy, int
       }
     }
   }
+  if (post) {
+    for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) post[p0 + (idx % b) + (idx / b) * ldy] = sS[idx];
+    return;
+  }
   const cplx* Q = S.chain + S.Qt_off[t];
   cta_gemv_n(b, b, nrhs, Q, b, true, sS, b, sO, b, false, sR);
   for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) y[p0 + (idx % b) + (idx / b) * ldy] = sO[idx];
+}
+
+// Slab sl of ns of a split record's backward rotation: rows [r0, r1) of
+// conj(Qt) post -> y.
+__device__ void bwd_slab_body(const SolveLevel& S, int t, int sl, int ns, cplx* y, long long ldy, int nrhs, const cplx* post, unsigned char* smraw) {
+  const int b = S.bsz[t];
+  const long long p0 = S.pos[t];
+  cplx* sS = reinterpret_cast<cplx*>(smraw);
+  cplx* sR = sS + 2 * (size_t)b * nrhs;
+  for (int idx = threadIdx.x; idx < b * nrhs; idx += blockDim.x) sS[idx] = post[p0 + (idx % b) + (idx / b) * ldy];
+  __syncthreads();
+  const int rows = (b + ns - 1) / ns, r0 = sl * rows, r1 = min(b, r0 + rows);
+  if (r1 > r0) cta_gemv_n(r1 - r0, b, nrhs, S.chain + S.Qt_off[t] + r0, b, true, sS, b, y + p0 + r0, ldy, false, sR);
 }
 
 // One persistent cooperative kernel per level and direction: the batches of
@@ -386,13 +426,21 @@ __device__ __forceinline__ void publish(int* p, int v) {
   if (threadIdx.x == 0) st_release(p, v);
 }
 
+// Records with large blocks are split: the b x b rotation, which sits on the
+// dependency chain, is cut into row slabs handed to different CTAs (item code
+// kSlabBase + 64 t + slab); the record's own item then only applies the
+// triangular inverse (forward) or runs before the slabs (backward).
+constexpr int kSlabBase = 1 << 30;
+
 // Forward (solve.hpp:43-59). items: >= 0 record cluster t, < 0 target -1-f.
-// cnt: [0] ticket, [1 + s] writers of segment s done.
-__global__ void __launch_bounds__(256) k_fwd_flow(SolveLevel S, SolveSched P, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv,
-                                                  int* cnt, int* fail) {
+// cnt: [0] ticket, [1 + s] writers of segment s done, [1 + nl + t] slabs of record t done.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv,
+                                                 int* cnt, int* fail, cplx* tmp) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_item, s_ok;
   int* seg = cnt + 1;
+  int* slab_done = cnt + 1 + S.nl;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(cnt, 1), s_ok = 1;
     __syncthreads();
@@ -400,12 +448,25 @@ __global__ void __launch_bounds__(256) k_fwd_flow(SolveLevel S, SolveSched P, So
     __syncthreads();
     if (it >= F.nf) return;
     const int code = F.f_items[it];
-    if (code >= 0) {
-      const int t = code, w = F.rec_widx[t];
+    if (code >= kSlabBase) {
+      // slab of a split record's rotation: reads the segment once its earlier writers are done
+      const int t = (code - kSlabBase) >> 6, sl = (code - kSlabBase) & 63, w = F.rec_widx[t];
       if (threadIdx.x == 0) s_ok = wait_ge(seg + t, w, fail);
       acquire_all(seg + t);
       if (!s_ok) return;
-      fwd_head_body(S, t, y, ldy, nrhs, explicit_inv, smraw);
+      fwd_slab_body(S, t, sl, F.rec_ns_f[t], y, ldy, nrhs, tmp, smraw);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(slab_done + t, 1);
+      }
+    } else if (code >= 0) {
+      const int t = code, w = F.rec_widx[t], ns = F.rec_ns_f[t];
+      if (threadIdx.x == 0) s_ok = ns ? wait_ge(slab_done + t, ns, fail) : wait_ge(seg + t, w, fail);
+      acquire_all(ns ? slab_done + t : seg + t);
+      if (!s_ok) return;
+      fwd_head_body(S, t, y, ldy, nrhs, explicit_inv, smraw, ns ? tmp : nullptr);
       publish(seg + t, w + 1);
     } else {
       const int f = -1 - code;
@@ -429,15 +490,18 @@ __global__ void __launch_bounds__(256) k_fwd_flow(SolveLevel S, SolveSched P, So
 
 // Backward (solve.hpp:65-83). items: >= 0 record cluster m, < 0 gather slot
 // -1-s. cnt: [0] ticket, [1 + m] slots of m done, [1 + nl + c] reads of c's
-// retained part done, [1 + 2 nl + c] record c done.
-__global__ void __launch_bounds__(256) k_bwd_flow(SolveLevel S, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
-                                                  int* cnt, int* fail) {
+// retained part done, [1 + 2 nl + c] record c done (split: its slabs done),
+// [1 + 3 nl + m] head of split record m done.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
+                                                 int* cnt, int* fail, cplx* tmp) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_item, s_ok;
   const int nl = S.nl;
   int* slots_done = cnt + 1;
   int* reads_done = cnt + 1 + nl;
   int* rec_done = cnt + 1 + 2 * nl;
+  int* head_done = cnt + 1 + 3 * nl;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(cnt, 1), s_ok = 1;
     __syncthreads();
@@ -445,7 +509,19 @@ __global__ void __launch_bounds__(256) k_bwd_flow(SolveLevel S, SolveFlow F, cpl
     __syncthreads();
     if (it >= F.nb) return;
     const int code = F.b_items[it];
-    if (code >= 0) {
+    if (code >= kSlabBase) {
+      const int m = (code - kSlabBase) >> 6, sl = (code - kSlabBase) & 63;
+      if (threadIdx.x == 0) s_ok = wait_ge(head_done + m, 1, fail);
+      acquire_all(head_done + m);
+      if (!s_ok) return;
+      bwd_slab_body(S, m, sl, F.rec_ns_b[m], y, ldy, nrhs, tmp, smraw);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(rec_done + m, 1);
+      }
+    } else if (code >= 0) {
       const int m = code;
       if (threadIdx.x == 0) {
         s_ok = wait_ge(slots_done + m, F.rec_nslot[m], fail);
@@ -454,14 +530,15 @@ __global__ void __launch_bounds__(256) k_bwd_flow(SolveLevel S, SolveFlow F, cpl
       acquire_all(slots_done + m);
       if (!s_ok) return;
       const int e = S.bsz[m] - S.kfin[m];
-      bwd_body(S, m, y, ldy, nrhs, explicit_inv, part + (size_t)F.slot_off[F.rec_slot0[m]] * nrhs, (long long)e * nrhs, smraw);
-      publish(rec_done + m, 1);
+      const int ns = F.rec_ns_b[m];
+      bwd_body(S, m, y, ldy, nrhs, explicit_inv, part + (size_t)F.slot_off[F.rec_slot0[m]] * nrhs, (long long)e * nrhs, smraw, ns ? tmp : nullptr);
+      publish(ns ? head_done + m : rec_done + m, 1);
     } else {
       const int sl = -1 - code;
       const int m = F.slot_m[sl], a = F.slot_c[sl];
       const int nC = S.C_ptr[m + 1] - S.C_ptr[m];
       const int c = a >= 0 ? S.C_nb[a] : -1;
-      if (threadIdx.x == 0 && c >= 0 && F.slot_final[sl]) s_ok = wait_ge(rec_done + c, 1, fail);
+      if (threadIdx.x == 0 && c >= 0 && F.slot_final[sl]) s_ok = wait_ge(rec_done + c, max(1, F.rec_ns_b[c]), fail);
       acquire_all(rec_done + (c >= 0 ? c : m));
       if (!s_ok) return;
       bwd_gather_to(S, m, a >= 0 ? a - S.C_ptr[m] : nC, y, ldy, nrhs, part + (size_t)F.slot_off[sl] * nrhs, reinterpret_cast<cplx*>(smraw));
@@ -619,7 +696,7 @@ void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s) {
 }
 
 
-static int flow_grid(const void* fn, size_t smem) {
+static int flow_grid(const void* fn, int nt, size_t smem) {
   static std::mutex mu;
   static std::map<std::tuple<int, const void*, size_t>, int> cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -629,33 +706,60 @@ static int flow_grid(const void* fn, size_t smem) {
   int dev = 0, nsm = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, nt, smem);
   if (per < 1) throw std::runtime_error("solve flow kernel does not fit on an SM");
   const int g = std::max(1, std::min(per, 2)) * nsm;
   cache[key] = g;
   return g;
 }
 
+// Threads per CTA of the dataflow kernels: a record's rotation (a b x b GEMV
+// by one CTA) sits on the dependency chain, so the coarse levels with large
+// blocks run wide CTAs. H2G_SOLVE_THREADS overrides (256 / 512 / 1024).
+static int flow_threads(int bmax) {
+  static const int forced = std::getenv("H2G_SOLVE_THREADS") ? std::atoi(std::getenv("H2G_SOLVE_THREADS")) : 0;
+  if (forced == 256 || forced == 512 || forced == 1024) return forced;
+  return bmax <= 48 ? 256 : (bmax <= 96 ? 512 : 1024);
+}
+
+template <int NT>
+static void fwd_flow_nt(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
+                        int* fail, cplx* tmp, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + NT * sizeof(cplx);
+  smem_attr((const void*)k_fwd_flow<NT>, smem);
+  const int grid = std::min(flow_grid((const void*)k_fwd_flow<NT>, NT, smem), F.nf);
+  k_fwd_flow<NT><<<grid, NT, smem, s>>>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp);
+}
+
 void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
-                     int* fail, cudaStream_t s) {
+                     int* fail, cplx* tmp, cudaStream_t s) {
   if (F.nf <= 0) return;
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
-  smem_attr((const void*)k_fwd_flow, smem);
-  cudaMemsetAsync(cnt, 0, (size_t)(S.nl + 1) * sizeof(int), s);
-  const int grid = std::min(flow_grid((const void*)k_fwd_flow, smem), F.nf);
-  k_fwd_flow<<<grid, 256, smem, s>>>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail);
+  cudaMemsetAsync(cnt, 0, (size_t)(2 * S.nl + 1) * sizeof(int), s);
+  const int nt = flow_threads(S.bmax);
+  if (nt == 256) fwd_flow_nt<256>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
+  else if (nt == 512) fwd_flow_nt<512>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
+  else fwd_flow_nt<1024>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_fwd_flow failed: ") + cudaGetErrorString(e));
 }
 
+template <int NT>
+static void bwd_flow_nt(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
+                        cplx* tmp, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + NT * sizeof(cplx);
+  smem_attr((const void*)k_bwd_flow<NT>, smem);
+  const int grid = std::min(flow_grid((const void*)k_bwd_flow<NT>, NT, smem), F.nb);
+  k_bwd_flow<NT><<<grid, NT, smem, s>>>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp);
+}
+
 void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
-                     cudaStream_t s) {
+                     cplx* tmp, cudaStream_t s) {
   if (F.nb <= 0) return;
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + 256 * sizeof(cplx);
-  smem_attr((const void*)k_bwd_flow, smem);
-  cudaMemsetAsync(cnt, 0, (size_t)(3 * S.nl + 1) * sizeof(int), s);
-  const int grid = std::min(flow_grid((const void*)k_bwd_flow, smem), F.nb);
-  k_bwd_flow<<<grid, 256, smem, s>>>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail);
+  cudaMemsetAsync(cnt, 0, (size_t)(4 * S.nl + 1) * sizeof(int), s);
+  const int nt = flow_threads(S.bmax);
+  if (nt == 256) bwd_flow_nt<256>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
+  else if (nt == 512) bwd_flow_nt<512>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
+  else bwd_flow_nt<1024>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_bwd_flow failed: ") + cudaGetErrorString(e));
 }

@@ -62,18 +62,23 @@ struct SolveFlow {
   const int* rec_slot0;          // first slot of a record
   const int* rec_nslot;
   const int* reader_need;        // slots that read the record's retained part before it rotates it
+  // split records (large blocks): number of rotation slabs, 0 = unsplit
+  const int* rec_ns_f;
+  const int* rec_ns_b;
 };
 
 // Whole level, all batches, one cooperative launch per direction; part holds
 // max_b nb * (maxc_b + 1) * bmax * nrhs gathered backward partials.
 void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
 void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s);
-// Dataflow versions (no grid-wide barriers). cnt: >= 3 nl + 1 ints (reset by
+// Dataflow versions (no grid-wide barriers). cnt: >= 4 nl + 1 ints (reset by
 // the launch); *fail is set when a dependency wait stalls (never reset here).
+// tmp: n x nrhs scratch (ld ldy) holding the split records' segments between
+// their slab and head items.
 void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
-                     int* fail, cudaStream_t s);
+                     int* fail, cplx* tmp, cudaStream_t s);
 void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
-                     cudaStream_t s);
+                     cplx* tmp, cudaStream_t s);
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s);
 void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s);
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s);
