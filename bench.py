@@ -229,8 +229,11 @@ def main():
         import torch
         import torch.distributed as dist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
+        # one GPU per rank: NCCL over NVLink; ranks sharing a GPU (single-GPU test boxes) or no GPU (reference arm on CPU): gloo
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        backend = "nccl" if ndev >= world else "gloo"
+        if ndev:
+            local = local % ndev
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
 
@@ -417,6 +420,21 @@ def main():
                      "algorithmic": {"flops": sch["flops"], "tflops": sch["flops"] / t_s / 1e12, "frac": sch["flops"] / t_s / 1e12 / peak_tf,
                                      "note": "SURVEY 8d count (full b_j x e x b_c products, as the reference's GEMMs execute them, "
                                              "including the exact-zero rows/columns k_schur skips)"}})
+        # per level: a launch is bound by whichever of its flops / bytes takes longer at peak
+        # (fine levels: e of a few columns, the target read-modify-write dominates -> HBM)
+        per_level, bound_ms = [], 0.0
+        for lv in chp.schur_levels():
+            if lv["ms"] <= 0:
+                continue
+            t_f, t_b = lv["flops"] / (peak_tf * 1e12), lv["bytes"] / (hbm * 1e9)
+            bound_ms += 1e3 * max(t_f, t_b)
+            per_level.append({"level": lv["level"], "ms": round(lv["ms"], 2), "tflops": round(lv["flops"] / lv["ms"] / 1e9, 2),
+                              "gbs": round(lv["bytes"] / lv["ms"] / 1e6, 1), "bound": "tensor" if t_f >= t_b else "hbm",
+                              "frac": round(1e3 * max(t_f, t_b) / lv["ms"], 3)})
+        roof["per_level"] = per_level
+        roof["per_level_note"] = ("executed flops / algorithmic bytes (targets read + written once per launch, panels read once per target) "
+                                  "per level against the FP64 and HBM peaks; frac = the larger of the two lower bounds / event time")
+        roof["frac_mixed_bound"] = bound_ms / sch["ms"]
     solve_roof = None
     if solve_ms > 0:
         sgbs = work["solve_bytes"] / (solve_ms / 1e3) / 1e9

@@ -278,6 +278,9 @@ int h2g_chain_timing(const h2g_chain* c, double* factor_ms, double* solve_ms, in
  * whole-map scans, factorization.hpp:268-293): its build time for this chain
  * (outside the device factor time of h2g_chain_timing) and whether it was
  * built (1) or reused from the matrix / context plan cache (0). */
+/* k_schur per level (4 doubles each: level, executed flops, executed bytes,
+ * event ms - the ms only after a profiled run); out may be null (count). */
+int h2g_chain_schur_levels(const h2g_chain* c, int32_t* nlevels, double* out);
 int h2g_chain_plan(const h2g_chain* c, double* plan_ms, int32_t* built);
 /* Drop the context's structure-keyed plan cache (a later factorize of a new
  * matrix handle then builds its plan from scratch: a cold-structure run). */

@@ -176,6 +176,7 @@ SYMBOLS = {
     "h2g_chain_kernel_stats": (C.c_int, [_P, C.c_int32, _D]),
     "h2g_factorize_dist": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_void_p, C.POINTER(_P), C.POINTER(_Err)]),
     "h2g_chain_dist_stats": (C.c_int, [_P, _D]),
+    "h2g_chain_schur_levels": (C.c_int, [_P, _I32, _D]),
     "h2g_partition_plan": (C.c_int, [C.POINTER(_Desc), C.c_int32, C.c_int32, _I64, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_Err)]),
 }
 
@@ -572,6 +573,14 @@ class FactorChain:
 
     def hash(self):
         return int(lib().h2g_chain_hash(self.h))
+
+    def schur_levels(self):
+        """k_schur per level: executed flops / bytes and (profiled runs) ms."""
+        n = C.c_int32()
+        lib().h2g_chain_schur_levels(self.h, C.byref(n), None)
+        out = np.zeros(4 * max(n.value, 1))
+        lib().h2g_chain_schur_levels(self.h, C.byref(n), _d(out))
+        return [dict(level=int(out[4 * i]), flops=out[4 * i + 1], bytes=out[4 * i + 2], ms=out[4 * i + 3]) for i in range(n.value)]
 
     def dist_stats(self):
         """factorize_dist: bytes this rank contributed / bytes exchanged by all

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <complex>
@@ -492,6 +493,8 @@ struct h2g_chain {
   double factor_flops = 0.0, schur_flops = 0.0, solve_bytes = 0.0, schur_bytes = 0.0;
   double schur_flops_exec = 0.0, schur_bytes_exec = 0.0;  // k_schur work after the exact-zero skip
   double kms[PC_N] = {0}, kflops[PC_N] = {0}, kbytes[PC_N] = {0};
+  // k_schur per level (profiling runs): level, executed flops, executed bytes, event ms
+  std::map<int, std::array<double, 3>> schur_levels;
   long long klaunch[PC_N] = {0};
 };
 
@@ -1383,16 +1386,32 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           if (cb.flags & 2) needU[cb.c] = 1;
         }
         auto lifted = [&](const PanelItem& pi) { return pi.lift && (pi.side == 0 ? needU[pi.entry] : needL[pi.entry]); };
-        long long ltop = 0;
-        for (size_t bi = 0; bi + 1 < SC.batch_ptr.size(); ++bi)
+        // a lifted panel lives only through its own batch (written by the
+        // panel GEMMs, read by that batch's Schur launches; the deferred
+        // launch may still read it while the next batch writes its own), so
+        // the buffer is two halves used by even / odd batches
+        long long lhalf = 0;
+        for (size_t bi = 0; bi + 1 < SC.batch_ptr.size(); ++bi) {
+          long long lb = 0;
           for (int it = W.panel_ptr[bi]; it < W.panel_ptr[bi + 1]; ++it) {
             const PanelItem& pi = W.panel[it];
             if (!lifted(pi)) continue;
             const int t = SC.batch_cl[SC.batch_ptr[bi] + pi.q];
             const long long em = cur.bsz[t] - cur.korig[t];
-            (pi.side == 0 ? liftU_off : liftL_off)[pi.entry] = ltop;
-            ltop += em * cur.bsz[pi.nb];
+            (pi.side == 0 ? liftU_off : liftL_off)[pi.entry] = lb;  // half-relative, rebased below
+            lb += em * cur.bsz[pi.nb];
           }
+          lhalf = std::max(lhalf, lb);
+        }
+        for (size_t bi = 1; bi + 1 < SC.batch_ptr.size(); bi += 2)
+          for (int it = W.panel_ptr[bi]; it < W.panel_ptr[bi + 1]; ++it) {
+            const PanelItem& pi = W.panel[it];
+            if (lifted(pi)) (pi.side == 0 ? liftU_off : liftL_off)[pi.entry] += lhalf;
+          }
+        const long long ltop = 2 * lhalf;
+        if (verbose)
+          std::fprintf(stderr, "[h2g] level %d entry: chain arena %.2f GB, lifted panels %.2f GB, complements %.2f GB; device free %.2f GB\n", l,
+                       top * 16 / 1e9, ltop * 16 / 1e9, (double)nl * bb * 16 / 1e9, BlockCache::get().headroom() / 1e9);
         ensure((size_t)(std::max<long long>(top, 1) + std::max<long long>(ltop, 1) + (long long)nl * bb) * 16 + (size_t(4) << 30), nullptr);
         CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
         DBuf lift;
@@ -1480,6 +1499,9 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           n_ptr.push_back(static_cast<int>(ndesc_f.size()));
         }
         DBuf ybuf, gbuf, cnbuf, dirbuf, lambuf, flagbuf, cmaxbuf;
+        if (verbose)
+          std::fprintf(stderr, "[h2g] level %d step-0 scratch: projected fill %.2f GB, Gram partials %.2f GB, directions %.2f GB; device free %.2f GB\n", l,
+                       ymax * 16 / 1e9, gmax * 16 / 1e9, (double)std::max(1, W.max_batch) * bb * 16 / 1e9, BlockCache::get().headroom() / 1e9);
         ybuf.alloc(ymax * 16, st);
         gbuf.alloc(gmax * 16, st);
         cnbuf.alloc(std::max<size_t>(ndesc_f.size(), 1) * 8, st);
@@ -1557,6 +1579,10 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         size_t pmax = 1;
         for (int bi = 0; bi < nbat0; ++bi) pmax = std::max<size_t>(pmax, W.panel_ptr[bi + 1] - W.panel_ptr[bi]);
         DBuf panbuf;
+        if (verbose)
+          std::fprintf(stderr, "[h2g] level %d panel scratch %.2f GB (%zu items), eigensolver workspace %.2f GB, level scratch %.2f GB; device free %.2f GB\n", l,
+                       pmax * bb * 16 / 1e9, pmax, (double)mb * eig1_ws_bytes(bm) / 1e9, level_scratch_bytes(nl, bm, mb) / 1e9,
+                       BlockCache::get().headroom() / 1e9);
         panbuf.alloc(pmax * bb * 16, st);
         DBuf dA1, dA2, dB1, dB2, dN, dR1, dR2, dP1, dP2, dP3, dPM, dPC;
         upload(dR1, gR1, st);
@@ -2056,7 +2082,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         rotbuf.release();
         eigws.release();
         scratch.release();
-        const double sflops_lv0 = sflops, flops_lv0 = flops, sexec_lv0 = C->schur_flops_exec;
+        const double sflops_lv0 = sflops, flops_lv0 = flops, sexec_lv0 = C->schur_flops_exec, sbexec_lv0 = C->schur_bytes_exec;
         // ---- records + diagnostics
         long long rsb = 0, rsa = 0, elim = 0, ledger = 0;
         std::vector<int> rec_order;
@@ -2242,6 +2268,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         for (int t = 0; t < nl; ++t) C->solve_bytes += 16.0 * (double)cur.bsz[t] * cur.bsz[t];  // second Qtilde pass
         C->solve_bytes += 4.0 * 16.0 * (double)S.n;
 
+        C->schur_levels[l] = {C->schur_flops_exec - sexec_lv0, C->schur_bytes_exec - sbexec_lv0, 0.0};
         mark("records done");
         if (verbose)
           std::fprintf(stderr, "[h2g] level %d: algorithmic GFLOP total %.1f, Schur %.1f (executed %.1f)\n", l, (flops - flops_lv0) / 1e9,
@@ -2620,6 +2647,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         cudaEventElapsedTime(&e, r.a, r.b);
         C->kms[r.cls] += e;
         per[{r.level, r.cls}] += e;
+        if (r.cls == PC_SCHUR && C->schur_levels.count(r.level)) C->schur_levels[r.level][2] += e;
       }
       if (verbose) {
         static const char* nm[PC_N] = {"complement", "gram", "colnorm", "eig1", "head", "panel", "schur", "merge", "root", "other", "eigvec", "eig1b"};
@@ -3024,6 +3052,19 @@ int h2g_chain_kernel_stats(const h2g_chain* c, int32_t cls, double* out) {
   out[1] = (double)c->klaunch[cls];
   out[2] = c->kflops[cls];
   out[3] = c->kbytes[cls];
+  return H2G_OK;
+}
+
+int h2g_chain_schur_levels(const h2g_chain* c, int32_t* nlevels, double* out) {
+  if (!c || !nlevels) return H2G_ERR_INVALID_INPUT;
+  *nlevels = static_cast<int32_t>(c->schur_levels.size());
+  if (out) {
+    size_t q = 0;
+    for (const auto& kv : c->schur_levels) {
+      out[q++] = kv.first;
+      for (double v : kv.second) out[q++] = v;
+    }
+  }
   return H2G_OK;
 }
 
