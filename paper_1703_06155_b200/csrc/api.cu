@@ -418,6 +418,8 @@ struct h2g_context {
   // helper stream for small independent kernels of the main chain
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
+  // device -> host copies of a streamed level's chain segments
+  cudaStream_t copy = nullptr;
   Prof prof_aux;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevError* d_err = nullptr;
@@ -453,6 +455,7 @@ struct ChainLevelHost {
   const cplx* chain_ptr() const { return harena.p ? harena.as<cplx>() : arena.as<cplx>(); }
   size_t chain_bytes() const { return harena.p ? harena.bytes : arena.bytes; }
   DBuf meta;                 // packed int / offset arrays
+  DBuf solve_meta;           // streamed level: the compact chain offsets the solve reads
   SolveLevel sl{};
   std::vector<int> batch_ptr, batch_maxc;
   const int* d_batch = nullptr;
@@ -973,6 +976,7 @@ int h2g_context_create(int device, h2g_context** out, h2g_error* err) {
     CK(cudaEventCreateWithFlags(&c->ev_crit, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_bulk, cudaEventDisableTiming));
     CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio_hi));
+    CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->ev_aux0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_aux1, cudaEventDisableTiming));
     BlockCache::get().add_stream(c->stream, device);
@@ -1003,6 +1007,7 @@ static void context_teardown(h2g_context* ctx) {
   cudaEventDestroy(ctx->ev_aux0);
   cudaEventDestroy(ctx->ev_aux1);
   cudaStreamDestroy(ctx->aux);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   cudaStreamDestroy(ctx->side);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_flag);
@@ -1361,9 +1366,8 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         std::vector<long long> Qt_off(nl), L11_off(nl), U11_off(nl), Linv_off(nl), Uinv_off(nl), Lself_off(nl), Uself_off(nl);
         std::vector<long long> Lbar_off(Y.R_nb.size()), Ubar_off(Y.C_nb.size());
         long long top = 0;
-        for (int t = 0; t < nl; ++t) {
+        auto place = [&](int t) {  // everything of cluster t but Qt
           const long long b = cur.bsz[t], em = b - cur.korig[t];
-          Qt_off[t] = top, top += b * b;
           L11_off[t] = top, top += em * em;
           U11_off[t] = top, top += em * em;
           Linv_off[t] = top, top += em * em;
@@ -1372,6 +1376,73 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           Uself_off[t] = top, top += b * em;
           for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) Lbar_off[a] = top, top += (long long)cur.bsz[Y.R_nb[a]] * em;
           for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) Ubar_off[a] = top, top += (long long)cur.bsz[Y.C_nb[a]] * em;
+        };
+        // Streamed chain (large segmented levels): only Qt, which later
+        // clusters' lifts and the collapse read, stays on the device for the
+        // whole level. Everything else of a cluster is read inside its own
+        // batch only (and by the solve), so it is laid out in elimination
+        // order, written to one of two device halves (segment parity) and
+        // copied to the level's pinned host arena when its segment ends.
+        // Logical layout (host arena, solve offsets): [all Qt | segment 0 | segment 1 | ...].
+        const int stream_env = std::getenv("H2G_CHAIN_STREAM") ? std::atoi(std::getenv("H2G_CHAIN_STREAM")) : -1;  // 0 never, 1 always
+        long long qtot = 0;
+        for (int t = 0; t < nl; ++t) qtot += (long long)cur.bsz[t] * cur.bsz[t];
+        bool streamed = false;
+        if (cur.has_front && cur.front.K > 1 && !hooks && stream_env != 0) {
+          long long ub = qtot;
+          for (int t = 0; t < nl; ++t) {
+            const long long b = cur.bsz[t], em = b - cur.korig[t];
+            ub += 4 * em * em + 2 * b * em;
+            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) ub += (long long)cur.bsz[Y.R_nb[a]] * em;
+            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) ub += (long long)cur.bsz[Y.C_nb[a]] * em;
+          }
+          size_t fr = 0, tot = 0;
+          cudaMemGetInfo(&fr, &tot);
+          streamed = stream_env > 0 || (double)ub * 16 > 0.08 * (double)tot;
+        }
+        std::vector<long long> seg_begin, seg_len;  // streamed: logical start / length of every segment's part (elements)
+        long long ring_half = 0;
+        if (!streamed) {
+          for (int t = 0; t < nl; ++t) {
+            Qt_off[t] = top, top += (long long)cur.bsz[t] * cur.bsz[t];
+            place(t);
+          }
+        } else {
+          for (int t = 0; t < nl; ++t) Qt_off[t] = top, top += (long long)cur.bsz[t] * cur.bsz[t];
+          const int Kc = cur.front.K;
+          const int nbat1 = static_cast<int>(SC.batch_ptr.size()) - 1;
+          for (int sg = 0; sg < Kc; ++sg) {
+            seg_begin.push_back(top);
+            for (int bi = cur.front.seg_first_batch[sg]; bi < cur.front.seg_first_batch[sg + 1] && bi < nbat1; ++bi)
+              for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) place(SC.batch_cl[p]);
+            seg_len.push_back(top - seg_begin.back());
+            ring_half = std::max(ring_half, seg_len.back());
+          }
+        }
+        // offsets of the finished chain (host copies, solve). Resident level:
+        // the device offsets. Streamed level: the compact layout [all Qt |
+        // segment 0 | segment 1 | ...] with every block at its final size
+        // (e = b - kfin instead of the bound b - korig), filled in as the
+        // segments end.
+        std::vector<long long> lQt(Qt_off), lL11(L11_off), lU11(U11_off), lLinv(Linv_off), lUinv(Uinv_off), lLself(Lself_off),
+            lUself(Uself_off), lLbar(Lbar_off), lUbar(Ubar_off);
+        const long long top_logical = top;
+        std::vector<std::vector<char>> seg_host;  // streamed: compact copy of every finished segment (pageable until the level ends)
+        long long compact_top = qtot;
+        if (streamed) {
+          std::vector<int> seg_of(nl, 0);
+          for (int sg = 0; sg < cur.front.K; ++sg)
+            for (int bi = cur.front.seg_first_batch[sg]; bi < cur.front.seg_first_batch[sg + 1] && bi + 1 < (int)SC.batch_ptr.size(); ++bi)
+              for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) seg_of[SC.batch_cl[p]] = sg;
+          auto dev = [&](long long o, int sg) { return qtot + (long long)(sg & 1) * ring_half + (o - seg_begin[sg]); };
+          for (int t = 0; t < nl; ++t) {
+            const int sg = seg_of[t];
+            L11_off[t] = dev(L11_off[t], sg), U11_off[t] = dev(U11_off[t], sg), Linv_off[t] = dev(Linv_off[t], sg);
+            Uinv_off[t] = dev(Uinv_off[t], sg), Lself_off[t] = dev(Lself_off[t], sg), Uself_off[t] = dev(Uself_off[t], sg);
+            for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) Lbar_off[a] = dev(Lbar_off[a], sg);
+            for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) Ubar_off[a] = dev(Ubar_off[a], sg);
+          }
+          top = qtot + 2 * ring_half;  // the device allocation
         }
         mark("offsets");
         auto CL = std::make_unique<ChainLevelHost>();
@@ -1414,6 +1485,12 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
                        top * 16 / 1e9, ltop * 16 / 1e9, (double)nl * bb * 16 / 1e9, BlockCache::get().headroom() / 1e9);
         ensure((size_t)(std::max<long long>(top, 1) + std::max<long long>(ltop, 1) + (long long)nl * bb) * 16 + (size_t(4) << 30), nullptr);
         CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
+        if (streamed) {
+          seg_host.resize(cur.front.K);
+          if (verbose)
+            std::fprintf(stderr, "[h2g] level %d: chain streamed to host memory: %.2f GB on the device (Qt %.2f GB + 2 x %.2f GB) instead of %.2f GB\n", l,
+                         top * 16 / 1e9, qtot * 16 / 1e9, ring_half * 16 / 1e9, top_logical * 16 / 1e9);
+        }
         DBuf lift;
         lift.alloc(std::max<long long>(ltop, 1) * 16, st);
         mark("chain allocated");
@@ -1434,6 +1511,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         size_t o_Qt = pk.add(Qt_off), o_L11 = pk.add(L11_off), o_U11 = pk.add(U11_off), o_Li = pk.add(Linv_off), o_Ui = pk.add(Uinv_off);
         size_t o_Lb = pk.add(Lbar_off), o_Ub = pk.add(Ubar_off), o_Ls = pk.add(Lself_off), o_Us = pk.add(Uself_off);
         size_t o_lL = pk.add(liftL_off), o_lU = pk.add(liftU_off);
+
         size_t o_bat = pk.add(SC.batch_cl);
         size_t o_sch = pk.add_raw(reinterpret_cast<const SchurTargetD*>(W.schur.data()), W.schur.size());
         size_t o_con = pk.add_raw(reinterpret_cast<const SchurContribD*>(W.contrib.data()), W.contrib.size());
@@ -1804,6 +1882,46 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           }
           CK(cudaMemcpyAsync(core_tab.p, core_ptr_h.data(), nfill * sizeof(cplx*), cudaMemcpyHostToDevice, st));
           CK(cudaStreamSynchronize(st));  // core_ptr_h is rewritten at the next segment end
+          if (streamed && seg_len[sg] > 0) {
+            // the segment's chain part is final (main and side streams have
+            // drained) and its eliminated sizes are known: every block moves
+            // to its compact place (the kernels already wrote it with its
+            // final leading dimension), then the segment leaves the device
+            CK(cudaStreamSynchronize(ctx->side));
+            std::vector<MoveDesc> mv;
+            const cplx* ringp = CL->arena.as<cplx>();
+            const long long seg0 = compact_top;
+            auto blockmv = [&](long long dev_off, long long len, long long& logical) {
+              logical = compact_top;
+              if (len > 0) mv.push_back({ringp + dev_off, reinterpret_cast<cplx*>((compact_top - seg0) * 16), len});
+              compact_top += len;
+            };
+            for (int bi2 = FP.seg_first_batch[sg]; bi2 < FP.seg_first_batch[sg + 1]; ++bi2)
+              for (int p = SC.batch_ptr[bi2]; p < SC.batch_ptr[bi2 + 1]; ++p) {
+                const int t = SC.batch_cl[p];
+                const long long b = cur.bsz[t], kft = kf[t], e = b - kft;
+                blockmv(L11_off[t], e * e, lL11[t]);
+                blockmv(U11_off[t], e * e, lU11[t]);
+                blockmv(Linv_off[t], e * e, lLinv[t]);
+                blockmv(Uinv_off[t], e * e, lUinv[t]);
+                blockmv(Lself_off[t], kft * e, lLself[t]);
+                blockmv(Uself_off[t], e * kft, lUself[t]);
+                for (int a = Y.R_ptr[t]; a < Y.R_ptr[t + 1]; ++a) blockmv(Lbar_off[a], (long long)cur.bsz[Y.R_nb[a]] * e, lLbar[a]);
+                for (int a = Y.C_ptr[t]; a < Y.C_ptr[t + 1]; ++a) blockmv(Ubar_off[a], (long long)cur.bsz[Y.C_nb[a]] * e, lUbar[a]);
+              }
+            const long long clen = compact_top - seg0;
+            if (clen > 0) {
+              DBuf cbuf, dmv;
+              cbuf.alloc((size_t)clen * 16, st);
+              for (auto& d : mv) d.dst = cbuf.as<cplx>() + reinterpret_cast<long long>(d.dst) / 16;
+              upload(dmv, mv, st);
+              launch_move(dmv.as<MoveDesc>(), static_cast<int>(mv.size()), st);
+              seg_host[sg].resize((size_t)clen * 16);
+              CK(cudaMemcpyAsync(seg_host[sg].data(), cbuf.p, (size_t)clen * 16, cudaMemcpyDeviceToHost, st));
+              CK(cudaStreamSynchronize(st));
+              ++launches;
+            }
+          }
         };
         // ---- multi-GPU subtree partition (h2g_factorize_dist): what the
         // interior phase of every subtree writes, derived from the work lists
@@ -2072,6 +2190,32 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         CK(cudaStreamSynchronize(st));
 
         mark("kfin read back");
+        if (streamed) {
+          // the level's chain in pinned host memory at its final size: Qt from
+          // the device, then the compact segments; the device copy goes away
+          CL->harena.alloc((size_t)std::max<long long>(compact_top, 1) * 16);
+          CK(cudaMemcpyAsync(CL->harena.p, CL->arena.p, (size_t)qtot * 16, cudaMemcpyDeviceToHost, st));
+          {
+            std::vector<std::thread> th;
+            size_t o = (size_t)qtot * 16;
+            for (auto& sgv : seg_host) {
+              char* dst = static_cast<char*>(CL->harena.p) + o;
+              const std::vector<char>* src = &sgv;
+              th.emplace_back([dst, src] {
+                if (!src->empty()) std::memcpy(dst, src->data(), src->size());
+              });
+              o += sgv.size();
+            }
+            for (auto& t2 : th) t2.join();
+          }
+          CK(cudaStreamSynchronize(st));
+          seg_host.clear();
+          seg_host.shrink_to_fit();
+          offloaded += CL->harena.bytes;
+          CL->arena.release();
+          if (verbose)
+            std::fprintf(stderr, "[h2g] level %d: chain %.2f GB in host memory (bound %.2f GB)\n", l, compact_top * 16 / 1e9, top_logical * 16 / 1e9);
+        }
         // level scratch is dead once the last batch has drained (keeps the
         // merge's peak memory down at config 3)
         lift.release();
@@ -2203,13 +2347,13 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         CL->R_nb = Y.R_nb;
         CL->C_ptr = Y.C_ptr;
         CL->C_nb = Y.C_nb;
-        CL->Qt_off = Qt_off;
-        CL->L11_off = L11_off;
-        CL->U11_off = U11_off;
-        CL->Lbar_off = Lbar_off;
-        CL->Ubar_off = Ubar_off;
-        CL->Lself_off = Lself_off;
-        CL->Uself_off = Uself_off;
+        CL->Qt_off = lQt;
+        CL->L11_off = lL11;
+        CL->U11_off = lU11;
+        CL->Lbar_off = lLbar;
+        CL->Ubar_off = lUbar;
+        CL->Lself_off = lLself;
+        CL->Uself_off = lUself;
         CL->batch_ptr = SC.batch_ptr;
         for (int bi = 0; bi + 1 < (int)SC.batch_ptr.size(); ++bi) {
           int mc = 0;
@@ -2263,6 +2407,25 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         SL.Ubar_off = DL.Ubar_off;
         SL.Lself_off = DL.Lself_off;
         SL.Uself_off = DL.Uself_off;
+        if (streamed) {
+          // the solve reads the compact host arena
+          Packer ps;
+          const size_t q_Qt = ps.add(lQt), q_L11 = ps.add(lL11), q_U11 = ps.add(lU11), q_Li = ps.add(lLinv), q_Ui = ps.add(lUinv),
+                       q_Lb = ps.add(lLbar), q_Ub = ps.add(lUbar), q_Ls = ps.add(lLself), q_Us = ps.add(lUself);
+          ps.upload(CL->solve_meta, st);
+          CK(cudaStreamSynchronize(st));
+          const DBuf& sm2 = CL->solve_meta;
+          SL.chain = CL->harena.as<cplx>();
+          SL.Qt_off = at<long long>(sm2, q_Qt);
+          SL.L11_off = at<long long>(sm2, q_L11);
+          SL.U11_off = at<long long>(sm2, q_U11);
+          SL.Linv_off = at<long long>(sm2, q_Li);
+          SL.Uinv_off = at<long long>(sm2, q_Ui);
+          SL.Lbar_off = at<long long>(sm2, q_Lb);
+          SL.Ubar_off = at<long long>(sm2, q_Ub);
+          SL.Lself_off = at<long long>(sm2, q_Ls);
+          SL.Uself_off = at<long long>(sm2, q_Us);
+        }
         // solve traffic (nrhs = 1): chain read (Qtilde twice) + vector
         C->solve_bytes += (double)lvl_bytes;
         for (int t = 0; t < nl; ++t) C->solve_bytes += 16.0 * (double)cur.bsz[t] * cur.bsz[t];  // second Qtilde pass

@@ -750,10 +750,10 @@ namespace h2g {
 // columns tc * (TM/16) + b.
 // Rows padded by one complex: the cp.async writes of a k-major operand hit
 // 8 consecutive k-rows, which would otherwise all start in the same bank.
-template <int TM>
+template <int TM, int NST = 3>
 struct TileSmem {
-  cplx a[3][8][TM + 1];
-  cplx b[3][8][TM + 1];
+  cplx a[NST][8][TM + 1];
+  cplx b[NST][8][TM + 1];
 };
 using Tile128Smem = TileSmem<64>;
 
@@ -943,11 +943,13 @@ struct SchurPanel {
 // drain or extra barrier per contribution; the loads of the next panel are in
 // flight while the current one is multiplied). Slices are 8 deep, zero padded;
 // the upper half of a slice is skipped when it holds no data (e <= 4 at the
-// fine levels). kv: 3 ints of shared memory.
+// fine levels). kv: NST ints of shared memory. NST = 3 stages (2 for the
+// target-prefetch variant of k_schur, which needs the shared memory).
 // mlim / nlim: rows / columns of the tile inside the target; a warp skips the
 // 8 x 8 blocks of its 32 x 32 share that lie outside (targets of ~100 rows
 // would otherwise pay for 128).
-__device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64>& S, const SchurPanel* tab, int n, int* kv, int mlim, int nlim) {
+template <int NST>
+__device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64, NST>& S, const SchurPanel* tab, int n, int* kv, int mlim, int nlim) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int wr = (warp % 2) * 32, wc = (warp / 2) * 32, g = lane / 4, tq = lane % 4;
   const int mi_n = min(4, max(0, (mlim - wr + 7) / 8)), ni_n = min(4, max(0, (nlim - wc + 7) / 8));
@@ -959,7 +961,7 @@ __device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64>& S, con
   auto issue = [&]() {
     if (li < n) {
       const SchurPanel P = tab[li];
-      const int st = issued % 3;
+      const int st = issued % NST;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int idx = threadIdx.x + u * 128;
@@ -983,13 +985,15 @@ __device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64>& S, con
     }
     cp_async_commit();
   };
-  issue();
-  issue();
+  // NST - 1 slices in flight ahead of the one being multiplied
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) issue();
   for (int s = 0; s < total; ++s) {
-    asm volatile("cp.async.wait_group 1;");
+    if constexpr (NST == 3) asm volatile("cp.async.wait_group 1;");
+    else asm volatile("cp.async.wait_group 0;");
     __syncthreads();
     issue();
-    const int st = s % 3;
+    const int st = s % NST;
     const int nh = kv[st] > 4 ? 8 : 4;
     if (mi_n == 0 || ni_n == 0) continue;
     for (int kk = 0; kk < nh; kk += 4) {

@@ -1319,11 +1319,18 @@ __global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch
 // every cluster of the batch that hits it are summed in a fixed order, then
 // subtracted once (:414-425, deposit_fill :363-365). 64 x 64 output tiles,
 // 4 x 4 complex micro-tile per thread, K staged through shared memory.
-template <int TM>
-__global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+// PF (TM = 64, levels whose eliminated sizes are small): the launch is bound
+// by the read-modify-write of the targets, not by the products, so the target
+// tile is fetched into shared memory by cp.async at the start (64 KB in flight
+// per CTA while the contribution tables and panels load) and the epilogue
+// subtracts from the staged copy; two CTAs per SM instead of three.
+template <int TM, bool PF = false>
+__global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
   constexpr int RM = TM / 8, RN = TM / 16;  // DFMA micro-tile (TM < 64)
   extern __shared__ __align__(16) unsigned char tsm[];
-  TileSmem<TM>& S = *reinterpret_cast<TileSmem<TM>*>(tsm);
+  using Smem = TileSmem<TM, PF ? 2 : 3>;
+  Smem& S = *reinterpret_cast<Smem*>(tsm);
+  cplx(*Tt)[TM] = reinterpret_cast<cplx(*)[TM]>(tsm + sizeof(Smem));  // PF: target tile, [column][row]
   const SchurTargetD tg = targets[blockIdx.x];
   int rows, cols, rs = 0, cs = 0, ldo = -1;
   cplx* out;
@@ -1354,6 +1361,14 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
   const int ntr = (rows - rs + TM - 1) / TM, ntc = (cols - cs + TM - 1) / TM;
   if ((int)blockIdx.y >= ntr * ntc) return;
   const int r0 = rs + (blockIdx.y % ntr) * TM, c0 = cs + (blockIdx.y / ntr) * TM;
+  if constexpr (PF) {
+    for (int idx = threadIdx.x; idx < TM * TM; idx += 128) {
+      const int i = idx % TM, j = idx / TM;
+      const bool v = r0 + i < rows && c0 + j < cols;
+      cp_async16(&Tt[j][i], v ? out + (r0 + i) + (size_t)(c0 + j) * ldo : out, v);
+    }
+    cp_async_commit();
+  }
   Acc64 acc;
   cplx accs[TM == 64 ? 1 : RM][TM == 64 ? 1 : RN];
   if constexpr (TM == 64) {
@@ -1432,6 +1447,10 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
       tile_acc<TM>(accs, S, P.A, P.arows, OP_N, P.ash, P.arows, P.B, P.e, OP_N, P.bsh, P.bcols, P.e);
     }
   }
+  if constexpr (PF) {
+    asm volatile("cp.async.wait_group 0;");
+    __syncthreads();
+  }
   // Epilogue: target -= acc. The target values of a row group are loaded
   // together before any store (the stores may alias later loads, so loads
   // interleaved with stores would serialise into one round trip each).
@@ -1451,7 +1470,7 @@ __global__ void __launch_bounds__(128, 3) k_schur(DevLevel L, const SchurTargetD
           for (int h = 0; h < 2; ++h) {
             const int ni = n0 + u, j = c0 + wc + ni * 8 + tq * 2 + h;
             ok[u][h] = i < rows && j < cols && (acc.re[mi][ni][h] != 0.0 || acc.im[mi][ni][h] != 0.0);
-            if (ok[u][h]) old[u][h] = out[i + (size_t)j * ldo];
+            if (ok[u][h]) old[u][h] = PF ? Tt[j - c0][i - r0] : out[i + (size_t)j * ldo];
           }
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -1924,6 +1943,15 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
     return;
   }
   const int t = (L.bmax + 63) / 64;
+  // small eliminated sizes (fine levels): bound by the targets' read-modify-write -> staged target tiles
+  static const int pf_bmax = std::getenv("H2G_SCHUR_PF_BMAX") ? std::atoi(std::getenv("H2G_SCHUR_PF_BMAX")) : 128;
+  if (L.bmax <= pf_bmax) {
+    const size_t sm = sizeof(TileSmem<64, 2>) + 64 * 64 * sizeof(cplx);
+    set_smem((const void*)k_schur<64, true>, sm);
+    k_schur<64, true><<<dim3(ntargets, t * t), 128, sm, s>>>(L, targets, contrib);
+    post_launch("k_schur");
+    return;
+  }
   set_smem((const void*)k_schur<64>, sizeof(Tile128Smem));
   k_schur<64><<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
   post_launch("k_schur");

@@ -201,3 +201,38 @@ def test_vie_stop_override_matches_oracle():
     xo, xg = och.solve(b), gch.solve(b)
     assert rel(xg, xo) <= 10 * 1e-4
     assert A.relative_residual(xg, b) <= 2 * A.relative_residual(xo, b) + 1e-14
+
+
+def test_segmented_fill_and_streamed_chain_equal_resident(monkeypatch):
+    """The large-configuration storage paths on a small input: segmented fill
+    storage (compact cores, H2G_FILL_SEGMENTS) and the chain streamed to pinned
+    host memory segment by segment (H2G_CHAIN_STREAM) run the same arithmetic as
+    the resident layout, so the segmented + streamed chain equals the
+    segmented + resident chain bit for bit, its records download the same, its
+    container file round-trips, and the solve reads it from host memory."""
+    A, _ = vie_problem(16, 0.5, 32, 1e-4)
+    arrays = A.arrays()
+    b = O.rhs(A.n, 21)
+    ctx = h2g.Context.default()
+    out = {}
+    for mode, stream in (("resident", "0"), ("streamed", "1")):
+        monkeypatch.setenv("H2G_FILL_SEGMENTS", "4")
+        monkeypatch.setenv("H2G_CHAIN_STREAM", stream)
+        ctx.clear_plans()
+        G = h2g.H2Matrix.upload(arrays, ctx)
+        ch = h2g.factorize(G, 1e-4)
+        out[mode] = (ch, ch.hash(), ch.solve(b), ch.all_records(), G)
+    monkeypatch.delenv("H2G_FILL_SEGMENTS")
+    monkeypatch.delenv("H2G_CHAIN_STREAM")
+    ctx.clear_plans()
+    assert out["resident"][1] == out["streamed"][1]
+    assert np.array_equal(out["resident"][2], out["streamed"][2])
+    assert out["resident"][3] == out["streamed"][3]
+    ch, G = out["streamed"][0], out["streamed"][4]
+    Q0, L0, U0 = out["resident"][0].record_mats(0, 3)
+    Q1, L1, U1 = ch.record_mats(0, 3)
+    assert np.array_equal(Q0, Q1) and np.array_equal(L0, L1) and np.array_equal(U0, U1)
+    # against the default storage (whole-level full blocks): same mathematics, different summation grouping
+    ref = h2g.factorize(h2g.H2Matrix.upload(arrays, ctx), 1e-4)
+    assert rel(out["streamed"][2], ref.solve(b)) <= 1e-3
+    assert G.relative_residual(out["streamed"][2], b) <= 2 * G.relative_residual(ref.solve(b), b) + 1e-12
