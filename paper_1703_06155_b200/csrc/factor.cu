@@ -110,7 +110,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 
 
-__global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, int p0, cplx* gws) {
+// gH != nullptr: the cluster's Gram columns do not fit its shared memory
+// (blocks beyond ~420 rows); each CTA then keeps its columns in global memory
+// (gH, bmax^2 + 16 bmax per batch slot, L2 resident) and only the vectors in shared.
+__global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, int p0, cplx* gws, cplx* gH) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -130,8 +133,8 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   cplx* H = ws;  // reflectors out (m x m, ld m)
   double* aux = reinterpret_cast<double*>(ws + 2 * bb);
   const int ncl = (m + kHC - 1) / kHC;
-  cplx* Hl = reinterpret_cast<cplx*>(smraw);  // m x ncl local columns (col c = rank + kHC * jl)
-  cplx* vbuf = Hl + (size_t)m * ncl;          // [2][m] reflector broadcast (owner)
+  cplx* Hl = gH ? gH + (size_t)q * (bb + 16 * (size_t)bm) + (size_t)rank * m * ncl : reinterpret_cast<cplx*>(smraw);  // m x ncl local columns (col c = rank + kHC * jl)
+  cplx* vbuf = gH ? reinterpret_cast<cplx*>(smraw) : Hl + (size_t)m * ncl;  // [2][m] reflector broadcast (owner)
   cplx* pbuf = vbuf + 2 * m;                  // [2][m] partial A v over own columns
   cplx* wfull = pbuf + 2 * m;                 // [2][m] reduced tau A v (each CTA its own copy)
   cplx* vv = wfull + 2 * m;                   // local copy of v (+ [m] next v, cluster path)
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
   };
   if (m > 1) {
     // column 0 lives in CTA 0 (Gram reduced and the cluster synchronised above)
-    const cplx* c0 = cl.map_shared_rank(Hl, 0);
+    const cplx* c0 = gH ? gH + (size_t)q * (bb + 16 * (size_t)bm) : cl.map_shared_rank(Hl, 0);
     for (int i = threadIdx.x; i < m; i += blockDim.x) colb[i] = c0[i];
     __syncthreads();
     reflector(0, colb);
@@ -591,6 +594,7 @@ __global__ void __launch_bounds__(256) k_eig1_refine(DevLevel L, const int* batc
 // work arrays in shared memory; eigenvalues closer than 1e-8 ||T|| form a
 // cluster handled by one CTA and Gram-Schmidt'ed against each other), then
 // the back-transformation by the tridiagonalisation reflectors (whole CTA).
+template <int kPer>  // entries of an eigenvector per lane: m <= 32 kPer
 __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl, cplx* gws, int wpc) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int q = blockIdx.x;
@@ -698,7 +702,6 @@ __global__ void __launch_bounds__(256) k_eigvec(DevLevel L, const int* batch_cl,
   // back-transform y = Q z, Q = H_0 ... H_{m-2}: reflectors staged CH at a
   // time in shared memory by the whole CTA (coalesced), then every warp
   // streams its vector through them (lane owns entries lane, lane + 32, ...)
-  constexpr int kPer = 16;  // m <= 512
   constexpr int CH = 8;
   cplx* Hs = reinterpret_cast<cplx*>(dg + (size_t)(2 + 7 * wpc) * m + (((2 + 7 * wpc) * m) & 1));  // [CH][m]
   __shared__ cplx ts[CH];
@@ -815,7 +818,9 @@ __global__ void __launch_bounds__(256) k_eig1b(DevLevel L, const int* batch_cl, 
 // the reflector (one warp), publishes it, one cluster barrier, and every CTA
 // applies it to its own later columns (a warp per column). Same reflector
 // convention and outputs as k_eig1b (Y unit lower trapezoidal, tau).
-__global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_cl, cplx* gws) {
+// gU != nullptr: the local columns live in global memory (blocks too large
+// for the cluster's shared memory, as in k_eig1c).
+__global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_cl, cplx* gws, cplx* gU) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -833,8 +838,8 @@ __global__ void __launch_bounds__(256) k_eig1b_cl(DevLevel L, const int* batch_c
   cplx* Y = ws;
   cplx* tau_g = ws + 2 * bb + 4 * bm + 4 * bb;
   const int ncl = (r + kHC - 1) / kHC;
-  cplx* Ul = reinterpret_cast<cplx*>(smraw);  // m x ncl, local column jl = global rank + kHC jl
-  cplx* pubw = Ul + (size_t)m * ncl;          // [2][m] published reflector (owner), w[0] = 1
+  cplx* Ul = gU ? gU + (size_t)q * (bb + 16 * (size_t)bm) + (size_t)rank * m * ncl : reinterpret_cast<cplx*>(smraw);  // m x ncl, local column jl = global rank + kHC jl
+  cplx* pubw = gU ? reinterpret_cast<cplx*>(smraw) : Ul + (size_t)m * ncl;  // [2][m] published reflector (owner), w[0] = 1
   cplx* wv = pubw + 2 * m;                    // local copy
   __shared__ cplx pubt[2];
   __shared__ cplx s_tk;
@@ -1799,8 +1804,14 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     // spread over 4 or 16 CTAs
     const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : (L.bmax <= 240 ? 8 : kHCmax));
     const int ncl = (L.bmax + kHC - 1) / kHC;
-    const size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 8 + 256;
-    if (smem > kSmemCap) throw std::runtime_error("k_eig1c: block too large for the 16-CTA cluster");
+    size_t smem = (size_t)L.bmax * ncl * sizeof(cplx) + (size_t)L.bmax * sizeof(cplx) * 8 + 256;
+    cplx* gH = nullptr;
+    const char* force_g = std::getenv("H2G_EIG_GLOBAL");  // tests: take the large-block path on small inputs
+    if (smem > kSmemCap || (force_g && std::atoi(force_g) && kHC > 1)) {
+      // too large for the cluster's shared memory: Gram columns in global memory (level scratch, free until k_head)
+      gH = workspace(L, (size_t)nb * ((size_t)L.bmax * L.bmax + 16 * (size_t)L.bmax) * sizeof(cplx));
+      smem = (size_t)L.bmax * sizeof(cplx) * 8 + 256;
+    }
     set_smem((const void*)k_eig1c, smem);
     allow_big_clusters((const void*)k_eig1c);
     cudaLaunchConfig_t cfg = {};
@@ -1815,7 +1826,7 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1c, L, batch_cl, p0, ws);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1c, L, batch_cl, p0, ws, gH);
     if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_eig1c failed: ") + cudaGetErrorString(e));
     post_launch("k_eig1c");
   }
@@ -1831,15 +1842,20 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
   }
   phase(1);
   if (mmax > 0) {
-    if (mmax > 512) throw std::runtime_error("k_eigvec: complement dimension > 512");
+    if (mmax > 1024) throw std::runtime_error("k_eigvec: complement dimension > 1024");
     // one warp per eigenvector; shared: d, e (2 bmax) + 7 bmax doubles per warp
     // + the staged reflector chunk (8 x bmax complex)
     int wpc = 8;
     auto need = [&](int w) { return (size_t)(2 + 7 * w) * L.bmax * sizeof(double) + 8 * (size_t)L.bmax * sizeof(cplx) + 64; };
     while (wpc > 1 && need(wpc) > kSmemCap) --wpc;
     const size_t vsm = need(wpc);
-    set_smem((const void*)k_eigvec, vsm);
-    k_eigvec<<<dim3(nb, (mmax + wpc - 1) / wpc), 256, vsm, s>>>(L, batch_cl, ws, wpc);
+    if (mmax <= 512) {
+      set_smem((const void*)k_eigvec<16>, vsm);
+      k_eigvec<16><<<dim3(nb, (mmax + wpc - 1) / wpc), 256, vsm, s>>>(L, batch_cl, ws, wpc);
+    } else {
+      set_smem((const void*)k_eigvec<32>, vsm);
+      k_eigvec<32><<<dim3(nb, (mmax + wpc - 1) / wpc), 256, vsm, s>>>(L, batch_cl, ws, wpc);
+    }
     post_launch("k_eigvec");
   }
   phase(2);
@@ -1847,8 +1863,13 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     // QR of the retained vectors on a cluster (columns in distributed shared memory)
     const int kHC = L.bmax <= 64 ? 1 : (L.bmax <= 128 ? 4 : (L.bmax <= 240 ? 8 : kHCmax));
     const int ncl = (L.bmax + kHC - 1) / kHC;
-    const size_t smem = ((size_t)L.bmax * ncl + 3 * (size_t)L.bmax) * sizeof(cplx) + 64;
-    if (smem > kSmemCap) throw std::runtime_error("k_eig1b_cl: block too large for the cluster");
+    size_t smem = ((size_t)L.bmax * ncl + 3 * (size_t)L.bmax) * sizeof(cplx) + 64;
+    cplx* gU = nullptr;
+    const char* force_g = std::getenv("H2G_EIG_GLOBAL");
+    if (smem > kSmemCap || (force_g && std::atoi(force_g) && kHC > 1)) {
+      gU = workspace(L, (size_t)nb * ((size_t)L.bmax * L.bmax + 16 * (size_t)L.bmax) * sizeof(cplx));
+      smem = 3 * (size_t)L.bmax * sizeof(cplx) + 64;
+    }
     set_smem((const void*)k_eig1b_cl, smem);
     allow_big_clusters((const void*)k_eig1b_cl);
     cudaLaunchConfig_t cfg = {};
@@ -1863,11 +1884,11 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1b_cl, L, batch_cl, ws);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_eig1b_cl, L, batch_cl, ws, gU);
     if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_eig1b_cl failed: ") + cudaGetErrorString(e));
     post_launch("k_eig1b_cl");
   }
-  if (mmax > 512) throw std::runtime_error("k_eig1_apply: complement dimension > 512");
+  if (mmax > 1024) throw std::runtime_error("k_eig1_apply: complement dimension > 1024");
   const dim3 ga(nb, (L.bmax + 7) / 8);
   if (L.bmax <= 128)
     k_eig1_apply<4><<<ga, 256, 0, s>>>(L, batch_cl, ws);
@@ -1875,8 +1896,12 @@ void launch_eig1(const DevLevel& L, const int* batch_cl, int p0, int nb, int mma
     k_eig1_apply<8><<<ga, 256, 0, s>>>(L, batch_cl, ws);
   else if (L.bmax <= 384)
     k_eig1_apply<12><<<ga, 256, 0, s>>>(L, batch_cl, ws);
-  else
+  else if (L.bmax <= 512)
     k_eig1_apply<16><<<ga, 256, 0, s>>>(L, batch_cl, ws);
+  else if (L.bmax <= 768)
+    k_eig1_apply<24><<<ga, 256, 0, s>>>(L, batch_cl, ws);
+  else
+    k_eig1_apply<32><<<ga, 256, 0, s>>>(L, batch_cl, ws);
   post_launch("k_eig1_apply");
 }
 
@@ -1944,7 +1969,7 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
   }
   const int t = (L.bmax + 63) / 64;
   // small eliminated sizes (fine levels): bound by the targets' read-modify-write -> staged target tiles
-  static const int pf_bmax = std::getenv("H2G_SCHUR_PF_BMAX") ? std::atoi(std::getenv("H2G_SCHUR_PF_BMAX")) : 128;
+  static const int pf_bmax = std::getenv("H2G_SCHUR_PF_BMAX") ? std::atoi(std::getenv("H2G_SCHUR_PF_BMAX")) : 0;
   if (L.bmax <= pf_bmax) {
     const size_t sm = sizeof(TileSmem<64, 2>) + 64 * 64 * sizeof(cplx);
     set_smem((const void*)k_schur<64, true>, sm);

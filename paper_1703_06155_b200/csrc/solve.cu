@@ -59,26 +59,42 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
 __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool conjA, const cplx* x, long long ldx, cplx* out, long long ldo,
                            bool subtract, cplx* red) {
   if (nrhs >= 4) {
-    // many right-hand sides: thread (row, group of 4 columns), the k loop
-    // serial with 4 independent accumulators per A element (A read once per
-    // column group, coalesced across rows)
-    const int ng = (nrhs + 3) / 4;
-    for (int idx = threadIdx.x; idx < m * ng; idx += blockDim.x) {
-      const int i = idx % m, c0 = (idx / m) * 4, nc = min(4, nrhs - c0);
-      cplx acc[4] = {czero(), czero(), czero(), czero()};
-      for (int p = 0; p < k; ++p) {
-        cplx a = A[i + (size_t)p * lda];
-        if (conjA) a.y = -a.y;
+    // many right-hand sides: the same (row, k-slice) threads, each A element
+    // read once for up to 8 columns (8 accumulators), the k-slices reduced
+    // through shared memory one column at a time
+    for (int c0 = 0; c0 < nrhs; c0 += 8) {
+      const int nc = min(8, nrhs - c0);
+      for (int i0 = 0; i0 < m; i0 += blockDim.x) {
+        const int mm = min(m - i0, (int)blockDim.x);
+        const int G = max(1, (int)blockDim.x / mm);
+        const int t = threadIdx.x, i = t % mm, g = t / mm;
+        cplx acc[8];
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < nc) cfma(acc[c], a, x[p + (size_t)(c0 + c) * ldx]);
-      }
+        for (int c = 0; c < 8; ++c) acc[c] = czero();
+        if (g < G) {
+#pragma unroll 2
+          for (int p = g; p < k; p += G) {
+            cplx a = A[(i0 + i) + (size_t)p * lda];
+            if (conjA) a.y = -a.y;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c < nc) {
-          cplx* o = out + i + (size_t)(c0 + c) * ldo;
-          *o = subtract ? csub(*o, acc[c]) : acc[c];
+            for (int c = 0; c < 8; ++c)
+              if (c < nc) cfma(acc[c], a, x[p + (size_t)(c0 + c) * ldx]);
+          }
         }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c >= nc) break;
+          __syncthreads();
+          if (g < G) red[g * mm + i] = acc[c];
+          __syncthreads();
+          if (t < mm) {
+            cplx s2 = red[t];
+            for (int q = 1; q < G; ++q) s2 = cadd(s2, red[q * mm + t]);
+            cplx* o = out + (i0 + t) + (size_t)(c0 + c) * ldo;
+            *o = subtract ? csub(*o, s2) : s2;
+          }
+        }
+      }
     }
     __syncthreads();
     return;
@@ -185,30 +201,46 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
     base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
   }
   if (nrhs >= 4) {
-    // many right-hand sides: thread (row, group of 4 columns), contributions
-    // and their columns serial, 4 accumulators per Lbar element
-    const int ng = (nrhs + 3) / 4;
-    for (int idx = threadIdx.x; idx < rows * ng; idx += blockDim.x) {
-      const int i = idx % rows, c0 = (idx / rows) * 4, nc = min(4, nrhs - c0);
-      cplx acc[4] = {czero(), czero(), czero(), czero()};
-      for (int ci = tg.c0; ci < tg.c1; ++ci) {
-        const SolveContribD cb = contrib[ci];
-        const int e = S.bsz[cb.m] - S.kfin[cb.m];
-        const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i;
-        const cplx* h = y + S.pos[cb.m];
-        for (int p = 0; p < e; ++p) {
-          const cplx mv = M[(size_t)p * rows];
+    // many right-hand sides: the same (row, k-slice) threads with up to 8
+    // columns per Lbar element, k-slices reduced one column at a time
+    for (int c0 = 0; c0 < nrhs; c0 += 8) {
+      const int nc = min(8, nrhs - c0);
+      for (int i0 = 0; i0 < rows; i0 += blockDim.x) {
+        const int mm = min(rows - i0, (int)blockDim.x);
+        const int G = max(1, (int)blockDim.x / mm);
+        const int t = threadIdx.x, i = t % mm, g = t / mm;
+        cplx acc[8];
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (c < nc) cfma(acc[c], mv, h[p + (size_t)(c0 + c) * ldy]);
+        for (int c = 0; c < 8; ++c) acc[c] = czero();
+        if (g < G) {
+          for (int ci = tg.c0; ci < tg.c1; ++ci) {
+            const SolveContribD cb = contrib[ci];
+            const int e = S.bsz[cb.m] - S.kfin[cb.m];
+            const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i0 + i;
+            const cplx* h = y + S.pos[cb.m] + (size_t)c0 * ldy;
+#pragma unroll 2
+            for (int p = g; p < e; p += G) {
+              const cplx mv = M[(size_t)p * rows];
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                if (c < nc) cfma(acc[c], mv, h[p + (size_t)c * ldy]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c >= nc) break;
+          __syncthreads();
+          if (g < G) red[g * mm + i] = acc[c];
+          __syncthreads();
+          if (t < mm) {
+            cplx s2 = red[t];
+            for (int q = 1; q < G; ++q) s2 = cadd(s2, red[q * mm + t]);
+            cplx* o = y + base + i0 + t + (size_t)(c0 + c) * ldy;
+            *o = csub(*o, s2);
+          }
         }
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c < nc) {
-          cplx* o = y + base + i + (size_t)(c0 + c) * ldy;
-          *o = csub(*o, acc[c]);
-        }
     }
     __syncthreads();
     return;

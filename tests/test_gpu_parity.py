@@ -236,3 +236,16 @@ def test_segmented_fill_and_streamed_chain_equal_resident(monkeypatch):
     ref = h2g.factorize(h2g.H2Matrix.upload(arrays, ctx), 1e-4)
     assert rel(out["streamed"][2], ref.solve(b)) <= 1e-3
     assert G.relative_residual(out["streamed"][2], b) <= 2 * G.relative_residual(ref.solve(b), b) + 1e-12
+
+
+def test_large_block_eigensolver_path_is_bitwise_the_shared_memory_one(monkeypatch):
+    """Blocks beyond ~420 rows keep the cluster's Gram columns in global memory
+    (k_eig1c, reached at config 3's coarse levels); forced here on config 1's
+    geometry, it must reproduce the shared-memory path bit for bit."""
+    A, _ = vie_problem(16, 0.5, 32, 1e-4)
+    G = upload(A)
+    ref = h2g.factorize(G, 1e-4)
+    monkeypatch.setenv("H2G_EIG_GLOBAL", "1")
+    alt = h2g.factorize(G, 1e-4)
+    monkeypatch.delenv("H2G_EIG_GLOBAL")
+    assert ref.hash() == alt.hash()
