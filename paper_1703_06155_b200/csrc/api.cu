@@ -456,6 +456,17 @@ struct ChainLevelHost {
   size_t chain_bytes() const { return harena.p ? harena.bytes : arena.bytes; }
   DBuf meta;                 // packed int / offset arrays
   DBuf solve_meta;           // streamed level: the compact chain offsets the solve reads
+  // streamed level until the end of the factorization: its Qt block and one
+  // compact chunk per segment (on the device while HBM has room, else pinned
+  // host memory), joined into one arena by assemble_streamed_chains
+  struct Chunk {
+    DBuf d;
+    HBuf h;
+    long long begin = 0, len = 0;  // compact element range
+  };
+  std::vector<Chunk> chunks;
+  DBuf qchunk;
+  long long compact_elems = 0;
   SolveLevel sl{};
   std::vector<int> batch_ptr, batch_maxc;
   const int* d_batch = nullptr;
@@ -1325,12 +1336,27 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
       M->dense.release();
       return true;
     };
+    // one device chunk of a finished streamed level to pinned host memory
+    auto offload_chunk = [&]() -> bool {
+      for (auto& X : C->levels)
+        for (auto& ck : X->chunks)
+          if (ck.d.p) {
+            ck.h.alloc(ck.d.bytes);
+            CK(cudaMemcpyAsync(ck.h.p, ck.d.p, ck.d.bytes, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            offloaded += ck.d.bytes;
+            ck.d.release();
+            return true;
+          }
+      return false;
+    };
     BlockCache::get().set_spill(st, [&]() -> bool {
       for (auto& X : C->levels)
         if (X->arena.p) {
           offload_chain(*X);
           return true;
         }
+      if (offload_chunk()) return true;
       return offload_dense();
     });
     auto ensure = [&](size_t need, ChainLevelHost* extra) {
@@ -1341,6 +1367,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         if (BlockCache::get().headroom() >= need + kMargin) return;
         if (X->arena.p) offload_chain(*X), BlockCache::get().trim();
       }
+      while (BlockCache::get().headroom() < need + kMargin && offload_chunk()) BlockCache::get().trim();
       if (extra && extra->arena.p && BlockCache::get().headroom() < need + kMargin) offload_chain(*extra), BlockCache::get().trim();
       if (BlockCache::get().headroom() < need + kMargin && offload_dense()) BlockCache::get().trim();
     };
@@ -1427,7 +1454,6 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         std::vector<long long> lQt(Qt_off), lL11(L11_off), lU11(U11_off), lLinv(Linv_off), lUinv(Uinv_off), lLself(Lself_off),
             lUself(Uself_off), lLbar(Lbar_off), lUbar(Ubar_off);
         const long long top_logical = top;
-        std::vector<std::vector<char>> seg_host;  // streamed: compact copy of every finished segment (pageable until the level ends)
         long long compact_top = qtot;
         if (streamed) {
           std::vector<int> seg_of(nl, 0);
@@ -1486,7 +1512,6 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         ensure((size_t)(std::max<long long>(top, 1) + std::max<long long>(ltop, 1) + (long long)nl * bb) * 16 + (size_t(4) << 30), nullptr);
         CL->arena.alloc(std::max<long long>(top, 1) * 16, st);
         if (streamed) {
-          seg_host.resize(cur.front.K);
           if (verbose)
             std::fprintf(stderr, "[h2g] level %d: chain streamed to host memory: %.2f GB on the device (Qt %.2f GB + 2 x %.2f GB) instead of %.2f GB\n", l,
                          top * 16 / 1e9, qtot * 16 / 1e9, ring_half * 16 / 1e9, top_logical * 16 / 1e9);
@@ -1911,14 +1936,22 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
               }
             const long long clen = compact_top - seg0;
             if (clen > 0) {
-              DBuf cbuf, dmv;
-              cbuf.alloc((size_t)clen * 16, st);
-              for (auto& d : mv) d.dst = cbuf.as<cplx>() + reinterpret_cast<long long>(d.dst) / 16;
+              ChainLevelHost::Chunk ck;
+              ck.begin = seg0, ck.len = clen;
+              cplx* dstb;
+              if (BlockCache::get().headroom() >= (size_t)clen * 16 + kMargin) {
+                ck.d.alloc((size_t)clen * 16, st);
+                dstb = ck.d.as<cplx>();
+              } else {
+                ck.h.alloc((size_t)clen * 16);  // HBM is short: the chunk goes to pinned host memory (mapped, written by the kernel)
+                dstb = ck.h.as<cplx>();
+              }
+              DBuf dmv;
+              for (auto& d : mv) d.dst = dstb + reinterpret_cast<long long>(d.dst) / 16;
               upload(dmv, mv, st);
               launch_move(dmv.as<MoveDesc>(), static_cast<int>(mv.size()), st);
-              seg_host[sg].resize((size_t)clen * 16);
-              CK(cudaMemcpyAsync(seg_host[sg].data(), cbuf.p, (size_t)clen * 16, cudaMemcpyDeviceToHost, st));
               CK(cudaStreamSynchronize(st));
+              CL->chunks.push_back(std::move(ck));
               ++launches;
             }
           }
@@ -2191,30 +2224,20 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
 
         mark("kfin read back");
         if (streamed) {
-          // the level's chain in pinned host memory at its final size: Qt from
-          // the device, then the compact segments; the device copy goes away
-          CL->harena.alloc((size_t)std::max<long long>(compact_top, 1) * 16);
-          CK(cudaMemcpyAsync(CL->harena.p, CL->arena.p, (size_t)qtot * 16, cudaMemcpyDeviceToHost, st));
-          {
-            std::vector<std::thread> th;
-            size_t o = (size_t)qtot * 16;
-            for (auto& sgv : seg_host) {
-              char* dst = static_cast<char*>(CL->harena.p) + o;
-              const std::vector<char>* src = &sgv;
-              th.emplace_back([dst, src] {
-                if (!src->empty()) std::memcpy(dst, src->data(), src->size());
-              });
-              o += sgv.size();
-            }
-            for (auto& t2 : th) t2.join();
-          }
+          // the halves are dead: Qt moves to its own buffer, the level's chain is
+          // its compact chunks until the end of the factorization
+          CL->qchunk.alloc((size_t)std::max<long long>(qtot, 1) * 16, st);
+          CK(cudaMemcpyAsync(CL->qchunk.p, CL->arena.p, (size_t)qtot * 16, cudaMemcpyDeviceToDevice, st));
           CK(cudaStreamSynchronize(st));
-          seg_host.clear();
-          seg_host.shrink_to_fit();
-          offloaded += CL->harena.bytes;
           CL->arena.release();
-          if (verbose)
-            std::fprintf(stderr, "[h2g] level %d: chain %.2f GB in host memory (bound %.2f GB)\n", l, compact_top * 16 / 1e9, top_logical * 16 / 1e9);
+          CL->compact_elems = compact_top;
+          if (verbose) {
+            double onhost = 0.0;
+            for (const auto& ck : CL->chunks)
+              if (ck.h.p) onhost += (double)ck.len * 16;
+            std::fprintf(stderr, "[h2g] level %d: chain %.2f GB at its final size (bound %.2f GB), %.2f GB of it in host memory\n", l,
+                         compact_top * 16 / 1e9, top_logical * 16 / 1e9, onhost / 1e9);
+          }
         }
         // level scratch is dead once the last batch has drained (keeps the
         // merge's peak memory down at config 3)
@@ -2415,7 +2438,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           ps.upload(CL->solve_meta, st);
           CK(cudaStreamSynchronize(st));
           const DBuf& sm2 = CL->solve_meta;
-          SL.chain = CL->harena.as<cplx>();
+          SL.chain = nullptr;  // set by assemble_streamed_chains at the end of the factorization
           SL.Qt_off = at<long long>(sm2, q_Qt);
           SL.L11_off = at<long long>(sm2, q_L11);
           SL.U11_off = at<long long>(sm2, q_U11);
@@ -2782,6 +2805,63 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         C->storage_bytes += 2 * 16 * (size_t)nroot * nroot;
         C->solve_bytes += 16.0 * (double)nroot * nroot;
       }
+    }
+    // ---- the chain returns to HBM: with the level pools gone, levels that
+    // were streamed or offloaded to host memory move back while they fit
+    // (coarsest first), so the solve reads them at HBM speed
+    {
+      cur.D.release();
+      cur.F.release();
+      cur.V0.release();
+      cur.Vp.release();
+      cur.fex.release();
+      // streamed levels: Qt block and chunks joined into one arena (HBM if it fits, else pinned host memory)
+      for (auto it = C->levels.rbegin(); it != C->levels.rend(); ++it) {
+        ChainLevelHost& X = **it;
+        if (X.compact_elems == 0 || X.arena.p || X.harena.p) continue;
+        CK(cudaStreamSynchronize(st));
+        BlockCache::get().trim();
+        const size_t bytes = (size_t)X.compact_elems * 16;
+        char* base;
+        if (BlockCache::get().headroom() >= bytes + (kMargin >> 2)) {
+          X.arena.alloc(bytes, st);
+          base = static_cast<char*>(X.arena.p);
+        } else {
+          X.harena.alloc(bytes);
+          base = static_cast<char*>(X.harena.p);
+        }
+        CK(cudaMemcpyAsync(base, X.qchunk.p, X.qchunk.bytes, cudaMemcpyDefault, st));
+        for (auto& ck : X.chunks)
+          CK(cudaMemcpyAsync(base + (size_t)ck.begin * 16, ck.d.p ? ck.d.p : ck.h.p, (size_t)ck.len * 16, cudaMemcpyDefault, st));
+        CK(cudaStreamSynchronize(st));
+        X.chunks.clear();
+        X.qchunk.release();
+        X.sl.chain = reinterpret_cast<cplx*>(base);
+      }
+      double back = 0.0, kept = 0.0;
+      bool synced = false;
+      for (auto it = C->levels.rbegin(); it != C->levels.rend(); ++it) {
+        ChainLevelHost& X = **it;
+        if (!X.harena.p || X.arena.p) continue;
+        if (!synced) {
+          CK(cudaStreamSynchronize(st));
+          BlockCache::get().trim();
+          synced = true;
+        }
+        const size_t bytes = X.harena.bytes;
+        if (BlockCache::get().headroom() < bytes + kMargin) {
+          kept += bytes;
+          continue;
+        }
+        X.arena.alloc(bytes, st);
+        CK(cudaMemcpyAsync(X.arena.p, X.harena.p, bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        X.sl.chain = X.arena.as<cplx>();
+        X.harena.release();
+        back += bytes;
+      }
+      if (verbose && (back > 0 || kept > 0))
+        std::fprintf(stderr, "[h2g] chain levels moved back to HBM: %.2f GB; left in host memory: %.2f GB\n", back / 1e9, kept / 1e9);
     }
     CK(cudaEventRecord(ctx->ev1, st));
     CK(cudaEventSynchronize(ctx->ev1));
