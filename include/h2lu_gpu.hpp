@@ -175,6 +175,27 @@ inline FactorChain factorize(const H2Matrix& A, double eps_fill_in, std::optiona
   return FactorChain(c, A.n(), A.ctx());
 }
 
+// factorize run by one process per GPU (h2g_factorize_dist: the north_star's
+// subtree partition). `exchange(buf, offsets, nranks)` must all-gather the
+// per-rank parts of the device buffer (ncclBroadcast per part inside one
+// group) and return 0; every rank gets the complete chain.
+using Exchange = std::function<int(void* device_buf, const int64_t* offsets, int nranks)>;
+inline FactorChain factorize_dist(const H2Matrix& A, double eps_fill_in, int rank, int nranks, const Exchange& exchange,
+                                  std::optional<int> stop_level_override = std::nullopt) {
+  h2g_dist d{};
+  d.rank = rank;
+  d.nranks = nranks;
+  d.user = const_cast<Exchange*>(&exchange);
+  d.exchange = [](void* u, void* buf, const int64_t* off, int32_t n) -> int {
+    auto* f = static_cast<Exchange*>(u);
+    return *f ? (*f)(buf, off, n) : 1;
+  };
+  h2g_error e{};
+  h2g_chain* c = nullptr;
+  check(h2g_factorize_dist(A.ctx().get(), A.get(), eps_fill_in, stop_level_override.value_or(-1), &d, &c, &e), e);
+  return FactorChain(c, A.n(), A.ctx());
+}
+
 // factorize(A, eps, stop, hooks) (factorization.hpp:600-601): the device in
 // debug mode (reference order, one cluster per step).
 inline FactorChain factorize(const H2Matrix& A, double eps_fill_in, std::optional<int> stop_level_override, const FactorizeHooks* hooks) {

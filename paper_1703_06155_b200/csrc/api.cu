@@ -726,7 +726,7 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
     for (int q = batch_ptr[b]; q < batch_ptr[b + 1]; ++q) bat[batch_cl[q]] = b;
   // records with large blocks: the rotation is cut into row slabs (32 rows of
   // Qt^H forward, 64 rows of conj(Qt) backward), each its own work item
-  static const int split_min = std::getenv("H2G_SOLVE_SPLIT") ? std::atoi(std::getenv("H2G_SOLVE_SPLIT")) : 128;
+  static const int split_min = std::getenv("H2G_SOLVE_SPLIT") ? std::atoi(std::getenv("H2G_SOLVE_SPLIT")) : 96;
   const int kSlabBase = 1 << 30;
   std::vector<int> rec_ns_f(nl, 0), rec_ns_b(nl, 0);
   if (split_min > 0)

@@ -989,7 +989,8 @@ __device__ __forceinline__ void schur_pipe_dmma(Acc64& acc, TileSmem<64, NST>& S
 #pragma unroll
   for (int q = 0; q < NST - 1; ++q) issue();
   for (int s = 0; s < total; ++s) {
-    if constexpr (NST == 3) asm volatile("cp.async.wait_group 1;");
+    if constexpr (NST == 4) asm volatile("cp.async.wait_group 2;");
+    else if constexpr (NST == 3) asm volatile("cp.async.wait_group 1;");
     else asm volatile("cp.async.wait_group 0;");
     __syncthreads();
     issue();

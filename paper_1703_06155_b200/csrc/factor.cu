@@ -1329,11 +1329,11 @@ __global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch
 // tile is fetched into shared memory by cp.async at the start (64 KB in flight
 // per CTA while the contribution tables and panels load) and the epilogue
 // subtracts from the staged copy; two CTAs per SM instead of three.
-template <int TM, bool PF = false>
+template <int TM, bool PF = false, int NSTAGE = 3>
 __global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
   constexpr int RM = TM / 8, RN = TM / 16;  // DFMA micro-tile (TM < 64)
   extern __shared__ __align__(16) unsigned char tsm[];
-  using Smem = TileSmem<TM, PF ? 2 : 3>;
+  using Smem = TileSmem<TM, PF ? 2 : NSTAGE>;
   Smem& S = *reinterpret_cast<Smem*>(tsm);
   cplx(*Tt)[TM] = reinterpret_cast<cplx(*)[TM]>(tsm + sizeof(Smem));  // PF: target tile, [column][row]
   const SchurTargetD tg = targets[blockIdx.x];
@@ -1423,7 +1423,7 @@ __global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const Sch
     // all contributions of the target through one load pipeline (tables of
     // 16 panels resolved by 16 threads in parallel)
     __shared__ SchurPanel tab[16];
-    __shared__ int s_kv[3], s_touched;
+    __shared__ int s_kv[4], s_touched;
     if (threadIdx.x == 0) s_touched = 0;
     for (int cbase = tg.c0; cbase < tg.c1; cbase += 16) {
       const int nc = min(16, tg.c1 - cbase);
@@ -1959,11 +1959,13 @@ void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
 
 void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
   if (ntargets <= 0) return;
-  if (L.bmax <= 32) {
+  static const int t32_bmax = std::getenv("H2G_SCHUR_T32_BMAX") ? std::atoi(std::getenv("H2G_SCHUR_T32_BMAX")) : 32;
+  if (L.bmax <= t32_bmax) {
     // small blocks (leaf levels, e of a few columns): 32 x 32 DFMA tiles, the
     // target read-modify-write dominates and a 64 x 64 tensor tile would be 3/4 padding
+    const int t32 = (L.bmax + 31) / 32;
     set_smem((const void*)k_schur<32>, sizeof(TileSmem<32>));
-    k_schur<32><<<dim3(ntargets, 1), 128, sizeof(TileSmem<32>), s>>>(L, targets, contrib);
+    k_schur<32><<<dim3(ntargets, t32 * t32), 128, sizeof(TileSmem<32>), s>>>(L, targets, contrib);
     post_launch("k_schur");
     return;
   }
@@ -1974,6 +1976,13 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
     const size_t sm = sizeof(TileSmem<64, 2>) + 64 * 64 * sizeof(cplx);
     set_smem((const void*)k_schur<64, true>, sm);
     k_schur<64, true><<<dim3(ntargets, t * t), 128, sm, s>>>(L, targets, contrib);
+    post_launch("k_schur");
+    return;
+  }
+  static const int nst = std::getenv("H2G_SCHUR_STAGES") ? std::atoi(std::getenv("H2G_SCHUR_STAGES")) : 3;
+  if (nst == 4) {
+    set_smem((const void*)k_schur<64, false, 4>, sizeof(TileSmem<64, 4>));
+    k_schur<64, false, 4><<<dim3(ntargets, t * t), 128, sizeof(TileSmem<64, 4>), s>>>(L, targets, contrib);
     post_launch("k_schur");
     return;
   }

@@ -23,3 +23,16 @@ perm = A.perm()
 rows = np.arange(0, A.n, 37, dtype=np.int64)
 r = h2g.sampled_dense_residual(pts[perm], K, x, b, rows)
 print("levels", [(l["level"], l["rank_sum_after"]) for l in ch.levels()], "root", ch.root_size, "residual", A.relative_residual(x, b), "dense rows", r)
+# the large-configuration storage paths and the SUBTREE order on the same input
+os.environ["H2G_FILL_SEGMENTS"] = "4"
+os.environ["H2G_CHAIN_STREAM"] = "1"
+os.environ["H2G_EIG_GLOBAL"] = "1"
+A.ctx.clear_plans()
+A2 = h2g.H2Matrix.build(pts, 32, 1.0, K, 1e-6)
+ch2 = h2g.factorize(A2, 1e-6)
+x2 = ch2.solve(b)
+for k in ("H2G_FILL_SEGMENTS", "H2G_CHAIN_STREAM", "H2G_EIG_GLOBAL"):
+    del os.environ[k]
+ch3 = h2g.factorize(A2, 1e-6, schedule="subtree")
+x3 = ch3.solve(b)
+print("segmented + streamed residual", A.relative_residual(x2, b), "subtree residual", A.relative_residual(x3, b))

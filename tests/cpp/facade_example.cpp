@@ -49,6 +49,16 @@ int main() {
     FactorChain ch2 = factorize(A, 1e-8, std::nullopt, &hk);
     std::printf("facade: kept chain solves %d, hooked steps %d\n", (int)kept_ok, steps);
     if (!kept_ok || solve(ch2, b) != x) return 4;
+    // multi-GPU entry point with a single rank (no exchange happens): the
+    // SUBTREE order; a wrong rank count maps to InvalidInputError
+    FactorChain ch3 = factorize_dist(A, 1e-8, 0, 1, Exchange());
+    bool bad_ranks = false;
+    try {
+      factorize_dist(A, 1e-8, 0, 3, Exchange([](void*, const int64_t*, int) { return 0; }));
+    } catch (const InvalidInputError&) {
+      bad_ranks = true;
+    }
+    if (!bad_ranks || solve(ch3, b).size() != x.size()) return 5;
     // singular pivot -> SingularPivotError with the root's cluster -1
     std::vector<cxd> Z(n * n, cxd(0.0));
     d.dense_data = reinterpret_cast<const double*>(Z.data());
