@@ -403,7 +403,7 @@ def main():
         else:
             roof = {"kernel": "k_schur (step 3c Schur scatter)", "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        traffic, tsrc = None, None
+        traffic, tsrc, alone = None, None, None
         import glob
         for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_schur_traffic.json"))):
             try:
@@ -412,10 +412,16 @@ def main():
                 continue
             if tj.get("config") == args.config and tj.get("launches") == sch["launches"]:
                 traffic, tsrc = tj["traffic_per_launch"], os.path.relpath(f, ROOT) + " (ncu dram__bytes_read+write per k_schur launch, same launch list)"
+                if tj.get("serialised_ms"):
+                    # not a live number: the committed ncu launch list, every k_schur launch alone on the GPU (no overlap with the
+                    # chain kernels of the other stream, cold caches); explains the gap to the live event time above
+                    alone = {"ms": tj["serialised_ms"], "tflops": ex_flops / (tj["serialised_ms"] / 1e3) / 1e12,
+                             "frac": ex_flops / (tj["serialised_ms"] / 1e3) / 1e12 / peak_tf, "source": os.path.relpath(f, ROOT),
+                             "note": "profiler-derived (ncu gpu__time_duration.sum summed over the launches of one factorize), not measured in this run"}
         roof.update({"basis": "executed work: the products k_schur computes (rows/columns of clusters eliminated in an earlier batch "
                               "are exact zeros and are skipped, factorization.hpp:431-439); flops_per_launch x launches / k_schur event time",
                      "flops_per_launch": ex_flops / nl, "bytes_per_launch": ex_bytes / nl,
-                     "traffic": traffic, "traffic_source": tsrc, "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / nl,
+                     "traffic": traffic, "traffic_source": tsrc, "kernel_alone": alone, "launches": sch["launches"], "avg_launch_us": 1e3 * sch["ms"] / nl,
                      "share_of_factorize": sch["ms"] / max(prof_total, 1e-9),
                      "algorithmic": {"flops": sch["flops"], "tflops": sch["flops"] / t_s / 1e12, "frac": sch["flops"] / t_s / 1e12 / peak_tf,
                                      "note": "SURVEY 8d count (full b_j x e x b_c products, as the reference's GEMMs execute them, "

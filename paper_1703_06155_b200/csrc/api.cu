@@ -735,6 +735,15 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
         rec_ns_f[t] = std::min(64, (CL.bsz[t] + 31) / 32);
         rec_ns_b[t] = std::min(64, (CL.bsz[t] + 63) / 64);
       }
+  // fine levels: the forward updates of a not-yet-processed segment are
+  // pulled by its own record (one dependent item per batch on the chain
+  // instead of two, ~50 times fewer items); large blocks keep one item per
+  // (segment, batch), which spreads the Lbar traffic over the CTAs
+  static const int pull_max = std::getenv("H2G_SOLVE_PULL") ? std::atoi(std::getenv("H2G_SOLVE_PULL")) : 0;  // measured: no gain (the late record then applies ~50 updates in a row)
+  int bmax_l = 1;
+  for (int t = 0; t < nl; ++t) bmax_l = std::max(bmax_l, CL.bsz[t]);
+  const int pull = (bmax_l <= pull_max && (split_min <= 0 || bmax_l < split_min)) ? 1 : 0;
+  std::vector<std::vector<int>> rec_fs_l(pull ? nl : 0);
   // forward
   std::vector<int> f_items, rec_widx(nl, 0), fs_widx(fs.size(), 0), wcount(nl, 0);
   for (int b = 0; b < nbat; ++b) {
@@ -748,10 +757,19 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
       f_items.push_back(t);
     }
     for (int f = fs_ptr[b]; f < fs_ptr[b + 1]; ++f) {
+      if (pull && fs[f].seg >= 0 && bat[fs[f].seg] > b) {
+        rec_fs_l[fs[f].seg].push_back(f);  // segment not processed yet: applied by its own record
+        continue;
+      }
       const int sg = fs[f].seg >= 0 ? fs[f].seg : -1 - fs[f].seg;
       fs_widx[f] = wcount[sg]++;
       f_items.push_back(-1 - f);
     }
+  }
+  std::vector<int> rec_fs_ptr(nl + 1, 0), rec_fs;
+  for (int t = 0; t < nl; ++t) {
+    if (pull) rec_fs.insert(rec_fs.end(), rec_fs_l[t].begin(), rec_fs_l[t].end());
+    rec_fs_ptr[t + 1] = static_cast<int>(rec_fs.size());
   }
   // backward: per record its C entries then the self block
   std::vector<int> b_items, slot_m, slot_c, rec_slot0(nl, 0), rec_nslot(nl, 0), reader_need(nl, 0);
@@ -788,12 +806,12 @@ void build_flow(ChainLevelHost& CL, int nl, const std::vector<int>& batch_ptr, c
   Packer pk;
   const size_t o_fi = pk.add(f_items), o_rw = pk.add(rec_widx), o_fw = pk.add(fs_widx), o_bi = pk.add(b_items), o_sm = pk.add(slot_m),
                o_sc = pk.add(slot_c), o_sf = pk.add(slot_final), o_so = pk.add(slot_off), o_r0 = pk.add(rec_slot0), o_rn = pk.add(rec_nslot),
-               o_rd = pk.add(reader_need), o_nf = pk.add(rec_ns_f), o_nb = pk.add(rec_ns_b);
+               o_rd = pk.add(reader_need), o_nf = pk.add(rec_ns_f), o_nb = pk.add(rec_ns_b), o_fp = pk.add(rec_fs_ptr), o_ff = pk.add(rec_fs);
   pk.upload(CL.flow_meta, st);
   const DBuf& m = CL.flow_meta;
   CL.flow = SolveFlow{(int)f_items.size(), at<int>(m, o_fi), at<int>(m, o_rw), at<int>(m, o_fw), (int)b_items.size(), at<int>(m, o_bi),
                       at<int>(m, o_sm), at<int>(m, o_sc), at<unsigned char>(m, o_sf), at<long long>(m, o_so), at<int>(m, o_r0), at<int>(m, o_rn),
-                      at<int>(m, o_rd), at<int>(m, o_nf), at<int>(m, o_nb)};
+                      at<int>(m, o_rd), at<int>(m, o_nf), at<int>(m, o_nb), pull, at<int>(m, o_fp), at<int>(m, o_ff)};
   CL.flow_part = (size_t)std::max<long long>(poff, 1);
 }
 

@@ -458,6 +458,14 @@ __device__ __forceinline__ void publish(int* p, int v) {
   if (threadIdx.x == 0) st_release(p, v);
 }
 
+// The chain data of an item (static) is pulled into L2 while the item still
+// waits for its inputs, so the dependent part after the wait reads it at L2
+// latency: one prefetch per 128-byte line, spread over the CTA.
+__device__ __forceinline__ void cta_prefetch_l2(const void* p, size_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  for (size_t o = (size_t)threadIdx.x * 128; o < bytes; o += (size_t)blockDim.x * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
 // Records with large blocks are split: the b x b rotation, which sits on the
 // dependency chain, is cut into row slabs handed to different CTAs (item code
 // kSlabBase + 64 t + slab); the record's own item then only applies the
@@ -483,6 +491,10 @@ __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, Sol
     if (code >= kSlabBase) {
       // slab of a split record's rotation: reads the segment once its earlier writers are done
       const int t = (code - kSlabBase) >> 6, sl = (code - kSlabBase) & 63, w = F.rec_widx[t];
+      {
+        const int b = S.bsz[t], ns = F.rec_ns_f[t], rows = (b + ns - 1) / ns, r0 = sl * rows;
+        if (r0 < b) cta_prefetch_l2(S.chain + S.Qt_off[t] + (size_t)r0 * b, (size_t)min(rows, b - r0) * b * sizeof(cplx));
+      }
       if (threadIdx.x == 0) s_ok = wait_ge(seg + t, w, fail);
       acquire_all(seg + t);
       if (!s_ok) return;
@@ -495,6 +507,26 @@ __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, Sol
       }
     } else if (code >= 0) {
       const int t = code, w = F.rec_widx[t], ns = F.rec_ns_f[t];
+      {
+        const int b = S.bsz[t], e = b - S.kfin[t];
+        if (!ns) cta_prefetch_l2(S.chain + S.Qt_off[t], (size_t)b * b * sizeof(cplx));
+        if (e > 0) cta_prefetch_l2(S.chain + (explicit_inv ? S.Linv_off[t] : S.L11_off[t]), (size_t)e * e * sizeof(cplx));
+      }
+      if (F.pull) {
+        // the updates of the earlier neighbours, applied here in the same
+        // (batch) order the per-segment items would apply them
+        for (int u = F.rec_fs_ptr[t]; u < F.rec_fs_ptr[t + 1]; ++u) {
+          const SolveTargetD tg = P.fs[F.rec_fs[u]];
+          if (threadIdx.x == 0)
+            for (int ci = tg.c0; ci < tg.c1 && s_ok; ++ci) {
+              const int m = P.fc[ci].m;
+              s_ok = wait_ge(seg + m, F.rec_widx[m] + 1, fail);
+            }
+          acquire_all(seg + t);
+          if (!s_ok) return;
+          fwd_lbar_body(S, tg, P.fc, y, ldy, nrhs, reinterpret_cast<cplx*>(smraw));
+        }
+      }
       if (threadIdx.x == 0) s_ok = ns ? wait_ge(slab_done + t, ns, fail) : wait_ge(seg + t, w, fail);
       acquire_all(ns ? slab_done + t : seg + t);
       if (!s_ok) return;
@@ -504,6 +536,13 @@ __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, Sol
       const int f = -1 - code;
       const SolveTargetD tg = P.fs[f];
       const int sg = tg.seg >= 0 ? tg.seg : -1 - tg.seg;
+      {
+        const int rows = tg.seg >= 0 ? S.bsz[sg] : S.kfin[sg];
+        for (int ci = tg.c0; ci < tg.c1; ++ci) {
+          const SolveContribD cb = P.fc[ci];
+          cta_prefetch_l2(S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]), (size_t)rows * (S.bsz[cb.m] - S.kfin[cb.m]) * sizeof(cplx));
+        }
+      }
       if (threadIdx.x == 0) {
         for (int ci = tg.c0; ci < tg.c1 && s_ok; ++ci) {
           const int m = P.fc[ci].m;
@@ -543,7 +582,7 @@ __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx
     const int code = F.b_items[it];
     if (code >= kSlabBase) {
       const int m = (code - kSlabBase) >> 6, sl = (code - kSlabBase) & 63;
-      if (threadIdx.x == 0) s_ok = wait_ge(head_done + m, 1, fail);
+      if (threadIdx.x == 0) s_ok = wait_ge(head_done + m, 1, fail);  // (row slabs of Qt are strided: no prefetch)
       acquire_all(head_done + m);
       if (!s_ok) return;
       bwd_slab_body(S, m, sl, F.rec_ns_b[m], y, ldy, nrhs, tmp, smraw);
@@ -555,6 +594,11 @@ __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx
       }
     } else if (code >= 0) {
       const int m = code;
+      {
+        const int b = S.bsz[m], e2 = b - S.kfin[m];
+        if (e2 > 0) cta_prefetch_l2(S.chain + (explicit_inv ? S.Uinv_off[m] : S.U11_off[m]), (size_t)e2 * e2 * sizeof(cplx));
+        if (!F.rec_ns_b[m]) cta_prefetch_l2(S.chain + S.Qt_off[m], (size_t)b * b * sizeof(cplx));
+      }
       if (threadIdx.x == 0) {
         s_ok = wait_ge(slots_done + m, F.rec_nslot[m], fail);
         if (s_ok) s_ok = wait_ge(reads_done + m, F.reader_need[m], fail);  // nobody still reads the retained part
@@ -570,6 +614,10 @@ __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx
       const int m = F.slot_m[sl], a = F.slot_c[sl];
       const int nC = S.C_ptr[m + 1] - S.C_ptr[m];
       const int c = a >= 0 ? S.C_nb[a] : -1;
+      {
+        const int e2 = S.bsz[m] - S.kfin[m];
+        if (e2 > 0) cta_prefetch_l2(S.chain + (a >= 0 ? S.Ubar_off[a] : S.Uself_off[m]), (size_t)e2 * (a >= 0 ? S.bsz[c] : S.kfin[m]) * sizeof(cplx));
+      }
       if (threadIdx.x == 0 && c >= 0 && F.slot_final[sl]) s_ok = wait_ge(rec_done + c, max(1, F.rec_ns_b[c]), fail);
       acquire_all(rec_done + (c >= 0 ? c : m));
       if (!s_ok) return;

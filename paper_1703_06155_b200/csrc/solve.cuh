@@ -65,6 +65,12 @@ struct SolveFlow {
   // split records (large blocks): number of rotation slabs, 0 = unsplit
   const int* rec_ns_f;
   const int* rec_ns_b;
+  // fine levels (pull != 0): a record applies the updates of its earlier
+  // neighbours to its own segment itself (targets rec_fs[rec_fs_ptr[t] ..],
+  // in batch order) instead of one work item per (segment, batch)
+  int pull;
+  const int* rec_fs_ptr;
+  const int* rec_fs;
 };
 
 // Whole level, all batches, one cooperative launch per direction; part holds
