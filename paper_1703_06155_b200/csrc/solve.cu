@@ -446,16 +446,25 @@ __device__ __forceinline__ bool wait_ge(const int* p, int v, int* fail) {
   }
   return true;
 }
-// after a wait by thread 0: every thread acquires too (fresh view of the data)
-__device__ __forceinline__ void acquire_all(const int* p) {
-  __syncthreads();
-  (void)ld_acquire(p);
-}
-// publish: the block's stores are visible before the counter moves
+// after a wait by thread 0: its acquire load (gpu scope) followed by the block
+// barrier orders the producers' stores before every thread's loads (the
+// consumer half of the CUTLASS semaphore pattern)
+__device__ __forceinline__ void acquire_all(const int*) { __syncthreads(); }
+// publish: the block's stores are visible before the counter moves. The
+// block barrier orders every thread's stores before thread 0's release store,
+// which is cumulative at gpu scope (the CUTLASS semaphore pattern): no
+// per-thread fence.
 __device__ __forceinline__ void publish(int* p, int v) {
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) st_release(p, v);
+}
+// same for a counter incremented by several items
+__device__ __forceinline__ void publish_add(int* p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p, 1);
+  }
 }
 
 // The chain data of an item (static) is pulled into L2 while the item still
@@ -499,12 +508,7 @@ __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, Sol
       acquire_all(seg + t);
       if (!s_ok) return;
       fwd_slab_body(S, t, sl, F.rec_ns_f[t], y, ldy, nrhs, tmp, smraw);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(slab_done + t, 1);
-      }
+      publish_add(slab_done + t);
     } else if (code >= 0) {
       const int t = code, w = F.rec_widx[t], ns = F.rec_ns_f[t];
       {
@@ -586,12 +590,7 @@ __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx
       acquire_all(head_done + m);
       if (!s_ok) return;
       bwd_slab_body(S, m, sl, F.rec_ns_b[m], y, ldy, nrhs, tmp, smraw);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(rec_done + m, 1);
-      }
+      publish_add(rec_done + m);
     } else if (code >= 0) {
       const int m = code;
       {
@@ -622,7 +621,6 @@ __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx
       acquire_all(rec_done + (c >= 0 ? c : m));
       if (!s_ok) return;
       bwd_gather_to(S, m, a >= 0 ? a - S.C_ptr[m] : nC, y, ldy, nrhs, part + (size_t)F.slot_off[sl] * nrhs, reinterpret_cast<cplx*>(smraw));
-      __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
