@@ -287,15 +287,17 @@ struct DBuf {
 // Pinned, device-mapped host memory. Used only when a configuration does not
 // fit in HBM (config 3: the level-12 -> 11 merge cores and the chains of
 // finished levels); kernels read / write it in place over the host link.
-// Process-wide cap on pinned staging memory (H2G_HOST_STAGING_GB, default
-// 96 GB): past it a staging request fails as a device out-of-memory instead
-// of exhausting the host.
+// Process-wide cap on pinned staging memory (H2G_HOST_STAGING_GB; default:
+// host RAM minus 20 GB, at least 75 % of it): past it a staging request fails
+// as a device out-of-memory instead of exhausting the host.
 std::atomic<size_t> g_pinned_bytes{0};
 size_t pinned_cap() {
   static const size_t cap = [] {
     if (const char* e = std::getenv("H2G_HOST_STAGING_GB")) return (size_t)(std::atof(e) * 1e9);
     const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
-    return pages > 0 && psz > 0 ? (size_t)(0.75 * (double)pages * (double)psz) : (size_t)96e9;  // 75 % of host RAM
+    if (pages <= 0 || psz <= 0) return (size_t)96e9;
+    const double ram = (double)pages * (double)psz;
+    return (size_t)std::max(0.75 * ram, ram - 20e9);
   }();
   return cap;
 }
@@ -622,6 +624,9 @@ PlanCache* get_plan(h2g_matrix* M, int stop, int schedule, bool* built) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     if (fill > 0.15 * (double)tot) segments = 16;
+    // the largest configurations: finer segments keep the fill front pool and
+    // the chain halves of the coarse levels (blocks of 400-660 rows) small
+    if (fill > 0.30 * (double)tot) segments = 64;
   }
   // the subtree partition exchanges whole fill blocks at the interior /
   // boundary border: whole-level storage (one collapse at the level end)
