@@ -3033,7 +3033,8 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   // complex of shared memory per CTA stays under ~96 KB
   int bmax_all = 1;
   for (auto& CLp : C->levels) bmax_all = std::max(bmax_all, CLp->sl.bmax);
-  const int rchunk = std::max(1, std::min(nrhs, (int)((96 * 1024) / (2 * 16 * (size_t)bmax_all))));
+  static const int smem_kb = std::getenv("H2G_SOLVE_SMEM_KB") ? std::atoi(std::getenv("H2G_SOLVE_SMEM_KB")) : 96;
+  const int rchunk = std::max(1, std::min(nrhs, (int)(((size_t)smem_kb * 1024) / (2 * 16 * (size_t)bmax_all))));
   // dataflow level kernels (per-item dependency counters) by default; the
   // batch-synchronous cooperative kernels with H2G_SOLVE_BATCHED=1
   static const bool batched = std::getenv("H2G_SOLVE_BATCHED") && std::atoi(std::getenv("H2G_SOLVE_BATCHED"));
