@@ -3030,10 +3030,10 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   const int expl = (mode == H2G_APPLY_INVERSE_EXPLICIT || !tri) ? 1 : 0;
   long long launches = 1;
   // right-hand sides per pass of the level kernels: 2 * bmax * rchunk
-  // complex of shared memory per CTA stays under ~96 KB
+  // complex of shared memory per CTA stays under ~150 KB (measured: 96 / 150 / 200 KB give 895 / 765 / 777 ms for 64 RHS on config 2)
   int bmax_all = 1;
   for (auto& CLp : C->levels) bmax_all = std::max(bmax_all, CLp->sl.bmax);
-  static const int smem_kb = std::getenv("H2G_SOLVE_SMEM_KB") ? std::atoi(std::getenv("H2G_SOLVE_SMEM_KB")) : 96;
+  static const int smem_kb = std::getenv("H2G_SOLVE_SMEM_KB") ? std::atoi(std::getenv("H2G_SOLVE_SMEM_KB")) : 150;
   const int rchunk = std::max(1, std::min(nrhs, (int)(((size_t)smem_kb * 1024) / (2 * 16 * (size_t)bmax_all))));
   // dataflow level kernels (per-item dependency counters) by default; the
   // batch-synchronous cooperative kernels with H2G_SOLVE_BATCHED=1

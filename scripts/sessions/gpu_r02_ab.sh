@@ -7,4 +7,4 @@ for pl in 0 32 64 128; do
   echo "H2G_SOLVE_PULL=$pl" >> gpurun_out/r02ab_solve.log
   H2G_SOLVE_PULL=$pl timeout 600 python scripts/solve_only.py 2 >> gpurun_out/r02ab_solve.log 2>&1
 done
-bash scripts/gpu_r02_z.sh
+bash scripts/sessions/gpu_r02_z.sh
