@@ -215,17 +215,20 @@ def test_segmented_fill_and_streamed_chain_equal_resident(monkeypatch):
     b = O.rhs(A.n, 21)
     ctx = h2g.Context.default()
     out = {}
-    for mode, stream in (("resident", "0"), ("streamed", "1")):
+    for mode, stream in (("resident", "0"), ("streamed", "1"), ("hostcores", "1")):
         monkeypatch.setenv("H2G_FILL_SEGMENTS", "4")
         monkeypatch.setenv("H2G_CHAIN_STREAM", stream)
+        # third variant: the fill cores staged in pinned host memory (deposits over the host link, bulk return in the merge)
+        monkeypatch.setenv("H2G_CORES_HOST", "1" if mode == "hostcores" else "0")
         ctx.clear_plans()
         G = h2g.H2Matrix.upload(arrays, ctx)
         ch = h2g.factorize(G, 1e-4)
         out[mode] = (ch, ch.hash(), ch.solve(b), ch.all_records(), G)
     monkeypatch.delenv("H2G_FILL_SEGMENTS")
     monkeypatch.delenv("H2G_CHAIN_STREAM")
+    monkeypatch.delenv("H2G_CORES_HOST")
     ctx.clear_plans()
-    assert out["resident"][1] == out["streamed"][1]
+    assert out["resident"][1] == out["streamed"][1] == out["hostcores"][1]
     assert np.array_equal(out["resident"][2], out["streamed"][2])
     assert out["resident"][3] == out["streamed"][3]
     ch, G = out["streamed"][0], out["streamed"][4]
