@@ -1589,7 +1589,8 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         std::vector<int> ndesc_f;  // fill index per colnorm entry
         long long ymax = 1, gmax = 1;
         // Gram partials: K split so that small Grams still spread over many CTAs
-        const int kPartW = bm <= 32 ? 128 : (bm <= 64 ? 256 : 512);
+        static const int partw_env = std::getenv("H2G_GRAM_PARTW") ? std::atoi(std::getenv("H2G_GRAM_PARTW")) : 0;
+        const int kPartW = partw_env > 0 ? partw_env : (bm <= 32 ? 128 : (bm <= 64 ? 256 : 512));
         for (int bi = 0; bi < nbat0; ++bi) {
           long long ytop = 0, gtop = 0;
           for (int p = SC.batch_ptr[bi]; p < SC.batch_ptr[bi + 1]; ++p) {
