@@ -302,31 +302,109 @@ size_t pinned_cap() {
   return cap;
 }
 
+// Pinning host memory costs ~0.45 s per GB on the B200 boxes (cudaHostAlloc at
+// 2.2 GB/s, profiles/r02_pinned_alloc.txt), and the host-staged configurations
+// pin and release hundreds of GB per factorization (fill cores of every
+// level, chain chunks). Released buffers of >= 64 MB are kept and handed out
+// again to requests they fit within 12 % (the host-staged fill cores use pages
+// of one size, so a level's pages serve the next level); they still count against the
+// staging cap and are given back to the system when the cap is near.
+class PinnedCache {
+ public:
+  static PinnedCache& get() {
+    static PinnedCache c;
+    return c;
+  }
+  // a cached buffer of capacity in [n, 1.125 n + 16 MB], or nullptr
+  void* take(size_t n, size_t* cap) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_.lower_bound(n);
+    if (it == free_.end() || it->first > n + n / 8 + (size_t(16) << 20)) return nullptr;
+    void* p = it->second;
+    *cap = it->first;
+    free_.erase(it);
+    return p;
+  }
+  void put(void* p, size_t cap) {
+    std::lock_guard<std::mutex> g(mu_);
+    free_.emplace(cap, p);
+  }
+  // give the largest cached buffer back to the system; false if none is left
+  bool drop_one() {
+    void* p = nullptr;
+    size_t cap = 0;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (free_.empty()) return false;
+      auto it = std::prev(free_.end());
+      p = it->second, cap = it->first;
+      free_.erase(it);
+    }
+    cudaFreeHost(p);
+    g_pinned_bytes -= cap;
+    return true;
+  }
+  void clear() {
+    while (drop_one()) {
+    }
+  }
+  ~PinnedCache() {
+    for (auto& kv : free_) cudaFreeHost(kv.second);  // process exit: errors after the runtime is gone are harmless
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+};
+
 struct HBuf {
   void* p = nullptr;
-  size_t bytes = 0;
+  size_t bytes = 0;  // requested size
+  size_t cap = 0;    // pinned capacity behind p (>= bytes when the buffer came from the cache)
   HBuf() = default;
   HBuf(const HBuf&) = delete;
   HBuf& operator=(const HBuf&) = delete;
-  HBuf(HBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  HBuf(HBuf&& o) noexcept : p(o.p), bytes(o.bytes), cap(o.cap) { o.p = nullptr, o.bytes = 0, o.cap = 0; }
   ~HBuf() { release(); }
   void release() {
-    if (p) cudaFreeHost(p), g_pinned_bytes -= bytes;
+    if (p) {
+      if (cap >= (size_t(64) << 20)) {
+        PinnedCache::get().put(p, cap);
+      } else {
+        cudaFreeHost(p);
+        g_pinned_bytes -= cap;
+      }
+    }
     p = nullptr;
-    bytes = 0;
+    bytes = cap = 0;
   }
   void alloc(size_t n) {
     release();
-    if (g_pinned_bytes + n > pinned_cap())
+    const size_t want = std::max<size_t>(n, 16);
+    if (void* q = PinnedCache::get().take(want, &cap)) {
+      p = q;
+      bytes = n;
+      return;
+    }
+    while (g_pinned_bytes + want > pinned_cap() && PinnedCache::get().drop_one()) {
+    }
+    if (g_pinned_bytes + want > pinned_cap())
       throw Error(H2G_ERR_CUDA, std::string("out of memory: staging ") + std::to_string(n) + " bytes in pinned host memory would exceed the " +
                                     std::to_string(pinned_cap()) + "-byte cap (H2G_HOST_STAGING_GB)");
-    if (cudaHostAlloc(&p, std::max<size_t>(n, 16), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      PinnedCache::get().clear();  // the system is short: cached buffers go back first
+      e = cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable);
+    }
+    if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
       throw Error(H2G_ERR_CUDA, std::string("pinned host allocation of ") + std::to_string(n) + " bytes failed");
     }
     bytes = n;
-    g_pinned_bytes += n;
+    cap = want;
+    g_pinned_bytes += want;
   }
   template <class T>
   T* as() const {
@@ -1402,7 +1480,10 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
     };
     std::vector<cplx*> core_ptr_h;  // per fill of the running level: its compact core (host copy of DevLevel::core_ptr)
     std::vector<DBuf> core_chunks;   // the cores, one chunk per segment; released after the merge
-    std::vector<HBuf> core_hchunks;  // ... or in pinned host memory when HBM is short
+    std::vector<HBuf> core_hchunks;  // ... or in pinned host memory when HBM is short (pages of kCorePage bytes)
+    const size_t kCorePage = size_t(1) << 30;
+    char* core_page = nullptr;  // the page being filled (belongs to core_hchunks)
+    size_t core_page_used = 0;
     if (stop <= L) {
       for (int l = L; l >= stop; --l, ++li) {
         NvtxRange nv_level("h2g level " + std::to_string(l));
@@ -1851,6 +1932,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         const size_t nfill = Y.frow.size();
         core_ptr_h.assign(nfill, nullptr);
         core_chunks.clear();
+        core_page = nullptr;
         DBuf core_tab, dzero;
         core_tab.alloc(std::max<size_t>(nfill, 1) * sizeof(cplx*), st, true);
         DL.core_ptr = core_tab.as<cplx*>();
@@ -1886,13 +1968,32 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
             } else {
               // HBM is short: this segment's cores live in pinned, device-mapped
               // host memory (written by the collapse and the later core
-              // deposits, read once by the merge)
-              core_hchunks.emplace_back();
-              core_hchunks.back().alloc((size_t)ctop * 16);
-              CK(cudaMemsetAsync(core_hchunks.back().p, 0, (size_t)ctop * 16, st));
-              base = core_hchunks.back().as<cplx>();
+              // deposits, read once by the merge): pages of one size, filled
+              // across segments, so that the pages a level releases serve the
+              // next level as they are (pinning costs ~0.45 s per GB)
+              for (size_t q = 0; q < cores.size(); ++q) {
+                const size_t need = (size_t)kf[Y.frow[cores[q]]] * kf[Y.fcol[cores[q]]] * 16;
+                if (need > kCorePage) {  // a single core beyond a page (never at the measured configurations)
+                  core_hchunks.emplace_back();
+                  core_hchunks.back().alloc(need);
+                  CK(cudaMemsetAsync(core_hchunks.back().p, 0, need, st));
+                  core_ptr_h[cores[q]] = core_hchunks.back().as<cplx>();
+                  core_page = nullptr;
+                  continue;
+                }
+                if (!core_page || core_page_used + need > kCorePage) {
+                  core_hchunks.emplace_back();
+                  core_hchunks.back().alloc(kCorePage);
+                  CK(cudaMemsetAsync(core_hchunks.back().p, 0, kCorePage, st));
+                  core_page = static_cast<char*>(core_hchunks.back().p);
+                  core_page_used = 0;
+                }
+                core_ptr_h[cores[q]] = reinterpret_cast<cplx*>(core_page + core_page_used);
+                core_page_used += need;
+              }
             }
-            for (size_t q = 0; q < cores.size(); ++q) core_ptr_h[cores[q]] = base + coff[q];
+            if (base)
+              for (size_t q = 0; q < cores.size(); ++q) core_ptr_h[cores[q]] = base + coff[q];
           }
           const cplx* chainp = CL->arena.as<cplx>();
           auto V = [&](int t) { return chainp + Qt_off[t] + (long long)(cur.bsz[t] - kf[t]) * cur.bsz[t]; };
@@ -2688,6 +2789,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         for (auto& ch : core_hchunks) core_host_bytes += ch.bytes;
         core_chunks.clear();
         core_hchunks.clear();
+        core_page = nullptr;
 
         if (verbose) {
           size_t fr = 0, tot = 0;
