@@ -309,6 +309,10 @@ size_t pinned_cap() {
 // again to requests they fit within 12 % (the host-staged fill cores use pages
 // of one size, so a level's pages serve the next level); they still count against the
 // staging cap and are given back to the system when the cap is near.
+// Host staging of many similar pieces (fill cores, chain chunks) goes through
+// pinned pages of one size, so the pages one level releases serve the next.
+constexpr size_t kStagePage = size_t(2) << 30;
+
 class PinnedCache {
  public:
   static PinnedCache& get() {
@@ -541,10 +545,15 @@ struct ChainLevelHost {
   // host memory), joined into one arena by assemble_streamed_chains
   struct Chunk {
     DBuf d;
-    HBuf h;
+    HBuf h;            // own pinned buffer (chunks beyond a staging page, chunks spilled later)
+    char* hp = nullptr;  // or a range of one of hpages
     long long begin = 0, len = 0;  // compact element range
+    const void* src() const { return d.p ? d.p : (hp ? static_cast<const void*>(hp) : h.p); }
   };
   std::vector<Chunk> chunks;
+  std::vector<HBuf> hpages;  // pinned staging pages (kStagePage bytes) holding host-resident chunks, filled across segments
+  char* hpage = nullptr;
+  size_t hpage_used = 0;
   DBuf qchunk;
   long long compact_elems = 0;
   SolveLevel sl{};
@@ -1481,7 +1490,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
     std::vector<cplx*> core_ptr_h;  // per fill of the running level: its compact core (host copy of DevLevel::core_ptr)
     std::vector<DBuf> core_chunks;   // the cores, one chunk per segment; released after the merge
     std::vector<HBuf> core_hchunks;  // ... or in pinned host memory when HBM is short (pages of kCorePage bytes)
-    const size_t kCorePage = size_t(1) << 30;
+    const size_t kCorePage = kStagePage;
     char* core_page = nullptr;  // the page being filled (belongs to core_hchunks)
     size_t core_page_used = 0;
     if (stop <= L) {
@@ -2062,22 +2071,44 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
               }
             const long long clen = compact_top - seg0;
             if (clen > 0) {
-              ChainLevelHost::Chunk ck;
-              ck.begin = seg0, ck.len = clen;
-              cplx* dstb;
               if (BlockCache::get().headroom() >= (size_t)clen * 16 + kMargin) {
+                ChainLevelHost::Chunk ck;
+                ck.begin = seg0, ck.len = clen;
                 ck.d.alloc((size_t)clen * 16, st);
-                dstb = ck.d.as<cplx>();
+                for (auto& d : mv) d.dst = ck.d.as<cplx>() + reinterpret_cast<long long>(d.dst) / 16;
+                CL->chunks.push_back(std::move(ck));
               } else {
-                ck.h.alloc((size_t)clen * 16);  // HBM is short: the chunk goes to pinned host memory (mapped, written by the kernel)
-                dstb = ck.h.as<cplx>();
+                // HBM is short: the segment goes to pinned host memory (mapped,
+                // written by the kernel), block after block into the level's
+                // staging pages; a page boundary starts a new chunk
+                for (auto& d : mv) {
+                  const long long rel = reinterpret_cast<long long>(d.dst) / 16;  // compact offset inside the segment
+                  const size_t need = (size_t)d.len * 16;
+                  if (need > kStagePage) throw Error(H2G_ERR_INTERNAL, "chain block larger than a staging page");
+                  if (!CL->hpage || CL->hpage_used + need > kStagePage) {
+                    CL->hpages.emplace_back();
+                    CL->hpages.back().alloc(kStagePage);
+                    CL->hpage = static_cast<char*>(CL->hpages.back().p);
+                    CL->hpage_used = 0;
+                    CL->chunks.emplace_back();
+                    CL->chunks.back().begin = seg0 + rel;
+                    CL->chunks.back().hp = CL->hpage;
+                  } else if (CL->chunks.empty() || CL->chunks.back().hp == nullptr ||
+                             CL->chunks.back().begin + CL->chunks.back().len != seg0 + rel) {
+                    // first host block of this segment in a page already in use
+                    CL->chunks.emplace_back();
+                    CL->chunks.back().begin = seg0 + rel;
+                    CL->chunks.back().hp = CL->hpage + CL->hpage_used;
+                  }
+                  d.dst = reinterpret_cast<cplx*>(CL->hpage + CL->hpage_used);
+                  CL->hpage_used += need;
+                  CL->chunks.back().len += d.len;
+                }
               }
               DBuf dmv;
-              for (auto& d : mv) d.dst = dstb + reinterpret_cast<long long>(d.dst) / 16;
               upload(dmv, mv, st);
               launch_move(dmv.as<MoveDesc>(), static_cast<int>(mv.size()), st);
               CK(cudaStreamSynchronize(st));
-              CL->chunks.push_back(std::move(ck));
               ++launches;
             }
           }
@@ -2360,7 +2391,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
           if (verbose) {
             double onhost = 0.0;
             for (const auto& ck : CL->chunks)
-              if (ck.h.p) onhost += (double)ck.len * 16;
+              if (!ck.d.p) onhost += (double)ck.len * 16;
             std::fprintf(stderr, "[h2g] level %d: chain %.2f GB at its final size (bound %.2f GB), %.2f GB of it in host memory\n", l,
                          compact_top * 16 / 1e9, top_logical * 16 / 1e9, onhost / 1e9);
           }
@@ -2999,9 +3030,11 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         }
         CK(cudaMemcpyAsync(base, X.qchunk.p, X.qchunk.bytes, cudaMemcpyDefault, st));
         for (auto& ck : X.chunks)
-          CK(cudaMemcpyAsync(base + (size_t)ck.begin * 16, ck.d.p ? ck.d.p : ck.h.p, (size_t)ck.len * 16, cudaMemcpyDefault, st));
+          CK(cudaMemcpyAsync(base + (size_t)ck.begin * 16, ck.src(), (size_t)ck.len * 16, cudaMemcpyDefault, st));
         CK(cudaStreamSynchronize(st));
         X.chunks.clear();
+        X.hpages.clear();
+        X.hpage = nullptr;
         X.qchunk.release();
         X.sl.chain = reinterpret_cast<cplx*>(base);
       }
