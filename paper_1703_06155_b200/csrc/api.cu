@@ -2222,6 +2222,26 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
             do_exchange();
           }
         };
+        // resolved Schur descriptors (k_schur_resolve), two halves by batch
+        // parity like the lifted panels; H2G_SCHUR_RESOLVE=0 resolves inside k_schur
+        static const bool schur_resolve = !(std::getenv("H2G_SCHUR_RESOLVE") && std::atoi(std::getenv("H2G_SCHUR_RESOLVE")) == 0);
+        std::vector<int> cbase(nbat, 0);
+        int rt_max = 1, rp_max = 1;
+        for (int bi = 0; bi < nbat; ++bi) {
+          const int s0 = W.schur_ptr[bi], s1 = W.schur_ptr[bi + 1];
+          int c_lo = INT32_MAX, c_hi = 0;
+          for (int q = s0; q < s1; ++q) c_lo = std::min(c_lo, W.schur[q].c0), c_hi = std::max(c_hi, W.schur[q].c1);
+          if (s1 > s0) {
+            cbase[bi] = c_lo;
+            rt_max = std::max(rt_max, s1 - s0);
+            rp_max = std::max(rp_max, c_hi - c_lo);
+          }
+        }
+        DBuf rtbuf, rpbuf;
+        if (schur_resolve && !hooks) {
+          rtbuf.alloc((size_t)2 * rt_max * sizeof(RTarget), st);
+          rpbuf.alloc((size_t)2 * rp_max * sizeof(RPanel), st);
+        }
         int prev_exec = -1;
         std::vector<char> rotated(nl, 0);
         std::vector<int> elimv(nl, 0);
@@ -2326,14 +2346,22 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
             // the side stream, overlapping the next batch
             const int s0 = W.schur_ptr[bi], ncr = W.schur_crit[bi], nbulk = W.schur_ptr[bi + 1] - s0 - ncr;
             if (bi > 0) CK(cudaStreamWaitEvent(st, ctx->ev_bulk, 0));
+            RTarget* rtp = nullptr;
+            RPanel* rpp = nullptr;
             pf.begin(PC_SCHUR, st);
-            launch_schur(DL, d_sch + s0, ncr, d_con, st);
+            if (rtbuf.p && ncr + nbulk > 0) {
+              rtp = rtbuf.as<RTarget>() + (size_t)(bi & 1) * rt_max;
+              rpp = rpbuf.as<RPanel>() + (size_t)(bi & 1) * rp_max - cbase[bi];
+              launch_schur_resolve(DL, d_sch + s0, ncr + nbulk, d_con, rtp, rpp, st);
+              ++launches;
+            }
+            launch_schur(DL, d_sch + s0, ncr, d_con, st, rtp, rpp);
             pf.end(st);
             CK(cudaEventRecord(ctx->ev_crit, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_crit, 0));
             ctx->prof_side.cur_level = l;
             ctx->prof_side.begin(PC_SCHUR, ctx->side);
-            if (!(DL.debug & 16)) launch_schur(DL, d_sch + s0 + ncr, nbulk, d_con, ctx->side);  // debug 16: timing experiment only (wrong results)
+            if (!(DL.debug & 16)) launch_schur(DL, d_sch + s0 + ncr, nbulk, d_con, ctx->side, rtp ? rtp + ncr : nullptr, rpp);  // debug 16: timing experiment only (wrong results)
             ctx->prof_side.end(ctx->side);
             CK(cudaEventRecord(ctx->ev_bulk, ctx->side));
             C->klaunch[PC_SCHUR] += (ncr > 0) + (nbulk > 0);

@@ -1329,8 +1329,71 @@ __global__ void __launch_bounds__(256) k_hlu_finish(DevLevel L, const int* batch
 // tile is fetched into shared memory by cp.async at the start (64 KB in flight
 // per CTA while the contribution tables and panels load) and the epilogue
 // subtracts from the staged copy; two CTAs per SM instead of three.
+// Target and panel descriptors of one batch, resolved once (one thread per
+// target) instead of by every tile's CTA.
+__global__ void __launch_bounds__(128) k_schur_resolve(DevLevel L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib,
+                                                       RTarget* rt, RPanel* rp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntargets) return;
+  const SchurTargetD tg = targets[i];
+  RTarget R{};
+  R.rs = R.cs = 0;
+  R.ldo = -1;
+  if ((tg.kind & 1) == 0) {
+    const int j = L.drow[tg.idx], c = L.dcol[tg.idx];
+    R.rows = L.bsz[j];
+    R.cols = L.bsz[c];
+    R.out = L.D + L.D_off[tg.idx];
+    if (tg.kind & 2) R.rs = R.rows - L.kfin[j];
+    if (tg.kind & 4) R.cs = R.cols - L.kfin[c];
+  } else {
+    const int j = L.frow[tg.idx], c = L.fcol[tg.idx];
+    R.rows = L.bsz[j];
+    R.cols = L.bsz[c];
+    if (tg.kind & 8) {
+      R.rs = R.rows - L.kfin[j];
+      R.cs = R.cols - L.kfin[c];
+      R.ldo = L.kfin[j];
+      R.out = L.core_ptr[tg.idx] - R.rs - (size_t)R.cs * R.ldo;
+    } else {
+      R.out = L.F + L.F_off[tg.idx];
+    }
+  }
+  if (R.ldo < 0) R.ldo = R.rows;
+  rt[i] = R;
+  for (int ci = tg.c0; ci < tg.c1; ++ci) {
+    const SchurContribD cb = contrib[ci];
+    const int t = cb.t;
+    const int kf = L.kfin[t], e = L.bsz[t] - kf;
+    RPanel P{};
+    P.e = e;
+    if (e > 0) {
+      if (cb.r >= 0) {
+        P.arows = L.bsz[L.R_nb[cb.r]];
+        P.A = (cb.flags & 1) ? L.lift + L.liftL_off[cb.r] : L.chain + L.Lbar_off[cb.r];
+        P.ro = 0;
+      } else {
+        P.arows = kf;
+        P.A = L.chain + L.Lself_off[t];
+        P.ro = e;
+      }
+      if (cb.c >= 0) {
+        P.bcols = L.bsz[L.C_nb[cb.c]];
+        P.B = (cb.flags & 2) ? L.lift + L.liftU_off[cb.c] : L.chain + L.Ubar_off[cb.c];
+        P.co = 0;
+      } else {
+        P.bcols = kf;
+        P.B = L.chain + L.Uself_off[t];
+        P.co = e;
+      }
+    }
+    rp[ci] = P;
+  }
+}
+
 template <int TM, bool PF = false, int NSTAGE = 3>
-__global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib) {
+__global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const SchurTargetD* targets, const SchurContribD* contrib,
+                                                         const RTarget* rt, const RPanel* rp) {
   constexpr int RM = TM / 8, RN = TM / 16;  // DFMA micro-tile (TM < 64)
   extern __shared__ __align__(16) unsigned char tsm[];
   using Smem = TileSmem<TM, PF ? 2 : NSTAGE>;
@@ -1339,7 +1402,10 @@ __global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const Sch
   const SchurTargetD tg = targets[blockIdx.x];
   int rows, cols, rs = 0, cs = 0, ldo = -1;
   cplx* out;
-  if ((tg.kind & 1) == 0) {
+  if (rt) {
+    const RTarget R = rt[blockIdx.x];
+    rows = R.rows, cols = R.cols, rs = R.rs, cs = R.cs, ldo = R.ldo, out = R.out;
+  } else if ((tg.kind & 1) == 0) {
     const int j = L.drow[tg.idx], c = L.dcol[tg.idx];
     rows = L.bsz[j];
     cols = L.bsz[c];
@@ -1388,6 +1454,16 @@ __global__ void __launch_bounds__(128, PF ? 2 : 3) k_schur(DevLevel L, const Sch
   // one contribution resolved against this tile; returns its e (0: the
   // cluster eliminated nothing), use = false when it misses the tile
   auto resolve = [&](int ci, SchurPanel& P, bool& use) {
+    if (rp) {
+      const RPanel Q = rp[ci];
+      use = false;
+      if (Q.e == 0) return 0;
+      P.A = Q.A, P.B = Q.B, P.arows = Q.arows, P.bcols = Q.bcols, P.e = Q.e;
+      P.ash = r0 - Q.ro;
+      P.bsh = c0 - Q.co;
+      use = !(P.ash >= P.arows || P.bsh >= P.bcols || P.ash + TM <= 0 || P.bsh + TM <= 0);
+      return Q.e;
+    }
     const SchurContribD cb = contrib[ci];
     const int t = cb.t;
     const int kf = L.kfin[t], e = L.bsz[t] - kf;
@@ -1957,7 +2033,15 @@ void launch_colnorm(const NormDesc* d, int n, cudaStream_t s) {
 }
 
 
-void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s) {
+void launch_schur_resolve(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, RTarget* rt, RPanel* rp,
+                          cudaStream_t s) {
+  if (ntargets <= 0) return;
+  k_schur_resolve<<<(ntargets + 127) / 128, 128, 0, s>>>(L, targets, ntargets, contrib, rt, rp);
+  post_launch("k_schur_resolve");
+}
+
+void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s, const RTarget* rt,
+                  const RPanel* rp) {
   if (ntargets <= 0) return;
   static const int t32_bmax = std::getenv("H2G_SCHUR_T32_BMAX") ? std::atoi(std::getenv("H2G_SCHUR_T32_BMAX")) : 32;
   if (L.bmax <= t32_bmax) {
@@ -1965,7 +2049,7 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
     // target read-modify-write dominates and a 64 x 64 tensor tile would be 3/4 padding
     const int t32 = (L.bmax + 31) / 32;
     set_smem((const void*)k_schur<32>, sizeof(TileSmem<32>));
-    k_schur<32><<<dim3(ntargets, t32 * t32), 128, sizeof(TileSmem<32>), s>>>(L, targets, contrib);
+    k_schur<32><<<dim3(ntargets, t32 * t32), 128, sizeof(TileSmem<32>), s>>>(L, targets, contrib, rt, rp);
     post_launch("k_schur");
     return;
   }
@@ -1975,19 +2059,19 @@ void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, 
   if (L.bmax <= pf_bmax) {
     const size_t sm = sizeof(TileSmem<64, 2>) + 64 * 64 * sizeof(cplx);
     set_smem((const void*)k_schur<64, true>, sm);
-    k_schur<64, true><<<dim3(ntargets, t * t), 128, sm, s>>>(L, targets, contrib);
+    k_schur<64, true><<<dim3(ntargets, t * t), 128, sm, s>>>(L, targets, contrib, rt, rp);
     post_launch("k_schur");
     return;
   }
   static const int nst = std::getenv("H2G_SCHUR_STAGES") ? std::atoi(std::getenv("H2G_SCHUR_STAGES")) : 3;
   if (nst == 4) {
     set_smem((const void*)k_schur<64, false, 4>, sizeof(TileSmem<64, 4>));
-    k_schur<64, false, 4><<<dim3(ntargets, t * t), 128, sizeof(TileSmem<64, 4>), s>>>(L, targets, contrib);
+    k_schur<64, false, 4><<<dim3(ntargets, t * t), 128, sizeof(TileSmem<64, 4>), s>>>(L, targets, contrib, rt, rp);
     post_launch("k_schur");
     return;
   }
   set_smem((const void*)k_schur<64>, sizeof(Tile128Smem));
-  k_schur<64><<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib);
+  k_schur<64><<<dim3(ntargets, t * t), 128, sizeof(Tile128Smem), s>>>(L, targets, contrib, rt, rp);
   post_launch("k_schur");
 }
 

@@ -150,7 +150,23 @@ void launch_mask(const MaskDesc* d, int n, cudaStream_t s);
 // emax: upper bound of the batch's eliminated sizes (b - korig); > 64 takes
 // the multi-CTA extended LU
 void launch_head2(const DevLevel& L, const int* batch_cl, int nb, int emax, cudaStream_t s);
-void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s);
+// Resolved Schur descriptors of one batch (k_schur_resolve, one thread per
+// target): what a k_schur CTA would otherwise find through two chains of
+// dependent index loads. rp is indexed by the global contribution index.
+struct RTarget {
+  cplx* out;
+  int rows, cols, rs, cs, ldo, pad;
+};
+struct RPanel {
+  const cplx* A;
+  const cplx* B;
+  int arows, bcols, ro, co, e, pad;
+};
+void launch_schur_resolve(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, RTarget* rt, RPanel* rp,
+                          cudaStream_t s);
+// rt / rp: resolved descriptors of these targets (nullptr: resolved inside the kernel)
+void launch_schur(const DevLevel& L, const SchurTargetD* targets, int ntargets, const SchurContribD* contrib, cudaStream_t s,
+                  const RTarget* rt = nullptr, const RPanel* rp = nullptr);
 void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim = 0);
