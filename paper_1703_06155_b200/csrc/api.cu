@@ -3238,15 +3238,22 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   // complex of shared memory per CTA stays under ~150 KB (measured: 96 / 150 / 200 KB give 895 / 765 / 777 ms for 64 RHS on config 2)
   int bmax_all = 1;
   for (auto& CLp : C->levels) bmax_all = std::max(bmax_all, CLp->sl.bmax);
-  static const int smem_kb = std::getenv("H2G_SOLVE_SMEM_KB") ? std::atoi(std::getenv("H2G_SOLVE_SMEM_KB")) : 150;
+  const int smem_kb = std::getenv("H2G_SOLVE_SMEM_KB") ? std::max(1, std::atoi(std::getenv("H2G_SOLVE_SMEM_KB"))) : 150;  // read per call (tests force several groups)
   const int rchunk = std::max(1, std::min(nrhs, (int)(((size_t)smem_kb * 1024) / (2 * 16 * (size_t)bmax_all))));
   // dataflow level kernels (per-item dependency counters) by default; the
   // batch-synchronous cooperative kernels with H2G_SOLVE_BATCHED=1
   static const bool batched = std::getenv("H2G_SOLVE_BATCHED") && std::atoi(std::getenv("H2G_SOLVE_BATCHED"));
+  // H2G_SOLVE_GROUPS=0: the groups of right-hand sides one after the other (one launch each) instead of side by side
+  const bool side_by_side = !(std::getenv("H2G_SOLVE_GROUPS") && !std::atoi(std::getenv("H2G_SOLVE_GROUPS")));
+  FlowGroups fg{};
   {
     int nlmax = 1;
     for (auto& CLp : C->levels) nlmax = std::max(nlmax, CLp->sl.nl);
-    const size_t cb = (size_t)(4 * nlmax + 2) * sizeof(int);  // [0] stall flag, [1..] counters
+    // [0] stall flag, then one counter block per right-hand-side group
+    fg.rchunk = rchunk;
+    fg.cstride = 4 * nlmax + 2;
+    fg.part_stride = 0;
+    const size_t cb = (1 + (size_t)fg.cstride * ((nrhs + rchunk - 1) / rchunk)) * sizeof(int);
     if (cb > C->flowcnt.bytes) C->flowcnt.alloc(cb, st);
     CK(cudaMemsetAsync(C->flowcnt.p, 0, sizeof(int), st));
   }
@@ -3254,14 +3261,18 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   if (fwd) {
     for (auto& CLp : C->levels) {
       ChainLevelHost& CL = *CLp;
-      for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
-        if (batched)
-          launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
-        else
-          launch_fwd_flow(CL.sl, CL.sched, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->flowcnt.as<int>() + 1,
-                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, st);
+      if (!batched && side_by_side) {
+        launch_fwd_flow(CL.sl, CL.sched, CL.flow, y, n, nrhs, expl, C->flowcnt.as<int>() + 1, C->flowcnt.as<int>(), tmp, fg, st);
         ++launches;
-      }
+      } else
+        for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
+          if (batched)
+            launch_fwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, st);
+          else
+            launch_fwd_flow(CL.sl, CL.sched, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->flowcnt.as<int>() + 1,
+                            C->flowcnt.as<int>(), tmp + (size_t)c0 * n, fg, st);
+          ++launches;
+        }
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 0, st);
       launches += 2;
     }
@@ -3279,16 +3290,23 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
       ChainLevelHost& CL = **it;
       launch_permute(CL.d_src.as<long long>(), static_cast<long long>(CL.src.size()), y, tmp, n, nrhs, 1, st);
       launches += 2;
-      const size_t need = (batched ? CL.part_need : CL.flow_part) * rchunk * 16;
+      const bool grouped = !batched && side_by_side;
+      const size_t per_group = (batched ? CL.part_need : CL.flow_part) * rchunk;
+      const size_t need = per_group * 16 * (grouped ? (nrhs + rchunk - 1) / rchunk : 1);
       if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
-      for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
-        if (batched)
-          launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
-        else
-          launch_bwd_flow(CL.sl, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1,
-                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, st);
+      if (grouped) {
+        fg.part_stride = (long long)per_group;
+        launch_bwd_flow(CL.sl, CL.flow, y, n, nrhs, expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1, C->flowcnt.as<int>(), tmp, fg, st);
         ++launches;
-      }
+      } else
+        for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
+          if (batched)
+            launch_bwd_level(CL.sl, CL.sched, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), st);
+          else
+            launch_bwd_flow(CL.sl, CL.flow, y + (size_t)c0 * n, n, std::min(rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1,
+                            C->flowcnt.as<int>(), tmp + (size_t)c0 * n, fg, st);
+          ++launches;
+        }
     }
   }
   CK(cudaGetLastError());

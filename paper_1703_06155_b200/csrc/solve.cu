@@ -485,9 +485,17 @@ constexpr int kSlabBase = 1 << 30;
 // cnt: [0] ticket, [1 + s] writers of segment s done, [1 + nl + t] slabs of record t done.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv,
-                                                 int* cnt, int* fail, cplx* tmp) {
+                                                 int* cnt, int* fail, cplx* tmp, FlowGroups G) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_item, s_ok;
+  {
+    // right-hand-side group blockIdx.y: its own columns, counters and ticket
+    const int g = blockIdx.y;
+    y += (size_t)g * G.rchunk * ldy;
+    tmp += (size_t)g * G.rchunk * ldy;
+    cnt += (size_t)g * G.cstride;
+    nrhs = min(G.rchunk, nrhs - g * G.rchunk);
+  }
   int* seg = cnt + 1;
   int* slab_done = cnt + 1 + S.nl;
   for (;;) {
@@ -569,9 +577,17 @@ __global__ void __launch_bounds__(NT) k_fwd_flow(SolveLevel S, SolveSched P, Sol
 // [1 + 3 nl + m] head of split record m done.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_bwd_flow(SolveLevel S, SolveFlow F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part,
-                                                 int* cnt, int* fail, cplx* tmp) {
+                                                 int* cnt, int* fail, cplx* tmp, FlowGroups G) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int s_item, s_ok;
+  {
+    const int g = blockIdx.y;
+    y += (size_t)g * G.rchunk * ldy;
+    tmp += (size_t)g * G.rchunk * ldy;
+    cnt += (size_t)g * G.cstride;
+    part += (size_t)g * G.part_stride;
+    nrhs = min(G.rchunk, nrhs - g * G.rchunk);
+  }
   const int nl = S.nl;
   int* slots_done = cnt + 1;
   int* reads_done = cnt + 1 + nl;
@@ -791,6 +807,13 @@ static int flow_grid(const void* fn, int nt, size_t smem) {
   return g;
 }
 
+// Right-hand-side groups (grid y): every group is an independent dataflow over
+// its own columns, counters and ticket, so the groups' latency chains overlap.
+// The x extent is cut so that all groups are resident together (CTAs are
+// placed x-first: a full-width x would run the groups one after the other).
+static int flow_ngroups(int nrhs, const FlowGroups& G) { return (nrhs + G.rchunk - 1) / G.rchunk; }
+static int group_grid(int resident, int ng) { return std::max(1, (resident + ng - 1) / ng); }
+
 // Threads per CTA of the dataflow kernels: a record's rotation (a b x b GEMV
 // by one CTA) sits on the dependency chain, so the coarse levels with large
 // blocks run wide CTAs. H2G_SOLVE_THREADS overrides (256 / 512 / 1024).
@@ -802,42 +825,44 @@ static int flow_threads(int bmax) {
 
 template <int NT>
 static void fwd_flow_nt(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
-                        int* fail, cplx* tmp, cudaStream_t s) {
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + NT * sizeof(cplx);
+                        int* fail, cplx* tmp, const FlowGroups& G, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * std::min(nrhs, G.rchunk) * sizeof(cplx) + NT * sizeof(cplx);
   smem_attr((const void*)k_fwd_flow<NT>, smem);
-  const int grid = std::min(flow_grid((const void*)k_fwd_flow<NT>, NT, smem), F.nf);
-  k_fwd_flow<NT><<<grid, NT, smem, s>>>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp);
+  const int ng = flow_ngroups(nrhs, G);
+  const int grid = std::min(group_grid(flow_grid((const void*)k_fwd_flow<NT>, NT, smem), ng), F.nf);
+  k_fwd_flow<NT><<<dim3(grid, ng), NT, smem, s>>>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, G);
 }
 
 void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
-                     int* fail, cplx* tmp, cudaStream_t s) {
+                     int* fail, cplx* tmp, const FlowGroups& G, cudaStream_t s) {
   if (F.nf <= 0) return;
-  cudaMemsetAsync(cnt, 0, (size_t)(2 * S.nl + 1) * sizeof(int), s);
+  cudaMemsetAsync(cnt, 0, ((size_t)(flow_ngroups(nrhs, G) - 1) * G.cstride + 2 * S.nl + 1) * sizeof(int), s);
   const int nt = flow_threads(S.bmax);
-  if (nt == 256) fwd_flow_nt<256>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
-  else if (nt == 512) fwd_flow_nt<512>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
-  else fwd_flow_nt<1024>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, s);
+  if (nt == 256) fwd_flow_nt<256>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, G, s);
+  else if (nt == 512) fwd_flow_nt<512>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, G, s);
+  else fwd_flow_nt<1024>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, G, s);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_fwd_flow failed: ") + cudaGetErrorString(e));
 }
 
 template <int NT>
 static void bwd_flow_nt(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
-                        cplx* tmp, cudaStream_t s) {
-  const size_t smem = 2 * (size_t)S.bmax * nrhs * sizeof(cplx) + NT * sizeof(cplx);
+                        cplx* tmp, const FlowGroups& G, cudaStream_t s) {
+  const size_t smem = 2 * (size_t)S.bmax * std::min(nrhs, G.rchunk) * sizeof(cplx) + NT * sizeof(cplx);
   smem_attr((const void*)k_bwd_flow<NT>, smem);
-  const int grid = std::min(flow_grid((const void*)k_bwd_flow<NT>, NT, smem), F.nb);
-  k_bwd_flow<NT><<<grid, NT, smem, s>>>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp);
+  const int ng = flow_ngroups(nrhs, G);
+  const int grid = std::min(group_grid(flow_grid((const void*)k_bwd_flow<NT>, NT, smem), ng), F.nb);
+  k_bwd_flow<NT><<<dim3(grid, ng), NT, smem, s>>>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, G);
 }
 
 void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
-                     cplx* tmp, cudaStream_t s) {
+                     cplx* tmp, const FlowGroups& G, cudaStream_t s) {
   if (F.nb <= 0) return;
-  cudaMemsetAsync(cnt, 0, (size_t)(4 * S.nl + 1) * sizeof(int), s);
+  cudaMemsetAsync(cnt, 0, ((size_t)(flow_ngroups(nrhs, G) - 1) * G.cstride + 4 * S.nl + 1) * sizeof(int), s);
   const int nt = flow_threads(S.bmax);
-  if (nt == 256) bwd_flow_nt<256>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
-  else if (nt == 512) bwd_flow_nt<512>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
-  else bwd_flow_nt<1024>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, s);
+  if (nt == 256) bwd_flow_nt<256>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, G, s);
+  else if (nt == 512) bwd_flow_nt<512>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, G, s);
+  else bwd_flow_nt<1024>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, G, s);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string("launch of k_bwd_flow failed: ") + cudaGetErrorString(e));
 }

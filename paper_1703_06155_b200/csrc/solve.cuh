@@ -73,18 +73,27 @@ struct SolveFlow {
   const int* rec_fs;
 };
 
+// Right-hand sides beyond what the shared-memory segment buffers hold are cut
+// into groups of rchunk columns; the dataflow kernels run the groups side by
+// side (grid y), each with its own counter block.
+struct FlowGroups {
+  int rchunk;             // columns per group
+  int cstride;            // ints between the counter blocks of two groups (>= 4 nl + 1)
+  long long part_stride;  // complex between the backward partial buffers of two groups
+};
+
 // Whole level, all batches, one cooperative launch per direction; part holds
 // max_b nb * (maxc_b + 1) * bmax * nrhs gathered backward partials.
 void launch_fwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cudaStream_t s);
 void launch_bwd_level(const SolveLevel& S, const SolveSched& P, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, cudaStream_t s);
-// Dataflow versions (no grid-wide barriers). cnt: >= 4 nl + 1 ints (reset by
-// the launch); *fail is set when a dependency wait stalls (never reset here).
+// Dataflow versions (no grid-wide barriers). cnt: >= 4 nl + 1 ints per group
+// (G.cstride apart, reset by the launch); nrhs counts all columns from y; *fail is set when a dependency wait stalls (never reset here).
 // tmp: n x nrhs scratch (ld ldy) holding the split records' segments between
 // their slab and head items.
 void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
-                     int* fail, cplx* tmp, cudaStream_t s);
+                     int* fail, cplx* tmp, const FlowGroups& G, cudaStream_t s);
 void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
-                     cplx* tmp, cudaStream_t s);
+                     cplx* tmp, const FlowGroups& G, cudaStream_t s);
 void launch_permute(const long long* src, long long len, cplx* y, cplx* tmp, long long ldy, int nrhs, int scatter, cudaStream_t s);
 void launch_root_trsv(const cplx* A, int n, cplx* y, long long ldy, int nrhs, int upper, cudaStream_t s);
 void launch_finite(const cplx* y, long long total, int* bad, cudaStream_t s);

@@ -1,7 +1,7 @@
 """Build and factorize one BASELINE config with level logging; report ranks,
 times and residuals (one JSON summary line at the end).
 
-usage: python scripts/try_config.py CONFIG [SCHEDULE] [EPS] [NRHS]
+usage: python scripts/try_config.py CONFIG [SCHEDULE] [EPS] [NRHS] [explicit]
 EPS overrides both eps_h2 and eps_fill (config 4's sweep); NRHS > 1 applies the
 factorization to that many seeded RHS at once (seeds 1234 + c). Config 4 uses
 the explicit-inverse application (h2g_solve mode APPLY_INVERSE_EXPLICIT)."""
@@ -48,9 +48,10 @@ else:
     b = np.stack([h2g.random_rhs(A.n, 1234 + j) for j in range(nrhs)], axis=1)
 if perm is not None:
     b = b[perm]  # original order -> tree order
-mode = "apply_inverse_explicit" if cfg == 4 else "solve"
+explicit = cfg == 4 or (len(sys.argv) > 5 and sys.argv[5] == "explicit")
+mode = "apply_inverse_explicit" if explicit else "solve"
 t0 = time.time()
-x = ch.apply_inverse_explicit(b) if cfg == 4 else ch.solve(b)
+x = ch.apply_inverse_explicit(b) if explicit else ch.solve(b)
 solve_wall = time.time() - t0
 solve_ms = ch.timing()["solve_ms"]
 print("%s wall %.3f s, device ms %.2f" % (mode, solve_wall, solve_ms), flush=True)
