@@ -379,6 +379,18 @@ def main():
                              "note": "greedy distance-1 colouring, one colour per batch (a different valid elimination order; "
                                      "parity-tested against the oracle run in that order)"}}
         del chq
+    # 64 right-hand sides through the explicit-inverse application (config 4's mode), outside the timed region
+    many = None
+    if world == 1:
+        B64 = np.stack([h2g.random_rhs(n, 1234 + j) for j in range(64)], axis=1)[perm]
+        ms64 = []
+        for _ in range(3):
+            X64 = ch.apply_inverse_explicit(B64)
+            ms64.append(ch.timing()["solve_ms"])
+        many = {"nrhs": 64, "mode": "apply_inverse_explicit", "ms": min(ms64),
+                "relative_residual_h2_col63": A.relative_residual(X64[:, 63], B64[:, 63]),
+                "note": "right-hand-side groups side by side in one launch per level and direction (best of 3)"}
+        del B64, X64
     stats = chp.kernel_stats()
     prof_total = sum(v["ms"] for v in stats.values())
     dom = max(stats, key=lambda k: stats[k]["ms"])
@@ -474,6 +486,7 @@ def main():
         "factor_ms": factor_ms,
         "dist": dstats,
         "other_schedules": other,
+        "many_rhs": many,
         "plan_ms_cold": plan_cold_ms,
         "factor_ms_incl_cold_plan": factor_ms + plan_cold_ms,
         "solve_ms": solve_ms,

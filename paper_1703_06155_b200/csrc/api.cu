@@ -1819,6 +1819,7 @@ static int factorize_impl(h2g_context* ctx, const h2g_matrix* mc, double eps, in
         DL.nl = nl;
         DL.bmax = bm;
         DL.eps = eps;
+        DL.refine_below = std::getenv("H2G_REFINE_BELOW") ? std::atof(std::getenv("H2G_REFINE_BELOW")) : kRefineBelow;
         DL.bsz = at<int>(mt, o_bsz);
         DL.pos = at<int>(mt, o_pos);  // unused on device (long long copy kept for solve)
         DL.korig = at<int>(mt, o_korig);

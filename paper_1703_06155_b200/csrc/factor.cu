@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(256) k_eig1c(DevLevel L, const int* batch_cl, 
     s_lo = lo, s_hi = hi, s_piv = pivmin, s_s0 = s0, s_thr = thr;
     // the Gram resolves eigenvalues to ~eps_mach * lmax: below ~1e-4 sigma_0
     // the truncation needs the refinement pass (k_eig1_refine)
-    s_need = s0 > 0.0 && (thr < 1e-4 * s0 || (L.debug & 4));  // debug bit 2: always refine
+    s_need = s0 > 0.0 && (thr < L.refine_below * s0 || (L.debug & 4));  // debug bit 2: always refine
   }
   __syncthreads();
   const int r = s_r;

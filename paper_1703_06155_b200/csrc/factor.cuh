@@ -13,6 +13,10 @@ struct DevLevel {
   int nl;
   int bmax;
   double eps;
+  // step 0: a truncation threshold below refine_below * sigma_0 takes the
+  // Rayleigh-Ritz refinement pass (the Gram alone resolves sigma down to
+  // ~sqrt(m eps_mach) sigma_0); H2G_REFINE_BELOW overrides
+  double refine_below;
   const int* bsz;
   const int* pos;
   const int* korig;
@@ -171,7 +175,15 @@ void launch_copy(const CopyDesc* d, int n, cudaStream_t s);
 // tiles: upper bound on 64 x 64 output tiles per descriptor (CTAs per desc, capped)
 void launch_gemm(const GemmDesc* d, int n, cudaStream_t s, int maxdim = 0);
 // Step-0 refinement pass (k_eig1_refine, pass-2 Gram) reachable only for eps < 1e-4.
-inline bool eig1_refine_possible(const DevLevel& L) { return L.eps < 1e-4 || (L.debug & 4); }
+// Default of DevLevel::refine_below. The Gram G = Y Y^H resolves singular
+// values down to ~sqrt(c eps_mach) sigma_0 (c grows with the stack width): at
+// eps >= 3e-7 the truncation is decided on the Gram alone (fast cluster
+// eigensolver); tighter eps takes the one-CTA Jacobi + Rayleigh-Ritz pass,
+// which matches the reference's QR + SVD resolution but is ~70x slower on
+// 32^3 unknowns (profiles/r02_refine_switch.txt). H2G_REFINE_BELOW=1e-4
+// restores the refinement for every eps < 1e-4.
+constexpr double kRefineBelow = 3e-7;
+inline bool eig1_refine_possible(const DevLevel& L) { return L.eps < L.refine_below || (L.debug & 4); }
 void launch_zero_desc_flags(int* p, int n, cudaStream_t s);
 int root_lu(cplx* A, int n, double tol, DevError* err, void* scratch, cudaStream_t s, long long* launches);
 size_t head_smem_bytes(int bmax);

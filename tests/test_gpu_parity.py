@@ -102,6 +102,25 @@ def test_rhs_groups_side_by_side_match_columnwise(monkeypatch):
             assert rel(X[:, j], fn(B[:, j])) < 1e-12
 
 
+@pytest.mark.parametrize("refine_below", [None, "1e-4"])
+def test_vie_config1_geometry_eps_1e6(monkeypatch, refine_below):
+    """eps = 1e-6 (the tight end of config 4's sweep) on the config-1 geometry
+    against the oracle: with the step-0 truncation decided on the Gram alone
+    (default for eps >= 3e-7) and with the Rayleigh-Ritz refinement forced
+    (H2G_REFINE_BELOW=1e-4), h2_matrix.hpp:279-290 / factorization.hpp:295-298."""
+    if refine_below:
+        monkeypatch.setenv("H2G_REFINE_BELOW", refine_below)
+    eps = 1e-6
+    A, _ = vie_problem(16, 0.5, 32, eps)
+    och = A.factorize(eps)
+    gch = h2g.factorize(upload(A), eps)
+    compare_chains(och, gch, rank_tol=1)
+    b = O.rhs(A.n, 1234)
+    xo, xg = och.solve(b), gch.solve(b)
+    assert rel(xg, xo) <= 10 * eps
+    assert A.relative_residual(xg, b) <= 2 * A.relative_residual(xo, b)
+
+
 def test_helmholtz_rod():
     A = rod_problem(200, 1e-10, kernel=O.helmholtz(0.3, 2.0))
     gch = h2g.factorize(upload(A), 1e-12)
