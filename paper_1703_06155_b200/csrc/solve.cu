@@ -36,6 +36,31 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
         for (int c = 0; c < 8; ++c)
           if (c < nc) cfma(acc[c], av, x[p + (size_t)(c0 + c) * ldx]);
       }
+      if (nc > 2) {
+        // several columns: transposed butterfly. Every step halves the values
+        // a lane carries (16 doubles -> 8 -> 4 -> 2 -> 1, then one plain step):
+        // 16 double shuffles instead of 80, and the same summation tree as the
+        // plain butterfly below (distance 16, 8, 4, 2, 1; IEEE addition is
+        // commutative), so the results are bit-identical to it.
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[2 * c] = acc[c].x, v[2 * c + 1] = acc[c].y;
+#pragma unroll
+        for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int j = 0; j < h; ++j) {
+            const double keep = up ? v[j + h] : v[j];
+            const double send = up ? v[j] : v[j + h];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        // lane bits 16 / 8 / 4 / 2 selected halves of 8 / 4 / 2 / 1: value index = those bits
+        const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        if (!(lane & 1) && (idx >> 1) < nc) reinterpret_cast<double*>(out + i + (size_t)(c0 + (idx >> 1)) * ldo)[idx & 1] = v[0];
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if (c >= nc) break;
