@@ -75,6 +75,9 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
   }
 }
 
+// inner dimensions up to this run one thread per result entry in the many-RHS paths
+constexpr int kSmallK = 32;
+
 // out = op(A) x for a column-major m x k matrix A (op: A or conj(A), no
 // transpose), x k x nrhs (global or shared). Coalesced: thread t owns row
 // i = t % m' of a chunk of m' <= blockDim rows and the k-slice p = g, g + G,
@@ -83,6 +86,25 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
 // out -= result instead of out = result. red: blockDim complex of shared.
 __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool conjA, const cplx* x, long long ldx, cplx* out, long long ldo,
                            bool subtract, cplx* red) {
+  if (nrhs >= 4 && k <= kSmallK) {
+    // many right-hand sides, short inner dimension (fine levels: a few
+    // eliminated rows): one thread per (row, column) entry of the result, the
+    // whole k range in registers -> no k-slices, no reduction barriers
+    for (int idx = threadIdx.x; idx < m * nrhs; idx += blockDim.x) {
+      const int i = idx % m, c = idx / m;
+      const cplx* xc = x + (size_t)c * ldx;
+      cplx acc = czero();
+      for (int p = 0; p < k; ++p) {
+        cplx a = A[i + (size_t)p * lda];
+        if (conjA) a.y = -a.y;
+        cfma(acc, a, xc[p]);
+      }
+      cplx* o = out + i + (size_t)c * ldo;
+      *o = subtract ? csub(*o, acc) : acc;
+    }
+    __syncthreads();
+    return;
+  }
   if (nrhs >= 4) {
     // many right-hand sides: the same (row, k-slice) threads, each A element
     // read once for up to 8 columns (8 accumulators), the k-slices reduced
@@ -224,6 +246,27 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
     const int m = -1 - tg.seg;
     rows = S.kfin[m];
     base = S.pos[m] + (S.bsz[m] - S.kfin[m]);
+  }
+  int ktot = 0;
+  for (int ci = tg.c0; ci < tg.c1; ++ci) ktot += S.bsz[contrib[ci].m] - S.kfin[contrib[ci].m];
+  if (nrhs >= 4 && ktot <= kSmallK) {
+    // many right-hand sides, few eliminated rows in all contributions (fine
+    // levels): one thread per (row, column) entry, contributions in order
+    for (int idx = threadIdx.x; idx < rows * nrhs; idx += blockDim.x) {
+      const int i = idx % rows, c = idx / rows;
+      cplx acc = czero();
+      for (int ci = tg.c0; ci < tg.c1; ++ci) {
+        const SolveContribD cb = contrib[ci];
+        const int e = S.bsz[cb.m] - S.kfin[cb.m];
+        const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i;
+        const cplx* h = y + S.pos[cb.m] + (size_t)c * ldy;
+        for (int p = 0; p < e; ++p) cfma(acc, M[(size_t)p * rows], h[p]);
+      }
+      cplx* o = y + base + i + (size_t)c * ldy;
+      *o = csub(*o, acc);
+    }
+    __syncthreads();
+    return;
   }
   if (nrhs >= 4) {
     // many right-hand sides: the same (row, k-slice) threads with up to 8
