@@ -75,8 +75,10 @@ __device__ void warp_gemv(int n, int nrhs, const cplx* A, int lda, int op, const
   }
 }
 
-// inner dimensions up to this run one thread per result entry in the many-RHS paths
-constexpr int kSmallK = 32;
+// inner dimensions up to this run one thread per result entry in the many-RHS
+// paths: every size by default (measured, profiles/r02_solve_smallk.txt);
+// H2G_SOLVE_SMALLK overrides (0: the k-sliced form; read once per device)
+__constant__ int kSmallK = 1 << 30;
 
 // out = op(A) x for a column-major m x k matrix A (op: A or conj(A), no
 // transpose), x k x nrhs (global or shared). Coalesced: thread t owns row
@@ -87,9 +89,36 @@ constexpr int kSmallK = 32;
 __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool conjA, const cplx* x, long long ldx, cplx* out, long long ldo,
                            bool subtract, cplx* red) {
   if (nrhs >= 4 && k <= kSmallK) {
-    // many right-hand sides, short inner dimension (fine levels: a few
-    // eliminated rows): one thread per (row, column) entry of the result, the
-    // whole k range in registers -> no k-slices, no reduction barriers
+    // many right-hand sides: one thread per (row, column) entry of the result
+    // (per row and 4 columns when that still fills the CTA), the whole k range
+    // in registers -> no k-slices, no reduction barriers. Measured faster than
+    // the k-sliced form below at every level (profiles/r02_solve_smallk.txt).
+    if (m * ((nrhs + 3) / 4) >= (int)blockDim.x) {
+      const int ncb = (nrhs + 3) / 4;
+      for (int idx = threadIdx.x; idx < m * ncb; idx += blockDim.x) {
+        const int i = idx % m, c0 = (idx / m) * 4, nc = min(4, nrhs - c0);
+        const cplx* xc = x + (size_t)c0 * ldx;
+        cplx acc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = czero();
+#pragma unroll 2
+        for (int p = 0; p < k; ++p) {
+          cplx a = A[i + (size_t)p * lda];
+          if (conjA) a.y = -a.y;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < nc) cfma(acc[c], a, xc[p + (size_t)c * ldx]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nc) {
+            cplx* o = out + i + (size_t)(c0 + c) * ldo;
+            *o = subtract ? csub(*o, acc[c]) : acc[c];
+          }
+      }
+      __syncthreads();
+      return;
+    }
     for (int idx = threadIdx.x; idx < m * nrhs; idx += blockDim.x) {
       const int i = idx % m, c = idx / m;
       const cplx* xc = x + (size_t)c * ldx;
@@ -250,8 +279,38 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
   int ktot = 0;
   for (int ci = tg.c0; ci < tg.c1; ++ci) ktot += S.bsz[contrib[ci].m] - S.kfin[contrib[ci].m];
   if (nrhs >= 4 && ktot <= kSmallK) {
-    // many right-hand sides, few eliminated rows in all contributions (fine
-    // levels): one thread per (row, column) entry, contributions in order
+    // many right-hand sides: one thread per (row, column) entry (per row and
+    // 4 columns when that still fills the CTA), contributions in order
+    if (rows * ((nrhs + 3) / 4) >= (int)blockDim.x) {
+      const int ncb = (nrhs + 3) / 4;
+      for (int idx = threadIdx.x; idx < rows * ncb; idx += blockDim.x) {
+        const int i = idx % rows, c0 = (idx / rows) * 4, nc = min(4, nrhs - c0);
+        cplx acc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = czero();
+        for (int ci = tg.c0; ci < tg.c1; ++ci) {
+          const SolveContribD cb = contrib[ci];
+          const int e = S.bsz[cb.m] - S.kfin[cb.m];
+          const cplx* M = S.chain + (cb.entry >= 0 ? S.Lbar_off[cb.entry] : S.Lself_off[cb.m]) + i;
+          const cplx* h = y + S.pos[cb.m] + (size_t)c0 * ldy;
+#pragma unroll 2
+          for (int p = 0; p < e; ++p) {
+            const cplx mv = M[(size_t)p * rows];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (c < nc) cfma(acc[c], mv, h[p + (size_t)c * ldy]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < nc) {
+            cplx* o = y + base + i + (size_t)(c0 + c) * ldy;
+            *o = csub(*o, acc[c]);
+          }
+      }
+      __syncthreads();
+      return;
+    }
     for (int idx = threadIdx.x; idx < rows * nrhs; idx += blockDim.x) {
       const int i = idx % rows, c = idx / rows;
       cplx acc = czero();
@@ -879,6 +938,18 @@ static int flow_grid(const void* fn, int nt, size_t smem) {
 // its own columns, counters and ticket, so the groups' latency chains overlap.
 // The x extent is cut so that all groups are resident together (CTAs are
 // placed x-first: a full-width x would run the groups one after the other).
+static void set_small_k_once() {
+  const char* e = std::getenv("H2G_SOLVE_SMALLK");
+  if (!e) return;
+  static std::mutex mu;
+  static std::map<int, bool> done;  // constant memory is per device
+  std::lock_guard<std::mutex> lk(mu);
+  bool& d = done[cur_device()];
+  if (d) return;
+  const int v = std::max(0, std::atoi(e));
+  cudaMemcpyToSymbol(kSmallK, &v, sizeof v);
+  d = true;
+}
 static int flow_ngroups(int nrhs, const FlowGroups& G) { return (nrhs + G.rchunk - 1) / G.rchunk; }
 static int group_grid(int resident, int ng) { return std::max(1, (resident + ng - 1) / ng); }
 
@@ -904,6 +975,7 @@ static void fwd_flow_nt(const SolveLevel& S, const SolveSched& P, const SolveFlo
 void launch_fwd_flow(const SolveLevel& S, const SolveSched& P, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, int* cnt,
                      int* fail, cplx* tmp, const FlowGroups& G, cudaStream_t s) {
   if (F.nf <= 0) return;
+  set_small_k_once();
   cudaMemsetAsync(cnt, 0, ((size_t)(flow_ngroups(nrhs, G) - 1) * G.cstride + 2 * S.nl + 1) * sizeof(int), s);
   const int nt = flow_threads(S.bmax);
   if (nt == 256) fwd_flow_nt<256>(S, P, F, y, ldy, nrhs, explicit_inv, cnt, fail, tmp, G, s);
@@ -926,6 +998,7 @@ static void bwd_flow_nt(const SolveLevel& S, const SolveFlow& F, cplx* y, long l
 void launch_bwd_flow(const SolveLevel& S, const SolveFlow& F, cplx* y, long long ldy, int nrhs, int explicit_inv, cplx* part, int* cnt, int* fail,
                      cplx* tmp, const FlowGroups& G, cudaStream_t s) {
   if (F.nb <= 0) return;
+  set_small_k_once();
   cudaMemsetAsync(cnt, 0, ((size_t)(flow_ngroups(nrhs, G) - 1) * G.cstride + 4 * S.nl + 1) * sizeof(int), s);
   const int nt = flow_threads(S.bmax);
   if (nt == 256) bwd_flow_nt<256>(S, F, y, ldy, nrhs, explicit_inv, part, cnt, fail, tmp, G, s);
