@@ -3247,6 +3247,9 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
   // H2G_SOLVE_GROUPS=0: the groups of right-hand sides one after the other (one launch each) instead of side by side
   const bool side_by_side = !(std::getenv("H2G_SOLVE_GROUPS") && !std::atoi(std::getenv("H2G_SOLVE_GROUPS")));
   FlowGroups fg{};
+  constexpr int kWaveGroups = 16;
+  // cap on the gathered-partials buffers of one backward wave (H2G_SOLVE_PART_GB)
+  const size_t part_budget = (size_t)((std::getenv("H2G_SOLVE_PART_GB") ? std::max(0.0, std::atof(std::getenv("H2G_SOLVE_PART_GB"))) : 8.0) * 1073741824.0);
   {
     int nlmax = 1;
     for (auto& CLp : C->levels) nlmax = std::max(nlmax, CLp->sl.nl);
@@ -3263,8 +3266,12 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
     for (auto& CLp : C->levels) {
       ChainLevelHost& CL = *CLp;
       if (!batched && side_by_side) {
-        launch_fwd_flow(CL.sl, CL.sched, CL.flow, y, n, nrhs, expl, C->flowcnt.as<int>() + 1, C->flowcnt.as<int>(), tmp, fg, st);
-        ++launches;
+        // waves of at most kWaveGroups groups (more groups than that only thin out each group's CTAs)
+        for (int c0 = 0; c0 < nrhs; c0 += kWaveGroups * rchunk) {
+          launch_fwd_flow(CL.sl, CL.sched, CL.flow, y + (size_t)c0 * n, n, std::min(kWaveGroups * rchunk, nrhs - c0), expl, C->flowcnt.as<int>() + 1,
+                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, fg, st);
+          ++launches;
+        }
       } else
         for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
           if (batched)
@@ -3293,12 +3300,20 @@ static void solve_device_impl(h2g_chain* C, cplx* y, int64_t n, int nrhs, int mo
       launches += 2;
       const bool grouped = !batched && side_by_side;
       const size_t per_group = (batched ? CL.part_need : CL.flow_part) * rchunk;
-      const size_t need = per_group * 16 * (grouped ? (nrhs + rchunk - 1) / rchunk : 1);
+      // groups per wave: every group of a wave has its own gathered-partials
+      // buffer, together at most part_budget (then kWaveGroups) of them
+      const int wave = grouped ? (int)std::max<size_t>(1, std::min<size_t>({(size_t)kWaveGroups, (size_t)(nrhs + rchunk - 1) / rchunk,
+                                                                             part_budget / std::max<size_t>(1, per_group * 16)}))
+                               : 1;
+      const size_t need = per_group * 16 * wave;
       if (need > C->partbuf.bytes) C->partbuf.alloc(need, st);
       if (grouped) {
         fg.part_stride = (long long)per_group;
-        launch_bwd_flow(CL.sl, CL.flow, y, n, nrhs, expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1, C->flowcnt.as<int>(), tmp, fg, st);
-        ++launches;
+        for (int c0 = 0; c0 < nrhs; c0 += wave * rchunk) {
+          launch_bwd_flow(CL.sl, CL.flow, y + (size_t)c0 * n, n, std::min(wave * rchunk, nrhs - c0), expl, C->partbuf.as<cplx>(), C->flowcnt.as<int>() + 1,
+                          C->flowcnt.as<int>(), tmp + (size_t)c0 * n, fg, st);
+          ++launches;
+        }
       } else
         for (int c0 = 0; c0 < nrhs; c0 += rchunk) {
           if (batched)

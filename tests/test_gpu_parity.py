@@ -81,7 +81,8 @@ def test_multi_rhs_matches_columnwise():
     assert rel(Xe, X) < 1e-12
 
 
-def test_rhs_groups_side_by_side_match_columnwise(monkeypatch):
+@pytest.mark.parametrize("smem_kb,part_gb", [("24", None), ("6", "0")])
+def test_rhs_groups_side_by_side_match_columnwise(monkeypatch, smem_kb, part_gb):
     """More right-hand sides than one shared-memory chunk holds run as groups
     side by side in one launch per level (grid y, own counters per group):
     bit-identical to the groups run one after the other, and equal to the
@@ -90,7 +91,12 @@ def test_rhs_groups_side_by_side_match_columnwise(monkeypatch):
     gch = h2g.factorize(upload(A), 1e-4)
     n = A.n
     B = np.stack([O.rhs(n, 100 + s) for s in range(21)], axis=1)
-    monkeypatch.setenv("H2G_SOLVE_SMEM_KB", "24")  # a few columns per group -> several groups, ragged last one
+    # a few columns per group -> several groups, ragged last one; second case: one
+    # column per group -> 21 groups in two forward waves (16 + 5), backward waves of
+    # one group (no room for more gathered-partials buffers)
+    monkeypatch.setenv("H2G_SOLVE_SMEM_KB", smem_kb)
+    if part_gb is not None:
+        monkeypatch.setenv("H2G_SOLVE_PART_GB", part_gb)
     for fn in (gch.apply_inverse, gch.apply_inverse_explicit):
         monkeypatch.setenv("H2G_SOLVE_GROUPS", "1")
         X = fn(B)
