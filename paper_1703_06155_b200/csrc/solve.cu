@@ -177,7 +177,9 @@ __device__ void cta_gemv_n(int m, int k, int nrhs, const cplx* A, int lda, bool 
   }
   for (int i0 = 0; i0 < m; i0 += blockDim.x) {
     const int mm = min(m - i0, (int)blockDim.x);
-    const int G = max(1, (int)blockDim.x / mm);
+    // k-slices: no more than k (a record with 2 eliminated rows would otherwise
+    // have its 2 result threads add up 128 partials, 126 of them empty)
+    const int G = max(1, min((int)blockDim.x / mm, k));
     const int t = threadIdx.x, i = t % mm, g = t / mm;
     for (int c = 0; c < nrhs; ++c) {
       cplx acc = czero();
@@ -374,7 +376,7 @@ __device__ void fwd_lbar_body(const SolveLevel& S, const SolveTargetD tg, const 
   }
   for (int i0 = 0; i0 < rows; i0 += blockDim.x) {
     const int mm = min(rows - i0, (int)blockDim.x);
-    const int G = max(1, (int)blockDim.x / mm);
+    const int G = max(1, min((int)blockDim.x / mm, ktot));  // ktot bounds every contribution's columns
     const int t = threadIdx.x, i = t % mm, g = t / mm;
     for (int c = 0; c < nrhs; ++c) {
       cplx acc = czero();
