@@ -128,3 +128,27 @@ def test_other_orders_against_the_reference_order_oracle(cfg2, schedule):
     rows = sampled_rows(cfg2["A"].n)
     r_d = h2g.sampled_dense_residual(cfg2["pts_tree"], cfg2["kernel"], x, cfg2["b"], rows)
     assert r_d <= 2 * meta["residual_sampled_dense"]
+
+
+def test_eps_sweep_tight_end_on_the_cube():
+    """eps = 1e-6 (the tight end of config 4's sweep) on the 32^3 cube: blocks of
+    up to ~590 rows run the step-0 eigensolver with its Gram columns in global
+    memory and the truncation decided on the Gram alone; 64 right-hand sides go
+    through the explicit inverse in groups side by side. No oracle at this size
+    and eps: the residuals through the H2 operator and on sampled dense rows are
+    the check (measured 5.2e-9 / 2.7e-7, profiles/r02_eps_sweep_32cube_64rhs.txt)."""
+    eps = 1e-6
+    c = BASELINE_CONFIGS[2]
+    k0, scale, diag = vie_constants(c["cells"], c["side"])
+    pts = vie_grid_points(c["cells"], c["side"])
+    K = h2g.helmholtz_kernel(k0, diag, scale)
+    A = h2g.H2Matrix.build(pts, c["leaf"], 1.0, K, eps)
+    perm = A.perm()
+    ch = h2g.factorize(A, eps)
+    B = np.stack([h2g.random_rhs(A.n, 1234 + j) for j in range(20)], axis=1)[perm]
+    X = ch.apply_inverse_explicit(B)
+    rows = sampled_rows(A.n)
+    for j in (0, 19):
+        assert A.relative_residual(X[:, j], B[:, j]) <= 5e-8
+        assert h2g.sampled_dense_residual(pts[perm], K, X[:, j], B[:, j], rows) <= 2e-6
+    assert rel(ch.solve(B[:, 0].copy()), X[:, 0]) <= 1e-9
